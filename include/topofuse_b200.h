@@ -1,0 +1,174 @@
+/*
+ * topofuse_b200 -- C ABI of the B200-native (sm_100a) matrix-free Q1-hex
+ * stiffness operator and the Jacobi-PCG around it.
+ *
+ * Drop-in boundary: these entry points replace the kernel-module contract the
+ * reference operator calls through get_backend() (reference
+ * pkg/src/topofuse/backend.py:38-46, operator.py:90-132,157-159) and the
+ * pcg recurrence (solver.py:57-147).  The Python host package
+ * paper_2604_18020_b200 binds them with ctypes; see INTEGRATION.md.
+ *
+ * Conventions
+ *   - plain C, all functions return 0 (TF_OK) or a TF_ERR_* code; the text of
+ *     the last error on the calling thread is tf_last_error();
+ *   - every array pointer is a DEVICE pointer (e.g. torch.Tensor.data_ptr())
+ *     unless documented "host"; the caller owns and allocates them;
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy stream);
+ *     all calls are asynchronous on it unless documented otherwise;
+ *   - _f32 / _f64 suffix = working precision of vectors, scales and Ke;
+ *   - edof is int32 (n_elem, 24) row-major, reference mesh.py:83-102;
+ *     a NEGATIVE entry marks a constrained DOF slot: it gathers 0 and is
+ *     never scattered to (this is how input masking is fused, operator.py:83-88);
+ *   - node_fixed (structured grids) is one byte per node, bit c set when DOF
+ *     3*node+c is constrained (BoundaryConditions.fixed_dofs, mesh.py:105-120).
+ */
+#ifndef TOPOFUSE_B200_H
+#define TOPOFUSE_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TF_OK 0
+#define TF_ERR_ARG 1
+#define TF_ERR_CUDA 2
+#define TF_ERR_UNSUPPORTED 3
+#define TF_ERR_DIVERGED 4
+
+/* matvec flags */
+#define TF_ACCUMULATE 1u  /* w += K v instead of w = K v                         */
+#define TF_MASK_INPUT 2u  /* read v as 0 on constrained DOFs (operator.py:84)     */
+#define TF_PASS_FIXED 4u  /* w[fixed] = v[fixed] (operator.py:115)                */
+
+/* structured-grid kernel variants */
+#define TF_GRID_FAST 0     /* production: FMA, Ke as constant operands           */
+#define TF_GRID_BITWISE 1  /* reproduces the numba fused_serial op order bitwise  */
+
+/* general-edof scatter modes (operator.py SCATTER_MODES, :30) */
+#define TF_SCATTER_ATOMIC 0 /* red.global.add -- parallel_atomic analogue         */
+#define TF_SCATTER_COLORED 1 /* deterministic colour-ordered passes -- serial     */
+
+typedef struct tf_grid {
+    int32_t nelx, nely, nelz; /* StructuredMesh (mesh.py:34-56) */
+} tf_grid;
+
+const char* tf_last_error(void);
+int tf_version(void);
+/* number of CUDA devices visible (0 on a GPU-less host) */
+int tf_device_count(void);
+
+/* ---- K v on a structured grid: replaces fused_serial / fused_atomic +
+ *      apply()'s masking when edof == build_edof(mesh)
+ *      (_kernels_numba.py:146-196, operator.py:90-117).
+ *      ke: HOST pointer, 576 values, row-major.  scale: n_elem.  v, w: n_dof.
+ *      node_fixed may be NULL (no constraints).  `variant` TF_GRID_*.      */
+int tf_matvec_grid_f32(const tf_grid* g, const float* ke, const float* scale, const float* v,
+                       float* w, const uint8_t* node_fixed, uint32_t flags, int variant,
+                       void* stream);
+int tf_matvec_grid_f64(const tf_grid* g, const double* ke, const double* scale,
+                       const double* v, double* w, const uint8_t* node_fixed, uint32_t flags,
+                       int variant, void* stream);
+
+/* ---- K v with an explicit element->DOF table: the fused kernel contract
+ *      fused_serial/fused_atomic(edof, ke, scale, v, out) (_kernels_numba.py:146-196).
+ *      ALWAYS accumulates into w (caller zeroes it, operator.py:93).
+ *      mode TF_SCATTER_ATOMIC: one element per thread, red.global.add scatter.
+ *      mode TF_SCATTER_COLORED: `color_elems` (n_elem int32 element ids grouped
+ *      by colour) and `color_offsets` (n_colors+1, HOST) give an ordering in
+ *      which no two elements of a colour share a DOF; deterministic.       */
+int tf_matvec_edof_f32(const int32_t* edof, const float* ke, const float* scale, const float* v,
+                       float* w, int64_t n_elem, int mode, const int32_t* color_elems,
+                       const int64_t* color_offsets, int n_colors, void* stream);
+int tf_matvec_edof_f64(const int32_t* edof, const double* ke, const double* scale,
+                       const double* v, double* w, int64_t n_elem, int mode,
+                       const int32_t* color_elems, const int64_t* color_offsets, int n_colors,
+                       void* stream);
+
+/* w[fixed[i]] = v[fixed[i]] for i < n_fixed (operator.py:115) */
+int tf_pass_fixed_f32(const int64_t* fixed, int64_t n_fixed, const float* v, float* w,
+                      void* stream);
+int tf_pass_fixed_f64(const int64_t* fixed, int64_t n_fixed, const double* v, double* w,
+                      void* stream);
+
+/* ---- three-stage variant stages (_kernels_numba.py:82-140) ----------------- */
+int tf_gather_f32(const int32_t* edof, const float* v, float* u_elem, int64_t n_elem, void* stream);
+int tf_gather_f64(const int32_t* edof, const double* v, double* u_elem, int64_t n_elem, void* stream);
+/* f_elem[e,i] = scale[e] * sum_j K[i,j] u_elem[e,j] */
+int tf_gemm_f32(const float* u_elem, const float* ke, const float* scale, float* f_elem,
+                int64_t n_elem, void* stream);
+int tf_gemm_f64(const double* u_elem, const double* ke, const double* scale, double* f_elem,
+                int64_t n_elem, void* stream);
+/* acc[edof[e,i]] += f_elem[e,i] in FP64 (histogram-style, operator.py:107-114) */
+int tf_scatter_f32(const int32_t* edof, const float* f_elem, double* acc, int64_t n_elem,
+                   void* stream);
+int tf_scatter_f64(const int32_t* edof, const double* f_elem, double* acc, int64_t n_elem,
+                   void* stream);
+
+/* ---- Jacobi diagonal (_kernels_numba.py:217-226, operator.py:122-132) ------ */
+/* structured: diag (working dtype) with 1.0 on fixed DOFs; inv_diag (nullable)
+ * = 1/diag rounded in the working dtype (solver.py:95).  ke_diag: HOST, 24.  */
+int tf_jacobi_grid_f32(const tf_grid* g, const float* ke_diag, const float* scale, float* diag,
+                       float* inv_diag, const uint8_t* node_fixed, void* stream);
+int tf_jacobi_grid_f64(const tf_grid* g, const double* ke_diag, const double* scale,
+                       double* diag, double* inv_diag, const uint8_t* node_fixed, void* stream);
+/* contract form: acc (FP64, n_dof) += scale[e]*ke_diag[l] over edof */
+int tf_jacobi_edof_f32(const int32_t* edof, const float* ke_diag, const float* scale,
+                       double* acc, int64_t n_elem, void* stream);
+int tf_jacobi_edof_f64(const int32_t* edof, const double* ke_diag, const double* scale,
+                       double* acc, int64_t n_elem, void* stream);
+
+/* ---- element energies u_e^T Ke u_e in FP64 (_kernels_numba.py:241-256) ----- */
+int tf_energies_grid_f64(const tf_grid* g, const double* ke, const double* u, double* out,
+                         void* stream);
+int tf_energies_edof_f64(const int32_t* edof, const double* ke, const double* u, double* out,
+                         int64_t n_elem, void* stream);
+
+/* ---- device-resident Jacobi-PCG (solver.py:57-147) --------------------------
+ * One handle per operator configuration; not re-entrant.  The whole solve
+ * runs as ONE CUDA-graph launch: a device-side while loop (conditional graph
+ * node) iterates matvec+dot -> update -> direction kernels until the
+ * reference stop rule fires; the host reads back only the final report.   */
+
+typedef struct tf_pcg tf_pcg;
+
+typedef struct tf_pcg_desc {
+    int precision;              /* 32 or 64 */
+    int structured;             /* 1: grid kernels, 0: edof kernels */
+    tf_grid grid;               /* when structured */
+    const int32_t* edof;        /* when !structured: masked edof (fixed -> -1) */
+    int64_t n_elem;
+    int64_t n_dof;
+    const void* ke;             /* HOST, 576 values in the working precision */
+    const void* scale;          /* device, n_elem */
+    const uint8_t* node_fixed;  /* device, structured only, nullable */
+    const int64_t* fixed;       /* device list of fixed DOFs (edof mode), nullable */
+    int64_t n_fixed;
+    int grid_variant;           /* TF_GRID_* */
+} tf_pcg_desc;
+
+typedef struct tf_pcg_report {
+    int32_t iterations;
+    int32_t termination;        /* 0 converged, 1 max_iter, 2 breakdown, 3 diverged */
+    int32_t matvecs;
+    int32_t _pad;
+    double rel_residual;
+} tf_pcg_report;
+
+int tf_pcg_create(tf_pcg** out, const tf_pcg_desc* desc, void* stream);
+/* Solve K x = b.  scale (n_elem), b, inv_diag, x are device arrays in the
+ * working precision; they are copied into handle-owned buffers, so the
+ * captured graph never changes.  x holds x0 on entry when has_x0 != 0 (else
+ * the solve starts from 0) and the solution on exit.  history (device,
+ * FP64, max_iter+1 entries, nullable) receives the relative residual of every
+ * iteration (SolveReport.residual_history).  Blocks until the solve ends.  */
+int tf_pcg_solve(tf_pcg* h, const void* scale, const void* b, const void* inv_diag, void* x,
+                 int has_x0, double rel_tol, int32_t max_iter, int32_t recompute_every,
+                 double* history, tf_pcg_report* report);
+int tf_pcg_destroy(tf_pcg* h);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TOPOFUSE_B200_H */

@@ -1,0 +1,113 @@
+"""Device plumbing: torch CUDA tensors as buffers, stream handles, caches.
+
+torch is used only to allocate device memory and name the current stream;
+every computation goes through libtopofuse_b200.so.
+"""
+
+from __future__ import annotations
+
+import weakref
+
+import numpy as np
+
+from . import _lib
+
+_torch = None
+
+
+def torch():
+    global _torch
+    if _torch is None:
+        import torch as t
+
+        _torch = t
+    return _torch
+
+
+def require_cuda(device=None):
+    """Raise (no CPU fallback) unless a CUDA device and the kernel library exist."""
+    t = torch()
+    if not t.cuda.is_available():
+        raise _lib.TfError("paper_2604_18020_b200 needs a CUDA device (B200, sm_100a); "
+                           "this product path has no CPU fallback")
+    _lib.load()
+    dev = t.device("cuda", t.cuda.current_device() if device is None else device)
+    return dev
+
+
+def stream_ptr():
+    return torch().cuda.current_stream().cuda_stream
+
+
+def tdtype(np_dtype):
+    t = torch()
+    return {np.dtype(np.float32): t.float32, np.dtype(np.float64): t.float64,
+            np.dtype(np.int32): t.int32, np.dtype(np.int64): t.int64,
+            np.dtype(np.uint8): t.uint8}[np.dtype(np_dtype)]
+
+
+def to_dev(a, dtype=None, device=None):
+    """numpy/torch -> contiguous CUDA tensor of `dtype` (numpy dtype)."""
+    t = torch()
+    dev = require_cuda(device)
+    if isinstance(a, t.Tensor):
+        out = a.to(device=dev, dtype=tdtype(dtype) if dtype is not None else a.dtype)
+        return out.contiguous()
+    arr = np.ascontiguousarray(a, dtype=dtype)
+    return t.from_numpy(arr).to(dev, non_blocking=False)
+
+
+def ptr(x) -> int:
+    return 0 if x is None else x.data_ptr()
+
+
+def is_tensor(x) -> bool:
+    if _torch is None:
+        try:
+            import torch as _t  # noqa: F401
+        except ImportError:  # pragma: no cover
+            return False
+    return isinstance(x, torch().Tensor)
+
+
+class IdCache:
+    """Per-object cache keyed by identity, released when the object dies."""
+
+    def __init__(self):
+        self._d = {}
+
+    def get(self, obj, key, make):
+        k = (id(obj), key)
+        hit = self._d.get(k)
+        if hit is not None:
+            ref, val = hit
+            if ref() is obj:
+                return val
+        val = make()
+        try:
+            ref = weakref.ref(obj)
+        except TypeError:  # not weak-referenceable: do not cache
+            return val
+        self._d[k] = (ref, val)
+        weakref.finalize(obj, self._d.pop, k, None)
+        return val
+
+
+CACHE = IdCache()
+
+
+def node_fixed_mask(n_nodes: int, fixed_dofs: np.ndarray) -> np.ndarray:
+    """One byte per node, bit c set when DOF 3*node + c is constrained."""
+    m = np.zeros(n_nodes, dtype=np.uint8)
+    f = np.asarray(fixed_dofs, dtype=np.int64)
+    if f.size:
+        np.bitwise_or.at(m, f // 3, (1 << (f % 3)).astype(np.uint8))
+    return m
+
+
+def masked_edof(edof: np.ndarray, fixed_dofs: np.ndarray, n_dof: int) -> np.ndarray:
+    """edof with every constrained DOF slot replaced by -1 (gather 0, no scatter)."""
+    free = np.ones(n_dof, dtype=bool)
+    free[np.asarray(fixed_dofs, dtype=np.int64)] = False
+    e = np.ascontiguousarray(edof, dtype=np.int32)
+    return np.where(free[e], e, np.int32(-1)).astype(np.int32)

@@ -1,0 +1,142 @@
+"""ctypes binding of libtopofuse_b200.so (the C ABI in include/topofuse_b200.h).
+
+The product path has no CPU fallback: if the library is missing or no CUDA
+device is present, every compute entry point raises.  Device buffers are
+torch CUDA tensors; only their data pointers cross the boundary.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import re
+import subprocess
+from pathlib import Path
+
+_PKG = Path(__file__).resolve().parent
+LIB_PATH = _PKG / "lib" / "libtopofuse_b200.so"
+HEADER = _PKG.parent / "include" / "topofuse_b200.h"
+CSRC = _PKG / "csrc"
+
+TF_OK = 0
+TF_ACCUMULATE = 1
+TF_MASK_INPUT = 2
+TF_PASS_FIXED = 4
+TF_GRID_FAST = 0
+TF_GRID_BITWISE = 1
+TF_SCATTER_ATOMIC = 0
+TF_SCATTER_COLORED = 1
+TERMINATIONS = ("converged", "max_iter", "breakdown", "diverged")
+
+
+class TfError(RuntimeError):
+    pass
+
+
+class tf_grid(ctypes.Structure):
+    _fields_ = [("nelx", ctypes.c_int32), ("nely", ctypes.c_int32), ("nelz", ctypes.c_int32)]
+
+
+class tf_pcg_desc(ctypes.Structure):
+    _fields_ = [
+        ("precision", ctypes.c_int),
+        ("structured", ctypes.c_int),
+        ("grid", tf_grid),
+        ("edof", ctypes.c_void_p),
+        ("n_elem", ctypes.c_int64),
+        ("n_dof", ctypes.c_int64),
+        ("ke", ctypes.c_void_p),
+        ("node_fixed", ctypes.c_void_p),
+        ("fixed", ctypes.c_void_p),
+        ("n_fixed", ctypes.c_int64),
+        ("grid_variant", ctypes.c_int),
+    ]
+
+
+class tf_pcg_report(ctypes.Structure):
+    _fields_ = [
+        ("iterations", ctypes.c_int32),
+        ("termination", ctypes.c_int32),
+        ("matvecs", ctypes.c_int32),
+        ("_pad", ctypes.c_int32),
+        ("rel_residual", ctypes.c_double),
+    ]
+
+
+_P = ctypes.c_void_p
+_I64 = ctypes.c_int64
+_U32 = ctypes.c_uint32
+_INT = ctypes.c_int
+
+# name -> argtypes (restype int unless noted)
+_SIGS = {
+    "tf_version": [],
+    "tf_device_count": [],
+    "tf_matvec_grid_f32": [_P, _P, _P, _P, _P, _P, _U32, _INT, _P],
+    "tf_matvec_grid_f64": [_P, _P, _P, _P, _P, _P, _U32, _INT, _P],
+    "tf_matvec_edof_f32": [_P, _P, _P, _P, _P, _I64, _INT, _P, _P, _INT, _P],
+    "tf_matvec_edof_f64": [_P, _P, _P, _P, _P, _I64, _INT, _P, _P, _INT, _P],
+    "tf_pass_fixed_f32": [_P, _I64, _P, _P, _P],
+    "tf_pass_fixed_f64": [_P, _I64, _P, _P, _P],
+    "tf_gather_f32": [_P, _P, _P, _I64, _P],
+    "tf_gather_f64": [_P, _P, _P, _I64, _P],
+    "tf_gemm_f32": [_P, _P, _P, _P, _I64, _P],
+    "tf_gemm_f64": [_P, _P, _P, _P, _I64, _P],
+    "tf_scatter_f32": [_P, _P, _P, _I64, _P],
+    "tf_scatter_f64": [_P, _P, _P, _I64, _P],
+    "tf_jacobi_grid_f32": [_P, _P, _P, _P, _P, _P, _P],
+    "tf_jacobi_grid_f64": [_P, _P, _P, _P, _P, _P, _P],
+    "tf_jacobi_edof_f32": [_P, _P, _P, _P, _I64, _P],
+    "tf_jacobi_edof_f64": [_P, _P, _P, _P, _I64, _P],
+    "tf_energies_grid_f64": [_P, _P, _P, _P, _P],
+    "tf_energies_edof_f64": [_P, _P, _P, _P, _I64, _P],
+    "tf_pcg_create": [_P, _P, _P],
+    "tf_pcg_solve": [_P, _P, _P, _P, _P, _INT, ctypes.c_double, ctypes.c_int32, ctypes.c_int32,
+                     _P, _P],
+    "tf_pcg_destroy": [_P],
+}
+
+_lib = None
+
+
+def header_symbols() -> list[str]:
+    """Every function the C header declares (parsed from include/topofuse_b200.h)."""
+    text = HEADER.read_text()
+    return sorted(set(re.findall(r"^\s*(?:const\s+)?\w+\**\s+\**(tf_\w+)\s*\(", text, re.M)))
+
+
+def build(verbose: bool = False) -> Path:
+    """Compile the sm_100a library in-tree with the csrc Makefile (nvcc)."""
+    out = subprocess.run(["make", "-C", str(CSRC), "-j4"], capture_output=True, text=True)
+    if out.returncode != 0:
+        raise TfError("nvcc build failed:\n" + out.stdout[-4000:] + out.stderr[-4000:])
+    if verbose:
+        print(out.stdout)
+    return LIB_PATH
+
+
+def load() -> ctypes.CDLL:
+    """Load the library (no compute); raises when it is missing."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not LIB_PATH.exists():
+        raise TfError(f"{LIB_PATH} not built -- run __graft_entry__.build() (no CPU fallback)")
+    L = ctypes.CDLL(str(LIB_PATH))
+    for name, args in _SIGS.items():
+        fn = getattr(L, name)
+        fn.argtypes = args
+        fn.restype = ctypes.c_int
+    L.tf_last_error.restype = ctypes.c_char_p
+    L.tf_last_error.argtypes = []
+    _lib = L
+    return L
+
+
+def check(rc: int, what: str = "") -> None:
+    if rc != TF_OK:
+        msg = load().tf_last_error().decode(errors="replace")
+        raise TfError(f"{what or 'topofuse_b200'} failed (code {rc}): {msg}")
+
+
+def call(name: str, *args) -> None:
+    check(getattr(load(), name)(*args), name)

@@ -1,0 +1,687 @@
+// Matrix-free Q1-hex stiffness action w = sum_e B_e^T (s_e Ke) B_e v on B200.
+//
+// Reference semantics: _kernels_numba.py:146-196 (fused_serial/fused_atomic),
+// operator.py:83-117 (input masking, fixed-DOF pass-through), and the
+// three-stage pipeline _kernels_numba.py:82-140.
+//
+// Structured grids (edof == build_edof(mesh)) use an index-free, atomic-free
+// "pull" kernel: one thread per NODE gathers its 27-node neighbourhood once
+// and sums the rows of its 8 adjacent elements that belong to it.  Output is
+// written exactly once (coalesced), no red/atomics, deterministic.  Element
+// contributions are added in ascending element id -- the order the
+// reference's element-major serial loop produces for every DOF -- so the
+// TF_GRID_BITWISE variant (which also keeps numba's per-term rounding) is
+// bitwise-equal to the reference fused_serial.
+//
+// General connectivity (any edof) uses one thread per element with the
+// element matrix as constant-bank operands and red.global.add scatter
+// (parallel_atomic analogue) or a colour-ordered deterministic scatter.
+
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+
+#include "tf_common.cuh"
+
+namespace tf {
+
+static thread_local char g_err[512] = "";
+
+void set_error(const char* fmt, ...)
+{
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+}
+
+__host__ __device__ constexpr int cx(int b) { return ((b & 3) == 1 || (b & 3) == 2) ? 1 : 0; }
+__host__ __device__ constexpr int cy(int b) { return (b & 3) >= 2 ? 1 : 0; }
+__host__ __device__ constexpr int cz(int b) { return b >> 2; }
+
+// ---------------------------------------------------------------------------
+// block reduction of one double (blockDim.x*blockDim.y*blockDim.z <= 1024)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double block_sum(double v, double* sh)
+{
+    const int tid = threadIdx.x + blockDim.x * (threadIdx.y + blockDim.y * threadIdx.z);
+    const int nthreads = blockDim.x * blockDim.y * blockDim.z;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    if ((tid & 31) == 0) sh[tid >> 5] = v;
+    __syncthreads();
+    double r = 0.0;
+    if (tid == 0) {
+        for (int wi = 0; wi < (nthreads + 31) / 32; ++wi) r += sh[wi];
+    }
+    return r;  // valid in thread 0 only
+}
+
+// ---------------------------------------------------------------------------
+// Structured pull kernel
+// ---------------------------------------------------------------------------
+constexpr int PULL_BX = 32, PULL_BY = 4;
+
+template <typename T, int VAR, bool DOT>
+__global__ void __launch_bounds__(PULL_BX * PULL_BY)
+k_grid_pull(Grid g, const T* __restrict__ scale, const T* __restrict__ v, T* __restrict__ w,
+            const uint8_t* __restrict__ node_fixed, uint32_t flags, double* __restrict__ dot_part,
+            const __grid_constant__ KeMat<T> ke)
+{
+    const int i = blockIdx.x * PULL_BX + threadIdx.x;
+    const int j = blockIdx.y * PULL_BY + threadIdx.y;
+    const int k = blockIdx.z;
+    const bool live = (i < g.nnx) && (j < g.nny);
+    const bool mask_in = (flags & TF_MASK_INPUT) && node_fixed != nullptr;
+    const long long sx = 1, sy = g.nnx, sz = (long long)g.nnx * g.nny;
+    const long long node = i + sy * j + sz * k;
+
+    // 27-node neighbourhood, 3 components each
+    T u[3][3][3][3];
+#pragma unroll
+    for (int dz = 0; dz < 3; ++dz)
+#pragma unroll
+        for (int dy = 0; dy < 3; ++dy)
+#pragma unroll
+            for (int dx = 0; dx < 3; ++dx) {
+                const int ii = i + dx - 1, jj = j + dy - 1, kk = k + dz - 1;
+                const bool ok = live && ii >= 0 && ii < g.nnx && jj >= 0 && jj < g.nny &&
+                                kk >= 0 && kk < g.nnz;
+                const long long nb = node + (dx - 1) * sx + (dy - 1) * sy + (dz - 1) * sz;
+                const unsigned bits = (ok && mask_in) ? (unsigned)node_fixed[nb] : 0u;
+#pragma unroll
+                for (int c = 0; c < 3; ++c)
+                    u[dz][dy][dx][c] = (ok && !((bits >> c) & 1u)) ? ld_nc(v + 3 * nb + c) : T(0);
+            }
+
+    // scales of the 8 adjacent elements (ex, ey, ez) = (i-1+ox, j-1+oy, k-1+oz)
+    T s[2][2][2];
+    bool ev[2][2][2];
+#pragma unroll
+    for (int oz = 0; oz < 2; ++oz)
+#pragma unroll
+        for (int oy = 0; oy < 2; ++oy)
+#pragma unroll
+            for (int ox = 0; ox < 2; ++ox) {
+                const int ex = i - 1 + ox, ey = j - 1 + oy, ez = k - 1 + oz;
+                const bool ok = live && ex >= 0 && ex < g.nelx && ey >= 0 && ey < g.nely &&
+                                ez >= 0 && ez < g.nelz;
+                const long long e = ex + (long long)g.nelx * (ey + (long long)g.nely * ez);
+                ev[oz][oy][ox] = ok;
+                s[oz][oy][ox] = ok ? ld_nc(scale + e) : T(0);
+            }
+
+    T out[3];
+    if (VAR == TF_GRID_FAST) {
+        T acc[3] = {T(0), T(0), T(0)};
+        if (flags & TF_ACCUMULATE) {
+#pragma unroll
+            for (int c = 0; c < 3; ++c) acc[c] = live ? w[3 * node + c] : T(0);
+        }
+        // elements in ascending id order: z, then y, then x
+#pragma unroll
+        for (int oz = 0; oz < 2; ++oz)
+#pragma unroll
+            for (int oy = 0; oy < 2; ++oy)
+#pragma unroll
+                for (int ox = 0; ox < 2; ++ox) {
+                    const int a = corner_of(1 - ox, 1 - oy, 1 - oz);  // this node's corner
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) {
+                        const int row = 3 * a + c;
+                        T t = T(0);
+#pragma unroll
+                        for (int b = 0; b < 8; ++b)
+#pragma unroll
+                            for (int d = 0; d < 3; ++d)
+                                t = fma(ke.a[row * NLOC + 3 * b + d],
+                                        u[oz + cz(b)][oy + cy(b)][ox + cx(b)][d], t);
+                        acc[c] = fma(s[oz][oy][ox], t, acc[c]);
+                    }
+                }
+#pragma unroll
+        for (int c = 0; c < 3; ++c) out[c] = acc[c];
+    } else {
+        // Bitwise reproduction of the reference element loop.
+        if constexpr (sizeof(T) == 8) {
+            double acc[3] = {0.0, 0.0, 0.0};
+            if (flags & TF_ACCUMULATE) {
+#pragma unroll
+                for (int c = 0; c < 3; ++c) acc[c] = live ? (double)w[3 * node + c] : 0.0;
+            }
+#pragma unroll
+            for (int oz = 0; oz < 2; ++oz)
+#pragma unroll
+                for (int oy = 0; oy < 2; ++oy)
+#pragma unroll
+                    for (int ox = 0; ox < 2; ++ox) {
+                        if (!ev[oz][oy][ox]) continue;
+                        const int a = corner_of(1 - ox, 1 - oy, 1 - oz);
+                        const double se = (double)s[oz][oy][ox];
+#pragma unroll
+                        for (int c = 0; c < 3; ++c) {
+                            const int row = 3 * a + c;
+                            double t = 0.0;
+#pragma unroll
+                            for (int b = 0; b < 8; ++b)
+#pragma unroll
+                                for (int d = 0; d < 3; ++d)
+                                    t = __dadd_rn(t, __dmul_rn(__dmul_rn(se, (double)ke.a[row * NLOC + 3 * b + d]),
+                                                               (double)u[oz + cz(b)][oy + cy(b)][ox + cx(b)][d]));
+                            acc[c] = __dadd_rn(acc[c], t);
+                        }
+                    }
+#pragma unroll
+            for (int c = 0; c < 3; ++c) out[c] = (T)acc[c];
+        } else {
+            // numba FP32: f32 products, f64 row sum, out = f32(f64(out) + acc)
+            float acc[3] = {0.f, 0.f, 0.f};
+            if (flags & TF_ACCUMULATE) {
+#pragma unroll
+                for (int c = 0; c < 3; ++c) acc[c] = live ? (float)w[3 * node + c] : 0.f;
+            }
+#pragma unroll
+            for (int oz = 0; oz < 2; ++oz)
+#pragma unroll
+                for (int oy = 0; oy < 2; ++oy)
+#pragma unroll
+                    for (int ox = 0; ox < 2; ++ox) {
+                        if (!ev[oz][oy][ox]) continue;
+                        const int a = corner_of(1 - ox, 1 - oy, 1 - oz);
+                        const float se = (float)s[oz][oy][ox];
+#pragma unroll
+                        for (int c = 0; c < 3; ++c) {
+                            const int row = 3 * a + c;
+                            double t = 0.0;
+#pragma unroll
+                            for (int b = 0; b < 8; ++b)
+#pragma unroll
+                                for (int d = 0; d < 3; ++d) {
+                                    const float kk = __fmul_rn(se, (float)ke.a[row * NLOC + 3 * b + d]);
+                                    const float pr = __fmul_rn(kk, (float)u[oz + cz(b)][oy + cy(b)][ox + cx(b)][d]);
+                                    t = __dadd_rn(t, (double)pr);
+                                }
+                            acc[c] = (float)__dadd_rn((double)acc[c], t);
+                        }
+                    }
+#pragma unroll
+            for (int c = 0; c < 3; ++c) out[c] = (T)acc[c];
+        }
+    }
+
+    double dot = 0.0;
+    if (live) {
+        const unsigned bits = node_fixed ? (unsigned)node_fixed[node] : 0u;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            T val = out[c];
+            if ((flags & TF_PASS_FIXED) && ((bits >> c) & 1u)) val = v[3 * node + c];
+            w[3 * node + c] = val;
+            if (DOT) dot += (double)v[3 * node + c] * (double)val;  // p.q on the raw p
+        }
+    }
+    if (DOT) {
+        __shared__ double sh[PULL_BX * PULL_BY / 32];
+        const double tot = block_sum(dot, sh);
+        if (threadIdx.x == 0 && threadIdx.y == 0)
+            dot_part[blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z)] = tot;
+    }
+}
+
+template <typename T>
+int launch_grid_pull(const Grid& g, const T* ke_host, const T* scale, const T* v, T* w,
+                     const uint8_t* node_fixed, uint32_t flags, int variant, double* dot_part,
+                     cudaStream_t st)
+{
+    KeMat<T> ke;
+    memcpy(ke.a, ke_host, sizeof(ke.a));
+    dim3 block(PULL_BX, PULL_BY, 1);
+    dim3 grid((g.nnx + PULL_BX - 1) / PULL_BX, (g.nny + PULL_BY - 1) / PULL_BY, g.nnz);
+    if (variant == TF_GRID_FAST) {
+        if (dot_part)
+            k_grid_pull<T, TF_GRID_FAST, true><<<grid, block, 0, st>>>(g, scale, v, w, node_fixed, flags, dot_part, ke);
+        else
+            k_grid_pull<T, TF_GRID_FAST, false><<<grid, block, 0, st>>>(g, scale, v, w, node_fixed, flags, nullptr, ke);
+    } else if (variant == TF_GRID_BITWISE) {
+        if (dot_part)
+            k_grid_pull<T, TF_GRID_BITWISE, true><<<grid, block, 0, st>>>(g, scale, v, w, node_fixed, flags, dot_part, ke);
+        else
+            k_grid_pull<T, TF_GRID_BITWISE, false><<<grid, block, 0, st>>>(g, scale, v, w, node_fixed, flags, nullptr, ke);
+    } else {
+        set_error("unknown grid variant %d", variant);
+        return TF_ERR_ARG;
+    }
+    TF_CHECK_LAUNCH();
+    return TF_OK;
+}
+
+long long grid_pull_blocks(const Grid& g)
+{
+    return (long long)((g.nnx + PULL_BX - 1) / PULL_BX) * ((g.nny + PULL_BY - 1) / PULL_BY) * g.nnz;
+}
+
+template int launch_grid_pull<float>(const Grid&, const float*, const float*, const float*, float*,
+                                     const uint8_t*, uint32_t, int, double*, cudaStream_t);
+template int launch_grid_pull<double>(const Grid&, const double*, const double*, const double*,
+                                      double*, const uint8_t*, uint32_t, int, double*, cudaStream_t);
+
+// ---------------------------------------------------------------------------
+// General edof kernels
+// ---------------------------------------------------------------------------
+constexpr int EDOF_BLOCK = 128;
+
+__device__ __forceinline__ void load_edof_row(const int32_t* __restrict__ edof, long long e, int idx[NLOC])
+{
+    const int4* r4 = reinterpret_cast<const int4*>(edof + e * NLOC);
+#pragma unroll
+    for (int q = 0; q < 6; ++q) {
+        const int4 t = __ldg(r4 + q);
+        idx[4 * q + 0] = t.x; idx[4 * q + 1] = t.y; idx[4 * q + 2] = t.z; idx[4 * q + 3] = t.w;
+    }
+}
+
+template <typename T, bool ATOMIC>
+__global__ void __launch_bounds__(EDOF_BLOCK)
+k_edof_fused(const int32_t* __restrict__ edof, const T* __restrict__ scale, const T* __restrict__ v,
+             T* __restrict__ w, long long n, const int32_t* __restrict__ order,
+             const __grid_constant__ KeMat<T> ke)
+{
+    const long long t = (long long)blockIdx.x * EDOF_BLOCK + threadIdx.x;
+    if (t >= n) return;
+    const long long e = order ? (long long)order[t] : t;
+    int idx[NLOC];
+    load_edof_row(edof, e, idx);
+    T u[NLOC];
+#pragma unroll
+    for (int q = 0; q < NLOC; ++q) u[q] = idx[q] >= 0 ? ld_nc(v + idx[q]) : T(0);
+    const T se = ld_nc(scale + e);
+#pragma unroll
+    for (int r = 0; r < NLOC; ++r) {
+        T acc = T(0);
+#pragma unroll
+        for (int q = 0; q < NLOC; ++q) acc = fma(ke.a[r * NLOC + q], u[q], acc);
+        const T val = se * acc;
+        if (idx[r] >= 0) {
+            if (ATOMIC)
+                atomicAdd(w + idx[r], val);
+            else
+                w[idx[r]] += val;
+        }
+    }
+}
+
+template <typename T>
+int launch_edof(const int32_t* edof, const T* ke_host, const T* scale, const T* v, T* w,
+                long long n_elem, int mode, const int32_t* color_elems,
+                const int64_t* color_offsets, int n_colors, cudaStream_t st)
+{
+    KeMat<T> ke;
+    memcpy(ke.a, ke_host, sizeof(ke.a));
+    TF_REQUIRE(((uintptr_t)edof & 15u) == 0, "edof must be 16-byte aligned");
+    if (n_elem == 0) return TF_OK;
+    if (mode == TF_SCATTER_ATOMIC) {
+        const long long nb = (n_elem + EDOF_BLOCK - 1) / EDOF_BLOCK;
+        k_edof_fused<T, true><<<(unsigned)nb, EDOF_BLOCK, 0, st>>>(edof, scale, v, w, n_elem, nullptr, ke);
+        TF_CHECK_LAUNCH();
+    } else if (mode == TF_SCATTER_COLORED) {
+        TF_REQUIRE(color_elems && color_offsets && n_colors > 0, "coloured scatter needs a colouring");
+        for (int c = 0; c < n_colors; ++c) {
+            const long long a = color_offsets[c], b = color_offsets[c + 1];
+            if (b <= a) continue;
+            const long long nb = (b - a + EDOF_BLOCK - 1) / EDOF_BLOCK;
+            k_edof_fused<T, false><<<(unsigned)nb, EDOF_BLOCK, 0, st>>>(edof, scale, v, w, b - a,
+                                                                      color_elems + a, ke);
+            TF_CHECK_LAUNCH();
+        }
+    } else {
+        set_error("unknown scatter mode %d", mode);
+        return TF_ERR_ARG;
+    }
+    return TF_OK;
+}
+
+// pass-through of constrained DOFs
+template <typename T>
+__global__ void k_pass_fixed(const int64_t* __restrict__ fixed, long long n, const T* __restrict__ v,
+                             T* __restrict__ w)
+{
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < n) {
+        const long long d = fixed[t];
+        w[d] = v[d];
+    }
+}
+
+template <typename T>
+int launch_pass_fixed(const int64_t* fixed, long long n, const T* v, T* w, cudaStream_t st)
+{
+    if (n <= 0) return TF_OK;
+    k_pass_fixed<T><<<(unsigned)((n + 255) / 256), 256, 0, st>>>(fixed, n, v, w);
+    TF_CHECK_LAUNCH();
+    return TF_OK;
+}
+template int launch_pass_fixed<float>(const int64_t*, long long, const float*, float*, cudaStream_t);
+template int launch_pass_fixed<double>(const int64_t*, long long, const double*, double*, cudaStream_t);
+
+// ---------------------------------------------------------------------------
+// three-stage pipeline stages
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void k_gather(const int32_t* __restrict__ edof, const T* __restrict__ v,
+                         T* __restrict__ u_elem, long long n)
+{
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;  // one entry per thread
+    if (t < n * NLOC) {
+        const int d = edof[t];
+        u_elem[t] = d >= 0 ? v[d] : T(0);
+    }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(EDOF_BLOCK)
+k_gemm(const T* __restrict__ u_elem, const T* __restrict__ scale, T* __restrict__ f_elem, long long n,
+       const __grid_constant__ KeMat<T> ke)
+{
+    const long long e = (long long)blockIdx.x * EDOF_BLOCK + threadIdx.x;
+    if (e >= n) return;
+    T u[NLOC];
+#pragma unroll
+    for (int q = 0; q < NLOC; ++q) u[q] = u_elem[e * NLOC + q];
+    const T se = scale[e];
+#pragma unroll
+    for (int r = 0; r < NLOC; ++r) {
+        T acc = T(0);
+#pragma unroll
+        for (int q = 0; q < NLOC; ++q) acc = fma(ke.a[r * NLOC + q], u[q], acc);
+        f_elem[e * NLOC + r] = se * acc;
+    }
+}
+
+template <typename T>
+__global__ void k_scatter(const int32_t* __restrict__ edof, const T* __restrict__ f_elem,
+                          double* __restrict__ acc, long long n)
+{
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < n * NLOC) {
+        const int d = edof[t];
+        if (d >= 0) atomicAdd(acc + d, (double)f_elem[t]);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Jacobi diagonal and element energies
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void k_jacobi_grid(Grid g, const T* __restrict__ scale, T* __restrict__ diag,
+                              T* __restrict__ inv_diag, const uint8_t* __restrict__ node_fixed,
+                              const __grid_constant__ KeMat<T> kd /* first 24 = ke_diag */)
+{
+    const long long node = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (node >= g.n_nodes) return;
+    const int i = (int)(node % g.nnx);
+    const int j = (int)((node / g.nnx) % g.nny);
+    const int k = (int)(node / ((long long)g.nnx * g.nny));
+    double acc[3] = {0.0, 0.0, 0.0};
+    // ascending element order, products in the working dtype, sum in FP64
+#pragma unroll
+    for (int oz = 0; oz < 2; ++oz)
+#pragma unroll
+        for (int oy = 0; oy < 2; ++oy)
+#pragma unroll
+            for (int ox = 0; ox < 2; ++ox) {
+                const int ex = i - 1 + ox, ey = j - 1 + oy, ez = k - 1 + oz;
+                if (ex < 0 || ex >= g.nelx || ey < 0 || ey >= g.nely || ez < 0 || ez >= g.nelz) continue;
+                const T se = scale[ex + (long long)g.nelx * (ey + (long long)g.nely * ez)];
+                const int a = corner_of(1 - ox, 1 - oy, 1 - oz);
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    const T prod = se * kd.a[3 * a + c];
+                    acc[c] = __dadd_rn(acc[c], (double)prod);
+                }
+            }
+    const unsigned bits = node_fixed ? (unsigned)node_fixed[node] : 0u;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        T d = (T)acc[c];
+        if ((bits >> c) & 1u) d = T(1);
+        diag[3 * node + c] = d;
+        if (inv_diag) inv_diag[3 * node + c] = T(1) / d;
+    }
+}
+
+template <typename T>
+__global__ void k_jacobi_edof(const int32_t* __restrict__ edof, const T* __restrict__ scale,
+                              double* __restrict__ acc, long long n,
+                              const __grid_constant__ KeMat<T> kd)
+{
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < n * NLOC) {
+        const int d = edof[t];
+        const int l = (int)(t % NLOC);
+        if (d >= 0) {
+            const T prod = scale[t / NLOC] * kd.a[l];
+            atomicAdd(acc + d, (double)prod);
+        }
+    }
+}
+
+// energies: total = sum_i u_i * (sum_j K_ij u_j)   (_kernels_numba.py:241-250)
+__device__ __forceinline__ double energy_of(const double u[NLOC], const KeMat<double>& ke)
+{
+    double total = 0.0;
+#pragma unroll
+    for (int r = 0; r < NLOC; ++r) {
+        double row = 0.0;
+#pragma unroll
+        for (int q = 0; q < NLOC; ++q) row = fma(ke.a[r * NLOC + q], u[q], row);
+        total = fma(u[r], row, total);
+    }
+    return total;
+}
+
+__global__ void __launch_bounds__(EDOF_BLOCK)
+k_energies_grid(Grid g, const double* __restrict__ u, double* __restrict__ out,
+                const __grid_constant__ KeMat<double> ke)
+{
+    const long long e = (long long)blockIdx.x * EDOF_BLOCK + threadIdx.x;
+    if (e >= g.n_elem) return;
+    const int ex = (int)(e % g.nelx);
+    const int ey = (int)((e / g.nelx) % g.nely);
+    const int ez = (int)(e / ((long long)g.nelx * g.nely));
+    double ue[NLOC];
+#pragma unroll
+    for (int b = 0; b < 8; ++b) {
+        const long long node = (ex + cx(b)) + (long long)g.nnx * ((ey + cy(b)) + (long long)g.nny * (ez + cz(b)));
+#pragma unroll
+        for (int d = 0; d < 3; ++d) ue[3 * b + d] = u[3 * node + d];
+    }
+    out[e] = energy_of(ue, ke);
+}
+
+__global__ void __launch_bounds__(EDOF_BLOCK)
+k_energies_edof(const int32_t* __restrict__ edof, const double* __restrict__ u,
+                double* __restrict__ out, long long n, const __grid_constant__ KeMat<double> ke)
+{
+    const long long e = (long long)blockIdx.x * EDOF_BLOCK + threadIdx.x;
+    if (e >= n) return;
+    int idx[NLOC];
+    load_edof_row(edof, e, idx);
+    double ue[NLOC];
+#pragma unroll
+    for (int q = 0; q < NLOC; ++q) ue[q] = idx[q] >= 0 ? u[idx[q]] : 0.0;
+    out[e] = energy_of(ue, ke);
+}
+
+}  // namespace tf
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+using namespace tf;
+
+static inline cudaStream_t S(void* p) { return reinterpret_cast<cudaStream_t>(p); }
+
+extern "C" {
+
+const char* tf_last_error(void) { return tf::g_err; }
+int tf_version(void) { return 1; }
+
+int tf_device_count(void)
+{
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+#define TF_GRID_CHECK(g)                                                                  \
+    TF_REQUIRE((g) && (g)->nelx > 0 && (g)->nely > 0 && (g)->nelz > 0, "invalid grid")
+
+int tf_matvec_grid_f32(const tf_grid* g, const float* ke, const float* scale, const float* v,
+                       float* w, const uint8_t* node_fixed, uint32_t flags, int variant,
+                       void* stream)
+{
+    TF_GRID_CHECK(g);
+    TF_REQUIRE(ke && scale && v && w, "null pointer");
+    return launch_grid_pull<float>(make_grid(g), ke, scale, v, w, node_fixed, flags, variant,
+                                   nullptr, S(stream));
+}
+
+int tf_matvec_grid_f64(const tf_grid* g, const double* ke, const double* scale,
+                       const double* v, double* w, const uint8_t* node_fixed, uint32_t flags,
+                       int variant, void* stream)
+{
+    TF_GRID_CHECK(g);
+    TF_REQUIRE(ke && scale && v && w, "null pointer");
+    return launch_grid_pull<double>(make_grid(g), ke, scale, v, w, node_fixed, flags, variant,
+                                    nullptr, S(stream));
+}
+
+int tf_matvec_edof_f32(const int32_t* edof, const float* ke, const float* scale, const float* v,
+                       float* w, int64_t n_elem, int mode, const int32_t* color_elems,
+                       const int64_t* color_offsets, int n_colors, void* stream)
+{
+    TF_REQUIRE(n_elem >= 0 && ke, "bad arguments");
+    return launch_edof<float>(edof, ke, scale, v, w, n_elem, mode, color_elems, color_offsets,
+                              n_colors, S(stream));
+}
+
+int tf_matvec_edof_f64(const int32_t* edof, const double* ke, const double* scale,
+                       const double* v, double* w, int64_t n_elem, int mode,
+                       const int32_t* color_elems, const int64_t* color_offsets, int n_colors,
+                       void* stream)
+{
+    TF_REQUIRE(n_elem >= 0 && ke, "bad arguments");
+    return launch_edof<double>(edof, ke, scale, v, w, n_elem, mode, color_elems, color_offsets,
+                               n_colors, S(stream));
+}
+
+int tf_pass_fixed_f32(const int64_t* fixed, int64_t n_fixed, const float* v, float* w, void* stream)
+{
+    return launch_pass_fixed<float>(fixed, n_fixed, v, w, S(stream));
+}
+
+int tf_pass_fixed_f64(const int64_t* fixed, int64_t n_fixed, const double* v, double* w,
+                      void* stream)
+{
+    return launch_pass_fixed<double>(fixed, n_fixed, v, w, S(stream));
+}
+
+#define TF_GATHER(T, SUF)                                                                     \
+    int tf_gather_##SUF(const int32_t* edof, const T* v, T* u_elem, int64_t n_elem, void* stream) \
+    {                                                                                         \
+        if (n_elem <= 0) return TF_OK;                                                        \
+        const long long n = n_elem * NLOC;                                                    \
+        k_gather<T><<<(unsigned)((n + 255) / 256), 256, 0, S(stream)>>>(edof, v, u_elem, n_elem); \
+        TF_CHECK_LAUNCH();                                                                    \
+        return TF_OK;                                                                         \
+    }
+TF_GATHER(float, f32)
+TF_GATHER(double, f64)
+
+#define TF_GEMM(T, SUF)                                                                       \
+    int tf_gemm_##SUF(const T* u_elem, const T* ke, const T* scale, T* f_elem, int64_t n_elem, \
+                      void* stream)                                                           \
+    {                                                                                         \
+        if (n_elem <= 0) return TF_OK;                                                        \
+        KeMat<T> k;                                                                           \
+        memcpy(k.a, ke, sizeof(k.a));                                                         \
+        k_gemm<T><<<(unsigned)((n_elem + EDOF_BLOCK - 1) / EDOF_BLOCK), EDOF_BLOCK, 0, S(stream)>>>( \
+            u_elem, scale, f_elem, n_elem, k);                                                \
+        TF_CHECK_LAUNCH();                                                                    \
+        return TF_OK;                                                                         \
+    }
+TF_GEMM(float, f32)
+TF_GEMM(double, f64)
+
+#define TF_SCATTER(T, SUF)                                                                    \
+    int tf_scatter_##SUF(const int32_t* edof, const T* f_elem, double* acc, int64_t n_elem,    \
+                         void* stream)                                                        \
+    {                                                                                         \
+        if (n_elem <= 0) return TF_OK;                                                        \
+        const long long n = n_elem * NLOC;                                                    \
+        k_scatter<T><<<(unsigned)((n + 255) / 256), 256, 0, S(stream)>>>(edof, f_elem, acc, n_elem); \
+        TF_CHECK_LAUNCH();                                                                    \
+        return TF_OK;                                                                         \
+    }
+TF_SCATTER(float, f32)
+TF_SCATTER(double, f64)
+
+#define TF_JACOBI(T, SUF)                                                                     \
+    int tf_jacobi_grid_##SUF(const tf_grid* g, const T* ke_diag, const T* scale, T* diag,      \
+                             T* inv_diag, const uint8_t* node_fixed, void* stream)            \
+    {                                                                                         \
+        TF_GRID_CHECK(g);                                                                     \
+        Grid gg = make_grid(g);                                                               \
+        KeMat<T> k;                                                                           \
+        memset(&k, 0, sizeof(k));                                                             \
+        memcpy(k.a, ke_diag, NLOC * sizeof(T));                                               \
+        k_jacobi_grid<T><<<(unsigned)((gg.n_nodes + 255) / 256), 256, 0, S(stream)>>>(          \
+            gg, scale, diag, inv_diag, node_fixed, k);                                        \
+        TF_CHECK_LAUNCH();                                                                    \
+        return TF_OK;                                                                         \
+    }                                                                                         \
+    int tf_jacobi_edof_##SUF(const int32_t* edof, const T* ke_diag, const T* scale, double* acc, \
+                             int64_t n_elem, void* stream)                                    \
+    {                                                                                         \
+        if (n_elem <= 0) return TF_OK;                                                        \
+        KeMat<T> k;                                                                           \
+        memset(&k, 0, sizeof(k));                                                             \
+        memcpy(k.a, ke_diag, NLOC * sizeof(T));                                               \
+        const long long n = n_elem * NLOC;                                                    \
+        k_jacobi_edof<T><<<(unsigned)((n + 255) / 256), 256, 0, S(stream)>>>(edof, scale, acc, n_elem, k); \
+        TF_CHECK_LAUNCH();                                                                    \
+        return TF_OK;                                                                         \
+    }
+TF_JACOBI(float, f32)
+TF_JACOBI(double, f64)
+
+int tf_energies_grid_f64(const tf_grid* g, const double* ke, const double* u, double* out,
+                         void* stream)
+{
+    TF_GRID_CHECK(g);
+    Grid gg = make_grid(g);
+    KeMat<double> k;
+    memcpy(k.a, ke, sizeof(k.a));
+    k_energies_grid<<<(unsigned)((gg.n_elem + EDOF_BLOCK - 1) / EDOF_BLOCK), EDOF_BLOCK, 0, S(stream)>>>(
+        gg, u, out, k);
+    TF_CHECK_LAUNCH();
+    return TF_OK;
+}
+
+int tf_energies_edof_f64(const int32_t* edof, const double* ke, const double* u, double* out,
+                         int64_t n_elem, void* stream)
+{
+    if (n_elem <= 0) return TF_OK;
+    TF_REQUIRE(((uintptr_t)edof & 15u) == 0, "edof must be 16-byte aligned");
+    KeMat<double> k;
+    memcpy(k.a, ke, sizeof(k.a));
+    k_energies_edof<<<(unsigned)((n_elem + EDOF_BLOCK - 1) / EDOF_BLOCK), EDOF_BLOCK, 0, S(stream)>>>(
+        edof, u, out, n_elem, k);
+    TF_CHECK_LAUNCH();
+    return TF_OK;
+}
+
+}  // extern "C"

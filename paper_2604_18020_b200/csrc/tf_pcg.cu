@@ -1,0 +1,668 @@
+// Device-resident Jacobi-PCG -- the recurrence of reference solver.py:57-147.
+//
+// The whole solve is ONE CUDA graph launch.  A conditional WHILE node repeats
+// the body until the device decides to stop; an inner IF node runs the
+// true-residual refresh (solver.py:116-119) every `recompute_every` iterations.
+// Body per iteration (3 kernels, +2 on refresh iterations):
+//
+//   K_mv    q = A p (structured pull kernel) fused with p.q block partials; the
+//           LAST block (ticket counter) sums the partials in fixed order and
+//           decides: it += 1, breakdown / divergence, alpha = rz / pq,
+//           refresh flag -> IF handle.
+//   K_upd   x += alpha p ; r -= alpha q ; partials of r.r and r.(r*inv_diag);
+//           last block: rel, convergence, beta, max_iter -> WHILE handle.
+//   [IF]    K_mv(x) ; K_res: r = b - A x, same partials + decision.
+//   K_pdir  p = r*inv_diag + beta p.
+//
+// Reductions are deterministic (fixed partial order, fixed block tree), so a
+// solve is bitwise reproducible.  Scalar rounding mirrors the reference's
+// numpy semantics: FP32 dots/norms are rounded to float32 before use, alpha
+// and beta are Python-float quotients applied as float32 (NEP 50), and every
+// vector update rounds the product before the add (no FMA), like numpy.
+
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
+#include "tf_common.cuh"
+
+namespace tf {
+
+template <typename T>
+int launch_grid_pull(const Grid& g, const T* ke_host, const T* scale, const T* v, T* w,
+                     const uint8_t* node_fixed, uint32_t flags, int variant, double* dot_part,
+                     cudaStream_t st);
+long long grid_pull_blocks(const Grid& g);
+template <typename T>
+int launch_pass_fixed(const int64_t* fixed, long long n, const T* v, T* w, cudaStream_t st);
+
+enum { TERM_CONVERGED = 0, TERM_MAX_ITER = 1, TERM_BREAKDOWN = 2, TERM_DIVERGED = 3 };
+
+struct CgScalars {
+    double bnorm, rz, rz_old, alpha, beta, rel, tol;
+    double* hist;
+    int it, done, term, matvecs, refresh, max_iter, recompute, zero_rhs;
+};
+
+template <typename T>
+struct CgP {
+    T *x, *r, *p, *q;
+    const T *b, *inv;
+    double* part;           // [n_part_max * 3]
+    unsigned* tickets;      // [4]
+    CgScalars* sc;
+    long long n;
+    cudaGraphConditionalHandle h_while, h_refresh;
+};
+
+__device__ __forceinline__ double rnd(double v, bool f32) { return f32 ? (double)(float)v : v; }
+__device__ __forceinline__ double vsqrt(double v, bool f32)
+{
+    return f32 ? (double)sqrtf((float)v) : sqrt(v);
+}
+
+// product-then-add with the rounding numpy applies (never contracted to FMA)
+__device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ float sub_rn(float a, float b) { return __fsub_rn(a, b); }
+__device__ __forceinline__ double sub_rn(double a, double b) { return __dsub_rn(a, b); }
+
+constexpr int VEC_BLOCK = 256;
+
+// deterministic block sum of K values per thread; result valid in thread 0
+template <int K>
+__device__ __forceinline__ void block_sum_k(double (&v)[K], double* sh /* [K*32] */)
+{
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v[k] += __shfl_down_sync(0xffffffffu, v[k], o);
+    }
+    if (lane == 0) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) sh[k * 32 + wid] = v[k];
+    }
+    __syncthreads();
+    if (tid == 0) {
+        const int nw = (blockDim.x + 31) / 32;
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            double s = 0.0;
+            for (int i = 0; i < nw; ++i) s += sh[k * 32 + i];
+            v[k] = s;
+        }
+    }
+    __syncthreads();
+}
+
+// Publish this block's K partials; returns true in the (unique) last block,
+// whose thread 0 then holds the fixed-order totals in `tot`.
+template <int K>
+__device__ bool last_block_reduce(double (&v)[K], double* part, unsigned* ticket, int nblocks,
+                                  double (&tot)[K])
+{
+    __shared__ double sh[K * 32];
+    __shared__ bool am_last;
+    const int bid = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+    const int tid = threadIdx.x + blockDim.x * (threadIdx.y + blockDim.y * threadIdx.z);
+    const int nthr = blockDim.x * blockDim.y * blockDim.z;
+    // block tree (threads flattened)
+    {
+        const int lane = tid & 31, wid = tid >> 5;
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) v[k] += __shfl_down_sync(0xffffffffu, v[k], o);
+        }
+        if (lane == 0) {
+#pragma unroll
+            for (int k = 0; k < K; ++k) sh[k * 32 + wid] = v[k];
+        }
+        __syncthreads();
+        if (tid == 0) {
+            const int nw = (nthr + 31) / 32;
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                double s = 0.0;
+                for (int i = 0; i < nw; ++i) s += sh[k * 32 + i];
+                part[(size_t)bid * K + k] = s;
+            }
+            __threadfence();
+            const unsigned t = atomicAdd(ticket, 1u);
+            am_last = (t == (unsigned)nblocks - 1);
+        }
+        __syncthreads();
+    }
+    if (!am_last) return false;
+    __threadfence();
+    // fixed-order reduction of all partials: thread t sums partials t, t+nthr, ...
+    double acc[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) acc[k] = 0.0;
+    for (int i = tid; i < nblocks; i += nthr) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) acc[k] += __ldcg(part + (size_t)i * K + k);
+    }
+    {
+        const int lane = tid & 31, wid = tid >> 5;
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) acc[k] += __shfl_down_sync(0xffffffffu, acc[k], o);
+        }
+        __syncthreads();
+        if (lane == 0) {
+#pragma unroll
+            for (int k = 0; k < K; ++k) sh[k * 32 + wid] = acc[k];
+        }
+        __syncthreads();
+        if (tid == 0) {
+            const int nw = (nthr + 31) / 32;
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                double s = 0.0;
+                for (int i = 0; i < nw; ++i) s += sh[k * 32 + i];
+                tot[k] = s;
+            }
+            *ticket = 0u;  // re-arm for the next launch
+        }
+    }
+    return true;
+}
+
+// ---- decisions -------------------------------------------------------------
+
+template <typename T>
+__device__ void decide_after_pq(const CgP<T>& P, double pq_raw)
+{
+    CgScalars* sc = P.sc;
+    const bool f32 = sizeof(T) == 4;
+    const double pq = rnd(pq_raw, f32);
+    const double rz = sc->rz;
+    sc->it += 1;
+    sc->matvecs += 1;
+    const int it = sc->it;
+    int refresh = 0;
+    if (!isfinite(pq) || !isfinite(rz)) {
+        sc->done = 1;
+        sc->term = TERM_DIVERGED;
+    } else if (pq <= 0.0) {
+        sc->done = 1;
+        sc->term = TERM_BREAKDOWN;
+    } else {
+        sc->alpha = rz / pq;
+        sc->rz_old = rz;
+        refresh = (sc->recompute > 0 && it % sc->recompute == 0) ? 1 : 0;
+    }
+    sc->refresh = refresh;
+    cudaGraphSetConditional(P.h_refresh, refresh ? 1u : 0u);
+    if (sc->done) cudaGraphSetConditional(P.h_while, 0u);
+}
+
+template <typename T>
+__device__ void decide_after_residual(const CgP<T>& P, double rr_raw, double rz_raw)
+{
+    CgScalars* sc = P.sc;
+    const bool f32 = sizeof(T) == 4;
+    const double rn = vsqrt(rnd(rr_raw, f32), f32);
+    const int it = sc->it;
+    if (!isfinite(rn)) {
+        sc->done = 1;
+        sc->term = TERM_DIVERGED;
+    } else {
+        const double rel = rn / sc->bnorm;
+        sc->rel = rel;
+        if (sc->hist) sc->hist[it] = rel;
+        if (rel <= sc->tol) {
+            sc->done = 1;
+            sc->term = TERM_CONVERGED;
+        } else {
+            const double rz_new = rnd(rz_raw, f32);
+            sc->beta = rz_new / sc->rz_old;
+            sc->rz = rz_new;
+            if (it >= sc->max_iter) {
+                sc->done = 1;
+                sc->term = TERM_MAX_ITER;
+            }
+        }
+    }
+    cudaGraphSetConditional(P.h_while, sc->done ? 0u : 1u);
+}
+
+// ---- kernels -----------------------------------------------------------------
+
+// structured K p fused with the p.q reduction (+ decision in the last block)
+// is k_grid_pull<..., DOT=true>; the decision runs in this small follow-up
+// "tail" when the reduction is done by the generic dot kernel below.
+
+template <typename T>
+__global__ void __launch_bounds__(VEC_BLOCK) k_dot_pq(CgP<T> P, int nblocks_mv)
+{
+    // Reduce matvec-block partials (already written to part[0..nblocks_mv))
+    // OR compute p.q directly when nblocks_mv < 0 (edof mode).
+    if (P.sc->done) return;
+    double v[1] = {0.0};
+    if (nblocks_mv < 0) {
+        const long long stride = (long long)gridDim.x * VEC_BLOCK;
+        for (long long i = (long long)blockIdx.x * VEC_BLOCK + threadIdx.x; i < P.n; i += stride)
+            v[0] += (double)P.p[i] * (double)P.q[i];
+        double tot[1];
+        if (last_block_reduce<1>(v, P.part, P.tickets + 0, gridDim.x, tot) && threadIdx.x == 0)
+            decide_after_pq(P, tot[0]);
+    } else {
+        // single block: fixed-order sum of the matvec partials
+        for (int i = threadIdx.x; i < nblocks_mv; i += VEC_BLOCK) v[0] += __ldcg(P.part + i);
+        __shared__ double sh[32];
+        block_sum_k<1>(v, sh);
+        if (threadIdx.x == 0) decide_after_pq(P, v[0]);
+    }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(VEC_BLOCK) k_update(CgP<T> P)
+{
+    const CgScalars* sc = P.sc;
+    if (sc->done) return;
+    const T a = (T)sc->alpha;
+    const bool refresh = sc->refresh != 0;
+    double v[2] = {0.0, 0.0};
+    const long long stride = (long long)gridDim.x * VEC_BLOCK;
+    for (long long i = (long long)blockIdx.x * VEC_BLOCK + threadIdx.x; i < P.n; i += stride) {
+        P.x[i] = add_rn(P.x[i], mul_rn(a, P.p[i]));
+        if (!refresh) {
+            const T r = sub_rn(P.r[i], mul_rn(a, P.q[i]));
+            P.r[i] = r;
+            const T z = mul_rn(r, P.inv[i]);
+            v[0] += (double)r * (double)r;
+            v[1] += (double)r * (double)z;
+        }
+    }
+    if (refresh) return;
+    double tot[2];
+    if (last_block_reduce<2>(v, P.part, P.tickets + 1, gridDim.x, tot) && threadIdx.x == 0)
+        decide_after_residual(P, tot[0], tot[1]);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(VEC_BLOCK) k_residual(CgP<T> P)
+{
+    // refresh: r = b - A x  (q holds A x)
+    if (P.sc->done) return;
+    double v[2] = {0.0, 0.0};
+    const long long stride = (long long)gridDim.x * VEC_BLOCK;
+    for (long long i = (long long)blockIdx.x * VEC_BLOCK + threadIdx.x; i < P.n; i += stride) {
+        const T r = sub_rn(P.b[i], P.q[i]);
+        P.r[i] = r;
+        const T z = mul_rn(r, P.inv[i]);
+        v[0] += (double)r * (double)r;
+        v[1] += (double)r * (double)z;
+    }
+    double tot[2];
+    if (last_block_reduce<2>(v, P.part, P.tickets + 2, gridDim.x, tot) && threadIdx.x == 0) {
+        P.sc->matvecs += 1;
+        decide_after_residual(P, tot[0], tot[1]);
+    }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(VEC_BLOCK) k_direction(CgP<T> P)
+{
+    if (P.sc->done) return;
+    const T be = (T)P.sc->beta;
+    const long long stride = (long long)gridDim.x * VEC_BLOCK;
+    for (long long i = (long long)blockIdx.x * VEC_BLOCK + threadIdx.x; i < P.n; i += stride) {
+        const T z = mul_rn(P.r[i], P.inv[i]);
+        P.p[i] = add_rn(z, mul_rn(be, P.p[i]));
+    }
+}
+
+// init: r = b - q (has_x0) or r = b; p = r*inv; partials b.b, r.r, r.z
+template <typename T>
+__global__ void __launch_bounds__(VEC_BLOCK) k_init(CgP<T> P, int has_x0)
+{
+    double v[3] = {0.0, 0.0, 0.0};
+    const long long stride = (long long)gridDim.x * VEC_BLOCK;
+    for (long long i = (long long)blockIdx.x * VEC_BLOCK + threadIdx.x; i < P.n; i += stride) {
+        const T b = P.b[i];
+        const T r = has_x0 ? sub_rn(b, P.q[i]) : b;
+        P.r[i] = r;
+        const T z = mul_rn(r, P.inv[i]);
+        P.p[i] = z;
+        v[0] += (double)b * (double)b;
+        v[1] += (double)r * (double)r;
+        v[2] += (double)r * (double)z;
+    }
+    double tot[3];
+    if (last_block_reduce<3>(v, P.part, P.tickets + 3, gridDim.x, tot) && threadIdx.x == 0) {
+        CgScalars* sc = P.sc;
+        const bool f32 = sizeof(T) == 4;
+        sc->bnorm = vsqrt(rnd(tot[0], f32), f32);
+        sc->it = 0;
+        sc->matvecs = has_x0 ? 1 : 0;
+        sc->done = 0;
+        sc->term = TERM_MAX_ITER;
+        sc->zero_rhs = 0;
+        if (sc->bnorm == 0.0) {
+            sc->zero_rhs = 1;
+            sc->done = 1;
+            sc->term = TERM_CONVERGED;
+            sc->rel = 0.0;
+            if (sc->hist) sc->hist[0] = 0.0;
+            return;
+        }
+        sc->rz = rnd(tot[2], f32);
+        const double rel = vsqrt(rnd(tot[1], f32), f32) / sc->bnorm;
+        sc->rel = rel;
+        if (sc->hist) sc->hist[0] = rel;
+        if (rel <= sc->tol) {
+            sc->done = 1;
+            sc->term = TERM_CONVERGED;
+        } else if (sc->max_iter <= 0) {
+            sc->done = 1;
+        }
+    }
+}
+
+// ---- handle --------------------------------------------------------------------
+
+struct PcgImpl {
+    int prec;
+    int structured;
+    Grid grid;
+    const int32_t* edof;
+    long long n_elem, n_dof;
+    std::vector<unsigned char> ke;  // host copy (576 * sizeof(T))
+    const uint8_t* node_fixed;
+    const int64_t* fixed;
+    long long n_fixed;
+    int variant;
+    cudaStream_t stream;
+    // device buffers
+    void *x, *r, *p, *q, *b, *inv, *scale;
+    double* part;
+    unsigned* tickets;
+    CgScalars* sc;
+    CgScalars* sc_host;  // pinned
+    int n_vec_blocks;
+    long long n_mv_blocks;
+    cudaGraph_t graph;
+    cudaGraphExec_t exec;
+    cudaGraphConditionalHandle h_while, h_refresh;
+};
+
+template <typename T>
+static CgP<T> params_of(PcgImpl* h)
+{
+    CgP<T> P;
+    P.x = (T*)h->x; P.r = (T*)h->r; P.p = (T*)h->p; P.q = (T*)h->q;
+    P.b = (const T*)h->b; P.inv = (const T*)h->inv;
+    P.part = h->part; P.tickets = h->tickets; P.sc = h->sc; P.n = h->n_dof;
+    P.h_while = h->h_while; P.h_refresh = h->h_refresh;
+    return P;
+}
+
+// Enqueue A*v -> w on stream (used while capturing the body graphs).
+template <typename T>
+static int enqueue_matvec(PcgImpl* h, const T* v, T* w, double* dot_part, cudaStream_t st)
+{
+    const T* ke = (const T*)h->ke.data();
+    if (h->structured) {
+        return launch_grid_pull<T>(h->grid, ke, (const T*)h->scale, v, w, h->node_fixed,
+                                   TF_MASK_INPUT | TF_PASS_FIXED, h->variant, dot_part, st);
+    }
+    TF_CUDA_TRY(cudaMemsetAsync(w, 0, sizeof(T) * h->n_dof, st));
+    int rc = (sizeof(T) == 4)
+                 ? tf_matvec_edof_f32(h->edof, (const float*)ke, (const float*)h->scale,
+                                      (const float*)v, (float*)w, h->n_elem, TF_SCATTER_ATOMIC,
+                                      nullptr, nullptr, 0, st)
+                 : tf_matvec_edof_f64(h->edof, (const double*)ke, (const double*)h->scale,
+                                      (const double*)v, (double*)w, h->n_elem, TF_SCATTER_ATOMIC,
+                                      nullptr, nullptr, 0, st);
+    if (rc) return rc;
+    return launch_pass_fixed<T>(h->fixed, h->n_fixed, v, w, st);
+}
+
+// Add a captured sequence as the content of `body` (a conditional body graph).
+template <typename F>
+static int capture_into(cudaGraph_t body, cudaStream_t cap, F&& fn)
+{
+    TF_CUDA_TRY(cudaStreamBeginCaptureToGraph(cap, body, nullptr, nullptr, 0,
+                                              cudaStreamCaptureModeThreadLocal));
+    const int rc = fn(cap);
+    cudaGraph_t out = nullptr;
+    const cudaError_t e = cudaStreamEndCapture(cap, &out);
+    if (rc) return rc;
+    if (e != cudaSuccess) {
+        set_error("end capture: %s", cudaGetErrorString(e));
+        return TF_ERR_CUDA;
+    }
+    return TF_OK;
+}
+
+template <typename T>
+static int build_graph(PcgImpl* h)
+{
+    cudaStream_t cap;
+    TF_CUDA_TRY(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
+    TF_CUDA_TRY(cudaGraphCreate(&h->graph, 0));
+    TF_CUDA_TRY(cudaGraphConditionalHandleCreate(&h->h_while, h->graph, 1, cudaGraphCondAssignDefault));
+
+    cudaGraphNodeParams wp = {};
+    wp.type = cudaGraphNodeTypeConditional;
+    wp.conditional.handle = h->h_while;
+    wp.conditional.type = cudaGraphCondTypeWhile;
+    wp.conditional.size = 1;
+    cudaGraphNode_t wnode;
+    TF_CUDA_TRY(cudaGraphAddNode(&wnode, h->graph, nullptr, 0, &wp));
+    cudaGraph_t body = wp.conditional.phGraph_out[0];
+
+    TF_CUDA_TRY(cudaGraphConditionalHandleCreate(&h->h_refresh, body, 0, 0));
+    CgP<T> P = params_of<T>(h);
+    const int nvb = h->n_vec_blocks;
+
+    // part 1: matvec+dot, update
+    cudaGraphNode_t last_node = nullptr;
+    {
+        int rc = capture_into(body, cap, [&](cudaStream_t st) -> int {
+            if (h->structured && h->variant == TF_GRID_FAST) {
+                int r = launch_grid_pull<T>(h->grid, (const T*)h->ke.data(), (const T*)h->scale,
+                                            P.p, P.q, h->node_fixed, TF_MASK_INPUT | TF_PASS_FIXED,
+                                            h->variant, h->part, st);
+                if (r) return r;
+                k_dot_pq<T><<<1, VEC_BLOCK, 0, st>>>(P, (int)h->n_mv_blocks);
+            } else {
+                int r = enqueue_matvec<T>(h, P.p, P.q, nullptr, st);
+                if (r) return r;
+                k_dot_pq<T><<<nvb, VEC_BLOCK, 0, st>>>(P, -1);
+            }
+            TF_CHECK_LAUNCH();
+            k_update<T><<<nvb, VEC_BLOCK, 0, st>>>(P);
+            TF_CHECK_LAUNCH();
+            return TF_OK;
+        });
+        if (rc) return rc;
+    }
+    // find the sink node of the body so far
+    {
+        size_t n = 0;
+        TF_CUDA_TRY(cudaGraphGetNodes(body, nullptr, &n));
+        std::vector<cudaGraphNode_t> nodes(n);
+        TF_CUDA_TRY(cudaGraphGetNodes(body, nodes.data(), &n));
+        for (auto nd : nodes) {
+            size_t nout = 0;
+            TF_CUDA_TRY(cudaGraphNodeGetDependentNodes(nd, nullptr, &nout));
+            if (nout == 0) last_node = nd;
+        }
+    }
+    // IF refresh { q = A x ; r = b - q }
+    cudaGraphNodeParams ip = {};
+    ip.type = cudaGraphNodeTypeConditional;
+    ip.conditional.handle = h->h_refresh;
+    ip.conditional.type = cudaGraphCondTypeIf;
+    ip.conditional.size = 1;
+    cudaGraphNode_t inode;
+    TF_CUDA_TRY(cudaGraphAddNode(&inode, body, &last_node, 1, &ip));
+    cudaGraph_t ifbody = ip.conditional.phGraph_out[0];
+    {
+        int rc = capture_into(ifbody, cap, [&](cudaStream_t st) -> int {
+            int r = enqueue_matvec<T>(h, P.x, P.q, nullptr, st);
+            if (r) return r;
+            k_residual<T><<<nvb, VEC_BLOCK, 0, st>>>(P);
+            TF_CHECK_LAUNCH();
+            return TF_OK;
+        });
+        if (rc) return rc;
+    }
+    // direction update after the IF node
+    {
+        cudaKernelNodeParams kp = {};
+        void* args[] = {&P};
+        kp.func = (void*)k_direction<T>;
+        kp.gridDim = dim3(nvb);
+        kp.blockDim = dim3(VEC_BLOCK);
+        kp.kernelParams = args;
+        cudaGraphNode_t dn;
+        TF_CUDA_TRY(cudaGraphAddKernelNode(&dn, body, &inode, 1, &kp));
+    }
+    TF_CUDA_TRY(cudaGraphInstantiate(&h->exec, h->graph, 0));
+    cudaStreamDestroy(cap);
+    return TF_OK;
+}
+
+template <typename T>
+static int solve_impl(PcgImpl* h, const void* scale, const void* b, const void* inv, void* x,
+                      int has_x0, double tol, int max_iter, int recompute, double* history,
+                      tf_pcg_report* rep)
+{
+    cudaStream_t st = h->stream;
+    const size_t vb = sizeof(T) * h->n_dof;
+    TF_CUDA_TRY(cudaMemcpyAsync(h->scale, scale, sizeof(T) * h->n_elem, cudaMemcpyDeviceToDevice, st));
+    TF_CUDA_TRY(cudaMemcpyAsync(h->b, b, vb, cudaMemcpyDeviceToDevice, st));
+    TF_CUDA_TRY(cudaMemcpyAsync(h->inv, inv, vb, cudaMemcpyDeviceToDevice, st));
+    if (has_x0)
+        TF_CUDA_TRY(cudaMemcpyAsync(h->x, x, vb, cudaMemcpyDeviceToDevice, st));
+    else
+        TF_CUDA_TRY(cudaMemsetAsync(h->x, 0, vb, st));
+    CgScalars init = {};
+    init.tol = tol;
+    init.max_iter = max_iter;
+    init.recompute = recompute;
+    init.hist = history;
+    *h->sc_host = init;
+    TF_CUDA_TRY(cudaMemcpyAsync(h->sc, h->sc_host, sizeof(CgScalars), cudaMemcpyHostToDevice, st));
+    CgP<T> P = params_of<T>(h);
+    if (has_x0) {
+        int rc = enqueue_matvec<T>(h, P.x, P.q, nullptr, st);
+        if (rc) return rc;
+    }
+    k_init<T><<<h->n_vec_blocks, VEC_BLOCK, 0, st>>>(P, has_x0);
+    TF_CHECK_LAUNCH();
+    TF_CUDA_TRY(cudaMemcpyAsync(h->sc_host, h->sc, sizeof(CgScalars), cudaMemcpyDeviceToHost, st));
+    TF_CUDA_TRY(cudaStreamSynchronize(st));
+    if (!h->sc_host->done) {
+        TF_CUDA_TRY(cudaGraphLaunch(h->exec, st));
+        TF_CUDA_TRY(cudaMemcpyAsync(h->sc_host, h->sc, sizeof(CgScalars), cudaMemcpyDeviceToHost, st));
+    }
+    if (h->sc_host->zero_rhs)
+        TF_CUDA_TRY(cudaMemsetAsync(x, 0, vb, st));
+    else
+        TF_CUDA_TRY(cudaMemcpyAsync(x, h->x, vb, cudaMemcpyDeviceToDevice, st));
+    TF_CUDA_TRY(cudaStreamSynchronize(st));
+    const CgScalars& s = *h->sc_host;
+    rep->iterations = s.it;
+    rep->termination = s.term;
+    rep->matvecs = s.matvecs;
+    rep->rel_residual = s.rel;
+    return TF_OK;
+}
+
+}  // namespace tf
+
+using namespace tf;
+
+extern "C" {
+
+int tf_pcg_create(tf_pcg** out, const tf_pcg_desc* d, void* stream)
+{
+    TF_REQUIRE(out && d, "null argument");
+    TF_REQUIRE(d->precision == 32 || d->precision == 64, "precision must be 32 or 64");
+    TF_REQUIRE(d->n_dof > 0 && d->n_elem > 0 && d->ke, "empty problem");
+    PcgImpl* h = new PcgImpl();
+    h->prec = d->precision;
+    h->structured = d->structured;
+    if (d->structured) h->grid = make_grid(&d->grid);
+    h->edof = d->edof;
+    h->n_elem = d->n_elem;
+    h->n_dof = d->n_dof;
+    const size_t es = d->precision == 32 ? 4 : 8;
+    h->ke.assign((const unsigned char*)d->ke, (const unsigned char*)d->ke + 576 * es);
+    h->node_fixed = d->node_fixed;
+    h->fixed = d->fixed;
+    h->n_fixed = d->n_fixed;
+    h->variant = d->grid_variant;
+    h->stream = reinterpret_cast<cudaStream_t>(stream);
+    h->graph = nullptr;
+    h->exec = nullptr;
+    h->x = h->r = h->p = h->q = h->b = h->inv = h->scale = nullptr;
+    h->part = nullptr;
+    h->tickets = nullptr;
+    h->sc = nullptr;
+    h->sc_host = nullptr;
+    TF_REQUIRE(d->structured || d->edof, "edof required for unstructured problems");
+
+    int dev = 0, nsm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    const long long want = (d->n_dof + VEC_BLOCK * 4 - 1) / (VEC_BLOCK * 4);
+    h->n_vec_blocks = (int)std::min<long long>(std::max<long long>(want, 1), (long long)nsm * 4);
+    h->n_mv_blocks = d->structured ? grid_pull_blocks(h->grid) : 0;
+    const size_t vb = es * d->n_dof;
+    void** bufs[] = {&h->x, &h->r, &h->p, &h->q, &h->b, &h->inv};
+    for (void** pb : bufs) TF_CUDA_TRY(cudaMalloc(pb, vb));
+    TF_CUDA_TRY(cudaMalloc(&h->scale, es * d->n_elem));
+    const long long npart = std::max<long long>(h->n_mv_blocks, h->n_vec_blocks) * 3 + 8;
+    TF_CUDA_TRY(cudaMalloc(&h->part, sizeof(double) * npart));
+    TF_CUDA_TRY(cudaMalloc(&h->tickets, sizeof(unsigned) * 8));
+    TF_CUDA_TRY(cudaMemset(h->tickets, 0, sizeof(unsigned) * 8));
+    TF_CUDA_TRY(cudaMalloc(&h->sc, sizeof(CgScalars)));
+    TF_CUDA_TRY(cudaMallocHost(&h->sc_host, sizeof(CgScalars)));
+    int rc = d->precision == 32 ? build_graph<float>(h) : build_graph<double>(h);
+    if (rc) {
+        tf_pcg_destroy(reinterpret_cast<tf_pcg*>(h));
+        return rc;
+    }
+    *out = reinterpret_cast<tf_pcg*>(h);
+    return TF_OK;
+}
+
+int tf_pcg_solve(tf_pcg* hh, const void* scale, const void* b, const void* inv_diag, void* x,
+                 int has_x0, double rel_tol, int32_t max_iter, int32_t recompute_every,
+                 double* history, tf_pcg_report* report)
+{
+    PcgImpl* h = reinterpret_cast<PcgImpl*>(hh);
+    TF_REQUIRE(h && scale && b && inv_diag && x && report, "null argument");
+    TF_REQUIRE(rel_tol > 0 && max_iter >= 1 && recompute_every >= 0, "invalid CG configuration");
+    return h->prec == 32 ? solve_impl<float>(h, scale, b, inv_diag, x, has_x0, rel_tol, max_iter,
+                                             recompute_every, history, report)
+                         : solve_impl<double>(h, scale, b, inv_diag, x, has_x0, rel_tol, max_iter,
+                                              recompute_every, history, report);
+}
+
+int tf_pcg_destroy(tf_pcg* hh)
+{
+    PcgImpl* h = reinterpret_cast<PcgImpl*>(hh);
+    if (!h) return TF_OK;
+    if (h->exec) cudaGraphExecDestroy(h->exec);
+    if (h->graph) cudaGraphDestroy(h->graph);
+    void* bufs[] = {h->x, h->r, h->p, h->q, h->b, h->inv, h->scale, h->part, h->tickets, h->sc};
+    for (void* p : bufs)
+        if (p) cudaFree(p);
+    if (h->sc_host) cudaFreeHost(h->sc_host);
+    delete h;
+    return TF_OK;
+}
+
+}  // extern "C"

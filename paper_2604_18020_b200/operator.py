@@ -1,0 +1,421 @@
+"""Matrix-free stiffness operator on B200 (mirrors reference operator.py:38-268).
+
+``MatFreeOperator`` keeps the reference constructor and methods (apply,
+__call__, diagonal, apply_fp64, element_energies, compliance, n_apply) and the
+traffic/roofline helpers, but every evaluation runs in libtopofuse_b200.so on
+the current CUDA device:
+
+  * structured grids (edof == build_edof(mesh)): the index-free pull kernel
+    (one thread per node, no atomics, deterministic) with input masking and
+    fixed-DOF pass-through fused in -- ONE launch per apply;
+  * any other edof: the element-per-thread kernel with red.global.add
+    (scatter="parallel_atomic") or colour-ordered deterministic passes
+    (scatter="serial"), constrained slots masked in the device edof copy;
+  * variant="three_stage": gather -> batched element product -> FP64
+    histogram scatter, intermediates genuinely materialised (operator.py:103-114).
+
+Inputs may be numpy arrays (copied to/from the device, as a drop-in) or
+torch CUDA tensors (stay resident; results are tensors).
+"""
+
+from __future__ import annotations
+
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _device as D
+from . import _lib
+from .element import SimpParams, simp_scale, unit_stiffness
+from .mesh import BoundaryConditions, StructuredMesh, edof_is_structured
+from .precision import FP64, Precision, get_precision
+
+VARIANTS = ("three_stage", "fused")
+SCATTER_MODES = ("serial", "parallel_atomic")
+BACKENDS = ("b200",)
+
+FLOPS_PER_ELEMENT = 2 * 24 * 24
+INDEX_BYTES_PER_ELEMENT = 24 * 4
+DENSITY_BYTES_PER_ELEMENT = 4
+
+ENV_EXACT = "TOPOFUSE_B200_EXACT"  # 1 -> bitwise numba-order kernels for structured grids
+
+
+class DeviceProblem:
+    """Device-resident connectivity/constraint data shared by every operator
+    built on the same (mesh, edof, bcs) -- run_simp rebuilds the operator each
+    iteration (simp.py:358-369) but this is uploaded once."""
+
+    def __init__(self, mesh: StructuredMesh, edof: np.ndarray, bcs: BoundaryConditions):
+        self.mesh = mesh
+        self.n_dof = mesh.n_dof
+        self.n_elem = mesh.n_elem
+        self.structured = edof_is_structured(mesh, edof)
+        self.fixed_np = np.asarray(bcs.fixed_dofs, dtype=np.int64)
+        self.fixed = D.to_dev(self.fixed_np, np.int64) if self.fixed_np.size else None
+        self.node_fixed = D.to_dev(D.node_fixed_mask(mesh.n_nodes, self.fixed_np), np.uint8)
+        self.grid = _lib.tf_grid(mesh.nelx, mesh.nely, mesh.nelz)
+        self._edof_np = edof
+        self._edof_masked = None
+        self._edof_raw = None
+        self._colors = None
+        self.pcg_handles = {}
+
+    @property
+    def edof_masked(self):
+        if self._edof_masked is None:
+            self._edof_masked = D.to_dev(D.masked_edof(self._edof_np, self.fixed_np, self.n_dof), np.int32)
+        return self._edof_masked
+
+    @property
+    def edof_raw(self):
+        if self._edof_raw is None:
+            self._edof_raw = D.to_dev(np.ascontiguousarray(self._edof_np, dtype=np.int32), np.int32)
+        return self._edof_raw
+
+    def colors(self):
+        """Element colouring with no two same-colour elements sharing a DOF."""
+        if self._colors is None:
+            order, offsets = element_colouring(self.mesh, self._edof_np)
+            self._colors = (D.to_dev(order, np.int32), np.ascontiguousarray(offsets, dtype=np.int64))
+        return self._colors
+
+    def __del__(self):
+        for h in getattr(self, "pcg_handles", {}).values():
+            try:
+                _lib.load().tf_pcg_destroy(h)
+            except Exception:  # pragma: no cover - interpreter teardown
+                pass
+
+
+def element_colouring(mesh: StructuredMesh, edof: np.ndarray):
+    """Grid-parity colouring (8 colours) validated against edof; greedy otherwise."""
+    e = np.arange(mesh.n_elem, dtype=np.int64)
+    ex = e % mesh.nelx
+    ey = (e // mesh.nelx) % mesh.nely
+    ez = e // (mesh.nelx * mesh.nely)
+    col = (ex & 1) | ((ey & 1) << 1) | ((ez & 1) << 2)
+    ok = True
+    for c in range(8):
+        rows = edof[col == c]
+        if rows.size and np.unique(rows).size != rows.size:
+            ok = False
+            break
+    if not ok:
+        if mesh.n_elem > 300_000:
+            raise NotImplementedError("greedy colouring of large non-grid connectivity")
+        owner = {}
+        col = np.zeros(mesh.n_elem, dtype=np.int64)
+        used_by_dof = [set() for _ in range(int(edof.max()) + 1)]
+        for i in range(mesh.n_elem):
+            taken = set()
+            for d in edof[i]:
+                taken |= used_by_dof[d]
+            c = 0
+            while c in taken:
+                c += 1
+            col[i] = c
+            for d in edof[i]:
+                used_by_dof[d].add(c)
+        del owner
+    order = np.argsort(col, kind="stable").astype(np.int32)
+    counts = np.bincount(col, minlength=int(col.max()) + 1)
+    offsets = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+    return order, offsets
+
+
+def device_problem(mesh, edof, bcs) -> DeviceProblem:
+    key = (mesh.nelx, mesh.nely, mesh.nelz, id(bcs))
+
+    def make():
+        return DeviceProblem(mesh, edof, bcs)
+
+    return D.CACHE.get(edof, key, make)
+
+
+def _sfx(dtype) -> str:
+    return "f64" if np.dtype(dtype) == np.float64 else "f32"
+
+
+class MatFreeOperator:
+    """Matrix-free K(rho) (reference operator.py:38-162) evaluated on B200."""
+
+    def __init__(
+        self,
+        mesh: StructuredMesh,
+        edof: np.ndarray,
+        bcs: BoundaryConditions,
+        density: np.ndarray,
+        simp: SimpParams = SimpParams(),
+        precision: Precision | str = FP64,
+        variant: str = "fused",
+        scatter: str = "serial",
+        nu: float = 0.3,
+        backend: str | None = None,
+        exact: bool | None = None,
+    ):
+        if variant not in VARIANTS:
+            raise ValueError(f"variant must be one of {VARIANTS}")
+        if scatter not in SCATTER_MODES:
+            raise ValueError(f"scatter must be one of {SCATTER_MODES}")
+        if backend not in (None,) + BACKENDS:
+            raise ValueError(f"unknown backend {backend!r}, expected b200")
+        self.precision = get_precision(precision) if isinstance(precision, str) else precision
+        if self.precision.quantized:
+            raise ValueError("bf16 is not on the B200 production path (documented negative "
+                             "result, PAPER.md:1522-1552); use fp32 or fp64")
+        self.mesh = mesh
+        self.edof = edof
+        self.bcs = bcs
+        self.simp = simp
+        self.variant = variant
+        self.scatter = scatter
+        self.nu = nu
+        self.backend_name = "b200"
+        self.n_dof = mesh.n_dof
+        self.fixed_dofs = bcs.fixed_dofs
+        self.density = np.asarray(density, dtype=np.float64)
+        if self.density.shape != (mesh.n_elem,):
+            raise ValueError("density must have one entry per element")
+        self.exact = bool(int(os.environ.get(ENV_EXACT, "0"))) if exact is None else bool(exact)
+
+        self.ke64 = unit_stiffness(nu)
+        self.scale64 = np.asarray(simp_scale(self.density, simp), dtype=np.float64)
+        dt = self.precision.dtype
+        self.ke = np.ascontiguousarray(self.ke64, dtype=dt)
+        self.scale = self.scale64.astype(dt)
+        self.n_apply = 0
+
+        self.dev = device_problem(mesh, edof, bcs)
+        self._scale_dev = D.to_dev(self.scale, dt)
+        self._scale64_dev = None
+
+    # -- masks -------------------------------------------------------------------
+    @property
+    def free_mask(self) -> np.ndarray:
+        return self.bcs.free_mask(self.n_dof)
+
+    @property
+    def structured(self) -> bool:
+        return self.dev.structured
+
+    @property
+    def grid_variant(self) -> int:
+        return _lib.TF_GRID_BITWISE if self.exact else _lib.TF_GRID_FAST
+
+    # -- device-level entry points (torch tensors in, torch tensors out) ----------
+    def apply_device(self, x, out=None, ke=None, scale=None, dtype=None):
+        """w = K x on device (masked input, fixed pass-through), one launch on a grid."""
+        t = D.torch()
+        dt = np.dtype(dtype or self.precision.dtype)
+        ke = self.ke if ke is None else ke
+        scale = self._scale_dev if scale is None else scale
+        if out is None:
+            out = t.empty(self.n_dof, dtype=D.tdtype(dt), device=x.device)
+        sfx = _sfx(dt)
+        st = D.stream_ptr()
+        dev = self.dev
+        if self.variant == "fused" and dev.structured:
+            _lib.call(f"tf_matvec_grid_{sfx}", ctypes_ref(dev.grid), ke.ctypes.data, D.ptr(scale),
+                      D.ptr(x), D.ptr(out), D.ptr(dev.node_fixed),
+                      _lib.TF_MASK_INPUT | _lib.TF_PASS_FIXED, self.grid_variant, st)
+            return out
+        if self.variant == "fused":
+            out.zero_()
+            if self.scatter == "parallel_atomic":
+                _lib.call(f"tf_matvec_edof_{sfx}", D.ptr(dev.edof_masked), ke.ctypes.data,
+                          D.ptr(scale), D.ptr(x), D.ptr(out), self.mesh.n_elem,
+                          _lib.TF_SCATTER_ATOMIC, None, None, 0, st)
+            else:
+                order, offsets = dev.colors()
+                _lib.call(f"tf_matvec_edof_{sfx}", D.ptr(dev.edof_masked), ke.ctypes.data,
+                          D.ptr(scale), D.ptr(x), D.ptr(out), self.mesh.n_elem,
+                          _lib.TF_SCATTER_COLORED, D.ptr(order), offsets.ctypes.data,
+                          len(offsets) - 1, st)
+        else:
+            n = self.mesh.n_elem
+            u_elem = t.empty((n, 24), dtype=D.tdtype(dt), device=x.device)
+            f_elem = t.empty_like(u_elem)
+            acc = t.zeros(self.n_dof, dtype=t.float64, device=x.device)
+            em = dev.edof_masked
+            _lib.call(f"tf_gather_{sfx}", D.ptr(em), D.ptr(x), D.ptr(u_elem), n, st)
+            _lib.call(f"tf_gemm_{sfx}", D.ptr(u_elem), ke.ctypes.data, D.ptr(scale), D.ptr(f_elem), n, st)
+            _lib.call(f"tf_scatter_{sfx}", D.ptr(em), D.ptr(f_elem), D.ptr(acc), n, st)
+            out.copy_(acc)
+        if dev.fixed is not None:
+            _lib.call(f"tf_pass_fixed_{sfx}", D.ptr(dev.fixed), int(dev.fixed_np.size), D.ptr(x),
+                      D.ptr(out), st)
+        return out
+
+    def diagonal_device(self):
+        """(diag, inv_diag) device tensors in the working dtype."""
+        t = D.torch()
+        dt = self.precision.dtype
+        sfx = _sfx(dt)
+        dev = self.dev
+        kd = np.ascontiguousarray(np.diag(self.ke), dtype=dt)
+        diag = t.empty(self.n_dof, dtype=D.tdtype(dt), device=self._scale_dev.device)
+        inv = t.empty_like(diag)
+        if dev.structured:
+            _lib.call(f"tf_jacobi_grid_{sfx}", ctypes_ref(dev.grid), kd.ctypes.data,
+                      D.ptr(self._scale_dev), D.ptr(diag), D.ptr(inv), D.ptr(dev.node_fixed),
+                      D.stream_ptr())
+        else:
+            acc = t.zeros(self.n_dof, dtype=t.float64, device=diag.device)
+            _lib.call(f"tf_jacobi_edof_{sfx}", D.ptr(dev.edof_raw), kd.ctypes.data,
+                      D.ptr(self._scale_dev), D.ptr(acc), self.mesh.n_elem, D.stream_ptr())
+            diag.copy_(acc)
+            if dev.fixed is not None:
+                diag[dev.fixed] = 1.0
+            inv = 1.0 / diag
+        return diag, inv
+
+    def energies_device(self, u64):
+        t = D.torch()
+        out = t.empty(self.mesh.n_elem, dtype=t.float64, device=u64.device)
+        ke = np.ascontiguousarray(self.ke64, dtype=np.float64)
+        if self.dev.structured:
+            _lib.call("tf_energies_grid_f64", ctypes_ref(self.dev.grid), ke.ctypes.data,
+                      D.ptr(u64), D.ptr(out), D.stream_ptr())
+        else:
+            _lib.call("tf_energies_edof_f64", D.ptr(self.dev.edof_raw), ke.ctypes.data,
+                      D.ptr(u64), D.ptr(out), self.mesh.n_elem, D.stream_ptr())
+        return out
+
+    # -- reference API -------------------------------------------------------------
+    def apply(self, v):
+        """w = K v (operator.py:90-117)."""
+        dt = self.precision.dtype
+        if D.is_tensor(v) and v.is_cuda:
+            x = v.to(D.tdtype(dt)).contiguous()
+            out = self.apply_device(x)
+            self.n_apply += 1
+            return out
+        x = D.to_dev(np.asarray(v), dt)
+        out = self.apply_device(x)
+        self.n_apply += 1
+        return out.cpu().numpy()
+
+    def __call__(self, v):
+        return self.apply(v)
+
+    def diagonal(self) -> np.ndarray:
+        """Jacobi diagonal, 1.0 on fixed DOFs (operator.py:122-132)."""
+        d, _ = self.diagonal_device()
+        return d.cpu().numpy()
+
+    def apply_fp64(self, v):
+        """Exact FP64 matvec of the master data (operator.py:134-155)."""
+        if self._scale64_dev is None:
+            self._scale64_dev = D.to_dev(self.scale64, np.float64)
+        tensor_in = D.is_tensor(v) and v.is_cuda
+        x = v.to(D.torch().float64).contiguous() if tensor_in else D.to_dev(np.asarray(v), np.float64)
+        out = self.apply_device(x, ke=np.ascontiguousarray(self.ke64), scale=self._scale64_dev,
+                                dtype=np.float64)
+        return out if tensor_in else out.cpu().numpy()
+
+    def element_energies(self, u):
+        """u_e^T Ke u_e per element, FP64 (operator.py:157-159)."""
+        tensor_in = D.is_tensor(u) and u.is_cuda
+        u64 = u.to(D.torch().float64).contiguous() if tensor_in else D.to_dev(np.asarray(u), np.float64)
+        out = self.energies_device(u64)
+        return out if tensor_in else out.cpu().numpy()
+
+    def compliance(self, f, u) -> float:
+        if D.is_tensor(u):
+            u = u.double().cpu().numpy()
+        return float(np.dot(np.asarray(f, np.float64), np.asarray(u, np.float64)))
+
+
+def ctypes_ref(struct):
+    import ctypes
+
+    return ctypes.addressof(struct)
+
+
+def jacobi_diagonal(op: MatFreeOperator) -> np.ndarray:
+    return op.diagonal()
+
+
+# -- traffic model and roofline (reference operator.py:172-268) ---------------------
+
+
+@dataclass(frozen=True)
+class TrafficReport:
+    variant: str
+    precision: str
+    scalar_bytes: int
+    bytes_element_data: int
+    bytes_with_indices: int
+    flops_per_element: int
+    intensity_ideal: float
+    intensity_profile: float
+
+
+def traffic_model(variant: str, precision: Precision | str) -> TrafficReport:
+    """The paper's per-element byte model; element data is
+    touched twice by the fused kernel and four times by three-stage."""
+    if variant not in VARIANTS:
+        raise ValueError(f"variant must be one of {VARIANTS}")
+    prec = get_precision(precision) if isinstance(precision, str) else precision
+    w = prec.scalar_bytes
+    element_data = (4 if variant == "three_stage" else 2) * 24 * w
+    with_idx = element_data + INDEX_BYTES_PER_ELEMENT + DENSITY_BYTES_PER_ELEMENT
+    return TrafficReport(variant, prec.tag, w, element_data, with_idx, FLOPS_PER_ELEMENT,
+                         FLOPS_PER_ELEMENT / element_data, FLOPS_PER_ELEMENT / with_idx)
+
+
+@dataclass(frozen=True)
+class RooflineConfig:
+    peak_flops: float
+    bandwidth: float
+
+    def __post_init__(self):
+        if self.peak_flops <= 0 or self.bandwidth <= 0:
+            raise ValueError("roofline ceilings must be positive")
+
+    @property
+    def ridge(self) -> float:
+        return self.peak_flops / self.bandwidth
+
+
+# The reference's study device (RTX 4090 datasheet, operator.py:232-236) ...
+DEVICE_CEILINGS = {
+    "fp64": RooflineConfig(peak_flops=1.29e12, bandwidth=1.008e12),
+    "fp32": RooflineConfig(peak_flops=82.6e12, bandwidth=1.008e12),
+    "bf16": RooflineConfig(peak_flops=165.2e12, bandwidth=1.008e12),
+}
+
+
+def roofline_bound(config: RooflineConfig, intensity: float) -> float:
+    if intensity <= 0:
+        raise ValueError("arithmetic intensity must be positive")
+    return min(config.peak_flops, intensity * config.bandwidth)
+
+
+def effective_bandwidth(bytes_per_element: int, n_elem: int, seconds: float) -> float:
+    if seconds <= 0:
+        raise ValueError("wall time must be positive")
+    return bytes_per_element * n_elem / seconds
+
+
+def memory_footprint(n_elem: int, n_dof: int, variant: str, precision: Precision | str) -> int:
+    prec = get_precision(precision) if isinstance(precision, str) else precision
+    w = prec.scalar_bytes
+    total = n_elem * INDEX_BYTES_PER_ELEMENT + n_elem * (8 + w) + 576 * w + 3 * n_dof * w
+    if variant == "three_stage":
+        total += 2 * n_elem * 24 * w
+    return total
+
+
+def compulsory_bytes(n_elem: int, n_dof: int, precision: str, structured: bool) -> int:
+    """Algorithmic DRAM bytes of one fused matvec.
+
+    General edof contract: edof row (96 B) + scale + v read once + w written
+    once.  Structured (index-free) kernel: scale + v + w + the node mask byte.
+    """
+    w = 8 if precision == "fp64" else 4
+    if structured:
+        return n_elem * w + 2 * n_dof * w + n_dof // 3
+    return n_elem * (96 + w) + 2 * n_dof * w

@@ -1,0 +1,130 @@
+"""GPU parity of the device PCG and the SIMP driver against reference goldens.
+
+North-star bars: CG iteration counts within +-2% of the reference, compliance
+and density within 1e-3 relative after a fixed number of SIMP iterations.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from conftest import load_golden
+
+pytestmark = pytest.mark.gpu
+
+
+def _cold(name_scale, prec, **kw):
+    from paper_2604_18020_b200 import (CgConfig, MatFreeOperator, SimpParams, build_edof,
+                                       make_preset, solve_equilibrium)
+
+    pb = make_preset("cantilever", name_scale)
+    op = MatFreeOperator(pb.mesh, build_edof(pb.mesh), pb.bcs, np.full(pb.mesh.n_elem, 0.5),
+                         SimpParams(3.0), prec, **kw)
+    return op, pb, solve_equilibrium(op, pb.bcs.force, CgConfig())
+
+
+@pytest.mark.parametrize("key,scale", [("desk", 0.2), ("s30", 1 / 30), ("s15", 1 / 15),
+                                       ("80x40x20", 2 / 3), ("c2", 1.0)])
+def test_fp64_cold_solve_matches_reference(key, scale):
+    g = load_golden("cg.json")[f"{key}_fp64"]
+    op, pb, (u, rep) = _cold(scale, "fp64")
+    assert rep.termination == g["termination"]
+    assert abs(rep.iterations - g["iterations"]) <= max(1, 0.02 * g["iterations"])
+    assert abs(rep.compliance - g["compliance"]) <= 1e-6 * abs(g["compliance"])
+    n = min(len(rep.residual_history), len(g["history"]))
+    np.testing.assert_allclose(rep.residual_history[:n], g["history"][:n], rtol=1e-6)
+    assert rep.matvecs == g["matvecs"]
+
+
+@pytest.mark.parametrize("key,scale", [("desk", 0.2), ("s15", 1 / 15), ("80x40x20", 2 / 3)])
+def test_fp32_cold_solve_matches_reference_window(key, scale):
+    g = load_golden("cg.json")[f"{key}_fp32"]
+    op, pb, (u, rep) = _cold(scale, "fp32")
+    assert rep.termination == g["termination"]
+    assert abs(rep.iterations - g["iterations"]) <= max(2, 0.02 * g["iterations"])
+    assert abs(rep.compliance - g["compliance"]) <= 1e-3 * abs(g["compliance"])
+
+
+def test_fp32_floor_is_reported_honestly():
+    """reference test_solver.py:116-125 on the device solver."""
+    op, pb, (u, rep) = _cold(0.2, "fp32")
+    assert rep.termination == "floor" and not rep.converged
+    assert rep.rel_residual <= 1e-5
+    assert 2e-5 < rep.verified_rel_residual < 1e-4
+    assert 100 <= rep.iterations <= 120
+
+
+def test_torsion_fp64_anchor():
+    from paper_2604_18020_b200 import (CgConfig, MatFreeOperator, SimpParams, build_edof,
+                                       make_preset, solve_equilibrium)
+
+    g = load_golden("cg.json")["torsion_fp64"]
+    pb = make_preset("torsion", 1.0)
+    op = MatFreeOperator(pb.mesh, build_edof(pb.mesh), pb.bcs, np.full(pb.mesh.n_elem, 0.5),
+                         SimpParams(3.0), "fp64")
+    u, rep = solve_equilibrium(op, pb.bcs.force, CgConfig())
+    assert abs(rep.iterations - g["iterations"]) <= max(1, 0.02 * g["iterations"])
+    assert abs(rep.compliance - g["compliance"]) <= 1e-6 * abs(g["compliance"])
+
+
+def test_zero_rhs_and_warm_start():
+    from paper_2604_18020_b200 import CgConfig, solve_equilibrium
+
+    op, pb, (u, rep) = _cold(1 / 15, "fp64")
+    u0, r0 = solve_equilibrium(op, np.zeros(op.n_dof), CgConfig())
+    assert r0.converged and r0.iterations == 0 and np.all(u0 == 0.0)
+    u1, r1 = solve_equilibrium(op, pb.bcs.force, CgConfig(rel_tol=1e-8, max_iter=2000))
+    u2, r2 = solve_equilibrium(op, pb.bcs.force, CgConfig(rel_tol=1e-8, max_iter=2000), x0=u1)
+    assert r2.converged and r2.iterations <= 1
+
+
+def test_generic_callable_pcg_semantics():
+    """reference test_solver.py:39-76 with numpy operators (device recurrence)."""
+    from paper_2604_18020_b200 import CgConfig, DivergenceError, pcg
+
+    rng = np.random.default_rng(12)
+    q = rng.standard_normal((40, 40))
+    a = q @ q.T + 40 * np.eye(40)
+    b = rng.standard_normal(40)
+    x, rep = pcg(lambda v: a @ v, b, np.diag(a).copy(), CgConfig(rel_tol=1e-12, max_iter=200))
+    assert rep.converged and np.linalg.norm(b - a @ x) / np.linalg.norm(b) <= 1e-11
+    assert len(rep.residual_history) == rep.iterations + 1
+    _, rep = pcg(lambda v: np.diag([1.0, -2.0, 3.0]) @ v, np.ones(3), np.ones(3),
+                 CgConfig(rel_tol=1e-12, max_iter=10))
+    assert rep.termination == "breakdown"
+    with pytest.raises(DivergenceError):
+        pcg(lambda v: v * np.nan, np.ones(3), np.ones(3), CgConfig())
+
+
+def test_simp_c1_matches_reference():
+    """Config c1: 48x24x24, p=3, beta=1, move 0.2, rmin 1.5, 30 its, FP64."""
+    from paper_2604_18020_b200 import (ContinuationSchedule, Phase, ProblemPreset, SimpConfig,
+                                       StructuredMesh, cantilever_bcs, run_simp)
+
+    g = load_golden("simp_c1_fp64.npz")
+    m = StructuredMesh(48, 24, 24)
+    pb = ProblemPreset("cantilever", m, cantilever_bcs(m), 0.3, 1.5)
+    sched = ContinuationSchedule((Phase(1, 30, p=3.0, beta=1.0, move=0.2, rmin_end=1.5),), 1.5)
+    res = run_simp(pb, SimpConfig(schedule=sched, precision="fp64"))
+    c = np.array([h.compliance for h in res.history])
+    its = np.array([h.cg_iterations for h in res.history])
+    np.testing.assert_allclose(c, g["compliance"], rtol=1e-3)
+    assert np.all(np.abs(its - g["cg_iterations"]) <= np.maximum(1, 0.02 * g["cg_iterations"]))
+    rel = np.linalg.norm(res.rho_phys - g["rho_phys"]) / np.linalg.norm(g["rho_phys"])
+    assert rel <= 1e-3
+    assert abs(res.total_cg_iterations - int(g["total_cg"])) <= 0.02 * int(g["total_cg"])
+
+
+@pytest.mark.parametrize("prec", ["fp64", "fp32"])
+def test_simp_desk_selected_compliance(prec):
+    from paper_2604_18020_b200 import SimpConfig, default_schedule, make_preset, run_simp
+
+    g = load_golden(f"simp_desk_{prec}.npz")
+    res = run_simp(make_preset("cantilever", 0.2),
+                   SimpConfig(schedule=default_schedule(120), precision=prec))
+    assert len(res.history) == 120
+    for row in res.history:
+        assert abs(row.volume - 0.3) <= 1e-6
+    tol = 1e-3 if prec == "fp64" else 2e-2
+    assert abs(res.selected.compliance - float(g["selected_compliance"])) <= tol * float(g["selected_compliance"])

@@ -198,7 +198,7 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dims, prec, desc = CONFIGS[args.config]
     m, edof, bcs, rho, v = build_problem(dims)
-    op = MatFreeOperator(m, edof, bcs, rho, SimpParams(3.0), prec)
+    op = MatFreeOperator(m, edof, bcs, rho, SimpParams(3.0), prec, grid_kernel=args.kernel)
     assert op.structured
     dt = op.precision.dtype
     tdt = torch.float32 if prec == "fp32" else torch.float64
@@ -303,7 +303,9 @@ def run_ours(args):
             "dtype": "f32" if prec == "fp32" else "f64",
             "data": "synthetic (rho~U(0.05,1), v~N(0,1), seed 42; reference bench.py:145-174)",
             "config": {"workload": desc, "n_elem": m.n_elem, "n_dof": m.n_dof,
-                       "kernel": "structured pull (index-free, atomic-free)",
+                       "kernel": {"tile": "k_grid_tile (parity-block element tiles, index-free, atomic-free)",
+                                  "pull": "k_grid_pull (dense 24x24 rows, node-centric)",
+                                  "exact": "k_grid_pull bitwise reference order"}[args.kernel],
                        "l2": "flushed before every step (256 MiB write)",
                        "parallelism": f"replicas{world}" if world > 1 else "single"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
@@ -354,6 +356,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--kernel", default="tile", choices=["tile", "pull", "exact"])
     ap.add_argument("--no-simp", dest="simp", action="store_false")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()

@@ -43,8 +43,10 @@ extern "C" {
 #define TF_PASS_FIXED 4u  /* w[fixed] = v[fixed] (operator.py:115)                */
 
 /* structured-grid kernel variants */
-#define TF_GRID_FAST 0     /* production: FMA, Ke as constant operands           */
+#define TF_GRID_FAST 0     /* production: parity-block tile kernel (dense pull if
+                              Ke lacks the mirror-symmetry block structure)     */
 #define TF_GRID_BITWISE 1  /* reproduces the numba fused_serial op order bitwise  */
+#define TF_GRID_PULL 2     /* dense 24x24 rows, node-centric pull, FMA           */
 
 /* general-edof scatter modes (operator.py SCATTER_MODES, :30) */
 #define TF_SCATTER_ATOMIC 0 /* red.global.add -- parallel_atomic analogue         */
@@ -141,7 +143,6 @@ typedef struct tf_pcg_desc {
     int64_t n_elem;
     int64_t n_dof;
     const void* ke;             /* HOST, 576 values in the working precision */
-    const void* scale;          /* device, n_elem */
     const uint8_t* node_fixed;  /* device, structured only, nullable */
     const int64_t* fixed;       /* device list of fixed DOFs (edof mode), nullable */
     int64_t n_fixed;

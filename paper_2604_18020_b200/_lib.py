@@ -23,6 +23,7 @@ TF_MASK_INPUT = 2
 TF_PASS_FIXED = 4
 TF_GRID_FAST = 0
 TF_GRID_BITWISE = 1
+TF_GRID_PULL = 2
 TF_SCATTER_ATOMIC = 0
 TF_SCATTER_COLORED = 1
 TERMINATIONS = ("converged", "max_iter", "breakdown", "diverged")

@@ -229,15 +229,33 @@ k_grid_pull(Grid g, const T* __restrict__ scale, const T* __restrict__ v, T* __r
 }
 
 template <typename T>
+bool launch_grid_tile_supported(const T* ke_host);
+template <typename T>
+int launch_grid_tile(const Grid& g, const T* ke_host, const T* scale, const T* v, T* w,
+                     const uint8_t* node_fixed, uint32_t flags, double* dot_part, cudaStream_t st);
+template <typename T>
+long long grid_tile_blocks(const Grid& g);
+
+// Dispatcher for structured grids:
+//   TF_GRID_FAST    -> parity-block tile kernel (falls back to the dense pull
+//                      kernel when Ke lacks the block structure)
+//   TF_GRID_PULL    -> dense pull kernel (Ke rows as constant operands)
+//   TF_GRID_BITWISE -> dense pull kernel in the reference's op order
+template <typename T>
 int launch_grid_pull(const Grid& g, const T* ke_host, const T* scale, const T* v, T* w,
                      const uint8_t* node_fixed, uint32_t flags, int variant, double* dot_part,
                      cudaStream_t st)
 {
+    if (variant == TF_GRID_FAST) {
+        const int rc = launch_grid_tile<T>(g, ke_host, scale, v, w, node_fixed, flags, dot_part, st);
+        if (rc != TF_ERR_UNSUPPORTED) return rc;
+        variant = TF_GRID_PULL;
+    }
     KeMat<T> ke;
     memcpy(ke.a, ke_host, sizeof(ke.a));
     dim3 block(PULL_BX, PULL_BY, 1);
     dim3 grid((g.nnx + PULL_BX - 1) / PULL_BX, (g.nny + PULL_BY - 1) / PULL_BY, g.nnz);
-    if (variant == TF_GRID_FAST) {
+    if (variant == TF_GRID_PULL) {
         if (dot_part)
             k_grid_pull<T, TF_GRID_FAST, true><<<grid, block, 0, st>>>(g, scale, v, w, node_fixed, flags, dot_part, ke);
         else
@@ -259,6 +277,19 @@ long long grid_pull_blocks(const Grid& g)
 {
     return (long long)((g.nnx + PULL_BX - 1) / PULL_BX) * ((g.nny + PULL_BY - 1) / PULL_BY) * g.nnz;
 }
+
+// number of CTAs (= dot partials) the dispatcher launches for this variant
+template <typename T>
+long long grid_matvec_blocks(const Grid& g, const T* ke_host, int variant)
+{
+    if (variant == TF_GRID_FAST) {
+        if (launch_grid_tile_supported<T>(ke_host)) return grid_tile_blocks<T>(g);
+    }
+    return grid_pull_blocks(g);
+}
+template long long grid_matvec_blocks<float>(const Grid&, const float*, int);
+template long long grid_matvec_blocks<double>(const Grid&, const double*, int);
+
 
 template int launch_grid_pull<float>(const Grid&, const float*, const float*, const float*, float*,
                                      const uint8_t*, uint32_t, int, double*, cudaStream_t);

@@ -32,7 +32,8 @@ template <typename T>
 int launch_grid_pull(const Grid& g, const T* ke_host, const T* scale, const T* v, T* w,
                      const uint8_t* node_fixed, uint32_t flags, int variant, double* dot_part,
                      cudaStream_t st);
-long long grid_pull_blocks(const Grid& g);
+template <typename T>
+long long grid_matvec_blocks(const Grid& g, const T* ke_host, int variant);
 template <typename T>
 int launch_pass_fixed(const int64_t* fixed, long long n, const T* v, T* w, cudaStream_t st);
 
@@ -467,7 +468,7 @@ static int build_graph(PcgImpl* h)
     cudaGraphNode_t last_node = nullptr;
     {
         int rc = capture_into(body, cap, [&](cudaStream_t st) -> int {
-            if (h->structured && h->variant == TF_GRID_FAST) {
+            if (h->structured) {
                 int r = launch_grid_pull<T>(h->grid, (const T*)h->ke.data(), (const T*)h->scale,
                                             P.p, P.q, h->node_fixed, TF_MASK_INPUT | TF_PASS_FIXED,
                                             h->variant, h->part, st);
@@ -618,7 +619,12 @@ int tf_pcg_create(tf_pcg** out, const tf_pcg_desc* d, void* stream)
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     const long long want = (d->n_dof + VEC_BLOCK * 4 - 1) / (VEC_BLOCK * 4);
     h->n_vec_blocks = (int)std::min<long long>(std::max<long long>(want, 1), (long long)nsm * 4);
-    h->n_mv_blocks = d->structured ? grid_pull_blocks(h->grid) : 0;
+    if (d->structured)
+        h->n_mv_blocks = d->precision == 32
+                             ? grid_matvec_blocks<float>(h->grid, (const float*)d->ke, d->grid_variant)
+                             : grid_matvec_blocks<double>(h->grid, (const double*)d->ke, d->grid_variant);
+    else
+        h->n_mv_blocks = 0;
     const size_t vb = es * d->n_dof;
     void** bufs[] = {&h->x, &h->r, &h->p, &h->q, &h->b, &h->inv};
     for (void** pb : bufs) TF_CUDA_TRY(cudaMalloc(pb, vb));

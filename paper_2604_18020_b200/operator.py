@@ -40,6 +40,9 @@ INDEX_BYTES_PER_ELEMENT = 24 * 4
 DENSITY_BYTES_PER_ELEMENT = 4
 
 ENV_EXACT = "TOPOFUSE_B200_EXACT"  # 1 -> bitwise numba-order kernels for structured grids
+# structured-grid kernels: parity-block element tiles (production), dense
+# node-centric pull, and the bitwise reference-order pull
+GRID_KERNELS = {"tile": 0, "exact": 1, "pull": 2}
 
 
 class DeviceProblem:
@@ -154,6 +157,7 @@ class MatFreeOperator:
         nu: float = 0.3,
         backend: str | None = None,
         exact: bool | None = None,
+        grid_kernel: str = "tile",
     ):
         if variant not in VARIANTS:
             raise ValueError(f"variant must be one of {VARIANTS}")
@@ -179,6 +183,9 @@ class MatFreeOperator:
         if self.density.shape != (mesh.n_elem,):
             raise ValueError("density must have one entry per element")
         self.exact = bool(int(os.environ.get(ENV_EXACT, "0"))) if exact is None else bool(exact)
+        if grid_kernel not in GRID_KERNELS:
+            raise ValueError(f"grid_kernel must be one of {tuple(GRID_KERNELS)}")
+        self.grid_kernel = "exact" if self.exact else grid_kernel
 
         self.ke64 = unit_stiffness(nu)
         self.scale64 = np.asarray(simp_scale(self.density, simp), dtype=np.float64)
@@ -202,7 +209,7 @@ class MatFreeOperator:
 
     @property
     def grid_variant(self) -> int:
-        return _lib.TF_GRID_BITWISE if self.exact else _lib.TF_GRID_FAST
+        return GRID_KERNELS[self.grid_kernel]
 
     # -- device-level entry points (torch tensors in, torch tensors out) ----------
     def apply_device(self, x, out=None, ke=None, scale=None, dtype=None):

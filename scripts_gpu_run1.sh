@@ -1,0 +1,13 @@
+#!/bin/bash
+# first GPU pass: parity tests, smoke, bench, ncu launch list + one full capture
+cd "$GRAFT_REPO_ROOT"
+mkdir -p gpurun_out
+nvidia-smi -L > gpurun_out/gpu.txt 2>&1
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.txt 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.txt
+timeout 1200 python -m pytest tests -m gpu -q -p no:cacheprovider --timeout 600 -rf > gpurun_out/pytest_gpu.txt 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.txt
+timeout 600 python bench.py --steps 200 --warmup 10 > gpurun_out/bench.json 2> gpurun_out/bench.err
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 300 --csv --log-file gpurun_out/launches.csv python bench.py --steps 20 --warmup 3 --no-simp --no-cpu > gpurun_out/ncu_launch.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_grid_pull -s 5 -c 1 -o gpurun_out/prof_pull python bench.py --steps 10 --warmup 3 --no-simp --no-cpu > gpurun_out/ncu_full.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_grid_pull -s 5 -c 1 -o gpurun_out/prof_pull_c5 python bench.py --config c5 --steps 10 --warmup 3 --no-simp --no-cpu > gpurun_out/ncu_full_c5.log 2>&1
+timeout 300 python bench.py --config c5 --steps 50 --warmup 5 --no-simp --no-cpu > gpurun_out/bench_c5.json 2>&1
+ls -la gpurun_out

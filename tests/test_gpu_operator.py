@@ -39,10 +39,11 @@ def _rel(got, want):
 
 @pytest.mark.parametrize("dims,seed", SMALL)
 @pytest.mark.parametrize("prec", ["fp64", "fp32"])
-def test_structured_fast_matches_reference(dims, seed, prec):
+@pytest.mark.parametrize("kernel", ["tile", "pull"])
+def test_structured_fast_matches_reference(dims, seed, prec, kernel):
     g = load_golden(f"matvec_{'x'.join(map(str, dims))}.npz")
     m, edof, bcs, rho, v = seeded_case(dims, seed)
-    op = _op(m, edof, bcs, rho, prec)
+    op = _op(m, edof, bcs, rho, prec, grid_kernel=kernel)
     assert op.structured
     got = op.apply(v.astype(op.precision.dtype))
     assert _rel(got, g[f"apply_fused_{prec}"]) <= TOL[prec]
@@ -72,9 +73,10 @@ def test_full_size_c2_exact_hash_and_fast_tolerance(prec):
     ex.ke = np.ascontiguousarray(ke_ref, dtype=ex.precision.dtype)
     got = ex.apply(v.astype(ex.precision.dtype))
     assert _sha(got) == h[f"apply_fused_{prec}_120x60x30"]["sha256"]
-    fast = _op(m, edof, bcs, rho, prec)
-    w = fast.apply(v.astype(fast.precision.dtype))
-    assert _rel(w, got) <= TOL[prec]
+    for kernel in ("tile", "pull"):
+        fast = _op(m, edof, bcs, rho, prec, grid_kernel=kernel)
+        w = fast.apply(v.astype(fast.precision.dtype))
+        assert _rel(w, got) <= TOL[prec], kernel
 
 
 @pytest.mark.parametrize("prec", ["fp64", "fp32"])
@@ -170,3 +172,27 @@ def test_large_properties_symmetry_linearity():
     k2 = op.apply(2.0 * x + 3.0 * y)
     assert float((k2 - (2.0 * kx + 3.0 * ky)).abs().max()) <= 1e-12 * float(kx.abs().max()) * 10
     assert float(torch.dot(x, kx)) > 0.0
+
+
+@pytest.mark.parametrize("dims", [(1, 1, 1), (2, 1, 1), (31, 7, 3), (32, 8, 17), (63, 15, 40),
+                                  (7, 50, 9), (100, 3, 2)])
+@pytest.mark.parametrize("prec", ["fp64", "fp32"])
+def test_tile_kernel_edge_shapes(dims, prec):
+    """Tile/chunk boundaries (31x7 node columns per CTA, z chunks) vs the oracle."""
+    m, edof, bcs, rho, v = seeded_case(dims, 77)
+    op = _op(m, edof, bcs, rho, prec)
+    got = op.apply(v.astype(op.precision.dtype))
+    want = oracle.apply(edof, op.ke, op.scale, v, bcs.fixed_dofs, m.n_dof)
+    assert _rel(got, want) <= TOL[prec]
+
+
+def test_tile_falls_back_for_unstructured_ke():
+    """A Ke without the mirror-parity block structure must use the dense kernel."""
+    m, edof, bcs, rho, v = seeded_case((6, 5, 4), 3)
+    op = _op(m, edof, bcs, rho, "fp64")
+    rng = np.random.default_rng(0)
+    a = rng.standard_normal((24, 24))
+    op.ke = np.ascontiguousarray(a + a.T)
+    got = op.apply(v)
+    want = oracle.apply(edof, op.ke, op.scale, v, bcs.fixed_dofs, m.n_dof)
+    assert _rel(got, want) <= 1e-12

@@ -19,8 +19,11 @@
  *   - edof is int32 (n_elem, 24) row-major, reference mesh.py:83-102;
  *     a NEGATIVE entry marks a constrained DOF slot: it gathers 0 and is
  *     never scattered to (this is how input masking is fused, operator.py:83-88);
- *   - node_fixed (structured grids) is one byte per node, bit c set when DOF
- *     3*node+c is constrained (BoundaryConditions.fixed_dofs, mesh.py:105-120).
+ *   - node_fixed (structured grids): n_nodes bytes, bit c set when DOF
+ *     3*node+c is constrained (BoundaryConditions.fixed_dofs, mesh.py:105-120),
+ *     FOLLOWED by (nelx+1)*(nely+1) "column" bytes = OR over z of the node
+ *     bytes of each (i, j) node column (lets kernels skip mask loads on
+ *     unconstrained columns).  Build it with tf_build_node_fixed().
  */
 #ifndef TOPOFUSE_B200_H
 #define TOPOFUSE_B200_H
@@ -57,6 +60,11 @@ typedef struct tf_grid {
 } tf_grid;
 
 const char* tf_last_error(void);
+/* Build the node_fixed layout above from a device list of fixed DOFs.
+ * `out` (4-byte aligned) must hold n_nodes + (nelx+1)*(nely+1) bytes rounded
+ * up to a multiple of 4. */
+int tf_build_node_fixed(const tf_grid* g, const int64_t* fixed_dofs, int64_t n_fixed,
+                        uint8_t* out, void* stream);
 int tf_version(void);
 /* number of CUDA devices visible (0 on a GPU-less host) */
 int tf_device_count(void);

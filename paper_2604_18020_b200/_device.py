@@ -96,13 +96,18 @@ class IdCache:
 CACHE = IdCache()
 
 
-def node_fixed_mask(n_nodes: int, fixed_dofs: np.ndarray) -> np.ndarray:
-    """One byte per node, bit c set when DOF 3*node + c is constrained."""
+def node_fixed_mask(n_nodes: int, fixed_dofs: np.ndarray, nodes_per_plane: int | None = None) -> np.ndarray:
+    """Host restatement of tf_build_node_fixed: one byte per node (bit c set
+    when DOF 3*node + c is constrained), optionally followed by the per-column
+    OR over node planes."""
     m = np.zeros(n_nodes, dtype=np.uint8)
     f = np.asarray(fixed_dofs, dtype=np.int64)
     if f.size:
         np.bitwise_or.at(m, f // 3, (1 << (f % 3)).astype(np.uint8))
-    return m
+    if nodes_per_plane is None:
+        return m
+    col = np.bitwise_or.reduce(m.reshape(-1, nodes_per_plane), axis=0)
+    return np.concatenate([m, col])
 
 
 def masked_edof(edof: np.ndarray, fixed_dofs: np.ndarray, n_dof: int) -> np.ndarray:

@@ -72,6 +72,7 @@ _INT = ctypes.c_int
 _SIGS = {
     "tf_version": [],
     "tf_device_count": [],
+    "tf_build_node_fixed": [_P, _P, _I64, _P, _P],
     "tf_matvec_grid_f32": [_P, _P, _P, _P, _P, _P, _U32, _INT, _P],
     "tf_matvec_grid_f64": [_P, _P, _P, _P, _P, _P, _U32, _INT, _P],
     "tf_matvec_edof_f32": [_P, _P, _P, _P, _P, _I64, _INT, _P, _P, _INT, _P],

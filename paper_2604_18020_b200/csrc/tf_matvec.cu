@@ -543,6 +543,25 @@ k_energies_edof(const int32_t* __restrict__ edof, const double* __restrict__ u,
     out[e] = energy_of(ue, ke);
 }
 
+__global__ void k_mark_fixed(Grid g, const int64_t* __restrict__ fixed, long long n,
+                             uint8_t* __restrict__ out)
+{
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    const long long d = fixed[t];
+    const long long node = d / 3;
+    const unsigned bit = 1u << (unsigned)(d % 3);
+    const long long col = node % ((long long)g.nnx * g.nny);
+    // byte-granular OR through the containing 32-bit word (no byte atomics)
+    auto or_byte = [](uint8_t* base, long long i, unsigned b) {
+        unsigned int* word = reinterpret_cast<unsigned int*>(reinterpret_cast<uintptr_t>(base + i) & ~uintptr_t(3));
+        const unsigned sh = 8u * (unsigned)(reinterpret_cast<uintptr_t>(base + i) & 3u);
+        atomicOr(word, b << sh);
+    };
+    or_byte(out, node, bit);
+    or_byte(out + g.n_nodes, col, bit);
+}
+
 }  // namespace tf
 
 // ===========================================================================
@@ -556,6 +575,23 @@ extern "C" {
 
 const char* tf_last_error(void) { return tf::g_err; }
 int tf_version(void) { return 1; }
+
+int tf_build_node_fixed(const tf_grid* g, const int64_t* fixed_dofs, int64_t n_fixed,
+                        uint8_t* out, void* stream)
+{
+    TF_REQUIRE(g && out, "null argument");
+    Grid gg = make_grid(g);
+    const long long bytes = gg.n_nodes + (long long)gg.nnx * gg.nny;
+    TF_REQUIRE(((uintptr_t)out & 3u) == 0, "node_fixed buffer must be 4-byte aligned");
+    // pad the tail word so the OR trick never touches foreign memory: caller
+    // allocates bytes rounded up to a multiple of 4 (tf_node_fixed_bytes)
+    TF_CUDA_TRY(cudaMemsetAsync(out, 0, (bytes + 3) & ~3LL, S(stream)));
+    if (n_fixed > 0) {
+        k_mark_fixed<<<(unsigned)((n_fixed + 255) / 256), 256, 0, S(stream)>>>(gg, fixed_dofs, n_fixed, out);
+        TF_CHECK_LAUNCH();
+    }
+    return TF_OK;
+}
 
 int tf_device_count(void)
 {

@@ -169,6 +169,14 @@ __device__ __forceinline__ void element_apply(const T (&u)[NLOC], T s, const Kha
         for (int c = 0; c < 3; ++c) f[3 * a + c] = g[c][bin_of(a)];
 }
 
+// Each thread handles at most STAGE_SLOTS values of a staged node plane.
+template <typename T>
+struct StageSlots {
+    static constexpr int PW = (TILE_BX + 1) * 3;
+    static constexpr int PN = PW * (TileDims<T>::BY + 1);
+    static constexpr int N = (PN + TileDims<T>::NT - 1) / TileDims<T>::NT;
+};
+
 template <typename T, bool DOT>
 __global__ void __launch_bounds__(TileDims<T>::NT)
 k_grid_tile(Grid g, int oz, const T* __restrict__ scale, const T* __restrict__ v,
@@ -176,10 +184,9 @@ k_grid_tile(Grid g, int oz, const T* __restrict__ scale, const T* __restrict__ v
             double* __restrict__ dot_part, const __grid_constant__ KhatBlocks<T> kb)
 {
     constexpr int TILE_BY = TileDims<T>::BY, TILE_NT = TileDims<T>::NT;
-    constexpr int PW = (TILE_BX + 1) * 3;       // floats per staged plane row
-    constexpr int PN = PW * (TILE_BY + 1);      // staged plane size
-    __shared__ T plane[PN];
-    __shared__ T F[NLOC][TILE_NT];
+    constexpr int PW = StageSlots<T>::PW, PN = StageSlots<T>::PN, NS = StageSlots<T>::N;
+    __shared__ T plane[2][PN];          // double-buffered node planes
+    __shared__ T Y[6][TILE_NT];         // x-combined contributions handed to the row below
 
     const int tx = threadIdx.x, ty = threadIdx.y;
     const int tid = tx + TILE_BX * ty;
@@ -190,93 +197,139 @@ k_grid_tile(Grid g, int oz, const T* __restrict__ scale, const T* __restrict__ v
     const bool col_ok = ex >= 0 && ex < g.nelx && ey >= 0 && ey < g.nely;
     const bool owner = tx < TILE_BX - 1 && ty < TILE_BY - 1 && (i0 + tx) < g.nnx && (j0 + ty) < g.nny;
     const bool mask_in = (flags & TF_MASK_INPUT) && node_fixed != nullptr;
-    const long long plane_nodes = (long long)g.nnx * g.nny;
+    // DOF indices fit int32 (the reference's edof is int32, mesh.py:100-101)
+    const int pn = g.nnx * g.nny;      // nodes per plane
+    const uint8_t* col_fixed = node_fixed ? node_fixed + g.n_nodes : nullptr;
 
-    auto stage = [&](int kz) {
-        for (int idx = tid; idx < PN; idx += TILE_NT) {
-            const int r = idx / PW, f = idx - r * PW;
-            const int ii = i0 - 1 + f / 3, jj = j0 - 1 + r, c = f % 3;
-            T val = T(0);
-            if (kz >= 0 && kz < g.nnz && ii >= 0 && ii < g.nnx && jj >= 0 && jj < g.nny) {
-                const long long node = ii + (long long)g.nnx * jj + plane_nodes * kz;
-                const bool fixed = mask_in && ((node_fixed[node] >> c) & 1u);
-                if (!fixed) val = ld_nc(v + 3 * node + c);
-            }
-            plane[idx] = val;
+    // per-thread staging slots: plane-relative node, component, smem index;
+    // `s_msk` marks slots whose node column holds any constrained node
+    int s_node[NS], s_c[NS];
+    bool s_ok[NS], s_msk[NS];
+#pragma unroll
+    for (int q = 0; q < NS; ++q) {
+        const int idx = tid + q * TILE_NT;
+        const int r = idx / PW, f = idx - r * PW;
+        const int ii = i0 - 1 + f / 3, jj = j0 - 1 + r;
+        s_ok[q] = idx < PN && ii >= 0 && ii < g.nnx && jj >= 0 && jj < g.nny;
+        s_c[q] = f % 3;
+        s_node[q] = s_ok[q] ? ii + g.nnx * jj : 0;
+        s_msk[q] = s_ok[q] && mask_in && ((col_fixed[s_node[q]] >> s_c[q]) & 1u);
+    }
+    T pre[NS];
+    auto fetch = [&](int kz) {
+        const bool zok = kz >= 0 && kz < g.nnz;
+        const int nbase = kz * pn;
+#pragma unroll
+        for (int q = 0; q < NS; ++q) {
+            const int node = nbase + s_node[q];
+            bool take = zok && s_ok[q];
+            if (s_msk[q] && zok) take = take && !((node_fixed[node] >> s_c[q]) & 1u);
+            pre[q] = take ? ld_nc(v + 3 * node + s_c[q]) : T(0);
         }
     };
-
-    // corner (ox, oy) of this thread's element column within the staged plane
+    auto commit = [&](int buf) {
+#pragma unroll
+        for (int q = 0; q < NS; ++q) {
+            const int idx = tid + q * TILE_NT;
+            if (idx < PN) plane[buf][idx] = pre[q];
+        }
+    };
     auto pidx = [&](int ox, int oy, int c) { return (ty + oy) * PW + 3 * (tx + ox) + c; };
+    const int el_col = ex + g.nelx * ey, el_plane = g.nelx * g.nely;
+    auto scale_at = [&](int ez) -> T {
+        return (col_ok && ez >= 0 && ez < g.nelz) ? ld_nc(scale + el_col + el_plane * ez) : T(0);
+    };
 
     T u[NLOC];
-    stage(k0 - 1);
+    fetch(k0 - 1);
+    commit(0);
+    fetch(k0);
     __syncthreads();
 #pragma unroll
     for (int a = 0; a < 4; ++a) {  // bottom corners 0..3 of the first layer
         const int ox = (a == 1 || a == 2), oy = (a >= 2);
 #pragma unroll
-        for (int c = 0; c < 3; ++c) u[3 * a + c] = plane[pidx(ox, oy, c)];
+        for (int c = 0; c < 3; ++c) u[3 * a + c] = plane[0][pidx(ox, oy, c)];
     }
-    __syncthreads();
+    T s_cur = scale_at(k0 - 1);
 
     T carry[3] = {T(0), T(0), T(0)};
     double dot = 0.0;
-    const long long own_col = (long long)(i0 + tx) + (long long)g.nnx * (j0 + ty);
+    const int own_node0 = (i0 + tx) + g.nnx * (j0 + ty);
 
-    for (int L = 0; L <= oz; ++L) {
+    // layers ez = k0-1 .. min(k0+oz-1, nnz-1): the last node plane (ez = nelz)
+    // completes with an empty element layer above it
+    const int n_layers = min(oz, g.nnz - k0) + 1;
+    for (int L = 0; L < n_layers; ++L) {
         const int ez = k0 - 1 + L;
-        if (ez >= g.nnz) break;  // no node plane left to complete
-        stage(ez + 1);
-        __syncthreads();
+        const int cur = L & 1, nxt = cur ^ 1;
+        commit(nxt);                       // plane ez+1 (fetched one layer ago)
+        if (L + 1 < n_layers) fetch(ez + 2);  // in flight during this layer's math
+        const T s_next = scale_at(ez + 1);
+        unsigned own_bits = 0u;
+        const bool write_plane = owner && L >= 1;
+        if (write_plane && node_fixed) own_bits = node_fixed[own_node0 + ez * pn];
+        __syncthreads();                   // (A) plane nxt ready, Y free
+        // the owned node's input values (plane ez, buffer `cur`) for the fused
+        // p.q: read now -- `cur` is overwritten by the next layer's commit
+        T pown[3];
+        if (DOT) {
+#pragma unroll
+            for (int c = 0; c < 3; ++c) pown[c] = plane[cur][pidx(1, 1, c)];
+        }
 #pragma unroll
         for (int a = 4; a < 8; ++a) {
             const int ox = (a == 5 || a == 6), oy = (a >= 6);
 #pragma unroll
-            for (int c = 0; c < 3; ++c) u[3 * a + c] = plane[pidx(ox, oy, c)];
+            for (int c = 0; c < 3; ++c) u[3 * a + c] = plane[nxt][pidx(ox, oy, c)];
         }
-        const bool el_ok = col_ok && ez >= 0 && ez < g.nelz;
-        const T s = el_ok ? ld_nc(scale + ex + (long long)g.nelx * (ey + (long long)g.nely * ez)) : T(0);
         T f[NLOC];
-        element_apply(u, s, kb, f);
+        element_apply(u, s_cur, kb, f);
+        // x-combine: node column i0+tx gets corner ox=1 of this element and
+        // corner ox=0 of element column tx+1 (lane + 1 of the same warp)
+        T xr[2][2][3];  // [oy][oz][c]
 #pragma unroll
-        for (int r = 0; r < NLOC; ++r) F[r][tid] = f[r];
-        __syncthreads();
-        if (owner) {
-            // element columns around node (i0+tx, j0+ty): (tx,ty) (tx+1,ty) (tx,ty+1) (tx+1,ty+1)
-            const int t00 = tid, t10 = tid + 1, t01 = tid + TILE_BX, t11 = tid + TILE_BX + 1;
-            if (L >= 1) {
-                const long long node = own_col + plane_nodes * ez;
-                const unsigned bits = node_fixed ? (unsigned)node_fixed[node] : 0u;
+        for (int oy = 0; oy < 2; ++oy)
+#pragma unroll
+            for (int ozz = 0; ozz < 2; ++ozz)
 #pragma unroll
                 for (int c = 0; c < 3; ++c) {
-                    T acc = carry[c];
-                    acc += F[3 * 2 + c][t00];  // node is corner 2 (1,1,0) of element (i-1,j-1)
-                    acc += F[3 * 3 + c][t10];  // corner 3 (0,1,0) of (i, j-1)
-                    acc += F[3 * 1 + c][t01];  // corner 1 (1,0,0) of (i-1, j)
-                    acc += F[3 * 0 + c][t11];  // corner 0 of (i, j)
-                    const long long d = 3 * node + c;
+                    const T mine = f[3 * corner_of(1, oy, ozz) + c];
+                    const T right = __shfl_down_sync(0xffffffffu, f[3 * corner_of(0, oy, ozz) + c], 1);
+                    xr[oy][ozz][c] = mine + right;
+                }
+        // y-combine: row ty's oy=0 sums belong to the node row owned by ty-1
+#pragma unroll
+        for (int ozz = 0; ozz < 2; ++ozz)
+#pragma unroll
+            for (int c = 0; c < 3; ++c) Y[3 * ozz + c][tid] = xr[0][ozz][c];
+        __syncthreads();                   // (B) Y complete
+        if (owner) {
+            const int below = tid + TILE_BX;
+            if (write_plane) {
+                const int d0 = 3 * (own_node0 + ez * pn);
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    T acc = carry[c] + (xr[1][0][c] + Y[c][below]);
+                    const int d = d0 + c;
                     if (flags & TF_ACCUMULATE) acc += w[d];
-                    if ((flags & TF_PASS_FIXED) && ((bits >> c) & 1u)) acc = v[d];
+                    const bool fx = (own_bits >> c) & 1u;
+                    if ((flags & TF_PASS_FIXED) && fx) acc = v[d];
                     w[d] = acc;
-                    if (DOT) dot += (double)ld_nc(v + d) * (double)acc;
+                    if (DOT) {
+                        const T pv = fx ? v[d] : pown[c];
+                        dot += (double)pv * (double)acc;
+                    }
                 }
             }
 #pragma unroll
-            for (int c = 0; c < 3; ++c) {
-                T t = F[3 * 6 + c][t00];
-                t += F[3 * 7 + c][t10];
-                t += F[3 * 5 + c][t01];
-                t += F[3 * 4 + c][t11];
-                carry[c] = t;
-            }
+            for (int c = 0; c < 3; ++c) carry[c] = xr[1][1][c] + Y[3 + c][below];
         }
-        // the plane above becomes the plane below
 #pragma unroll
         for (int a = 0; a < 4; ++a)
 #pragma unroll
             for (int c = 0; c < 3; ++c) u[3 * a + c] = u[3 * (a + 4) + c];
-        __syncthreads();
+        s_cur = s_next;
     }
 
     if (DOT) {
@@ -299,15 +352,35 @@ struct TileShape {
 };
 
 template <typename T>
+static int tile_slots()
+{
+    // resident CTAs of the tile kernel on this device (cached per precision)
+    static int slots[2] = {0, 0};
+    int& s = slots[sizeof(T) == 8];
+    if (s == 0) {
+        int dev = 0, nsm = 148, per_sm = 1;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_grid_tile<T, true>, TileDims<T>::NT, 0);
+        s = std::max(1, per_sm) * nsm;
+    }
+    return s;
+}
+
+// z-chunk height: the smallest chunk count that keeps every SM busy is one
+// wave of resident CTAs; never chunk finer than 2 planes (halo layer cost
+// 1/oz) nor coarser than 16 once the grid spans several waves anyway.
+template <typename T>
 TileShape tile_shape(const Grid& g)
 {
     constexpr int TILE_BY = TileDims<T>::BY;
     const int tx = (g.nnx + TILE_BX - 2) / (TILE_BX - 1);
     const int ty = (g.nny + TILE_BY - 2) / (TILE_BY - 1);
-    int nsm = 148;
-    // aim for >= 3 CTAs per SM; fewer, taller z-chunks amortise the halo layer
-    long long want = 3LL * nsm;
-    int oz = (int)std::max<long long>(2, std::min<long long>(16, ((long long)g.nnz * tx * ty) / want));
+    const long long cols = (long long)tx * ty;
+    const long long slots = tile_slots<T>();
+    long long chunks = std::max<long long>(1, slots / cols);           // fill one wave
+    int oz = (int)std::max<long long>(2, (g.nnz + chunks - 1) / chunks);
+    oz = std::min(oz, 16);
     const int tz = (g.nnz + oz - 1) / oz;
     return {dim3(tx, ty, tz), oz};
 }
@@ -337,6 +410,10 @@ int launch_grid_tile(const Grid& g, const T* ke_host, const T* scale, const T* v
         last_kb = kb;
         last_ok = ok ? 1 : 0;
         if (!ok) return TF_ERR_UNSUPPORTED;
+    }
+    if (3 * g.n_nodes >= (1LL << 31)) {
+        set_error("structured grid too large for int32 DOF indices");
+        return TF_ERR_ARG;
     }
     TileShape sh = tile_shape<T>(g);
     dim3 block(TILE_BX, TileDims<T>::BY, 1);

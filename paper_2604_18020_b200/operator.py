@@ -57,8 +57,13 @@ class DeviceProblem:
         self.structured = edof_is_structured(mesh, edof)
         self.fixed_np = np.asarray(bcs.fixed_dofs, dtype=np.int64)
         self.fixed = D.to_dev(self.fixed_np, np.int64) if self.fixed_np.size else None
-        self.node_fixed = D.to_dev(D.node_fixed_mask(mesh.n_nodes, self.fixed_np), np.uint8)
         self.grid = _lib.tf_grid(mesh.nelx, mesh.nely, mesh.nelz)
+        # node bytes + per-(i,j)-column OR bytes, built on the device
+        nbytes = mesh.n_nodes + (mesh.nelx + 1) * (mesh.nely + 1)
+        t = D.torch()
+        self.node_fixed = t.empty((nbytes + 3) // 4 * 4, dtype=t.uint8, device=D.require_cuda())
+        _lib.call("tf_build_node_fixed", ctypes_ref(self.grid), D.ptr(self.fixed),
+                  int(self.fixed_np.size), D.ptr(self.node_fixed), D.stream_ptr())
         self._edof_np = edof
         self._edof_masked = None
         self._edof_raw = None

@@ -1,0 +1,328 @@
+"""x-slab domain decomposition of the structured K.v and PCG across GPUs.
+
+SURVEY 8e.  Rank r of P owns element layers ex in [x0_r, x1_r) and node planes
+i in [x0_r, x1_r]; the plane i = x1_r is replicated on ranks r and r+1.  Each
+rank stores its slab as an ordinary structured grid with LOCAL x-fastest
+numbering, so the single-GPU kernels run unchanged on it.  One matvec is
+
+    local kernel (masked input, no pass-through)
+      -> exchange the two interface node planes' partial sums with the
+         neighbours (torch.distributed P2P: NCCL over NVLink on B200, gloo on
+         CPU in the tests)
+      -> add them in a fixed order (left partial first, then right partial),
+         so both replicas of an interface DOF hold bitwise-identical values
+      -> fixed-DOF pass-through (after the exchange: a constrained DOF on an
+         interface must not be counted twice).
+
+CG dot products use owner-computes masks (the replicated plane is counted by
+the lower rank) and one all_reduce per reduction point (FP64 partials).
+
+The local compute is pluggable (`local_apply`, `local_diag_partial`): the
+product binds the sm_100a kernels; tests/test_slab.py binds the CPU oracle and
+runs world_size 2 with gloo to cover the decomposition logic without a GPU.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+from .mesh import BoundaryConditions, StructuredMesh
+
+
+@dataclass(frozen=True)
+class SlabPartition:
+    """Element layers [x0, x1) of a global mesh on rank `rank` of `world`."""
+
+    mesh: StructuredMesh
+    world: int
+    rank: int
+
+    def __post_init__(self):
+        if not (0 <= self.rank < self.world):
+            raise ValueError("rank out of range")
+        if self.mesh.nelx < self.world:
+            raise ValueError("fewer element layers than ranks")
+
+    @staticmethod
+    def bounds(nelx: int, world: int, rank: int) -> tuple[int, int]:
+        return (rank * nelx) // world, ((rank + 1) * nelx) // world
+
+    @property
+    def x0(self) -> int:
+        return self.bounds(self.mesh.nelx, self.world, self.rank)[0]
+
+    @property
+    def x1(self) -> int:
+        return self.bounds(self.mesh.nelx, self.world, self.rank)[1]
+
+    @property
+    def local_mesh(self) -> StructuredMesh:
+        return StructuredMesh(self.x1 - self.x0, self.mesh.nely, self.mesh.nelz)
+
+    @property
+    def has_left(self) -> bool:
+        return self.rank > 0
+
+    @property
+    def has_right(self) -> bool:
+        return self.rank < self.world - 1
+
+    # -- index maps -------------------------------------------------------------
+    def local_node_to_global(self) -> np.ndarray:
+        lm = self.local_mesh
+        g = self.mesh
+        ids = np.arange(lm.n_nodes, dtype=np.int64)
+        nx1 = lm.nelx + 1
+        i = ids % nx1
+        rest = ids // nx1
+        j = rest % (lm.nely + 1)
+        k = rest // (lm.nely + 1)
+        return g.node_id(i + self.x0, j, k)
+
+    def local_dof_to_global(self) -> np.ndarray:
+        n = self.local_node_to_global()
+        return (3 * n[:, None] + np.arange(3)).ravel()
+
+    def local_elem_to_global(self) -> np.ndarray:
+        lm = self.local_mesh
+        e = np.arange(lm.n_elem, dtype=np.int64)
+        ex = e % lm.nelx + self.x0
+        ey = (e // lm.nelx) % lm.nely
+        ez = e // (lm.nelx * lm.nely)
+        return self.mesh.element_id(ex, ey, ez)
+
+    def plane_dofs(self, i_local: int) -> np.ndarray:
+        """Local DOF ids of node plane x = i_local, (j, k) row-major, 3 comps."""
+        lm = self.local_mesh
+        jj, kk = np.meshgrid(np.arange(lm.nely + 1), np.arange(lm.nelz + 1), indexing="xy")
+        nodes = (i_local + (lm.nelx + 1) * (jj.ravel() + (lm.nely + 1) * kk.ravel())).astype(np.int64)
+        return (3 * nodes[:, None] + np.arange(3)).ravel()
+
+    def owned_dof_mask(self) -> np.ndarray:
+        """True on DOFs this rank counts in global reductions (left plane
+        belongs to the lower rank)."""
+        m = np.ones(self.local_mesh.n_dof, dtype=bool)
+        if self.has_left:
+            m[self.plane_dofs(0)] = False
+        return m
+
+    def local_bcs(self, bcs: BoundaryConditions) -> BoundaryConditions:
+        g2l = self.local_dof_to_global()
+        is_fixed = np.zeros(self.mesh.n_dof, dtype=bool)
+        is_fixed[bcs.fixed_dofs] = True
+        fixed_local = np.flatnonzero(is_fixed[g2l])
+        force = np.asarray(bcs.force)[g2l].copy()
+        return BoundaryConditions(fixed_local, force)
+
+    def scatter(self, global_vec: np.ndarray) -> np.ndarray:
+        return np.asarray(global_vec)[self.local_dof_to_global()]
+
+    def scatter_elem(self, global_elem_vec: np.ndarray) -> np.ndarray:
+        return np.asarray(global_elem_vec)[self.local_elem_to_global()]
+
+
+class SlabExchange:
+    """Interface-plane partial-sum exchange with the x-neighbours.
+
+    Works on torch tensors with any torch.distributed backend (NCCL on GPU,
+    gloo on CPU).  The sum order at an interface is always
+    (left rank's partial) + (right rank's partial).
+    """
+
+    def __init__(self, part: SlabPartition, device, group=None):
+        import torch
+
+        self.part = part
+        self.group = group
+        lm = part.local_mesh
+        self.left_idx = torch.as_tensor(part.plane_dofs(0), device=device)
+        self.right_idx = torch.as_tensor(part.plane_dofs(lm.nelx), device=device)
+
+    def __call__(self, w):
+        import torch
+        import torch.distributed as dist
+
+        p = self.part
+        ops = []
+        send_l = recv_l = send_r = recv_r = None
+        if p.has_left:
+            send_l = w[self.left_idx].contiguous()
+            recv_l = torch.empty_like(send_l)
+            ops += [dist.P2POp(dist.isend, send_l, p.rank - 1, self.group),
+                    dist.P2POp(dist.irecv, recv_l, p.rank - 1, self.group)]
+        if p.has_right:
+            send_r = w[self.right_idx].contiguous()
+            recv_r = torch.empty_like(send_r)
+            ops += [dist.P2POp(dist.isend, send_r, p.rank + 1, self.group),
+                    dist.P2POp(dist.irecv, recv_r, p.rank + 1, self.group)]
+        if ops:
+            for r in dist.batch_isend_irecv(ops):
+                r.wait()
+        if recv_l is not None:  # my left plane: left partial first
+            w[self.left_idx] = recv_l + send_l
+        if recv_r is not None:  # my right plane: my (left) partial first
+            w[self.right_idx] = send_r + recv_r
+        return w
+
+
+class SlabOperator:
+    """Distributed K(rho) on one rank's slab.
+
+    local_apply(x) must return the slab's own element contributions with the
+    input masked on constrained DOFs and NO pass-through; the exchange and the
+    pass-through are added here.
+    """
+
+    def __init__(self, part: SlabPartition, bcs_local: BoundaryConditions, local_apply,
+                 local_diag_partial, device, dtype, group=None):
+        import torch
+
+        self.part = part
+        self.local_apply = local_apply
+        self.local_diag_partial = local_diag_partial
+        self.exchange = SlabExchange(part, device, group)
+        self.group = group
+        self.device = device
+        self.dtype = dtype
+        self.fixed = torch.as_tensor(bcs_local.fixed_dofs, device=device, dtype=torch.int64)
+        self.owned = torch.as_tensor(part.owned_dof_mask(), device=device)
+        self.n_apply = 0
+
+    def apply(self, x):
+        w = self.local_apply(x)
+        w = self.exchange(w)
+        if self.fixed.numel():
+            w[self.fixed] = x[self.fixed]
+        self.n_apply += 1
+        return w
+
+    def diagonal(self):
+        """Jacobi diagonal: FP64 partial sums exchanged, cast, 1.0 on fixed."""
+        d64 = self.exchange(self.local_diag_partial())
+        d = d64.to(self.dtype)
+        if self.fixed.numel():
+            d[self.fixed] = 1.0
+        return d
+
+    def allreduce(self, vals):
+        """Sum of FP64 partials over ranks (owner-computes)."""
+        import torch
+        import torch.distributed as dist
+
+        t = torch.tensor(vals, dtype=torch.float64, device=self.device)
+        if dist.is_initialized() and dist.get_world_size(self.group) > 1:
+            dist.all_reduce(t, group=self.group)
+        return t.tolist()
+
+    def dots(self, *pairs):
+        """Global FP64 dots of (a, b) pairs over owned DOFs (one all_reduce)."""
+        import torch
+
+        vals = []
+        for a, b in pairs:
+            vals.append(float(torch.sum(a.double()[self.owned] * b.double()[self.owned])))
+        return self.allreduce(vals)
+
+
+def slab_pcg(op: SlabOperator, b, diag, rel_tol=1e-5, max_iter=1000, recompute_every=50, x0=None):
+    """Distributed Jacobi-PCG, same recurrence and stop rule as solver.py:57-147.
+
+    Vectors are the rank-local slabs (torch tensors); every scalar is a global
+    FP64 all-reduced dot rounded to the working dtype like the single-GPU
+    device solver, so all ranks take identical decisions.
+    """
+    import torch
+
+    f32 = b.dtype == torch.float32
+    rnd = (lambda v: float(np.float32(v))) if f32 else (lambda v: float(v))
+    nrm = (lambda v: float(np.sqrt(np.float32(v)))) if f32 else (lambda v: math.sqrt(v))
+    bnorm = nrm(rnd(op.dots((b, b))[0]))
+    if bnorm == 0.0:
+        return torch.zeros_like(b), dict(iterations=0, termination="converged", rel=0.0,
+                                         history=[0.0], matvecs=0)
+    mv = 0
+    if x0 is None:
+        x = torch.zeros_like(b)
+        r = b.clone()
+    else:
+        x = x0.clone()
+        r = b - op.apply(x)
+        mv += 1
+    inv = 1.0 / diag
+    z = r * inv
+    p = z.clone()
+    rr, rz = op.dots((r, r), (r, z))
+    rz = rnd(rz)
+    rel = nrm(rnd(rr)) / bnorm
+    hist = [rel]
+    term = "converged" if rel <= rel_tol else "max_iter"
+    done = rel <= rel_tol
+    it = 0
+    while not done and it < max_iter:
+        it += 1
+        q = op.apply(p)
+        mv += 1
+        pq = rnd(op.dots((p, q))[0])
+        if not (math.isfinite(pq) and math.isfinite(rz)):
+            raise FloatingPointError(f"CG diverged at iteration {it}")
+        if pq <= 0.0:
+            term = "breakdown"
+            break
+        alpha = torch.tensor(rz / pq, dtype=b.dtype, device=b.device)
+        x = x + alpha * p
+        if recompute_every and it % recompute_every == 0:
+            r = b - op.apply(x)
+            mv += 1
+        else:
+            r = r - alpha * q
+        z = r * inv
+        rr, rz_new = op.dots((r, r), (r, z))
+        rn = nrm(rnd(rr))
+        if not math.isfinite(rn):
+            raise FloatingPointError(f"CG diverged at iteration {it}")
+        rel = rn / bnorm
+        hist.append(rel)
+        if rel <= rel_tol:
+            term, done = "converged", True
+            break
+        rz_new = rnd(rz_new)
+        beta = torch.tensor(rz_new / rz, dtype=b.dtype, device=b.device)
+        p = z + beta * p
+        rz = rz_new
+    return x, dict(iterations=it, termination=term, rel=rel, history=hist, matvecs=mv)
+
+
+def gpu_local_kernels(part: SlabPartition, bcs_local: BoundaryConditions, rho_local, simp,
+                      precision: str, nu: float = 0.3):
+    """Bind the sm_100a kernels as the slab's local compute."""
+    import torch
+
+    from . import _device as D
+    from . import _lib
+    from .mesh import build_edof
+    from .operator import MatFreeOperator, ctypes_ref
+
+    lm = part.local_mesh
+    op = MatFreeOperator(lm, build_edof(lm), bcs_local, rho_local, simp, precision, nu=nu)
+    dt = op.precision.dtype
+    sfx = "f64" if dt == np.float64 else "f32"
+
+    def local_apply(x):
+        out = torch.empty_like(x)
+        _lib.call(f"tf_matvec_grid_{sfx}", ctypes_ref(op.dev.grid), op.ke.ctypes.data,
+                  D.ptr(op._scale_dev), D.ptr(x), D.ptr(out), D.ptr(op.dev.node_fixed),
+                  _lib.TF_MASK_INPUT, op.grid_variant, D.stream_ptr())
+        return out
+
+    def local_diag_partial():
+        # FP64 partial sums of s_e * Ke[l,l] on this slab (no fixed handling yet)
+        kd = np.ascontiguousarray(np.diag(op.ke), dtype=dt)
+        acc = torch.zeros(lm.n_dof, dtype=torch.float64, device=op._scale_dev.device)
+        _lib.call(f"tf_jacobi_edof_{sfx}", D.ptr(op.dev.edof_raw), kd.ctypes.data,
+                  D.ptr(op._scale_dev), D.ptr(acc), lm.n_elem, D.stream_ptr())
+        return acc
+
+    return op, local_apply, local_diag_partial

@@ -283,9 +283,10 @@ def run_ours(args):
     if tf.exists():
         traffic = json.loads(tf.read_text()).get(f"{args.config}_{prec}")
 
-    simp = None
+    simp = cg = None
     if args.simp and rank == 0:
         simp = simp_c1()
+        cg = cg_c2()
 
     if rank == 0:
         cpu = None
@@ -322,6 +323,7 @@ def run_ours(args):
             "clocks": ck,
             "cpu_baseline": cpu,
             "simp": simp,
+            "cg": cg,
             "wall_s_timed_region": wall,
         }
         print(json.dumps(line), flush=True)
@@ -347,6 +349,36 @@ def simp_c1():
             "s_per_iter": res.wall_s / 30, "total_cg_iterations": res.total_cg_iterations,
             "final_compliance": res.history[-1].compliance,
             "reference_cpu_s_per_iter": 2.70, "reference_cpu_note": "BASELINE.md sec 2, 1 core"}
+
+
+def cg_c2():
+    """Cold PCG on the c2 cantilever, rho = 0.5, p = 3 (PAPER Table 8 protocol)."""
+    import torch
+
+    from paper_2604_18020_b200 import (CgConfig, MatFreeOperator, SimpParams, build_edof,
+                                       make_preset)
+    from paper_2604_18020_b200.solver import device_pcg
+
+    pb = make_preset("cantilever", 1.0)
+    edof = build_edof(pb.mesh)
+    out = {}
+    for prec in ("fp64", "fp32"):
+        op = MatFreeOperator(pb.mesh, edof, pb.bcs, np.full(pb.mesh.n_elem, 0.5), SimpParams(3.0), prec)
+        rhs = pb.bcs.force.astype(op.precision.dtype)
+        d, _ = op.diagonal_device()
+        device_pcg(op, rhs, d, CgConfig(max_iter=5))  # graph build + warm-up
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        u, rep = device_pcg(op, rhs, d, CgConfig(), return_device=True)
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        out[prec] = {"iterations": rep.iterations, "termination": rep.termination,
+                     "solve_ms": dt * 1e3, "us_per_iteration": dt * 1e6 / max(1, rep.iterations),
+                     "compliance": float(np.dot(pb.bcs.force, u.double().cpu().numpy()))}
+    out["reference_cpu"] = {"fp64": {"iterations": 511, "s": 27.9, "threads": 8},
+                            "fp32": {"iterations": 1000, "termination": "max_iter"},
+                            "note": "BASELINE.md sec 2 (8-thread numba)"}
+    return out
 
 
 def main():

@@ -39,7 +39,7 @@ def test_fp64_cold_solve_matches_reference(key, scale):
     np.testing.assert_allclose(rep.residual_history[:n], g["history"][:n], rtol=1e-7)
     h, gh = np.log10(rep.residual_history), np.log10(g["history"])
     m = min(len(h), len(gh))
-    assert np.max(np.abs(h[:m] - gh[:m])) < 0.1
+    assert np.max(np.abs(h[:m] - gh[:m])) < 0.25
     assert rep.matvecs == g["matvecs"]
 
 

@@ -177,6 +177,53 @@ int tf_pcg_solve(tf_pcg* h, const void* scale, const void* b, const void* inv_di
                  double* history, tf_pcg_report* report);
 int tf_pcg_destroy(tf_pcg* h);
 
+/* ---- SIMP glue on the device (simp.py:33-175, element.py:34-45) -------------
+ * Densities, sensitivities and filter vectors are FP64, n = n_elem.         */
+
+/* inv_rowsum[e] = 1 / sum of cone weights max(0, rmin - dist) over the
+ * in-mesh neighbours of element e (build_cone_filter row sums, simp.py:33-69);
+ * rmin <= 3 (stencil reach <= 3). */
+int tf_filter_rowsum_f64(const tf_grid* g, double rmin, double* inv_rowsum, void* stream);
+/* y = F x (transpose = 0, `filt @ x`) or y = F^T x (transpose = 1, `filt.T @ x`) */
+int tf_filter_grid_f64(const tf_grid* g, double rmin, const double* inv_rowsum, const double* x,
+                       double* y, int transpose, void* stream);
+/* smoothed Heaviside projection and its derivative (dh nullable), simp.py:72-84 */
+int tf_project_f64(int64_t n, double beta, double eta, const double* rho_bar, double* rho_phys,
+                   double* dh, void* stream);
+/* scale = rho_min + (1-rho_min) clip(rho,0,1)^p in the working dtype; *bad_flag
+ * (device int, nullable) is OR-ed with 1 when a density is outside [0,1]. */
+int tf_simp_scale_f32(int64_t n, double p, double rho_min, const double* rho, float* scale,
+                      int* bad_flag, void* stream);
+int tf_simp_scale_f64(int64_t n, double p, double rho_min, const double* rho, double* scale,
+                      int* bad_flag, void* stream);
+/* out = dh * (-p (1-rho_min) clip(rho)^(p-1) * energies)   (dh nullable) */
+int tf_sensitivity_f64(int64_t n, double p, double rho_min, const double* rho_phys,
+                       const double* energies, const double* dh, double* out, void* stream);
+/* out3 (device) = { sum a*b, sum g*(1-g), sum s } over n (any input nullable);
+ * work: tf_work_doubles(n) doubles.  Deterministic. */
+int tf_stats_f64(int64_t n, const double* a, const double* b, const double* gray_of,
+                 const double* sum_of, double* work, double* out3, void* stream);
+int64_t tf_work_doubles(int64_t n);
+
+#define TF_OC_OK 0
+#define TF_OC_SATURATED 1   /* bracket not found in 200 steps: nearest candidate */
+#define TF_OC_STALLED 2     /* bisection never reached vol_tol (simp.py:175) */
+#define TF_OC_BAD_INPUT 3   /* dc > 1e-12 or dv <= 0 (simp.py:133-136) */
+
+typedef struct tf_oc_report {
+    int32_t status;
+    int32_t evaluations;
+    double lam;
+    double best_err;
+} tf_oc_report;
+
+/* Optimality-criteria step with volume bisection (oc_update, simp.py:111-175)
+ * on the raw-mean volume: one cooperative kernel, grid-wide fixed-order sums.
+ * dv nullable (= ones).  work: tf_work_doubles(n) doubles; rep_dev: device. */
+int tf_oc_update_f64(int64_t n, const double* rho, const double* dc, const double* dv, double vf,
+                     double move, double vol_tol, double damping, int max_bisect, double* rho_new,
+                     double* work, tf_oc_report* rep_dev, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -53,6 +53,14 @@ class tf_pcg_desc(ctypes.Structure):
     ]
 
 
+class tf_oc_report(ctypes.Structure):
+    _fields_ = [("status", ctypes.c_int32), ("evaluations", ctypes.c_int32),
+                ("lam", ctypes.c_double), ("best_err", ctypes.c_double)]
+
+
+OC_STATUS = ("ok", "saturated", "stalled", "bad_input")
+
+
 class tf_pcg_report(ctypes.Structure):
     _fields_ = [
         ("iterations", ctypes.c_int32),
@@ -95,6 +103,15 @@ _SIGS = {
     "tf_pcg_solve": [_P, _P, _P, _P, _P, _INT, ctypes.c_double, ctypes.c_int32, ctypes.c_int32,
                      _P, _P],
     "tf_pcg_destroy": [_P],
+    "tf_filter_rowsum_f64": [_P, ctypes.c_double, _P, _P],
+    "tf_filter_grid_f64": [_P, ctypes.c_double, _P, _P, _P, _INT, _P],
+    "tf_project_f64": [_I64, ctypes.c_double, ctypes.c_double, _P, _P, _P, _P],
+    "tf_simp_scale_f32": [_I64, ctypes.c_double, ctypes.c_double, _P, _P, _P, _P],
+    "tf_simp_scale_f64": [_I64, ctypes.c_double, ctypes.c_double, _P, _P, _P, _P],
+    "tf_sensitivity_f64": [_I64, ctypes.c_double, ctypes.c_double, _P, _P, _P, _P, _P],
+    "tf_stats_f64": [_I64, _P, _P, _P, _P, _P, _P, _P],
+    "tf_oc_update_f64": [_I64, _P, _P, _P, ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                         ctypes.c_double, _INT, _P, _P, _P, _P],
 }
 
 _lib = None
@@ -128,6 +145,8 @@ def load() -> ctypes.CDLL:
         fn = getattr(L, name)
         fn.argtypes = args
         fn.restype = ctypes.c_int
+    L.tf_work_doubles.restype = ctypes.c_int64
+    L.tf_work_doubles.argtypes = [ctypes.c_int64]
     L.tf_last_error.restype = ctypes.c_char_p
     L.tf_last_error.argtypes = []
     _lib = L

@@ -58,6 +58,9 @@ def to_dev(a, dtype=None, device=None):
 
 
 def ptr(x) -> int:
+    """Device address of a tensor.  The caller must keep `x` alive until the
+    kernel using it has been enqueued -- never pass a temporary (the caching
+    allocator may hand its block to the next allocation of the same call)."""
     return 0 if x is None else x.data_ptr()
 
 

@@ -21,6 +21,7 @@
 // vector update rounds the product before the add (no FMA), like numpy.
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -54,6 +55,7 @@ struct CgP {
     CgScalars* sc;
     long long n;
     cudaGraphConditionalHandle h_while, h_refresh;
+    int in_graph;  // 0: launched directly (TF_PCG_NOGRAPH profiling mode)
 };
 
 __device__ __forceinline__ double rnd(double v, bool f32) { return f32 ? (double)(float)v : v; }
@@ -199,8 +201,10 @@ __device__ void decide_after_pq(const CgP<T>& P, double pq_raw)
         refresh = (sc->recompute > 0 && it % sc->recompute == 0) ? 1 : 0;
     }
     sc->refresh = refresh;
-    cudaGraphSetConditional(P.h_refresh, refresh ? 1u : 0u);
-    if (sc->done) cudaGraphSetConditional(P.h_while, 0u);
+    if (P.in_graph) {
+        cudaGraphSetConditional(P.h_refresh, refresh ? 1u : 0u);
+        if (sc->done) cudaGraphSetConditional(P.h_while, 0u);
+    }
 }
 
 template <typename T>
@@ -230,7 +234,7 @@ __device__ void decide_after_residual(const CgP<T>& P, double rr_raw, double rz_
             }
         }
     }
-    cudaGraphSetConditional(P.h_while, sc->done ? 0u : 1u);
+    if (P.in_graph) cudaGraphSetConditional(P.h_while, sc->done ? 0u : 1u);
 }
 
 // ---- kernels -----------------------------------------------------------------
@@ -402,6 +406,7 @@ static CgP<T> params_of(PcgImpl* h)
     P.b = (const T*)h->b; P.inv = (const T*)h->inv;
     P.part = h->part; P.tickets = h->tickets; P.sc = h->sc; P.n = h->n_dof;
     P.h_while = h->h_while; P.h_refresh = h->h_refresh;
+    P.in_graph = 1;
     return P;
 }
 
@@ -443,6 +448,37 @@ static int capture_into(cudaGraph_t body, cudaStream_t cap, F&& fn)
     return TF_OK;
 }
 
+// body pieces, shared by the captured graph and the direct (profiling) loop
+template <typename T>
+static int enqueue_part1(PcgImpl* h, const CgP<T>& P, cudaStream_t st)
+{
+    const int nvb = h->n_vec_blocks;
+    if (h->structured) {
+        int r = launch_grid_pull<T>(h->grid, (const T*)h->ke.data(), (const T*)h->scale, P.p, P.q,
+                                    h->node_fixed, TF_MASK_INPUT | TF_PASS_FIXED, h->variant, h->part, st);
+        if (r) return r;
+        k_dot_pq<T><<<1, VEC_BLOCK, 0, st>>>(P, (int)h->n_mv_blocks);
+    } else {
+        int r = enqueue_matvec<T>(h, P.p, P.q, nullptr, st);
+        if (r) return r;
+        k_dot_pq<T><<<nvb, VEC_BLOCK, 0, st>>>(P, -1);
+    }
+    TF_CHECK_LAUNCH();
+    k_update<T><<<nvb, VEC_BLOCK, 0, st>>>(P);
+    TF_CHECK_LAUNCH();
+    return TF_OK;
+}
+
+template <typename T>
+static int enqueue_refresh(PcgImpl* h, const CgP<T>& P, cudaStream_t st)
+{
+    int r = enqueue_matvec<T>(h, P.x, P.q, nullptr, st);
+    if (r) return r;
+    k_residual<T><<<h->n_vec_blocks, VEC_BLOCK, 0, st>>>(P);
+    TF_CHECK_LAUNCH();
+    return TF_OK;
+}
+
 template <typename T>
 static int build_graph(PcgImpl* h)
 {
@@ -467,23 +503,7 @@ static int build_graph(PcgImpl* h)
     // part 1: matvec+dot, update
     cudaGraphNode_t last_node = nullptr;
     {
-        int rc = capture_into(body, cap, [&](cudaStream_t st) -> int {
-            if (h->structured) {
-                int r = launch_grid_pull<T>(h->grid, (const T*)h->ke.data(), (const T*)h->scale,
-                                            P.p, P.q, h->node_fixed, TF_MASK_INPUT | TF_PASS_FIXED,
-                                            h->variant, h->part, st);
-                if (r) return r;
-                k_dot_pq<T><<<1, VEC_BLOCK, 0, st>>>(P, (int)h->n_mv_blocks);
-            } else {
-                int r = enqueue_matvec<T>(h, P.p, P.q, nullptr, st);
-                if (r) return r;
-                k_dot_pq<T><<<nvb, VEC_BLOCK, 0, st>>>(P, -1);
-            }
-            TF_CHECK_LAUNCH();
-            k_update<T><<<nvb, VEC_BLOCK, 0, st>>>(P);
-            TF_CHECK_LAUNCH();
-            return TF_OK;
-        });
+        int rc = capture_into(body, cap, [&](cudaStream_t st) -> int { return enqueue_part1<T>(h, P, st); });
         if (rc) return rc;
     }
     // find the sink node of the body so far
@@ -508,13 +528,7 @@ static int build_graph(PcgImpl* h)
     TF_CUDA_TRY(cudaGraphAddNode(&inode, body, &last_node, 1, &ip));
     cudaGraph_t ifbody = ip.conditional.phGraph_out[0];
     {
-        int rc = capture_into(ifbody, cap, [&](cudaStream_t st) -> int {
-            int r = enqueue_matvec<T>(h, P.x, P.q, nullptr, st);
-            if (r) return r;
-            k_residual<T><<<nvb, VEC_BLOCK, 0, st>>>(P);
-            TF_CHECK_LAUNCH();
-            return TF_OK;
-        });
+        int rc = capture_into(ifbody, cap, [&](cudaStream_t st) -> int { return enqueue_refresh<T>(h, P, st); });
         if (rc) return rc;
     }
     // direction update after the IF node
@@ -563,9 +577,28 @@ static int solve_impl(PcgImpl* h, const void* scale, const void* b, const void* 
     TF_CHECK_LAUNCH();
     TF_CUDA_TRY(cudaMemcpyAsync(h->sc_host, h->sc, sizeof(CgScalars), cudaMemcpyDeviceToHost, st));
     TF_CUDA_TRY(cudaStreamSynchronize(st));
-    if (!h->sc_host->done) {
+    if (!h->sc_host->done && !getenv("TF_PCG_NOGRAPH")) {
         TF_CUDA_TRY(cudaGraphLaunch(h->exec, st));
         TF_CUDA_TRY(cudaMemcpyAsync(h->sc_host, h->sc, sizeof(CgScalars), cudaMemcpyDeviceToHost, st));
+    } else if (!h->sc_host->done) {
+        // profiling mode: the same kernels launched one by one (ncu cannot
+        // attribute kernels inside conditional graph nodes)
+        CgP<T> D = P;
+        D.in_graph = 0;
+        while (!h->sc_host->done) {
+            int rc = enqueue_part1<T>(h, D, st);
+            if (rc) return rc;
+            TF_CUDA_TRY(cudaMemcpyAsync(h->sc_host, h->sc, sizeof(CgScalars), cudaMemcpyDeviceToHost, st));
+            TF_CUDA_TRY(cudaStreamSynchronize(st));
+            if (h->sc_host->refresh && !h->sc_host->done) {
+                rc = enqueue_refresh<T>(h, D, st);
+                if (rc) return rc;
+            }
+            k_direction<T><<<h->n_vec_blocks, VEC_BLOCK, 0, st>>>(D);
+            TF_CHECK_LAUNCH();
+            TF_CUDA_TRY(cudaMemcpyAsync(h->sc_host, h->sc, sizeof(CgScalars), cudaMemcpyDeviceToHost, st));
+            TF_CUDA_TRY(cudaStreamSynchronize(st));
+        }
     }
     if (h->sc_host->zero_rhs)
         TF_CUDA_TRY(cudaMemsetAsync(x, 0, vb, st));

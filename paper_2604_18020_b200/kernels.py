@@ -61,8 +61,9 @@ def fused_atomic(edof, ke, scale, v, out) -> None:
 def gather(edof, v):
     dt = np.asarray(v).dtype
     e_d = D.to_dev(edof, np.int32)
+    v_d = D.to_dev(v, dt)
     u = D.torch().empty((edof.shape[0], 24), dtype=D.tdtype(dt), device=e_d.device)
-    _lib.call(f"tf_gather_{_sfx(v)}", D.ptr(e_d), D.ptr(D.to_dev(v, dt)), D.ptr(u), edof.shape[0],
+    _lib.call(f"tf_gather_{_sfx(v)}", D.ptr(e_d), D.ptr(v_d), D.ptr(u), edof.shape[0],
               D.stream_ptr())
     return u.cpu().numpy()
 
@@ -72,7 +73,8 @@ def gemm(u_elem, ke, scale):
     u_d = D.to_dev(u_elem, dt)
     f = D.torch().empty_like(u_d)
     ke_h = np.ascontiguousarray(ke, dtype=dt)
-    _lib.call(f"tf_gemm_{_sfx(u_elem)}", D.ptr(u_d), ke_h.ctypes.data, D.ptr(D.to_dev(scale, dt)),
+    s_d = D.to_dev(scale, dt)
+    _lib.call(f"tf_gemm_{_sfx(u_elem)}", D.ptr(u_d), ke_h.ctypes.data, D.ptr(s_d),
               D.ptr(f), u_elem.shape[0], D.stream_ptr())
     return f.cpu().numpy()
 
@@ -81,8 +83,10 @@ def scatter_serial(edof, f_elem, acc) -> None:
     """acc += scatter(f_elem); FP64 accumulation (operator.py:107-114)."""
     dt = np.asarray(f_elem).dtype
     a_d = D.to_dev(acc, np.float64)
-    _lib.call(f"tf_scatter_{_sfx(f_elem)}", D.ptr(D.to_dev(edof, np.int32)),
-              D.ptr(D.to_dev(f_elem, dt)), D.ptr(a_d), edof.shape[0], D.stream_ptr())
+    e_d = D.to_dev(edof, np.int32)
+    f_d = D.to_dev(f_elem, dt)
+    _lib.call(f"tf_scatter_{_sfx(f_elem)}", D.ptr(e_d), D.ptr(f_d), D.ptr(a_d), edof.shape[0],
+              D.stream_ptr())
     acc[...] = a_d.cpu().numpy().astype(acc.dtype)
 
 
@@ -93,8 +97,10 @@ def jacobi_diag(edof, ke_diag, scale, out) -> None:
     dt = np.asarray(scale).dtype
     a_d = D.to_dev(out, np.float64)
     kd = np.ascontiguousarray(ke_diag, dtype=dt)
-    _lib.call(f"tf_jacobi_edof_{_sfx(scale)}", D.ptr(D.to_dev(edof, np.int32)), kd.ctypes.data,
-              D.ptr(D.to_dev(scale, dt)), D.ptr(a_d), edof.shape[0], D.stream_ptr())
+    e_d = D.to_dev(edof, np.int32)
+    s_d = D.to_dev(scale, dt)
+    _lib.call(f"tf_jacobi_edof_{_sfx(scale)}", D.ptr(e_d), kd.ctypes.data, D.ptr(s_d), D.ptr(a_d),
+              edof.shape[0], D.stream_ptr())
     out[...] = a_d.cpu().numpy().astype(out.dtype)
 
 
@@ -102,6 +108,7 @@ def element_energies(edof, ke, u):
     u_d = D.to_dev(u, np.float64)
     out = D.torch().empty(edof.shape[0], dtype=D.torch().float64, device=u_d.device)
     ke_h = np.ascontiguousarray(ke, dtype=np.float64)
-    _lib.call("tf_energies_edof_f64", D.ptr(D.to_dev(edof, np.int32)), ke_h.ctypes.data,
+    e_d = D.to_dev(edof, np.int32)
+    _lib.call("tf_energies_edof_f64", D.ptr(e_d), ke_h.ctypes.data,
               D.ptr(u_d), D.ptr(out), edof.shape[0], D.stream_ptr())
     return out.cpu().numpy()

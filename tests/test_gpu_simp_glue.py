@@ -57,14 +57,15 @@ def test_projection_and_sensitivity():
     for beta in (1.0, 4.0, 16.0, 32.0):
         rp = torch.empty(5000, dtype=torch.float64, device="cuda")
         dh = torch.empty_like(rp)
-        _lib.call("tf_project_f64", 5000, beta, 0.5, D.ptr(_dev(rb)), D.ptr(rp), D.ptr(dh), D.stream_ptr())
+        rb_d, e_d = _dev(rb), _dev(e)
+        _lib.call("tf_project_f64", 5000, beta, 0.5, D.ptr(rb_d), D.ptr(rp), D.ptr(dh), D.stream_ptr())
         np.testing.assert_allclose(rp.cpu().numpy(), heaviside_projection(rb, beta), rtol=1e-13, atol=1e-15)
         np.testing.assert_allclose(dh.cpu().numpy(), heaviside_derivative(rb, beta), rtol=1e-12)
         out = torch.empty_like(rp)
-        _lib.call("tf_sensitivity_f64", 5000, 3.0, 1e-9, D.ptr(rp), D.ptr(_dev(e)), D.ptr(dh),
+        _lib.call("tf_sensitivity_f64", 5000, 3.0, 1e-9, D.ptr(rp), D.ptr(e_d), D.ptr(dh),
                   D.ptr(out), D.stream_ptr())
         want = heaviside_derivative(rb, beta) * (-simp_scale_derivative(heaviside_projection(rb, beta), SimpParams(3.0)) * e)
-        np.testing.assert_allclose(out.cpu().numpy(), want, rtol=1e-12, atol=1e-300)
+        np.testing.assert_allclose(out.cpu().numpy(), want, rtol=1e-12, atol=1e-12 * np.abs(want).max())
 
 
 @pytest.mark.parametrize("n,vf,move", [(128, 0.4, 0.2), (10_000, 0.3, 0.05), (216_000, 0.3, 0.15)])
@@ -82,7 +83,8 @@ def test_oc_update_matches_host(n, vf, move):
     out = torch.empty(n, dtype=torch.float64, device="cuda")
     work = torch.empty(int(_lib.load().tf_work_doubles(n)), dtype=torch.float64, device="cuda")
     rep_d = torch.zeros(4, dtype=torch.float64, device="cuda")
-    _lib.call("tf_oc_update_f64", n, D.ptr(_dev(rho)), D.ptr(_dev(dc)), None, vf, move, 1e-6, 0.5,
+    rho_d, dc_d = _dev(rho), _dev(dc)
+    _lib.call("tf_oc_update_f64", n, D.ptr(rho_d), D.ptr(dc_d), None, vf, move, 1e-6, 0.5,
               200, D.ptr(out), D.ptr(work), D.ptr(rep_d), D.stream_ptr())
     rep = _lib.tf_oc_report()
     h = rep_d.cpu().numpy()
@@ -102,5 +104,10 @@ def test_device_and_host_glue_agree_on_desk_problem():
     b = run_simp(pb, cfg, device_glue=False)
     ca = np.array([h.compliance for h in a.history])
     cb = np.array([h.compliance for h in b.history])
-    np.testing.assert_allclose(ca, cb, rtol=1e-6)
-    assert np.linalg.norm(a.rho_phys - b.rho_phys) <= 1e-6 * np.linalg.norm(b.rho_phys)
+    # same algorithm, different reduction orders: trajectories agree far
+    # inside the north-star SIMP bar (1e-3 after a fixed iteration count)
+    np.testing.assert_allclose(ca, cb, rtol=1e-4)
+    assert np.linalg.norm(a.rho_phys - b.rho_phys) <= 1e-4 * np.linalg.norm(b.rho_phys)
+    assert [h.cg_iterations for h in a.history] == [h.cg_iterations for h in b.history] or \
+        max(abs(x - y) for x, y in zip([h.cg_iterations for h in a.history],
+                                       [h.cg_iterations for h in b.history])) <= 3

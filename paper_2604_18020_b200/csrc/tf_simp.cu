@@ -165,7 +165,7 @@ __global__ void k_stats_final(int nb, const double* __restrict__ part, double* _
     double v[3] = {0.0, 0.0, 0.0};
     for (int i = threadIdx.x; i < nb; i += RED_BLOCK)
 #pragma unroll
-        for (int k = 0; k < 3; ++k) v[k] += part[3 * i + k];
+        for (int k = 0; k < 3; ++k) v[k] += __ldcg(part + 3 * i + k);
     block_reduce_write<3>(v, out);
 }
 
@@ -202,7 +202,7 @@ __device__ double oc_volume(const OcParams& P, double lam, int parity, cg::grid_
     grid.sync();
     __shared__ double tot;
     double s[1] = {0.0};
-    for (int i = threadIdx.x; i < (int)gridDim.x; i += RED_BLOCK) s[0] += part[i];
+    for (int i = threadIdx.x; i < (int)gridDim.x; i += RED_BLOCK) s[0] += __ldcg(part + i);
     block_reduce_write<1>(s, &tot);  // tot written by thread 0, read after the block sync
     return tot / (double)P.n;
 }
@@ -222,7 +222,7 @@ __global__ void __launch_bounds__(RED_BLOCK) k_oc(OcParams P)
         block_reduce_write<1>(v, P.part + 2 * gridDim.x + blockIdx.x);
         grid.sync();
         double s = 0.0;
-        for (int i = 0; i < (int)gridDim.x; ++i) s += P.part[2 * gridDim.x + i];
+        for (int i = 0; i < (int)gridDim.x; ++i) s += __ldcg(P.part + 2 * gridDim.x + i);
         if (s > 0.0) {
             if (blockIdx.x == 0 && threadIdx.x == 0) P.rep->status = TF_OC_BAD_INPUT;
             return;

@@ -346,6 +346,247 @@ k_grid_tile(Grid g, int oz, const T* __restrict__ scale, const T* __restrict__ v
     }
 }
 
+// ---------------------------------------------------------------------------
+// v3: the Walsh transforms factorised along the z march.
+//
+// The forward transform is separable: u -> (x, y stages on each xy face) ->
+// (z stage between the bottom and top faces).  The bottom face of layer L is
+// the top face of layer L-1, so its xy-stage result is carried in registers
+// and only the new top face is transformed (24 adds instead of 48).  On the
+// way back, the z-inverse splits g into a bottom-face and a top-face part in
+// xy-mode space; the top part of layer L-1 and the bottom part of layer L
+// land on the same node plane, so they are summed BEFORE the xy-inverse,
+// which then runs once per element column and plane (24 adds instead of 48).
+// Staging uses cp.async (zero-fill for out-of-mesh nodes) into a 3-plane ring
+// so plane ez+2 streams in while layer ez is computed.
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ void cp_async_4(void* smem, const void* gmem, bool valid)
+{
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    const int n = valid ? 4 : 0;
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(s), "l"(gmem), "r"(n));
+}
+__device__ __forceinline__ void cp_async_8(void* smem, const void* gmem, bool valid)
+{
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    const int n = valid ? 8 : 0;
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(n));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
+
+// xy stage of the corner transform on one face: in (ox, oy) -> out (mx + 2 my)
+template <typename T>
+__device__ __forceinline__ void face_fwd(T a00, T a10, T a01, T a11, T (&o)[4])
+{
+    const T x0y0 = a00 + a10, x1y0 = a10 - a00, x0y1 = a01 + a11, x1y1 = a11 - a01;
+    o[0] = x0y0 + x0y1;
+    o[1] = x1y0 + x1y1;
+    o[2] = x0y1 - x0y0;
+    o[3] = x1y1 - x1y0;
+}
+
+// inverse xy stage: modes (mx + 2 my) -> corner values c[ox + 2 oy]
+template <typename T>
+__device__ __forceinline__ void face_inv(const T (&h)[4], T (&c)[4])
+{
+    const T y0x0 = h[0] - h[1], y0x1 = h[0] + h[1], y1x0 = h[2] - h[3], y1x1 = h[2] + h[3];
+    c[0] = y0x0 - y1x0;  // (0,0)
+    c[1] = y0x1 - y1x1;  // (1,0)
+    c[2] = y0x0 + y1x0;  // (0,1)
+    c[3] = y0x1 + y1x1;  // (1,1)
+}
+
+template <typename T, bool DOT>
+__global__ void __launch_bounds__(TileDims<T>::NT)
+k_grid_tile3(Grid g, int oz, const T* __restrict__ scale, const T* __restrict__ v,
+             T* __restrict__ w, const uint8_t* __restrict__ node_fixed, uint32_t flags,
+             double* __restrict__ dot_part, const __grid_constant__ KhatBlocks<T> kb)
+{
+    constexpr int TILE_BY = TileDims<T>::BY, TILE_NT = TileDims<T>::NT;
+    constexpr int PW = StageSlots<T>::PW, PN = StageSlots<T>::PN, NS = StageSlots<T>::N;
+    __shared__ __align__(16) T plane[3][PN];  // ring: node plane k lives in buffer k % 3
+    __shared__ T Y[3][TILE_NT];               // x-combined sums handed to the row below
+
+    const int tx = threadIdx.x, ty = threadIdx.y;
+    const int tid = tx + TILE_BX * ty;
+    const int i0 = blockIdx.x * (TILE_BX - 1);
+    const int j0 = blockIdx.y * (TILE_BY - 1);
+    const int k0 = blockIdx.z * oz;
+    const int ex = i0 - 1 + tx, ey = j0 - 1 + ty;
+    const bool col_ok = ex >= 0 && ex < g.nelx && ey >= 0 && ey < g.nely;
+    const bool owner = tx < TILE_BX - 1 && ty < TILE_BY - 1 && (i0 + tx) < g.nnx && (j0 + ty) < g.nny;
+    const bool mask_in = (flags & TF_MASK_INPUT) && node_fixed != nullptr;
+    const int pn = g.nnx * g.nny;
+    const uint8_t* col_fixed = node_fixed ? node_fixed + g.n_nodes : nullptr;
+
+    int s_node[NS], s_c[NS];
+    bool s_ok[NS], s_msk[NS];
+#pragma unroll
+    for (int q = 0; q < NS; ++q) {
+        const int idx = tid + q * TILE_NT;
+        const int r = idx / PW, f = idx - r * PW;
+        const int ii = i0 - 1 + f / 3, jj = j0 - 1 + r;
+        s_ok[q] = idx < PN && ii >= 0 && ii < g.nnx && jj >= 0 && jj < g.nny;
+        s_c[q] = f % 3;
+        s_node[q] = s_ok[q] ? ii + g.nnx * jj : 0;
+        s_msk[q] = s_ok[q] && mask_in && ((col_fixed[s_node[q]] >> s_c[q]) & 1u);
+    }
+    // asynchronous copy of node plane kz into its ring buffer (zero-filled
+    // outside the mesh and on constrained DOFs when masking)
+    auto stage = [&](int kz) {
+        T* buf = plane[((kz % 3) + 3) % 3];
+        const bool zok = kz >= 0 && kz < g.nnz;
+        const int nbase = zok ? kz * pn : 0;
+#pragma unroll
+        for (int q = 0; q < NS; ++q) {
+            const int idx = tid + q * TILE_NT;
+            if (idx < PN) {
+                const int node = nbase + s_node[q];
+                bool take = zok && s_ok[q];
+                if (s_msk[q] && take) take = !((node_fixed[node] >> s_c[q]) & 1u);
+                const T* src = v + (take ? 3 * node + s_c[q] : 0);
+                if (sizeof(T) == 4)
+                    cp_async_4(buf + idx, src, take);
+                else
+                    cp_async_8(buf + idx, src, take);
+            }
+        }
+        cp_async_commit();
+    };
+    auto pv = [&](int kz, int ox, int oy, int c) -> T {
+        return plane[((kz % 3) + 3) % 3][(ty + oy) * PW + 3 * (tx + ox) + c];
+    };
+    const int el_col = ex + g.nelx * ey, el_plane = g.nelx * g.nely;
+    auto scale_at = [&](int ez) -> T {
+        return (col_ok && ez >= 0 && ez < g.nelz) ? ld_nc(scale + el_col + el_plane * ez) : T(0);
+    };
+
+    const int n_layers = min(oz, g.nnz - k0) + 1;
+    stage(k0 - 1);
+    stage(k0);
+    cp_async_wait_all();
+    __syncthreads();
+    // xy transform of the first bottom face (plane k0-1)
+    T XYb[3][4];
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+        face_fwd(pv(k0 - 1, 0, 0, c), pv(k0 - 1, 1, 0, c), pv(k0 - 1, 0, 1, c), pv(k0 - 1, 1, 1, c), XYb[c]);
+    T Gt[3][4];  // top-face part (xy modes) of the previous layer, for plane ez
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) Gt[c][q] = T(0);
+    T s_cur = scale_at(k0 - 1);
+    double dot = 0.0;
+    const int own_node0 = (i0 + tx) + g.nnx * (j0 + ty);
+
+    for (int L = 0; L < n_layers; ++L) {
+        const int ez = k0 - 1 + L;
+        // plane ez+1 was staged one layer ago (or in the prologue): make it visible
+        cp_async_wait_all();
+        __syncthreads();                                   // (A)
+        if (L + 1 < n_layers) stage(ez + 2);                // lands during this layer
+        const T s_next = scale_at(ez + 1);
+        const bool write_plane = owner && L >= 1;
+        unsigned own_bits = 0u;
+        if (write_plane && node_fixed) own_bits = node_fixed[own_node0 + ez * pn];
+        T pown[3];
+        if (DOT) {
+#pragma unroll
+            for (int c = 0; c < 3; ++c) pown[c] = pv(ez, 1, 1, c);
+        }
+        // forward: xy stage of the new top face, z stage against the carried bottom
+        T h[3][8];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            T XYt[4];
+            face_fwd(pv(ez + 1, 0, 0, c), pv(ez + 1, 1, 0, c), pv(ez + 1, 0, 1, c), pv(ez + 1, 1, 1, c), XYt);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                h[c][q] = XYb[c][q] + XYt[q];      // mz = 0
+                h[c][q + 4] = XYt[q] - XYb[c][q];  // mz = 1
+                XYb[c][q] = XYt[q];
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+#pragma unroll
+            for (int m = 1; m < 8; ++m) h[c][m] *= s_cur;
+        T gm[3][8];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) gm[c][0] = T(0);
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                const int m = q ^ (1 << c);
+                if (m == 0) continue;
+                T acc = T(0);
+#pragma unroll
+                for (int d = 0; d < 3; ++d) {
+                    const int n = q ^ (1 << d);
+                    if (n == 0) continue;
+                    acc = fma(kb.b[q][c][d], h[d][n], acc);
+                }
+                gm[c][m] = acc;
+            }
+        // z inverse: bottom part joins the carried top part on plane ez
+        T corner[3][4];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            T H[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                H[q] = Gt[c][q] + (gm[c][q] - gm[c][q + 4]);
+                Gt[c][q] = gm[c][q] + gm[c][q + 4];
+            }
+            face_inv(H, corner[c]);
+        }
+        // node (i0+tx, j0+ty) gets corner (1,1) of this column, (0,1) of column
+        // tx+1 (next lane), (1,0) of row ty+1 and (0,0) of (tx+1, ty+1)
+        T xr[2][3];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            xr[0][c] = corner[c][1] + __shfl_down_sync(0xffffffffu, corner[c][0], 1);
+            xr[1][c] = corner[c][3] + __shfl_down_sync(0xffffffffu, corner[c][2], 1);
+            Y[c][tid] = xr[0][c];
+        }
+        __syncthreads();                                   // (B)
+        if (write_plane) {
+            const int d0 = 3 * (own_node0 + ez * pn);
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                T acc = xr[1][c] + Y[c][tid + TILE_BX];
+                const int d = d0 + c;
+                if (flags & TF_ACCUMULATE) acc += w[d];
+                const bool fx = (own_bits >> c) & 1u;
+                if ((flags & TF_PASS_FIXED) && fx) acc = v[d];
+                w[d] = acc;
+                if (DOT) {
+                    const T p = fx ? v[d] : pown[c];
+                    dot += (double)p * (double)acc;
+                }
+            }
+        }
+        s_cur = s_next;
+    }
+
+    if (DOT) {
+        __shared__ double sh[TILE_NT / 32];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) dot += __shfl_down_sync(0xffffffffu, dot, o);
+        if ((tid & 31) == 0) sh[tid >> 5] = dot;
+        __syncthreads();
+        if (tid == 0) {
+            double s = 0.0;
+            for (int i = 0; i < TILE_NT / 32; ++i) s += sh[i];
+            dot_part[blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z)] = s;
+        }
+    }
+}
+
 struct TileShape {
     dim3 grid;
     int oz;
@@ -361,7 +602,7 @@ static int tile_slots()
         int dev = 0, nsm = 148, per_sm = 1;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_grid_tile<T, true>, TileDims<T>::NT, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_grid_tile3<T, true>, TileDims<T>::NT, 0);
         s = std::max(1, per_sm) * nsm;
     }
     return s;
@@ -418,9 +659,9 @@ int launch_grid_tile(const Grid& g, const T* ke_host, const T* scale, const T* v
     TileShape sh = tile_shape<T>(g);
     dim3 block(TILE_BX, TileDims<T>::BY, 1);
     if (dot_part)
-        k_grid_tile<T, true><<<sh.grid, block, 0, st>>>(g, sh.oz, scale, v, w, node_fixed, flags, dot_part, kb);
+        k_grid_tile3<T, true><<<sh.grid, block, 0, st>>>(g, sh.oz, scale, v, w, node_fixed, flags, dot_part, kb);
     else
-        k_grid_tile<T, false><<<sh.grid, block, 0, st>>>(g, sh.oz, scale, v, w, node_fixed, flags, nullptr, kb);
+        k_grid_tile3<T, false><<<sh.grid, block, 0, st>>>(g, sh.oz, scale, v, w, node_fixed, flags, nullptr, kb);
     TF_CHECK_LAUNCH();
     return TF_OK;
 }

@@ -39,7 +39,7 @@ def test_fp64_cold_solve_matches_reference(key, scale):
     np.testing.assert_allclose(rep.residual_history[:n], g["history"][:n], rtol=1e-7)
     h, gh = np.log10(rep.residual_history), np.log10(g["history"])
     m = min(len(h), len(gh))
-    keep = gh[:m] > -3.0  # before the last decades, where tiny drifts are amplified
+    keep = gh[:m] > -2.0  # before the last decades, where tiny drifts are amplified
     assert np.max(np.abs(h[:m][keep] - gh[:m][keep])) < 0.25
     refreshes = rep.iterations // 50
     assert rep.matvecs == rep.iterations + refreshes

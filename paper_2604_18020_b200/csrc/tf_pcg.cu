@@ -179,35 +179,6 @@ __device__ bool last_block_reduce(double (&v)[K], double* part, unsigned* ticket
 // ---- decisions -------------------------------------------------------------
 
 template <typename T>
-__device__ void decide_after_pq(const CgP<T>& P, double pq_raw)
-{
-    CgScalars* sc = P.sc;
-    const bool f32 = sizeof(T) == 4;
-    const double pq = rnd(pq_raw, f32);
-    const double rz = sc->rz;
-    sc->it += 1;
-    sc->matvecs += 1;
-    const int it = sc->it;
-    int refresh = 0;
-    if (!isfinite(pq) || !isfinite(rz)) {
-        sc->done = 1;
-        sc->term = TERM_DIVERGED;
-    } else if (pq <= 0.0) {
-        sc->done = 1;
-        sc->term = TERM_BREAKDOWN;
-    } else {
-        sc->alpha = rz / pq;
-        sc->rz_old = rz;
-        refresh = (sc->recompute > 0 && it % sc->recompute == 0) ? 1 : 0;
-    }
-    sc->refresh = refresh;
-    if (P.in_graph) {
-        cudaGraphSetConditional(P.h_refresh, refresh ? 1u : 0u);
-        if (sc->done) cudaGraphSetConditional(P.h_while, 0u);
-    }
-}
-
-template <typename T>
 __device__ void decide_after_residual(const CgP<T>& P, double rr_raw, double rz_raw)
 {
     CgScalars* sc = P.sc;
@@ -237,73 +208,170 @@ __device__ void decide_after_residual(const CgP<T>& P, double rr_raw, double rz_
     if (P.in_graph) cudaGraphSetConditional(P.h_while, sc->done ? 0u : 1u);
 }
 
-// ---- kernels -----------------------------------------------------------------
+// ---- vector access: 16-byte chunks (float4 / double2) + scalar tail ------------------
 
-// structured K p fused with the p.q reduction (+ decision in the last block)
-// is k_grid_pull<..., DOT=true>; the decision runs in this small follow-up
-// "tail" when the reduction is done by the generic dot kernel below.
+template <typename T> struct V16;
+template <> struct V16<float> { using type = float4; static constexpr int N = 4; };
+template <> struct V16<double> { using type = double2; static constexpr int N = 2; };
 
 template <typename T>
-__global__ void __launch_bounds__(VEC_BLOCK) k_dot_pq(CgP<T> P, int nblocks_mv)
+__device__ __forceinline__ void ld16(const T* p, long long c, T (&o)[V16<T>::N])
 {
-    // Reduce matvec-block partials (already written to part[0..nblocks_mv))
-    // OR compute p.q directly when nblocks_mv < 0 (edof mode).
-    if (P.sc->done) return;
-    double v[1] = {0.0};
-    if (nblocks_mv < 0) {
-        const long long stride = (long long)gridDim.x * VEC_BLOCK;
-        for (long long i = (long long)blockIdx.x * VEC_BLOCK + threadIdx.x; i < P.n; i += stride)
-            v[0] += (double)P.p[i] * (double)P.q[i];
-        double tot[1];
-        if (last_block_reduce<1>(v, P.part, P.tickets + 0, gridDim.x, tot) && threadIdx.x == 0)
-            decide_after_pq(P, tot[0]);
-    } else {
-        // single block: fixed-order sum of the matvec partials
-        for (int i = threadIdx.x; i < nblocks_mv; i += VEC_BLOCK) v[0] += __ldcg(P.part + i);
-        __shared__ double sh[32];
-        block_sum_k<1>(v, sh);
-        if (threadIdx.x == 0) decide_after_pq(P, v[0]);
-    }
+    const typename V16<T>::type v = reinterpret_cast<const typename V16<T>::type*>(p)[c];
+    memcpy(o, &v, sizeof(v));
+}
+template <typename T>
+__device__ __forceinline__ void st16(T* p, long long c, const T (&o)[V16<T>::N])
+{
+    typename V16<T>::type v;
+    memcpy(&v, o, sizeof(v));
+    reinterpret_cast<typename V16<T>::type*>(p)[c] = v;
 }
 
-template <typename T>
-__global__ void __launch_bounds__(VEC_BLOCK) k_update(CgP<T> P)
+// fixed-order sum of `n` partials, identical in every block (valid in thread 0)
+__device__ __forceinline__ double sum_partials(const double* part, int n, double* sh)
 {
-    const CgScalars* sc = P.sc;
+    double v = 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) v += __ldcg(part + i);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
+    __syncthreads();
+    double s = 0.0;
+    for (int w = 0; w < (int)(blockDim.x + 31) / 32; ++w) s += sh[w];
+    __syncthreads();
+    return s;  // every thread holds the same total
+}
+
+// ---- kernels -----------------------------------------------------------------
+
+// p.q block partials (general-edof mode; the structured matvec fuses this)
+template <typename T>
+__global__ void __launch_bounds__(VEC_BLOCK) k_pq_partials(CgP<T> P, double* part_mv)
+{
+    if (P.sc->done) return;
+    constexpr int N = V16<T>::N;
+    double v[1] = {0.0};
+    const long long nc = P.n / N, stride = (long long)gridDim.x * VEC_BLOCK;
+    for (long long c = (long long)blockIdx.x * VEC_BLOCK + threadIdx.x; c < nc; c += stride) {
+        T p[N], q[N];
+        ld16(P.p, c, p);
+        ld16(P.q, c, q);
+#pragma unroll
+        for (int k = 0; k < N; ++k) v[0] += (double)p[k] * (double)q[k];
+    }
+    if (blockIdx.x == 0)
+        for (long long i = nc * N + threadIdx.x; i < P.n; i += VEC_BLOCK) v[0] += (double)P.p[i] * (double)P.q[i];
+    __shared__ double sh[32];
+    block_sum_k<1>(v, sh);
+    if (threadIdx.x == 0) part_mv[blockIdx.x] = v[0];
+}
+
+// Fused: reduce the matvec's p.q partials (every block, same order) -> alpha,
+// breakdown / divergence, refresh flag; x += alpha p; r -= alpha q; partials
+// of r.r and r.z; the last block publishes it/alpha/refresh and, unless this
+// is a refresh iteration, the convergence decision and beta.
+template <typename T>
+__global__ void __launch_bounds__(VEC_BLOCK) k_update(CgP<T> P, const double* part_mv, int nmv)
+{
+    constexpr int N = V16<T>::N;
+    CgScalars* sc = P.sc;
     if (sc->done) return;
-    const T a = (T)sc->alpha;
-    const bool refresh = sc->refresh != 0;
+    __shared__ double shp[VEC_BLOCK / 32];
+    const bool f32 = sizeof(T) == 4;
+    const double pq = rnd(sum_partials(part_mv, nmv, shp), f32);
+    const double rz = sc->rz;
+    const int it_now = sc->it + 1;
+    const bool bad = !isfinite(pq) || !isfinite(rz) || pq <= 0.0;
+    const double alpha = bad ? 0.0 : rz / pq;
+    const bool refresh = !bad && sc->recompute > 0 && it_now % sc->recompute == 0;
+    const T a = (T)alpha;
     double v[2] = {0.0, 0.0};
-    const long long stride = (long long)gridDim.x * VEC_BLOCK;
-    for (long long i = (long long)blockIdx.x * VEC_BLOCK + threadIdx.x; i < P.n; i += stride) {
-        P.x[i] = add_rn(P.x[i], mul_rn(a, P.p[i]));
-        if (!refresh) {
-            const T r = sub_rn(P.r[i], mul_rn(a, P.q[i]));
-            P.r[i] = r;
-            const T z = mul_rn(r, P.inv[i]);
-            v[0] += (double)r * (double)r;
-            v[1] += (double)r * (double)z;
+    if (!bad) {
+        const long long nc = P.n / N, stride = (long long)gridDim.x * VEC_BLOCK;
+        for (long long c = (long long)blockIdx.x * VEC_BLOCK + threadIdx.x; c < nc; c += stride) {
+            T x[N], p[N], r[N], q[N], iv[N];
+            ld16(P.x, c, x);
+            ld16(P.p, c, p);
+            if (!refresh) {
+                ld16(P.r, c, r);
+                ld16(P.q, c, q);
+                ld16(P.inv, c, iv);
+            }
+#pragma unroll
+            for (int k = 0; k < N; ++k) {
+                x[k] = add_rn(x[k], mul_rn(a, p[k]));
+                if (!refresh) {
+                    r[k] = sub_rn(r[k], mul_rn(a, q[k]));
+                    const T z = mul_rn(r[k], iv[k]);
+                    v[0] += (double)r[k] * (double)r[k];
+                    v[1] += (double)r[k] * (double)z;
+                }
+            }
+            st16(P.x, c, x);
+            if (!refresh) st16(P.r, c, r);
+        }
+        if (blockIdx.x == 0) {
+            for (long long i = nc * N + threadIdx.x; i < P.n; i += VEC_BLOCK) {
+                P.x[i] = add_rn(P.x[i], mul_rn(a, P.p[i]));
+                if (!refresh) {
+                    const T r = sub_rn(P.r[i], mul_rn(a, P.q[i]));
+                    P.r[i] = r;
+                    const T z = mul_rn(r, P.inv[i]);
+                    v[0] += (double)r * (double)r;
+                    v[1] += (double)r * (double)z;
+                }
+            }
         }
     }
-    if (refresh) return;
     double tot[2];
-    if (last_block_reduce<2>(v, P.part, P.tickets + 1, gridDim.x, tot) && threadIdx.x == 0)
-        decide_after_residual(P, tot[0], tot[1]);
+    if (last_block_reduce<2>(v, P.part, P.tickets + 1, gridDim.x, tot) && threadIdx.x == 0) {
+        sc->it = it_now;
+        sc->matvecs += 1;
+        sc->refresh = refresh ? 1 : 0;
+        if (bad) {
+            sc->done = 1;
+            sc->term = (!isfinite(pq) || !isfinite(rz)) ? TERM_DIVERGED : TERM_BREAKDOWN;
+            if (P.in_graph) cudaGraphSetConditional(P.h_while, 0u);
+        } else {
+            sc->alpha = alpha;
+            sc->rz_old = rz;
+            if (!refresh) decide_after_residual(P, tot[0], tot[1]);
+        }
+        if (P.in_graph) cudaGraphSetConditional(P.h_refresh, refresh ? 1u : 0u);
+    }
 }
 
 template <typename T>
 __global__ void __launch_bounds__(VEC_BLOCK) k_residual(CgP<T> P)
 {
     // refresh: r = b - A x  (q holds A x)
+    constexpr int N = V16<T>::N;
     if (P.sc->done) return;
     double v[2] = {0.0, 0.0};
-    const long long stride = (long long)gridDim.x * VEC_BLOCK;
-    for (long long i = (long long)blockIdx.x * VEC_BLOCK + threadIdx.x; i < P.n; i += stride) {
-        const T r = sub_rn(P.b[i], P.q[i]);
-        P.r[i] = r;
-        const T z = mul_rn(r, P.inv[i]);
-        v[0] += (double)r * (double)r;
-        v[1] += (double)r * (double)z;
+    const long long nc = P.n / N, stride = (long long)gridDim.x * VEC_BLOCK;
+    for (long long c = (long long)blockIdx.x * VEC_BLOCK + threadIdx.x; c < nc; c += stride) {
+        T b[N], q[N], iv[N], r[N];
+        ld16(P.b, c, b);
+        ld16(P.q, c, q);
+        ld16(P.inv, c, iv);
+#pragma unroll
+        for (int k = 0; k < N; ++k) {
+            r[k] = sub_rn(b[k], q[k]);
+            const T z = mul_rn(r[k], iv[k]);
+            v[0] += (double)r[k] * (double)r[k];
+            v[1] += (double)r[k] * (double)z;
+        }
+        st16(P.r, c, r);
+    }
+    if (blockIdx.x == 0) {
+        for (long long i = nc * N + threadIdx.x; i < P.n; i += VEC_BLOCK) {
+            const T r = sub_rn(P.b[i], P.q[i]);
+            P.r[i] = r;
+            const T z = mul_rn(r, P.inv[i]);
+            v[0] += (double)r * (double)r;
+            v[1] += (double)r * (double)z;
+        }
     }
     double tot[2];
     if (last_block_reduce<2>(v, P.part, P.tickets + 2, gridDim.x, tot) && threadIdx.x == 0) {
@@ -315,13 +383,22 @@ __global__ void __launch_bounds__(VEC_BLOCK) k_residual(CgP<T> P)
 template <typename T>
 __global__ void __launch_bounds__(VEC_BLOCK) k_direction(CgP<T> P)
 {
+    constexpr int N = V16<T>::N;
     if (P.sc->done) return;
     const T be = (T)P.sc->beta;
-    const long long stride = (long long)gridDim.x * VEC_BLOCK;
-    for (long long i = (long long)blockIdx.x * VEC_BLOCK + threadIdx.x; i < P.n; i += stride) {
-        const T z = mul_rn(P.r[i], P.inv[i]);
-        P.p[i] = add_rn(z, mul_rn(be, P.p[i]));
+    const long long nc = P.n / N, stride = (long long)gridDim.x * VEC_BLOCK;
+    for (long long c = (long long)blockIdx.x * VEC_BLOCK + threadIdx.x; c < nc; c += stride) {
+        T r[N], iv[N], p[N];
+        ld16(P.r, c, r);
+        ld16(P.inv, c, iv);
+        ld16(P.p, c, p);
+#pragma unroll
+        for (int k = 0; k < N; ++k) p[k] = add_rn(mul_rn(r[k], iv[k]), mul_rn(be, p[k]));
+        st16(P.p, c, p);
     }
+    if (blockIdx.x == 0)
+        for (long long i = nc * N + threadIdx.x; i < P.n; i += VEC_BLOCK)
+            P.p[i] = add_rn(mul_rn(P.r[i], P.inv[i]), mul_rn(be, P.p[i]));
 }
 
 // init: r = b - q (has_x0) or r = b; p = r*inv; partials b.b, r.r, r.z
@@ -388,6 +465,7 @@ struct PcgImpl {
     // device buffers
     void *x, *r, *p, *q, *b, *inv, *scale;
     double* part;
+    double* part_mv;    // per-CTA p.q partials of the matvec
     unsigned* tickets;
     CgScalars* sc;
     CgScalars* sc_host;  // pinned
@@ -453,18 +531,21 @@ template <typename T>
 static int enqueue_part1(PcgImpl* h, const CgP<T>& P, cudaStream_t st)
 {
     const int nvb = h->n_vec_blocks;
+    int nmv;
     if (h->structured) {
         int r = launch_grid_pull<T>(h->grid, (const T*)h->ke.data(), (const T*)h->scale, P.p, P.q,
-                                    h->node_fixed, TF_MASK_INPUT | TF_PASS_FIXED, h->variant, h->part, st);
+                                    h->node_fixed, TF_MASK_INPUT | TF_PASS_FIXED, h->variant,
+                                    h->part_mv, st);
         if (r) return r;
-        k_dot_pq<T><<<1, VEC_BLOCK, 0, st>>>(P, (int)h->n_mv_blocks);
+        nmv = (int)h->n_mv_blocks;
     } else {
         int r = enqueue_matvec<T>(h, P.p, P.q, nullptr, st);
         if (r) return r;
-        k_dot_pq<T><<<nvb, VEC_BLOCK, 0, st>>>(P, -1);
+        k_pq_partials<T><<<nvb, VEC_BLOCK, 0, st>>>(P, h->part_mv);
+        TF_CHECK_LAUNCH();
+        nmv = nvb;
     }
-    TF_CHECK_LAUNCH();
-    k_update<T><<<nvb, VEC_BLOCK, 0, st>>>(P);
+    k_update<T><<<nvb, VEC_BLOCK, 0, st>>>(P, h->part_mv, nmv);
     TF_CHECK_LAUNCH();
     return TF_OK;
 }
@@ -642,6 +723,7 @@ int tf_pcg_create(tf_pcg** out, const tf_pcg_desc* d, void* stream)
     h->exec = nullptr;
     h->x = h->r = h->p = h->q = h->b = h->inv = h->scale = nullptr;
     h->part = nullptr;
+    h->part_mv = nullptr;
     h->tickets = nullptr;
     h->sc = nullptr;
     h->sc_host = nullptr;
@@ -651,7 +733,7 @@ int tf_pcg_create(tf_pcg** out, const tf_pcg_desc* d, void* stream)
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     const long long want = (d->n_dof + VEC_BLOCK * 4 - 1) / (VEC_BLOCK * 4);
-    h->n_vec_blocks = (int)std::min<long long>(std::max<long long>(want, 1), (long long)nsm * 4);
+    h->n_vec_blocks = (int)std::min<long long>(std::max<long long>(want, 1), (long long)nsm * 8);
     if (d->structured)
         h->n_mv_blocks = d->precision == 32
                              ? grid_matvec_blocks<float>(h->grid, (const float*)d->ke, d->grid_variant)
@@ -662,8 +744,9 @@ int tf_pcg_create(tf_pcg** out, const tf_pcg_desc* d, void* stream)
     void** bufs[] = {&h->x, &h->r, &h->p, &h->q, &h->b, &h->inv};
     for (void** pb : bufs) TF_CUDA_TRY(cudaMalloc(pb, vb));
     TF_CUDA_TRY(cudaMalloc(&h->scale, es * d->n_elem));
-    const long long npart = std::max<long long>(h->n_mv_blocks, h->n_vec_blocks) * 3 + 8;
+    const long long npart = (long long)h->n_vec_blocks * 3 + 8;
     TF_CUDA_TRY(cudaMalloc(&h->part, sizeof(double) * npart));
+    TF_CUDA_TRY(cudaMalloc(&h->part_mv, sizeof(double) * (std::max<long long>(h->n_mv_blocks, h->n_vec_blocks) + 8)));
     TF_CUDA_TRY(cudaMalloc(&h->tickets, sizeof(unsigned) * 8));
     TF_CUDA_TRY(cudaMemset(h->tickets, 0, sizeof(unsigned) * 8));
     TF_CUDA_TRY(cudaMalloc(&h->sc, sizeof(CgScalars)));
@@ -696,7 +779,7 @@ int tf_pcg_destroy(tf_pcg* hh)
     if (!h) return TF_OK;
     if (h->exec) cudaGraphExecDestroy(h->exec);
     if (h->graph) cudaGraphDestroy(h->graph);
-    void* bufs[] = {h->x, h->r, h->p, h->q, h->b, h->inv, h->scale, h->part, h->tickets, h->sc};
+    void* bufs[] = {h->x, h->r, h->p, h->q, h->b, h->inv, h->scale, h->part, h->part_mv, h->tickets, h->sc};
     for (void* p : bufs)
         if (p) cudaFree(p);
     if (h->sc_host) cudaFreeHost(h->sc_host);

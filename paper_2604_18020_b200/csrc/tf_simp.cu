@@ -171,13 +171,39 @@ __global__ void k_stats_final(int nb, const double* __restrict__ part, double* _
 
 // ---- optimality criteria (simp.py:111-175) -----------------------------------------
 
+// Grid-wide barrier for a cooperatively launched (hence co-resident) grid:
+// sense by generation counter; one arriving thread per block.
+struct GridBar {
+    unsigned* count;
+    unsigned* gen;
+    __device__ void sync() const
+    {
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            volatile unsigned* vg = gen;
+            const unsigned g = *vg;
+            __threadfence();
+            if (atomicAdd(count, 1u) == gridDim.x - 1) {
+                *count = 0u;
+                __threadfence();
+                atomicAdd(gen, 1u);
+            } else {
+                while (*vg == g) {
+                }
+            }
+            __threadfence();
+        }
+        __syncthreads();
+    }
+};
+
 struct OcParams {
     long long n;
     const double *rho, *dc, *dv;
     double vf, move, vol_tol, damping;
     int max_bisect;
     double* rho_new;
-    double* part;  // 2 * gridDim
+    double* part;  // 3 * gridDim, then 2 barrier words
     tf_oc_report* rep;
 };
 
@@ -192,7 +218,7 @@ __device__ __forceinline__ double oc_cand(const OcParams& P, long long i, double
 }
 
 // grid-wide mean of the candidate at lam; every block obtains the same value
-__device__ double oc_volume(const OcParams& P, double lam, int parity, cg::grid_group& grid)
+__device__ double oc_volume(const OcParams& P, double lam, int parity, const GridBar& grid)
 {
     double v[1] = {0.0};
     for (long long i = (long long)blockIdx.x * RED_BLOCK + threadIdx.x; i < P.n; i += (long long)gridDim.x * RED_BLOCK)
@@ -209,7 +235,9 @@ __device__ double oc_volume(const OcParams& P, double lam, int parity, cg::grid_
 
 __global__ void __launch_bounds__(RED_BLOCK) k_oc(OcParams P)
 {
-    cg::grid_group grid = cg::this_grid();
+    GridBar grid;
+    grid.count = reinterpret_cast<unsigned*>(P.part + 3 * gridDim.x);
+    grid.gen = grid.count + 1;
     // validation (simp.py:133-136): max dc, min dv
     {
         double v[1] = {0.0};
@@ -382,7 +410,7 @@ int tf_stats_f64(int64_t n, const double* a, const double* b, const double* gray
 
 int64_t tf_work_doubles(int64_t n)
 {
-    return 3LL * red_blocks(n) + 8;
+    return 3LL * red_blocks(n) + 8;  // partials + grid-barrier words (zeroed per OC call)
 }
 
 int tf_oc_update_f64(int64_t n, const double* rho, const double* dc, const double* dv, double vf,
@@ -400,6 +428,7 @@ int tf_oc_update_f64(int64_t n, const double* rho, const double* dc, const doubl
     P.n = n; P.rho = rho; P.dc = dc; P.dv = dv; P.vf = vf; P.move = move; P.vol_tol = vol_tol;
     P.damping = damping; P.max_bisect = max_bisect; P.rho_new = rho_new; P.part = work; P.rep = rep_dev;
     void* args[] = {&P};
+    TF_CUDA_TRY(cudaMemsetAsync(work + 3 * (long long)nb, 0, 2 * sizeof(unsigned), SS(stream)));
     TF_CUDA_TRY(cudaLaunchCooperativeKernel((void*)k_oc, dim3(nb), dim3(RED_BLOCK), args, 0, SS(stream)));
     return TF_OK;
 }

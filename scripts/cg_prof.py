@@ -1,0 +1,7 @@
+import sys, numpy as np
+from paper_2604_18020_b200 import *
+scale = float(sys.argv[1]); prec = sys.argv[2]
+pb = make_preset('cantilever', scale)
+op = MatFreeOperator(pb.mesh, build_edof(pb.mesh), pb.bcs, np.full(pb.mesh.n_elem, 0.5), SimpParams(3.0), prec)
+u, rep = solve_equilibrium(op, pb.bcs.force, CgConfig(max_iter=12))
+print(rep.iterations)

@@ -68,7 +68,8 @@ def test_projection_and_sensitivity():
         np.testing.assert_allclose(out.cpu().numpy(), want, rtol=1e-12, atol=1e-12 * np.abs(want).max())
 
 
-@pytest.mark.parametrize("n,vf,move", [(128, 0.4, 0.2), (10_000, 0.3, 0.05), (216_000, 0.3, 0.15)])
+@pytest.mark.parametrize("n,vf,move", [(128, 0.4, 0.2), (10_000, 0.3, 0.05), (216_000, 0.3, 0.15),
+                                        (10_000, 0.45, 0.1), (216_000, 0.5, 0.2), (50_000, 0.6, 0.02)])
 def test_oc_update_matches_host(n, vf, move):
     import torch
 
@@ -90,8 +91,11 @@ def test_oc_update_matches_host(n, vf, move):
     h = rep_d.cpu().numpy()
     ctypes.memmove(ctypes.addressof(rep), h.ctypes.data, ctypes.sizeof(rep))
     got = out.cpu().numpy()
-    assert _lib.OC_STATUS[rep.status] == "ok"
-    assert abs(got.mean() - vf) <= 1e-6
+    reachable = np.mean(np.maximum(0.0, rho - move)) <= vf <= np.mean(np.minimum(1.0, rho + move))
+    # unreachable targets saturate at the nearest candidate, like simp.py:146-159
+    assert _lib.OC_STATUS[rep.status] == ("ok" if reachable else "saturated")
+    if reachable:
+        assert abs(got.mean() - vf) <= 1e-6
     assert np.abs(got - want).max() <= 1e-9
 
 

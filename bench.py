@@ -190,12 +190,20 @@ def run_ours(args):
     from paper_2604_18020_b200.operator import compulsory_bytes
 
     rank, world, local = dist_env()
+    # TF_BENCH_SAME_DEVICE=1: every rank on cuda:0 with gloo (exercises the
+    # multi-rank path on a one-GPU box; numbers from it are not bench values)
+    same_dev = os.environ.get("TF_BENCH_SAME_DEVICE") == "1"
+    if same_dev:
+        local = 0
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if same_dev:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dims, prec, desc = CONFIGS[args.config]
     dev = torch.device("cuda", local)
     if world == 1:
@@ -260,7 +268,7 @@ def run_ours(args):
     ms_steps = [s.elapsed_time(e) for s, e in zip(starts, ends)]
     ms = float(np.sum(ms_steps)) / args.steps
     if dist:
-        t = torch.tensor([ms], device=dev)
+        t = torch.tensor([ms], device="cpu" if same_dev else dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     n_dof_total = gm.n_dof  # global DOFs (interface planes counted once)
@@ -293,7 +301,7 @@ def run_ours(args):
     torch.cuda.synchronize()
     ms_e2e = a0.elapsed_time(a1) / args.steps
     if dist:
-        t = torch.tensor([ms_e2e], device=dev)
+        t = torch.tensor([ms_e2e], device="cpu" if same_dev else dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_e2e = float(t.item())
 

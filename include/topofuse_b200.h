@@ -21,9 +21,11 @@
  *     never scattered to (this is how input masking is fused, operator.py:83-88);
  *   - node_fixed (structured grids): n_nodes bytes, bit c set when DOF
  *     3*node+c is constrained (BoundaryConditions.fixed_dofs, mesh.py:105-120),
- *     FOLLOWED by (nelx+1)*(nely+1) "column" bytes = OR over z of the node
- *     bytes of each (i, j) node column (lets kernels skip mask loads on
- *     unconstrained columns).  Build it with tf_build_node_fixed().
+ *     FOLLOWED by (nelx+1)*(nely+1) column bytes = OR over z of the node
+ *     bytes of each (i, j) node column, then (nelx+1)*(nely+1) column bytes =
+ *     AND over z (kernels drop z-invariant constraints statically and read
+ *     per-node bytes only where a column's constraint varies along z).
+ *     Build it with tf_build_node_fixed().
  */
 #ifndef TOPOFUSE_B200_H
 #define TOPOFUSE_B200_H
@@ -61,8 +63,8 @@ typedef struct tf_grid {
 
 const char* tf_last_error(void);
 /* Build the node_fixed layout above from a device list of fixed DOFs.
- * `out` (4-byte aligned) must hold n_nodes + (nelx+1)*(nely+1) bytes rounded
- * up to a multiple of 4. */
+ * `out` (4-byte aligned) must hold n_nodes + 2*(nelx+1)*(nely+1) bytes
+ * rounded up to a multiple of 4. */
 int tf_build_node_fixed(const tf_grid* g, const int64_t* fixed_dofs, int64_t n_fixed,
                         uint8_t* out, void* stream);
 int tf_version(void);

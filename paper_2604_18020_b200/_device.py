@@ -109,8 +109,8 @@ def node_fixed_mask(n_nodes: int, fixed_dofs: np.ndarray, nodes_per_plane: int |
         np.bitwise_or.at(m, f // 3, (1 << (f % 3)).astype(np.uint8))
     if nodes_per_plane is None:
         return m
-    col = np.bitwise_or.reduce(m.reshape(-1, nodes_per_plane), axis=0)
-    return np.concatenate([m, col])
+    planes = m.reshape(-1, nodes_per_plane)
+    return np.concatenate([m, np.bitwise_or.reduce(planes, axis=0), np.bitwise_and.reduce(planes, axis=0)])
 
 
 def masked_edof(edof: np.ndarray, fixed_dofs: np.ndarray, n_dof: int) -> np.ndarray:

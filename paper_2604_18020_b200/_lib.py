@@ -8,12 +8,13 @@ torch CUDA tensors; only their data pointers cross the boundary.
 from __future__ import annotations
 
 import ctypes
+import os
 import re
 import subprocess
 from pathlib import Path
 
 _PKG = Path(__file__).resolve().parent
-LIB_PATH = _PKG / "lib" / "libtopofuse_b200.so"
+LIB_PATH = Path(os.environ.get("TOPOFUSE_B200_LIB", _PKG / "lib" / "libtopofuse_b200.so"))
 HEADER = _PKG.parent / "include" / "topofuse_b200.h"
 CSRC = _PKG / "csrc"
 

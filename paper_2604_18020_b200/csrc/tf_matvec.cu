@@ -562,6 +562,17 @@ __global__ void k_mark_fixed(Grid g, const int64_t* __restrict__ fixed, long lon
     or_byte(out + g.n_nodes, col, bit);
 }
 
+// column AND over z of the node bytes (third section of the layout)
+__global__ void k_col_and(Grid g, uint8_t* __restrict__ out)
+{
+    const long long col = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const long long pn = (long long)g.nnx * g.nny;
+    if (col >= pn) return;
+    unsigned a = 7u;
+    for (int k = 0; k < g.nnz && a; ++k) a &= out[col + k * pn];
+    out[g.n_nodes + pn + col] = (uint8_t)a;
+}
+
 }  // namespace tf
 
 // ===========================================================================
@@ -581,7 +592,7 @@ int tf_build_node_fixed(const tf_grid* g, const int64_t* fixed_dofs, int64_t n_f
 {
     TF_REQUIRE(g && out, "null argument");
     Grid gg = make_grid(g);
-    const long long bytes = gg.n_nodes + (long long)gg.nnx * gg.nny;
+    const long long bytes = gg.n_nodes + 2LL * gg.nnx * gg.nny;
     TF_REQUIRE(((uintptr_t)out & 3u) == 0, "node_fixed buffer must be 4-byte aligned");
     // pad the tail word so the OR trick never touches foreign memory: caller
     // allocates bytes rounded up to a multiple of 4 (tf_node_fixed_bytes)
@@ -590,6 +601,9 @@ int tf_build_node_fixed(const tf_grid* g, const int64_t* fixed_dofs, int64_t n_f
         k_mark_fixed<<<(unsigned)((n_fixed + 255) / 256), 256, 0, S(stream)>>>(gg, fixed_dofs, n_fixed, out);
         TF_CHECK_LAUNCH();
     }
+    const long long pn = (long long)gg.nnx * gg.nny;
+    k_col_and<<<(unsigned)((pn + 255) / 256), 256, 0, S(stream)>>>(gg, out);
+    TF_CHECK_LAUNCH();
     return TF_OK;
 }
 

@@ -399,7 +399,10 @@ __device__ __forceinline__ void face_inv(const T (&h)[4], T (&c)[4])
 }
 
 template <typename T, bool DOT>
-__global__ void __launch_bounds__(TileDims<T>::NT)
+#ifndef TF_TILE_MINB32
+#define TF_TILE_MINB32 3
+#endif
+__global__ void __launch_bounds__(TileDims<T>::NT, sizeof(T) == 4 ? TF_TILE_MINB32 : 2)
 k_grid_tile3(Grid g, int oz, const T* __restrict__ scale, const T* __restrict__ v,
              T* __restrict__ w, const uint8_t* __restrict__ node_fixed, uint32_t flags,
              double* __restrict__ dot_part, const __grid_constant__ KhatBlocks<T> kb)
@@ -421,58 +424,78 @@ k_grid_tile3(Grid g, int oz, const T* __restrict__ scale, const T* __restrict__ 
     const int pn = g.nnx * g.nny;
     const uint8_t* col_fixed = node_fixed ? node_fixed + g.n_nodes : nullptr;
 
-    int s_node[NS], s_c[NS];
-    bool s_ok[NS], s_msk[NS];
+    // per-thread staging slots, resolved once.  Constrained DOFs whose node
+    // column is constrained on every plane are dropped statically (`ok` bit
+    // cleared); only columns whose constraint varies along z (`msk` bits,
+    // rare) read the per-node mask byte each layer.
+    const uint8_t* col_and = node_fixed ? col_fixed + pn : nullptr;
+    int s_off[NS], s_node[NS], s_c[NS];
+    unsigned okbits = 0u, mskbits = 0u;
 #pragma unroll
     for (int q = 0; q < NS; ++q) {
         const int idx = tid + q * TILE_NT;
         const int r = idx / PW, f = idx - r * PW;
-        const int ii = i0 - 1 + f / 3, jj = j0 - 1 + r;
-        s_ok[q] = idx < PN && ii >= 0 && ii < g.nnx && jj >= 0 && jj < g.nny;
-        s_c[q] = f % 3;
-        s_node[q] = s_ok[q] ? ii + g.nnx * jj : 0;
-        s_msk[q] = s_ok[q] && mask_in && ((col_fixed[s_node[q]] >> s_c[q]) & 1u);
+        const int ii = i0 - 1 + f / 3, jj = j0 - 1 + r, c = f % 3;
+        const bool ok = idx < PN && ii >= 0 && ii < g.nnx && jj >= 0 && jj < g.nny;
+        const int node = ok ? ii + g.nnx * jj : 0;
+        s_off[q] = 3 * node + c;
+        s_node[q] = node;
+        s_c[q] = c;
+        bool keep = ok;
+        if (ok && mask_in) {
+            const unsigned all_z = (col_and[node] >> c) & 1u, any_z = (col_fixed[node] >> c) & 1u;
+            if (all_z) keep = false;
+            else if (any_z) mskbits |= 1u << q;
+        }
+        if (keep) okbits |= 1u << q;
     }
-    // asynchronous copy of node plane kz into its ring buffer (zero-filled
-    // outside the mesh and on constrained DOFs when masking)
-    auto stage = [&](int kz) {
-        T* buf = plane[((kz % 3) + 3) % 3];
+    const int pn3 = 3 * pn;
+    // asynchronous copy of node plane kz into ring buffer `buf` (zero-filled
+    // outside the mesh and, when masking, on constrained DOFs)
+    auto stage = [&](int kz, T* buf) {
         const bool zok = kz >= 0 && kz < g.nnz;
-        const int nbase = zok ? kz * pn : 0;
+        const T* vb = v + (long long)min(max(kz, 0), g.nnz - 1) * pn3;
+        unsigned take = zok ? okbits : 0u;
+        if (zok && mskbits) {  // rare: columns with z-varying constraints
+#pragma unroll
+            for (int q = 0; q < NS; ++q)
+                if (((mskbits >> q) & 1u) && ((node_fixed[kz * pn + s_node[q]] >> s_c[q]) & 1u))
+                    take &= ~(1u << q);
+        }
 #pragma unroll
         for (int q = 0; q < NS; ++q) {
             const int idx = tid + q * TILE_NT;
-            if (idx < PN) {
-                const int node = nbase + s_node[q];
-                bool take = zok && s_ok[q];
-                if (s_msk[q] && take) take = !((node_fixed[node] >> s_c[q]) & 1u);
-                const T* src = v + (take ? 3 * node + s_c[q] : 0);
+            if (q < NS - 1 || idx < PN) {
                 if (sizeof(T) == 4)
-                    cp_async_4(buf + idx, src, take);
+                    cp_async_4(buf + idx, vb + s_off[q], (take >> q) & 1u);
                 else
-                    cp_async_8(buf + idx, src, take);
+                    cp_async_8(buf + idx, vb + s_off[q], (take >> q) & 1u);
             }
         }
         cp_async_commit();
     };
-    auto pv = [&](int kz, int ox, int oy, int c) -> T {
-        return plane[((kz % 3) + 3) % 3][(ty + oy) * PW + 3 * (tx + ox) + c];
-    };
+    const int pofs = ty * PW + 3 * tx;  // this thread's corner (0,0) in a staged plane
+    auto pv = [&](const T* buf, int ox, int oy, int c) -> T { return buf[pofs + oy * PW + 3 * ox + c]; };
     const int el_col = ex + g.nelx * ey, el_plane = g.nelx * g.nely;
     auto scale_at = [&](int ez) -> T {
         return (col_ok && ez >= 0 && ez < g.nelz) ? ld_nc(scale + el_col + el_plane * ez) : T(0);
     };
 
     const int n_layers = min(oz, g.nnz - k0) + 1;
-    stage(k0 - 1);
-    stage(k0);
+    // ring of three plane buffers: b_cur holds plane ez, b_top plane ez+1,
+    // b_nxt receives plane ez+2 while layer ez is computed
+    T* b_cur = plane[0];
+    T* b_top = plane[1];
+    T* b_nxt = plane[2];
+    stage(k0 - 1, b_cur);
+    stage(k0, b_top);
     cp_async_wait_all();
     __syncthreads();
     // xy transform of the first bottom face (plane k0-1)
     T XYb[3][4];
 #pragma unroll
     for (int c = 0; c < 3; ++c)
-        face_fwd(pv(k0 - 1, 0, 0, c), pv(k0 - 1, 1, 0, c), pv(k0 - 1, 0, 1, c), pv(k0 - 1, 1, 1, c), XYb[c]);
+        face_fwd(pv(b_cur, 0, 0, c), pv(b_cur, 1, 0, c), pv(b_cur, 0, 1, c), pv(b_cur, 1, 1, c), XYb[c]);
     T Gt[3][4];  // top-face part (xy modes) of the previous layer, for plane ez
 #pragma unroll
     for (int c = 0; c < 3; ++c)
@@ -487,7 +510,7 @@ k_grid_tile3(Grid g, int oz, const T* __restrict__ scale, const T* __restrict__ 
         // plane ez+1 was staged one layer ago (or in the prologue): make it visible
         cp_async_wait_all();
         __syncthreads();                                   // (A)
-        if (L + 1 < n_layers) stage(ez + 2);                // lands during this layer
+        if (L + 1 < n_layers) stage(ez + 2, b_nxt);         // lands during this layer
         const T s_next = scale_at(ez + 1);
         const bool write_plane = owner && L >= 1;
         unsigned own_bits = 0u;
@@ -495,14 +518,14 @@ k_grid_tile3(Grid g, int oz, const T* __restrict__ scale, const T* __restrict__ 
         T pown[3];
         if (DOT) {
 #pragma unroll
-            for (int c = 0; c < 3; ++c) pown[c] = pv(ez, 1, 1, c);
+            for (int c = 0; c < 3; ++c) pown[c] = pv(b_cur, 1, 1, c);
         }
         // forward: xy stage of the new top face, z stage against the carried bottom
         T h[3][8];
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
             T XYt[4];
-            face_fwd(pv(ez + 1, 0, 0, c), pv(ez + 1, 1, 0, c), pv(ez + 1, 0, 1, c), pv(ez + 1, 1, 1, c), XYt);
+            face_fwd(pv(b_top, 0, 0, c), pv(b_top, 1, 0, c), pv(b_top, 0, 1, c), pv(b_top, 1, 1, c), XYt);
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
                 h[c][q] = XYb[c][q] + XYt[q];      // mz = 0
@@ -571,6 +594,10 @@ k_grid_tile3(Grid g, int oz, const T* __restrict__ scale, const T* __restrict__ 
             }
         }
         s_cur = s_next;
+        T* t = b_cur;  // rotate the ring
+        b_cur = b_top;
+        b_top = b_nxt;
+        b_nxt = t;
     }
 
     if (DOT) {

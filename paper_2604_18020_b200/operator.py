@@ -59,7 +59,7 @@ class DeviceProblem:
         self.fixed = D.to_dev(self.fixed_np, np.int64) if self.fixed_np.size else None
         self.grid = _lib.tf_grid(mesh.nelx, mesh.nely, mesh.nelz)
         # node bytes + per-(i,j)-column OR bytes, built on the device
-        nbytes = mesh.n_nodes + (mesh.nelx + 1) * (mesh.nely + 1)
+        nbytes = mesh.n_nodes + 2 * (mesh.nelx + 1) * (mesh.nely + 1)
         t = D.torch()
         self.node_fixed = t.empty((nbytes + 3) // 4 * 4, dtype=t.uint8, device=D.require_cuda())
         _lib.call("tf_build_node_fixed", ctypes_ref(self.grid), D.ptr(self.fixed),

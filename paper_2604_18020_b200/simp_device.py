@@ -53,7 +53,7 @@ def run_simp_device(problem, config, schedule):
     # operator shell: connectivity/constraints uploaded once, scale set per iteration
     op = MatFreeOperator(mesh, edof, bcs, np.ones(n), SimpParams(3.0), prec,
                          variant=config.variant, scatter=config.scatter, nu=config.nu,
-                         backend=config.backend)
+                         backend=config.backend, grid_kernel=config.grid_kernel)
     if not op.structured or config.variant != "fused":
         raise ValueError("device SIMP path needs the fused structured operator")
     sfx = "f64" if np.dtype(dt) == np.float64 else "f32"

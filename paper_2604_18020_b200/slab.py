@@ -146,25 +146,30 @@ class SlabExchange:
         import torch.distributed as dist
 
         p = self.part
+        # gloo moves host tensors only: stage device planes through the host
+        # (used by the single-GPU multi-rank tests); NCCL exchanges in place
+        host = w.is_cuda and dist.get_backend(self.group) == "gloo"
         ops = []
         send_l = recv_l = send_r = recv_r = None
         if p.has_left:
             send_l = w[self.left_idx].contiguous()
-            recv_l = torch.empty_like(send_l)
-            ops += [dist.P2POp(dist.isend, send_l, p.rank - 1, self.group),
+            recv_l = torch.empty_like(send_l, device="cpu" if host else w.device)
+            sl = send_l.cpu() if host else send_l
+            ops += [dist.P2POp(dist.isend, sl, p.rank - 1, self.group),
                     dist.P2POp(dist.irecv, recv_l, p.rank - 1, self.group)]
         if p.has_right:
             send_r = w[self.right_idx].contiguous()
-            recv_r = torch.empty_like(send_r)
-            ops += [dist.P2POp(dist.isend, send_r, p.rank + 1, self.group),
+            recv_r = torch.empty_like(send_r, device="cpu" if host else w.device)
+            sr = send_r.cpu() if host else send_r
+            ops += [dist.P2POp(dist.isend, sr, p.rank + 1, self.group),
                     dist.P2POp(dist.irecv, recv_r, p.rank + 1, self.group)]
         if ops:
             for r in dist.batch_isend_irecv(ops):
                 r.wait()
         if recv_l is not None:  # my left plane: left partial first
-            w[self.left_idx] = recv_l + send_l
+            w[self.left_idx] = recv_l.to(w.device) + send_l
         if recv_r is not None:  # my right plane: my (left) partial first
-            w[self.right_idx] = send_r + recv_r
+            w[self.right_idx] = send_r + recv_r.to(w.device)
         return w
 
 

@@ -100,18 +100,22 @@ def test_oc_update_matches_host(n, vf, move):
 
 
 def test_device_and_host_glue_agree_on_desk_problem():
-    from paper_2604_18020_b200 import SimpConfig, default_schedule, make_preset, run_simp
+    """Same algorithm, different reduction orders.  A single-phase (p=3, beta=1)
+    schedule is not chaotic, so the two trajectories must agree tightly; the
+    late beta=16..32 continuation phases amplify 1e-12 differences into
+    neighbouring local optima (see test_gpu_solver.test_simp_desk_*)."""
+    from paper_2604_18020_b200 import SimpConfig, make_preset, run_simp
+    from paper_2604_18020_b200.simp import ContinuationSchedule, Phase
 
     pb = make_preset("cantilever", 0.2)
-    cfg = SimpConfig(schedule=default_schedule(30), precision="fp64")
+    sched = ContinuationSchedule((Phase(1, 30, p=3.0, beta=1.0, move=0.2, rmin_end=1.5),), 1.5)
+    cfg = SimpConfig(schedule=sched, precision="fp64")
     a = run_simp(pb, cfg, device_glue=True)
     b = run_simp(pb, cfg, device_glue=False)
     ca = np.array([h.compliance for h in a.history])
     cb = np.array([h.compliance for h in b.history])
-    # same algorithm, different reduction orders: trajectories agree far
-    # inside the north-star SIMP bar (1e-3 after a fixed iteration count)
-    np.testing.assert_allclose(ca, cb, rtol=1e-4)
-    assert np.linalg.norm(a.rho_phys - b.rho_phys) <= 1e-4 * np.linalg.norm(b.rho_phys)
+    np.testing.assert_allclose(ca, cb, rtol=1e-7)
+    assert np.linalg.norm(a.rho_phys - b.rho_phys) <= 1e-7 * np.linalg.norm(b.rho_phys)
     assert [h.cg_iterations for h in a.history] == [h.cg_iterations for h in b.history] or \
         max(abs(x - y) for x, y in zip([h.cg_iterations for h in a.history],
                                        [h.cg_iterations for h in b.history])) <= 3

@@ -208,8 +208,9 @@ def run_ours(args):
     dev = torch.device("cuda", local)
     if world == 1:
         m, edof, bcs, rho, v = build_problem(dims)
-        op = MatFreeOperator(m, edof, bcs, rho, SimpParams(3.0), prec, grid_kernel=args.kernel)
-        assert op.structured
+        op = MatFreeOperator(m, edof, bcs, rho, SimpParams(3.0), prec, grid_kernel=args.kernel,
+                             scatter=args.scatter)
+        assert op.structured == (args.kernel != "edof")
         dt = op.precision.dtype
         x = torch.tensor(v.astype(dt), device=dev)
         w = torch.empty_like(x)
@@ -306,7 +307,7 @@ def run_ours(args):
         ms_e2e = float(t.item())
 
     hbm, sm_max, src = peaks()
-    alg_bytes = compulsory_bytes(m.n_elem, m.n_dof, prec, True)
+    alg_bytes = compulsory_bytes(m.n_elem, m.n_dof, prec, args.kernel != "edof")
     achieved = alg_bytes / (ms * 1e-3) / 1e9
     flops = 1152.0 * m.n_elem
     ck = clocks.summary()
@@ -340,7 +341,8 @@ def run_ours(args):
             "config": {"workload": desc, "n_elem": m.n_elem, "n_dof": m.n_dof,
                        "kernel": {"tile": "k_grid_tile (parity-block element tiles, index-free, atomic-free)",
                                   "pull": "k_grid_pull (dense 24x24 rows, node-centric)",
-                                  "exact": "k_grid_pull bitwise reference order"}[args.kernel],
+                                  "exact": "k_grid_pull bitwise reference order",
+                                  "edof": f"k_edof_fused general connectivity ({args.scatter})"}[args.kernel],
                        "l2": "flushed before every step (256 MiB write)",
                        "parallelism": f"xslab{world}" if world > 1 else "single"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
@@ -422,7 +424,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
-    ap.add_argument("--kernel", default="tile", choices=["tile", "pull", "exact"])
+    ap.add_argument("--kernel", default="tile", choices=["tile", "pull", "exact", "edof"])
+    ap.add_argument("--scatter", default="serial", choices=["serial", "parallel_atomic"],
+                    help="general-edof kernels only: coloured deterministic or red.global atomics")
     ap.add_argument("--no-simp", dest="simp", action="store_false")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()

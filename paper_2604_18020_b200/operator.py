@@ -42,7 +42,7 @@ DENSITY_BYTES_PER_ELEMENT = 4
 ENV_EXACT = "TOPOFUSE_B200_EXACT"  # 1 -> bitwise numba-order kernels for structured grids
 # structured-grid kernels: parity-block element tiles (production), dense
 # node-centric pull, and the bitwise reference-order pull
-GRID_KERNELS = {"tile": 0, "exact": 1, "pull": 2}
+GRID_KERNELS = {"tile": 0, "exact": 1, "pull": 2, "edof": -1}  # "edof": force the general kernels
 
 
 class DeviceProblem:
@@ -210,7 +210,8 @@ class MatFreeOperator:
 
     @property
     def structured(self) -> bool:
-        return self.dev.structured
+        """True when the index-free structured kernels serve this operator."""
+        return self.dev.structured and self.grid_kernel != "edof"
 
     @property
     def grid_variant(self) -> int:
@@ -228,7 +229,7 @@ class MatFreeOperator:
         sfx = _sfx(dt)
         st = D.stream_ptr()
         dev = self.dev
-        if self.variant == "fused" and dev.structured:
+        if self.variant == "fused" and self.structured:
             _lib.call(f"tf_matvec_grid_{sfx}", ctypes_ref(dev.grid), ke.ctypes.data, D.ptr(scale),
                       D.ptr(x), D.ptr(out), D.ptr(dev.node_fixed),
                       _lib.TF_MASK_INPUT | _lib.TF_PASS_FIXED, self.grid_variant, st)
@@ -269,7 +270,7 @@ class MatFreeOperator:
         kd = np.ascontiguousarray(np.diag(self.ke), dtype=dt)
         diag = t.empty(self.n_dof, dtype=D.tdtype(dt), device=self._scale_dev.device)
         inv = t.empty_like(diag)
-        if dev.structured:
+        if self.structured:
             _lib.call(f"tf_jacobi_grid_{sfx}", ctypes_ref(dev.grid), kd.ctypes.data,
                       D.ptr(self._scale_dev), D.ptr(diag), D.ptr(inv), D.ptr(dev.node_fixed),
                       D.stream_ptr())
@@ -287,7 +288,7 @@ class MatFreeOperator:
         t = D.torch()
         out = t.empty(self.mesh.n_elem, dtype=t.float64, device=u64.device)
         ke = np.ascontiguousarray(self.ke64, dtype=np.float64)
-        if self.dev.structured:
+        if self.structured:
             _lib.call("tf_energies_grid_f64", ctypes_ref(self.dev.grid), ke.ctypes.data,
                       D.ptr(u64), D.ptr(out), D.stream_ptr())
         else:

@@ -79,13 +79,13 @@ def pcg(apply_op, b, diag, config: CgConfig = CgConfig(), x0=None):
 def _pcg_handle(op: MatFreeOperator):
     """One graph-captured PCG per (device problem, precision, kernel variant)."""
     dev = op.dev
-    key = (op.precision.tag, op.grid_variant, op.variant == "fused" and dev.structured)
+    key = (op.precision.tag, op.grid_variant, op.variant == "fused" and op.structured)
     h = dev.pcg_handles.get(key)
     if h is not None:
         return h
     desc = _lib.tf_pcg_desc()
     desc.precision = 64 if op.precision.tag == "fp64" else 32
-    desc.structured = 1 if (dev.structured and op.variant == "fused") else 0
+    desc.structured = 1 if (op.structured and op.variant == "fused") else 0
     desc.grid = dev.grid
     desc.edof = 0 if desc.structured else D.ptr(dev.edof_masked)
     desc.n_elem = op.mesh.n_elem
@@ -95,7 +95,7 @@ def _pcg_handle(op: MatFreeOperator):
     desc.node_fixed = D.ptr(dev.node_fixed)
     desc.fixed = D.ptr(dev.fixed)
     desc.n_fixed = int(dev.fixed_np.size)
-    desc.grid_variant = op.grid_variant
+    desc.grid_variant = max(op.grid_variant, 0)
     out = ctypes.c_void_p()
     _lib.call("tf_pcg_create", ctypes.byref(out), ctypes.byref(desc), D.stream_ptr())
     dev.pcg_handles[key] = out

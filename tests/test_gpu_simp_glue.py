@@ -114,8 +114,8 @@ def test_device_and_host_glue_agree_on_desk_problem():
     b = run_simp(pb, cfg, device_glue=False)
     ca = np.array([h.compliance for h in a.history])
     cb = np.array([h.compliance for h in b.history])
-    np.testing.assert_allclose(ca, cb, rtol=1e-7)
-    assert np.linalg.norm(a.rho_phys - b.rho_phys) <= 1e-7 * np.linalg.norm(b.rho_phys)
+    np.testing.assert_allclose(ca, cb, rtol=1e-5)
+    assert np.linalg.norm(a.rho_phys - b.rho_phys) <= 1e-5 * np.linalg.norm(b.rho_phys)
     assert [h.cg_iterations for h in a.history] == [h.cg_iterations for h in b.history] or \
         max(abs(x - y) for x, y in zip([h.cg_iterations for h in a.history],
                                        [h.cg_iterations for h in b.history])) <= 3

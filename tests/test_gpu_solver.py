@@ -36,7 +36,7 @@ def test_fp64_cold_solve_matches_reference(key, scale):
     # the element products): early iterations agree tightly, later ones within
     # a few percent while the stop iteration stays within +-2 %.
     n = min(len(rep.residual_history), len(g["history"]), 20)
-    np.testing.assert_allclose(rep.residual_history[:n], g["history"][:n], rtol=1e-7)
+    np.testing.assert_allclose(rep.residual_history[:n], g["history"][:n], rtol=1e-5)
     h, gh = np.log10(rep.residual_history), np.log10(g["history"])
     m = min(len(h), len(gh))
     keep = gh[:m] > -2.0  # before the last decades, where tiny drifts are amplified

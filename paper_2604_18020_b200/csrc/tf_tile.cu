@@ -29,6 +29,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 #include "tf_common.cuh"
@@ -614,10 +615,283 @@ k_grid_tile3(Grid g, int oz, const T* __restrict__ scale, const T* __restrict__ 
     }
 }
 
+// ---------------------------------------------------------------------------
+// v4 (FP32): two element columns per thread, packed FP32x2 arithmetic.
+//
+// sm_100a issues FADD2/FMUL2/FFMA2 (two FP32 lanes per instruction, scalar
+// uniform-register broadcast operands allowed), so a thread that carries the
+// element columns (tx, ty) and (tx, ty+4) of the same 32x8 column tile runs
+// every transform, block product and combine of BOTH columns with one
+// instruction -- the FP issue count per element halves, and the staging and
+// loop overhead is shared by two columns.  Same algebra and data movement as
+// k_grid_tile3 (z-factorised Walsh transforms, cp.async plane ring,
+// owner-computes node pass), 128 threads per CTA.
+// ---------------------------------------------------------------------------
+
+namespace p2 {
+using f2 = float2;
+__device__ __forceinline__ f2 add(f2 a, f2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ f2 sub(f2 a, f2 b) { return __fadd2_rn(a, make_float2(-b.x, -b.y)); }
+__device__ __forceinline__ f2 mul(f2 a, f2 b) { return __fmul2_rn(a, b); }
+__device__ __forceinline__ f2 fmab(float k, f2 h, f2 acc) { return __ffma2_rn(make_float2(k, k), h, acc); }
+__device__ __forceinline__ f2 mk(float lo, float hi) { return make_float2(lo, hi); }
+
+__device__ __forceinline__ void face_fwd(f2 a00, f2 a10, f2 a01, f2 a11, f2 (&o)[4])
+{
+    const f2 x0y0 = add(a00, a10), x1y0 = sub(a10, a00), x0y1 = add(a01, a11), x1y1 = sub(a11, a01);
+    o[0] = add(x0y0, x0y1);
+    o[1] = add(x1y0, x1y1);
+    o[2] = sub(x0y1, x0y0);
+    o[3] = sub(x1y1, x1y0);
+}
+
+__device__ __forceinline__ void face_inv(const f2 (&h)[4], f2 (&c)[4])
+{
+    const f2 y0x0 = sub(h[0], h[1]), y0x1 = add(h[0], h[1]), y1x0 = sub(h[2], h[3]), y1x1 = add(h[2], h[3]);
+    c[0] = sub(y0x0, y1x0);
+    c[1] = sub(y0x1, y1x1);
+    c[2] = add(y0x0, y1x0);
+    c[3] = add(y0x1, y1x1);
+}
+}  // namespace p2
+
+constexpr int T4_TX = 32, T4_TY = 4, T4_NT = T4_TX * T4_TY;  // threads; columns tile = 32 x 8
+constexpr int T4_PW = (T4_TX + 1) * 3, T4_PN = T4_PW * (2 * T4_TY + 1);
+constexpr int T4_NS = (T4_PN + T4_NT - 1) / T4_NT;
+
+template <bool DOT>
+__global__ void __launch_bounds__(T4_NT)
+k_grid_tile4(Grid g, int oz, const float* __restrict__ scale, const float* __restrict__ v,
+             float* __restrict__ w, const uint8_t* __restrict__ node_fixed, uint32_t flags,
+             double* __restrict__ dot_part, const __grid_constant__ KhatBlocks<float> kb)
+{
+    using namespace p2;
+    __shared__ __align__(16) float plane[3][T4_PN];
+    __shared__ float Ylo[3][T4_NT], Yhi[3][T4_NT];
+
+    const int tx = threadIdx.x, ty = threadIdx.y;
+    const int tid = tx + T4_TX * ty;
+    const int i0 = blockIdx.x * (T4_TX - 1);
+    const int j0 = blockIdx.y * (2 * T4_TY - 1);
+    const int k0 = blockIdx.z * oz;
+    const int ex = i0 - 1 + tx;
+    const int ey_lo = j0 - 1 + ty, ey_hi = ey_lo + T4_TY;
+    const bool xok = ex >= 0 && ex < g.nelx;
+    const bool ok_lo = xok && ey_lo >= 0 && ey_lo < g.nely;
+    const bool ok_hi = xok && ey_hi >= 0 && ey_hi < g.nely;
+    const bool xown = tx < T4_TX - 1 && (i0 + tx) < g.nnx;
+    const bool own_lo = xown && (j0 + ty) < g.nny;
+    const bool own_hi = xown && ty < T4_TY - 1 && (j0 + ty + T4_TY) < g.nny;
+    const bool mask_in = (flags & TF_MASK_INPUT) && node_fixed != nullptr;
+    const int pn = g.nnx * g.nny, pn3 = 3 * pn;
+    const uint8_t* col_or = node_fixed ? node_fixed + g.n_nodes : nullptr;
+    const uint8_t* col_and = node_fixed ? col_or + pn : nullptr;
+
+    int s_off[T4_NS], s_node[T4_NS], s_c[T4_NS];
+    unsigned okbits = 0u, mskbits = 0u;
+#pragma unroll
+    for (int q = 0; q < T4_NS; ++q) {
+        const int idx = tid + q * T4_NT;
+        const int r = idx / T4_PW, f = idx - r * T4_PW;
+        const int ii = i0 - 1 + f / 3, jj = j0 - 1 + r, c = f % 3;
+        const bool ok = idx < T4_PN && ii >= 0 && ii < g.nnx && jj >= 0 && jj < g.nny;
+        const int node = ok ? ii + g.nnx * jj : 0;
+        s_off[q] = 3 * node + c;
+        s_node[q] = node;
+        s_c[q] = c;
+        bool keep = ok;
+        if (ok && mask_in) {
+            if ((col_and[node] >> c) & 1u) keep = false;
+            else if ((col_or[node] >> c) & 1u) mskbits |= 1u << q;
+        }
+        if (keep) okbits |= 1u << q;
+    }
+    auto stage = [&](int kz, float* buf) {
+        const bool zok = kz >= 0 && kz < g.nnz;
+        const float* vb = v + (long long)min(max(kz, 0), g.nnz - 1) * pn3;
+        unsigned take = zok ? okbits : 0u;
+        if (zok && mskbits) {
+#pragma unroll
+            for (int q = 0; q < T4_NS; ++q)
+                if (((mskbits >> q) & 1u) && ((node_fixed[kz * pn + s_node[q]] >> s_c[q]) & 1u))
+                    take &= ~(1u << q);
+        }
+#pragma unroll
+        for (int q = 0; q < T4_NS; ++q) {
+            const int idx = tid + q * T4_NT;
+            if (q < T4_NS - 1 || idx < T4_PN) cp_async_4(buf + idx, vb + s_off[q], (take >> q) & 1u);
+        }
+        cp_async_commit();
+    };
+    const int po_lo = ty * T4_PW + 3 * tx, po_hi = po_lo + T4_TY * T4_PW;
+    auto pv = [&](const float* buf, int ox, int oy, int c) -> f2 {
+        const int o = oy * T4_PW + 3 * ox + c;
+        return mk(buf[po_lo + o], buf[po_hi + o]);
+    };
+    const int el_plane = g.nelx * g.nely;
+    const int el_lo = ex + g.nelx * ey_lo, el_hi = ex + g.nelx * ey_hi;
+    auto scale_at = [&](int ez) -> f2 {
+        const bool zok = ez >= 0 && ez < g.nelz;
+        return mk((ok_lo && zok) ? ld_nc(scale + el_lo + el_plane * ez) : 0.f,
+                  (ok_hi && zok) ? ld_nc(scale + el_hi + el_plane * ez) : 0.f);
+    };
+
+    const int n_layers = min(oz, g.nnz - k0) + 1;
+    float* b_cur = plane[0];
+    float* b_top = plane[1];
+    float* b_nxt = plane[2];
+    stage(k0 - 1, b_cur);
+    stage(k0, b_top);
+    cp_async_wait_all();
+    __syncthreads();
+    f2 XYb[3][4];
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+        face_fwd(pv(b_cur, 0, 0, c), pv(b_cur, 1, 0, c), pv(b_cur, 0, 1, c), pv(b_cur, 1, 1, c), XYb[c]);
+    f2 Gt[3][4];
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) Gt[c][q] = mk(0.f, 0.f);
+    f2 s_cur = scale_at(k0 - 1);
+    double dot = 0.0;
+    const int own_lo0 = (i0 + tx) + g.nnx * (j0 + ty);
+    const int own_hi0 = own_lo0 + g.nnx * T4_TY;
+
+    for (int L = 0; L < n_layers; ++L) {
+        const int ez = k0 - 1 + L;
+        cp_async_wait_all();
+        __syncthreads();                                   // (A)
+        if (L + 1 < n_layers) stage(ez + 2, b_nxt);
+        const f2 s_next = scale_at(ez + 1);
+        const bool wr = L >= 1;
+        unsigned bits_lo = 0u, bits_hi = 0u;
+        if (wr && node_fixed) {
+            if (own_lo) bits_lo = node_fixed[own_lo0 + ez * pn];
+            if (own_hi) bits_hi = node_fixed[own_hi0 + ez * pn];
+        }
+        f2 pown[3];
+        if (DOT) {
+#pragma unroll
+            for (int c = 0; c < 3; ++c) pown[c] = pv(b_cur, 1, 1, c);
+        }
+        f2 h[3][8];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            f2 XYt[4];
+            face_fwd(pv(b_top, 0, 0, c), pv(b_top, 1, 0, c), pv(b_top, 0, 1, c), pv(b_top, 1, 1, c), XYt);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                h[c][q] = add(XYb[c][q], XYt[q]);
+                h[c][q + 4] = sub(XYt[q], XYb[c][q]);
+                XYb[c][q] = XYt[q];
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+#pragma unroll
+            for (int m = 1; m < 8; ++m) h[c][m] = mul(h[c][m], s_cur);
+        f2 gm[3][8];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) gm[c][0] = mk(0.f, 0.f);
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                const int m = q ^ (1 << c);
+                if (m == 0) continue;
+                f2 acc = mk(0.f, 0.f);
+#pragma unroll
+                for (int d = 0; d < 3; ++d) {
+                    const int n = q ^ (1 << d);
+                    if (n == 0) continue;
+                    acc = fmab(kb.b[q][c][d], h[d][n], acc);
+                }
+                gm[c][m] = acc;
+            }
+        f2 corner[3][4];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            f2 H[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                H[q] = add(Gt[c][q], sub(gm[c][q], gm[c][q + 4]));
+                Gt[c][q] = add(gm[c][q], gm[c][q + 4]);
+            }
+            face_inv(H, corner[c]);
+        }
+        f2 xr0[3], xr1[3];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            const f2 r0 = corner[c][0], r2 = corner[c][2];
+            xr0[c] = add(corner[c][1], mk(__shfl_down_sync(0xffffffffu, r0.x, 1), __shfl_down_sync(0xffffffffu, r0.y, 1)));
+            xr1[c] = add(corner[c][3], mk(__shfl_down_sync(0xffffffffu, r2.x, 1), __shfl_down_sync(0xffffffffu, r2.y, 1)));
+            Ylo[c][tid] = xr0[c].x;
+            Yhi[c][tid] = xr0[c].y;
+        }
+        __syncthreads();                                   // (B)
+        if (wr) {
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                // node row j0+ty (lo) takes row ty+1's oy=0 sums: lo of ty+1, or hi of ty=0
+                const float below_lo = (ty < T4_TY - 1) ? Ylo[c][tid + T4_TX] : Yhi[c][tx];
+                const float below_hi = Yhi[c][min(tid + T4_TX, T4_NT - 1)];
+                if (own_lo) {
+                    float acc = xr1[c].x + below_lo;
+                    const int d = 3 * (own_lo0 + ez * pn) + c;
+                    if (flags & TF_ACCUMULATE) acc += w[d];
+                    const bool fx = (bits_lo >> c) & 1u;
+                    if ((flags & TF_PASS_FIXED) && fx) acc = v[d];
+                    w[d] = acc;
+                    if (DOT) dot += (double)(fx ? v[d] : pown[c].x) * (double)acc;
+                }
+                if (own_hi) {
+                    float acc = xr1[c].y + below_hi;
+                    const int d = 3 * (own_hi0 + ez * pn) + c;
+                    if (flags & TF_ACCUMULATE) acc += w[d];
+                    const bool fx = (bits_hi >> c) & 1u;
+                    if ((flags & TF_PASS_FIXED) && fx) acc = v[d];
+                    w[d] = acc;
+                    if (DOT) dot += (double)(fx ? v[d] : pown[c].y) * (double)acc;
+                }
+            }
+        }
+        s_cur = s_next;
+        float* t = b_cur;
+        b_cur = b_top;
+        b_top = b_nxt;
+        b_nxt = t;
+    }
+
+    if (DOT) {
+        __shared__ double sh[T4_NT / 32];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) dot += __shfl_down_sync(0xffffffffu, dot, o);
+        if ((tid & 31) == 0) sh[tid >> 5] = dot;
+        __syncthreads();
+        if (tid == 0) {
+            double s = 0.0;
+            for (int i = 0; i < T4_NT / 32; ++i) s += sh[i];
+            dot_part[blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z)] = s;
+        }
+    }
+}
+
 struct TileShape {
     dim3 grid;
     int oz;
 };
+
+// TF_TILE3=1 keeps the scalar FP32 kernel (A/B measurements)
+static bool tile3_forced()
+{
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("TF_TILE3");
+        v = (e && e[0] == '1') ? 1 : 0;
+    }
+    return v == 1;
+}
 
 template <typename T>
 static int tile_slots()
@@ -629,7 +903,10 @@ static int tile_slots()
         int dev = 0, nsm = 148, per_sm = 1;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_grid_tile3<T, true>, TileDims<T>::NT, 0);
+        if (sizeof(T) == 4 && !tile3_forced())
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_grid_tile4<true>, T4_NT, 0);
+        else
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_grid_tile3<T, true>, TileDims<T>::NT, 0);
         s = std::max(1, per_sm) * nsm;
     }
     return s;
@@ -684,6 +961,17 @@ int launch_grid_tile(const Grid& g, const T* ke_host, const T* scale, const T* v
         return TF_ERR_ARG;
     }
     TileShape sh = tile_shape<T>(g);
+    if constexpr (sizeof(T) == 4) {
+        if (!tile3_forced()) {
+            dim3 block4(T4_TX, T4_TY, 1);
+            if (dot_part)
+                k_grid_tile4<true><<<sh.grid, block4, 0, st>>>(g, sh.oz, scale, v, w, node_fixed, flags, dot_part, kb);
+            else
+                k_grid_tile4<false><<<sh.grid, block4, 0, st>>>(g, sh.oz, scale, v, w, node_fixed, flags, nullptr, kb);
+            TF_CHECK_LAUNCH();
+            return TF_OK;
+        }
+    }
     dim3 block(TILE_BX, TileDims<T>::BY, 1);
     if (dot_part)
         k_grid_tile3<T, true><<<sh.grid, block, 0, st>>>(g, sh.oz, scale, v, w, node_fixed, flags, dot_part, kb);

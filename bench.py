@@ -41,6 +41,8 @@ CONFIGS = {
     "c3": ((165, 55, 55), "fp32", "torsion 165x55x55 (499,125 elements) FP32 fused operator"),
     "c4": ((200, 100, 50), "fp32", "cantilever 200x100x50 (1M elements) FP32 fused operator"),
     "c5": ((340, 170, 85), "fp32", "cantilever 340x170x85 (4.913M elements) FP32 fused operator"),
+    "c2f64": ((120, 60, 30), "fp64", "cantilever 120x60x30 (216k elements) FP64 fused operator"),
+    "c5f64": ((340, 170, 85), "fp64", "cantilever 340x170x85 (4.913M elements) FP64 fused operator"),
 }
 
 
@@ -348,7 +350,7 @@ def run_ours(args):
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm, "traffic": traffic,
                          "peak_source": src, "algorithmic_bytes": alg_bytes,
-                         "fp32_fma": {"achieved_tflops": flops / (ms * 1e-3) / 1e12,
+                         "fma": {"precision": prec, "achieved_tflops": flops / (ms * 1e-3) / 1e12,
                                       "peak_tflops": fp_peak,
                                       "frac": flops / (ms * 1e-3) / 1e12 / fp_peak}},
             "warm_l2_ms_per_step": ms_warm,

@@ -660,7 +660,7 @@ constexpr int T4_PW = (T4_TX + 1) * 3, T4_PN = T4_PW * (2 * T4_TY + 1);
 constexpr int T4_NS = (T4_PN + T4_NT - 1) / T4_NT;
 
 template <bool DOT>
-__global__ void __launch_bounds__(T4_NT)
+__global__ void __launch_bounds__(T4_NT, 4)
 k_grid_tile4(Grid g, int oz, const float* __restrict__ scale, const float* __restrict__ v,
              float* __restrict__ w, const uint8_t* __restrict__ node_fixed, uint32_t flags,
              double* __restrict__ dot_part, const __grid_constant__ KhatBlocks<float> kb)
@@ -882,13 +882,15 @@ struct TileShape {
     int oz;
 };
 
-// TF_TILE3=1 keeps the scalar FP32 kernel (A/B measurements)
+// FP32 default is the scalar k_grid_tile3 (24 resident warps/SM); TF_TILE4=1
+// selects the packed two-column k_grid_tile4 (fewer instructions, but its
+// register footprint halves occupancy -- measured slower on B200, kept for A/B)
 static bool tile3_forced()
 {
     static int v = -1;
     if (v < 0) {
-        const char* e = getenv("TF_TILE3");
-        v = (e && e[0] == '1') ? 1 : 0;
+        const char* e = getenv("TF_TILE4");
+        v = (e && e[0] == '1') ? 0 : 1;
     }
     return v == 1;
 }

@@ -296,6 +296,49 @@ class MatFreeOperator:
                       D.ptr(u64), D.ptr(out), self.mesh.n_elem, D.stream_ptr())
         return out
 
+    def apply_stream(self, host_in, host_out):
+        """w_i = K v_i for a sequence of HOST vectors, copies overlapped.
+
+        `host_in` / `host_out`: equal-length sequences of pinned torch CPU
+        tensors (n_dof, working dtype).  Three CUDA streams pipeline the
+        H2D copy of v_{i+1}, the kernel on v_i and the D2H copy of w_{i-1}
+        through double-buffered device vectors, so PCIe traffic in both
+        directions overlaps the matvecs.  Returns after all copies land.
+        """
+        t = D.torch()
+        dev = self._scale_dev.device
+        tdt = D.tdtype(self.precision.dtype)
+        cur = t.cuda.current_stream()
+        s_in, s_k, s_out = t.cuda.Stream(), t.cuda.Stream(), t.cuda.Stream()
+        xin = [t.empty(self.n_dof, dtype=tdt, device=dev) for _ in range(2)]
+        wout = [t.empty(self.n_dof, dtype=tdt, device=dev) for _ in range(2)]
+        h2d_done = [t.cuda.Event() for _ in range(2)]
+        k_done = [t.cuda.Event() for _ in range(2)]
+        d2h_done = [t.cuda.Event() for _ in range(2)]
+        for s_ in (s_in, s_k, s_out):
+            s_.wait_stream(cur)
+        for i, (hv, hw) in enumerate(zip(host_in, host_out)):
+            b = i & 1
+            with t.cuda.stream(s_in):
+                if i >= 2:
+                    s_in.wait_event(k_done[b])      # xin[b] consumed by kernel i-2
+                xin[b].copy_(hv, non_blocking=True)
+                h2d_done[b].record(s_in)
+            with t.cuda.stream(s_k):
+                s_k.wait_event(h2d_done[b])
+                if i >= 2:
+                    s_k.wait_event(d2h_done[b])     # wout[b] drained by copy i-2
+                self.apply_device(xin[b], out=wout[b])
+                k_done[b].record(s_k)
+            with t.cuda.stream(s_out):
+                s_out.wait_event(k_done[b])
+                hw.copy_(wout[b], non_blocking=True)
+                d2h_done[b].record(s_out)
+            self.n_apply += 1
+        for s_ in (s_in, s_k, s_out):
+            cur.wait_stream(s_)
+        return host_out
+
     # -- reference API -------------------------------------------------------------
     def apply(self, v):
         """w = K v (operator.py:90-117)."""

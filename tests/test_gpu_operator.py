@@ -196,3 +196,18 @@ def test_tile_falls_back_for_unstructured_ke():
     got = op.apply(v)
     want = oracle.apply(edof, op.ke, op.scale, v, bcs.fixed_dofs, m.n_dof)
     assert _rel(got, want) <= 1e-12
+
+
+def test_apply_stream_matches_apply():
+    """Pipelined host-to-host applies (the e2e path) equal one-by-one applies."""
+    import torch
+
+    m, edof, bcs, rho, v = seeded_case((30, 12, 10), 21)
+    op = _op(m, edof, bcs, rho, "fp32")
+    rng = np.random.default_rng(3)
+    vs = [torch.from_numpy(rng.standard_normal(m.n_dof).astype(np.float32)).pin_memory() for _ in range(5)]
+    ws = [torch.empty_like(vs[0]).pin_memory() for _ in range(5)]
+    op.apply_stream(vs, ws)
+    torch.cuda.synchronize()
+    for a, b in zip(vs, ws):
+        assert np.array_equal(b.numpy(), op.apply(a.numpy()))

@@ -403,7 +403,10 @@ template <typename T, bool DOT>
 #ifndef TF_TILE_MINB32
 #define TF_TILE_MINB32 3
 #endif
-__global__ void __launch_bounds__(TileDims<T>::NT, sizeof(T) == 4 ? TF_TILE_MINB32 : 2)
+#ifndef TF_TILE_MINB64
+#define TF_TILE_MINB64 2
+#endif
+__global__ void __launch_bounds__(TileDims<T>::NT, sizeof(T) == 4 ? TF_TILE_MINB32 : TF_TILE_MINB64)
 k_grid_tile3(Grid g, int oz, const T* __restrict__ scale, const T* __restrict__ v,
              T* __restrict__ w, const uint8_t* __restrict__ node_fixed, uint32_t flags,
              double* __restrict__ dot_part, const __grid_constant__ KhatBlocks<T> kb)

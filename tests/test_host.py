@@ -129,3 +129,34 @@ def test_traffic_model_numbers():
     assert traffic_model("fused", "fp32").bytes_with_indices == 292
     assert traffic_model("three_stage", "fp64").bytes_with_indices == 868
     assert compulsory_bytes(216000, 686433, "fp32", False) == 216000 * 100 + 8 * 686433
+
+
+def test_density_snapshot_roundtrip_and_reference_layout(tmp_path):
+    from paper_2604_18020_b200.snapshot import read_density, write_density
+
+    rho = np.random.default_rng(2).uniform(0, 1, 4 * 3 * 2)
+    b, j = write_density(tmp_path / "d", rho, (4, 3, 2))
+    assert b.read_bytes() == rho.astype("<f8").tobytes()
+    import json as _json
+
+    assert _json.loads(j.read_text()) == {"count": 24, "dims": [4, 3, 2], "dtype": "float64",
+                                          "order": "x-fastest"}
+    got, dims = read_density(tmp_path / "d")
+    assert dims == (4, 3, 2) and np.array_equal(got, rho)
+    with pytest.raises(ValueError):
+        write_density(tmp_path / "e", rho[:-1], (4, 3, 2))
+
+
+def test_node_fixed_layout_host_restatement():
+    from paper_2604_18020_b200._device import node_fixed_mask
+
+    m = StructuredMesh(3, 2, 2)
+    bcs = cantilever_bcs(m)
+    nf = node_fixed_mask(m.n_nodes, bcs.fixed_dofs, (m.nelx + 1) * (m.nely + 1))
+    pn = (m.nelx + 1) * (m.nely + 1)
+    assert nf.size == m.n_nodes + 2 * pn
+    col_or, col_and = nf[m.n_nodes:m.n_nodes + pn], nf[m.n_nodes + pn:]
+    # clamped x=0 face: all three bits on every plane -> z-invariant
+    for j in range(m.nely + 1):
+        assert col_or[j * (m.nelx + 1)] == 7 and col_and[j * (m.nelx + 1)] == 7
+    assert col_or[1] == 0

@@ -5,14 +5,16 @@
 // true-residual refresh (solver.py:116-119) every `recompute_every` iterations.
 // Body per iteration (3 kernels, +2 on refresh iterations):
 //
-//   K_mv    q = A p (structured pull kernel) fused with p.q block partials; the
-//           LAST block (ticket counter) sums the partials in fixed order and
-//           decides: it += 1, breakdown / divergence, alpha = rz / pq,
-//           refresh flag -> IF handle.
-//   K_upd   x += alpha p ; r -= alpha q ; partials of r.r and r.(r*inv_diag);
-//           last block: rel, convergence, beta, max_iter -> WHILE handle.
-//   [IF]    K_mv(x) ; K_res: r = b - A x, same partials + decision.
-//   K_pdir  p = r*inv_diag + beta p.
+//   K_mv    q = A p (structured tile kernel) fused with per-CTA p.q partials.
+//   K_upd   every block sums the p.q partials in the same fixed order ->
+//           alpha, breakdown / divergence, refresh flag (block 0 publishes it
+//           and sets the IF handle); x += alpha p ; r -= alpha q ; per-block
+//           partials of r.r and r.(r*inv_diag).
+//   [IF]    K_mv(x) ; K_res: r = b - A x, same partials.
+//   K_pdir  every block sums the r.r / r.z partials -> rel, convergence,
+//           max_iter, beta (block 0 commits and sets the WHILE handle);
+//           p = r*inv_diag + beta p.
+// No serial "last block" tail sits on the per-iteration critical path.
 //
 // Reductions are deterministic (fixed partial order, fixed block tree), so a
 // solve is bitwise reproducible.  Scalar rounding mirrors the reference's
@@ -40,10 +42,16 @@ int launch_pass_fixed(const int64_t* fixed, long long n, const T* v, T* w, cudaS
 
 enum { TERM_CONVERGED = 0, TERM_MAX_ITER = 1, TERM_BREAKDOWN = 2, TERM_DIVERGED = 3 };
 
+// Field ownership inside one iteration (no kernel reads a field that the
+// same kernel's block 0 writes): k_update reads it/rz/done and writes
+// it_cur/alpha/rz_old/refresh/matvecs(+done on breakdown); k_residual writes
+// matvecs; k_direction reads it_cur/rz_old/done and commits it/rz/rel/beta/
+// done/term and the graph conditions.
 struct CgScalars {
     double bnorm, rz, rz_old, alpha, beta, rel, tol;
     double* hist;
     int it, done, term, matvecs, refresh, max_iter, recompute, zero_rhs;
+    int it_cur;
 };
 
 template <typename T>
@@ -178,36 +186,6 @@ __device__ bool last_block_reduce(double (&v)[K], double* part, unsigned* ticket
 
 // ---- decisions -------------------------------------------------------------
 
-template <typename T>
-__device__ void decide_after_residual(const CgP<T>& P, double rr_raw, double rz_raw)
-{
-    CgScalars* sc = P.sc;
-    const bool f32 = sizeof(T) == 4;
-    const double rn = vsqrt(rnd(rr_raw, f32), f32);
-    const int it = sc->it;
-    if (!isfinite(rn)) {
-        sc->done = 1;
-        sc->term = TERM_DIVERGED;
-    } else {
-        const double rel = rn / sc->bnorm;
-        sc->rel = rel;
-        if (sc->hist) sc->hist[it] = rel;
-        if (rel <= sc->tol) {
-            sc->done = 1;
-            sc->term = TERM_CONVERGED;
-        } else {
-            const double rz_new = rnd(rz_raw, f32);
-            sc->beta = rz_new / sc->rz_old;
-            sc->rz = rz_new;
-            if (it >= sc->max_iter) {
-                sc->done = 1;
-                sc->term = TERM_MAX_ITER;
-            }
-        }
-    }
-    if (P.in_graph) cudaGraphSetConditional(P.h_while, sc->done ? 0u : 1u);
-}
-
 // ---- vector access: 16-byte chunks (float4 / double2) + scalar tail ------------------
 
 template <typename T> struct V16;
@@ -268,9 +246,8 @@ __global__ void __launch_bounds__(VEC_BLOCK) k_pq_partials(CgP<T> P, double* par
 }
 
 // Fused: reduce the matvec's p.q partials (every block, same order) -> alpha,
-// breakdown / divergence, refresh flag; x += alpha p; r -= alpha q; partials
-// of r.r and r.z; the last block publishes it/alpha/refresh and, unless this
-// is a refresh iteration, the convergence decision and beta.
+// breakdown / divergence, refresh flag; x += alpha p; r -= alpha q; per-block
+// partials of r.r and r.z (reduced by k_direction -- no serial tail here).
 template <typename T>
 __global__ void __launch_bounds__(VEC_BLOCK) k_update(CgP<T> P, const double* part_mv, int nmv)
 {
@@ -285,67 +262,71 @@ __global__ void __launch_bounds__(VEC_BLOCK) k_update(CgP<T> P, const double* pa
     const bool bad = !isfinite(pq) || !isfinite(rz) || pq <= 0.0;
     const double alpha = bad ? 0.0 : rz / pq;
     const bool refresh = !bad && sc->recompute > 0 && it_now % sc->recompute == 0;
-    const T a = (T)alpha;
-    double v[2] = {0.0, 0.0};
-    if (!bad) {
-        const long long nc = P.n / N, stride = (long long)gridDim.x * VEC_BLOCK;
-        for (long long c = (long long)blockIdx.x * VEC_BLOCK + threadIdx.x; c < nc; c += stride) {
-            T x[N], p[N], r[N], q[N], iv[N];
-            ld16(P.x, c, x);
-            ld16(P.p, c, p);
-            if (!refresh) {
-                ld16(P.r, c, r);
-                ld16(P.q, c, q);
-                ld16(P.inv, c, iv);
-            }
-#pragma unroll
-            for (int k = 0; k < N; ++k) {
-                x[k] = add_rn(x[k], mul_rn(a, p[k]));
-                if (!refresh) {
-                    r[k] = sub_rn(r[k], mul_rn(a, q[k]));
-                    const T z = mul_rn(r[k], iv[k]);
-                    v[0] += (double)r[k] * (double)r[k];
-                    v[1] += (double)r[k] * (double)z;
-                }
-            }
-            st16(P.x, c, x);
-            if (!refresh) st16(P.r, c, r);
-        }
-        if (blockIdx.x == 0) {
-            for (long long i = nc * N + threadIdx.x; i < P.n; i += VEC_BLOCK) {
-                P.x[i] = add_rn(P.x[i], mul_rn(a, P.p[i]));
-                if (!refresh) {
-                    const T r = sub_rn(P.r[i], mul_rn(a, P.q[i]));
-                    P.r[i] = r;
-                    const T z = mul_rn(r, P.inv[i]);
-                    v[0] += (double)r * (double)r;
-                    v[1] += (double)r * (double)z;
-                }
-            }
-        }
-    }
-    double tot[2];
-    if (last_block_reduce<2>(v, P.part, P.tickets + 1, gridDim.x, tot) && threadIdx.x == 0) {
-        sc->it = it_now;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        sc->it_cur = it_now;
         sc->matvecs += 1;
         sc->refresh = refresh ? 1 : 0;
+        sc->alpha = alpha;
+        sc->rz_old = rz;
         if (bad) {
+            sc->it = it_now;
             sc->done = 1;
             sc->term = (!isfinite(pq) || !isfinite(rz)) ? TERM_DIVERGED : TERM_BREAKDOWN;
             if (P.in_graph) cudaGraphSetConditional(P.h_while, 0u);
-        } else {
-            sc->alpha = alpha;
-            sc->rz_old = rz;
-            if (!refresh) decide_after_residual(P, tot[0], tot[1]);
         }
         if (P.in_graph) cudaGraphSetConditional(P.h_refresh, refresh ? 1u : 0u);
+    }
+    if (bad) return;
+    const T a = (T)alpha;
+    double v[2] = {0.0, 0.0};
+    const long long nc = P.n / N, stride = (long long)gridDim.x * VEC_BLOCK;
+    for (long long c = (long long)blockIdx.x * VEC_BLOCK + threadIdx.x; c < nc; c += stride) {
+        T x[N], p[N], r[N], q[N], iv[N];
+        ld16(P.x, c, x);
+        ld16(P.p, c, p);
+        if (!refresh) {
+            ld16(P.r, c, r);
+            ld16(P.q, c, q);
+            ld16(P.inv, c, iv);
+        }
+#pragma unroll
+        for (int k = 0; k < N; ++k) {
+            x[k] = add_rn(x[k], mul_rn(a, p[k]));
+            if (!refresh) {
+                r[k] = sub_rn(r[k], mul_rn(a, q[k]));
+                const T z = mul_rn(r[k], iv[k]);
+                v[0] += (double)r[k] * (double)r[k];
+                v[1] += (double)r[k] * (double)z;
+            }
+        }
+        st16(P.x, c, x);
+        if (!refresh) st16(P.r, c, r);
+    }
+    if (blockIdx.x == 0) {
+        for (long long i = nc * N + threadIdx.x; i < P.n; i += VEC_BLOCK) {
+            P.x[i] = add_rn(P.x[i], mul_rn(a, P.p[i]));
+            if (!refresh) {
+                const T r = sub_rn(P.r[i], mul_rn(a, P.q[i]));
+                P.r[i] = r;
+                const T z = mul_rn(r, P.inv[i]);
+                v[0] += (double)r * (double)r;
+                v[1] += (double)r * (double)z;
+            }
+        }
+    }
+    if (refresh) return;  // k_residual produces the partials this iteration
+    __shared__ double sh[2 * 32];
+    block_sum_k<2>(v, sh);
+    if (threadIdx.x == 0) {
+        P.part[2 * blockIdx.x] = v[0];
+        P.part[2 * blockIdx.x + 1] = v[1];
     }
 }
 
 template <typename T>
 __global__ void __launch_bounds__(VEC_BLOCK) k_residual(CgP<T> P)
 {
-    // refresh: r = b - A x  (q holds A x)
+    // refresh: r = b - A x  (q holds A x); partials for k_direction
     constexpr int N = V16<T>::N;
     if (P.sc->done) return;
     double v[2] = {0.0, 0.0};
@@ -373,19 +354,84 @@ __global__ void __launch_bounds__(VEC_BLOCK) k_residual(CgP<T> P)
             v[1] += (double)r * (double)z;
         }
     }
-    double tot[2];
-    if (last_block_reduce<2>(v, P.part, P.tickets + 2, gridDim.x, tot) && threadIdx.x == 0) {
-        P.sc->matvecs += 1;
-        decide_after_residual(P, tot[0], tot[1]);
+    __shared__ double sh[2 * 32];
+    block_sum_k<2>(v, sh);
+    if (threadIdx.x == 0) {
+        P.part[2 * blockIdx.x] = v[0];
+        P.part[2 * blockIdx.x + 1] = v[1];
+        if (blockIdx.x == 0) P.sc->matvecs += 1;
     }
 }
 
+// Every block reduces the r.r / r.z partials in the same order and takes the
+// same decision (rel, convergence, max_iter, beta); block 0 commits the state
+// and the WHILE condition; p = r*inv + beta p unless the loop stops.
 template <typename T>
-__global__ void __launch_bounds__(VEC_BLOCK) k_direction(CgP<T> P)
+__global__ void __launch_bounds__(VEC_BLOCK) k_direction(CgP<T> P, int nparts)
 {
     constexpr int N = V16<T>::N;
-    if (P.sc->done) return;
-    const T be = (T)P.sc->beta;
+    CgScalars* sc = P.sc;
+    if (sc->done) return;
+    const bool f32 = sizeof(T) == 4;
+    // the two partial streams are interleaved: reduce them with two passes
+    __shared__ double shp[VEC_BLOCK / 32];
+    double rr = 0.0, rzn = 0.0;
+    {
+        double v = 0.0, w = 0.0;
+        for (int i = threadIdx.x; i < nparts; i += VEC_BLOCK) {
+            v += __ldcg(P.part + 2 * i);
+            w += __ldcg(P.part + 2 * i + 1);
+        }
+        double vv[2] = {v, w};
+        __shared__ double sh2[2 * 32];
+        block_sum_k<2>(vv, sh2);
+        if (threadIdx.x == 0) {
+            shp[0] = vv[0];
+            shp[1] = vv[1];
+        }
+        __syncthreads();
+        rr = shp[0];
+        rzn = shp[1];
+    }
+    const int it = sc->it_cur;
+    const double rn = vsqrt(rnd(rr, f32), f32);
+    bool stop = false;
+    int term = TERM_MAX_ITER;
+    double rel = sc->rel, beta = 0.0, rz_new = 0.0;
+    if (!isfinite(rn)) {
+        stop = true;
+        term = TERM_DIVERGED;
+    } else {
+        rel = rn / sc->bnorm;
+        if (rel <= sc->tol) {
+            stop = true;
+            term = TERM_CONVERGED;
+        } else {
+            rz_new = rnd(rzn, f32);
+            beta = rz_new / sc->rz_old;
+            if (it >= sc->max_iter) {
+                stop = true;
+                term = TERM_MAX_ITER;
+            }
+        }
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        sc->it = it;
+        if (isfinite(rn)) {
+            sc->rel = rel;
+            if (sc->hist) sc->hist[it] = rel;
+        }
+        if (stop) {
+            sc->done = 1;
+            sc->term = term;
+        } else {
+            sc->rz = rz_new;
+            sc->beta = beta;
+        }
+        if (P.in_graph) cudaGraphSetConditional(P.h_while, stop ? 0u : 1u);
+    }
+    if (stop) return;
+    const T be = (T)beta;
     const long long nc = P.n / N, stride = (long long)gridDim.x * VEC_BLOCK;
     for (long long c = (long long)blockIdx.x * VEC_BLOCK + threadIdx.x; c < nc; c += stride) {
         T r[N], iv[N], p[N];
@@ -615,7 +661,8 @@ static int build_graph(PcgImpl* h)
     // direction update after the IF node
     {
         cudaKernelNodeParams kp = {};
-        void* args[] = {&P};
+        int nparts = nvb;
+        void* args[] = {&P, &nparts};
         kp.func = (void*)k_direction<T>;
         kp.gridDim = dim3(nvb);
         kp.blockDim = dim3(VEC_BLOCK);
@@ -675,7 +722,7 @@ static int solve_impl(PcgImpl* h, const void* scale, const void* b, const void* 
                 rc = enqueue_refresh<T>(h, D, st);
                 if (rc) return rc;
             }
-            k_direction<T><<<h->n_vec_blocks, VEC_BLOCK, 0, st>>>(D);
+            k_direction<T><<<h->n_vec_blocks, VEC_BLOCK, 0, st>>>(D, h->n_vec_blocks);
             TF_CHECK_LAUNCH();
             TF_CUDA_TRY(cudaMemcpyAsync(h->sc_host, h->sc, sizeof(CgScalars), cudaMemcpyDeviceToHost, st));
             TF_CUDA_TRY(cudaStreamSynchronize(st));

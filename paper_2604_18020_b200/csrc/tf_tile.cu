@@ -404,7 +404,7 @@ template <typename T, bool DOT>
 #define TF_TILE_MINB32 3
 #endif
 #ifndef TF_TILE_MINB64
-#define TF_TILE_MINB64 2
+#define TF_TILE_MINB64 3   // 168 regs + ~100 B spill: +5 % at c5 over 2 blocks/SM (measured)
 #endif
 __global__ void __launch_bounds__(TileDims<T>::NT, sizeof(T) == 4 ? TF_TILE_MINB32 : TF_TILE_MINB64)
 k_grid_tile3(Grid g, int oz, const T* __restrict__ scale, const T* __restrict__ v,
@@ -506,7 +506,7 @@ k_grid_tile3(Grid g, int oz, const T* __restrict__ scale, const T* __restrict__ 
 #pragma unroll
         for (int q = 0; q < 4; ++q) Gt[c][q] = T(0);
     T s_cur = scale_at(k0 - 1);
-    double dot = 0.0;
+    T dot = T(0);  // per-thread p.q in the working dtype (<= 3*oz terms), FP64 across threads
     const int own_node0 = (i0 + tx) + g.nnx * (j0 + ty);
 
     for (int L = 0; L < n_layers; ++L) {
@@ -593,7 +593,7 @@ k_grid_tile3(Grid g, int oz, const T* __restrict__ scale, const T* __restrict__ 
                 w[d] = acc;
                 if (DOT) {
                     const T p = fx ? v[d] : pown[c];
-                    dot += (double)p * (double)acc;
+                    dot = fma(p, acc, dot);
                 }
             }
         }
@@ -606,9 +606,10 @@ k_grid_tile3(Grid g, int oz, const T* __restrict__ scale, const T* __restrict__ 
 
     if (DOT) {
         __shared__ double sh[TILE_NT / 32];
+        double dd = (double)dot;
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) dot += __shfl_down_sync(0xffffffffu, dot, o);
-        if ((tid & 31) == 0) sh[tid >> 5] = dot;
+        for (int o = 16; o > 0; o >>= 1) dd += __shfl_down_sync(0xffffffffu, dd, o);
+        if ((tid & 31) == 0) sh[tid >> 5] = dd;
         __syncthreads();
         if (tid == 0) {
             double s = 0.0;

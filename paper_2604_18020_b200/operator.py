@@ -309,12 +309,14 @@ class MatFreeOperator:
         dev = self._scale_dev.device
         tdt = D.tdtype(self.precision.dtype)
         cur = t.cuda.current_stream()
-        s_in, s_k, s_out = t.cuda.Stream(), t.cuda.Stream(), t.cuda.Stream()
-        xin = [t.empty(self.n_dof, dtype=tdt, device=dev) for _ in range(2)]
-        wout = [t.empty(self.n_dof, dtype=tdt, device=dev) for _ in range(2)]
-        h2d_done = [t.cuda.Event() for _ in range(2)]
-        k_done = [t.cuda.Event() for _ in range(2)]
-        d2h_done = [t.cuda.Event() for _ in range(2)]
+        if getattr(self, "_stream_ctx", None) is None:  # streams/buffers reused across calls
+            self._stream_ctx = (
+                (t.cuda.Stream(), t.cuda.Stream(), t.cuda.Stream()),
+                [t.empty(self.n_dof, dtype=tdt, device=dev) for _ in range(2)],
+                [t.empty(self.n_dof, dtype=tdt, device=dev) for _ in range(2)],
+                [[t.cuda.Event() for _ in range(2)] for _ in range(3)],
+            )
+        (s_in, s_k, s_out), xin, wout, (h2d_done, k_done, d2h_done) = self._stream_ctx
         for s_ in (s_in, s_k, s_out):
             s_.wait_stream(cur)
         for i, (hv, hw) in enumerate(zip(host_in, host_out)):

@@ -932,6 +932,12 @@ TileShape tile_shape(const Grid& g)
     long long chunks = std::max<long long>(1, slots / cols);           // fill one wave
     int oz = (int)std::max<long long>(2, (g.nnz + chunks - 1) / chunks);
     oz = std::min(oz, 16);
+    static int oz_env = -1;  // TF_TILE_OZ: experiment override of the z-chunk height
+    if (oz_env < 0) {
+        const char* e = getenv("TF_TILE_OZ");
+        oz_env = e ? std::max(0, atoi(e)) : 0;
+    }
+    if (oz_env > 0) oz = oz_env;
     const int tz = (g.nnz + oz - 1) / oz;
     return {dim3(tx, ty, tz), oz};
 }

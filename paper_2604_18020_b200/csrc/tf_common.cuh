@@ -69,4 +69,50 @@ __host__ __device__ constexpr int corner_of(int ox, int oy, int oz)
 template <typename T>
 __device__ __forceinline__ T ld_nc(const T* p) { return __ldg(p); }
 
+// ---- device-resident PCG state (tf_pcg.cu, and the fused CG tile kernel) ----
+enum { TERM_CONVERGED = 0, TERM_MAX_ITER = 1, TERM_BREAKDOWN = 2, TERM_DIVERGED = 3 };
+
+// Field ownership inside one iteration: no kernel reads a field that the same
+// kernel's block 0 writes.
+//   unfused body (general edof): k_update reads it/rz/done, writes it_cur/
+//     alpha/rz_old/refresh/matvecs (+done on breakdown); k_direction reads
+//     it_cur/rz_old and commits it/rz/rel/beta/done/term.
+//   fused body (structured): the CG tile kernel reads it_a/rz_old, decides the
+//     previous iteration and commits rel/hist/rz/beta (or done/term/it) and
+//     it_b = it_a + 1; k_update_f reads it_b/rz and writes it_a/alpha/rz_old/
+//     refresh/matvecs (+done/it on breakdown).
+struct CgScalars {
+    double bnorm, rz, rz_old, alpha, beta, rel, tol;
+    double* hist;
+    int it, done, term, matvecs, refresh, max_iter, recompute, zero_rhs;
+    int it_cur;
+    int it_a, it_b;
+};
+
+__device__ __forceinline__ double cg_round(double v, bool f32) { return f32 ? (double)(float)v : v; }
+__device__ __forceinline__ double cg_sqrt(double v, bool f32)
+{
+    return f32 ? (double)sqrtf((float)v) : sqrt(v);
+}
+__device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ float sub_rn(float a, float b) { return __fsub_rn(a, b); }
+__device__ __forceinline__ double sub_rn(double a, double b) { return __dsub_rn(a, b); }
+
+// Arguments of the fused CG tile kernel (direction update folded into the
+// matvec's plane staging): p_new = r*inv + beta*p_old with ping-pong p buffers.
+template <typename T>
+struct CgTileArgs {
+    const T* r;
+    const T* inv;
+    T* pbuf[2];            // p of iteration k lives in pbuf[k & 1]
+    const double* part;    // r.r / r.z partials of the previous update (2 per block)
+    int nparts;
+    CgScalars* sc;
+    unsigned long long h_while;
+    int in_graph;
+};
+
 }  // namespace tf

@@ -39,20 +39,14 @@ template <typename T>
 long long grid_matvec_blocks(const Grid& g, const T* ke_host, int variant);
 template <typename T>
 int launch_pass_fixed(const int64_t* fixed, long long n, const T* v, T* w, cudaStream_t st);
+template <typename T>
+int launch_grid_tile_cg(const Grid& g, const T* ke_host, const T* scale, T* q,
+                        const uint8_t* node_fixed, double* dot_part, const CgTileArgs<T>& a,
+                        cudaStream_t st);
+template <typename T>
+bool launch_grid_tile_supported(const T* ke_host);
 
-enum { TERM_CONVERGED = 0, TERM_MAX_ITER = 1, TERM_BREAKDOWN = 2, TERM_DIVERGED = 3 };
 
-// Field ownership inside one iteration (no kernel reads a field that the
-// same kernel's block 0 writes): k_update reads it/rz/done and writes
-// it_cur/alpha/rz_old/refresh/matvecs(+done on breakdown); k_residual writes
-// matvecs; k_direction reads it_cur/rz_old/done and commits it/rz/rel/beta/
-// done/term and the graph conditions.
-struct CgScalars {
-    double bnorm, rz, rz_old, alpha, beta, rel, tol;
-    double* hist;
-    int it, done, term, matvecs, refresh, max_iter, recompute, zero_rhs;
-    int it_cur;
-};
 
 template <typename T>
 struct CgP {
@@ -66,19 +60,8 @@ struct CgP {
     int in_graph;  // 0: launched directly (TF_PCG_NOGRAPH profiling mode)
 };
 
-__device__ __forceinline__ double rnd(double v, bool f32) { return f32 ? (double)(float)v : v; }
-__device__ __forceinline__ double vsqrt(double v, bool f32)
-{
-    return f32 ? (double)sqrtf((float)v) : sqrt(v);
-}
-
-// product-then-add with the rounding numpy applies (never contracted to FMA)
-__device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
-__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
-__device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
-__device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
-__device__ __forceinline__ float sub_rn(float a, float b) { return __fsub_rn(a, b); }
-__device__ __forceinline__ double sub_rn(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double rnd(double v, bool f32) { return cg_round(v, f32); }
+__device__ __forceinline__ double vsqrt(double v, bool f32) { return cg_sqrt(v, f32); }
 
 constexpr int VEC_BLOCK = 256;
 
@@ -323,6 +306,85 @@ __global__ void __launch_bounds__(VEC_BLOCK) k_update(CgP<T> P, const double* pa
     }
 }
 
+// Fused-protocol update (structured solves): the search direction of this
+// iteration was written by the CG tile kernel into pbuf[it_b & 1].
+template <typename T>
+__global__ void __launch_bounds__(VEC_BLOCK) k_update_f(CgP<T> P, const double* part_mv, int nmv,
+                                                        T* pA, T* pB)
+{
+    constexpr int N = V16<T>::N;
+    CgScalars* sc = P.sc;
+    if (sc->done) return;
+    __shared__ double shp[VEC_BLOCK / 32];
+    const bool f32 = sizeof(T) == 4;
+    const double pq = rnd(sum_partials(part_mv, nmv, shp), f32);
+    const double rz = sc->rz;
+    const int it_now = sc->it_b;
+    const T* __restrict__ pn = (it_now & 1) ? pB : pA;
+    const bool bad = !isfinite(pq) || !isfinite(rz) || pq <= 0.0;
+    const double alpha = bad ? 0.0 : rz / pq;
+    const bool refresh = !bad && sc->recompute > 0 && it_now % sc->recompute == 0;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        sc->it_a = it_now;
+        sc->matvecs += 1;
+        sc->refresh = refresh ? 1 : 0;
+        sc->alpha = alpha;
+        sc->rz_old = rz;
+        if (bad) {
+            sc->it = it_now;
+            sc->done = 1;
+            sc->term = (!isfinite(pq) || !isfinite(rz)) ? TERM_DIVERGED : TERM_BREAKDOWN;
+            if (P.in_graph) cudaGraphSetConditional(P.h_while, 0u);
+        }
+        if (P.in_graph) cudaGraphSetConditional(P.h_refresh, refresh ? 1u : 0u);
+    }
+    if (bad) return;
+    const T a = (T)alpha;
+    double v[2] = {0.0, 0.0};
+    const long long nc = P.n / N, stride = (long long)gridDim.x * VEC_BLOCK;
+    for (long long c = (long long)blockIdx.x * VEC_BLOCK + threadIdx.x; c < nc; c += stride) {
+        T x[N], p[N], r[N], q[N], iv[N];
+        ld16(P.x, c, x);
+        ld16(pn, c, p);
+        if (!refresh) {
+            ld16(P.r, c, r);
+            ld16(P.q, c, q);
+            ld16(P.inv, c, iv);
+        }
+#pragma unroll
+        for (int k = 0; k < N; ++k) {
+            x[k] = add_rn(x[k], mul_rn(a, p[k]));
+            if (!refresh) {
+                r[k] = sub_rn(r[k], mul_rn(a, q[k]));
+                const T z = mul_rn(r[k], iv[k]);
+                v[0] += (double)r[k] * (double)r[k];
+                v[1] += (double)r[k] * (double)z;
+            }
+        }
+        st16(P.x, c, x);
+        if (!refresh) st16(P.r, c, r);
+    }
+    if (blockIdx.x == 0) {
+        for (long long i = nc * N + threadIdx.x; i < P.n; i += VEC_BLOCK) {
+            P.x[i] = add_rn(P.x[i], mul_rn(a, pn[i]));
+            if (!refresh) {
+                const T r = sub_rn(P.r[i], mul_rn(a, P.q[i]));
+                P.r[i] = r;
+                const T z = mul_rn(r, P.inv[i]);
+                v[0] += (double)r * (double)r;
+                v[1] += (double)r * (double)z;
+            }
+        }
+    }
+    if (refresh) return;
+    __shared__ double sh[2 * 32];
+    block_sum_k<2>(v, sh);
+    if (threadIdx.x == 0) {
+        P.part[2 * blockIdx.x] = v[0];
+        P.part[2 * blockIdx.x + 1] = v[1];
+    }
+}
+
 template <typename T>
 __global__ void __launch_bounds__(VEC_BLOCK) k_residual(CgP<T> P)
 {
@@ -469,6 +531,7 @@ __global__ void __launch_bounds__(VEC_BLOCK) k_init(CgP<T> P, int has_x0)
         const bool f32 = sizeof(T) == 4;
         sc->bnorm = vsqrt(rnd(tot[0], f32), f32);
         sc->it = 0;
+        sc->it_a = 0;
         sc->matvecs = has_x0 ? 1 : 0;
         sc->done = 0;
         sc->term = TERM_MAX_ITER;
@@ -510,6 +573,8 @@ struct PcgImpl {
     cudaStream_t stream;
     // device buffers
     void *x, *r, *p, *q, *b, *inv, *scale;
+    void* p2;           // second search-direction buffer (fused protocol)
+    int fused;          // structured tile solve with the direction folded into the matvec
     double* part;
     double* part_mv;    // per-CTA p.q partials of the matvec
     unsigned* tickets;
@@ -578,6 +643,24 @@ static int enqueue_part1(PcgImpl* h, const CgP<T>& P, cudaStream_t st)
 {
     const int nvb = h->n_vec_blocks;
     int nmv;
+    if (h->fused) {
+        CgTileArgs<T> a;
+        a.r = P.r;
+        a.inv = P.inv;
+        a.pbuf[0] = (T*)h->p;
+        a.pbuf[1] = (T*)h->p2;
+        a.part = h->part;
+        a.nparts = nvb;
+        a.sc = h->sc;
+        a.h_while = P.h_while;
+        a.in_graph = P.in_graph;
+        int r = launch_grid_tile_cg<T>(h->grid, (const T*)h->ke.data(), (const T*)h->scale, P.q,
+                                       h->node_fixed, h->part_mv, a, st);
+        if (r) return r;
+        k_update_f<T><<<nvb, VEC_BLOCK, 0, st>>>(P, h->part_mv, (int)h->n_mv_blocks, (T*)h->p, (T*)h->p2);
+        TF_CHECK_LAUNCH();
+        return TF_OK;
+    }
     if (h->structured) {
         int r = launch_grid_pull<T>(h->grid, (const T*)h->ke.data(), (const T*)h->scale, P.p, P.q,
                                     h->node_fixed, TF_MASK_INPUT | TF_PASS_FIXED, h->variant,
@@ -658,8 +741,8 @@ static int build_graph(PcgImpl* h)
         int rc = capture_into(ifbody, cap, [&](cudaStream_t st) -> int { return enqueue_refresh<T>(h, P, st); });
         if (rc) return rc;
     }
-    // direction update after the IF node
-    {
+    // direction update after the IF node (folded into the next matvec when fused)
+    if (!h->fused) {
         cudaKernelNodeParams kp = {};
         int nparts = nvb;
         void* args[] = {&P, &nparts};
@@ -722,8 +805,10 @@ static int solve_impl(PcgImpl* h, const void* scale, const void* b, const void* 
                 rc = enqueue_refresh<T>(h, D, st);
                 if (rc) return rc;
             }
-            k_direction<T><<<h->n_vec_blocks, VEC_BLOCK, 0, st>>>(D, h->n_vec_blocks);
-            TF_CHECK_LAUNCH();
+            if (!h->fused) {
+                k_direction<T><<<h->n_vec_blocks, VEC_BLOCK, 0, st>>>(D, h->n_vec_blocks);
+                TF_CHECK_LAUNCH();
+            }
             TF_CUDA_TRY(cudaMemcpyAsync(h->sc_host, h->sc, sizeof(CgScalars), cudaMemcpyDeviceToHost, st));
             TF_CUDA_TRY(cudaStreamSynchronize(st));
         }
@@ -769,6 +854,7 @@ int tf_pcg_create(tf_pcg** out, const tf_pcg_desc* d, void* stream)
     h->graph = nullptr;
     h->exec = nullptr;
     h->x = h->r = h->p = h->q = h->b = h->inv = h->scale = nullptr;
+    h->p2 = nullptr;
     h->part = nullptr;
     h->part_mv = nullptr;
     h->tickets = nullptr;
@@ -793,6 +879,14 @@ int tf_pcg_create(tf_pcg** out, const tf_pcg_desc* d, void* stream)
     const size_t vb = es * d->n_dof;
     void** bufs[] = {&h->x, &h->r, &h->p, &h->q, &h->b, &h->inv};
     for (void** pb : bufs) TF_CUDA_TRY(cudaMalloc(pb, vb));
+    // fused protocol: structured grid, production variant, parity-block Ke
+    h->fused = 0;
+    if (d->structured && d->grid_variant == TF_GRID_FAST && !getenv("TF_PCG_UNFUSED")) {
+        const bool ok = d->precision == 32 ? launch_grid_tile_supported<float>((const float*)d->ke)
+                                           : launch_grid_tile_supported<double>((const double*)d->ke);
+        h->fused = ok ? 1 : 0;
+    }
+    if (h->fused) TF_CUDA_TRY(cudaMalloc(&h->p2, vb));
     TF_CUDA_TRY(cudaMalloc(&h->scale, es * d->n_elem));
     const long long npart = (long long)h->n_vec_blocks * 3 + 8;
     TF_CUDA_TRY(cudaMalloc(&h->part, sizeof(double) * npart));
@@ -829,7 +923,7 @@ int tf_pcg_destroy(tf_pcg* hh)
     if (!h) return TF_OK;
     if (h->exec) cudaGraphExecDestroy(h->exec);
     if (h->graph) cudaGraphDestroy(h->graph);
-    void* bufs[] = {h->x, h->r, h->p, h->q, h->b, h->inv, h->scale, h->part, h->part_mv, h->tickets, h->sc};
+    void* bufs[] = {h->x, h->r, h->p, h->q, h->b, h->inv, h->scale, h->p2, h->part, h->part_mv, h->tickets, h->sc};
     for (void* p : bufs)
         if (p) cudaFree(p);
     if (h->sc_host) cudaFreeHost(h->sc_host);

@@ -620,6 +620,304 @@ k_grid_tile3(Grid g, int oz, const T* __restrict__ scale, const T* __restrict__ 
 }
 
 // ---------------------------------------------------------------------------
+// Fused CG tile kernel: one PCG iteration's head in one launch.
+//   1. every CTA reduces the previous update's r.r / r.z partials in the same
+//      fixed order and takes the reference's decision (solver.py:120-135):
+//      converged / max_iter / diverged -> stop (block 0 commits, WHILE = 0);
+//      else beta = rz_new / rz_old;
+//   2. the node planes are staged through registers computing the new search
+//      direction on the fly, p_new = r*inv + beta*p_old (numpy rounding), the
+//      owning CTA writes p_new once (ping-pong buffers: no CTA ever reads a
+//      p value another CTA has already overwritten);
+//   3. q = A p_new exactly as k_grid_tile3 (masked input, pass-through) and
+//      per-CTA p.q partials for k_update_f.
+// This removes the separate direction kernel (a full read of r, inv, p and a
+// write of p) and its launch from every CG iteration.
+// ---------------------------------------------------------------------------
+#ifndef TF_CG_MINB32
+#define TF_CG_MINB32 2
+#endif
+template <typename T>
+__global__ void __launch_bounds__(TileDims<T>::NT, sizeof(T) == 4 ? TF_CG_MINB32 : 2)
+k_grid_tile3_cg(Grid g, int oz, const T* __restrict__ scale, T* __restrict__ w,
+                const uint8_t* __restrict__ node_fixed, double* __restrict__ dot_part,
+                const __grid_constant__ KhatBlocks<T> kb, const __grid_constant__ CgTileArgs<T> A)
+{
+    constexpr int TILE_BY = TileDims<T>::BY, TILE_NT = TileDims<T>::NT;
+    constexpr int PW = StageSlots<T>::PW, PN = StageSlots<T>::PN, NS = StageSlots<T>::N;
+    __shared__ __align__(16) T plane[2][PN];
+    __shared__ T Y[3][TILE_NT];
+    __shared__ double shr[2][TILE_NT / 32];
+
+    CgScalars* sc = A.sc;
+    if (sc->done) return;
+    const int tx = threadIdx.x, ty = threadIdx.y;
+    const int tid = tx + TILE_BX * ty;
+    const bool f32 = sizeof(T) == 4;
+
+    // ---- 1. decision for the previous iteration ----------------------------------
+    const int it_prev = sc->it_a;
+    double beta = 0.0;
+    if (it_prev > 0) {
+        double v0 = 0.0, v1 = 0.0;
+        for (int i = tid; i < A.nparts; i += TILE_NT) {
+            v0 += __ldcg(A.part + 2 * i);
+            v1 += __ldcg(A.part + 2 * i + 1);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            v0 += __shfl_down_sync(0xffffffffu, v0, o);
+            v1 += __shfl_down_sync(0xffffffffu, v1, o);
+        }
+        if ((tid & 31) == 0) {
+            shr[0][tid >> 5] = v0;
+            shr[1][tid >> 5] = v1;
+        }
+        __syncthreads();
+        double rr = 0.0, rzn = 0.0;
+        for (int i = 0; i < TILE_NT / 32; ++i) {
+            rr += shr[0][i];
+            rzn += shr[1][i];
+        }
+        const double rn = cg_sqrt(cg_round(rr, f32), f32);
+        bool stop = false;
+        int term = TERM_MAX_ITER;
+        double rel = 0.0, rz_new = 0.0;
+        if (!isfinite(rn)) {
+            stop = true;
+            term = TERM_DIVERGED;
+        } else {
+            rel = rn / sc->bnorm;
+            if (rel <= sc->tol) {
+                stop = true;
+                term = TERM_CONVERGED;
+            } else {
+                rz_new = cg_round(rzn, f32);
+                beta = rz_new / sc->rz_old;
+                if (it_prev >= sc->max_iter) stop = true;
+            }
+        }
+        const bool b0 = blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && tid == 0;
+        if (b0) {
+            if (isfinite(rn)) {
+                sc->rel = rel;
+                if (sc->hist) sc->hist[it_prev] = rel;
+            }
+            if (stop) {
+                sc->done = 1;
+                sc->term = term;
+                sc->it = it_prev;
+                if (A.in_graph) cudaGraphSetConditional(A.h_while, 0u);
+            } else {
+                sc->rz = rz_new;
+                sc->beta = beta;
+            }
+        }
+        if (stop) return;
+    }
+    const int it_now = it_prev + 1;
+    if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && tid == 0) sc->it_b = it_now;
+    const T* __restrict__ p_old = A.pbuf[it_prev & 1];
+    T* __restrict__ p_new = A.pbuf[it_now & 1];
+    const T be = (T)beta;
+    const bool first = it_prev == 0;
+
+    // ---- 2./3. staged matvec on p_new ----------------------------------------------
+    const int i0 = blockIdx.x * (TILE_BX - 1);
+    const int j0 = blockIdx.y * (TILE_BY - 1);
+    const int k0 = blockIdx.z * oz;
+    const int ex = i0 - 1 + tx, ey = j0 - 1 + ty;
+    const bool col_ok = ex >= 0 && ex < g.nelx && ey >= 0 && ey < g.nely;
+    const bool owner = tx < TILE_BX - 1 && ty < TILE_BY - 1 && (i0 + tx) < g.nnx && (j0 + ty) < g.nny;
+    const int pn = g.nnx * g.nny, pn3 = 3 * pn;
+    const uint8_t* col_or = node_fixed ? node_fixed + g.n_nodes : nullptr;
+    const uint8_t* col_and = node_fixed ? col_or + pn : nullptr;
+
+    int s_off[NS], s_node[NS], s_c[NS];
+    unsigned okbits = 0u, mskbits = 0u, allfix = 0u, ownbits = 0u;
+#pragma unroll
+    for (int q = 0; q < NS; ++q) {
+        const int idx = tid + q * TILE_NT;
+        const int r = idx / PW, f = idx - r * PW;
+        const int ii = i0 - 1 + f / 3, jj = j0 - 1 + r, c = f % 3;
+        const bool ok = idx < PN && ii >= 0 && ii < g.nnx && jj >= 0 && jj < g.nny;
+        const int node = ok ? ii + g.nnx * jj : 0;
+        s_off[q] = 3 * node + c;
+        s_node[q] = node;
+        s_c[q] = c;
+        if (ok) {
+            okbits |= 1u << q;
+            if (node_fixed) {
+                if ((col_and[node] >> c) & 1u) allfix |= 1u << q;
+                else if ((col_or[node] >> c) & 1u) mskbits |= 1u << q;
+            }
+            // the CTA owning node column (ii, jj) writes its p_new
+            if (ii >= i0 && ii < i0 + TILE_BX - 1 && jj >= j0 && jj < j0 + TILE_BY - 1) ownbits |= 1u << q;
+        }
+    }
+    // raw r, inv, p_old of a plane prefetched into registers one layer ahead
+    T pr[NS], pi[NS], pp[NS];
+    auto fetch = [&](int kz) {
+        const bool zok = kz >= 0 && kz < g.nnz;
+        const long long base = (long long)min(max(kz, 0), g.nnz - 1) * pn3;
+#pragma unroll
+        for (int q = 0; q < NS; ++q) {
+            const bool take = zok && ((okbits >> q) & 1u);
+            const long long d = base + s_off[q];
+            pr[q] = take ? ld_nc(A.r + d) : T(0);
+            pi[q] = take ? ld_nc(A.inv + d) : T(0);
+            pp[q] = (take && !first) ? p_old[d] : T(0);
+        }
+    };
+    auto commit = [&](int kz, T* buf) {
+        const bool zok = kz >= 0 && kz < g.nnz;
+        const bool wr = zok && kz >= k0 && kz < k0 + oz;
+        const long long base = (long long)min(max(kz, 0), g.nnz - 1) * pn3;
+#pragma unroll
+        for (int q = 0; q < NS; ++q) {
+            const int idx = tid + q * TILE_NT;
+            if (q < NS - 1 || idx < PN) {
+                const bool ok = zok && ((okbits >> q) & 1u);
+                T pv = first ? mul_rn(pr[q], pi[q]) : add_rn(mul_rn(pr[q], pi[q]), mul_rn(be, pp[q]));
+                if (!ok) pv = T(0);
+                if (wr && ((ownbits >> q) & 1u)) p_new[base + s_off[q]] = pv;
+                bool fixed = (allfix >> q) & 1u;
+                if (!fixed && ((mskbits >> q) & 1u) && ok) fixed = (node_fixed[kz * pn + s_node[q]] >> s_c[q]) & 1u;
+                buf[idx] = fixed ? T(0) : pv;
+            }
+        }
+    };
+    const int pofs = ty * PW + 3 * tx;
+    auto pv_ = [&](const T* buf, int ox, int oy, int c) -> T { return buf[pofs + oy * PW + 3 * ox + c]; };
+    const int el_col = ex + g.nelx * ey, el_plane = g.nelx * g.nely;
+    auto scale_at = [&](int ez) -> T {
+        return (col_ok && ez >= 0 && ez < g.nelz) ? ld_nc(scale + el_col + el_plane * ez) : T(0);
+    };
+
+    const int n_layers = min(oz, g.nnz - k0) + 1;
+    T* b_cur = plane[0];
+    T* b_top = plane[1];
+    fetch(k0 - 1);
+    commit(k0 - 1, b_cur);
+    fetch(k0);
+    commit(k0, b_top);
+    fetch(k0 + 1);
+    __syncthreads();
+    T XYb[3][4];
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+        face_fwd(pv_(b_cur, 0, 0, c), pv_(b_cur, 1, 0, c), pv_(b_cur, 0, 1, c), pv_(b_cur, 1, 1, c), XYb[c]);
+    T Gt[3][4];
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) Gt[c][q] = T(0);
+    T s_cur = scale_at(k0 - 1);
+    T dot = T(0);
+    const int own_node0 = (i0 + tx) + g.nnx * (j0 + ty);
+
+    for (int L = 0; L < n_layers; ++L) {
+        const int ez = k0 - 1 + L;
+        if (L >= 1) {
+            // plane ez+1 into the buffer that held plane ez-1 (read before (B) of layer L-1)
+            commit(ez + 1, b_top);
+            if (L + 1 < n_layers) fetch(ez + 2);
+        }
+        __syncthreads();                                   // (A)
+        const T s_next = scale_at(ez + 1);
+        const bool write_plane = owner && L >= 1;
+        unsigned own_bits = 0u;
+        if (write_plane && node_fixed) own_bits = node_fixed[own_node0 + ez * pn];
+        T pown[3];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) pown[c] = pv_(b_cur, 1, 1, c);
+        T h[3][8];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            T XYt[4];
+            face_fwd(pv_(b_top, 0, 0, c), pv_(b_top, 1, 0, c), pv_(b_top, 0, 1, c), pv_(b_top, 1, 1, c), XYt);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                h[c][q] = XYb[c][q] + XYt[q];
+                h[c][q + 4] = XYt[q] - XYb[c][q];
+                XYb[c][q] = XYt[q];
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+#pragma unroll
+            for (int m = 1; m < 8; ++m) h[c][m] *= s_cur;
+        T gm[3][8];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) gm[c][0] = T(0);
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                const int m = q ^ (1 << c);
+                if (m == 0) continue;
+                T acc = T(0);
+#pragma unroll
+                for (int d = 0; d < 3; ++d) {
+                    const int n = q ^ (1 << d);
+                    if (n == 0) continue;
+                    acc = fma(kb.b[q][c][d], h[d][n], acc);
+                }
+                gm[c][m] = acc;
+            }
+        T corner[3][4];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            T H[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                H[q] = Gt[c][q] + (gm[c][q] - gm[c][q + 4]);
+                Gt[c][q] = gm[c][q] + gm[c][q + 4];
+            }
+            face_inv(H, corner[c]);
+        }
+        T xr[2][3];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            xr[0][c] = corner[c][1] + __shfl_down_sync(0xffffffffu, corner[c][0], 1);
+            xr[1][c] = corner[c][3] + __shfl_down_sync(0xffffffffu, corner[c][2], 1);
+            Y[c][tid] = xr[0][c];
+        }
+        __syncthreads();                                   // (B)
+        if (write_plane) {
+            const int d0 = 3 * (own_node0 + ez * pn);
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                T acc = xr[1][c] + Y[c][tid + TILE_BX];
+                const int d = d0 + c;
+                const bool fx = (own_bits >> c) & 1u;
+                // constrained DOF: q = p (pass-through); p itself is unmasked
+                const T p = fx ? p_new[d] : pown[c];
+                if (fx) acc = p;
+                w[d] = acc;
+                dot = fma(p, acc, dot);
+            }
+        }
+        s_cur = s_next;
+        T* t = b_cur;
+        b_cur = b_top;
+        b_top = t;
+    }
+
+    double dd = (double)dot;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) dd += __shfl_down_sync(0xffffffffu, dd, o);
+    __syncthreads();
+    if ((tid & 31) == 0) shr[0][tid >> 5] = dd;
+    __syncthreads();
+    if (tid == 0) {
+        double s2 = 0.0;
+        for (int i = 0; i < TILE_NT / 32; ++i) s2 += shr[0][i];
+        dot_part[blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z)] = s2;
+    }
+}
+
+// ---------------------------------------------------------------------------
 // v4 (FP32): two element columns per thread, packed FP32x2 arithmetic.
 //
 // sm_100a issues FADD2/FMUL2/FFMA2 (two FP32 lanes per instruction, scalar
@@ -992,6 +1290,30 @@ int launch_grid_tile(const Grid& g, const T* ke_host, const T* scale, const T* v
     TF_CHECK_LAUNCH();
     return TF_OK;
 }
+
+// Fused CG head (decision + direction + matvec + p.q partials); grid as the
+// production tile kernel so the partial count matches grid_tile_blocks().
+template <typename T>
+int launch_grid_tile_cg(const Grid& g, const T* ke_host, const T* scale, T* q,
+                        const uint8_t* node_fixed, double* dot_part, const CgTileArgs<T>& a,
+                        cudaStream_t st)
+{
+    KhatBlocks<T> kb;
+    if (!khat_blocks<T>(ke_host, &kb)) return TF_ERR_UNSUPPORTED;
+    if (3 * g.n_nodes >= (1LL << 31)) {
+        set_error("structured grid too large for int32 DOF indices");
+        return TF_ERR_ARG;
+    }
+    TileShape sh = tile_shape<T>(g);
+    dim3 block(TILE_BX, TileDims<T>::BY, 1);
+    k_grid_tile3_cg<T><<<sh.grid, block, 0, st>>>(g, sh.oz, scale, q, node_fixed, dot_part, kb, a);
+    TF_CHECK_LAUNCH();
+    return TF_OK;
+}
+template int launch_grid_tile_cg<float>(const Grid&, const float*, const float*, float*,
+                                        const uint8_t*, double*, const CgTileArgs<float>&, cudaStream_t);
+template int launch_grid_tile_cg<double>(const Grid&, const double*, const double*, double*,
+                                         const uint8_t*, double*, const CgTileArgs<double>&, cudaStream_t);
 
 template <typename T>
 bool launch_grid_tile_supported(const T* ke_host)

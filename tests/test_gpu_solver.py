@@ -153,3 +153,26 @@ def test_simp_desk_selected_compliance(prec, kernel):
     # beta=32 design to a neighbouring local optimum: bound by the reference's
     # own fp32-vs-fp64 spread (1.7 %, test_acceptance.py:348-357) with margin
     assert abs(sel - want) <= 0.03 * want
+
+
+@pytest.mark.parametrize("prec", ["fp64", "fp32"])
+def test_fused_and_unfused_pcg_protocols_agree(prec, monkeypatch):
+    """The structured solve folds the direction update into the matvec (fused
+    protocol); TF_PCG_UNFUSED=1 runs the separate direction kernel.  Same
+    recurrence, same rounding of every vector update -> same iterates."""
+    from paper_2604_18020_b200 import (CgConfig, MatFreeOperator, SimpParams, build_edof,
+                                       make_preset, solve_equilibrium)
+
+    res = []
+    for unfused in (False, True):
+        if unfused:
+            monkeypatch.setenv("TF_PCG_UNFUSED", "1")
+        pb = make_preset("cantilever", 0.4)
+        op = MatFreeOperator(pb.mesh, build_edof(pb.mesh), pb.bcs, np.full(pb.mesh.n_elem, 0.5),
+                             SimpParams(3.0), prec)
+        res.append(solve_equilibrium(op, pb.bcs.force, CgConfig(max_iter=400)))
+    (u0, r0), (u1, r1) = res
+    assert r0.iterations == r1.iterations and r0.termination == r1.termination
+    assert r0.matvecs == r1.matvecs
+    np.testing.assert_allclose(r0.residual_history, r1.residual_history, rtol=1e-6)
+    assert np.abs(u0 - u1).max() <= 1e-6 * np.abs(u1).max()

@@ -1230,6 +1230,9 @@ TileShape tile_shape(const Grid& g)
     long long chunks = std::max<long long>(1, slots / cols);           // fill one wave
     int oz = (int)std::max<long long>(2, (g.nnz + chunks - 1) / chunks);
     oz = std::min(oz, 16);
+    // big grids: taller chunks halve the halo layer when >= 1.5 waves remain
+    // (c5: 100.8 vs 104.6 us measured; smaller grids keep 16)
+    if (oz == 16 && cols * ((g.nnz + 31) / 32) * 2 >= 3 * slots) oz = 32;
     static int oz_env = -1;  // TF_TILE_OZ: experiment override of the z-chunk height
     if (oz_env < 0) {
         const char* e = getenv("TF_TILE_OZ");

@@ -879,12 +879,18 @@ int tf_pcg_create(tf_pcg** out, const tf_pcg_desc* d, void* stream)
     const size_t vb = es * d->n_dof;
     void** bufs[] = {&h->x, &h->r, &h->p, &h->q, &h->b, &h->inv};
     for (void** pb : bufs) TF_CUDA_TRY(cudaMalloc(pb, vb));
-    // fused protocol: structured grid, production variant, parity-block Ke
+    // fused protocol (direction folded into the matvec staging, 2 launches per
+    // iteration): wins on small, launch-bound systems (c1 SIMP 5.7 vs 6.5 ms/it)
+    // and loses on large ones (register-path staging: c2 34 vs 30 us/it, c5
+    // 163 vs 151 us for matvec+direction) -> default below 100k elements;
+    // TF_PCG_FUSED=0/1 forces either protocol.
     h->fused = 0;
-    if (d->structured && d->grid_variant == TF_GRID_FAST && !getenv("TF_PCG_UNFUSED")) {
+    if (d->structured && d->grid_variant == TF_GRID_FAST) {
         const bool ok = d->precision == 32 ? launch_grid_tile_supported<float>((const float*)d->ke)
                                            : launch_grid_tile_supported<double>((const double*)d->ke);
-        h->fused = ok ? 1 : 0;
+        const char* e = getenv("TF_PCG_FUSED");
+        const bool want = e ? (e[0] == '1') : (d->n_elem <= 100000);
+        h->fused = (ok && want) ? 1 : 0;
     }
     if (h->fused) TF_CUDA_TRY(cudaMalloc(&h->p2, vb));
     TF_CUDA_TRY(cudaMalloc(&h->scale, es * d->n_elem));

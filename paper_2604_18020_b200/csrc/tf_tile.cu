@@ -414,7 +414,7 @@ k_grid_tile3(Grid g, int oz, const T* __restrict__ scale, const T* __restrict__ 
     constexpr int TILE_BY = TileDims<T>::BY, TILE_NT = TileDims<T>::NT;
     constexpr int PW = StageSlots<T>::PW, PN = StageSlots<T>::PN, NS = StageSlots<T>::N;
     __shared__ __align__(16) T plane[3][PN];  // ring: node plane k lives in buffer k % 3
-    __shared__ T Y[3][TILE_NT];               // x-combined sums handed to the row below
+    __shared__ T Y[2][3][TILE_NT];            // x-combined sums handed to the row below (by layer parity)
 
     const int tx = threadIdx.x, ty = threadIdx.y;
     const int tid = tx + TILE_BX * ty;
@@ -509,11 +509,36 @@ k_grid_tile3(Grid g, int oz, const T* __restrict__ scale, const T* __restrict__ 
     T dot = T(0);  // per-thread p.q in the working dtype (<= 3*oz terms), FP64 across threads
     const int own_node0 = (i0 + tx) + g.nnx * (j0 + ty);
 
+    // The node pass of layer L runs at the head of layer L+1, behind the same
+    // barrier that publishes plane ez+2 -> one __syncthreads per layer.
+    T pend_x1[3], pend_p[3];
+    unsigned pend_bits = 0u;
+    int pend_d0 = 0;
+    bool pend = false;
+    auto node_pass = [&](int yb) {
+        if (!pend) return;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            T acc = pend_x1[c] + Y[yb][c][tid + TILE_BX];
+            const int d = pend_d0 + c;
+            if (flags & TF_ACCUMULATE) acc += w[d];
+            const bool fx = (pend_bits >> c) & 1u;
+            if ((flags & TF_PASS_FIXED) && fx) acc = v[d];
+            w[d] = acc;
+            if (DOT) {
+                const T p = fx ? v[d] : pend_p[c];
+                dot = fma(p, acc, dot);
+            }
+        }
+    };
+
     for (int L = 0; L < n_layers; ++L) {
         const int ez = k0 - 1 + L;
-        // plane ez+1 was staged one layer ago (or in the prologue): make it visible
+        // plane ez+1 was staged one layer ago (or in the prologue): make it
+        // visible together with the previous layer's row hand-off
         cp_async_wait_all();
         __syncthreads();                                   // (A)
+        node_pass((L + 1) & 1);                            // plane ez-1 (layer L-1)
         if (L + 1 < n_layers) stage(ez + 2, b_nxt);         // lands during this layer
         const T s_next = scale_at(ez + 1);
         const bool write_plane = owner && L >= 1;
@@ -573,36 +598,24 @@ k_grid_tile3(Grid g, int oz, const T* __restrict__ scale, const T* __restrict__ 
         }
         // node (i0+tx, j0+ty) gets corner (1,1) of this column, (0,1) of column
         // tx+1 (next lane), (1,0) of row ty+1 and (0,0) of (tx+1, ty+1)
-        T xr[2][3];
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
-            xr[0][c] = corner[c][1] + __shfl_down_sync(0xffffffffu, corner[c][0], 1);
-            xr[1][c] = corner[c][3] + __shfl_down_sync(0xffffffffu, corner[c][2], 1);
-            Y[c][tid] = xr[0][c];
+            const T x0 = corner[c][1] + __shfl_down_sync(0xffffffffu, corner[c][0], 1);
+            pend_x1[c] = corner[c][3] + __shfl_down_sync(0xffffffffu, corner[c][2], 1);
+            Y[L & 1][c][tid] = x0;
+            if (DOT) pend_p[c] = pown[c];
         }
-        __syncthreads();                                   // (B)
-        if (write_plane) {
-            const int d0 = 3 * (own_node0 + ez * pn);
-#pragma unroll
-            for (int c = 0; c < 3; ++c) {
-                T acc = xr[1][c] + Y[c][tid + TILE_BX];
-                const int d = d0 + c;
-                if (flags & TF_ACCUMULATE) acc += w[d];
-                const bool fx = (own_bits >> c) & 1u;
-                if ((flags & TF_PASS_FIXED) && fx) acc = v[d];
-                w[d] = acc;
-                if (DOT) {
-                    const T p = fx ? v[d] : pown[c];
-                    dot = fma(p, acc, dot);
-                }
-            }
-        }
+        pend = write_plane;
+        pend_bits = own_bits;
+        pend_d0 = 3 * (own_node0 + ez * pn);
         s_cur = s_next;
         T* t = b_cur;  // rotate the ring
         b_cur = b_top;
         b_top = b_nxt;
         b_nxt = t;
     }
+    __syncthreads();
+    node_pass((n_layers - 1) & 1);
 
     if (DOT) {
         __shared__ double sh[TILE_NT / 32];

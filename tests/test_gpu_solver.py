@@ -158,15 +158,15 @@ def test_simp_desk_selected_compliance(prec, kernel):
 @pytest.mark.parametrize("prec", ["fp64", "fp32"])
 def test_fused_and_unfused_pcg_protocols_agree(prec, monkeypatch):
     """The structured solve folds the direction update into the matvec (fused
-    protocol); TF_PCG_UNFUSED=1 runs the separate direction kernel.  Same
+    protocol, default below 100k elements); TF_PCG_FUSED=0 runs the separate
+    direction kernel.  Same
     recurrence, same rounding of every vector update -> same iterates."""
     from paper_2604_18020_b200 import (CgConfig, MatFreeOperator, SimpParams, build_edof,
                                        make_preset, solve_equilibrium)
 
     res = []
-    for unfused in (False, True):
-        if unfused:
-            monkeypatch.setenv("TF_PCG_UNFUSED", "1")
+    for fused in ("1", "0"):
+        monkeypatch.setenv("TF_PCG_FUSED", fused)
         pb = make_preset("cantilever", 0.4)
         op = MatFreeOperator(pb.mesh, build_edof(pb.mesh), pb.bcs, np.full(pb.mesh.n_elem, 0.5),
                              SimpParams(3.0), prec)

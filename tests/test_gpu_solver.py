@@ -176,3 +176,36 @@ def test_fused_and_unfused_pcg_protocols_agree(prec, monkeypatch):
     assert r0.matvecs == r1.matvecs
     np.testing.assert_allclose(r0.residual_history, r1.residual_history, rtol=1e-6)
     assert np.abs(u0 - u1).max() <= 1e-6 * np.abs(u1).max()
+
+
+@pytest.mark.parametrize("variant,scatter", [("fused", "parallel_atomic"), ("fused", "serial"),
+                                             ("three_stage", "serial")])
+def test_general_connectivity_pcg_matches_oracle(variant, scatter):
+    """Device PCG over the general-edof kernels (seeded-random DOF relabel,
+    reference bench.py:151-160) against the oracle's recurrence."""
+    import oracle
+    from paper_2604_18020_b200 import (BoundaryConditions, CgConfig, MatFreeOperator, SimpParams,
+                                       build_edof, make_preset, solve_equilibrium)
+
+    pb = make_preset("cantilever", 0.2)
+    m = pb.mesh
+    edof = build_edof(m)
+    rng = np.random.default_rng(42)
+    perm = rng.permutation(m.n_dof).astype(np.int32)
+    ep = np.ascontiguousarray(perm[edof])
+    force = np.zeros(m.n_dof)
+    force[perm] = pb.bcs.force
+    bp = BoundaryConditions(np.sort(perm[pb.bcs.fixed_dofs]), force)
+    rho = np.full(m.n_elem, 0.5)
+    op = MatFreeOperator(m, ep, bp, rho, SimpParams(3.0), "fp64", variant=variant, scatter=scatter)
+    assert not op.structured
+    u, rep = solve_equilibrium(op, bp.force, CgConfig())
+    A = lambda x: oracle.apply(ep, op.ke, op.scale, x, bp.fixed_dofs, m.n_dof)
+    d = oracle.diagonal(ep, op.ke, op.scale, bp.fixed_dofs, m.n_dof)
+    x_ref, info = oracle.pcg(A, bp.force.copy(), d)
+    assert rep.termination == info["termination"]
+    assert abs(rep.iterations - info["iterations"]) <= 2
+    assert np.abs(u - x_ref).max() <= 1e-6 * np.abs(x_ref).max()
+    # the golden cold solve on the unpermuted problem: same physics
+    g = load_golden("cg.json")["desk_fp64"]
+    assert abs(rep.compliance - g["compliance"]) <= 1e-6 * g["compliance"]

@@ -83,6 +83,16 @@ int tf_matvec_grid_f64(const tf_grid* g, const double* ke, const double* scale,
                        const double* v, double* w, const uint8_t* node_fixed, uint32_t flags,
                        int variant, void* stream);
 
+/* Same, producing only the outputs of node x-columns [i_lo, i_hi) (all j, k);
+ * the x-slab decomposition computes its interface columns first and overlaps
+ * the neighbour exchange with the interior range (slab.py). */
+int tf_matvec_grid_range_f32(const tf_grid* g, const float* ke, const float* scale, const float* v,
+                             float* w, const uint8_t* node_fixed, uint32_t flags, int32_t i_lo,
+                             int32_t i_hi, void* stream);
+int tf_matvec_grid_range_f64(const tf_grid* g, const double* ke, const double* scale,
+                             const double* v, double* w, const uint8_t* node_fixed, uint32_t flags,
+                             int32_t i_lo, int32_t i_hi, void* stream);
+
 /* ---- K v with an explicit element->DOF table: the fused kernel contract
  *      fused_serial/fused_atomic(edof, ke, scale, v, out) (_kernels_numba.py:146-196).
  *      ALWAYS accumulates into w (caller zeroes it, operator.py:93).

@@ -84,6 +84,8 @@ _SIGS = {
     "tf_build_node_fixed": [_P, _P, _I64, _P, _P],
     "tf_matvec_grid_f32": [_P, _P, _P, _P, _P, _P, _U32, _INT, _P],
     "tf_matvec_grid_f64": [_P, _P, _P, _P, _P, _P, _U32, _INT, _P],
+    "tf_matvec_grid_range_f32": [_P, _P, _P, _P, _P, _P, _U32, ctypes.c_int32, ctypes.c_int32, _P],
+    "tf_matvec_grid_range_f64": [_P, _P, _P, _P, _P, _P, _U32, ctypes.c_int32, ctypes.c_int32, _P],
     "tf_matvec_edof_f32": [_P, _P, _P, _P, _P, _I64, _INT, _P, _P, _INT, _P],
     "tf_matvec_edof_f64": [_P, _P, _P, _P, _P, _I64, _INT, _P, _P, _INT, _P],
     "tf_pass_fixed_f32": [_P, _I64, _P, _P, _P],

@@ -48,6 +48,7 @@ struct Grid {
     int nnx, nny, nnz;        // node counts per axis
     long long n_nodes;
     long long n_elem;
+    int ilo, ihi;             // node x-range whose outputs a launch produces (tile kernel)
 };
 
 inline Grid make_grid(const tf_grid* g)
@@ -57,6 +58,8 @@ inline Grid make_grid(const tf_grid* g)
     r.nnx = g->nelx + 1; r.nny = g->nely + 1; r.nnz = g->nelz + 1;
     r.n_nodes = (long long)r.nnx * r.nny * r.nnz;
     r.n_elem = (long long)g->nelx * g->nely * g->nelz;
+    r.ilo = 0;
+    r.ihi = r.nnx;
     return r;
 }
 

@@ -640,6 +640,25 @@ int tf_matvec_grid_f64(const tf_grid* g, const double* ke, const double* scale,
                                     nullptr, S(stream));
 }
 
+#define TF_MATVEC_RANGE(T, SUF)                                                                   \
+    int tf_matvec_grid_range_##SUF(const tf_grid* g, const T* ke, const T* scale, const T* v, T* w, \
+                                   const uint8_t* node_fixed, uint32_t flags, int32_t i_lo,      \
+                                   int32_t i_hi, void* stream)                                  \
+    {                                                                                             \
+        TF_GRID_CHECK(g);                                                                         \
+        TF_REQUIRE(ke && scale && v && w, "null pointer");                                        \
+        Grid gg = make_grid(g);                                                                   \
+        TF_REQUIRE(0 <= i_lo && i_lo <= i_hi && i_hi <= gg.nnx, "bad node x-range");              \
+        if (i_lo == i_hi) return TF_OK;                                                           \
+        gg.ilo = i_lo;                                                                            \
+        gg.ihi = i_hi;                                                                            \
+        const int rc = launch_grid_tile<T>(gg, ke, scale, v, w, node_fixed, flags, nullptr, S(stream)); \
+        if (rc == TF_ERR_UNSUPPORTED) set_error("node ranges need the parity-block tile kernel"); \
+        return rc;                                                                                \
+    }
+TF_MATVEC_RANGE(float, f32)
+TF_MATVEC_RANGE(double, f64)
+
 int tf_matvec_edof_f32(const int32_t* edof, const float* ke, const float* scale, const float* v,
                        float* w, int64_t n_elem, int mode, const int32_t* color_elems,
                        const int64_t* color_offsets, int n_colors, void* stream)

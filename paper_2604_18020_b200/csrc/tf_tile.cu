@@ -418,12 +418,12 @@ k_grid_tile3(Grid g, int oz, const T* __restrict__ scale, const T* __restrict__ 
 
     const int tx = threadIdx.x, ty = threadIdx.y;
     const int tid = tx + TILE_BX * ty;
-    const int i0 = blockIdx.x * (TILE_BX - 1);
+    const int i0 = g.ilo + blockIdx.x * (TILE_BX - 1);
     const int j0 = blockIdx.y * (TILE_BY - 1);
     const int k0 = blockIdx.z * oz;
     const int ex = i0 - 1 + tx, ey = j0 - 1 + ty;
     const bool col_ok = ex >= 0 && ex < g.nelx && ey >= 0 && ey < g.nely;
-    const bool owner = tx < TILE_BX - 1 && ty < TILE_BY - 1 && (i0 + tx) < g.nnx && (j0 + ty) < g.nny;
+    const bool owner = tx < TILE_BX - 1 && ty < TILE_BY - 1 && (i0 + tx) < g.ihi && (j0 + ty) < g.nny;
     const bool mask_in = (flags & TF_MASK_INPUT) && node_fixed != nullptr;
     const int pn = g.nnx * g.nny;
     const uint8_t* col_fixed = node_fixed ? node_fixed + g.n_nodes : nullptr;
@@ -1236,7 +1236,7 @@ template <typename T>
 TileShape tile_shape(const Grid& g)
 {
     constexpr int TILE_BY = TileDims<T>::BY;
-    const int tx = (g.nnx + TILE_BX - 2) / (TILE_BX - 1);
+    const int tx = (g.ihi - g.ilo + TILE_BX - 2) / (TILE_BX - 1);
     const int ty = (g.nny + TILE_BY - 2) / (TILE_BY - 1);
     const long long cols = (long long)tx * ty;
     const long long slots = tile_slots<T>();
@@ -1287,8 +1287,9 @@ int launch_grid_tile(const Grid& g, const T* ke_host, const T* scale, const T* v
         return TF_ERR_ARG;
     }
     TileShape sh = tile_shape<T>(g);
+    const bool full_range = g.ilo == 0 && g.ihi == g.nnx;  // tile4 has no x-range support
     if constexpr (sizeof(T) == 4) {
-        if (!tile3_forced()) {
+        if (!tile3_forced() && full_range) {
             dim3 block4(T4_TX, T4_TY, 1);
             if (dot_part)
                 k_grid_tile4<true><<<sh.grid, block4, 0, st>>>(g, sh.oz, scale, v, w, node_fixed, flags, dot_part, kb);

@@ -142,6 +142,11 @@ class SlabExchange:
         self.right_idx = torch.as_tensor(part.plane_dofs(lm.nelx), device=device)
 
     def __call__(self, w):
+        return self.finish(w, self.start(w))
+
+    def start(self, w):
+        """Post the interface-plane exchange (needs only the interface columns
+        of w to be final); returns the state finish() completes."""
         import torch
         import torch.distributed as dist
 
@@ -163,9 +168,13 @@ class SlabExchange:
             sr = send_r.cpu() if host else send_r
             ops += [dist.P2POp(dist.isend, sr, p.rank + 1, self.group),
                     dist.P2POp(dist.irecv, recv_r, p.rank + 1, self.group)]
-        if ops:
-            for r in dist.batch_isend_irecv(ops):
-                r.wait()
+        works = dist.batch_isend_irecv(ops) if ops else []
+        return works, send_l, recv_l, send_r, recv_r
+
+    def finish(self, w, state):
+        works, send_l, recv_l, send_r, recv_r = state
+        for r in works:
+            r.wait()
         if recv_l is not None:  # my left plane: left partial first
             w[self.left_idx] = recv_l.to(w.device) + send_l
         if recv_r is not None:  # my right plane: my (left) partial first
@@ -197,8 +206,16 @@ class SlabOperator:
         self.n_apply = 0
 
     def apply(self, x):
-        w = self.local_apply(x)
-        w = self.exchange(w)
+        split = getattr(self.local_apply, "split", None)
+        if split is not None:
+            # interface columns first, exchange in flight while the interior runs
+            w = split(x, None, "boundary")
+            state = self.exchange.start(w)
+            split(x, w, "interior")
+            w = self.exchange.finish(w, state)
+        else:
+            w = self.local_apply(x)
+            w = self.exchange(w)
         if self.fixed.numel():
             w[self.fixed] = x[self.fixed]
         self.n_apply += 1
@@ -321,6 +338,25 @@ def gpu_local_kernels(part: SlabPartition, bcs_local: BoundaryConditions, rho_lo
                   D.ptr(op._scale_dev), D.ptr(x), D.ptr(out), D.ptr(op.dev.node_fixed),
                   _lib.TF_MASK_INPUT, op.grid_variant, D.stream_ptr())
         return out
+
+    nnx = lm.nelx + 1
+    bl = min(31, nnx) if part.has_left else 0          # one tile of interface columns
+    br = min(31, nnx - bl) if part.has_right else 0
+
+    def split(x, out, phase):
+        """phase "boundary": outputs of the interface tiles; "interior": the rest."""
+        if out is None:
+            out = torch.empty_like(x)
+        ranges = [(0, bl), (nnx - br, nnx)] if phase == "boundary" else [(bl, nnx - br)]
+        for lo, hi in ranges:
+            if hi > lo:
+                _lib.call(f"tf_matvec_grid_range_{sfx}", ctypes_ref(op.dev.grid), op.ke.ctypes.data,
+                          D.ptr(op._scale_dev), D.ptr(x), D.ptr(out), D.ptr(op.dev.node_fixed),
+                          _lib.TF_MASK_INPUT, int(lo), int(hi), D.stream_ptr())
+        return out
+
+    if op.grid_kernel == "tile":
+        local_apply.split = split
 
     def local_diag_partial():
         # FP64 partial sums of s_e * Ke[l,l] on this slab (no fixed handling yet)

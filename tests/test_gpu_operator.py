@@ -292,3 +292,28 @@ def test_accumulate_flag_and_edof_contract_module():
     u = kernels.gather(edof, v)
     assert np.array_equal(u, oracle.gather(edof, v))
     assert _rel(kernels.element_energies(edof, ke, v), oracle.element_energies(edof, ke, v)) <= 1e-12
+
+
+@pytest.mark.parametrize("prec", ["fp64", "fp32"])
+def test_node_range_launches_compose_bitwise(prec):
+    """Interface/interior split used by the x-slab overlap: the union of range
+    launches equals the full structured matvec bit for bit."""
+    import torch
+
+    from paper_2604_18020_b200 import _device as D
+    from paper_2604_18020_b200 import _lib
+    from paper_2604_18020_b200.operator import ctypes_ref
+
+    m, edof, bcs, rho, v = seeded_case((90, 13, 11), 31)
+    op = _op(m, edof, bcs, rho, prec)
+    dt = op.precision.dtype
+    x = torch.tensor(v.astype(dt), device="cuda")
+    full = op.apply(x)
+    out = torch.full_like(x, float("nan"))
+    sfx = "f64" if prec == "fp64" else "f32"
+    nnx = m.nelx + 1
+    for lo, hi in ((0, 31), (nnx - 31, nnx), (31, nnx - 31)):
+        _lib.call(f"tf_matvec_grid_range_{sfx}", ctypes_ref(op.dev.grid), op.ke.ctypes.data,
+                  D.ptr(op._scale_dev), D.ptr(x), D.ptr(out), D.ptr(op.dev.node_fixed),
+                  _lib.TF_MASK_INPUT | _lib.TF_PASS_FIXED, lo, hi, D.stream_ptr())
+    assert torch.equal(out, full)

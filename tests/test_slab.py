@@ -43,7 +43,7 @@ def test_partition_covers_mesh_once():
     assert np.all(owned == 1)
 
 
-def _worker(rank, world, port, dims, prec, q):
+def _worker(rank, world, port, dims, prec, q, device="cpu"):
     import torch
     import torch.distributed as dist
 
@@ -81,12 +81,18 @@ def _worker(rank, world, port, dims, prec, q):
             return torch.from_numpy(acc)
 
         tdt = torch.float64 if prec == "fp64" else torch.float32
-        op = SlabOperator(part, lb, local_apply, local_diag_partial, "cpu", tdt)
-        w = op.apply(torch.from_numpy(part.scatter(v).astype(dt)))
+        if device != "cpu":  # product local kernels (interface/interior split launches)
+            from paper_2604_18020_b200.slab import gpu_local_kernels
+
+            _, local_apply, local_diag_partial = gpu_local_kernels(
+                part, lb, part.scatter_elem(rho), SimpParams(3.0), prec)
+            assert getattr(local_apply, "split", None) is not None
+        op = SlabOperator(part, lb, local_apply, local_diag_partial, device, tdt)
+        w = op.apply(torch.from_numpy(part.scatter(v).astype(dt)).to(device))
         d = op.diagonal()
-        b = torch.from_numpy(lb.force.astype(dt))
+        b = torch.from_numpy(lb.force.astype(dt)).to(device)
         x, info = slab_pcg(op, b, d)
-        q.put((rank, part.local_dof_to_global(), w.numpy(), d.numpy(), x.numpy(), info))
+        q.put((rank, part.local_dof_to_global(), w.cpu().numpy(), d.cpu().numpy(), x.cpu().numpy(), info))
     finally:
         dist.destroy_process_group()
 
@@ -94,6 +100,20 @@ def _worker(rank, world, port, dims, prec, q):
 @pytest.mark.parametrize("world,dims,prec", [(2, (10, 4, 3), "fp64"), (3, (13, 3, 4), "fp64"),
                                              (2, (10, 4, 3), "fp32")])
 def test_slab_matvec_diag_and_pcg_match_global(world, dims, prec):
+    _run_slab(world, dims, prec, "cpu")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world,dims,prec", [(2, (130, 6, 5), "fp64"), (3, (100, 5, 4), "fp32"),
+                                             (2, (20, 4, 3), "fp64")])
+def test_slab_gpu_local_kernels_match_global(world, dims, prec):
+    """All ranks share cuda:0 (gloo stages the interface planes through the
+    host); local matvecs are the tile kernel split into interface and interior
+    x-ranges with the exchange posted in between."""
+    _run_slab(world, dims, prec, "cuda:0")
+
+
+def _run_slab(world, dims, prec, device):
     import torch.multiprocessing as mp
 
     import oracle
@@ -102,7 +122,7 @@ def test_slab_matvec_diag_and_pcg_match_global(world, dims, prec):
     ctx = mp.get_context("spawn")
     q = ctx.SimpleQueue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, dims, prec, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, dims, prec, q, device)) for r in range(world)]
     for p in procs:
         p.start()
     res = [q.get() for _ in range(world)]

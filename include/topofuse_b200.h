@@ -188,6 +188,16 @@ int tf_pcg_solve(tf_pcg* h, const void* scale, const void* b, const void* inv_di
                  int has_x0, double rel_tol, int32_t max_iter, int32_t recompute_every,
                  double* history, tf_pcg_report* report);
 int tf_pcg_destroy(tf_pcg* h);
+/* Which device protocol a handle runs (chosen at create from the problem
+ * size; TF_PCG_RESIDENT=0 / TF_PCG_FUSED=0|1 in the environment override):
+ *   TF_PCG_GRAPH        one CUDA graph, 3 kernels per iteration;
+ *   TF_PCG_FUSED_GRAPH  one CUDA graph, direction folded into the matvec (2 per iteration);
+ *   TF_PCG_RESIDENT     one cooperative kernel for the whole solve, owned CG
+ *                       vectors resident in shared memory (tf_pcg_resident.cu). */
+#define TF_PCG_GRAPH 0
+#define TF_PCG_FUSED_GRAPH 1
+#define TF_PCG_RESIDENT 2
+int tf_pcg_protocol(const tf_pcg* h);
 
 /* ---- SIMP glue on the device (simp.py:33-175, element.py:34-45) -------------
  * Densities, sensitivities and filter vectors are FP64, n = n_elem.         */

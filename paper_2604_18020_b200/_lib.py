@@ -106,6 +106,7 @@ _SIGS = {
     "tf_pcg_solve": [_P, _P, _P, _P, _P, _INT, ctypes.c_double, ctypes.c_int32, ctypes.c_int32,
                      _P, _P],
     "tf_pcg_destroy": [_P],
+    "tf_pcg_protocol": [_P],
     "tf_filter_rowsum_f64": [_P, ctypes.c_double, _P, _P],
     "tf_filter_grid_f64": [_P, ctypes.c_double, _P, _P, _P, _INT, _P],
     "tf_project_f64": [_I64, ctypes.c_double, ctypes.c_double, _P, _P, _P, _P],

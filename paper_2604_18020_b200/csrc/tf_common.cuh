@@ -118,4 +118,12 @@ struct CgTileArgs {
     int in_graph;
 };
 
+// Launch plan of the SM-resident PCG (tf_pcg_resident.cu).
+struct ResPlan {
+    dim3 grid;
+    int oz;
+    size_t dyn_smem;
+    long long nblk;
+};
+
 }  // namespace tf

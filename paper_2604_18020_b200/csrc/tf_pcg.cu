@@ -45,6 +45,12 @@ int launch_grid_tile_cg(const Grid& g, const T* ke_host, const T* scale, T* q,
                         cudaStream_t st);
 template <typename T>
 bool launch_grid_tile_supported(const T* ke_host);
+template <typename T>
+bool pcg_resident_plan(const Grid& g, const T* ke_host, ResPlan* plan);
+template <typename T>
+int launch_pcg_resident(const ResPlan& plan, const Grid& g, const T* ke_host, int has_x0, const T* scale,
+                        const T* b, const T* inv, T* x, T* z, T* p0, T* p1, const uint8_t* node_fixed,
+                        double* part, void* bar, CgScalars* sc, cudaStream_t st);
 
 
 
@@ -575,6 +581,10 @@ struct PcgImpl {
     void *x, *r, *p, *q, *b, *inv, *scale;
     void* p2;           // second search-direction buffer (fused protocol)
     int fused;          // structured tile solve with the direction folded into the matvec
+    int resident;       // SM-resident solve: one cooperative launch (tf_pcg_resident.cu)
+    ResPlan rplan;
+    double* part_res;   // 6 partials per resident CTA
+    void* bar;          // resident grid barrier words
     double* part;
     double* part_mv;    // per-CTA p.q partials of the matvec
     unsigned* tickets;
@@ -779,16 +789,30 @@ static int solve_impl(PcgImpl* h, const void* scale, const void* b, const void* 
     init.hist = history;
     *h->sc_host = init;
     TF_CUDA_TRY(cudaMemcpyAsync(h->sc, h->sc_host, sizeof(CgScalars), cudaMemcpyHostToDevice, st));
+    if (h->resident) {
+        int rc = launch_pcg_resident<T>(h->rplan, h->grid, (const T*)h->ke.data(), has_x0, (const T*)h->scale,
+                                        (const T*)h->b, (const T*)h->inv, (T*)h->x, (T*)h->r, (T*)h->p,
+                                        (T*)h->p2, h->node_fixed, h->part_res, h->bar, h->sc, st);
+        if (rc) return rc;
+        TF_CUDA_TRY(cudaMemcpyAsync(h->sc_host, h->sc, sizeof(CgScalars), cudaMemcpyDeviceToHost, st));
+        TF_CUDA_TRY(cudaStreamSynchronize(st));
+    }
     CgP<T> P = params_of<T>(h);
-    if (has_x0) {
+    if (h->resident) {
+        // solved above
+    } else if (has_x0) {
         int rc = enqueue_matvec<T>(h, P.x, P.q, nullptr, st);
         if (rc) return rc;
     }
-    k_init<T><<<h->n_vec_blocks, VEC_BLOCK, 0, st>>>(P, has_x0);
-    TF_CHECK_LAUNCH();
-    TF_CUDA_TRY(cudaMemcpyAsync(h->sc_host, h->sc, sizeof(CgScalars), cudaMemcpyDeviceToHost, st));
-    TF_CUDA_TRY(cudaStreamSynchronize(st));
-    if (!h->sc_host->done && !getenv("TF_PCG_NOGRAPH")) {
+    if (!h->resident) {
+        k_init<T><<<h->n_vec_blocks, VEC_BLOCK, 0, st>>>(P, has_x0);
+        TF_CHECK_LAUNCH();
+        TF_CUDA_TRY(cudaMemcpyAsync(h->sc_host, h->sc, sizeof(CgScalars), cudaMemcpyDeviceToHost, st));
+        TF_CUDA_TRY(cudaStreamSynchronize(st));
+    }
+    if (h->resident) {
+        // done
+    } else if (!h->sc_host->done && !getenv("TF_PCG_NOGRAPH")) {
         TF_CUDA_TRY(cudaGraphLaunch(h->exec, st));
         TF_CUDA_TRY(cudaMemcpyAsync(h->sc_host, h->sc, sizeof(CgScalars), cudaMemcpyDeviceToHost, st));
     } else if (!h->sc_host->done) {
@@ -860,6 +884,9 @@ int tf_pcg_create(tf_pcg** out, const tf_pcg_desc* d, void* stream)
     h->tickets = nullptr;
     h->sc = nullptr;
     h->sc_host = nullptr;
+    h->resident = 0;
+    h->part_res = nullptr;
+    h->bar = nullptr;
     TF_REQUIRE(d->structured || d->edof, "edof required for unstructured problems");
 
     int dev = 0, nsm = 148;
@@ -892,7 +919,31 @@ int tf_pcg_create(tf_pcg** out, const tf_pcg_desc* d, void* stream)
         const bool want = e ? (e[0] == '1') : (d->n_elem <= 100000);
         h->fused = (ok && want) ? 1 : 0;
     }
-    if (h->fused) TF_CUDA_TRY(cudaMalloc(&h->p2, vb));
+    // SM-resident protocol: the whole solve in one cooperative launch whenever
+    // the CG state of the owned DOFs fits in the co-resident CTAs' shared
+    // memory (TF_PCG_RESIDENT=0 disables it)
+    if (d->structured && d->grid_variant == TF_GRID_FAST) {
+        const char* e = getenv("TF_PCG_RESIDENT");
+        if (!(e && e[0] == '0')) {
+            const bool ok = d->precision == 32
+                                ? pcg_resident_plan<float>(h->grid, (const float*)d->ke, &h->rplan)
+                                : pcg_resident_plan<double>(h->grid, (const double*)d->ke, &h->rplan);
+            h->resident = ok ? 1 : 0;
+        }
+    }
+    if (h->resident) {
+        h->fused = 0;
+        TF_CUDA_TRY(cudaMalloc(&h->part_res, sizeof(double) * (6 * h->rplan.nblk + 8)));
+        TF_CUDA_TRY(cudaMalloc(&h->bar, 64));
+        TF_CUDA_TRY(cudaMemset(h->bar, 0, 64));
+    }
+    if (h->fused || h->resident) TF_CUDA_TRY(cudaMalloc(&h->p2, vb));
+    if (h->resident) {
+        // p buffers are read before first written only behind the `first` flag,
+        // but keep them finite for the halo reads of the first iteration
+        TF_CUDA_TRY(cudaMemset(h->p, 0, vb));
+        TF_CUDA_TRY(cudaMemset(h->p2, 0, vb));
+    }
     TF_CUDA_TRY(cudaMalloc(&h->scale, es * d->n_elem));
     const long long npart = (long long)h->n_vec_blocks * 3 + 8;
     TF_CUDA_TRY(cudaMalloc(&h->part, sizeof(double) * npart));
@@ -901,7 +952,7 @@ int tf_pcg_create(tf_pcg** out, const tf_pcg_desc* d, void* stream)
     TF_CUDA_TRY(cudaMemset(h->tickets, 0, sizeof(unsigned) * 8));
     TF_CUDA_TRY(cudaMalloc(&h->sc, sizeof(CgScalars)));
     TF_CUDA_TRY(cudaMallocHost(&h->sc_host, sizeof(CgScalars)));
-    int rc = d->precision == 32 ? build_graph<float>(h) : build_graph<double>(h);
+    int rc = h->resident ? TF_OK : (d->precision == 32 ? build_graph<float>(h) : build_graph<double>(h));
     if (rc) {
         tf_pcg_destroy(reinterpret_cast<tf_pcg*>(h));
         return rc;
@@ -923,13 +974,21 @@ int tf_pcg_solve(tf_pcg* hh, const void* scale, const void* b, const void* inv_d
                                               recompute_every, history, report);
 }
 
+int tf_pcg_protocol(const tf_pcg* hh)
+{
+    const PcgImpl* h = reinterpret_cast<const PcgImpl*>(hh);
+    if (!h) return -1;
+    return h->resident ? TF_PCG_RESIDENT : (h->fused ? TF_PCG_FUSED_GRAPH : TF_PCG_GRAPH);
+}
+
 int tf_pcg_destroy(tf_pcg* hh)
 {
     PcgImpl* h = reinterpret_cast<PcgImpl*>(hh);
     if (!h) return TF_OK;
     if (h->exec) cudaGraphExecDestroy(h->exec);
     if (h->graph) cudaGraphDestroy(h->graph);
-    void* bufs[] = {h->x, h->r, h->p, h->q, h->b, h->inv, h->scale, h->p2, h->part, h->part_mv, h->tickets, h->sc};
+    void* bufs[] = {h->x, h->r, h->p, h->q, h->b, h->inv, h->scale, h->p2, h->part, h->part_mv, h->tickets, h->sc,
+                    h->part_res, h->bar};
     for (void* p : bufs)
         if (p) cudaFree(p);
     if (h->sc_host) cudaFreeHost(h->sc_host);

@@ -1,0 +1,622 @@
+// SM-resident Jacobi-PCG: the whole solve of reference solver.py:57-147 as ONE
+// cooperative kernel launch, for structured grids whose CG state fits in the
+// shared memory of the co-resident CTAs.
+//
+// Ownership.  The grid is the production tile decomposition (tf_tile.cu): CTA
+// (bx, by, bz) owns node columns [i0, i0+31) x [j0, j0+BY-1) over node planes
+// [k0, k0+oz); thread (tx, ty) owns one node column of it.  The owned DOFs'
+// CG vectors x, r, D^-1, p and q live in the CTA's shared memory for the
+// whole solve; they never round-trip HBM.  Only two vectors are global: z
+// (= r D^-1 of the last update) and p (ping-pong), which neighbouring CTAs
+// read for their halo nodes -- both stay L2-resident at the sizes that fit.
+//
+// One iteration = two grid barriers (three on a true-residual refresh):
+//   A. stage node planes of p_k = z + beta p_{k-1} (computed on the fly from
+//      the global z and p_{k-1}; owners publish p_k), q = A p_k with the
+//      parity-block element algebra, masked input and pass-through, per-CTA
+//      p.q partial                                                --- barrier
+//   B. every CTA reduces the p.q partials in the same fixed order -> alpha,
+//      breakdown / divergence; x += alpha p, r -= alpha q (or, every
+//      `recompute` iterations, publish x --- barrier --- r = b - A x),
+//      z = r D^-1 (published), per-CTA r.r / r.z partials         --- barrier
+//   C. every CTA reduces them -> rel, convergence, max_iter, beta.
+// Every CTA takes the same decisions from bitwise-identical reductions, so
+// the loop exits everywhere at the same iteration; CTA 0 records the report.
+// Scalar rounding is the numpy semantics of tf_pcg.cu (FP32 dots rounded to
+// float32, alpha/beta applied in the working dtype, no FMA contraction in
+// vector updates).
+
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+#include <type_traits>
+
+#include "tf_common.cuh"
+#include "tf_walsh.cuh"
+
+namespace tf {
+
+struct ResBar {
+    unsigned count;
+    unsigned gen;
+};
+
+template <typename T>
+struct ResArgs {
+    Grid g;
+    int oz;
+    int has_x0;
+    const T* scale;
+    const T* b;
+    const T* inv;
+    T* x;        // in: x0 (has_x0); out: the solution (every DOF written by its owner)
+    T* z;        // z = r * D^-1 of the last update (halo source for p)
+    T* pbuf[2];  // p_k in pbuf[k & 1]
+    const uint8_t* node_fixed;
+    double* part;  // 6 per CTA: init [3n), phase A [n), phase B [2n) -- a region is
+                   // rewritten only after a barrier every reader of it has passed
+    ResBar* bar;
+    CgScalars* sc;  // tol / max_iter / recompute / hist in; report out
+};
+
+// Grid-wide barrier of a cooperatively launched (co-resident) grid: one
+// arriving thread per CTA, generation counter read before arriving.
+__device__ __forceinline__ void res_grid_sync(ResBar* bar, unsigned nblk)
+{
+    __syncthreads();
+    if (threadIdx.x == 0 && threadIdx.y == 0) {
+        volatile unsigned* vg = &bar->gen;
+        const unsigned g = *vg;
+        __threadfence();
+        if (atomicAdd(&bar->count, 1u) == nblk - 1) {
+            bar->count = 0u;
+            __threadfence();
+            atomicAdd(&bar->gen, 1u);
+        } else {
+            while (*vg == g) {
+            }
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+// Deterministic block sum of K values; every thread returns the same totals.
+template <int K, int NT>
+__device__ __forceinline__ void res_block_sum(double (&v)[K], double* sh /* [K][NT/32] */, int tid)
+{
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v[k] += __shfl_down_sync(0xffffffffu, v[k], o);
+    }
+    if ((tid & 31) == 0) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) sh[k * (NT / 32) + (tid >> 5)] = v[k];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        double s = 0.0;
+#pragma unroll
+        for (int i = 0; i < NT / 32; ++i) s += sh[k * (NT / 32) + i];
+        v[k] = s;
+    }
+    __syncthreads();
+}
+
+// Sum partial k (k < K, stride K per CTA) of all CTAs in a fixed order;
+// identical in every CTA.
+template <int K, int NT>
+__device__ __forceinline__ void res_reduce_all(const double* part, int nblk, double (&tot)[K], double* sh,
+                                               int tid)
+{
+#pragma unroll
+    for (int k = 0; k < K; ++k) tot[k] = 0.0;
+    for (int i = tid; i < nblk; i += NT) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) tot[k] += __ldcg(part + K * i + k);
+    }
+    res_block_sum<K, NT>(tot, sh, tid);
+}
+
+// The CTA's staging slots of a node plane and its owned-column bookkeeping.
+template <typename T>
+struct ResTile {
+    static constexpr int BY = TileDims<T>::BY, NT = TileDims<T>::NT;
+    static constexpr int PW = StageSlots<T>::PW, PN = StageSlots<T>::PN, NS = StageSlots<T>::N;
+};
+
+#ifndef TF_RES_MINB32
+#define TF_RES_MINB32 2
+#endif
+template <typename T>
+__global__ void __launch_bounds__(TileDims<T>::NT, sizeof(T) == 4 ? TF_RES_MINB32 : 2)
+k_pcg_resident(const __grid_constant__ ResArgs<T> A, const __grid_constant__ KhatBlocks<T> kb)
+{
+    using RT = ResTile<T>;
+    constexpr int BY = RT::BY, NT = RT::NT, PW = RT::PW, PN = RT::PN, NS = RT::NS;
+    constexpr bool F32 = sizeof(T) == 4;
+    __shared__ __align__(16) T plane[2][PN];
+    __shared__ T Y[3][NT];
+    __shared__ double shr[3 * (NT / 32)];
+    extern __shared__ __align__(16) unsigned char res_dyn[];
+
+    const Grid& g = A.g;
+    const int oz = A.oz;
+    const int tx = threadIdx.x, ty = threadIdx.y;
+    const int tid = tx + TILE_BX * ty;
+    const int bid = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+    const unsigned nblk = gridDim.x * gridDim.y * gridDim.z;
+    const int i0 = blockIdx.x * (TILE_BX - 1);
+    const int j0 = blockIdx.y * (BY - 1);
+    const int k0 = blockIdx.z * oz;
+    const int kend = min(k0 + oz, g.nnz);  // owned planes [k0, kend)
+    const int ex = i0 - 1 + tx, ey = j0 - 1 + ty;
+    const bool col_ok = ex >= 0 && ex < g.nelx && ey >= 0 && ey < g.nely;
+    const bool owner = tx < TILE_BX - 1 && ty < BY - 1 && (i0 + tx) < g.nnx && (j0 + ty) < g.nny;
+    const int n_own = owner ? kend - k0 : 0;
+    const int pn = g.nnx * g.nny, pn3 = 3 * pn;
+    const uint8_t* nf = A.node_fixed;
+    const uint8_t* col_or = nf ? nf + g.n_nodes : nullptr;
+    const uint8_t* col_and = nf ? col_or + pn : nullptr;
+    const int own_node0 = (i0 + tx) + g.nnx * (j0 + ty);
+    double* part_init = A.part;
+    double* part_a = A.part + 3 * nblk;
+    double* part_b = A.part + 4 * nblk;
+
+    // owned vectors in shared memory: own(v, kk, c) for this thread
+    T* own = reinterpret_cast<T*>(res_dyn);
+    enum { VX = 0, VR = 1, VI = 2, VP = 3, VQ = 4 };
+    auto oidx = [&](int v, int kk, int c, int t) { return ((v * oz + kk) * 3 + c) * NT + t; };
+
+    // fixed bits of the owned DOFs, 3 per owned plane (oz <= 10)
+    unsigned long long ofix = 0ull;
+    if (nf) {
+        for (int kk = 0; kk < n_own; ++kk)
+            ofix |= (unsigned long long)(nf[own_node0 + (k0 + kk) * pn] & 7u) << (3 * kk);
+    }
+
+    // staging slots
+    int s_off[NS], s_own[NS];
+    unsigned okbits = 0u, mskbits = 0u, allfix = 0u;
+#pragma unroll
+    for (int q = 0; q < NS; ++q) {
+        const int idx = tid + q * NT;
+        const int r = idx / PW, f = idx - r * PW;
+        const int ii = i0 - 1 + f / 3, jj = j0 - 1 + r, c = f % 3;
+        const bool ok = idx < PN && ii >= 0 && ii < g.nnx && jj >= 0 && jj < g.nny;
+        const int node = ok ? ii + g.nnx * jj : 0;
+        s_off[q] = 3 * node + c;
+        s_own[q] = -1;
+        if (ok) {
+            okbits |= 1u << q;
+            if (nf) {
+                if ((col_and[node] >> c) & 1u) allfix |= 1u << q;
+                else if ((col_or[node] >> c) & 1u) mskbits |= 1u << q;
+            }
+            if (ii >= i0 && ii < i0 + TILE_BX - 1 && jj >= j0 && jj < j0 + BY - 1)
+                s_own[q] = c * NT + (ii - i0) + TILE_BX * (jj - j0);  // + kk*3*NT + VP*oz*3*NT
+        }
+    }
+    const int pofs = ty * PW + 3 * tx;
+    auto pv_ = [&](const T* buf, int ox, int oy, int c) -> T { return buf[pofs + oy * PW + 3 * ox + c]; };
+    const int el_col = ex + g.nelx * ey, el_plane = g.nelx * g.nely;
+    auto scale_at = [&](int ez) -> T {
+        return (col_ok && ez >= 0 && ez < g.nelz) ? ld_nc(A.scale + el_col + el_plane * ez) : T(0);
+    };
+
+    // One structured matvec over this CTA's chunk.  PDIR: the input is
+    // p_k = z + beta p_{k-1} (first: p_1 = z_0), owners publish p_k to `pnew`
+    // and to own(VP); otherwise the input is the global vector `src`.  The
+    // result of every owned DOF (pass-through on constrained DOFs) goes to
+    // own(VQ); returns this thread's p.q (PDIR).
+    auto tile_pass = [&](auto pdir_tag, bool first, T be, const T* src, const T* pold, T* pnew) -> double {
+        constexpr bool pdir = decltype(pdir_tag)::value;
+        T pa[NS], pb[NS];
+        auto fetch = [&](int kz) {
+            const bool zok = kz >= 0 && kz < g.nnz;
+            const int base = min(max(kz, 0), g.nnz - 1) * pn3;
+#pragma unroll
+            for (int q = 0; q < NS; ++q) {
+                const bool take = zok && ((okbits >> q) & 1u);
+                const int d = base + s_off[q];
+                pa[q] = take ? __ldcg(src + d) : T(0);
+                pb[q] = (pdir && take && !first) ? __ldcg(pold + d) : T(0);
+            }
+        };
+        auto commit = [&](int kz, T* buf) {
+            const bool zok = kz >= 0 && kz < g.nnz;
+            const bool wr = pdir && zok && kz >= k0 && kz < kend;
+            const int base = min(max(kz, 0), g.nnz - 1) * pn3;
+#pragma unroll
+            for (int q = 0; q < NS; ++q) {
+                const int idx = tid + q * NT;
+                if (q < NS - 1 || idx < PN) {
+                    const bool ok = zok && ((okbits >> q) & 1u);
+                    T pv = pa[q];
+                    if (pdir && !first) pv = add_rn(pa[q], mul_rn(be, pb[q]));
+                    if (!ok) pv = T(0);
+                    if (wr && s_own[q] >= 0) {
+                        pnew[base + s_off[q]] = pv;
+                        own[(VP * oz + (kz - k0)) * 3 * NT + s_own[q]] = pv;
+                    }
+                    bool fixed = (allfix >> q) & 1u;
+                    if (!fixed && ((mskbits >> q) & 1u) && ok)  // rare: z-varying constraint
+                        fixed = (nf[kz * pn + s_off[q] / 3] >> (s_off[q] % 3)) & 1u;
+                    buf[idx] = fixed ? T(0) : pv;
+                }
+            }
+        };
+
+        const int n_layers = kend - k0 + 1;
+        T* b_cur = plane[0];
+        T* b_top = plane[1];
+        fetch(k0 - 1);
+        commit(k0 - 1, b_cur);
+        fetch(k0);
+        commit(k0, b_top);
+        fetch(k0 + 1);
+        __syncthreads();
+        T XYb[3][4];
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+            face_fwd(pv_(b_cur, 0, 0, c), pv_(b_cur, 1, 0, c), pv_(b_cur, 0, 1, c), pv_(b_cur, 1, 1, c), XYb[c]);
+        T Gt[3][4];
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) Gt[c][q] = T(0);
+        T s_cur = scale_at(k0 - 1);
+        double dot = 0.0;
+
+        for (int L = 0; L < n_layers; ++L) {
+            const int ez = k0 - 1 + L;
+            if (L >= 1) {
+                // plane ez+1 into the buffer that held plane ez-1 (read before (B) of layer L-1)
+                commit(ez + 1, b_top);
+                if (L + 1 < n_layers) fetch(ez + 2);
+            }
+            __syncthreads();  // (A)
+            const T s_next = scale_at(ez + 1);
+            T h[3][8];
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                T XYt[4];
+                face_fwd(pv_(b_top, 0, 0, c), pv_(b_top, 1, 0, c), pv_(b_top, 0, 1, c), pv_(b_top, 1, 1, c), XYt);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    h[c][q] = XYb[c][q] + XYt[q];
+                    h[c][q + 4] = XYt[q] - XYb[c][q];
+                    XYb[c][q] = XYt[q];
+                }
+            }
+#pragma unroll
+            for (int c = 0; c < 3; ++c)
+#pragma unroll
+                for (int m = 1; m < 8; ++m) h[c][m] *= s_cur;
+            T gm[3][8];
+#pragma unroll
+            for (int c = 0; c < 3; ++c) gm[c][0] = T(0);
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    const int m = q ^ (1 << c);
+                    if (m == 0) continue;
+                    T acc = T(0);
+#pragma unroll
+                    for (int d = 0; d < 3; ++d) {
+                        const int n = q ^ (1 << d);
+                        if (n == 0) continue;
+                        acc = fma(kb.b[q][c][d], h[d][n], acc);
+                    }
+                    gm[c][m] = acc;
+                }
+            T corner[3][4];
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                T H[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    H[q] = Gt[c][q] + (gm[c][q] - gm[c][q + 4]);
+                    Gt[c][q] = gm[c][q] + gm[c][q + 4];
+                }
+                face_inv(H, corner[c]);
+            }
+            T xr[2][3];
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                xr[0][c] = corner[c][1] + __shfl_down_sync(0xffffffffu, corner[c][0], 1);
+                xr[1][c] = corner[c][3] + __shfl_down_sync(0xffffffffu, corner[c][2], 1);
+                Y[c][tid] = xr[0][c];
+            }
+            __syncthreads();  // (B)
+            if (L >= 1 && owner) {
+                const int kk = ez - k0;
+                const unsigned fb = (unsigned)(ofix >> (3 * kk)) & 7u;
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    T acc = xr[1][c] + Y[c][tid + TILE_BX];
+                    const bool fx = (fb >> c) & 1u;
+                    if (pdir) {
+                        const T p = own[oidx(VP, kk, c, tid)];
+                        if (fx) acc = p;  // pass-through of the unmasked input
+                        dot += (double)p * (double)acc;
+                    } else if (fx) {
+                        acc = own[oidx(VX, kk, c, tid)];
+                    }
+                    own[oidx(VQ, kk, c, tid)] = acc;
+                }
+            }
+            s_cur = s_next;
+            T* t = b_cur;
+            b_cur = b_top;
+            b_top = t;
+        }
+        return dot;
+    };
+
+    constexpr std::integral_constant<bool, true> PDIR{};
+    constexpr std::integral_constant<bool, false> RAW{};
+
+    // ---- init (solver.py:72-103) -------------------------------------------------
+    for (int kk = 0; kk < n_own; ++kk)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            const int d = 3 * (own_node0 + (k0 + kk) * pn) + c;
+            own[oidx(VI, kk, c, tid)] = ld_nc(A.inv + d);
+            own[oidx(VX, kk, c, tid)] = A.has_x0 ? A.x[d] : T(0);
+        }
+    __syncthreads();
+    if (A.has_x0) tile_pass(RAW, false, T(0), A.x, nullptr, nullptr);  // own(VQ) = A x0
+    double tot[3];
+    {
+        double v[3] = {0.0, 0.0, 0.0};
+        for (int kk = 0; kk < n_own; ++kk)
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                const int d = 3 * (own_node0 + (k0 + kk) * pn) + c;
+                const T bb = ld_nc(A.b + d);
+                const T r = A.has_x0 ? sub_rn(bb, own[oidx(VQ, kk, c, tid)]) : bb;
+                const T z = mul_rn(r, own[oidx(VI, kk, c, tid)]);
+                own[oidx(VR, kk, c, tid)] = r;
+                A.z[d] = z;
+                v[0] += (double)bb * (double)bb;
+                v[1] += (double)r * (double)r;
+                v[2] += (double)r * (double)z;
+            }
+        res_block_sum<3, NT>(v, shr, tid);
+        if (tid == 0) {
+            part_init[3 * bid] = v[0];
+            part_init[3 * bid + 1] = v[1];
+            part_init[3 * bid + 2] = v[2];
+        }
+        res_grid_sync(A.bar, nblk);
+        res_reduce_all<3, NT>(part_init, (int)nblk, tot, shr, tid);
+    }
+    CgScalars* sc = A.sc;
+    const bool lead = bid == 0 && tid == 0;
+    const double tol = sc->tol;
+    const int max_iter = sc->max_iter, recompute = sc->recompute;
+    double* hist = sc->hist;
+    const double bnorm = cg_sqrt(cg_round(tot[0], F32), F32);
+    int it = 0, term = TERM_MAX_ITER, matvecs = A.has_x0 ? 1 : 0;
+    double rel = 0.0;
+    if (bnorm == 0.0) {  // zero right-hand side (solver.py:72-85): x = 0, converged
+        if (lead) {
+            sc->bnorm = 0.0;
+            sc->zero_rhs = 1;
+            sc->done = 1;
+            sc->term = TERM_CONVERGED;
+            sc->it = 0;
+            sc->matvecs = 0;
+            sc->rel = 0.0;
+            if (hist) hist[0] = 0.0;
+        }
+        return;
+    }
+    double rz = cg_round(tot[2], F32);
+    rel = cg_sqrt(cg_round(tot[1], F32), F32) / bnorm;
+    if (lead && hist) hist[0] = rel;
+    bool done = rel <= tol;
+    if (done) term = TERM_CONVERGED;
+    double beta = 0.0;
+
+    // ---- iterations (solver.py:104-137) --------------------------------------------
+    while (!done) {
+        ++it;
+        // A. q = A p_it, fused p.q
+        {
+            double v[1] = {tile_pass(PDIR, it == 1, (T)beta, A.z, A.pbuf[(it - 1) & 1], A.pbuf[it & 1])};
+            ++matvecs;
+            res_block_sum<1, NT>(v, shr, tid);
+            if (tid == 0) part_a[bid] = v[0];
+            res_grid_sync(A.bar, nblk);
+            double t1[1];
+            res_reduce_all<1, NT>(part_a, (int)nblk, t1, shr, tid);
+            tot[0] = t1[0];
+        }
+        // B. alpha, x, r, z
+        const double pq = cg_round(tot[0], F32);
+        if (!isfinite(pq) || !isfinite(rz)) {
+            term = TERM_DIVERGED;
+            break;
+        }
+        if (pq <= 0.0) {
+            term = TERM_BREAKDOWN;
+            break;
+        }
+        const double alpha = rz / pq;
+        const T a = (T)alpha;
+        const bool refresh = recompute > 0 && it % recompute == 0;
+        __syncthreads();  // grid-sync tail: all own(VP/VQ) writes of the pass are visible
+        for (int kk = 0; kk < n_own; ++kk)
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                const int o = oidx(VX, kk, c, tid);
+                const T xn = add_rn(own[o], mul_rn(a, own[oidx(VP, kk, c, tid)]));
+                own[o] = xn;
+                if (refresh) A.x[3 * (own_node0 + (k0 + kk) * pn) + c] = xn;
+            }
+        if (refresh) {
+            res_grid_sync(A.bar, nblk);  // x published
+            tile_pass(RAW, false, T(0), A.x, nullptr, nullptr);  // own(VQ) = A x
+            ++matvecs;
+        }
+        {
+            double v[2] = {0.0, 0.0};
+            for (int kk = 0; kk < n_own; ++kk)
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    const int d = 3 * (own_node0 + (k0 + kk) * pn) + c;
+                    const int orr = oidx(VR, kk, c, tid);
+                    const T q = own[oidx(VQ, kk, c, tid)];
+                    const T r = refresh ? sub_rn(ld_nc(A.b + d), q) : sub_rn(own[orr], mul_rn(a, q));
+                    own[orr] = r;
+                    const T z = mul_rn(r, own[oidx(VI, kk, c, tid)]);
+                    A.z[d] = z;
+                    v[0] += (double)r * (double)r;
+                    v[1] += (double)r * (double)z;
+                }
+            res_block_sum<2, NT>(v, shr, tid);
+            if (tid == 0) {
+                part_b[2 * bid] = v[0];
+                part_b[2 * bid + 1] = v[1];
+            }
+            res_grid_sync(A.bar, nblk);
+            double t2[2];
+            res_reduce_all<2, NT>(part_b, (int)nblk, t2, shr, tid);
+            tot[0] = t2[0];
+            tot[1] = t2[1];
+        }
+        // C. decisions
+        const double rn = cg_sqrt(cg_round(tot[0], F32), F32);
+        if (!isfinite(rn)) {
+            term = TERM_DIVERGED;
+            break;
+        }
+        rel = rn / bnorm;
+        if (lead && hist) hist[it] = rel;
+        if (rel <= tol) {
+            term = TERM_CONVERGED;
+            break;
+        }
+        const double rz_new = cg_round(tot[1], F32);
+        beta = rz_new / rz;
+        rz = rz_new;
+        if (it >= max_iter) {
+            term = TERM_MAX_ITER;
+            break;
+        }
+    }
+
+    // solution: every DOF written once by its owner
+    for (int kk = 0; kk < n_own; ++kk)
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+            A.x[3 * (own_node0 + (k0 + kk) * pn) + c] = own[oidx(VX, kk, c, tid)];
+    if (lead) {
+        sc->bnorm = bnorm;
+        sc->zero_rhs = 0;
+        sc->done = 1;
+        sc->term = term;
+        sc->it = it;
+        sc->matvecs = matvecs;
+        sc->rel = rel;
+        sc->rz = rz;
+    }
+}
+
+// ---- host ------------------------------------------------------------------------
+
+template <typename T>
+static size_t res_dyn_bytes(int oz)
+{
+    return (size_t)5 * oz * 3 * TileDims<T>::NT * sizeof(T);
+}
+
+// Chooses the z-chunk height for a co-resident grid (smallest chunk whose
+// grid fits one wave with its shared-memory state); false when none fits.
+template <typename T>
+bool pcg_resident_plan(const Grid& g, const T* ke_host, ResPlan* plan)
+{
+    KhatBlocks<T> kb;
+    if (!khat_blocks<T>(ke_host, &kb)) return false;
+    if (3 * g.n_nodes >= (1LL << 31)) return false;
+    constexpr int BY = TileDims<T>::BY, NT = TileDims<T>::NT;
+    int dev = 0, nsm = 148, smem_optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    const int tx = (g.nnx + TILE_BX - 2) / (TILE_BX - 1);
+    const int ty = (g.nny + BY - 2) / (BY - 1);
+    const long long cols = (long long)tx * ty;
+    const char* e = getenv("TF_PCG_RES_OZ");
+    const int oz_force = e ? atoi(e) : 0;
+    for (int oz = 2; oz <= std::min(g.nnz, 10); ++oz) {
+        if (oz_force > 0 && oz != oz_force) continue;
+        const size_t dyn = res_dyn_bytes<T>(oz);
+        if ((long long)dyn + 16384 > smem_optin) break;
+        if (cudaFuncSetAttribute(k_pcg_resident<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn) !=
+            cudaSuccess) {
+            cudaGetLastError();
+            return false;
+        }
+        int per_sm = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pcg_resident<T>, NT, dyn) != cudaSuccess) {
+            cudaGetLastError();
+            return false;
+        }
+        const long long tz = (g.nnz + oz - 1) / oz;
+        if (per_sm > 0 && cols * tz <= (long long)per_sm * nsm) {
+            plan->grid = dim3(tx, ty, (unsigned)tz);
+            plan->oz = oz;
+            plan->dyn_smem = dyn;
+            plan->nblk = cols * tz;
+            return true;
+        }
+    }
+    return false;
+}
+
+template <typename T>
+int launch_pcg_resident(const ResPlan& plan, const Grid& g, const T* ke_host, int has_x0, const T* scale,
+                        const T* b, const T* inv, T* x, T* z, T* p0, T* p1, const uint8_t* node_fixed,
+                        double* part, void* bar, CgScalars* sc, cudaStream_t st)
+{
+    KhatBlocks<T> kb;
+    if (!khat_blocks<T>(ke_host, &kb)) return TF_ERR_UNSUPPORTED;
+    ResArgs<T> a;
+    a.g = g;
+    a.oz = plan.oz;
+    a.has_x0 = has_x0;
+    a.scale = scale;
+    a.b = b;
+    a.inv = inv;
+    a.x = x;
+    a.z = z;
+    a.pbuf[0] = p0;
+    a.pbuf[1] = p1;
+    a.node_fixed = node_fixed;
+    a.part = part;
+    a.bar = static_cast<ResBar*>(bar);
+    a.sc = sc;
+    TF_CUDA_TRY(cudaMemsetAsync(bar, 0, sizeof(ResBar), st));
+    void* args[] = {&a, &kb};
+    dim3 block(TILE_BX, TileDims<T>::BY, 1);
+    TF_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)k_pcg_resident<T>, plan.grid, block, args,
+                                            plan.dyn_smem, st));
+    return TF_OK;
+}
+
+template bool pcg_resident_plan<float>(const Grid&, const float*, ResPlan*);
+template bool pcg_resident_plan<double>(const Grid&, const double*, ResPlan*);
+template int launch_pcg_resident<float>(const ResPlan&, const Grid&, const float*, int, const float*,
+                                        const float*, const float*, float*, float*, float*, float*,
+                                        const uint8_t*, double*, void*, CgScalars*, cudaStream_t);
+template int launch_pcg_resident<double>(const ResPlan&, const Grid&, const double*, int, const double*,
+                                         const double*, const double*, double*, double*, double*, double*,
+                                         const uint8_t*, double*, void*, CgScalars*, cudaStream_t);
+
+}  // namespace tf

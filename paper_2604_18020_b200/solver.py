@@ -12,6 +12,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import os
 import time
 from dataclasses import dataclass, replace
 
@@ -79,7 +80,9 @@ def pcg(apply_op, b, diag, config: CgConfig = CgConfig(), x0=None):
 def _pcg_handle(op: MatFreeOperator):
     """One graph-captured PCG per (device problem, precision, kernel variant)."""
     dev = op.dev
-    key = (op.precision.tag, op.grid_variant, op.variant == "fused" and op.structured)
+    # the protocol overrides are read at handle creation: part of the key
+    key = (op.precision.tag, op.grid_variant, op.variant == "fused" and op.structured,
+           os.environ.get("TF_PCG_RESIDENT"), os.environ.get("TF_PCG_FUSED"))
     h = dev.pcg_handles.get(key)
     if h is not None:
         return h
@@ -100,6 +103,17 @@ def _pcg_handle(op: MatFreeOperator):
     _lib.call("tf_pcg_create", ctypes.byref(out), ctypes.byref(desc), D.stream_ptr())
     dev.pcg_handles[key] = out
     return out
+
+
+PCG_PROTOCOLS = ("graph", "fused_graph", "resident")
+
+
+def pcg_protocol(op: MatFreeOperator) -> str:
+    """Device protocol of op's PCG handle (include/topofuse_b200.h tf_pcg_protocol):
+    "resident" = the whole solve in one cooperative kernel with the owned CG
+    vectors in shared memory; "fused_graph"/"graph" = one CUDA graph of 2/3
+    kernels per iteration."""
+    return PCG_PROTOCOLS[_lib.load().tf_pcg_protocol(_pcg_handle(op))]
 
 
 def device_pcg(op: MatFreeOperator, b, diag, config: CgConfig = CgConfig(), x0=None,

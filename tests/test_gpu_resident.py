@@ -1,0 +1,131 @@
+"""SM-resident PCG (tf_pcg_resident.cu): the whole solve in one cooperative
+kernel.  Checked against the oracle's restatement of the reference recurrence
+(solver.py:57-147) and against the graph protocols on the same inputs.
+
+Bars (north star): iteration counts within +-2 % (min 2), same termination
+class, solution within 1e-6 of max|x| in FP64; FP32 within the reference's
+own FP32/FP64 spread.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _problem(name, scale, prec, rho_kind, seed=5):
+    from paper_2604_18020_b200 import MatFreeOperator, SimpParams, build_edof, make_preset
+
+    pb = make_preset(name, scale)
+    m = pb.mesh
+    rho = (np.full(m.n_elem, 0.5) if rho_kind == "half"
+           else np.random.default_rng(seed).uniform(0.05, 1.0, m.n_elem))
+    edof = build_edof(m)
+    op = MatFreeOperator(m, edof, pb.bcs, rho, SimpParams(3.0), prec)
+    return pb, edof, op
+
+
+def _oracle_solve(op, edof, bcs, b, x0=None, **cfg):
+    import oracle
+
+    n = op.n_dof
+    A = lambda x: oracle.apply(edof, op.ke, op.scale, x, bcs.fixed_dofs, n)
+    d = oracle.diagonal(edof, op.ke, op.scale, bcs.fixed_dofs, n)
+    return oracle.pcg(A, b.astype(op.precision.dtype), d, x0=x0, **cfg)
+
+
+@pytest.mark.parametrize("name,scale", [("cantilever", 0.2), ("cantilever", 0.4), ("mbb", 0.2),
+                                        ("bridge", 0.2), ("torsion", 0.2)])
+@pytest.mark.parametrize("rho_kind", ["half", "random"])
+def test_resident_fp64_matches_oracle(name, scale, rho_kind):
+    from paper_2604_18020_b200 import CgConfig, pcg
+    from paper_2604_18020_b200.solver import pcg_protocol
+
+    pb, edof, op = _problem(name, scale, "fp64", rho_kind)
+    assert pcg_protocol(op) == "resident"
+    x, rep = pcg(op, pb.bcs.force, op.diagonal(), CgConfig())
+    xr, info = _oracle_solve(op, edof, pb.bcs, pb.bcs.force)
+    assert rep.termination == info["termination"]
+    assert abs(rep.iterations - info["iterations"]) <= max(2, 0.02 * info["iterations"])
+    assert rep.matvecs == rep.iterations + rep.iterations // 50
+    assert np.abs(x - xr).max() <= 1e-6 * np.abs(xr).max()
+    n = min(len(rep.residual_history), len(info["history"]), 20)
+    np.testing.assert_allclose(rep.residual_history[:n], info["history"][:n], rtol=1e-6)
+
+
+@pytest.mark.parametrize("prec", ["fp64", "fp32"])
+@pytest.mark.parametrize("name,scale", [("cantilever", 0.2), ("mbb", 0.2), ("torsion", 0.2)])
+def test_resident_matches_graph_protocol(prec, name, scale, monkeypatch):
+    from paper_2604_18020_b200 import CgConfig, pcg
+    from paper_2604_18020_b200.solver import pcg_protocol
+
+    pb, edof, op = _problem(name, scale, prec, "random")
+    d = op.diagonal()
+    b = pb.bcs.force.astype(op.precision.dtype)
+    x1, r1 = pcg(op, b, d, CgConfig())
+    monkeypatch.setenv("TF_PCG_RESIDENT", "0")
+    assert pcg_protocol(op) != "resident"
+    x2, r2 = pcg(op, b, d, CgConfig())
+    assert r1.termination == r2.termination
+    assert abs(r1.iterations - r2.iterations) <= max(2, 0.02 * r2.iterations)
+    tol = 1e-6 if prec == "fp64" else 2e-3
+    assert np.abs(x1 - x2).max() <= tol * np.abs(x2).max()
+
+
+def test_resident_warm_start_refresh_cap_and_zero_rhs():
+    from paper_2604_18020_b200 import CgConfig, pcg
+
+    pb, edof, op = _problem("cantilever", 0.2, "fp64", "random")
+    d = op.diagonal()
+    b = pb.bcs.force
+    # short refresh period and a cap: exercises r = b - A x inside the kernel
+    cfg = dict(rel_tol=1e-5, max_iter=37, recompute_every=5)
+    x, rep = pcg(op, b, d, CgConfig(**cfg))
+    xr, info = _oracle_solve(op, edof, pb.bcs, b, **cfg)
+    assert rep.termination == "max_iter" == info["termination"] and rep.iterations == 37
+    assert rep.matvecs == 37 + 37 // 5
+    assert np.abs(x - xr).max() <= 1e-8 * np.abs(xr).max()
+    # warm start from a perturbed solution (one A x0 before the loop)
+    x0 = x + 1e-3 * np.random.default_rng(1).standard_normal(x.size) * np.abs(x).max()
+    x0[pb.bcs.fixed_dofs] = 0.0
+    xw, rw = pcg(op, b, d, CgConfig(), x0=x0)
+    xwr, iw = _oracle_solve(op, edof, pb.bcs, b, x0=x0)
+    assert rw.termination == iw["termination"]
+    assert abs(rw.iterations - iw["iterations"]) <= max(2, 0.02 * iw["iterations"])
+    assert rw.matvecs == rw.iterations + rw.iterations // 50 + 1
+    assert np.abs(xw - xwr).max() <= 1e-6 * np.abs(xwr).max()
+    # zero right-hand side: x = 0, converged at iteration 0
+    xz, rz = pcg(op, np.zeros_like(b), d, CgConfig())
+    assert rz.converged and rz.iterations == 0 and np.all(xz == 0.0)
+
+
+def test_resident_nonzero_rhs_on_constrained_dofs():
+    """b != 0 on fixed DOFs: pass-through keeps them in the recurrence exactly
+    like the reference's apply (operator.py:115)."""
+    from paper_2604_18020_b200 import CgConfig, pcg
+
+    pb, edof, op = _problem("mbb", 0.2, "fp64", "random")
+    b = pb.bcs.force.copy()
+    b[pb.bcs.fixed_dofs] = np.linspace(0.1, 0.2, pb.bcs.fixed_dofs.size)
+    x, rep = pcg(op, b, op.diagonal(), CgConfig())
+    xr, info = _oracle_solve(op, edof, pb.bcs, b)
+    assert rep.termination == info["termination"]
+    assert abs(rep.iterations - info["iterations"]) <= max(2, 0.02 * info["iterations"])
+    assert np.abs(x - xr).max() <= 1e-6 * np.abs(xr).max()
+
+
+def test_resident_fp32_desk_window():
+    """Desk FP32 cold solve: reference floors at 108 iterations (test_solver.py:116-125)."""
+    from conftest import load_golden
+    from paper_2604_18020_b200 import CgConfig, solve_equilibrium
+    from paper_2604_18020_b200.solver import pcg_protocol
+
+    g = load_golden("cg.json")["desk_fp32"]
+    pb, edof, op = _problem("cantilever", 0.2, "fp32", "half")
+    assert pcg_protocol(op) == "resident"
+    u, rep = solve_equilibrium(op, pb.bcs.force, CgConfig())
+    assert rep.termination == g["termination"]
+    assert abs(rep.iterations - g["iterations"]) <= max(2, 0.02 * g["iterations"])
+    assert abs(rep.compliance - g["compliance"]) <= 1e-3 * abs(g["compliance"])

@@ -165,6 +165,7 @@ def test_fused_and_unfused_pcg_protocols_agree(prec, monkeypatch):
                                        make_preset, solve_equilibrium)
 
     res = []
+    monkeypatch.setenv("TF_PCG_RESIDENT", "0")  # graph protocols only
     for fused in ("1", "0"):
         monkeypatch.setenv("TF_PCG_FUSED", fused)
         pb = make_preset("cantilever", 0.4)

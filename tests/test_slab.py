@@ -43,7 +43,7 @@ def test_partition_covers_mesh_once():
     assert np.all(owned == 1)
 
 
-def _worker(rank, world, port, dims, prec, q, device="cpu"):
+def _worker(rank, world, port, dims, prec, q, device="cpu", max_iter=1000):
     import torch
     import torch.distributed as dist
 
@@ -91,7 +91,7 @@ def _worker(rank, world, port, dims, prec, q, device="cpu"):
         w = op.apply(torch.from_numpy(part.scatter(v).astype(dt)).to(device))
         d = op.diagonal()
         b = torch.from_numpy(lb.force.astype(dt)).to(device)
-        x, info = slab_pcg(op, b, d)
+        x, info = slab_pcg(op, b, d, max_iter=max_iter)
         q.put((rank, part.local_dof_to_global(), w.cpu().numpy(), d.cpu().numpy(), x.cpu().numpy(), info))
     finally:
         dist.destroy_process_group()
@@ -104,16 +104,20 @@ def test_slab_matvec_diag_and_pcg_match_global(world, dims, prec):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("world,dims,prec", [(2, (130, 6, 5), "fp64"), (3, (100, 5, 4), "fp32"),
-                                             (2, (20, 4, 3), "fp64")])
-def test_slab_gpu_local_kernels_match_global(world, dims, prec):
+@pytest.mark.parametrize("world,dims,prec,max_iter", [(2, (130, 6, 5), "fp64", 1000),
+                                                      (3, (100, 5, 4), "fp32", 40),
+                                                      (2, (20, 4, 3), "fp64", 1000)])
+def test_slab_gpu_local_kernels_match_global(world, dims, prec, max_iter):
     """All ranks share cuda:0 (gloo stages the interface planes through the
     host); local matvecs are the tile kernel split into interface and interior
-    x-ranges with the exchange posted in between."""
-    _run_slab(world, dims, prec, "cuda:0")
+    x-ranges with the exchange posted in between.  The FP32 case stops at a
+    fixed iteration count: this slender beam does not converge in FP32 within
+    the reference's 1000-iteration cap (neither does the reference), and
+    beyond ~100 iterations FP32 round-off differences are chaotically amplified."""
+    _run_slab(world, dims, prec, "cuda:0", max_iter)
 
 
-def _run_slab(world, dims, prec, device):
+def _run_slab(world, dims, prec, device, max_iter=1000):
     import torch.multiprocessing as mp
 
     import oracle
@@ -122,7 +126,8 @@ def _run_slab(world, dims, prec, device):
     ctx = mp.get_context("spawn")
     q = ctx.SimpleQueue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, dims, prec, q, device)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, dims, prec, q, device, max_iter))
+             for r in range(world)]
     for p in procs:
         p.start()
     res = [q.get() for _ in range(world)]
@@ -142,7 +147,7 @@ def _run_slab(world, dims, prec, device):
     w_ref = oracle.apply(edof, ke, scale, v, bcs.fixed_dofs, m.n_dof)
     d_ref = oracle.diagonal(edof, ke, scale, bcs.fixed_dofs, m.n_dof)
     A = lambda x: oracle.apply(edof, ke, scale, x, bcs.fixed_dofs, m.n_dof)
-    x_ref, info_ref = oracle.pcg(A, bcs.force.astype(dt), d_ref)
+    x_ref, info_ref = oracle.pcg(A, bcs.force.astype(dt), d_ref, max_iter=max_iter)
     tol = 1e-12 if prec == "fp64" else 1e-5
     # solution bar: 1e-3 of max|x| (north star), widened for FP32 to twice the
     # reference recurrence's own FP32-vs-FP64 spread on this problem (an
@@ -153,7 +158,7 @@ def _run_slab(world, dims, prec, device):
         s64 = simp_scale(rho, SimpParams(3.0))
         d64 = oracle.diagonal(edof, ke64, s64, bcs.fixed_dofs, m.n_dof)
         x64, _ = oracle.pcg(lambda x: oracle.apply(edof, ke64, s64, x, bcs.fixed_dofs, m.n_dof),
-                            bcs.force, d64)
+                            bcs.force, d64, max_iter=max_iter)
         xtol = max(xtol, 2.0 * np.abs(x_ref - x64).max())
     for rank, g2l, w, d, x, info in res:
         assert np.abs(w - w_ref[g2l]).max() <= tol * np.abs(w_ref).max()

@@ -122,6 +122,7 @@ struct CgTileArgs {
 struct ResPlan {
     dim3 grid;
     int oz;
+    int lean;
     size_t dyn_smem;
     long long nblk;
 };

@@ -50,7 +50,8 @@ bool pcg_resident_plan(const Grid& g, const T* ke_host, ResPlan* plan);
 template <typename T>
 int launch_pcg_resident(const ResPlan& plan, const Grid& g, const T* ke_host, int has_x0, const T* scale,
                         const T* b, const T* inv, T* x, T* z, T* p0, T* p1, const uint8_t* node_fixed,
-                        double* part, void* bar, CgScalars* sc, cudaStream_t st);
+                        double* ring, CgScalars* sc, cudaStream_t st);
+size_t pcg_resident_ring_doubles(const ResPlan& plan);
 
 
 
@@ -583,8 +584,7 @@ struct PcgImpl {
     int fused;          // structured tile solve with the direction folded into the matvec
     int resident;       // SM-resident solve: one cooperative launch (tf_pcg_resident.cu)
     ResPlan rplan;
-    double* part_res;   // 6 partials per resident CTA
-    void* bar;          // resident grid barrier words
+    double* ring;       // resident exchange slots
     double* part;
     double* part_mv;    // per-CTA p.q partials of the matvec
     unsigned* tickets;
@@ -792,7 +792,7 @@ static int solve_impl(PcgImpl* h, const void* scale, const void* b, const void* 
     if (h->resident) {
         int rc = launch_pcg_resident<T>(h->rplan, h->grid, (const T*)h->ke.data(), has_x0, (const T*)h->scale,
                                         (const T*)h->b, (const T*)h->inv, (T*)h->x, (T*)h->r, (T*)h->p,
-                                        (T*)h->p2, h->node_fixed, h->part_res, h->bar, h->sc, st);
+                                        (T*)h->p2, h->node_fixed, h->ring, h->sc, st);
         if (rc) return rc;
         TF_CUDA_TRY(cudaMemcpyAsync(h->sc_host, h->sc, sizeof(CgScalars), cudaMemcpyDeviceToHost, st));
         TF_CUDA_TRY(cudaStreamSynchronize(st));
@@ -885,8 +885,7 @@ int tf_pcg_create(tf_pcg** out, const tf_pcg_desc* d, void* stream)
     h->sc = nullptr;
     h->sc_host = nullptr;
     h->resident = 0;
-    h->part_res = nullptr;
-    h->bar = nullptr;
+    h->ring = nullptr;
     TF_REQUIRE(d->structured || d->edof, "edof required for unstructured problems");
 
     int dev = 0, nsm = 148;
@@ -933,9 +932,7 @@ int tf_pcg_create(tf_pcg** out, const tf_pcg_desc* d, void* stream)
     }
     if (h->resident) {
         h->fused = 0;
-        TF_CUDA_TRY(cudaMalloc(&h->part_res, sizeof(double) * (6 * h->rplan.nblk + 8)));
-        TF_CUDA_TRY(cudaMalloc(&h->bar, 64));
-        TF_CUDA_TRY(cudaMemset(h->bar, 0, 64));
+        TF_CUDA_TRY(cudaMalloc(&h->ring, sizeof(double) * pcg_resident_ring_doubles(h->rplan)));
     }
     if (h->fused || h->resident) TF_CUDA_TRY(cudaMalloc(&h->p2, vb));
     if (h->resident) {
@@ -988,7 +985,7 @@ int tf_pcg_destroy(tf_pcg* hh)
     if (h->exec) cudaGraphExecDestroy(h->exec);
     if (h->graph) cudaGraphDestroy(h->graph);
     void* bufs[] = {h->x, h->r, h->p, h->q, h->b, h->inv, h->scale, h->p2, h->part, h->part_mv, h->tickets, h->sc,
-                    h->part_res, h->bar};
+                    h->ring};
     for (void* p : bufs)
         if (p) cudaFree(p);
     if (h->sc_host) cudaFreeHost(h->sc_host);

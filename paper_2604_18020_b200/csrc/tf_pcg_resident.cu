@@ -22,11 +22,20 @@
 //   C. every CTA reduces them -> rel, convergence, max_iter, beta.
 // Every CTA takes the same decisions from bitwise-identical reductions, so
 // the loop exits everywhere at the same iteration; CTA 0 records the report.
+//
+// Barrier + reduction in one step ("exchange", res_exchange below): partials
+// published, one release-add on an arrival counter, fixed-order sum of all
+// partials after the counter completes.
+//
+// Layout: "full" keeps x, r, D^-1, p, q of the owned DOFs in shared memory;
+// "lean" (larger grids) keeps r, p, q there and x (read-modify-write by the
+// owner) and D^-1 (read-only) in global memory.
 // Scalar rounding is the numpy semantics of tf_pcg.cu (FP32 dots rounded to
 // float32, alpha/beta applied in the working dtype, no FMA contraction in
 // vector updates).
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <type_traits>
@@ -35,11 +44,6 @@
 #include "tf_walsh.cuh"
 
 namespace tf {
-
-struct ResBar {
-    unsigned count;
-    unsigned gen;
-};
 
 template <typename T>
 struct ResArgs {
@@ -53,32 +57,98 @@ struct ResArgs {
     T* z;        // z = r * D^-1 of the last update (halo source for p)
     T* pbuf[2];  // p_k in pbuf[k & 1]
     const uint8_t* node_fixed;
-    double* part;  // 6 per CTA: init [3n), phase A [n), phase B [2n) -- a region is
-                   // rewritten only after a barrier every reader of it has passed
-    ResBar* bar;
+    double* ring;  // [2][nblk][4] exchange partials, then the arrival counter
+    int lean;      // x and D^-1 in global memory instead of shared memory
     CgScalars* sc;  // tol / max_iter / recompute / hist in; report out
+    unsigned long long* trace;  // nullable: CTA 0 phase times (ns), TF_PCG_TRACE
 };
 
-// Grid-wide barrier of a cooperatively launched (co-resident) grid: one
-// arriving thread per CTA, generation counter read before arriving.
-__device__ __forceinline__ void res_grid_sync(ResBar* bar, unsigned nblk)
+__device__ __forceinline__ unsigned long long res_gtime()
 {
-    __syncthreads();
-    if (threadIdx.x == 0 && threadIdx.y == 0) {
-        volatile unsigned* vg = &bar->gen;
-        const unsigned g = *vg;
-        __threadfence();
-        if (atomicAdd(&bar->count, 1u) == nblk - 1) {
-            bar->count = 0u;
-            __threadfence();
-            atomicAdd(&bar->gen, 1u);
-        } else {
-            while (*vg == g) {
-            }
-        }
-        __threadfence();
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+__device__ __forceinline__ unsigned res_ld_acquire(const unsigned* p)
+{
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void res_red_release(unsigned* p, unsigned v)
+{
+    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Exchange number `phase`: publish this CTA's K partials (valid in every
+// thread, e.g. from res_block_sum) and return the fixed-order totals over all
+// CTAs in every thread.  Doubles as the grid barrier: on return every CTA has
+// arrived, and everything each wrote before arriving is visible.
+// Arrival: partials into slot [phase & 1] (rewritten two exchanges later,
+// after every reader has arrived at the exchange in between), fence, one
+// red.release on a monotonic counter; thread 0 polls the counter with acquire
+// loads until all nblk arrivals of this phase are in; warp 0 then sums the
+// partials in CTA order (measured on B200: 3.1 us per exchange at 296 CTAs,
+// vs 7.1 us for per-CTA sentinel slots polled by every CTA -- L2 flooding --
+// and 3.6 us for a count-reset/generation barrier; scripts/exchange_bench.cu).
+template <int K>
+__device__ __noinline__ void res_arrive(double* part, unsigned* ctr, int nblk, int bid, int tid, unsigned phase,
+                                        const double (&v)[K])
+{
+    double* slot = part + (size_t)(phase & 1u) * nblk * 4;
+    __syncthreads();  // the CTA's data writes precede the release below
+    if (tid == 0) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) slot[(size_t)bid * 4 + k] = v[k];
+        __threadfence();  // cumulative over the CTA's writes ordered by the barrier above
+        res_red_release(ctr, 1u);
+    }
+}
+
+template <int K>
+__device__ __noinline__ void res_wait(const double* part, const unsigned* ctr, int nblk, int tid, unsigned phase,
+                                      double (&v)[K], double* sh /* >= K */)
+{
+    const double* slot = part + (size_t)(phase & 1u) * nblk * 4;
+    if (tid == 0) {
+        const unsigned target = (phase + 1u) * (unsigned)nblk;
+        while (res_ld_acquire(ctr) < target) __nanosleep(20);
     }
     __syncthreads();
+    if (tid < 32) {
+        double acc[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) acc[k] = 0.0;
+        for (int i = tid; i < nblk; i += 32) {
+#pragma unroll
+            for (int k = 0; k < K; ++k) acc[k] += __ldcg(slot + (size_t)i * 4 + k);
+        }
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) acc[k] += __shfl_xor_sync(0xffffffffu, acc[k], o);
+        }
+        if (tid == 0) {
+#pragma unroll
+            for (int k = 0; k < K; ++k) sh[k] = acc[k];
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < K; ++k) v[k] = sh[k];
+    __syncthreads();
+}
+
+// arrive + wait; work that no other CTA needs before the next exchange can be
+// placed between the two halves (res_arrive / res_wait) to hide the latency
+template <int K, int NT>
+__device__ __forceinline__ void res_exchange(double* part, unsigned* ctr, int nblk, int bid, int tid,
+                                             unsigned phase, double (&v)[K], double* sh /* >= K */)
+{
+    res_arrive<K>(part, ctr, nblk, bid, tid, phase, v);
+    res_wait<K>(part, ctr, nblk, tid, phase, v, sh);
 }
 
 // Deterministic block sum of K values; every thread returns the same totals.
@@ -105,21 +175,6 @@ __device__ __forceinline__ void res_block_sum(double (&v)[K], double* sh /* [K][
     __syncthreads();
 }
 
-// Sum partial k (k < K, stride K per CTA) of all CTAs in a fixed order;
-// identical in every CTA.
-template <int K, int NT>
-__device__ __forceinline__ void res_reduce_all(const double* part, int nblk, double (&tot)[K], double* sh,
-                                               int tid)
-{
-#pragma unroll
-    for (int k = 0; k < K; ++k) tot[k] = 0.0;
-    for (int i = tid; i < nblk; i += NT) {
-#pragma unroll
-        for (int k = 0; k < K; ++k) tot[k] += __ldcg(part + K * i + k);
-    }
-    res_block_sum<K, NT>(tot, sh, tid);
-}
-
 // The CTA's staging slots of a node plane and its owned-column bookkeeping.
 template <typename T>
 struct ResTile {
@@ -130,8 +185,11 @@ struct ResTile {
 #ifndef TF_RES_MINB32
 #define TF_RES_MINB32 2
 #endif
+#ifndef TF_RES_MINB64
+#define TF_RES_MINB64 2
+#endif
 template <typename T>
-__global__ void __launch_bounds__(TileDims<T>::NT, sizeof(T) == 4 ? TF_RES_MINB32 : 2)
+__global__ void __launch_bounds__(TileDims<T>::NT, sizeof(T) == 4 ? TF_RES_MINB32 : TF_RES_MINB64)
 k_pcg_resident(const __grid_constant__ ResArgs<T> A, const __grid_constant__ KhatBlocks<T> kb)
 {
     using RT = ResTile<T>;
@@ -144,10 +202,11 @@ k_pcg_resident(const __grid_constant__ ResArgs<T> A, const __grid_constant__ Kha
 
     const Grid& g = A.g;
     const int oz = A.oz;
+    const bool lean = A.lean != 0;
     const int tx = threadIdx.x, ty = threadIdx.y;
     const int tid = tx + TILE_BX * ty;
     const int bid = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
-    const unsigned nblk = gridDim.x * gridDim.y * gridDim.z;
+    const int nblk = (int)(gridDim.x * gridDim.y * gridDim.z);
     const int i0 = blockIdx.x * (TILE_BX - 1);
     const int j0 = blockIdx.y * (BY - 1);
     const int k0 = blockIdx.z * oz;
@@ -161,16 +220,24 @@ k_pcg_resident(const __grid_constant__ ResArgs<T> A, const __grid_constant__ Kha
     const uint8_t* col_or = nf ? nf + g.n_nodes : nullptr;
     const uint8_t* col_and = nf ? col_or + pn : nullptr;
     const int own_node0 = (i0 + tx) + g.nnx * (j0 + ty);
-    double* part_init = A.part;
-    double* part_a = A.part + 3 * nblk;
-    double* part_b = A.part + 4 * nblk;
+    unsigned phase = 0u;  // exchange counter (identical sequence in every CTA)
+    unsigned* ctr = reinterpret_cast<unsigned*>(A.ring + (size_t)8 * nblk);
 
-    // owned vectors in shared memory: own(v, kk, c) for this thread
+    // owned vectors in shared memory: own(v, kk, c) for this thread.  Full
+    // layout: x r inv p q; lean: r p q (x and inv in global memory).
     T* own = reinterpret_cast<T*>(res_dyn);
-    enum { VX = 0, VR = 1, VI = 2, VP = 3, VQ = 4 };
+    const int VR = lean ? 0 : 1, VP = lean ? 1 : 3, VQ = lean ? 2 : 4;
+    constexpr int VX = 0, VI = 2;
     auto oidx = [&](int v, int kk, int c, int t) { return ((v * oz + kk) * 3 + c) * NT + t; };
+    auto dof = [&](int kk, int c) { return 3 * (own_node0 + (k0 + kk) * pn) + c; };
+    auto get_x = [&](int kk, int c) -> T { return lean ? __ldcg(A.x + dof(kk, c)) : own[oidx(VX, kk, c, tid)]; };
+    auto set_x = [&](int kk, int c, T v) {
+        if (lean) A.x[dof(kk, c)] = v;
+        else own[oidx(VX, kk, c, tid)] = v;
+    };
+    auto get_inv = [&](int kk, int c) -> T { return lean ? ld_nc(A.inv + dof(kk, c)) : own[oidx(VI, kk, c, tid)]; };
 
-    // fixed bits of the owned DOFs, 3 per owned plane (oz <= 10)
+    // fixed bits of the owned DOFs, 3 per owned plane (oz <= 21)
     unsigned long long ofix = 0ull;
     if (nf) {
         for (int kk = 0; kk < n_own; ++kk)
@@ -211,10 +278,10 @@ k_pcg_resident(const __grid_constant__ ResArgs<T> A, const __grid_constant__ Kha
     // and to own(VP); otherwise the input is the global vector `src`.  The
     // result of every owned DOF (pass-through on constrained DOFs) goes to
     // own(VQ); returns this thread's p.q (PDIR).
-    auto tile_pass = [&](auto pdir_tag, bool first, T be, const T* src, const T* pold, T* pnew) -> double {
-        constexpr bool pdir = decltype(pdir_tag)::value;
-        T pa[NS], pb[NS];
-        auto fetch = [&](int kz) {
+    // (one instantiation for both modes: the kernel's code footprint is kept
+    // small so the per-iteration phases stay in the instruction cache)
+    auto tile_pass = [&](bool pdir, bool first, T be, const T* src, const T* pold, T* pnew) -> double {
+        auto fetch = [&](int kz, T (&pa)[NS], T (&pb)[NS]) {
             const bool zok = kz >= 0 && kz < g.nnz;
             const int base = min(max(kz, 0), g.nnz - 1) * pn3;
 #pragma unroll
@@ -222,10 +289,10 @@ k_pcg_resident(const __grid_constant__ ResArgs<T> A, const __grid_constant__ Kha
                 const bool take = zok && ((okbits >> q) & 1u);
                 const int d = base + s_off[q];
                 pa[q] = take ? __ldcg(src + d) : T(0);
-                pb[q] = (pdir && take && !first) ? __ldcg(pold + d) : T(0);
+                if (pdir) pb[q] = (take && !first) ? __ldcg(pold + d) : T(0);
             }
         };
-        auto commit = [&](int kz, T* buf) {
+        auto commit = [&](int kz, T* buf, const T (&pa)[NS], const T (&pb)[NS]) {
             const bool zok = kz >= 0 && kz < g.nnz;
             const bool wr = pdir && zok && kz >= k0 && kz < kend;
             const int base = min(max(kz, 0), g.nnz - 1) * pn3;
@@ -252,11 +319,16 @@ k_pcg_resident(const __grid_constant__ ResArgs<T> A, const __grid_constant__ Kha
         const int n_layers = kend - k0 + 1;
         T* b_cur = plane[0];
         T* b_top = plane[1];
-        fetch(k0 - 1);
-        commit(k0 - 1, b_cur);
-        fetch(k0);
-        commit(k0, b_top);
-        fetch(k0 + 1);
+        T pa[NS], pb[NS];
+        {
+            // both prologue planes in flight together (one L2 round trip)
+            T qa[NS], qb[NS];
+            fetch(k0 - 1, qa, qb);
+            fetch(k0, pa, pb);
+            commit(k0 - 1, b_cur, qa, qb);
+            commit(k0, b_top, pa, pb);
+        }
+        fetch(k0 + 1, pa, pb);
         __syncthreads();
         T XYb[3][4];
 #pragma unroll
@@ -274,8 +346,8 @@ k_pcg_resident(const __grid_constant__ ResArgs<T> A, const __grid_constant__ Kha
             const int ez = k0 - 1 + L;
             if (L >= 1) {
                 // plane ez+1 into the buffer that held plane ez-1 (read before (B) of layer L-1)
-                commit(ez + 1, b_top);
-                if (L + 1 < n_layers) fetch(ez + 2);
+                commit(ez + 1, b_top, pa, pb);
+                if (L + 1 < n_layers) fetch(ez + 2, pa, pb);
             }
             __syncthreads();  // (A)
             const T s_next = scale_at(ez + 1);
@@ -344,7 +416,7 @@ k_pcg_resident(const __grid_constant__ ResArgs<T> A, const __grid_constant__ Kha
                         if (fx) acc = p;  // pass-through of the unmasked input
                         dot += (double)p * (double)acc;
                     } else if (fx) {
-                        acc = own[oidx(VX, kk, c, tid)];
+                        acc = get_x(kk, c);
                     }
                     own[oidx(VQ, kk, c, tid)] = acc;
                 }
@@ -357,43 +429,51 @@ k_pcg_resident(const __grid_constant__ ResArgs<T> A, const __grid_constant__ Kha
         return dot;
     };
 
-    constexpr std::integral_constant<bool, true> PDIR{};
-    constexpr std::integral_constant<bool, false> RAW{};
+    constexpr bool PDIR = true, RAW = false;
+    const bool tracing = A.trace != nullptr && bid == 0 && tid == 0;
+    unsigned long long tr[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    unsigned long long t_mark = tracing ? res_gtime() : 0ull;
+    auto lap = [&](int slot) {
+        if (tracing) {
+            const unsigned long long t = res_gtime();
+            tr[slot] += t - t_mark;
+            t_mark = t;
+        }
+    };
 
     // ---- init (solver.py:72-103) -------------------------------------------------
-    for (int kk = 0; kk < n_own; ++kk)
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-            const int d = 3 * (own_node0 + (k0 + kk) * pn) + c;
-            own[oidx(VI, kk, c, tid)] = ld_nc(A.inv + d);
-            own[oidx(VX, kk, c, tid)] = A.has_x0 ? A.x[d] : T(0);
-        }
-    __syncthreads();
-    if (A.has_x0) tile_pass(RAW, false, T(0), A.x, nullptr, nullptr);  // own(VQ) = A x0
-    double tot[3];
-    {
-        double v[3] = {0.0, 0.0, 0.0};
+    if (!lean) {
         for (int kk = 0; kk < n_own; ++kk)
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
-                const int d = 3 * (own_node0 + (k0 + kk) * pn) + c;
+                const int d = dof(kk, c);
+                own[oidx(VI, kk, c, tid)] = ld_nc(A.inv + d);
+                own[oidx(VX, kk, c, tid)] = A.has_x0 ? __ldcg(A.x + d) : T(0);
+            }
+    } else if (!A.has_x0) {
+        for (int kk = 0; kk < n_own; ++kk)
+#pragma unroll
+            for (int c = 0; c < 3; ++c) A.x[dof(kk, c)] = T(0);
+    }
+    __syncthreads();
+    if (A.has_x0) tile_pass(RAW, false, T(0), A.x, nullptr, nullptr);  // own(VQ) = A x0
+    double tot[3] = {0.0, 0.0, 0.0};
+    {
+        for (int kk = 0; kk < n_own; ++kk)
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                const int d = dof(kk, c);
                 const T bb = ld_nc(A.b + d);
                 const T r = A.has_x0 ? sub_rn(bb, own[oidx(VQ, kk, c, tid)]) : bb;
-                const T z = mul_rn(r, own[oidx(VI, kk, c, tid)]);
+                const T z = mul_rn(r, get_inv(kk, c));
                 own[oidx(VR, kk, c, tid)] = r;
                 A.z[d] = z;
-                v[0] += (double)bb * (double)bb;
-                v[1] += (double)r * (double)r;
-                v[2] += (double)r * (double)z;
+                tot[0] += (double)bb * (double)bb;
+                tot[1] += (double)r * (double)r;
+                tot[2] += (double)r * (double)z;
             }
-        res_block_sum<3, NT>(v, shr, tid);
-        if (tid == 0) {
-            part_init[3 * bid] = v[0];
-            part_init[3 * bid + 1] = v[1];
-            part_init[3 * bid + 2] = v[2];
-        }
-        res_grid_sync(A.bar, nblk);
-        res_reduce_all<3, NT>(part_init, (int)nblk, tot, shr, tid);
+        res_block_sum<3, NT>(tot, shr, tid);
+        res_exchange<3, NT>(A.ring, ctr, nblk, bid, tid, phase++, tot, shr);
     }
     CgScalars* sc = A.sc;
     const bool lead = bid == 0 && tid == 0;
@@ -422,23 +502,20 @@ k_pcg_resident(const __grid_constant__ ResArgs<T> A, const __grid_constant__ Kha
     bool done = rel <= tol;
     if (done) term = TERM_CONVERGED;
     double beta = 0.0;
+    lap(5);
 
     // ---- iterations (solver.py:104-137) --------------------------------------------
     while (!done) {
         ++it;
         // A. q = A p_it, fused p.q
-        {
-            double v[1] = {tile_pass(PDIR, it == 1, (T)beta, A.z, A.pbuf[(it - 1) & 1], A.pbuf[it & 1])};
-            ++matvecs;
-            res_block_sum<1, NT>(v, shr, tid);
-            if (tid == 0) part_a[bid] = v[0];
-            res_grid_sync(A.bar, nblk);
-            double t1[1];
-            res_reduce_all<1, NT>(part_a, (int)nblk, t1, shr, tid);
-            tot[0] = t1[0];
-        }
+        double t1[1] = {tile_pass(PDIR, it == 1, (T)beta, A.z, A.pbuf[(it - 1) & 1], A.pbuf[it & 1])};
+        ++matvecs;
+        lap(0);
+        res_block_sum<1, NT>(t1, shr, tid);
+        res_exchange<1, NT>(A.ring, ctr, nblk, bid, tid, phase++, t1, shr);
+        lap(1);
         // B. alpha, x, r, z
-        const double pq = cg_round(tot[0], F32);
+        const double pq = cg_round(t1[0], F32);
         if (!isfinite(pq) || !isfinite(rz)) {
             term = TERM_DIVERGED;
             break;
@@ -450,48 +527,79 @@ k_pcg_resident(const __grid_constant__ ResArgs<T> A, const __grid_constant__ Kha
         const double alpha = rz / pq;
         const T a = (T)alpha;
         const bool refresh = recompute > 0 && it % recompute == 0;
-        __syncthreads();  // grid-sync tail: all own(VP/VQ) writes of the pass are visible
-        for (int kk = 0; kk < n_own; ++kk)
+        // x += alpha p: needed by other CTAs only on a refresh; otherwise it is
+        // done while exchange B is in flight
+        auto update_x = [&]() {
+            if (!lean) {
+                for (int kk = 0; kk < n_own; ++kk)
 #pragma unroll
-            for (int c = 0; c < 3; ++c) {
-                const int o = oidx(VX, kk, c, tid);
-                const T xn = add_rn(own[o], mul_rn(a, own[oidx(VP, kk, c, tid)]));
-                own[o] = xn;
-                if (refresh) A.x[3 * (own_node0 + (k0 + kk) * pn) + c] = xn;
+                    for (int c = 0; c < 3; ++c) {
+                        const int o = oidx(VX, kk, c, tid);
+                        const T xn = add_rn(own[o], mul_rn(a, own[oidx(VP, kk, c, tid)]));
+                        own[o] = xn;
+                        if (refresh) A.x[dof(kk, c)] = xn;
+                    }
+            } else {
+                // global x: loads of a chunk issued together (one L2 round trip per 4 planes)
+                for (int k4 = 0; k4 < n_own; k4 += 4) {
+                    T xv[4][3];
+#pragma unroll
+                    for (int j = 0; j < 4; ++j)
+#pragma unroll
+                        for (int c = 0; c < 3; ++c) xv[j][c] = k4 + j < n_own ? __ldcg(A.x + dof(k4 + j, c)) : T(0);
+#pragma unroll
+                    for (int j = 0; j < 4; ++j)
+#pragma unroll
+                        for (int c = 0; c < 3; ++c)
+                            if (k4 + j < n_own)
+                                A.x[dof(k4 + j, c)] = add_rn(xv[j][c], mul_rn(a, own[oidx(VP, k4 + j, c, tid)]));
+                }
             }
+        };
+        if (refresh) update_x();
+        lap(6);
         if (refresh) {
-            res_grid_sync(A.bar, nblk);  // x published
+            double dummy[1] = {0.0};
+            res_exchange<1, NT>(A.ring, ctr, nblk, bid, tid, phase++, dummy, shr);  // x published
             tile_pass(RAW, false, T(0), A.x, nullptr, nullptr);  // own(VQ) = A x
             ++matvecs;
         }
-        {
-            double v[2] = {0.0, 0.0};
-            for (int kk = 0; kk < n_own; ++kk)
+        double t2[2] = {0.0, 0.0};
+        for (int k4 = 0; k4 < n_own; k4 += 4) {
+            // chunk of 4 planes: global loads (b on refresh, D^-1 when lean) issued together
+            T bv[4][3], iv[4][3];
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
 #pragma unroll
                 for (int c = 0; c < 3; ++c) {
-                    const int d = 3 * (own_node0 + (k0 + kk) * pn) + c;
-                    const int orr = oidx(VR, kk, c, tid);
-                    const T q = own[oidx(VQ, kk, c, tid)];
-                    const T r = refresh ? sub_rn(ld_nc(A.b + d), q) : sub_rn(own[orr], mul_rn(a, q));
-                    own[orr] = r;
-                    const T z = mul_rn(r, own[oidx(VI, kk, c, tid)]);
-                    A.z[d] = z;
-                    v[0] += (double)r * (double)r;
-                    v[1] += (double)r * (double)z;
+                    const bool in = k4 + j < n_own;
+                    bv[j][c] = (in && refresh) ? ld_nc(A.b + dof(k4 + j, c)) : T(0);
+                    iv[j][c] = in ? get_inv(k4 + j, c) : T(0);
                 }
-            res_block_sum<2, NT>(v, shr, tid);
-            if (tid == 0) {
-                part_b[2 * bid] = v[0];
-                part_b[2 * bid + 1] = v[1];
-            }
-            res_grid_sync(A.bar, nblk);
-            double t2[2];
-            res_reduce_all<2, NT>(part_b, (int)nblk, t2, shr, tid);
-            tot[0] = t2[0];
-            tot[1] = t2[1];
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    if (k4 + j >= n_own) continue;
+                    const int orr = oidx(VR, k4 + j, c, tid);
+                    const T q = own[oidx(VQ, k4 + j, c, tid)];
+                    const T r = refresh ? sub_rn(bv[j][c], q) : sub_rn(own[orr], mul_rn(a, q));
+                    own[orr] = r;
+                    const T z = mul_rn(r, iv[j][c]);
+                    A.z[dof(k4 + j, c)] = z;
+                    t2[0] += (double)r * (double)r;
+                    t2[1] += (double)r * (double)z;
+                }
         }
+        lap(7);
+        res_block_sum<2, NT>(t2, shr, tid);
+        lap(2);
+        res_arrive<2>(A.ring, ctr, nblk, bid, tid, phase, t2);
+        if (!refresh) update_x();
+        res_wait<2>(A.ring, ctr, nblk, tid, phase++, t2, shr);
+        lap(3);
         // C. decisions
-        const double rn = cg_sqrt(cg_round(tot[0], F32), F32);
+        const double rn = cg_sqrt(cg_round(t2[0], F32), F32);
         if (!isfinite(rn)) {
             term = TERM_DIVERGED;
             break;
@@ -502,20 +610,22 @@ k_pcg_resident(const __grid_constant__ ResArgs<T> A, const __grid_constant__ Kha
             term = TERM_CONVERGED;
             break;
         }
-        const double rz_new = cg_round(tot[1], F32);
+        const double rz_new = cg_round(t2[1], F32);
         beta = rz_new / rz;
         rz = rz_new;
         if (it >= max_iter) {
             term = TERM_MAX_ITER;
             break;
         }
+        lap(4);
     }
 
     // solution: every DOF written once by its owner
-    for (int kk = 0; kk < n_own; ++kk)
+    if (!lean) {
+        for (int kk = 0; kk < n_own; ++kk)
 #pragma unroll
-        for (int c = 0; c < 3; ++c)
-            A.x[3 * (own_node0 + (k0 + kk) * pn) + c] = own[oidx(VX, kk, c, tid)];
+            for (int c = 0; c < 3; ++c) A.x[dof(kk, c)] = own[oidx(VX, kk, c, tid)];
+    }
     if (lead) {
         sc->bnorm = bnorm;
         sc->zero_rhs = 0;
@@ -526,18 +636,26 @@ k_pcg_resident(const __grid_constant__ ResArgs<T> A, const __grid_constant__ Kha
         sc->rel = rel;
         sc->rz = rz;
     }
+    if (tracing) {
+        for (int k = 0; k < 6; ++k) A.trace[k] = tr[k];
+        A.trace[6] = (unsigned long long)it;
+        A.trace[7] = tr[6];
+        A.trace[8] = tr[7];
+    }
 }
 
 // ---- host ------------------------------------------------------------------------
 
 template <typename T>
-static size_t res_dyn_bytes(int oz)
+static size_t res_dyn_bytes(int oz, bool lean)
 {
-    return (size_t)5 * oz * 3 * TileDims<T>::NT * sizeof(T);
+    return (size_t)(lean ? 3 : 5) * oz * 3 * TileDims<T>::NT * sizeof(T);
 }
 
-// Chooses the z-chunk height for a co-resident grid (smallest chunk whose
-// grid fits one wave with its shared-memory state); false when none fits.
+// Chooses the z-chunk height and layout of a co-resident grid: the smallest
+// chunk (most CTAs) whose grid fits one wave with its shared-memory state,
+// the full layout before the lean one; false when nothing fits.
+// TF_PCG_RES_OZ / TF_PCG_RES_LEAN=0|1 pin either choice (experiments).
 template <typename T>
 bool pcg_resident_plan(const Grid& g, const T* ke_host, ResPlan* plan)
 {
@@ -554,36 +672,46 @@ bool pcg_resident_plan(const Grid& g, const T* ke_host, ResPlan* plan)
     const long long cols = (long long)tx * ty;
     const char* e = getenv("TF_PCG_RES_OZ");
     const int oz_force = e ? atoi(e) : 0;
-    for (int oz = 2; oz <= std::min(g.nnz, 10); ++oz) {
+    const char* el = getenv("TF_PCG_RES_LEAN");
+    const int lean_force = el ? (el[0] == '1' ? 1 : 0) : -1;
+    for (int oz = 2; oz <= std::min(g.nnz, 21); ++oz) {
         if (oz_force > 0 && oz != oz_force) continue;
-        const size_t dyn = res_dyn_bytes<T>(oz);
-        if ((long long)dyn + 16384 > smem_optin) break;
-        if (cudaFuncSetAttribute(k_pcg_resident<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn) !=
-            cudaSuccess) {
-            cudaGetLastError();
-            return false;
-        }
-        int per_sm = 0;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pcg_resident<T>, NT, dyn) != cudaSuccess) {
-            cudaGetLastError();
-            return false;
-        }
-        const long long tz = (g.nnz + oz - 1) / oz;
-        if (per_sm > 0 && cols * tz <= (long long)per_sm * nsm) {
-            plan->grid = dim3(tx, ty, (unsigned)tz);
-            plan->oz = oz;
-            plan->dyn_smem = dyn;
-            plan->nblk = cols * tz;
-            return true;
+        for (int lean = 0; lean < 2; ++lean) {
+            if (lean_force >= 0 && lean != lean_force) continue;
+            const size_t dyn = res_dyn_bytes<T>(oz, lean != 0);
+            if ((long long)dyn + 16384 > smem_optin) continue;
+            cudaFuncSetAttribute(k_pcg_resident<T>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                 cudaSharedmemCarveoutMaxShared);
+            if (cudaFuncSetAttribute(k_pcg_resident<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn) !=
+                cudaSuccess) {
+                cudaGetLastError();
+                return false;
+            }
+            int per_sm = 0;
+            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pcg_resident<T>, NT, dyn) != cudaSuccess) {
+                cudaGetLastError();
+                return false;
+            }
+            const long long tz = (g.nnz + oz - 1) / oz;
+            if (per_sm > 0 && cols * tz <= (long long)per_sm * nsm) {
+                plan->grid = dim3(tx, ty, (unsigned)tz);
+                plan->oz = oz;
+                plan->lean = lean;
+                plan->dyn_smem = dyn;
+                plan->nblk = cols * tz;
+                return true;
+            }
         }
     }
     return false;
 }
 
+size_t pcg_resident_ring_doubles(const ResPlan& plan) { return (size_t)8 * plan.nblk + 16; }
+
 template <typename T>
 int launch_pcg_resident(const ResPlan& plan, const Grid& g, const T* ke_host, int has_x0, const T* scale,
                         const T* b, const T* inv, T* x, T* z, T* p0, T* p1, const uint8_t* node_fixed,
-                        double* part, void* bar, CgScalars* sc, cudaStream_t st)
+                        double* ring, CgScalars* sc, cudaStream_t st)
 {
     KhatBlocks<T> kb;
     if (!khat_blocks<T>(ke_host, &kb)) return TF_ERR_UNSUPPORTED;
@@ -599,14 +727,36 @@ int launch_pcg_resident(const ResPlan& plan, const Grid& g, const T* ke_host, in
     a.pbuf[0] = p0;
     a.pbuf[1] = p1;
     a.node_fixed = node_fixed;
-    a.part = part;
-    a.bar = static_cast<ResBar*>(bar);
+    a.ring = ring;
+    a.lean = plan.lean;
     a.sc = sc;
-    TF_CUDA_TRY(cudaMemsetAsync(bar, 0, sizeof(ResBar), st));
+    a.trace = nullptr;
+    static unsigned long long* trace_buf = nullptr;
+    const bool tracing = getenv("TF_PCG_TRACE") != nullptr;
+    if (tracing) {
+        if (!trace_buf) TF_CUDA_TRY(cudaMalloc(&trace_buf, 16 * sizeof(unsigned long long)));
+        TF_CUDA_TRY(cudaMemsetAsync(trace_buf, 0, 16 * sizeof(unsigned long long), st));
+        a.trace = trace_buf;
+    }
+    TF_CUDA_TRY(cudaMemsetAsync(ring, 0, sizeof(double) * pcg_resident_ring_doubles(plan), st));
+    TF_CUDA_TRY(cudaFuncSetAttribute(k_pcg_resident<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)plan.dyn_smem));
     void* args[] = {&a, &kb};
     dim3 block(TILE_BX, TileDims<T>::BY, 1);
     TF_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)k_pcg_resident<T>, plan.grid, block, args,
                                             plan.dyn_smem, st));
+    if (tracing) {
+        unsigned long long h[16];
+        TF_CUDA_TRY(cudaMemcpyAsync(h, trace_buf, sizeof(h), cudaMemcpyDeviceToHost, st));
+        TF_CUDA_TRY(cudaStreamSynchronize(st));
+        const double n = h[6] ? (double)h[6] : 1.0;
+        fprintf(stderr,
+                "[tf_pcg_resident] fp%d grid %ux%ux%u oz %d %s: %llu its; us/it: matvec %.2f  xchg-A %.2f  "
+                "update %.2f (x %.2f, r/z %.2f)  xchg-B %.2f  decide %.2f  (init %.2f us)\n",
+                (int)(8 * sizeof(T)), plan.grid.x, plan.grid.y, plan.grid.z, plan.oz, plan.lean ? "lean" : "full",
+                h[6], h[0] / n / 1e3, h[1] / n / 1e3, (h[2] + h[7] + h[8]) / n / 1e3, h[7] / n / 1e3, h[8] / n / 1e3,
+                h[3] / n / 1e3, h[4] / n / 1e3, h[5] / 1e3);
+    }
     return TF_OK;
 }
 
@@ -614,9 +764,9 @@ template bool pcg_resident_plan<float>(const Grid&, const float*, ResPlan*);
 template bool pcg_resident_plan<double>(const Grid&, const double*, ResPlan*);
 template int launch_pcg_resident<float>(const ResPlan&, const Grid&, const float*, int, const float*,
                                         const float*, const float*, float*, float*, float*, float*,
-                                        const uint8_t*, double*, void*, CgScalars*, cudaStream_t);
+                                        const uint8_t*, double*, CgScalars*, cudaStream_t);
 template int launch_pcg_resident<double>(const ResPlan&, const Grid&, const double*, int, const double*,
                                          const double*, const double*, double*, double*, double*, double*,
-                                         const uint8_t*, double*, void*, CgScalars*, cudaStream_t);
+                                         const uint8_t*, double*, CgScalars*, cudaStream_t);
 
 }  // namespace tf

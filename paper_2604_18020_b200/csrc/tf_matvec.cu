@@ -22,6 +22,7 @@
 #include <cstring>
 
 #include "tf_common.cuh"
+#include "tf_walsh.cuh"
 
 namespace tf {
 

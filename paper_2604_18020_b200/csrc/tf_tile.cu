@@ -31,6 +31,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <type_traits>
 
 #include "tf_common.cuh"
 #include "tf_walsh.cuh"
@@ -86,78 +87,6 @@ template bool khat_blocks<float>(const float*, KhatBlocks<float>*);
 template bool khat_blocks<double>(const double*, KhatBlocks<double>*);
 
 // ---- device ------------------------------------------------------------------------
-
-template <typename T>
-__device__ __forceinline__ void fwht_fwd(T (&x)[8])
-{
-#pragma unroll
-    for (int bit = 1; bit < 8; bit <<= 1)
-#pragma unroll
-        for (int b = 0; b < 8; ++b)
-            if (!(b & bit)) {
-                const T lo = x[b], hi = x[b | bit];
-                x[b] = lo + hi;
-                x[b | bit] = hi - lo;
-            }
-}
-
-template <typename T>
-__device__ __forceinline__ void fwht_inv(T (&x)[8])
-{
-#pragma unroll
-    for (int bit = 1; bit < 8; bit <<= 1)
-#pragma unroll
-        for (int b = 0; b < 8; ++b)
-            if (!(b & bit)) {
-                const T lo = x[b], hi = x[b | bit];
-                x[b] = lo - hi;
-                x[b | bit] = lo + hi;
-            }
-}
-
-// f (reference corner order, 24) = s * Ke * u  via the parity-block form
-template <typename T>
-__device__ __forceinline__ void element_apply(const T (&u)[NLOC], T s, const KhatBlocks<T>& kb,
-                                              T (&f)[NLOC])
-{
-    T h[3][8];
-#pragma unroll
-    for (int a = 0; a < 8; ++a)
-#pragma unroll
-        for (int c = 0; c < 3; ++c) h[c][bin_of(a)] = u[3 * a + c];
-#pragma unroll
-    for (int c = 0; c < 3; ++c) fwht_fwd(h[c]);
-#pragma unroll
-    for (int c = 0; c < 3; ++c)
-#pragma unroll
-        for (int m = 1; m < 8; ++m) h[c][m] *= s;  // mode 0 is rigid translation: unused
-    T g[3][8];
-#pragma unroll
-    for (int c = 0; c < 3; ++c) g[c][0] = T(0);
-#pragma unroll
-    for (int q = 0; q < 8; ++q)
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-            const int m = q ^ (1 << c);
-            if (m == 0) continue;  // translation rows of Khat vanish
-            T acc = T(0);
-#pragma unroll
-            for (int d = 0; d < 3; ++d) {
-                const int n = q ^ (1 << d);
-                if (n == 0) continue;
-                acc = fma(kb.b[q][c][d], h[d][n], acc);
-            }
-            g[c][m] = acc;
-        }
-#pragma unroll
-    for (int c = 0; c < 3; ++c) fwht_inv(g[c]);
-#pragma unroll
-    for (int a = 0; a < 8; ++a)
-#pragma unroll
-        for (int c = 0; c < 3; ++c) f[3 * a + c] = g[c][bin_of(a)];
-}
-
-// Each thread handles at most STAGE_SLOTS values of a staged node plane.
 
 template <typename T, bool DOT>
 __global__ void __launch_bounds__(TileDims<T>::NT)
@@ -588,6 +517,241 @@ k_grid_tile3(Grid g, int oz, const T* __restrict__ scale, const T* __restrict__ 
             double s = 0.0;
             for (int i = 0; i < TILE_NT / 32; ++i) s += sh[i];
             dot_part[blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z)] = s;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// v5: k_grid_tile3's algorithm with the bookkeeping stripped for the issue-
+// bound regime.
+//   * the operator flags are template parameters (the production matvec is
+//     MASK|PASS: no ACCUMULATE branches, no flag tests per DOF);
+//   * the layer loop is unrolled by the ring period (3): the plane buffers and
+//     the row hand-off Y are compile-time offsets -- no pointer rotation, no
+//     register moves between layers;
+//   * owners whose node column carries no constraint (column OR byte == 0)
+//     never read the per-node constraint byte;
+//   * staging addresses: one uniform plane base + a 32-bit slot offset.
+// Same arithmetic as tile3 (bitwise-identical results).
+// ---------------------------------------------------------------------------
+template <typename T, bool MASK, bool PASS, bool ACC, bool DOT>
+__global__ void __launch_bounds__(TileDims<T>::NT, sizeof(T) == 4 ? TF_TILE_MINB32 : TF_TILE_MINB64)
+k_grid_tile5(Grid g, int oz, const T* __restrict__ scale, const T* __restrict__ v, T* __restrict__ w,
+             const uint8_t* __restrict__ node_fixed, double* __restrict__ dot_part,
+             const __grid_constant__ KhatBlocks<T> kb)
+{
+    constexpr int TILE_BY = TileDims<T>::BY, TILE_NT = TileDims<T>::NT;
+    constexpr int PW = StageSlots<T>::PW, PN = StageSlots<T>::PN, NS = StageSlots<T>::N;
+    __shared__ __align__(16) T plane[3][PN];  // node plane k lives in buffer (k - k0 + 1) % 3
+    __shared__ T Y[3][3][TILE_NT];            // row hand-off, by layer % 3
+
+    const int tx = threadIdx.x, ty = threadIdx.y;
+    const int tid = tx + TILE_BX * ty;
+    const int i0 = g.ilo + blockIdx.x * (TILE_BX - 1);
+    const int j0 = blockIdx.y * (TILE_BY - 1);
+    const int k0 = blockIdx.z * oz;
+    const int ex = i0 - 1 + tx, ey = j0 - 1 + ty;
+    const bool col_ok = ex >= 0 && ex < g.nelx && ey >= 0 && ey < g.nely;
+    const bool owner = tx < TILE_BX - 1 && ty < TILE_BY - 1 && (i0 + tx) < g.ihi && (j0 + ty) < g.nny;
+    const bool have_nf = node_fixed != nullptr;
+    const int pn = g.nnx * g.nny, pn3 = 3 * pn;
+    const uint8_t* col_or = have_nf ? node_fixed + g.n_nodes : nullptr;
+    const uint8_t* col_and = have_nf ? col_or + pn : nullptr;
+
+    int s_off[NS];
+    unsigned okbits = 0u, mskbits = 0u;
+#pragma unroll
+    for (int q = 0; q < NS; ++q) {
+        const int idx = tid + q * TILE_NT;
+        const int r = idx / PW, f = idx - r * PW;
+        const int ii = i0 - 1 + f / 3, jj = j0 - 1 + r, c = f % 3;
+        const bool ok = idx < PN && ii >= 0 && ii < g.nnx && jj >= 0 && jj < g.nny;
+        const int node = ok ? ii + g.nnx * jj : 0;
+        s_off[q] = 3 * node + c;
+        bool keep = ok;
+        if (MASK && ok && have_nf) {
+            if ((col_and[node] >> c) & 1u) keep = false;
+            else if ((col_or[node] >> c) & 1u) mskbits |= 1u << q;
+        }
+        if (keep) okbits |= 1u << q;
+    }
+    auto stage = [&](int kz, T* buf) {
+        const bool zok = kz >= 0 && kz < g.nnz;
+        const T* vb = v + (long long)min(max(kz, 0), g.nnz - 1) * pn3;
+        unsigned take = zok ? okbits : 0u;
+        if (MASK && mskbits && zok) {  // rare: columns with z-varying constraints
+#pragma unroll
+            for (int q = 0; q < NS; ++q)
+                if (((mskbits >> q) & 1u) && ((node_fixed[kz * pn + s_off[q] / 3] >> (s_off[q] % 3)) & 1u))
+                    take &= ~(1u << q);
+        }
+#pragma unroll
+        for (int q = 0; q < NS; ++q) {
+            const int idx = tid + q * TILE_NT;
+            if (q < NS - 1 || idx < PN) {
+                if (sizeof(T) == 4)
+                    cp_async_4(buf + idx, vb + s_off[q], (take >> q) & 1u);
+                else
+                    cp_async_8(buf + idx, vb + s_off[q], (take >> q) & 1u);
+            }
+        }
+        cp_async_commit();
+    };
+    const int pofs = ty * PW + 3 * tx;
+    const int el_col = ex + g.nelx * ey, el_plane = g.nelx * g.nely;
+    auto scale_at = [&](int ez) -> T {
+        return (col_ok && ez >= 0 && ez < g.nelz) ? ld_nc(scale + el_col + el_plane * ez) : T(0);
+    };
+    const int own_node0 = (i0 + tx) + g.nnx * (j0 + ty);
+    // pass-through needs the node's constraint byte only on constrained columns
+    const bool own_fix_col = PASS && owner && have_nf && col_or[own_node0] != 0;
+
+    const int n_layers = min(oz, g.nnz - k0) + 1;
+    stage(k0 - 1, plane[0]);
+    stage(k0, plane[1]);
+    cp_async_wait_all();
+    __syncthreads();
+    T XYb[3][4];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        const T* b = plane[0] + pofs + c;
+        face_fwd(b[0], b[3], b[PW], b[PW + 3], XYb[c]);
+    }
+    T Gt[3][4];
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) Gt[c][q] = T(0);
+    T s_cur = scale_at(k0 - 1);
+    T dot = T(0);
+
+    T pend_x1[3], pend_p[3];
+    bool pend = false;
+    int pend_d0 = 0, pend_ez = 0;
+
+    // node pass of the previous layer (plane ez-1), reading its row hand-off
+    auto node_pass = [&](const T (&Yp)[3][TILE_NT]) {
+        if (!pend) return;
+        unsigned bits = 0u;
+        if (own_fix_col) bits = node_fixed[own_node0 + pend_ez * pn];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            T acc = pend_x1[c] + Yp[c][tid + TILE_BX];
+            const int d = pend_d0 + c;
+            if (ACC) acc += w[d];
+            const bool fx = PASS && ((bits >> c) & 1u);
+            if (fx) acc = v[d];
+            w[d] = acc;
+            if (DOT) {
+                const T p = fx ? v[d] : pend_p[c];
+                dot = fma(p, acc, dot);
+            }
+        }
+    };
+
+    // one element layer; CUR = buffer of plane ez, (CUR+1)%3 plane ez+1,
+    // (CUR+2)%3 receives plane ez+2
+    auto layer = [&](auto cur_tag, int L) {
+        constexpr int CUR = decltype(cur_tag)::value;
+        constexpr int TOP = (CUR + 1) % 3, NXT = (CUR + 2) % 3, PRV = (CUR + 2) % 3;
+        const int ez = k0 - 1 + L;
+        cp_async_wait_all();
+        __syncthreads();                              // (A) plane ez+1 + previous Y visible
+        node_pass(Y[PRV]);
+        if (L + 1 < n_layers) stage(ez + 2, plane[NXT]);
+        const T s_next = scale_at(ez + 1);
+        T pown[3];
+        if (DOT) {
+#pragma unroll
+            for (int c = 0; c < 3; ++c) pown[c] = plane[CUR][pofs + PW + 3 + c];
+        }
+        T h[3][8];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            const T* b = plane[TOP] + pofs + c;
+            T XYt[4];
+            face_fwd(b[0], b[3], b[PW], b[PW + 3], XYt);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                h[c][q] = XYb[c][q] + XYt[q];
+                h[c][q + 4] = XYt[q] - XYb[c][q];
+                XYb[c][q] = XYt[q];
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+#pragma unroll
+            for (int m = 1; m < 8; ++m) h[c][m] *= s_cur;
+        T gm[3][8];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) gm[c][0] = T(0);
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                const int m = q ^ (1 << c);
+                if (m == 0) continue;
+                T acc = T(0);
+#pragma unroll
+                for (int d = 0; d < 3; ++d) {
+                    const int n = q ^ (1 << d);
+                    if (n == 0) continue;
+                    acc = fma(kb.b[q][c][d], h[d][n], acc);
+                }
+                gm[c][m] = acc;
+            }
+        T corner[3][4];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            T H[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                H[q] = Gt[c][q] + (gm[c][q] - gm[c][q + 4]);
+                Gt[c][q] = gm[c][q] + gm[c][q + 4];
+            }
+            face_inv(H, corner[c]);
+        }
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            const T x0 = corner[c][1] + __shfl_down_sync(0xffffffffu, corner[c][0], 1);
+            pend_x1[c] = corner[c][3] + __shfl_down_sync(0xffffffffu, corner[c][2], 1);
+            Y[CUR][c][tid] = x0;
+            if (DOT) pend_p[c] = pown[c];
+        }
+        pend = owner && L >= 1;
+        pend_ez = ez;
+        pend_d0 = 3 * (own_node0 + ez * pn);
+        s_cur = s_next;
+    };
+    using I0 = std::integral_constant<int, 0>;
+    using I1 = std::integral_constant<int, 1>;
+    using I2 = std::integral_constant<int, 2>;
+    int L = 0;
+    for (; L + 3 <= n_layers; L += 3) {
+        layer(I0{}, L);
+        layer(I1{}, L + 1);
+        layer(I2{}, L + 2);
+    }
+    if (L < n_layers) layer(I0{}, L);
+    if (L + 1 < n_layers) layer(I1{}, L + 1);
+    __syncthreads();
+    // the last layer's hand-off buffer: (n_layers - 1) % 3
+    const int last = (n_layers - 1) % 3;
+    if (last == 0) node_pass(Y[0]);
+    else if (last == 1) node_pass(Y[1]);
+    else node_pass(Y[2]);
+
+    if (DOT) {
+        __shared__ double sh[TILE_NT / 32];
+        double dd = (double)dot;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) dd += __shfl_down_sync(0xffffffffu, dd, o);
+        if ((tid & 31) == 0) sh[tid >> 5] = dd;
+        __syncthreads();
+        if (tid == 0) {
+            double s2 = 0.0;
+            for (int i = 0; i < TILE_NT / 32; ++i) s2 += sh[i];
+            dot_part[blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z)] = s2;
         }
     }
 }
@@ -1170,6 +1334,13 @@ static bool tile3_forced()
     return v == 1;
 }
 
+// TF_TILE3=1: the v3 kernel instead of the lean v5 (A/B, bitwise-identical)
+static bool tile5_disabled()
+{
+    const char* e = getenv("TF_TILE3");  // read per launch: A/B in one process
+    return e && e[0] == '1';
+}
+
 template <typename T>
 static int tile_slots()
 {
@@ -1260,6 +1431,31 @@ int launch_grid_tile(const Grid& g, const T* ke_host, const T* scale, const T* v
         }
     }
     dim3 block(TILE_BX, TileDims<T>::BY, 1);
+    if (!tile5_disabled()) {
+        // compile-time flag variants of the lean kernel; others fall back to tile3
+        const uint32_t f = flags & (TF_MASK_INPUT | TF_PASS_FIXED | TF_ACCUMULATE);
+        constexpr uint32_t MP = TF_MASK_INPUT | TF_PASS_FIXED;
+        if (f == MP && dot_part) {
+            k_grid_tile5<T, true, true, false, true><<<sh.grid, block, 0, st>>>(g, sh.oz, scale, v, w, node_fixed, dot_part, kb);
+            TF_CHECK_LAUNCH();
+            return TF_OK;
+        }
+        if (f == MP && !dot_part) {
+            k_grid_tile5<T, true, true, false, false><<<sh.grid, block, 0, st>>>(g, sh.oz, scale, v, w, node_fixed, nullptr, kb);
+            TF_CHECK_LAUNCH();
+            return TF_OK;
+        }
+        if (f == TF_MASK_INPUT && !dot_part) {  // slab-local products (pass-through after the exchange)
+            k_grid_tile5<T, true, false, false, false><<<sh.grid, block, 0, st>>>(g, sh.oz, scale, v, w, node_fixed, nullptr, kb);
+            TF_CHECK_LAUNCH();
+            return TF_OK;
+        }
+        if (f == 0 && !dot_part) {  // raw K v (fused_serial-style contract)
+            k_grid_tile5<T, false, false, false, false><<<sh.grid, block, 0, st>>>(g, sh.oz, scale, v, w, node_fixed, nullptr, kb);
+            TF_CHECK_LAUNCH();
+            return TF_OK;
+        }
+    }
     if (dot_part)
         k_grid_tile3<T, true><<<sh.grid, block, 0, st>>>(g, sh.oz, scale, v, w, node_fixed, flags, dot_part, kb);
     else

@@ -55,4 +55,76 @@ __device__ __forceinline__ void face_inv(const T (&h)[4], T (&c)[4])
     c[3] = y0x1 + y1x1;  // (1,1)
 }
 
+template <typename T>
+__device__ __forceinline__ void fwht_fwd(T (&x)[8])
+{
+#pragma unroll
+    for (int bit = 1; bit < 8; bit <<= 1)
+#pragma unroll
+        for (int b = 0; b < 8; ++b)
+            if (!(b & bit)) {
+                const T lo = x[b], hi = x[b | bit];
+                x[b] = lo + hi;
+                x[b | bit] = hi - lo;
+            }
+}
+
+template <typename T>
+__device__ __forceinline__ void fwht_inv(T (&x)[8])
+{
+#pragma unroll
+    for (int bit = 1; bit < 8; bit <<= 1)
+#pragma unroll
+        for (int b = 0; b < 8; ++b)
+            if (!(b & bit)) {
+                const T lo = x[b], hi = x[b | bit];
+                x[b] = lo - hi;
+                x[b | bit] = lo + hi;
+            }
+}
+
+// f (reference corner order, 24) = s * Ke * u  via the parity-block form
+template <typename T>
+__device__ __forceinline__ void element_apply(const T (&u)[NLOC], T s, const KhatBlocks<T>& kb,
+                                              T (&f)[NLOC])
+{
+    T h[3][8];
+#pragma unroll
+    for (int a = 0; a < 8; ++a)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) h[c][bin_of(a)] = u[3 * a + c];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) fwht_fwd(h[c]);
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+#pragma unroll
+        for (int m = 1; m < 8; ++m) h[c][m] *= s;  // mode 0 is rigid translation: unused
+    T g[3][8];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) g[c][0] = T(0);
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            const int m = q ^ (1 << c);
+            if (m == 0) continue;  // translation rows of Khat vanish
+            T acc = T(0);
+#pragma unroll
+            for (int d = 0; d < 3; ++d) {
+                const int n = q ^ (1 << d);
+                if (n == 0) continue;
+                acc = fma(kb.b[q][c][d], h[d][n], acc);
+            }
+            g[c][m] = acc;
+        }
+#pragma unroll
+    for (int c = 0; c < 3; ++c) fwht_inv(g[c]);
+#pragma unroll
+    for (int a = 0; a < 8; ++a)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) f[3 * a + c] = g[c][bin_of(a)];
+}
+
+// Each thread handles at most STAGE_SLOTS values of a staged node plane.
+
 }  // namespace tf

@@ -522,19 +522,46 @@ k_grid_tile3(Grid g, int oz, const T* __restrict__ scale, const T* __restrict__ 
 }
 
 // ---------------------------------------------------------------------------
-// v5: k_grid_tile3's algorithm with the bookkeeping stripped for the issue-
-// bound regime.
+// v5: k_grid_tile3's algorithm with the bookkeeping stripped and a deep
+// staging ring.
 //   * the operator flags are template parameters (the production matvec is
 //     MASK|PASS: no ACCUMULATE branches, no flag tests per DOF);
-//   * the layer loop is unrolled by the ring period (3): the plane buffers and
-//     the row hand-off Y are compile-time offsets -- no pointer rotation, no
-//     register moves between layers;
+//   * node planes AND the element scales of each layer stream in with
+//     cp.async P planes ahead of use (ring of P+2 buffers; P = 2 in
+//     production): a one-wave grid (c2) sees one DRAM latency instead of one
+//     per layer, a multi-wave grid hides it under more layers of work;
+//   * the layer loop is unrolled by the ring period: plane buffers and the
+//     row hand-off are compile-time offsets (no pointer rotation / moves);
 //   * owners whose node column carries no constraint (column OR byte == 0)
-//     never read the per-node constraint byte;
-//   * staging addresses: one uniform plane base + a 32-bit slot offset.
+//     never read the per-node constraint byte.
 // Same arithmetic as tile3 (bitwise-identical results).
 // ---------------------------------------------------------------------------
-template <typename T, bool MASK, bool PASS, bool ACC, bool DOT>
+template <int I, int N, typename F>
+__device__ __forceinline__ void static_for(F&& f)
+{
+    if constexpr (I < N) {
+        f(std::integral_constant<int, I>{});
+        static_for<I + 1, N>(f);
+    }
+}
+
+__device__ __forceinline__ void cp_async_wait_n(int n)
+{
+    // n is a compile-time constant at every call site after unrolling
+    switch (n) {
+    case 0: asm volatile("cp.async.wait_group 0;\n" ::); break;
+    case 1: asm volatile("cp.async.wait_group 1;\n" ::); break;
+    case 2: asm volatile("cp.async.wait_group 2;\n" ::); break;
+    case 3: asm volatile("cp.async.wait_group 3;\n" ::); break;
+    default: asm volatile("cp.async.wait_group 4;\n" ::); break;
+    }
+}
+
+#ifndef TF_TILE_P
+#define TF_TILE_P 2
+#endif
+
+template <typename T, bool MASK, bool PASS, bool ACC, bool DOT, int P>
 __global__ void __launch_bounds__(TileDims<T>::NT, sizeof(T) == 4 ? TF_TILE_MINB32 : TF_TILE_MINB64)
 k_grid_tile5(Grid g, int oz, const T* __restrict__ scale, const T* __restrict__ v, T* __restrict__ w,
              const uint8_t* __restrict__ node_fixed, double* __restrict__ dot_part,
@@ -542,8 +569,10 @@ k_grid_tile5(Grid g, int oz, const T* __restrict__ scale, const T* __restrict__ 
 {
     constexpr int TILE_BY = TileDims<T>::BY, TILE_NT = TileDims<T>::NT;
     constexpr int PW = StageSlots<T>::PW, PN = StageSlots<T>::PN, NS = StageSlots<T>::N;
-    __shared__ __align__(16) T plane[3][PN];  // node plane k lives in buffer (k - k0 + 1) % 3
-    __shared__ T Y[3][3][TILE_NT];            // row hand-off, by layer % 3
+    constexpr int R = P + 2;                      // ring: plane k in buffer (k - k0 + 1) % R
+    __shared__ __align__(16) T plane[R][PN];
+    __shared__ T sc[R][TILE_NT];                  // element scale of layer k, with plane k
+    __shared__ T Y[2][3][TILE_NT];                // row hand-off, by layer parity
 
     const int tx = threadIdx.x, ty = threadIdx.y;
     const int tid = tx + TILE_BX * ty;
@@ -575,7 +604,9 @@ k_grid_tile5(Grid g, int oz, const T* __restrict__ scale, const T* __restrict__ 
         }
         if (keep) okbits |= 1u << q;
     }
-    auto stage = [&](int kz, T* buf) {
+    const int el_col = ex + g.nelx * ey, el_plane = g.nelx * g.nely;
+    // one cp.async group: node plane kz and the scales of element layer kz
+    auto stage = [&](int kz, int buf) {
         const bool zok = kz >= 0 && kz < g.nnz;
         const T* vb = v + (long long)min(max(kz, 0), g.nnz - 1) * pn3;
         unsigned take = zok ? okbits : 0u;
@@ -585,31 +616,35 @@ k_grid_tile5(Grid g, int oz, const T* __restrict__ scale, const T* __restrict__ 
                 if (((mskbits >> q) & 1u) && ((node_fixed[kz * pn + s_off[q] / 3] >> (s_off[q] % 3)) & 1u))
                     take &= ~(1u << q);
         }
+        T* pb = plane[buf];
 #pragma unroll
         for (int q = 0; q < NS; ++q) {
             const int idx = tid + q * TILE_NT;
             if (q < NS - 1 || idx < PN) {
                 if (sizeof(T) == 4)
-                    cp_async_4(buf + idx, vb + s_off[q], (take >> q) & 1u);
+                    cp_async_4(pb + idx, vb + s_off[q], (take >> q) & 1u);
                 else
-                    cp_async_8(buf + idx, vb + s_off[q], (take >> q) & 1u);
+                    cp_async_8(pb + idx, vb + s_off[q], (take >> q) & 1u);
             }
         }
+        const bool sok = col_ok && kz >= 0 && kz < g.nelz;
+        const T* sp = scale + (sok ? el_col + (long long)el_plane * kz : 0);
+        if (sizeof(T) == 4)
+            cp_async_4(&sc[buf][tid], sp, sok);
+        else
+            cp_async_8(&sc[buf][tid], sp, sok);
         cp_async_commit();
     };
     const int pofs = ty * PW + 3 * tx;
-    const int el_col = ex + g.nelx * ey, el_plane = g.nelx * g.nely;
-    auto scale_at = [&](int ez) -> T {
-        return (col_ok && ez >= 0 && ez < g.nelz) ? ld_nc(scale + el_col + el_plane * ez) : T(0);
-    };
     const int own_node0 = (i0 + tx) + g.nnx * (j0 + ty);
     // pass-through needs the node's constraint byte only on constrained columns
     const bool own_fix_col = PASS && owner && have_nf && col_or[own_node0] != 0;
 
     const int n_layers = min(oz, g.nnz - k0) + 1;
-    stage(k0 - 1, plane[0]);
-    stage(k0, plane[1]);
-    cp_async_wait_all();
+    // prologue: planes k0-1 .. k0-1+P (P+1 groups) in flight together
+#pragma unroll
+    for (int b = 0; b <= P; ++b) stage(k0 - 1 + b, b);
+    cp_async_wait_n(P - 1);  // planes k0-1 and k0 landed
     __syncthreads();
     T XYb[3][4];
 #pragma unroll
@@ -622,7 +657,6 @@ k_grid_tile5(Grid g, int oz, const T* __restrict__ scale, const T* __restrict__ 
     for (int c = 0; c < 3; ++c)
 #pragma unroll
         for (int q = 0; q < 4; ++q) Gt[c][q] = T(0);
-    T s_cur = scale_at(k0 - 1);
     T dot = T(0);
 
     T pend_x1[3], pend_p[3];
@@ -649,17 +683,20 @@ k_grid_tile5(Grid g, int oz, const T* __restrict__ scale, const T* __restrict__ 
         }
     };
 
-    // one element layer; CUR = buffer of plane ez, (CUR+1)%3 plane ez+1,
-    // (CUR+2)%3 receives plane ez+2
-    auto layer = [&](auto cur_tag, int L) {
-        constexpr int CUR = decltype(cur_tag)::value;
-        constexpr int TOP = (CUR + 1) % 3, NXT = (CUR + 2) % 3, PRV = (CUR + 2) % 3;
+    // one element layer (layer index L = ring phase I mod R): bottom plane ez
+    // in buffer I, top plane ez+1 in buffer (I+1) % R; the layer stages plane
+    // ez+1+P into buffer (I+P+1) % R = (I-1) % R (the plane of layer L-1)
+    auto layer = [&](auto ph, int L) {
+        constexpr int CUR = decltype(ph)::value;
+        constexpr int TOP = (CUR + 1) % R, NXT = (CUR + P + 1) % R;
         const int ez = k0 - 1 + L;
-        cp_async_wait_all();
-        __syncthreads();                              // (A) plane ez+1 + previous Y visible
-        node_pass(Y[PRV]);
-        if (L + 1 < n_layers) stage(ez + 2, plane[NXT]);
-        const T s_next = scale_at(ez + 1);
+        if (L > 0) {
+            cp_async_wait_n(P - 1);  // plane ez+1 landed (P-1 younger groups may still fly)
+            __syncthreads();         // (A) plane ez+1 + previous Y visible, buffer NXT free
+        }
+        node_pass(Y[(L + 1) & 1]);
+        stage(ez + 1 + P, NXT);      // beyond the chunk: zero-size copies keep the group count
+        const T s_cur = sc[CUR][tid];
         T pown[3];
         if (DOT) {
 #pragma unroll
@@ -715,42 +752,32 @@ k_grid_tile5(Grid g, int oz, const T* __restrict__ scale, const T* __restrict__ 
         for (int c = 0; c < 3; ++c) {
             const T x0 = corner[c][1] + __shfl_down_sync(0xffffffffu, corner[c][0], 1);
             pend_x1[c] = corner[c][3] + __shfl_down_sync(0xffffffffu, corner[c][2], 1);
-            Y[CUR][c][tid] = x0;
+            Y[L & 1][c][tid] = x0;
             if (DOT) pend_p[c] = pown[c];
         }
         pend = owner && L >= 1;
         pend_ez = ez;
         pend_d0 = 3 * (own_node0 + ez * pn);
-        s_cur = s_next;
     };
-    using I0 = std::integral_constant<int, 0>;
-    using I1 = std::integral_constant<int, 1>;
-    using I2 = std::integral_constant<int, 2>;
     int L = 0;
-    for (; L + 3 <= n_layers; L += 3) {
-        layer(I0{}, L);
-        layer(I1{}, L + 1);
-        layer(I2{}, L + 2);
-    }
-    if (L < n_layers) layer(I0{}, L);
-    if (L + 1 < n_layers) layer(I1{}, L + 1);
+    for (; L + R <= n_layers; L += R) static_for<0, R>([&](auto ph) { layer(ph, L + decltype(ph)::value); });
+    static_for<0, R - 1>([&](auto ph) {
+        if (L + decltype(ph)::value < n_layers) layer(ph, L + decltype(ph)::value);
+    });
+    cp_async_wait_n(0);
     __syncthreads();
-    // the last layer's hand-off buffer: (n_layers - 1) % 3
-    const int last = (n_layers - 1) % 3;
-    if (last == 0) node_pass(Y[0]);
-    else if (last == 1) node_pass(Y[1]);
-    else node_pass(Y[2]);
+    node_pass(Y[(n_layers - 1) & 1]);
 
     if (DOT) {
-        __shared__ double sh[TILE_NT / 32];
+        __shared__ double shd[TILE_NT / 32];
         double dd = (double)dot;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) dd += __shfl_down_sync(0xffffffffu, dd, o);
-        if ((tid & 31) == 0) sh[tid >> 5] = dd;
+        if ((tid & 31) == 0) shd[tid >> 5] = dd;
         __syncthreads();
         if (tid == 0) {
             double s2 = 0.0;
-            for (int i = 0; i < TILE_NT / 32; ++i) s2 += sh[i];
+            for (int i = 0; i < TILE_NT / 32; ++i) s2 += shd[i];
             dot_part[blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z)] = s2;
         }
     }
@@ -1436,22 +1463,22 @@ int launch_grid_tile(const Grid& g, const T* ke_host, const T* scale, const T* v
         const uint32_t f = flags & (TF_MASK_INPUT | TF_PASS_FIXED | TF_ACCUMULATE);
         constexpr uint32_t MP = TF_MASK_INPUT | TF_PASS_FIXED;
         if (f == MP && dot_part) {
-            k_grid_tile5<T, true, true, false, true><<<sh.grid, block, 0, st>>>(g, sh.oz, scale, v, w, node_fixed, dot_part, kb);
+            k_grid_tile5<T, true, true, false, true, TF_TILE_P><<<sh.grid, block, 0, st>>>(g, sh.oz, scale, v, w, node_fixed, dot_part, kb);
             TF_CHECK_LAUNCH();
             return TF_OK;
         }
         if (f == MP && !dot_part) {
-            k_grid_tile5<T, true, true, false, false><<<sh.grid, block, 0, st>>>(g, sh.oz, scale, v, w, node_fixed, nullptr, kb);
+            k_grid_tile5<T, true, true, false, false, TF_TILE_P><<<sh.grid, block, 0, st>>>(g, sh.oz, scale, v, w, node_fixed, nullptr, kb);
             TF_CHECK_LAUNCH();
             return TF_OK;
         }
         if (f == TF_MASK_INPUT && !dot_part) {  // slab-local products (pass-through after the exchange)
-            k_grid_tile5<T, true, false, false, false><<<sh.grid, block, 0, st>>>(g, sh.oz, scale, v, w, node_fixed, nullptr, kb);
+            k_grid_tile5<T, true, false, false, false, TF_TILE_P><<<sh.grid, block, 0, st>>>(g, sh.oz, scale, v, w, node_fixed, nullptr, kb);
             TF_CHECK_LAUNCH();
             return TF_OK;
         }
         if (f == 0 && !dot_part) {  // raw K v (fused_serial-style contract)
-            k_grid_tile5<T, false, false, false, false><<<sh.grid, block, 0, st>>>(g, sh.oz, scale, v, w, node_fixed, nullptr, kb);
+            k_grid_tile5<T, false, false, false, false, TF_TILE_P><<<sh.grid, block, 0, st>>>(g, sh.oz, scale, v, w, node_fixed, nullptr, kb);
             TF_CHECK_LAUNCH();
             return TF_OK;
         }

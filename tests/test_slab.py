@@ -159,7 +159,10 @@ def _run_slab(world, dims, prec, device, max_iter=1000):
         d64 = oracle.diagonal(edof, ke64, s64, bcs.fixed_dofs, m.n_dof)
         x64, _ = oracle.pcg(lambda x: oracle.apply(edof, ke64, s64, x, bcs.fixed_dofs, m.n_dof),
                             bcs.force, d64, max_iter=max_iter)
-        xtol = max(xtol, 2.0 * np.abs(x_ref - x64).max())
+        # 4x: slab and oracle round their FP32 dots differently (FP64 all-reduce
+        # vs numpy sdot); the FP32/FP64 spread bounds the recurrence's
+        # round-off amplification, not the exact gap between two FP32 runs
+        xtol = max(xtol, 4.0 * np.abs(x_ref - x64).max())
     for rank, g2l, w, d, x, info in res:
         assert np.abs(w - w_ref[g2l]).max() <= tol * np.abs(w_ref).max()
         assert np.abs(d - d_ref[g2l]).max() <= tol * np.abs(d_ref).max()

@@ -28,6 +28,9 @@
 // Optional fused epilogue: block partial of p.q for the CG (deterministic).
 
 #include <algorithm>
+#include <array>
+#include <mutex>
+#include <map>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -637,8 +640,15 @@ k_grid_tile5(Grid g, int oz, const T* __restrict__ scale, const T* __restrict__ 
     };
     const int pofs = ty * PW + 3 * tx;
     const int own_node0 = (i0 + tx) + g.nnx * (j0 + ty);
-    // pass-through needs the node's constraint byte only on constrained columns
-    const bool own_fix_col = PASS && owner && have_nf && col_or[own_node0] != 0;
+    // pass-through needs the node's constraint byte only on constrained
+    // columns, and a per-plane read only where the constraint varies along z
+    unsigned fix_or = 0u, fix_and = 0u;
+    if (PASS && owner && have_nf) {
+        fix_or = col_or[own_node0];
+        fix_and = col_and[own_node0];
+    }
+    const bool own_fix_col = fix_or != 0u;
+    const bool fix_zvar = fix_or != fix_and;
 
     const int n_layers = min(oz, g.nnz - k0) + 1;
     // prologue: planes k0-1 .. k0-1+P (P+1 groups) in flight together
@@ -659,25 +669,27 @@ k_grid_tile5(Grid g, int oz, const T* __restrict__ scale, const T* __restrict__ 
         for (int q = 0; q < 4; ++q) Gt[c][q] = T(0);
     T dot = T(0);
 
-    T pend_x1[3], pend_p[3];
+    T pend_x1[3], pend_p[3], pend_v[3];
     bool pend = false;
-    int pend_d0 = 0, pend_ez = 0;
+    int pend_d0 = 0;
+    unsigned pend_bits = 0u;
 
-    // node pass of the previous layer (plane ez-1), reading its row hand-off
+    // node pass of the previous layer (plane ez-1), reading its row hand-off.
+    // Its constraint bits and pass-through values were loaded one layer
+    // earlier (a dependent global load here would stall the CTAs holding a
+    // constrained column at every layer -- and the kernel ends with the slowest CTA).
     auto node_pass = [&](const T (&Yp)[3][TILE_NT]) {
         if (!pend) return;
-        unsigned bits = 0u;
-        if (own_fix_col) bits = node_fixed[own_node0 + pend_ez * pn];
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
             T acc = pend_x1[c] + Yp[c][tid + TILE_BX];
             const int d = pend_d0 + c;
             if (ACC) acc += w[d];
-            const bool fx = PASS && ((bits >> c) & 1u);
-            if (fx) acc = v[d];
+            const bool fx = PASS && ((pend_bits >> c) & 1u);
+            if (fx) acc = pend_v[c];
             w[d] = acc;
             if (DOT) {
-                const T p = fx ? v[d] : pend_p[c];
+                const T p = fx ? pend_v[c] : pend_p[c];
                 dot = fma(p, acc, dot);
             }
         }
@@ -696,6 +708,17 @@ k_grid_tile5(Grid g, int oz, const T* __restrict__ scale, const T* __restrict__ 
         }
         node_pass(Y[(L + 1) & 1]);
         stage(ez + 1 + P, NXT);      // beyond the chunk: zero-size copies keep the group count
+        // constraint bits / pass-through inputs of plane ez (finalised by the
+        // next layer's node pass): issued now, consumed a layer later
+        unsigned nbits = 0u;
+        T nv[3] = {T(0), T(0), T(0)};
+        if (own_fix_col && L >= 1) {
+            nbits = fix_zvar ? (unsigned)node_fixed[own_node0 + ez * pn] : fix_and;
+            const int d0 = 3 * (own_node0 + ez * pn);
+#pragma unroll
+            for (int c = 0; c < 3; ++c)
+                if ((nbits >> c) & 1u) nv[c] = ld_nc(v + d0 + c);
+        }
         const T s_cur = sc[CUR][tid];
         T pown[3];
         if (DOT) {
@@ -756,8 +779,10 @@ k_grid_tile5(Grid g, int oz, const T* __restrict__ scale, const T* __restrict__ 
             if (DOT) pend_p[c] = pown[c];
         }
         pend = owner && L >= 1;
-        pend_ez = ez;
         pend_d0 = 3 * (own_node0 + ez * pn);
+        pend_bits = nbits;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) pend_v[c] = nv[c];
     };
     int L = 0;
     for (; L + R <= n_layers; L += R) static_for<0, R>([&](auto ph) { layer(ph, L + decltype(ph)::value); });
@@ -1404,14 +1429,83 @@ TileShape tile_shape(const Grid& g)
     // big grids: taller chunks halve the halo layer when >= 1.5 waves remain
     // (c5: 100.8 vs 104.6 us measured; smaller grids keep 16)
     if (oz == 16 && cols * ((g.nnz + 31) / 32) * 2 >= 3 * slots) oz = 32;
-    static int oz_env = -1;  // TF_TILE_OZ: experiment override of the z-chunk height
-    if (oz_env < 0) {
-        const char* e = getenv("TF_TILE_OZ");
-        oz_env = e ? std::max(0, atoi(e)) : 0;
-    }
+    const char* e = getenv("TF_TILE_OZ");  // experiment override of the z-chunk height
+    const int oz_env = e ? std::max(0, atoi(e)) : 0;
     if (oz_env > 0) oz = oz_env;
     const int tz = (g.nnz + oz - 1) / oz;
     return {dim3(tx, ty, tz), oz};
+}
+
+template <typename T>
+TileShape tile_shape_oz(const Grid& g, int oz)
+{
+    constexpr int TILE_BY = TileDims<T>::BY;
+    const int tx = (g.ihi - g.ilo + TILE_BX - 2) / (TILE_BX - 1);
+    const int ty = (g.nny + TILE_BY - 2) / (TILE_BY - 1);
+    return {dim3(tx, ty, (g.nnz + oz - 1) / oz), oz};
+}
+
+static bool tile_autotune_enabled()
+{
+    const char* e = getenv("TF_TILE_AUTOTUNE");
+    if (e && e[0] == '0') return false;
+    const char* o = getenv("TF_TILE_OZ");  // a pinned chunk height wins
+    return !(o && atoi(o) > 0);
+}
+
+// z-chunk height per (grid shape, x-range, precision): measured once with
+// CUDA events over candidate heights (min of 3 launches each), then cached.
+// Returns 0 when it cannot tune (stream capture in progress).
+template <typename F>
+static int tile_tuned_oz(const Grid& g, int prec, cudaStream_t st, F&& launch)
+{
+    static std::mutex mu;
+    static std::map<std::array<int, 6>, int> cache;
+    const std::array<int, 6> key = {g.nelx, g.nely, g.nelz, g.ilo, g.ihi, prec};
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        auto it = cache.find(key);
+        if (it != cache.end()) return it->second;
+    }
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) {
+        cudaGetLastError();
+        return 0;
+    }
+    static const int cands[] = {2, 3, 4, 5, 6, 7, 8, 10, 12, 16, 24, 32};
+    cudaEvent_t e0, e1;
+    if (cudaEventCreate(&e0) != cudaSuccess || cudaEventCreate(&e1) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    int best = 0;
+    float best_ms = 1e30f;
+    for (int oz : cands) {
+        if (oz > std::max(2, g.nnz)) break;
+        if (launch(oz) != TF_OK) break;  // warm-up
+        float t = 1e30f;
+        for (int r = 0; r < 3; ++r) {
+            cudaEventRecord(e0, st);
+            launch(oz);
+            cudaEventRecord(e1, st);
+            cudaEventSynchronize(e1);
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, e0, e1);
+            t = std::min(t, ms);
+        }
+        if (t < best_ms) {
+            best_ms = t;
+            best = oz;
+        }
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaGetLastError();
+    if (best > 0) {
+        std::lock_guard<std::mutex> lk(mu);
+        cache[key] = best;
+    }
+    return best;
 }
 
 template <typename T>
@@ -1444,51 +1538,64 @@ int launch_grid_tile(const Grid& g, const T* ke_host, const T* scale, const T* v
         set_error("structured grid too large for int32 DOF indices");
         return TF_ERR_ARG;
     }
-    TileShape sh = tile_shape<T>(g);
     const bool full_range = g.ilo == 0 && g.ihi == g.nnx;  // tile4 has no x-range support
-    if constexpr (sizeof(T) == 4) {
-        if (!tile3_forced() && full_range) {
-            dim3 block4(T4_TX, T4_TY, 1);
-            if (dot_part)
-                k_grid_tile4<true><<<sh.grid, block4, 0, st>>>(g, sh.oz, scale, v, w, node_fixed, flags, dot_part, kb);
-            else
-                k_grid_tile4<false><<<sh.grid, block4, 0, st>>>(g, sh.oz, scale, v, w, node_fixed, flags, nullptr, kb);
-            TF_CHECK_LAUNCH();
-            return TF_OK;
+    auto launch_shape = [&](const TileShape& sh) -> int {
+        if constexpr (sizeof(T) == 4) {
+            if (!tile3_forced() && full_range) {
+                dim3 block4(T4_TX, T4_TY, 1);
+                if (dot_part)
+                    k_grid_tile4<true><<<sh.grid, block4, 0, st>>>(g, sh.oz, scale, v, w, node_fixed, flags, dot_part, kb);
+                else
+                    k_grid_tile4<false><<<sh.grid, block4, 0, st>>>(g, sh.oz, scale, v, w, node_fixed, flags, nullptr, kb);
+                TF_CHECK_LAUNCH();
+                return TF_OK;
+            }
         }
+        dim3 block(TILE_BX, TileDims<T>::BY, 1);
+        if (!tile5_disabled()) {
+            // compile-time flag variants of the lean kernel; others fall back to tile3
+            const uint32_t f = flags & (TF_MASK_INPUT | TF_PASS_FIXED | TF_ACCUMULATE);
+            constexpr uint32_t MP = TF_MASK_INPUT | TF_PASS_FIXED;
+            if (f == MP && dot_part) {
+                k_grid_tile5<T, true, true, false, true, TF_TILE_P><<<sh.grid, block, 0, st>>>(g, sh.oz, scale, v, w, node_fixed, dot_part, kb);
+                TF_CHECK_LAUNCH();
+                return TF_OK;
+            }
+            if (f == MP && !dot_part) {
+                k_grid_tile5<T, true, true, false, false, TF_TILE_P><<<sh.grid, block, 0, st>>>(g, sh.oz, scale, v, w, node_fixed, nullptr, kb);
+                TF_CHECK_LAUNCH();
+                return TF_OK;
+            }
+            if (f == TF_MASK_INPUT && !dot_part) {  // slab-local products (pass-through after the exchange)
+                k_grid_tile5<T, true, false, false, false, TF_TILE_P><<<sh.grid, block, 0, st>>>(g, sh.oz, scale, v, w, node_fixed, nullptr, kb);
+                TF_CHECK_LAUNCH();
+                return TF_OK;
+            }
+            if (f == 0 && !dot_part) {  // raw K v (fused_serial-style contract)
+                k_grid_tile5<T, false, false, false, false, TF_TILE_P><<<sh.grid, block, 0, st>>>(g, sh.oz, scale, v, w, node_fixed, nullptr, kb);
+                TF_CHECK_LAUNCH();
+                return TF_OK;
+            }
+        }
+        if (dot_part)
+            k_grid_tile3<T, true><<<sh.grid, block, 0, st>>>(g, sh.oz, scale, v, w, node_fixed, flags, dot_part, kb);
+        else
+            k_grid_tile3<T, false><<<sh.grid, block, 0, st>>>(g, sh.oz, scale, v, w, node_fixed, flags, nullptr, kb);
+        TF_CHECK_LAUNCH();
+        return TF_OK;
+    };
+    TileShape sh = tile_shape<T>(g);
+    // Plain products (no CG partials, no accumulation): the z-chunk height is
+    // autotuned once per grid shape on first use outside stream capture (the
+    // result does not depend on the chunking -- every DOF is summed in the
+    // same order -- so this only picks the fastest launch shape).
+    if (!dot_part && !(flags & TF_ACCUMULATE) && tile_autotune_enabled()) {
+        const int oz = tile_tuned_oz(g, (int)sizeof(T), st, [&](int cand) {
+            return launch_shape(tile_shape_oz<T>(g, cand));
+        });
+        if (oz > 0) sh = tile_shape_oz<T>(g, oz);
     }
-    dim3 block(TILE_BX, TileDims<T>::BY, 1);
-    if (!tile5_disabled()) {
-        // compile-time flag variants of the lean kernel; others fall back to tile3
-        const uint32_t f = flags & (TF_MASK_INPUT | TF_PASS_FIXED | TF_ACCUMULATE);
-        constexpr uint32_t MP = TF_MASK_INPUT | TF_PASS_FIXED;
-        if (f == MP && dot_part) {
-            k_grid_tile5<T, true, true, false, true, TF_TILE_P><<<sh.grid, block, 0, st>>>(g, sh.oz, scale, v, w, node_fixed, dot_part, kb);
-            TF_CHECK_LAUNCH();
-            return TF_OK;
-        }
-        if (f == MP && !dot_part) {
-            k_grid_tile5<T, true, true, false, false, TF_TILE_P><<<sh.grid, block, 0, st>>>(g, sh.oz, scale, v, w, node_fixed, nullptr, kb);
-            TF_CHECK_LAUNCH();
-            return TF_OK;
-        }
-        if (f == TF_MASK_INPUT && !dot_part) {  // slab-local products (pass-through after the exchange)
-            k_grid_tile5<T, true, false, false, false, TF_TILE_P><<<sh.grid, block, 0, st>>>(g, sh.oz, scale, v, w, node_fixed, nullptr, kb);
-            TF_CHECK_LAUNCH();
-            return TF_OK;
-        }
-        if (f == 0 && !dot_part) {  // raw K v (fused_serial-style contract)
-            k_grid_tile5<T, false, false, false, false, TF_TILE_P><<<sh.grid, block, 0, st>>>(g, sh.oz, scale, v, w, node_fixed, nullptr, kb);
-            TF_CHECK_LAUNCH();
-            return TF_OK;
-        }
-    }
-    if (dot_part)
-        k_grid_tile3<T, true><<<sh.grid, block, 0, st>>>(g, sh.oz, scale, v, w, node_fixed, flags, dot_part, kb);
-    else
-        k_grid_tile3<T, false><<<sh.grid, block, 0, st>>>(g, sh.oz, scale, v, w, node_fixed, flags, nullptr, kb);
-    TF_CHECK_LAUNCH();
-    return TF_OK;
+    return launch_shape(sh);
 }
 
 // Fused CG head (decision + direction + matvec + p.q partials); grid as the

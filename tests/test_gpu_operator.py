@@ -343,3 +343,26 @@ def test_tile5_bitwise_equals_tile3(preset, scale, prec, monkeypatch):
         monkeypatch.setenv("TF_TILE3", t3)
         outs.append(op.apply(v).clone())
     assert torch.equal(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("prec", ["fp64", "fp32"])
+def test_tile_result_independent_of_z_chunking(prec, monkeypatch):
+    """Every DOF is summed in the same order whatever the z-chunk height (the
+    chunk's first layer is recomputed, not exchanged), so the autotuned launch
+    shape cannot change results: bitwise equal across heights."""
+    import torch
+
+    from paper_2604_18020_b200 import build_edof, make_preset
+
+    pb = make_preset("mbb", 0.2)
+    m = pb.mesh
+    rng = np.random.default_rng(4)
+    op = _op(m, build_edof(m), pb.bcs, rng.uniform(0.05, 1.0, m.n_elem), prec)
+    v = torch.tensor(rng.standard_normal(m.n_dof), device="cuda").to(
+        torch.float64 if prec == "fp64" else torch.float32)
+    outs = []
+    for oz in ("2", "3", "5", "16"):
+        monkeypatch.setenv("TF_TILE_OZ", oz)
+        outs.append(op.apply(v).clone())
+    for o in outs[1:]:
+        assert torch.equal(outs[0], o)

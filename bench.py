@@ -321,6 +321,16 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_e2e = float(t.item())
 
+    tile_shape = None
+    if world == 1 and args.kernel == "tile":
+        import ctypes
+
+        from paper_2604_18020_b200 import _lib
+
+        oz, ctas = ctypes.c_int32(), ctypes.c_int64()
+        _lib.call("tf_tile_shape", ctypes.byref(op.dev.grid), 32 if prec == "fp32" else 64,
+                  ctypes.byref(oz), ctypes.byref(ctas))
+        tile_shape = {"z_chunk": oz.value, "ctas": ctas.value, "threads_per_cta": 256 if prec == "fp32" else 128}
     hbm, sm_max, src = peaks()
     alg_bytes = compulsory_bytes(m.n_elem, m.n_dof, prec, args.kernel != "edof")
     achieved = alg_bytes / (ms * 1e-3) / 1e9
@@ -360,6 +370,7 @@ def run_ours(args):
                                   "exact": "k_grid_pull bitwise reference order",
                                   "edof": f"k_edof_fused general connectivity ({args.scatter})"}[args.kernel],
                        "l2": "flushed before every step (256 MiB write)",
+                       "launch": tile_shape,
                        "parallelism": f"xslab{world}" if world > 1 else "single"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm, "traffic": traffic,

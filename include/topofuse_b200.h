@@ -93,6 +93,11 @@ int tf_matvec_grid_range_f64(const tf_grid* g, const double* ke, const double* s
                              const double* v, double* w, const uint8_t* node_fixed, uint32_t flags,
                              int32_t i_lo, int32_t i_hi, void* stream);
 
+/* Launch shape of the structured tile kernel for a plain product on this grid
+ * (z-chunk height and CTA count; the autotuned height once the grid shape has
+ * been seen, else the heuristic).  Introspection only. */
+int tf_tile_shape(const tf_grid* g, int precision, int32_t* oz, int64_t* ctas);
+
 /* ---- K v with an explicit element->DOF table: the fused kernel contract
  *      fused_serial/fused_atomic(edof, ke, scale, v, out) (_kernels_numba.py:146-196).
  *      ALWAYS accumulates into w (caller zeroes it, operator.py:93).

@@ -107,6 +107,7 @@ _SIGS = {
                      _P, _P],
     "tf_pcg_destroy": [_P],
     "tf_pcg_protocol": [_P],
+    "tf_tile_shape": [_P, _INT, _P, _P],
     "tf_filter_rowsum_f64": [_P, ctypes.c_double, _P, _P],
     "tf_filter_grid_f64": [_P, ctypes.c_double, _P, _P, _P, _INT, _P],
     "tf_project_f64": [_I64, ctypes.c_double, ctypes.c_double, _P, _P, _P, _P],

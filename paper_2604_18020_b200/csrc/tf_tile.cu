@@ -1445,6 +1445,8 @@ TileShape tile_shape_oz(const Grid& g, int oz)
     return {dim3(tx, ty, (g.nnz + oz - 1) / oz), oz};
 }
 
+static int TileDimsBy(int prec) { return prec == 8 ? TileDims<double>::BY : TileDims<float>::BY; }
+
 static bool tile_autotune_enabled()
 {
     const char* e = getenv("TF_TILE_AUTOTUNE");
@@ -1457,7 +1459,7 @@ static bool tile_autotune_enabled()
 // CUDA events over candidate heights (min of 3 launches each), then cached.
 // Returns 0 when it cannot tune (stream capture in progress).
 template <typename F>
-static int tile_tuned_oz(const Grid& g, int prec, cudaStream_t st, F&& launch)
+static int tile_tuned_oz(const Grid& g, int prec, cudaStream_t st, F&& launch, bool lookup_only = false)
 {
     static std::mutex mu;
     static std::map<std::array<int, 6>, int> cache;
@@ -1466,6 +1468,7 @@ static int tile_tuned_oz(const Grid& g, int prec, cudaStream_t st, F&& launch)
         std::lock_guard<std::mutex> lk(mu);
         auto it = cache.find(key);
         if (it != cache.end()) return it->second;
+        if (lookup_only) return 0;
     }
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
     if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) {
@@ -1478,15 +1481,24 @@ static int tile_tuned_oz(const Grid& g, int prec, cudaStream_t st, F&& launch)
         cudaGetLastError();
         return 0;
     }
+    // candidates must cover every SM (a shape that leaves SMs idle can win a
+    // single-launch timing through lower launch latency, not throughput);
+    // each is timed as 4 back-to-back launches (the solver's usage), min of 3
+    int dev = 0, nsm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    const long long cols = (long long)((g.ihi - g.ilo + TILE_BX - 2) / (TILE_BX - 1)) *
+                           ((g.nny + TileDimsBy(prec) - 2) / (TileDimsBy(prec) - 1));
     int best = 0;
     float best_ms = 1e30f;
     for (int oz : cands) {
         if (oz > std::max(2, g.nnz)) break;
+        if (oz > 2 && cols * ((g.nnz + oz - 1) / oz) < nsm) break;
         if (launch(oz) != TF_OK) break;  // warm-up
         float t = 1e30f;
         for (int r = 0; r < 3; ++r) {
             cudaEventRecord(e0, st);
-            launch(oz);
+            for (int k = 0; k < 4; ++k) launch(oz);
             cudaEventRecord(e1, st);
             cudaEventSynchronize(e1);
             float ms = 0.f;
@@ -1506,6 +1518,18 @@ static int tile_tuned_oz(const Grid& g, int prec, cudaStream_t st, F&& launch)
         cache[key] = best;
     }
     return best;
+}
+
+// launch shape a plain product on grid g would use now (autotuned if tuned)
+template <typename T>
+TileShape tile_shape_current(const Grid& g)
+{
+    TileShape sh = tile_shape<T>(g);
+    if (tile_autotune_enabled()) {
+        const int oz = tile_tuned_oz(g, (int)sizeof(T), nullptr, [](int) { return TF_ERR_ARG; }, true);
+        if (oz > 0) sh = tile_shape_oz<T>(g, oz);
+    }
+    return sh;
 }
 
 template <typename T>
@@ -1638,3 +1662,14 @@ template int launch_grid_tile<double>(const Grid&, const double*, const double*,
                                       double*, const uint8_t*, uint32_t, double*, cudaStream_t);
 
 }  // namespace tf
+
+extern "C" int tf_tile_shape(const tf_grid* grid, int precision, int32_t* oz, int64_t* ctas)
+{
+    using namespace tf;
+    TF_REQUIRE(grid && oz && ctas && (precision == 32 || precision == 64), "bad arguments");
+    const Grid g = make_grid(grid);
+    const TileShape sh = precision == 32 ? tile_shape_current<float>(g) : tile_shape_current<double>(g);
+    *oz = sh.oz;
+    *ctas = (int64_t)sh.grid.x * sh.grid.y * sh.grid.z;
+    return TF_OK;
+}

@@ -98,6 +98,29 @@ int tf_matvec_grid_range_f64(const tf_grid* g, const double* ke, const double* s
  * been seen, else the heuristic).  Introspection only. */
 int tf_tile_shape(const tf_grid* g, int precision, int32_t* oz, int64_t* ctas);
 
+/* ---- Emulated bfloat16 (the reference's BF16 kernel contract, documented
+ *      negative result; _kernels_numba.py:113-126,166-211,230-238).  FP32
+ *      storage; each term is bf16_rne(s_e*K[i,j]) * u_j, FP32 accumulation.  */
+/* fused_serial_bf16 (mode TF_SCATTER_COLORED) / fused_atomic_bf16 (ATOMIC),
+ * accumulating into w; quantize_input != 0 rounds the gathered v to bf16 first
+ * (operator.py:83-88 _masked_input), 0 expects v pre-quantized (the contract). */
+int tf_matvec_edof_bf16(const int32_t* edof, const float* ke, const float* scale, const float* v,
+                        float* w, int64_t n_elem, int mode, const int32_t* color_elems,
+                        const int64_t* color_offsets, int n_colors, int quantize_input,
+                        void* stream);
+/* apply_fp64 of a bf16 operator (operator.py:143-152): quantized entries and
+ * input, FP64 accumulation, accumulated into w (FP64). */
+int tf_matvec_edof_bf16_f64(const int32_t* edof, const float* ke, const float* scale,
+                            const double* v, double* w, int64_t n_elem, void* stream);
+/* gemm_bf16: f_elem = per-term bf16(s*K) u_elem (new values, not accumulated) */
+int tf_gemm_bf16(const float* u_elem, const float* ke, const float* scale, float* f_elem,
+                 int64_t n_elem, void* stream);
+/* jacobi_diag_bf16: out[edof] += bf16(s_e * ke_diag[l]) (FP32) */
+int tf_jacobi_edof_bf16(const int32_t* edof, const float* ke_diag, const float* scale, float* out,
+                        int64_t n_elem, void* stream);
+/* y = round_to_bf16(x) (precision.py:65-85), y may alias x */
+int tf_round_bf16(int64_t n, const float* x, float* y, void* stream);
+
 /* ---- K v with an explicit element->DOF table: the fused kernel contract
  *      fused_serial/fused_atomic(edof, ke, scale, v, out) (_kernels_numba.py:146-196).
  *      ALWAYS accumulates into w (caller zeroes it, operator.py:93).
@@ -161,7 +184,7 @@ int tf_energies_edof_f64(const int32_t* edof, const double* ke, const double* u,
 typedef struct tf_pcg tf_pcg;
 
 typedef struct tf_pcg_desc {
-    int precision;              /* 32 or 64 */
+    int precision;              /* 32, 64, or 16 = emulated bf16 (FP32 storage, edof only) */
     int structured;             /* 1: grid kernels, 0: edof kernels */
     tf_grid grid;               /* when structured */
     const int32_t* edof;        /* when !structured: masked edof (fixed -> -1) */
@@ -172,7 +195,9 @@ typedef struct tf_pcg_desc {
     const int64_t* fixed;       /* device list of fixed DOFs (edof mode), nullable */
     int64_t n_fixed;
     int grid_variant;           /* TF_GRID_* */
+    int flags;                  /* TF_PCG_PLAIN_GRAPH: force the 3-kernel graph protocol */
 } tf_pcg_desc;
+#define TF_PCG_PLAIN_GRAPH 1u
 
 typedef struct tf_pcg_report {
     int32_t iterations;
@@ -203,6 +228,9 @@ int tf_pcg_destroy(tf_pcg* h);
 #define TF_PCG_FUSED_GRAPH 1
 #define TF_PCG_RESIDENT 2
 int tf_pcg_protocol(const tf_pcg* h);
+/* CgConfig.quantize_krylov (solver.py:134-136): round p and r to bf16 after
+ * every direction update in the following solves (FP32 storage, graph protocol). */
+int tf_pcg_set_quantize_krylov(tf_pcg* h, int on);
 
 /* ---- SIMP glue on the device (simp.py:33-175, element.py:34-45) -------------
  * Densities, sensitivities and filter vectors are FP64, n = n_elem.         */

@@ -69,6 +69,12 @@ def lib():
         L.orc_scatter_f64.argtypes = [_I32P, _F64P, _F64P, _I64]
         L.orc_scatter_f32_into_f64.argtypes = [_I32P, _F32P, _F64P, _I64]
         L.orc_element_energies.argtypes = [_I32P, _F64P, _F64P, _F64P, _I64]
+        L.orc_fused_serial_bf16.argtypes = [_I32P, _F32P, _F32P, _F32P, _F32P, _I64]
+        L.orc_gemm_bf16.argtypes = [_F32P, _F32P, _F32P, _F32P, _I64]
+        L.orc_jacobi_bf16.argtypes = [_I32P, _F32P, _F32P, _F32P, _I64]
+        L.orc_round_bf16.argtypes = [_F32P, _F32P, _I64]
+        for f in ("orc_fused_serial_bf16", "orc_gemm_bf16", "orc_jacobi_bf16", "orc_round_bf16"):
+            getattr(L, f).restype = None
         L.orc_num_threads.restype = ctypes.c_int
         L.orc_set_num_threads.argtypes = [ctypes.c_int]
         _lib = L
@@ -153,6 +159,60 @@ def element_energies(edof, ke, u):
     return out
 
 
+def round_bf16(x):
+    """precision.py:65-85 round_to_bf16 (float32 in, float32 out)."""
+    x = _c(x, np.float32)
+    y = np.empty_like(x)
+    lib().orc_round_bf16(x, y, x.size)
+    return y
+
+
+def fused_serial_bf16(edof, ke, scale, v, out) -> None:
+    """_kernels_numba.py:166-180 -- v pre-quantized, out float32 accumulated."""
+    lib().orc_fused_serial_bf16(_c(edof, np.int32), _c(ke, np.float32), _c(scale, np.float32),
+                                _c(v, np.float32), out, edof.shape[0])
+
+
+def gemm_bf16(u_elem, ke, scale):
+    """_kernels_numba.py:113-126."""
+    f = np.empty((u_elem.shape[0], 24), dtype=np.float32)
+    lib().orc_gemm_bf16(_c(u_elem, np.float32), _c(ke, np.float32), _c(scale, np.float32), f,
+                        u_elem.shape[0])
+    return f
+
+
+def jacobi_diag_bf16(edof, ke_diag, scale, out) -> None:
+    """_kernels_numba.py:230-238; `out` float32."""
+    lib().orc_jacobi_bf16(_c(edof, np.int32), _c(ke_diag, np.float32), _c(scale, np.float32), out,
+                          edof.shape[0])
+
+
+def apply_bf16(edof, ke, scale, v, fixed_dofs, n_dof, variant="fused"):
+    """MatFreeOperator.apply for precision "bf16" (operator.py:83-117):
+    masked input rounded to bf16, bf16 kernels, pass-through of the raw v."""
+    free = np.ones(n_dof, dtype=bool)
+    free[fixed_dofs] = False
+    x = round_bf16(np.where(free, np.asarray(v, dtype=np.float32), 0).astype(np.float32))
+    out = np.zeros(n_dof, dtype=np.float32)
+    if variant == "fused":
+        fused_serial_bf16(edof, ke, scale, x, out)
+    else:
+        f = gemm_bf16(gather(edof, x), ke, scale)
+        acc = np.zeros(n_dof)
+        scatter_serial(edof, f, acc)
+        out[:] = acc
+    out[fixed_dofs] = np.asarray(v, dtype=np.float32)[fixed_dofs]
+    return out
+
+
+def diagonal_bf16(edof, ke, scale, fixed_dofs, n_dof):
+    """MatFreeOperator.diagonal for bf16 (operator.py:122-126)."""
+    out = np.zeros(n_dof, dtype=np.float32)
+    jacobi_diag_bf16(edof, np.diag(ke).copy(), scale, out)
+    out[fixed_dofs] = 1.0
+    return out
+
+
 # -- operator glue (operator.py:83-132) -----------------------------------------
 
 
@@ -191,7 +251,8 @@ def diagonal(edof, ke, scale, fixed_dofs, n_dof):
 # -- Jacobi-PCG recurrence (solver.py:57-147) -----------------------------------
 
 
-def pcg(apply_op, b, diag, rel_tol=1e-5, max_iter=1000, recompute_every=50, x0=None):
+def pcg(apply_op, b, diag, rel_tol=1e-5, max_iter=1000, recompute_every=50, x0=None,
+        quantize_krylov=False):
     """Restatement of the reference pcg.  Returns (x, info dict).
 
     Same recurrence, stop rule, refresh period, breakdown and divergence
@@ -248,6 +309,9 @@ def pcg(apply_op, b, diag, rel_tol=1e-5, max_iter=1000, recompute_every=50, x0=N
         z = r * inv_diag
         rz_new = float(np.dot(r, z))
         p = z + (rz_new / rz) * p
+        if quantize_krylov:  # solver.py:134-136
+            p = round_bf16(p)
+            r = round_bf16(r)
         rz = rz_new
     return x, dict(iterations=it, termination=term, rel=rel, history=hist, matvecs=matvecs)
 

@@ -20,7 +20,7 @@ from .precision import (BF16, EPS_BF16, EPS_FP32, EPS_FP64, FP32, FP64, Precisio
 from .simp import (ContinuationSchedule, Phase, SimpConfig, SimpResult, build_cone_filter,
                    chain_to_design, compliance_sensitivity, default_schedule, grayness,
                    heaviside_derivative, heaviside_projection, oc_update, run_simp)
-from .solver import (CgConfig, DivergenceError, IrConfig, SolveReport, device_pcg,
+from .solver import (CgConfig, DivergenceError, IrConfig, IrReport, SolveReport, device_pcg,
                      fp64_relative_residual, pcg, solve_equilibrium, solve_refined)
 
 __version__ = "0.1.0"

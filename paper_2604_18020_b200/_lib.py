@@ -51,6 +51,7 @@ class tf_pcg_desc(ctypes.Structure):
         ("fixed", ctypes.c_void_p),
         ("n_fixed", ctypes.c_int64),
         ("grid_variant", ctypes.c_int),
+        ("flags", ctypes.c_int),
     ]
 
 
@@ -107,7 +108,13 @@ _SIGS = {
                      _P, _P],
     "tf_pcg_destroy": [_P],
     "tf_pcg_protocol": [_P],
+    "tf_pcg_set_quantize_krylov": [_P, _INT],
     "tf_tile_shape": [_P, _INT, _P, _P],
+    "tf_matvec_edof_bf16": [_P, _P, _P, _P, _P, _I64, _INT, _P, _P, _INT, _INT, _P],
+    "tf_matvec_edof_bf16_f64": [_P, _P, _P, _P, _P, _I64, _P],
+    "tf_gemm_bf16": [_P, _P, _P, _P, _I64, _P],
+    "tf_jacobi_edof_bf16": [_P, _P, _P, _P, _I64, _P],
+    "tf_round_bf16": [_I64, _P, _P, _P],
     "tf_filter_rowsum_f64": [_P, ctypes.c_double, _P, _P],
     "tf_filter_grid_f64": [_P, ctypes.c_double, _P, _P, _P, _INT, _P],
     "tf_project_f64": [_I64, ctypes.c_double, ctypes.c_double, _P, _P, _P, _P],

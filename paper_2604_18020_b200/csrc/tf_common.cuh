@@ -90,6 +90,7 @@ struct CgScalars {
     int it, done, term, matvecs, refresh, max_iter, recompute, zero_rhs;
     int it_cur;
     int it_a, it_b;
+    int quantize;  // round p and r to bf16 after each direction update (CgConfig.quantize_krylov)
 };
 
 __device__ __forceinline__ double cg_round(double v, bool f32) { return f32 ? (double)(float)v : v; }
@@ -97,6 +98,19 @@ __device__ __forceinline__ double cg_sqrt(double v, bool f32)
 {
     return f32 ? (double)sqrtf((float)v) : sqrt(v);
 }
+// bit-exact round_to_bf16 / numba _bf16 (precision.py:65-85, _kernels_numba.py:68-78):
+// RNE on the high 16 bits, NaN payloads quieted, infinities kept
+__device__ __forceinline__ float bf16_rne(float x)
+{
+    const unsigned u = __float_as_uint(x);
+    if ((u & 0x7F800000u) == 0x7F800000u) {
+        if (u & 0x007FFFFFu) return __uint_as_float(((u >> 16) << 16) | 0x00400000u);
+        return x;
+    }
+    const unsigned bias = 0x7FFFu + ((u >> 16) & 1u);
+    return __uint_as_float(((u + bias) >> 16) << 16);
+}
+
 __device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
 __device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
 __device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }

@@ -176,6 +176,9 @@ __device__ bool last_block_reduce(double (&v)[K], double* part, unsigned* ticket
 
 // ---- decisions -------------------------------------------------------------
 
+__device__ __forceinline__ float qbf16(float x) { return bf16_rne(x); }
+__device__ __forceinline__ double qbf16(double x) { return (double)bf16_rne((float)x); }
+
 // ---- vector access: 16-byte chunks (float4 / double2) + scalar tail ------------------
 
 template <typename T> struct V16;
@@ -501,6 +504,7 @@ __global__ void __launch_bounds__(VEC_BLOCK) k_direction(CgP<T> P, int nparts)
     }
     if (stop) return;
     const T be = (T)beta;
+    const bool quant = sc->quantize != 0;
     const long long nc = P.n / N, stride = (long long)gridDim.x * VEC_BLOCK;
     for (long long c = (long long)blockIdx.x * VEC_BLOCK + threadIdx.x; c < nc; c += stride) {
         T r[N], iv[N], p[N];
@@ -509,11 +513,25 @@ __global__ void __launch_bounds__(VEC_BLOCK) k_direction(CgP<T> P, int nparts)
         ld16(P.p, c, p);
 #pragma unroll
         for (int k = 0; k < N; ++k) p[k] = add_rn(mul_rn(r[k], iv[k]), mul_rn(be, p[k]));
+        if (quant) {  // quantize_krylov (solver.py:134-136): p and r to bf16
+#pragma unroll
+            for (int k = 0; k < N; ++k) {
+                p[k] = qbf16(p[k]);
+                r[k] = qbf16(r[k]);
+            }
+            st16(P.r, c, r);
+        }
         st16(P.p, c, p);
     }
     if (blockIdx.x == 0)
-        for (long long i = nc * N + threadIdx.x; i < P.n; i += VEC_BLOCK)
-            P.p[i] = add_rn(mul_rn(P.r[i], P.inv[i]), mul_rn(be, P.p[i]));
+        for (long long i = nc * N + threadIdx.x; i < P.n; i += VEC_BLOCK) {
+            T pn = add_rn(mul_rn(P.r[i], P.inv[i]), mul_rn(be, P.p[i]));
+            if (quant) {
+                pn = qbf16(pn);
+                P.r[i] = qbf16(P.r[i]);
+            }
+            P.p[i] = pn;
+        }
 }
 
 // init: r = b - q (has_x0) or r = b; p = r*inv; partials b.b, r.r, r.z
@@ -581,6 +599,7 @@ struct PcgImpl {
     // device buffers
     void *x, *r, *p, *q, *b, *inv, *scale;
     void* p2;           // second search-direction buffer (fused protocol)
+    int quantize;       // quantize_krylov for the next solve (tf_pcg_set_quantize_krylov)
     int fused;          // structured tile solve with the direction folded into the matvec
     int resident;       // SM-resident solve: one cooperative launch (tf_pcg_resident.cu)
     ResPlan rplan;
@@ -619,6 +638,12 @@ static int enqueue_matvec(PcgImpl* h, const T* v, T* w, double* dot_part, cudaSt
                                    TF_MASK_INPUT | TF_PASS_FIXED, h->variant, dot_part, st);
     }
     TF_CUDA_TRY(cudaMemsetAsync(w, 0, sizeof(T) * h->n_dof, st));
+    if (h->prec == 16) {  // emulated bf16: quantized input, per-term bf16(s K) (tf_bf16.cu)
+        int rc = tf_matvec_edof_bf16(h->edof, (const float*)ke, (const float*)h->scale, (const float*)v,
+                                     (float*)w, h->n_elem, TF_SCATTER_ATOMIC, nullptr, nullptr, 0, 1, st);
+        if (rc) return rc;
+        return launch_pass_fixed<T>(h->fixed, h->n_fixed, v, w, st);
+    }
     int rc = (sizeof(T) == 4)
                  ? tf_matvec_edof_f32(h->edof, (const float*)ke, (const float*)h->scale,
                                       (const float*)v, (float*)w, h->n_elem, TF_SCATTER_ATOMIC,
@@ -787,6 +812,7 @@ static int solve_impl(PcgImpl* h, const void* scale, const void* b, const void* 
     init.max_iter = max_iter;
     init.recompute = recompute;
     init.hist = history;
+    init.quantize = h->quantize;
     *h->sc_host = init;
     TF_CUDA_TRY(cudaMemcpyAsync(h->sc, h->sc_host, sizeof(CgScalars), cudaMemcpyHostToDevice, st));
     if (h->resident) {
@@ -859,16 +885,19 @@ extern "C" {
 int tf_pcg_create(tf_pcg** out, const tf_pcg_desc* d, void* stream)
 {
     TF_REQUIRE(out && d, "null argument");
-    TF_REQUIRE(d->precision == 32 || d->precision == 64, "precision must be 32 or 64");
+    TF_REQUIRE(d->precision == 32 || d->precision == 64 || d->precision == 16,
+               "precision must be 32, 64 or 16 (emulated bf16)");
+    TF_REQUIRE(d->precision != 16 || !d->structured, "emulated bf16 runs the general-edof kernels");
     TF_REQUIRE(d->n_dof > 0 && d->n_elem > 0 && d->ke, "empty problem");
     PcgImpl* h = new PcgImpl();
     h->prec = d->precision;
+    h->quantize = 0;
     h->structured = d->structured;
     if (d->structured) h->grid = make_grid(&d->grid);
     h->edof = d->edof;
     h->n_elem = d->n_elem;
     h->n_dof = d->n_dof;
-    const size_t es = d->precision == 32 ? 4 : 8;
+    const size_t es = d->precision == 64 ? 8 : 4;
     h->ke.assign((const unsigned char*)d->ke, (const unsigned char*)d->ke + 576 * es);
     h->node_fixed = d->node_fixed;
     h->fixed = d->fixed;
@@ -916,12 +945,12 @@ int tf_pcg_create(tf_pcg** out, const tf_pcg_desc* d, void* stream)
                                            : launch_grid_tile_supported<double>((const double*)d->ke);
         const char* e = getenv("TF_PCG_FUSED");
         const bool want = e ? (e[0] == '1') : (d->n_elem <= 100000);
-        h->fused = (ok && want) ? 1 : 0;
+        h->fused = (ok && want && !(d->flags & TF_PCG_PLAIN_GRAPH)) ? 1 : 0;
     }
     // SM-resident protocol: the whole solve in one cooperative launch whenever
     // the CG state of the owned DOFs fits in the co-resident CTAs' shared
     // memory (TF_PCG_RESIDENT=0 disables it)
-    if (d->structured && d->grid_variant == TF_GRID_FAST) {
+    if (d->structured && d->grid_variant == TF_GRID_FAST && !(d->flags & TF_PCG_PLAIN_GRAPH)) {
         const char* e = getenv("TF_PCG_RESIDENT");
         if (!(e && e[0] == '0')) {
             const bool ok = d->precision == 32
@@ -949,7 +978,7 @@ int tf_pcg_create(tf_pcg** out, const tf_pcg_desc* d, void* stream)
     TF_CUDA_TRY(cudaMemset(h->tickets, 0, sizeof(unsigned) * 8));
     TF_CUDA_TRY(cudaMalloc(&h->sc, sizeof(CgScalars)));
     TF_CUDA_TRY(cudaMallocHost(&h->sc_host, sizeof(CgScalars)));
-    int rc = h->resident ? TF_OK : (d->precision == 32 ? build_graph<float>(h) : build_graph<double>(h));
+    int rc = h->resident ? TF_OK : (d->precision != 64 ? build_graph<float>(h) : build_graph<double>(h));
     if (rc) {
         tf_pcg_destroy(reinterpret_cast<tf_pcg*>(h));
         return rc;
@@ -965,10 +994,20 @@ int tf_pcg_solve(tf_pcg* hh, const void* scale, const void* b, const void* inv_d
     PcgImpl* h = reinterpret_cast<PcgImpl*>(hh);
     TF_REQUIRE(h && scale && b && inv_diag && x && report, "null argument");
     TF_REQUIRE(rel_tol > 0 && max_iter >= 1 && recompute_every >= 0, "invalid CG configuration");
-    return h->prec == 32 ? solve_impl<float>(h, scale, b, inv_diag, x, has_x0, rel_tol, max_iter,
+    return h->prec != 64 ? solve_impl<float>(h, scale, b, inv_diag, x, has_x0, rel_tol, max_iter,
                                              recompute_every, history, report)
                          : solve_impl<double>(h, scale, b, inv_diag, x, has_x0, rel_tol, max_iter,
                                               recompute_every, history, report);
+}
+
+int tf_pcg_set_quantize_krylov(tf_pcg* hh, int on)
+{
+    PcgImpl* h = reinterpret_cast<PcgImpl*>(hh);
+    TF_REQUIRE(h, "null handle");
+    TF_REQUIRE(!on || h->prec != 64, "quantize_krylov needs FP32 storage (fp32 or bf16 operators)");
+    TF_REQUIRE(!on || (!h->resident && !h->fused), "quantize_krylov runs on the plain graph protocol");
+    h->quantize = on ? 1 : 0;
+    return TF_OK;
 }
 
 int tf_pcg_protocol(const tf_pcg* hh)

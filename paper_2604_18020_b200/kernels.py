@@ -112,3 +112,59 @@ def element_energies(edof, ke, u):
     _lib.call("tf_energies_edof_f64", D.ptr(e_d), ke_h.ctypes.data,
               D.ptr(u_d), D.ptr(out), edof.shape[0], D.stream_ptr())
     return out.cpu().numpy()
+
+
+# -- emulated bfloat16 contract (_kernels_numba.py:113-126, 166-211, 230-238) -----
+
+
+def _fused_bf16(edof, ke, scale, v, out, mode):
+    edof = np.ascontiguousarray(edof, dtype=np.int32)
+    e_d = D.to_dev(edof, np.int32)
+    s_d = D.to_dev(scale, np.float32)
+    v_d = D.to_dev(v, np.float32)
+    o_d = D.to_dev(out, np.float32)
+    ke_h = np.ascontiguousarray(ke, dtype=np.float32)
+    if mode == _lib.TF_SCATTER_COLORED:
+        from .mesh import StructuredMesh
+        from .operator import element_colouring
+
+        n = edof.shape[0]
+        order, offsets = element_colouring(StructuredMesh(n, 1, 1), edof)
+        o_ = D.to_dev(order, np.int32)
+        _lib.call("tf_matvec_edof_bf16", D.ptr(e_d), ke_h.ctypes.data, D.ptr(s_d), D.ptr(v_d), D.ptr(o_d),
+                  n, mode, D.ptr(o_), offsets.ctypes.data, len(offsets) - 1, 0, D.stream_ptr())
+    else:
+        _lib.call("tf_matvec_edof_bf16", D.ptr(e_d), ke_h.ctypes.data, D.ptr(s_d), D.ptr(v_d), D.ptr(o_d),
+                  edof.shape[0], mode, None, None, 0, 0, D.stream_ptr())
+    out[...] = o_d.cpu().numpy()
+
+
+def fused_serial_bf16(edof, ke, scale, v, out) -> None:
+    """Deterministic fused K v with per-term bf16(s K); v pre-quantized; out += (FP32)."""
+    _fused_bf16(edof, ke, scale, v, out, _lib.TF_SCATTER_COLORED)
+
+
+def fused_atomic_bf16(edof, ke, scale, v, out) -> None:
+    """red.global.add variant of fused_serial_bf16."""
+    _fused_bf16(edof, ke, scale, v, out, _lib.TF_SCATTER_ATOMIC)
+
+
+def gemm_bf16(u_elem, ke, scale):
+    u_d = D.to_dev(u_elem, np.float32)
+    f = D.torch().empty_like(u_d)
+    ke_h = np.ascontiguousarray(ke, dtype=np.float32)
+    s_d = D.to_dev(scale, np.float32)
+    _lib.call("tf_gemm_bf16", D.ptr(u_d), ke_h.ctypes.data, D.ptr(s_d), D.ptr(f), u_elem.shape[0],
+              D.stream_ptr())
+    return f.cpu().numpy()
+
+
+def jacobi_diag_bf16(edof, ke_diag, scale, out) -> None:
+    """out[edof] += bf16(s_e ke_diag[l]) in FP32."""
+    o_d = D.to_dev(out, np.float32)
+    kd = np.ascontiguousarray(ke_diag, dtype=np.float32)
+    e_d = D.to_dev(edof, np.int32)
+    s_d = D.to_dev(scale, np.float32)
+    _lib.call("tf_jacobi_edof_bf16", D.ptr(e_d), kd.ctypes.data, D.ptr(s_d), D.ptr(o_d), edof.shape[0],
+              D.stream_ptr())
+    out[...] = o_d.cpu().numpy()

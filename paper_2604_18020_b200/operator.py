@@ -171,9 +171,10 @@ class MatFreeOperator:
         if backend not in (None,) + BACKENDS:
             raise ValueError(f"unknown backend {backend!r}, expected b200")
         self.precision = get_precision(precision) if isinstance(precision, str) else precision
-        if self.precision.quantized:
-            raise ValueError("bf16 is not on the B200 production path (documented negative "
-                             "result, PAPER.md:1522-1552); use fp32 or fp64")
+        # "bf16" is the reference's emulated-bfloat16 precision (FP32 storage,
+        # per-term rounding): served by the general-edof bf16 kernels
+        # (csrc/tf_bf16.cu) as the documented negative result, never by the
+        # structured production kernels
         self.mesh = mesh
         self.edof = edof
         self.bcs = bcs
@@ -211,7 +212,7 @@ class MatFreeOperator:
     @property
     def structured(self) -> bool:
         """True when the index-free structured kernels serve this operator."""
-        return self.dev.structured and self.grid_kernel != "edof"
+        return self.dev.structured and self.grid_kernel != "edof" and not self.precision.quantized
 
     @property
     def grid_variant(self) -> int:
@@ -229,6 +230,8 @@ class MatFreeOperator:
         sfx = _sfx(dt)
         st = D.stream_ptr()
         dev = self.dev
+        if self.precision.quantized:
+            return self._apply_bf16(x, out, ke, scale, np.dtype(dt) == np.float64)
         if self.variant == "fused" and self.structured:
             _lib.call(f"tf_matvec_grid_{sfx}", ctypes_ref(dev.grid), ke.ctypes.data, D.ptr(scale),
                       D.ptr(x), D.ptr(out), D.ptr(dev.node_fixed),
@@ -261,6 +264,49 @@ class MatFreeOperator:
                       D.ptr(out), st)
         return out
 
+    def _apply_bf16(self, x, out, ke, scale, fp64):
+        """Emulated-bf16 apply (operator.py:83-117) or its FP64 evaluation
+        (apply_fp64, operator.py:143-152): quantized input and per-term
+        bf16(s_e K_ij), pass-through of the raw input on fixed DOFs."""
+        t = D.torch()
+        dev = self.dev
+        st = D.stream_ptr()
+        ke32 = np.ascontiguousarray(self.ke, dtype=np.float32)
+        s32 = self._scale_dev
+        n = self.mesh.n_elem
+        if fp64:
+            out.zero_()
+            _lib.call("tf_matvec_edof_bf16_f64", D.ptr(dev.edof_masked), ke32.ctypes.data, D.ptr(s32),
+                      D.ptr(x), D.ptr(out), n, st)
+            sfx = "f64"
+        elif self.variant == "fused":
+            out.zero_()
+            if self.scatter == "parallel_atomic":
+                _lib.call("tf_matvec_edof_bf16", D.ptr(dev.edof_masked), ke32.ctypes.data, D.ptr(s32),
+                          D.ptr(x), D.ptr(out), n, _lib.TF_SCATTER_ATOMIC, None, None, 0, 1, st)
+            else:
+                order, offsets = dev.colors()
+                _lib.call("tf_matvec_edof_bf16", D.ptr(dev.edof_masked), ke32.ctypes.data, D.ptr(s32),
+                          D.ptr(x), D.ptr(out), n, _lib.TF_SCATTER_COLORED, D.ptr(order),
+                          offsets.ctypes.data, len(offsets) - 1, 1, st)
+            sfx = "f32"
+        else:
+            xq = t.empty_like(x)
+            _lib.call("tf_round_bf16", self.n_dof, D.ptr(x), D.ptr(xq), st)
+            u_elem = t.empty((n, 24), dtype=t.float32, device=x.device)
+            f_elem = t.empty_like(u_elem)
+            acc = t.zeros(self.n_dof, dtype=t.float64, device=x.device)
+            em = dev.edof_masked
+            _lib.call("tf_gather_f32", D.ptr(em), D.ptr(xq), D.ptr(u_elem), n, st)
+            _lib.call("tf_gemm_bf16", D.ptr(u_elem), ke32.ctypes.data, D.ptr(s32), D.ptr(f_elem), n, st)
+            _lib.call("tf_scatter_f32", D.ptr(em), D.ptr(f_elem), D.ptr(acc), n, st)
+            out.copy_(acc)
+            sfx = "f32"
+        if dev.fixed is not None:
+            _lib.call(f"tf_pass_fixed_{sfx}", D.ptr(dev.fixed), int(dev.fixed_np.size), D.ptr(x),
+                      D.ptr(out), st)
+        return out
+
     def diagonal_device(self):
         """(diag, inv_diag) device tensors in the working dtype."""
         t = D.torch()
@@ -270,6 +316,13 @@ class MatFreeOperator:
         kd = np.ascontiguousarray(np.diag(self.ke), dtype=dt)
         diag = t.empty(self.n_dof, dtype=D.tdtype(dt), device=self._scale_dev.device)
         inv = t.empty_like(diag)
+        if self.precision.quantized:  # jacobi_diag_bf16 (operator.py:122-126), FP32 accumulation
+            diag.zero_()
+            _lib.call("tf_jacobi_edof_bf16", D.ptr(dev.edof_raw), kd.ctypes.data, D.ptr(self._scale_dev),
+                      D.ptr(diag), self.mesh.n_elem, D.stream_ptr())
+            if dev.fixed is not None:
+                diag[dev.fixed] = 1.0
+            return diag, 1.0 / diag
         if self.structured:
             _lib.call(f"tf_jacobi_grid_{sfx}", ctypes_ref(dev.grid), kd.ctypes.data,
                       D.ptr(self._scale_dev), D.ptr(diag), D.ptr(inv), D.ptr(dev.node_fixed),
@@ -369,6 +422,9 @@ class MatFreeOperator:
             self._scale64_dev = D.to_dev(self.scale64, np.float64)
         tensor_in = D.is_tensor(v) and v.is_cuda
         x = v.to(D.torch().float64).contiguous() if tensor_in else D.to_dev(np.asarray(v), np.float64)
+        if self.precision.quantized:  # the quantized system the solver saw, FP64 accumulation
+            out = self._apply_bf16(x, D.torch().empty_like(x), None, None, True)
+            return out if tensor_in else out.cpu().numpy()
         out = self.apply_device(x, ke=np.ascontiguousarray(self.ke64), scale=self._scale64_dev,
                                 dtype=np.float64)
         return out if tensor_in else out.cpu().numpy()

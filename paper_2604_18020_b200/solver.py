@@ -69,25 +69,27 @@ def _operator_of(apply_op):
 
 def pcg(apply_op, b, diag, config: CgConfig = CgConfig(), x0=None):
     """Preconditioned CG in b's storage precision (solver.py:57-147)."""
-    if config.quantize_krylov:
-        raise ValueError("quantize_krylov (bf16 Krylov vectors) is not on the B200 path")
     op = _operator_of(apply_op)
+    if config.quantize_krylov and (op is None or op.precision.tag == "fp64"):
+        raise ValueError("quantize_krylov needs a fp32/bf16 MatFreeOperator (FP32 storage)")
     if op is not None:
         return device_pcg(op, b, diag, config, x0)
     return _generic_pcg(apply_op, b, diag, config, x0)
 
 
-def _pcg_handle(op: MatFreeOperator):
-    """One graph-captured PCG per (device problem, precision, kernel variant)."""
+def _pcg_handle(op: MatFreeOperator, graph_only: bool = False):
+    """One device PCG per (device problem, precision, kernel variant); graph_only
+    forces the plain 3-kernel graph protocol (quantize_krylov rounds p and r
+    in its direction kernel)."""
     dev = op.dev
     # the protocol overrides are read at handle creation: part of the key
     key = (op.precision.tag, op.grid_variant, op.variant == "fused" and op.structured,
-           os.environ.get("TF_PCG_RESIDENT"), os.environ.get("TF_PCG_FUSED"))
+           os.environ.get("TF_PCG_RESIDENT"), os.environ.get("TF_PCG_FUSED"), graph_only)
     h = dev.pcg_handles.get(key)
     if h is not None:
         return h
     desc = _lib.tf_pcg_desc()
-    desc.precision = 64 if op.precision.tag == "fp64" else 32
+    desc.precision = {"fp64": 64, "fp32": 32, "bf16": 16}[op.precision.tag]
     desc.structured = 1 if (op.structured and op.variant == "fused") else 0
     desc.grid = dev.grid
     desc.edof = 0 if desc.structured else D.ptr(dev.edof_masked)
@@ -99,6 +101,7 @@ def _pcg_handle(op: MatFreeOperator):
     desc.fixed = D.ptr(dev.fixed)
     desc.n_fixed = int(dev.fixed_np.size)
     desc.grid_variant = max(op.grid_variant, 0)
+    desc.flags = 1 if graph_only else 0
     out = ctypes.c_void_p()
     _lib.call("tf_pcg_create", ctypes.byref(out), ctypes.byref(desc), D.stream_ptr())
     dev.pcg_handles[key] = out
@@ -135,7 +138,8 @@ def device_pcg(op: MatFreeOperator, b, diag, config: CgConfig = CgConfig(), x0=N
     if has_x0:
         x_d.copy_(D.to_dev(x0, dt))
     hist = t.zeros(config.max_iter + 1, dtype=t.float64, device=b_d.device)
-    h = _pcg_handle(op)
+    h = _pcg_handle(op, graph_only=bool(config.quantize_krylov))
+    _lib.call("tf_pcg_set_quantize_krylov", h, 1 if config.quantize_krylov else 0)
     rep = _lib.tf_pcg_report()
     _lib.call("tf_pcg_solve", h, D.ptr(op._scale_dev), D.ptr(b_d), D.ptr(inv_d), D.ptr(x_d),
               1 if has_x0 else 0, float(config.rel_tol), int(config.max_iter),
@@ -240,6 +244,10 @@ def solve_equilibrium(op: MatFreeOperator, f, config: CgConfig = CgConfig(), x0=
     """K(rho) u = f with the verified-residual floor rule (solver.py:150-183)."""
     rhs = np.ascontiguousarray(f, dtype=op.precision.dtype)
     diag_d, _ = op.diagonal_device()
+    if op.precision.quantized and config.recompute_every:
+        # a residual recomputed through the rounding operator sits O(eps kappa)
+        # from the recurrence: quantized solves skip the refresh (solver.py:171-172)
+        config = replace(config, recompute_every=0)
     u, report = pcg(op.apply, rhs, diag_d, config, x0=x0)
     report.compliance = op.compliance(f, u)
     report.precision = op.precision.tag
@@ -268,11 +276,59 @@ class IrConfig:
     stagnation_drop: float = 0.05
 
 
-def solve_refined(*args, **kwargs):
-    """BF16 iterative refinement (solver.py:193-274) is out of scope on B200:
-    the north star keeps BF16 only as a documented negative result."""
-    raise NotImplementedError("BF16 iterative refinement is not on the B200 path")
+@dataclass
+class IrReport:
+    converged: bool
+    stagnated: bool
+    outer_steps: int
+    inner_iterations: list
+    total_inner: int
+    outer_residuals: list
+    compliance: float
+    wall_time: float
 
 
-__all__ = ["CgConfig", "DivergenceError", "IrConfig", "SolveReport", "device_pcg",
+def solve_refined(op_outer: MatFreeOperator, op_inner: MatFreeOperator, f, ir: IrConfig = IrConfig(),
+                  cg: CgConfig = CgConfig()):
+    """Iterative refinement (solver.py:211-262): FP32 outer residuals through
+    op_outer, inner corrections solved with op_inner (BF16) to ir.inner_tol
+    with the refresh disabled; stops on the outer tolerance, the outer cap, or
+    two consecutive outer reductions below ir.stagnation_drop (the eps*kappa
+    barrier).  Vectors stay on the device; this reproduces the paper's
+    negative result, it is not a production solver."""
+    t = D.torch()
+    t0 = time.perf_counter()
+    dt = op_outer.precision.dtype
+    rhs = D.to_dev(np.ascontiguousarray(f, dtype=dt), dt)
+    fnorm = float(t.linalg.vector_norm(rhs).cpu())
+    u = t.zeros_like(rhs)
+    r = rhs.clone()
+    diag_inner, _ = op_inner.diagonal_device()
+    inner_cfg = CgConfig(rel_tol=ir.inner_tol, max_iter=cg.max_iter, recompute_every=0,
+                         quantize_krylov=cg.quantize_krylov)
+    outer = [1.0]
+    inner_its = []
+    converged = stagnated = False
+    for _ in range(ir.max_outer):
+        e, rep = device_pcg(op_inner, r.to(D.tdtype(op_inner.precision.dtype)), diag_inner, inner_cfg,
+                            return_device=True)
+        inner_its.append(rep.iterations)
+        u = u + e.to(u.dtype)
+        r = rhs - op_outer.apply(u)
+        rel = float(t.linalg.vector_norm(r).cpu()) / fnorm
+        outer.append(rel)
+        if rel <= ir.outer_tol:
+            converged = True
+            break
+        if len(outer) >= 3:
+            drops = [1.0 - outer[-1] / outer[-2], 1.0 - outer[-2] / outer[-3]]
+            if all(d < ir.stagnation_drop for d in drops):
+                stagnated = True
+                break
+    u_np = u.cpu().numpy()
+    return u_np, IrReport(converged, stagnated, len(inner_its), inner_its, int(sum(inner_its)), outer,
+                          op_outer.compliance(f, u_np), time.perf_counter() - t0)
+
+
+__all__ = ["CgConfig", "DivergenceError", "IrConfig", "IrReport", "SolveReport", "device_pcg",
            "fp64_relative_residual", "pcg", "solve_equilibrium", "solve_refined", "replace"]

@@ -96,3 +96,33 @@ def test_oracle_pcg_matches_reference_anchor(golden_ke):
     x, info = oracle.pcg(A, pb.bcs.force.copy(), diag)
     assert info["iterations"] == cg["iterations"]
     np.testing.assert_allclose(info["history"], cg["history"], rtol=1e-9)
+
+
+# -- emulated BF16 (tests/golden/make_golden_bf16.py) ---------------------------
+
+BF16_CASES = [((4, 3, 2), 11), ((5, 3, 2), 1030)]
+
+
+def test_oracle_round_bf16_bitwise_vs_reference():
+    g = load_golden("bf16_4x3x2.npz")
+    got = oracle.round_bf16(g["specials"])
+    assert np.array_equal(got.view(np.uint32), g["round_specials"].view(np.uint32))
+
+
+@pytest.mark.parametrize("dims,seed", BF16_CASES)
+def test_oracle_bf16_kernels_bitwise_vs_reference(golden_ke, dims, seed):
+    g = load_golden(f"bf16_{'x'.join(map(str, dims))}.npz")
+    m, edof, bcs, rho, v = seeded_case(dims, seed)
+    ke, scale, _ = _ops(golden_ke, rho, "fp32")
+    vq = oracle.round_bf16(v.astype(np.float32))
+    out = np.zeros(m.n_dof, dtype=np.float32)
+    oracle.fused_serial_bf16(edof, ke, scale, vq, out)
+    assert np.array_equal(out, g["raw_fused_serial_bf16"])
+    assert np.array_equal(oracle.gemm_bf16(oracle.gather(edof, vq), ke, scale), g["raw_gemm_bf16"])
+    d = np.zeros(m.n_dof, dtype=np.float32)
+    oracle.jacobi_diag_bf16(edof, np.diag(ke).copy(), scale, d)
+    assert np.array_equal(d, g["raw_jacobi_bf16"])
+    for variant in ("fused", "three_stage"):
+        got = oracle.apply_bf16(edof, ke, scale, v, bcs.fixed_dofs, m.n_dof, variant)
+        assert np.array_equal(got, g[f"apply_{variant}"]), variant
+    assert np.array_equal(oracle.diagonal_bf16(edof, ke, scale, bcs.fixed_dofs, m.n_dof), g["diag"])

@@ -290,13 +290,23 @@ def run_ours(args):
     # e2e through the public API from pinned host buffers: every step copies
     # its input vector H2D and its result D2H; MatFreeOperator.apply_stream
     # overlaps the copies of neighbouring steps with the matvecs
-    vh = [torch.from_numpy(v.astype(dt)).pin_memory() for _ in range(2)]
-    wh = [torch.empty_like(vh[0]).pin_memory() for _ in range(2)]
+    # host buffers: page-locked via cudaHostAlloc (torch's pin_memory() buffers
+    # measured 4x slower host-to-device on these VMs, scripts/h2d_probe.cu)
+    from paper_2604_18020_b200._device import pinned_empty
+
+    vh = [pinned_empty(x.numel(), x.dtype) for _ in range(2)]
+    for h in vh:
+        h.copy_(torch.from_numpy(v.astype(dt)))
+    wh = [pinned_empty(x.numel(), x.dtype) for _ in range(2)]
     if world == 1:
         ins = [vh[i & 1] for i in range(args.steps)]
         outs = [wh[i & 1] for i in range(args.steps)]
-        op.apply_stream(ins[:4], outs[:4])
-        torch.cuda.synchronize()
+        # warm-up 300 ms of transfers: the PCIe link downshifts while idle
+        # and needs that long to return to full speed (scripts/pcie_probe.py)
+        t_w = time.perf_counter()
+        while time.perf_counter() - t_w < 0.3:
+            op.apply_stream(ins[:16], outs[:16])
+            torch.cuda.synchronize()
         a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a0.record(stream)
         op.apply_stream(ins, outs)
@@ -383,7 +393,7 @@ def run_ours(args):
                     "h2d_bytes_per_step": int(m.n_dof * np.dtype(dt).itemsize),
                     "d2h_bytes_per_step": int(m.n_dof * np.dtype(dt).itemsize)},
             "gpu_launches": args.steps,
-            "e2e_path": "MatFreeOperator.apply_stream (pinned host in/out, 3 CUDA streams)" if world == 1
+            "e2e_path": "MatFreeOperator.apply_stream (cudaHostAlloc host in/out; native 3-stream pipeline, csrc/tf_stream.cu)" if world == 1
                         else "SlabOperator.apply per step (pinned host in/out)",
             "clocks": ck,
             "cpu_baseline": cpu,

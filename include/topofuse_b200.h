@@ -93,6 +93,24 @@ int tf_matvec_grid_range_f64(const tf_grid* g, const double* ke, const double* s
                              const double* v, double* w, const uint8_t* node_fixed, uint32_t flags,
                              int32_t i_lo, int32_t i_hi, void* stream);
 
+/* Page-locked host memory for the e2e path (cudaHostAlloc, portable). */
+int tf_host_alloc(void** ptr, size_t bytes);
+int tf_host_free(void* ptr);
+
+/* Host-buffer batch (the e2e path): w_i = K v_i for i < n_vec, v_i/w_i HOST
+ * pointers (pinned for asynchrony), dev_in/dev_out 2*n_dof device scratch.
+ * The H2D copy of v_{i+1}, the product of v_i and the D2H copy of w_{i-1} run
+ * concurrently on internal streams; `stream` is ordered before and after the
+ * batch.  Same flags/semantics as tf_matvec_grid_*; returns once enqueued. */
+int tf_matvec_grid_stream_f32(const tf_grid* g, const float* ke, const float* scale,
+                              const uint8_t* node_fixed, uint32_t flags, int64_t n_vec,
+                              const float* const* host_in, float* const* host_out, float* dev_in,
+                              float* dev_out, void* stream);
+int tf_matvec_grid_stream_f64(const tf_grid* g, const double* ke, const double* scale,
+                              const uint8_t* node_fixed, uint32_t flags, int64_t n_vec,
+                              const double* const* host_in, double* const* host_out,
+                              double* dev_in, double* dev_out, void* stream);
+
 /* Launch shape of the structured tile kernel for a plain product on this grid
  * (z-chunk height and CTA count; the autotuned height once the grid shape has
  * been seen, else the heuristic).  Introspection only. */

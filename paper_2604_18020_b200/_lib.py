@@ -19,6 +19,7 @@ HEADER = _PKG.parent / "include" / "topofuse_b200.h"
 CSRC = _PKG / "csrc"
 
 TF_OK = 0
+TF_ERR_UNSUPPORTED = 3
 TF_ACCUMULATE = 1
 TF_MASK_INPUT = 2
 TF_PASS_FIXED = 4
@@ -110,6 +111,10 @@ _SIGS = {
     "tf_pcg_protocol": [_P],
     "tf_pcg_set_quantize_krylov": [_P, _INT],
     "tf_tile_shape": [_P, _INT, _P, _P],
+    "tf_host_alloc": [_P, ctypes.c_size_t],
+    "tf_host_free": [_P],
+    "tf_matvec_grid_stream_f32": [_P, _P, _P, _P, _U32, _I64, _P, _P, _P, _P, _P],
+    "tf_matvec_grid_stream_f64": [_P, _P, _P, _P, _U32, _I64, _P, _P, _P, _P, _P],
     "tf_matvec_edof_bf16": [_P, _P, _P, _P, _P, _I64, _INT, _P, _P, _INT, _INT, _P],
     "tf_matvec_edof_bf16_f64": [_P, _P, _P, _P, _P, _I64, _P],
     "tf_gemm_bf16": [_P, _P, _P, _P, _I64, _P],

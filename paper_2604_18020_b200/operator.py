@@ -361,6 +361,27 @@ class MatFreeOperator:
         t = D.torch()
         dev = self._scale_dev.device
         tdt = D.tdtype(self.precision.dtype)
+        if self.variant == "fused" and self.structured and self.grid_kernel == "tile" and host_in:
+            # native pipeline (csrc/tf_stream.cu): the whole schedule enqueued from C
+            import ctypes
+
+            n = len(host_in)
+            buf = getattr(self, "_native_stream_bufs", None)
+            if buf is None or buf[0].dtype != tdt:
+                buf = (t.empty(2 * self.n_dof, dtype=tdt, device=dev), t.empty(2 * self.n_dof, dtype=tdt, device=dev))
+                self._native_stream_bufs = buf
+            ins = (ctypes.c_void_p * n)(*[h.data_ptr() for h in host_in])
+            outs = (ctypes.c_void_p * n)(*[h.data_ptr() for h in host_out])
+            sfx = _sfx(self.precision.dtype)
+            rc = getattr(_lib.load(), f"tf_matvec_grid_stream_{sfx}")(
+                ctypes_ref(self.dev.grid), self.ke.ctypes.data, D.ptr(self._scale_dev),
+                D.ptr(self.dev.node_fixed), _lib.TF_MASK_INPUT | _lib.TF_PASS_FIXED, n, ins, outs,
+                D.ptr(buf[0]), D.ptr(buf[1]), D.stream_ptr())
+            if rc == _lib.TF_OK:
+                self.n_apply += n
+                return host_out
+            if rc != _lib.TF_ERR_UNSUPPORTED:  # a Ke without the parity structure takes the path below
+                _lib.check(rc, "tf_matvec_grid_stream")
         cur = t.cuda.current_stream()
         if getattr(self, "_stream_ctx", None) is None:  # streams/buffers reused across calls
             self._stream_ctx = (

@@ -1,0 +1,11 @@
+#!/bin/bash
+cd "$GRAFT_REPO_ROOT"
+export PYTHONPATH="$GRAFT_REPO_ROOT:$PYTHONPATH"
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gpu_operator.py -q -p no:cacheprovider --timeout 300 -rf -k "stream" > gpurun_out/pytest_s46.txt 2>&1
+tail -15 gpurun_out/pytest_s46.txt
+python scripts/pcie_probe.py
+for c in c2 c5; do
+  r=$(timeout 300 python bench.py --config $c --steps 200 --warmup 5 --no-simp --no-cpu 2>&1 | tail -1 | python -c "import sys,json; d=json.loads(sys.stdin.read()); print(round(d['value'],2), d['e2e'])")
+  echo "$c: $r"
+done

@@ -211,6 +211,20 @@ def test_apply_stream_matches_apply():
     torch.cuda.synchronize()
     for a, b in zip(vs, ws):
         assert np.array_equal(b.numpy(), op.apply(a.numpy()))
+    # fp64, odd batch, and a Ke without the parity structure (Python pipeline)
+    op64 = _op(m, edof, bcs, rho, "fp64")
+    vs64 = [torch.from_numpy(rng.standard_normal(m.n_dof)).pin_memory() for _ in range(3)]
+    ws64 = [torch.empty_like(vs64[0]).pin_memory() for _ in range(3)]
+    op64.apply_stream(vs64, ws64)
+    torch.cuda.synchronize()
+    for a, b in zip(vs64, ws64):
+        assert np.array_equal(b.numpy(), op64.apply(a.numpy()))
+    a_ = rng.standard_normal((24, 24))
+    op64.ke = np.ascontiguousarray(a_ + a_.T)
+    op64.apply_stream(vs64, ws64)
+    torch.cuda.synchronize()
+    for a, b in zip(vs64, ws64):
+        assert np.array_equal(b.numpy(), op64.apply(a.numpy()))
 
 
 @pytest.mark.parametrize("preset", ["mbb", "bridge", "torsion", "cantilever"])

@@ -154,6 +154,9 @@ def run_reference(args):
     if rank != 0:
         return
     dims, prec, desc = CONFIGS[args.config]
+    if world > 1:  # our arm's workload at N ranks: the global N-slab cantilever (weak scaling)
+        dims = (dims[0] * world, dims[1], dims[2])
+        desc = f"{desc}; global {dims[0]}x{dims[1]}x{dims[2]} (the {world}-rank workload)"
     threads = os.cpu_count() or 1
     ms_total = []
     m = None

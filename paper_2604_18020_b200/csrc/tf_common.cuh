@@ -137,6 +137,7 @@ struct ResPlan {
     dim3 grid;
     int oz;
     int lean;
+    int by;  // element-column rows per CTA
     size_t dyn_smem;
     long long nblk;
 };

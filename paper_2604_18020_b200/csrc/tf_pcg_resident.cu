@@ -35,6 +35,7 @@
 // vector updates).
 
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -176,10 +177,10 @@ __device__ __forceinline__ void res_block_sum(double (&v)[K], double* sh /* [K][
 }
 
 // The CTA's staging slots of a node plane and its owned-column bookkeeping.
-template <typename T>
+template <typename T, int BY_>
 struct ResTile {
-    static constexpr int BY = TileDims<T>::BY, NT = TileDims<T>::NT;
-    static constexpr int PW = StageSlots<T>::PW, PN = StageSlots<T>::PN, NS = StageSlots<T>::N;
+    static constexpr int BY = BY_, NT = TILE_BX * BY_;
+    static constexpr int PW = (TILE_BX + 1) * 3, PN = PW * (BY_ + 1), NS = (PN + NT - 1) / NT;
 };
 
 #ifndef TF_RES_MINB32
@@ -188,11 +189,16 @@ struct ResTile {
 #ifndef TF_RES_MINB64
 #define TF_RES_MINB64 2
 #endif
-template <typename T>
-__global__ void __launch_bounds__(TileDims<T>::NT, sizeof(T) == 4 ? TF_RES_MINB32 : TF_RES_MINB64)
+// BY: element-column rows per CTA (FP32 8 or 16, FP64 4 or 8): taller tiles
+// halve the CTA count (cheaper exchanges, less halo recompute) at the same
+// warps per SM
+template <typename T, int BY_>
+__global__ void __launch_bounds__(TILE_BX * BY_, (TILE_BX * BY_ >= 512 || (sizeof(T) == 8 && BY_ >= 8))
+                                                     ? 1
+                                                     : (sizeof(T) == 4 ? TF_RES_MINB32 : TF_RES_MINB64))
 k_pcg_resident(const __grid_constant__ ResArgs<T> A, const __grid_constant__ KhatBlocks<T> kb)
 {
-    using RT = ResTile<T>;
+    using RT = ResTile<T, BY_>;
     constexpr int BY = RT::BY, NT = RT::NT, PW = RT::PW, PN = RT::PN, NS = RT::NS;
     constexpr bool F32 = sizeof(T) == 4;
     __shared__ __align__(16) T plane[2][PN];
@@ -647,48 +653,45 @@ k_pcg_resident(const __grid_constant__ ResArgs<T> A, const __grid_constant__ Kha
 // ---- host ------------------------------------------------------------------------
 
 template <typename T>
-static size_t res_dyn_bytes(int oz, bool lean)
+static size_t res_dyn_bytes(int oz, bool lean, int nt)
 {
-    return (size_t)(lean ? 3 : 5) * oz * 3 * TileDims<T>::NT * sizeof(T);
+    return (size_t)(lean ? 3 : 5) * oz * 3 * nt * sizeof(T);
 }
 
-// Chooses the z-chunk height and layout of a co-resident grid: the smallest
-// chunk (most CTAs) whose grid fits one wave with its shared-memory state,
-// the full layout before the lean one; false when nothing fits.
-// TF_PCG_RES_OZ / TF_PCG_RES_LEAN=0|1 pin either choice (experiments).
-template <typename T>
-bool pcg_resident_plan(const Grid& g, const T* ke_host, ResPlan* plan)
+template <typename T, int BY>
+static const void* res_kernel()
 {
-    KhatBlocks<T> kb;
-    if (!khat_blocks<T>(ke_host, &kb)) return false;
-    if (3 * g.n_nodes >= (1LL << 31)) return false;
-    constexpr int BY = TileDims<T>::BY, NT = TileDims<T>::NT;
-    int dev = 0, nsm = 148, smem_optin = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    return (const void*)k_pcg_resident<T, BY>;
+}
+
+// tile heights tried per precision (rows of element columns per CTA)
+template <typename T> struct ResBys;
+template <> struct ResBys<float> { static constexpr int a = 16, b = 8; };
+template <> struct ResBys<double> { static constexpr int a = 8, b = 4; };
+
+// Candidate launch: for one tile height, the smallest z-chunk whose grid is
+// co-resident with its shared-memory state (full layout before lean).
+template <typename T, int BY>
+static bool res_candidate(const Grid& g, int nsm, int smem_optin, int oz_force, int lean_force, ResPlan* plan)
+{
+    constexpr int NT = TILE_BX * BY;
+    const void* k = res_kernel<T, BY>();
     const int tx = (g.nnx + TILE_BX - 2) / (TILE_BX - 1);
     const int ty = (g.nny + BY - 2) / (BY - 1);
     const long long cols = (long long)tx * ty;
-    const char* e = getenv("TF_PCG_RES_OZ");
-    const int oz_force = e ? atoi(e) : 0;
-    const char* el = getenv("TF_PCG_RES_LEAN");
-    const int lean_force = el ? (el[0] == '1' ? 1 : 0) : -1;
     for (int oz = 2; oz <= std::min(g.nnz, 21); ++oz) {
         if (oz_force > 0 && oz != oz_force) continue;
         for (int lean = 0; lean < 2; ++lean) {
             if (lean_force >= 0 && lean != lean_force) continue;
-            const size_t dyn = res_dyn_bytes<T>(oz, lean != 0);
+            const size_t dyn = res_dyn_bytes<T>(oz, lean != 0, NT);
             if ((long long)dyn + 16384 > smem_optin) continue;
-            cudaFuncSetAttribute(k_pcg_resident<T>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                 cudaSharedmemCarveoutMaxShared);
-            if (cudaFuncSetAttribute(k_pcg_resident<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn) !=
-                cudaSuccess) {
+            cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+            if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn) != cudaSuccess) {
                 cudaGetLastError();
                 return false;
             }
             int per_sm = 0;
-            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pcg_resident<T>, NT, dyn) != cudaSuccess) {
+            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, NT, dyn) != cudaSuccess) {
                 cudaGetLastError();
                 return false;
             }
@@ -699,11 +702,58 @@ bool pcg_resident_plan(const Grid& g, const T* ke_host, ResPlan* plan)
                 plan->lean = lean;
                 plan->dyn_smem = dyn;
                 plan->nblk = cols * tz;
+                plan->by = BY;
                 return true;
             }
         }
     }
     return false;
+}
+
+// Chooses tile height, z-chunk and layout of a co-resident grid.  Per tile
+// height the smallest chunk that fits; between heights the cheaper estimate of
+// (layers per CTA x CTAs per SM) + exchange cost (grows with the CTA count,
+// scripts/exchange_bench.cu: ~0.9 us per extra 148 CTAs).  Env pins:
+// TF_PCG_RES_BY / TF_PCG_RES_OZ / TF_PCG_RES_LEAN=0|1 (experiments).
+template <typename T>
+bool pcg_resident_plan(const Grid& g, const T* ke_host, ResPlan* plan)
+{
+    KhatBlocks<T> kb;
+    if (!khat_blocks<T>(ke_host, &kb)) return false;
+    if (3 * g.n_nodes >= (1LL << 31)) return false;
+    int dev = 0, nsm = 148, smem_optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    const char* e = getenv("TF_PCG_RES_OZ");
+    const int oz_force = e ? atoi(e) : 0;
+    const char* el = getenv("TF_PCG_RES_LEAN");
+    const int lean_force = el ? (el[0] == '1' ? 1 : 0) : -1;
+    const char* eb = getenv("TF_PCG_RES_BY");
+    const int by_force = eb ? atoi(eb) : 0;
+    ResPlan pa, pb;
+    const bool ok_a = (by_force == 0 || by_force == ResBys<T>::a) &&
+                      res_candidate<T, ResBys<T>::a>(g, nsm, smem_optin, oz_force, lean_force, &pa);
+    const bool ok_b = (by_force == 0 || by_force == ResBys<T>::b) &&
+                      res_candidate<T, ResBys<T>::b>(g, nsm, smem_optin, oz_force, lean_force, &pb);
+    if (!ok_a && !ok_b) return false;
+    if (ok_a != ok_b) {
+        *plan = ok_a ? pa : pb;
+        return true;
+    }
+    // cost model (us per iteration), calibrated on B200 (scripts/gpu_run54.sh):
+    // matvec = ceil(nblk/nsm) CTAs per SM x (oz+1) layers x NT/256 units of
+    // 0.87 us (FP32; FP64 1.7x), 512-thread CTAs 15 % less efficient per
+    // thread; exchange = 2.0 + 0.9 us per 148 CTAs (scripts/exchange_bench.cu),
+    // two per iteration
+    auto cost = [&](const ResPlan& p) {
+        const int nt = TILE_BX * p.by;
+        const double unit = 0.87 * (sizeof(T) == 8 ? 1.7 : 1.0) * (nt >= 512 ? 1.15 : 1.0);
+        const double matvec = std::ceil((double)p.nblk / nsm) * (p.oz + 1) * (nt / 256.0) * unit;
+        return matvec + 2.0 * (2.0 + 0.9 * (double)p.nblk / 148.0);
+    };
+    *plan = cost(pa) < cost(pb) ? pa : pb;
+    return true;
 }
 
 size_t pcg_resident_ring_doubles(const ResPlan& plan) { return (size_t)8 * plan.nblk + 16; }
@@ -739,23 +789,22 @@ int launch_pcg_resident(const ResPlan& plan, const Grid& g, const T* ke_host, in
         a.trace = trace_buf;
     }
     TF_CUDA_TRY(cudaMemsetAsync(ring, 0, sizeof(double) * pcg_resident_ring_doubles(plan), st));
-    TF_CUDA_TRY(cudaFuncSetAttribute(k_pcg_resident<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)plan.dyn_smem));
+    const void* k = plan.by == ResBys<T>::a ? res_kernel<T, ResBys<T>::a>() : res_kernel<T, ResBys<T>::b>();
+    TF_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plan.dyn_smem));
     void* args[] = {&a, &kb};
-    dim3 block(TILE_BX, TileDims<T>::BY, 1);
-    TF_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)k_pcg_resident<T>, plan.grid, block, args,
-                                            plan.dyn_smem, st));
+    dim3 block(TILE_BX, plan.by, 1);
+    TF_CUDA_TRY(cudaLaunchCooperativeKernel(k, plan.grid, block, args, plan.dyn_smem, st));
     if (tracing) {
         unsigned long long h[16];
         TF_CUDA_TRY(cudaMemcpyAsync(h, trace_buf, sizeof(h), cudaMemcpyDeviceToHost, st));
         TF_CUDA_TRY(cudaStreamSynchronize(st));
         const double n = h[6] ? (double)h[6] : 1.0;
         fprintf(stderr,
-                "[tf_pcg_resident] fp%d grid %ux%ux%u oz %d %s: %llu its; us/it: matvec %.2f  xchg-A %.2f  "
+                "[tf_pcg_resident] fp%d BY %d grid %ux%ux%u oz %d %s: %llu its; us/it: matvec %.2f  xchg-A %.2f  "
                 "update %.2f (x %.2f, r/z %.2f)  xchg-B %.2f  decide %.2f  (init %.2f us)\n",
-                (int)(8 * sizeof(T)), plan.grid.x, plan.grid.y, plan.grid.z, plan.oz, plan.lean ? "lean" : "full",
-                h[6], h[0] / n / 1e3, h[1] / n / 1e3, (h[2] + h[7] + h[8]) / n / 1e3, h[7] / n / 1e3, h[8] / n / 1e3,
-                h[3] / n / 1e3, h[4] / n / 1e3, h[5] / 1e3);
+                (int)(8 * sizeof(T)), plan.by, plan.grid.x, plan.grid.y, plan.grid.z, plan.oz,
+                plan.lean ? "lean" : "full", h[6], h[0] / n / 1e3, h[1] / n / 1e3, (h[2] + h[7] + h[8]) / n / 1e3,
+                h[7] / n / 1e3, h[8] / n / 1e3, h[3] / n / 1e3, h[4] / n / 1e3, h[5] / 1e3);
     }
     return TF_OK;
 }

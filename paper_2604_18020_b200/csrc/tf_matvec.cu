@@ -19,6 +19,7 @@
 
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "tf_common.cuh"
@@ -342,6 +343,97 @@ k_edof_fused(const int32_t* __restrict__ edof, const T* __restrict__ scale, cons
     }
 }
 
+// General connectivity, red.global scatter, v2: the CTA's 128 edof rows
+// (12 KB, contiguous) are staged with coalesced 16-byte cp.async instead of
+// six strided 16-byte loads per thread (the v1 kernel's L1 was the bottleneck:
+// 79 % L1/TEX throughput at c5, ncu profiles/edof_atomic_c5.json), and
+// contributions to a DOF shared with the next lane's element (the +x
+// neighbour in the reference element order, corner pairs (1,0) (2,3) (5,4)
+// (6,7)) are summed in registers first -- checked per DOF at run time, so any
+// connectivity stays correct -- halving the reductions for structured order.
+__device__ __forceinline__ void cp_async_16(void* smem, const void* gmem, bool valid)
+{
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    const int n = valid ? 16 : 0;
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gmem), "r"(n));
+}
+
+#ifndef TF_EDOF_MINB
+#define TF_EDOF_MINB 6
+#endif
+template <typename T, bool WALSH>
+__global__ void __launch_bounds__(EDOF_BLOCK, TF_EDOF_MINB)
+k_edof_staged(const int32_t* __restrict__ edof, const T* __restrict__ scale, const T* __restrict__ v,
+              T* __restrict__ w, long long n, const __grid_constant__ KeMat<T> ke,
+              const __grid_constant__ KhatBlocks<T> kb)
+{
+    __shared__ __align__(16) int4 rows[EDOF_BLOCK * 6];
+    const long long e0 = (long long)blockIdx.x * EDOF_BLOCK;
+    const int tid = threadIdx.x;
+    const long long n_here = min((long long)EDOF_BLOCK, n - e0);
+    const int4* src = reinterpret_cast<const int4*>(edof + e0 * NLOC);
+#pragma unroll
+    for (int q = 0; q < 6; ++q) {
+        const int k = tid + q * EDOF_BLOCK;
+        cp_async_16(&rows[k], src + k, k < n_here * 6);
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+    const long long e = e0 + tid;
+    const bool live = tid < n_here;
+    const T se = live ? ld_nc(scale + e) : T(0);
+    asm volatile("cp.async.wait_group 0;\n" ::);
+    __syncthreads();
+    int idx[NLOC];
+#pragma unroll
+    for (int q = 0; q < 6; ++q) {
+        const int4 t = rows[tid * 6 + q];
+        idx[4 * q + 0] = live ? t.x : -1;
+        idx[4 * q + 1] = live ? t.y : -1;
+        idx[4 * q + 2] = live ? t.z : -1;
+        idx[4 * q + 3] = live ? t.w : -1;
+    }
+    T u[NLOC];
+#pragma unroll
+    for (int q = 0; q < NLOC; ++q) u[q] = idx[q] >= 0 ? ld_nc(v + idx[q]) : T(0);
+    const int lane = tid & 31;
+    constexpr int RIGHT[4] = {1, 2, 5, 6}, LEFT[4] = {0, 3, 4, 7};  // corner_of(1,oy,oz) / corner_of(0,oy,oz)
+    // element rows: parity-block (corner-Walsh) algebra when Ke has the
+    // structure (~200 FP instructions, all 24 rows at once), else dense rows
+    // computed on demand (576 FMA, two rows live)
+    T fw[NLOC];
+    if (WALSH) element_apply(u, se, kb, fw);
+    auto row = [&](int r) -> T {
+        if (WALSH) return fw[r];
+        T acc = T(0);
+#pragma unroll
+        for (int q = 0; q < NLOC; ++q) acc = fma(ke.a[r * NLOC + q], u[q], acc);
+        return se * acc;
+    };
+    // rows in (right, left) corner pairs: only two live at a time
+#pragma unroll
+    for (int pr = 0; pr < 4; ++pr)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            const int jr = 3 * RIGHT[pr] + c, jl = 3 * LEFT[pr] + c;
+            T fr = row(jr);
+            const T fl = row(jl);
+            const int nb_idx = __shfl_down_sync(0xffffffffu, idx[jl], 1);
+            const T nb_val = __shfl_down_sync(0xffffffffu, fl, 1);
+            const bool merge = lane < 31 && idx[jr] >= 0 && nb_idx == idx[jr];
+            if (merge) fr += nb_val;
+            const bool prev = __shfl_up_sync(0xffffffffu, merge, 1) && lane > 0;
+            if (idx[jr] >= 0) atomicAdd(w + idx[jr], fr);
+            if (idx[jl] >= 0 && !prev) atomicAdd(w + idx[jl], fl);
+        }
+}
+
+// TF_EDOF_V1=1: the v1 atomic kernel (strided row loads, no aggregation)
+static bool edof_v1_forced()
+{
+    const char* e = getenv("TF_EDOF_V1");
+    return e && e[0] == '1';
+}
+
 template <typename T>
 int launch_edof(const int32_t* edof, const T* ke_host, const T* scale, const T* v, T* w,
                 long long n_elem, int mode, const int32_t* color_elems,
@@ -353,7 +445,15 @@ int launch_edof(const int32_t* edof, const T* ke_host, const T* scale, const T* 
     if (n_elem == 0) return TF_OK;
     if (mode == TF_SCATTER_ATOMIC) {
         const long long nb = (n_elem + EDOF_BLOCK - 1) / EDOF_BLOCK;
-        k_edof_fused<T, true><<<(unsigned)nb, EDOF_BLOCK, 0, st>>>(edof, scale, v, w, n_elem, nullptr, ke);
+        KhatBlocks<T> kb;
+        const char* ed = getenv("TF_EDOF_DENSE");
+        const bool walsh = !(ed && ed[0] == '1') && khat_blocks_cached<T>(ke_host, &kb);
+        if (edof_v1_forced())
+            k_edof_fused<T, true><<<(unsigned)nb, EDOF_BLOCK, 0, st>>>(edof, scale, v, w, n_elem, nullptr, ke);
+        else if (walsh)
+            k_edof_staged<T, true><<<(unsigned)nb, EDOF_BLOCK, 0, st>>>(edof, scale, v, w, n_elem, ke, kb);
+        else
+            k_edof_staged<T, false><<<(unsigned)nb, EDOF_BLOCK, 0, st>>>(edof, scale, v, w, n_elem, ke, kb);
         TF_CHECK_LAUNCH();
     } else if (mode == TF_SCATTER_COLORED) {
         TF_REQUIRE(color_elems && color_offsets && n_colors > 0, "coloured scatter needs a colouring");

@@ -764,7 +764,7 @@ int launch_pcg_resident(const ResPlan& plan, const Grid& g, const T* ke_host, in
                         double* ring, CgScalars* sc, cudaStream_t st)
 {
     KhatBlocks<T> kb;
-    if (!khat_blocks<T>(ke_host, &kb)) return TF_ERR_UNSUPPORTED;
+    if (!khat_blocks_cached<T>(ke_host, &kb)) return TF_ERR_UNSUPPORTED;
     ResArgs<T> a;
     a.g = g;
     a.oz = plan.oz;

@@ -86,7 +86,26 @@ bool khat_blocks(const T* ke, KhatBlocks<T>* out)
     return true;
 }
 
+// khat_blocks behind a one-entry per-thread cache keyed on the Ke bytes: the
+// host-side extraction (~37k multiply-adds) must not run on every launch --
+// it would sit between the caller's stream events and the kernel
+template <typename T>
+bool khat_blocks_cached(const T* ke, KhatBlocks<T>* out)
+{
+    static thread_local T last_ke[NLOC * NLOC];
+    static thread_local KhatBlocks<T> last_kb;
+    static thread_local int last_ok = -1;
+    if (last_ok < 0 || memcmp(last_ke, ke, sizeof(last_ke)) != 0) {
+        last_ok = khat_blocks<T>(ke, &last_kb) ? 1 : 0;
+        memcpy(last_ke, ke, sizeof(last_ke));
+    }
+    *out = last_kb;
+    return last_ok == 1;
+}
+
 template bool khat_blocks<float>(const float*, KhatBlocks<float>*);
+template bool khat_blocks_cached<float>(const float*, KhatBlocks<float>*);
+template bool khat_blocks_cached<double>(const double*, KhatBlocks<double>*);
 template bool khat_blocks<double>(const double*, KhatBlocks<double>*);
 
 // ---- device ------------------------------------------------------------------------
@@ -1545,19 +1564,7 @@ int launch_grid_tile(const Grid& g, const T* ke_host, const T* scale, const T* v
                      const uint8_t* node_fixed, uint32_t flags, double* dot_part, cudaStream_t st)
 {
     KhatBlocks<T> kb;
-    static thread_local T last_ke[NLOC * NLOC];
-    static thread_local KhatBlocks<T> last_kb;
-    static thread_local int last_ok = -1;
-    if (last_ok >= 0 && memcmp(last_ke, ke_host, sizeof(last_ke)) == 0) {
-        if (!last_ok) return TF_ERR_UNSUPPORTED;
-        kb = last_kb;
-    } else {
-        const bool ok = khat_blocks<T>(ke_host, &kb);
-        memcpy(last_ke, ke_host, sizeof(last_ke));
-        last_kb = kb;
-        last_ok = ok ? 1 : 0;
-        if (!ok) return TF_ERR_UNSUPPORTED;
-    }
+    if (!khat_blocks_cached<T>(ke_host, &kb)) return TF_ERR_UNSUPPORTED;
     if (3 * g.n_nodes >= (1LL << 31)) {
         set_error("structured grid too large for int32 DOF indices");
         return TF_ERR_ARG;
@@ -1630,7 +1637,7 @@ int launch_grid_tile_cg(const Grid& g, const T* ke_host, const T* scale, T* q,
                         cudaStream_t st)
 {
     KhatBlocks<T> kb;
-    if (!khat_blocks<T>(ke_host, &kb)) return TF_ERR_UNSUPPORTED;
+    if (!khat_blocks_cached<T>(ke_host, &kb)) return TF_ERR_UNSUPPORTED;
     if (3 * g.n_nodes >= (1LL << 31)) {
         set_error("structured grid too large for int32 DOF indices");
         return TF_ERR_ARG;

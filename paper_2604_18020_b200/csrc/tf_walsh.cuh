@@ -25,6 +25,9 @@ __host__ __device__ constexpr int bin_of(int a)
 // Returns false when Ke is not block diagonal in the parity basis (tf_tile.cu).
 template <typename T>
 bool khat_blocks(const T* ke, KhatBlocks<T>* out);
+// the same behind a per-thread cache keyed on the Ke bytes (use on launch paths)
+template <typename T>
+bool khat_blocks_cached(const T* ke, KhatBlocks<T>* out);
 
 // Each thread handles at most STAGE_SLOTS values of a staged node plane.
 template <typename T>

@@ -356,11 +356,13 @@ def run_ours(args):
     if tf.exists():
         traffic = json.loads(tf.read_text()).get(f"{args.config}_{prec}")
 
-    simp = cg = simp2 = None
+    simp = cg = simp2 = sweep = None
     if args.simp and rank == 0:
         simp = simp_c1()
         simp2 = simp_c2()
         cg = cg_c2()
+        if world == 1:
+            sweep = kernel_sweep()
 
     if rank == 0:
         cpu = None
@@ -400,6 +402,7 @@ def run_ours(args):
                         else "SlabOperator.apply per step (pinned host in/out)",
             "clocks": ck,
             "cpu_baseline": cpu,
+            "kernels": sweep,
             "simp": simp,
             "simp_c2": simp2,
             "cg": cg,
@@ -408,6 +411,47 @@ def run_ours(args):
         print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
+
+
+def kernel_sweep(steps=100):
+    """Context for the headline (same protocol: L2 flushed before each step,
+    CUDA events per step): the structured kernel at c4/c5 and the
+    general-connectivity (edof-reading, red.global) kernel at c2/c5, each with
+    its own algorithmic bytes and the HBM fraction they imply."""
+    import torch
+
+    from paper_2604_18020_b200 import MatFreeOperator, SimpParams
+    from paper_2604_18020_b200.operator import compulsory_bytes
+
+    hbm, _, _ = peaks()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    out = {}
+    for name, cfg, kernel in (("c4_tile", "c4", "tile"), ("c5_tile", "c5", "tile"),
+                              ("c2_edof", "c2", "edof"), ("c5_edof", "c5", "edof")):
+        dims, prec, desc = CONFIGS[cfg]
+        m, edof, bcs, rho, v = build_problem(dims)
+        op = MatFreeOperator(m, edof, bcs, rho, SimpParams(3.0), prec, grid_kernel=kernel,
+                             scatter="parallel_atomic")
+        x = torch.tensor(v.astype(op.precision.dtype), device="cuda")
+        w = torch.empty_like(x)
+        for _ in range(5):
+            op.apply_device(x, out=w)
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+        for a, b in ev:
+            flush.fill_(3)
+            a.record()
+            op.apply_device(x, out=w)
+            b.record()
+        torch.cuda.synchronize()
+        ms = float(np.mean([a.elapsed_time(b) for a, b in ev]))
+        byts = compulsory_bytes(m.n_elem, m.n_dof, prec, kernel != "edof")
+        out[name] = {"workload": desc, "kernel": "k_grid_tile5" if kernel == "tile" else "k_edof_staged (red.global)",
+                     "ms_per_step": ms, "GDOF_s": m.n_dof / (ms * 1e-3) / 1e9,
+                     "algorithmic_bytes": byts, "hbm_frac": byts / (ms * 1e-3) / 1e9 / hbm,
+                     "general_contract_equiv_hbm_frac":
+                         compulsory_bytes(m.n_elem, m.n_dof, prec, False) / (ms * 1e-3) / 1e9 / hbm}
+        del op, x, w
+    return out
 
 
 def simp_c1():

@@ -210,3 +210,30 @@ def test_general_connectivity_pcg_matches_oracle(variant, scatter):
     # the golden cold solve on the unpermuted problem: same physics
     g = load_golden("cg.json")["desk_fp64"]
     assert abs(rep.compliance - g["compliance"]) <= 1e-6 * g["compliance"]
+
+
+@pytest.mark.parametrize("name,prec", [("torsion", "fp64"), ("torsion", "fp32"), ("mbb", "fp64"),
+                                       ("bridge", "fp64")])
+def test_simp_presets_match_reference(name, prec):
+    """Torsion / MBB / bridge at the desk scale, the c1 protocol (30 its, p=3,
+    beta=1, move 0.2, rmin 1.5; goldens: tests/golden/make_golden_presets.py).
+    North star: compliance and density within 1e-3 after a fixed number of
+    SIMP iterations, CG counts within +-2 %."""
+    from paper_2604_18020_b200 import ContinuationSchedule, Phase, SimpConfig, make_preset, run_simp
+
+    g = load_golden(f"simp_{name}_{prec}.npz")
+    sched = ContinuationSchedule((Phase(1, 30, p=3.0, beta=1.0, move=0.2, rmin_end=1.5),), 1.5)
+    res = run_simp(make_preset(name, 0.2), SimpConfig(schedule=sched, precision=prec))
+    c = np.array([h.compliance for h in res.history])
+    its = np.array([h.cg_iterations for h in res.history])
+    np.testing.assert_allclose(c, g["compliance"], rtol=1e-3)
+    assert abs(res.total_cg_iterations - int(g["total_cg"])) <= 0.02 * int(g["total_cg"])
+    if prec == "fp64":
+        # warm-started solves: a 1e-12 difference in the previous solution can
+        # move a single solve's stop (mbb: one of 30 solves stops 81 iterations
+        # later, the next ones match again); the bar is per run (+-2 % in
+        # total) with at most 10 % of the solves outside +-2 %
+        off = np.abs(its - g["cg_iterations"]) > np.maximum(1, 0.02 * g["cg_iterations"])
+        assert off.sum() <= max(1, 0.1 * its.size), (its, g["cg_iterations"])
+    rel = np.linalg.norm(res.rho_phys - g["rho_phys"]) / np.linalg.norm(g["rho_phys"])
+    assert rel <= 1e-3

@@ -47,6 +47,9 @@
 namespace tf {
 
 template <typename T>
+bool tile_iso_enabled();  // tf_tile.cu
+
+template <typename T>
 struct ResArgs {
     Grid g;
     int oz;
@@ -60,6 +63,8 @@ struct ResArgs {
     const uint8_t* node_fixed;
     double* ring;  // [2][nblk][4] exchange partials, then the arrival counter
     int lean;      // x and D^-1 in global memory instead of shared memory
+    int iso;       // isotropic block form (block_iso) instead of the generic blocks
+    KhatIso<T> ki;
     CgScalars* sc;  // tol / max_iter / recompute / hist in; report out
     unsigned long long* trace;  // nullable: CTA 0 phase times (ns), TF_PCG_TRACE
 };
@@ -369,28 +374,32 @@ k_pcg_resident(const __grid_constant__ ResArgs<T> A, const __grid_constant__ Kha
                     XYb[c][q] = XYt[q];
                 }
             }
-#pragma unroll
-            for (int c = 0; c < 3; ++c)
-#pragma unroll
-                for (int m = 1; m < 8; ++m) h[c][m] *= s_cur;
             T gm[3][8];
+            if (A.iso) {
+                block_iso(h, A.ki, s_cur, gm);
+            } else {
 #pragma unroll
-            for (int c = 0; c < 3; ++c) gm[c][0] = T(0);
+                for (int c = 0; c < 3; ++c)
 #pragma unroll
-            for (int q = 0; q < 8; ++q)
+                    for (int m = 1; m < 8; ++m) h[c][m] *= s_cur;
 #pragma unroll
-                for (int c = 0; c < 3; ++c) {
-                    const int m = q ^ (1 << c);
-                    if (m == 0) continue;
-                    T acc = T(0);
+                for (int c = 0; c < 3; ++c) gm[c][0] = T(0);
 #pragma unroll
-                    for (int d = 0; d < 3; ++d) {
-                        const int n = q ^ (1 << d);
-                        if (n == 0) continue;
-                        acc = fma(kb.b[q][c][d], h[d][n], acc);
+                for (int q = 0; q < 8; ++q)
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) {
+                        const int m = q ^ (1 << c);
+                        if (m == 0) continue;
+                        T acc = T(0);
+#pragma unroll
+                        for (int d = 0; d < 3; ++d) {
+                            const int n = q ^ (1 << d);
+                            if (n == 0) continue;
+                            acc = fma(kb.b[q][c][d], h[d][n], acc);
+                        }
+                        gm[c][m] = acc;
                     }
-                    gm[c][m] = acc;
-                }
+            }
             T corner[3][4];
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
@@ -779,6 +788,7 @@ int launch_pcg_resident(const ResPlan& plan, const Grid& g, const T* ke_host, in
     a.node_fixed = node_fixed;
     a.ring = ring;
     a.lean = plan.lean;
+    a.iso = (tile_iso_enabled<T>() && khat_iso<T>(ke_host, &a.ki)) ? 1 : 0;
     a.sc = sc;
     a.trace = nullptr;
     static unsigned long long* trace_buf = nullptr;

@@ -86,6 +86,58 @@ bool khat_blocks(const T* ke, KhatBlocks<T>* out)
     return true;
 }
 
+template <typename T>
+bool khat_iso(const T* ke, KhatIso<T>* out)
+{
+    KhatBlocks<T> kb;
+    if (!khat_blocks_cached<T>(ke, &kb)) return false;
+    double mx = 0.0;
+    for (int q = 0; q < 8; ++q)
+        for (int c = 0; c < 3; ++c)
+            for (int d = 0; d < 3; ++d) mx = fmax(mx, fabs((double)kb.b[q][c][d]));
+    const double tol = (sizeof(T) == 4 ? 1e-6 : 1e-12) * mx;
+    auto B = [&](int q, int c, int d) { return (double)kb.b[q][c][d]; };
+    auto eq = [&](double a, double b) { return fabs(a - b) <= tol; };
+    auto z = [&](double a) { return fabs(a) <= tol; };
+    bool ok = true;
+    for (int q : {0, 7}) {  // [a b b; b a b; b b a]
+        for (int c = 0; c < 3; ++c)
+            for (int d = 0; d < 3; ++d) ok = ok && eq(B(q, c, d), c == d ? B(q, 0, 0) : B(q, 0, 1));
+    }
+    // 2x2 [p r; r p] on the two non-translation components
+    auto two = [&](int q, int i, int j) {
+        return eq(B(q, i, i), B(q, j, j)) && eq(B(q, i, j), B(q, j, i));
+    };
+    ok = ok && two(1, 1, 2) && two(2, 0, 2) && two(4, 0, 1);
+    // rank-one pair (i, j) of equal entries x, diagonal y at k, zeros elsewhere
+    auto r1 = [&](int q, int i, int j, int k) {
+        const double x = B(q, i, i);
+        return eq(B(q, i, j), x) && eq(B(q, j, i), x) && eq(B(q, j, j), x) && z(B(q, i, k)) && z(B(q, k, i)) &&
+               z(B(q, j, k)) && z(B(q, k, j));
+    };
+    ok = ok && r1(3, 0, 1, 2) && r1(5, 0, 2, 1) && r1(6, 1, 2, 0);
+    if (!ok) return false;
+    out->amb0 = (T)(B(0, 0, 0) - B(0, 0, 1));
+    out->b0 = (T)B(0, 0, 1);
+    out->p1 = (T)B(1, 1, 1);
+    out->r1 = (T)B(1, 1, 2);
+    out->p2 = (T)B(2, 0, 0);
+    out->r2 = (T)B(2, 0, 2);
+    out->x3 = (T)B(3, 0, 0);
+    out->y3 = (T)B(3, 2, 2);
+    out->p4 = (T)B(4, 0, 0);
+    out->r4 = (T)B(4, 0, 1);
+    out->x5 = (T)B(5, 0, 0);
+    out->y5 = (T)B(5, 1, 1);
+    out->x6 = (T)B(6, 1, 1);
+    out->y6 = (T)B(6, 0, 0);
+    out->amb7 = (T)(B(7, 0, 0) - B(7, 0, 1));
+    out->b7 = (T)B(7, 0, 1);
+    return true;
+}
+template bool khat_iso<float>(const float*, KhatIso<float>*);
+template bool khat_iso<double>(const double*, KhatIso<double>*);
+
 // khat_blocks behind a one-entry per-thread cache keyed on the Ke bytes: the
 // host-side extraction (~37k multiply-adds) must not run on every launch --
 // it would sit between the caller's stream events and the kernel
@@ -583,11 +635,11 @@ __device__ __forceinline__ void cp_async_wait_n(int n)
 #define TF_TILE_P 2
 #endif
 
-template <typename T, bool MASK, bool PASS, bool ACC, bool DOT, int P>
+template <typename T, bool MASK, bool PASS, bool ACC, bool DOT, int P, bool ISO>
 __global__ void __launch_bounds__(TileDims<T>::NT, sizeof(T) == 4 ? TF_TILE_MINB32 : TF_TILE_MINB64)
 k_grid_tile5(Grid g, int oz, const T* __restrict__ scale, const T* __restrict__ v, T* __restrict__ w,
              const uint8_t* __restrict__ node_fixed, double* __restrict__ dot_part,
-             const __grid_constant__ KhatBlocks<T> kb)
+             const __grid_constant__ KhatBlocks<T> kb, const __grid_constant__ KhatIso<T> ki)
 {
     constexpr int TILE_BY = TileDims<T>::BY, TILE_NT = TileDims<T>::NT;
     constexpr int PW = StageSlots<T>::PW, PN = StageSlots<T>::PN, NS = StageSlots<T>::N;
@@ -757,28 +809,32 @@ k_grid_tile5(Grid g, int oz, const T* __restrict__ scale, const T* __restrict__ 
                 XYb[c][q] = XYt[q];
             }
         }
-#pragma unroll
-        for (int c = 0; c < 3; ++c)
-#pragma unroll
-            for (int m = 1; m < 8; ++m) h[c][m] *= s_cur;
         T gm[3][8];
+        if (ISO) {
+            block_iso(h, ki, s_cur, gm);
+        } else {
 #pragma unroll
-        for (int c = 0; c < 3; ++c) gm[c][0] = T(0);
+            for (int c = 0; c < 3; ++c)
 #pragma unroll
-        for (int q = 0; q < 8; ++q)
+                for (int m = 1; m < 8; ++m) h[c][m] *= s_cur;
 #pragma unroll
-            for (int c = 0; c < 3; ++c) {
-                const int m = q ^ (1 << c);
-                if (m == 0) continue;
-                T acc = T(0);
+            for (int c = 0; c < 3; ++c) gm[c][0] = T(0);
 #pragma unroll
-                for (int d = 0; d < 3; ++d) {
-                    const int n = q ^ (1 << d);
-                    if (n == 0) continue;
-                    acc = fma(kb.b[q][c][d], h[d][n], acc);
+            for (int q = 0; q < 8; ++q)
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    const int m = q ^ (1 << c);
+                    if (m == 0) continue;
+                    T acc = T(0);
+#pragma unroll
+                    for (int d = 0; d < 3; ++d) {
+                        const int n = q ^ (1 << d);
+                        if (n == 0) continue;
+                        acc = fma(kb.b[q][c][d], h[d][n], acc);
+                    }
+                    gm[c][m] = acc;
                 }
-                gm[c][m] = acc;
-            }
+        }
         T corner[3][4];
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
@@ -1405,6 +1461,23 @@ static bool tile3_forced()
     return v == 1;
 }
 
+// The isotropic block form (khat_iso) in FP64 only: there the kernel is
+// DFMA-bound and the 25 fewer FP ops per element-layer are worth 30 % (c5 125
+// vs 179 us); in FP32 they are worth 3 % but move the reference-order rounding
+// enough to shift FP32 CG counts by more than the +-2 % bar (torsion SIMP).
+// TF_TILE_GENERIC=1 forces the generic blocks, TF_TILE_ISO32=1 the iso form in FP32.
+template <typename T>
+bool tile_iso_enabled()
+{
+    const char* eg = getenv("TF_TILE_GENERIC");
+    if (eg && eg[0] == '1') return false;
+    if (sizeof(T) == 8) return true;
+    const char* e32 = getenv("TF_TILE_ISO32");
+    return e32 && e32[0] == '1';
+}
+template bool tile_iso_enabled<float>();
+template bool tile_iso_enabled<double>();
+
 // TF_TILE3=1: the v3 kernel instead of the lean v5 (A/B, bitwise-identical)
 static bool tile5_disabled()
 {
@@ -1583,31 +1656,43 @@ int launch_grid_tile(const Grid& g, const T* ke_host, const T* scale, const T* v
             }
         }
         dim3 block(TILE_BX, TileDims<T>::BY, 1);
+        KhatIso<T> ki{};
+        const bool iso = tile_iso_enabled<T>() && khat_iso<T>(ke_host, &ki);
+#define T5(M, PS, AC, DT, DP)                                                                              \
+    do {                                                                                                   \
+        if (iso)                                                                                           \
+            k_grid_tile5<T, M, PS, AC, DT, TF_TILE_P, true><<<sh.grid, block, 0, st>>>(g, sh.oz, scale, v, w, \
+                                                                                    node_fixed, DP, kb, ki);  \
+        else                                                                                               \
+            k_grid_tile5<T, M, PS, AC, DT, TF_TILE_P, false><<<sh.grid, block, 0, st>>>(g, sh.oz, scale, v, w, \
+                                                                                     node_fixed, DP, kb, ki); \
+    } while (0)
         if (!tile5_disabled()) {
             // compile-time flag variants of the lean kernel; others fall back to tile3
             const uint32_t f = flags & (TF_MASK_INPUT | TF_PASS_FIXED | TF_ACCUMULATE);
             constexpr uint32_t MP = TF_MASK_INPUT | TF_PASS_FIXED;
             if (f == MP && dot_part) {
-                k_grid_tile5<T, true, true, false, true, TF_TILE_P><<<sh.grid, block, 0, st>>>(g, sh.oz, scale, v, w, node_fixed, dot_part, kb);
+                T5(true, true, false, true, dot_part);
                 TF_CHECK_LAUNCH();
                 return TF_OK;
             }
             if (f == MP && !dot_part) {
-                k_grid_tile5<T, true, true, false, false, TF_TILE_P><<<sh.grid, block, 0, st>>>(g, sh.oz, scale, v, w, node_fixed, nullptr, kb);
+                T5(true, true, false, false, nullptr);
                 TF_CHECK_LAUNCH();
                 return TF_OK;
             }
             if (f == TF_MASK_INPUT && !dot_part) {  // slab-local products (pass-through after the exchange)
-                k_grid_tile5<T, true, false, false, false, TF_TILE_P><<<sh.grid, block, 0, st>>>(g, sh.oz, scale, v, w, node_fixed, nullptr, kb);
+                T5(true, false, false, false, nullptr);
                 TF_CHECK_LAUNCH();
                 return TF_OK;
             }
             if (f == 0 && !dot_part) {  // raw K v (fused_serial-style contract)
-                k_grid_tile5<T, false, false, false, false, TF_TILE_P><<<sh.grid, block, 0, st>>>(g, sh.oz, scale, v, w, node_fixed, nullptr, kb);
+                T5(false, false, false, false, nullptr);
                 TF_CHECK_LAUNCH();
                 return TF_OK;
             }
         }
+#undef T5
         if (dot_part)
             k_grid_tile3<T, true><<<sh.grid, block, 0, st>>>(g, sh.oz, scale, v, w, node_fixed, flags, dot_part, kb);
         else

@@ -22,6 +22,56 @@ __host__ __device__ constexpr int bin_of(int a)
     return (a & 4) | ((a & 3) == 0 ? 0 : (a & 3) == 1 ? 1 : (a & 3) == 2 ? 3 : 2);
 }
 
+// Isotropic-material form of the parity blocks (unit_stiffness of any nu has
+// it): q=0/7 blocks [a b b; b a b; b b a], q=1/2/4 2x2 [p r; r p], q=3/5/6 a
+// rank-one 2x2 of equal entries x plus one diagonal y, all else zero.  Lets
+// the block product run in 33 FP ops instead of ~57, with the element scale
+// folded into the 16 coefficients (16 FMUL instead of 21).  Host-checked
+// (khat_iso); any other Ke keeps the generic block product.
+template <typename T>
+struct KhatIso {
+    T amb0, b0, p1, r1, p2, r2, x3, y3, p4, r4, x5, y5, x6, y6, amb7, b7;
+};
+
+template <typename T>
+bool khat_iso(const T* ke, KhatIso<T>* out);
+
+// gm[c][m] (m = 1..7) = sum_d s * Khat[q][c][d] h[d][q ^ (1<<d)] in the iso form
+template <typename T>
+__device__ __forceinline__ void block_iso(const T (&h)[3][8], const KhatIso<T>& k, T s, T (&gm)[3][8])
+{
+    const T amb0 = s * k.amb0, b0 = s * k.b0, p1 = s * k.p1, r1 = s * k.r1, p2 = s * k.p2, r2 = s * k.r2;
+    const T x3 = s * k.x3, y3 = s * k.y3, p4 = s * k.p4, r4 = s * k.r4, x5 = s * k.x5, y5 = s * k.y5;
+    const T x6 = s * k.x6, y6 = s * k.y6, amb7 = s * k.amb7, b7 = s * k.b7;
+    const T t0 = b0 * ((h[0][1] + h[1][2]) + h[2][4]);
+    gm[0][1] = fma(amb0, h[0][1], t0);
+    gm[1][2] = fma(amb0, h[1][2], t0);
+    gm[2][4] = fma(amb0, h[2][4], t0);
+    gm[1][3] = fma(r1, h[2][5], p1 * h[1][3]);
+    gm[2][5] = fma(r1, h[1][3], p1 * h[2][5]);
+    gm[0][3] = fma(r2, h[2][6], p2 * h[0][3]);
+    gm[2][6] = fma(r2, h[0][3], p2 * h[2][6]);
+    const T s3 = x3 * (h[0][2] + h[1][1]);
+    gm[0][2] = s3;
+    gm[1][1] = s3;
+    gm[2][7] = y3 * h[2][7];
+    gm[0][5] = fma(r4, h[1][6], p4 * h[0][5]);
+    gm[1][6] = fma(r4, h[0][5], p4 * h[1][6]);
+    const T s5 = x5 * (h[0][4] + h[2][1]);
+    gm[0][4] = s5;
+    gm[2][1] = s5;
+    gm[1][7] = y5 * h[1][7];
+    const T s6 = x6 * (h[1][4] + h[2][2]);
+    gm[1][4] = s6;
+    gm[2][2] = s6;
+    gm[0][7] = y6 * h[0][7];
+    const T t7 = b7 * ((h[0][6] + h[1][5]) + h[2][3]);
+    gm[0][6] = fma(amb7, h[0][6], t7);
+    gm[1][5] = fma(amb7, h[1][5], t7);
+    gm[2][3] = fma(amb7, h[2][3], t7);
+    gm[0][0] = gm[1][0] = gm[2][0] = T(0);
+}
+
 // Returns false when Ke is not block diagonal in the parity basis (tf_tile.cu).
 template <typename T>
 bool khat_blocks(const T* ke, KhatBlocks<T>* out);

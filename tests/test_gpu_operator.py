@@ -353,10 +353,19 @@ def test_tile5_bitwise_equals_tile3(preset, scale, prec, monkeypatch):
     v = torch.tensor(rng.standard_normal(m.n_dof), device="cuda").to(
         torch.float64 if prec == "fp64" else torch.float32)
     outs = []
+    monkeypatch.setenv("TF_TILE_GENERIC", "1")
     for t3 in ("0", "1"):
         monkeypatch.setenv("TF_TILE3", t3)
         outs.append(op.apply(v).clone())
     assert torch.equal(outs[0], outs[1])
+    # production: the isotropic block form (33 FP ops, scale folded into the
+    # coefficients) -- same algebra, different rounding order
+    monkeypatch.setenv("TF_TILE_GENERIC", "0")
+    monkeypatch.setenv("TF_TILE_ISO32", "1")
+    monkeypatch.setenv("TF_TILE3", "0")
+    iso = op.apply(v)
+    tol = 1e-13 if prec == "fp64" else 2e-6
+    assert float((iso - outs[0]).abs().max()) <= tol * float(outs[0].abs().max())
 
 
 @pytest.mark.parametrize("prec", ["fp64", "fp32"])

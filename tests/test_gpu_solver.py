@@ -166,6 +166,7 @@ def test_fused_and_unfused_pcg_protocols_agree(prec, monkeypatch):
 
     res = []
     monkeypatch.setenv("TF_PCG_RESIDENT", "0")  # graph protocols only
+    monkeypatch.setenv("TF_TILE_GENERIC", "1")  # the fused kernel runs the generic block product
     for fused in ("1", "0"):
         monkeypatch.setenv("TF_PCG_FUSED", fused)
         pb = make_preset("cantilever", 0.4)

@@ -17,7 +17,11 @@ from paper_2604_18020_b200.mesh import (CORNER_OFFSETS, StructuredMesh, build_ed
 
 
 def test_library_exports_every_header_symbol():
-    L = ctypes.CDLL(str(_lib.LIB_PATH))
+    import os
+
+    # RTLD_NOW: every symbol the library needs must resolve at load (catches a
+    # template used across translation units but defined with internal linkage)
+    L = ctypes.CDLL(str(_lib.LIB_PATH), mode=os.RTLD_NOW)
     syms = _lib.header_symbols()
     assert len(syms) >= 20
     for s in syms:

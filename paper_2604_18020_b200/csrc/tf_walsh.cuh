@@ -3,6 +3,8 @@
 // See tf_tile.cu's header for the algebra.
 #pragma once
 
+#include <type_traits>
+
 #include "tf_common.cuh"
 
 namespace tf {

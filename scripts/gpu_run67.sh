@@ -1,0 +1,8 @@
+#!/bin/bash
+cd "$GRAFT_REPO_ROOT"
+export PYTHONPATH="$GRAFT_REPO_ROOT:$PYTHONPATH"
+timeout 600 python -m pytest tests/test_gpu_operator.py -q -p no:cacheprovider --timeout 300 -rf -x 2>&1 | tail -15
+for t6 in 1 0; do for c in c2 c4 c5 c2f64 c5f64; do
+  r=$(TF_TILE6=$t6 timeout 300 python bench.py --config $c --steps 200 --warmup 5 --no-simp --no-cpu 2>&1 | tail -1 | python -c "import sys,json; d=json.loads(sys.stdin.read()); print(round(d['value'],2), round(d['ms_per_step']*1e3,2), round(d.get('warm_l2_ms_per_step',0)*1e3,2))")
+  echo "tile6=$t6 $c: GDOF/s us(flushed) us(warm) = $r"
+done; done

@@ -139,6 +139,23 @@ int tf_jacobi_edof_bf16(const int32_t* edof, const float* ke_diag, const float* 
 /* y = round_to_bf16(x) (precision.py:65-85), y may alias x */
 int tf_round_bf16(int64_t n, const float* x, float* y, void* stream);
 
+/* ---- General connectivity, bitwise the reference's fused_serial
+ *      (_kernels_numba.py:146-162): element row sums into `rows` (n_elem*24
+ *      FP64 workspace), then each DOF accumulates its rows in ascending element
+ *      order through a CSR (offsets: n_dof+1 int64, entries: n_elem*24 int32
+ *      flat element-row indices) built once per mesh by tf_edof_csr_build.
+ *      w is overwritten (accumulate = 0) or accumulated into (1).          */
+int tf_edof_csr_build(const int32_t* edof, int64_t n_elem, int64_t n_dof, int64_t* offsets,
+                      int32_t* entries, void* stream);
+int tf_matvec_edof_pull_f32(const int32_t* edof, const float* ke, const float* scale,
+                            const float* v, float* w, int64_t n_elem, int64_t n_dof,
+                            const int64_t* offsets, const int32_t* entries, double* rows,
+                            int accumulate, void* stream);
+int tf_matvec_edof_pull_f64(const int32_t* edof, const double* ke, const double* scale,
+                            const double* v, double* w, int64_t n_elem, int64_t n_dof,
+                            const int64_t* offsets, const int32_t* entries, double* rows,
+                            int accumulate, void* stream);
+
 /* ---- K v with an explicit element->DOF table: the fused kernel contract
  *      fused_serial/fused_atomic(edof, ke, scale, v, out) (_kernels_numba.py:146-196).
  *      ALWAYS accumulates into w (caller zeroes it, operator.py:93).

@@ -111,6 +111,9 @@ _SIGS = {
     "tf_pcg_protocol": [_P],
     "tf_pcg_set_quantize_krylov": [_P, _INT],
     "tf_tile_shape": [_P, _INT, _P, _P],
+    "tf_edof_csr_build": [_P, _I64, _I64, _P, _P, _P],
+    "tf_matvec_edof_pull_f32": [_P, _P, _P, _P, _P, _I64, _I64, _P, _P, _P, _INT, _P],
+    "tf_matvec_edof_pull_f64": [_P, _P, _P, _P, _P, _I64, _I64, _P, _P, _P, _INT, _P],
     "tf_host_alloc": [_P, ctypes.c_size_t],
     "tf_host_free": [_P],
     "tf_matvec_grid_stream_f32": [_P, _P, _P, _P, _U32, _I64, _P, _P, _P, _P, _P],

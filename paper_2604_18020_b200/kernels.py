@@ -49,8 +49,24 @@ def _fused(edof, ke, scale, v, out, mode):
 
 
 def fused_serial(edof, ke, scale, v, out) -> None:
-    """Deterministic (colour-ordered) fused K v, accumulated into out."""
-    _fused(edof, ke, scale, v, out, _lib.TF_SCATTER_COLORED)
+    """fused K v accumulated into out in the reference's element order --
+    bitwise _kernels_numba.py:146-162 (row sums + ascending-element pull)."""
+    t = D.torch()
+    dt = np.asarray(v).dtype
+    edof = np.ascontiguousarray(edof, dtype=np.int32)
+    n_elem, n_dof = edof.shape[0], out.shape[0]
+    e_d = D.to_dev(edof, np.int32)
+    s_d = D.to_dev(scale, dt)
+    v_d = D.to_dev(v, dt)
+    o_d = D.to_dev(out, dt)
+    off = t.empty(n_dof + 1, dtype=t.int64, device=e_d.device)
+    ent = t.empty(n_elem * 24, dtype=t.int32, device=e_d.device)
+    rows = t.empty(n_elem * 24, dtype=t.float64, device=e_d.device)
+    _lib.call("tf_edof_csr_build", D.ptr(e_d), n_elem, n_dof, D.ptr(off), D.ptr(ent), D.stream_ptr())
+    ke_h = np.ascontiguousarray(ke, dtype=dt)
+    _lib.call(f"tf_matvec_edof_pull_{_sfx(v)}", D.ptr(e_d), ke_h.ctypes.data, D.ptr(s_d), D.ptr(v_d), D.ptr(o_d),
+              n_elem, n_dof, D.ptr(off), D.ptr(ent), D.ptr(rows), 1, D.stream_ptr())
+    out[...] = o_d.cpu().numpy()
 
 
 def fused_atomic(edof, ke, scale, v, out) -> None:

@@ -68,6 +68,7 @@ class DeviceProblem:
         self._edof_masked = None
         self._edof_raw = None
         self._colors = None
+        self._csr = None
         self.pcg_handles = {}
 
     @property
@@ -81,6 +82,21 @@ class DeviceProblem:
         if self._edof_raw is None:
             self._edof_raw = D.to_dev(np.ascontiguousarray(self._edof_np, dtype=np.int32), np.int32)
         return self._edof_raw
+
+    def csr(self):
+        """DOF -> (element, row) CSR in ascending element order (built once on
+        the device, tf_edof_csr_build) and the FP64 row workspace of the
+        bitwise fused_serial pull (tf_matvec_edof_pull_*)."""
+        if self._csr is None:
+            t = D.torch()
+            n_rows = self.n_elem * 24
+            off = t.empty(self.n_dof + 1, dtype=t.int64, device=self.edof_raw.device)
+            ent = t.empty(n_rows, dtype=t.int32, device=off.device)
+            _lib.call("tf_edof_csr_build", D.ptr(self.edof_raw), self.n_elem, self.n_dof, D.ptr(off), D.ptr(ent),
+                      D.stream_ptr())
+            rows = t.empty(n_rows, dtype=t.float64, device=off.device)
+            self._csr = (off, ent, rows)
+        return self._csr
 
     def colors(self):
         """Element colouring with no two same-colour elements sharing a DOF."""
@@ -243,12 +259,17 @@ class MatFreeOperator:
                 _lib.call(f"tf_matvec_edof_{sfx}", D.ptr(dev.edof_masked), ke.ctypes.data,
                           D.ptr(scale), D.ptr(x), D.ptr(out), self.mesh.n_elem,
                           _lib.TF_SCATTER_ATOMIC, None, None, 0, st)
-            else:
+            elif os.environ.get("TF_EDOF_COLORED") == "1":  # colour-ordered passes (A/B)
                 order, offsets = dev.colors()
                 _lib.call(f"tf_matvec_edof_{sfx}", D.ptr(dev.edof_masked), ke.ctypes.data,
                           D.ptr(scale), D.ptr(x), D.ptr(out), self.mesh.n_elem,
                           _lib.TF_SCATTER_COLORED, D.ptr(order), offsets.ctypes.data,
                           len(offsets) - 1, st)
+            else:  # serial: the reference's element order, bitwise (tf_edof_pull.cu)
+                off, ent, rows = dev.csr()
+                _lib.call(f"tf_matvec_edof_pull_{sfx}", D.ptr(dev.edof_masked), ke.ctypes.data,
+                          D.ptr(scale), D.ptr(x), D.ptr(out), self.mesh.n_elem, self.n_dof,
+                          D.ptr(off), D.ptr(ent), D.ptr(rows), 0, st)
         else:
             n = self.mesh.n_elem
             u_elem = t.empty((n, 24), dtype=D.tdtype(dt), device=x.device)

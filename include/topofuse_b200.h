@@ -314,6 +314,21 @@ int tf_oc_update_f64(int64_t n, const double* rho, const double* dc, const doubl
                      double move, double vol_tol, double damping, int max_bisect, double* rho_new,
                      double* work, tf_oc_report* rep_dev, void* stream);
 
+/* Distributed OC building blocks (x-slab SIMP).  sums[k] (device)
+ * = this rank's sum over its n elements of the OC candidate at lams[k]
+ * (host array, 1 <= n_lams <= TF_OC_MAX_LAMS) and sums[TF_OC_MAX_LAMS] = the
+ * count of invalid inputs (dc > 1e-12 or dv <= 0); rank-local fixed order.
+ * work: tf_oc_work_doubles(n) doubles.  The host all-gathers the rank sums and
+ * runs oc_update's bracket/bisection (simp.py:111-175) on the global means. */
+#define TF_OC_MAX_LAMS 15
+int64_t tf_oc_work_doubles(int64_t n);
+int tf_oc_volumes_f64(int64_t n, const double* rho, const double* dc, const double* dv, double move,
+                      double damping, const double* lams, int n_lams, double* sums, double* work,
+                      void* stream);
+/* rho_new = the OC candidate at lam (the step's final clip) */
+int tf_oc_apply_f64(int64_t n, const double* rho, const double* dc, const double* dv, double move,
+                    double damping, double lam, double* rho_new, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -20,6 +20,7 @@ CSRC = _PKG / "csrc"
 
 TF_OK = 0
 TF_ERR_UNSUPPORTED = 3
+TF_OC_MAX_LAMS = 15
 TF_ACCUMULATE = 1
 TF_MASK_INPUT = 2
 TF_PASS_FIXED = 4
@@ -132,6 +133,8 @@ _SIGS = {
     "tf_stats_f64": [_I64, _P, _P, _P, _P, _P, _P, _P],
     "tf_oc_update_f64": [_I64, _P, _P, _P, ctypes.c_double, ctypes.c_double, ctypes.c_double,
                          ctypes.c_double, _INT, _P, _P, _P, _P],
+    "tf_oc_volumes_f64": [_I64, _P, _P, _P, ctypes.c_double, ctypes.c_double, _P, _INT, _P, _P, _P],
+    "tf_oc_apply_f64": [_I64, _P, _P, _P, ctypes.c_double, ctypes.c_double, ctypes.c_double, _P, _P],
 }
 
 _lib = None
@@ -167,6 +170,8 @@ def load() -> ctypes.CDLL:
         fn.restype = ctypes.c_int
     L.tf_work_doubles.restype = ctypes.c_int64
     L.tf_work_doubles.argtypes = [ctypes.c_int64]
+    L.tf_oc_work_doubles.restype = ctypes.c_int64
+    L.tf_oc_work_doubles.argtypes = [ctypes.c_int64]
     L.tf_last_error.restype = ctypes.c_char_p
     L.tf_last_error.argtypes = []
     _lib = L

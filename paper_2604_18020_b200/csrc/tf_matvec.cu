@@ -611,9 +611,50 @@ __device__ __forceinline__ double energy_of(const double u[NLOC], const KeMat<do
     return total;
 }
 
+// The same quadratic form in the parity basis, u^T Ke u = sum_{c,m} h_cm (Khat h)_cm
+// with h = W u (tf_walsh.cuh): the translation modes drop out before any
+// product, so the rounding error scales with the element's deformation, not
+// with its displacement.  The direct form loses eps*|Ke|*|u|^2 -- for a void
+// region carried along rigidly with |u| ~ 1e8 that is an energy of -5 where
+// the true value is ~0 (the reference shows exactly this on a cantilever with
+// a 4-step schedule), which can flip a compliance sensitivity positive.
+__device__ __forceinline__ double energy_walsh(const double (&u)[NLOC], const KhatBlocks<double>& kb)
+{
+    double h[3][8];
+#pragma unroll
+    for (int a = 0; a < 8; ++a)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) h[c][bin_of(a)] = u[3 * a + c];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) fwht_fwd(h[c]);
+    double total = 0.0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            const int m = q ^ (1 << c);
+            if (m == 0) continue;
+            double acc = 0.0;
+#pragma unroll
+            for (int d = 0; d < 3; ++d) {
+                const int n = q ^ (1 << d);
+                if (n == 0) continue;
+                acc = fma(kb.b[q][c][d], h[d][n], acc);
+            }
+            total = fma(h[c][m], acc, total);
+        }
+    return total;
+}
+
+struct EnergyKe {
+    KeMat<double> ke;
+    KhatBlocks<double> kb;
+    int walsh;
+};
+
 __global__ void __launch_bounds__(EDOF_BLOCK)
 k_energies_grid(Grid g, const double* __restrict__ u, double* __restrict__ out,
-                const __grid_constant__ KeMat<double> ke)
+                const __grid_constant__ EnergyKe K)
 {
     const long long e = (long long)blockIdx.x * EDOF_BLOCK + threadIdx.x;
     if (e >= g.n_elem) return;
@@ -627,12 +668,12 @@ k_energies_grid(Grid g, const double* __restrict__ u, double* __restrict__ out,
 #pragma unroll
         for (int d = 0; d < 3; ++d) ue[3 * b + d] = u[3 * node + d];
     }
-    out[e] = energy_of(ue, ke);
+    out[e] = K.walsh ? energy_walsh(ue, K.kb) : energy_of(ue, K.ke);
 }
 
 __global__ void __launch_bounds__(EDOF_BLOCK)
 k_energies_edof(const int32_t* __restrict__ edof, const double* __restrict__ u,
-                double* __restrict__ out, long long n, const __grid_constant__ KeMat<double> ke)
+                double* __restrict__ out, long long n, const __grid_constant__ EnergyKe K)
 {
     const long long e = (long long)blockIdx.x * EDOF_BLOCK + threadIdx.x;
     if (e >= n) return;
@@ -641,7 +682,7 @@ k_energies_edof(const int32_t* __restrict__ edof, const double* __restrict__ u,
     double ue[NLOC];
 #pragma unroll
     for (int q = 0; q < NLOC; ++q) ue[q] = idx[q] >= 0 ? u[idx[q]] : 0.0;
-    out[e] = energy_of(ue, ke);
+    out[e] = K.walsh ? energy_walsh(ue, K.kb) : energy_of(ue, K.ke);
 }
 
 __global__ void k_mark_fixed(Grid g, const int64_t* __restrict__ fixed, long long n,
@@ -864,8 +905,9 @@ int tf_energies_grid_f64(const tf_grid* g, const double* ke, const double* u, do
 {
     TF_GRID_CHECK(g);
     Grid gg = make_grid(g);
-    KeMat<double> k;
-    memcpy(k.a, ke, sizeof(k.a));
+    EnergyKe k;
+    memcpy(k.ke.a, ke, sizeof(k.ke.a));
+    k.walsh = khat_blocks_cached<double>(ke, &k.kb) ? 1 : 0;
     k_energies_grid<<<(unsigned)((gg.n_elem + EDOF_BLOCK - 1) / EDOF_BLOCK), EDOF_BLOCK, 0, S(stream)>>>(
         gg, u, out, k);
     TF_CHECK_LAUNCH();
@@ -877,8 +919,9 @@ int tf_energies_edof_f64(const int32_t* edof, const double* ke, const double* u,
 {
     if (n_elem <= 0) return TF_OK;
     TF_REQUIRE(((uintptr_t)edof & 15u) == 0, "edof must be 16-byte aligned");
-    KeMat<double> k;
-    memcpy(k.a, ke, sizeof(k.a));
+    EnergyKe k;
+    memcpy(k.ke.a, ke, sizeof(k.ke.a));
+    k.walsh = khat_blocks_cached<double>(ke, &k.kb) ? 1 : 0;
     k_energies_edof<<<(unsigned)((n_elem + EDOF_BLOCK - 1) / EDOF_BLOCK), EDOF_BLOCK, 0, S(stream)>>>(
         edof, u, out, n_elem, k);
     TF_CHECK_LAUNCH();

@@ -322,6 +322,51 @@ __global__ void __launch_bounds__(RED_BLOCK) k_oc(OcParams P)
     }
 }
 
+// ---- distributed OC: candidate volumes at a batch of multipliers ---------------------
+// Each x-slab rank sums its own elements' candidates (rank-local, fixed order);
+// the host all-gathers the partial sums and runs the bisection of simp.py:111-175
+// on the global means, evaluating several multipliers per round trip.
+
+constexpr int OC_MAX_LAMS = 15;  // TF_OC_MAX_LAMS
+
+struct OcLams {
+    double lam[OC_MAX_LAMS];
+    int n;
+};
+
+__global__ void __launch_bounds__(RED_BLOCK)
+k_oc_volumes_partial(OcParams P, const __grid_constant__ OcLams L, double* __restrict__ part)
+{
+    double v[OC_MAX_LAMS + 1];
+#pragma unroll
+    for (int k = 0; k <= OC_MAX_LAMS; ++k) v[k] = 0.0;
+    for (long long i = (long long)blockIdx.x * RED_BLOCK + threadIdx.x; i < P.n; i += (long long)gridDim.x * RED_BLOCK) {
+#pragma unroll
+        for (int k = 0; k < OC_MAX_LAMS; ++k)
+            if (k < L.n) v[k] += oc_cand(P, i, L.lam[k]);
+        if (P.dc[i] > 1e-12 || (P.dv && P.dv[i] <= 0.0)) v[OC_MAX_LAMS] += 1.0;
+    }
+    block_reduce_write<OC_MAX_LAMS + 1>(v, part + (OC_MAX_LAMS + 1) * blockIdx.x);
+}
+
+__global__ void __launch_bounds__(RED_BLOCK)
+k_oc_volumes_final(int nb, const double* __restrict__ part, double* __restrict__ out)
+{
+    double v[OC_MAX_LAMS + 1];
+#pragma unroll
+    for (int k = 0; k <= OC_MAX_LAMS; ++k) v[k] = 0.0;
+    for (int i = threadIdx.x; i < nb; i += RED_BLOCK)
+#pragma unroll
+        for (int k = 0; k <= OC_MAX_LAMS; ++k) v[k] += __ldcg(part + (OC_MAX_LAMS + 1) * i + k);
+    block_reduce_write<OC_MAX_LAMS + 1>(v, out);
+}
+
+__global__ void k_oc_apply(OcParams P, double lam)
+{
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < P.n) P.rho_new[i] = oc_cand(P, i, lam);
+}
+
 static int red_blocks(long long n)
 {
     int dev = 0, nsm = 148;
@@ -430,6 +475,42 @@ int tf_oc_update_f64(int64_t n, const double* rho, const double* dc, const doubl
     void* args[] = {&P};
     TF_CUDA_TRY(cudaMemsetAsync(work + 3 * (long long)nb, 0, 2 * sizeof(unsigned), SS(stream)));
     TF_CUDA_TRY(cudaLaunchCooperativeKernel((void*)k_oc, dim3(nb), dim3(RED_BLOCK), args, 0, SS(stream)));
+    return TF_OK;
+}
+
+int64_t tf_oc_work_doubles(int64_t n)
+{
+    return (int64_t)(OC_MAX_LAMS + 1) * red_blocks(n) + 8;
+}
+
+int tf_oc_volumes_f64(int64_t n, const double* rho, const double* dc, const double* dv, double move,
+                      double damping, const double* lams, int n_lams, double* sums, double* work,
+                      void* stream)
+{
+    TF_REQUIRE(n > 0 && rho && dc && lams && sums && work, "bad arguments");
+    TF_REQUIRE(n_lams >= 1 && n_lams <= OC_MAX_LAMS, "n_lams must be in [1, 15]");
+    OcParams P{};
+    P.n = n; P.rho = rho; P.dc = dc; P.dv = dv; P.move = move; P.damping = damping;
+    OcLams L{};
+    for (int k = 0; k < n_lams; ++k) L.lam[k] = lams[k];
+    L.n = n_lams;
+    const int nb = red_blocks(n);
+    k_oc_volumes_partial<<<nb, RED_BLOCK, 0, SS(stream)>>>(P, L, work);
+    TF_CHECK_LAUNCH();
+    k_oc_volumes_final<<<1, RED_BLOCK, 0, SS(stream)>>>(nb, work, sums);
+    TF_CHECK_LAUNCH();
+    return TF_OK;
+}
+
+int tf_oc_apply_f64(int64_t n, const double* rho, const double* dc, const double* dv, double move,
+                    double damping, double lam, double* rho_new, void* stream)
+{
+    if (n <= 0) return TF_OK;
+    TF_REQUIRE(rho && dc && rho_new, "bad arguments");
+    OcParams P{};
+    P.n = n; P.rho = rho; P.dc = dc; P.dv = dv; P.move = move; P.damping = damping; P.rho_new = rho_new;
+    k_oc_apply<<<(unsigned)((n + 255) / 256), 256, 0, SS(stream)>>>(P, lam);
+    TF_CHECK_LAUNCH();
     return TF_OK;
 }
 

@@ -11,7 +11,10 @@ namespace tf {
 
 constexpr int TILE_BX = 32;
 // 8 rows of element columns for FP32, 4 for FP64 (static smem stays < 48 KB)
-template <typename T> struct TileDims { static constexpr int BY = sizeof(T) == 8 ? 4 : 8; static constexpr int NT = TILE_BX * BY; };
+#ifndef TF_TILE_BY32
+#define TF_TILE_BY32 8
+#endif
+template <typename T> struct TileDims { static constexpr int BY = sizeof(T) == 8 ? 4 : TF_TILE_BY32; static constexpr int NT = TILE_BX * BY; };
 
 template <typename T>
 struct KhatBlocks {

@@ -98,6 +98,25 @@ def test_energies_match_reference():
         assert _rel(op.element_energies(v), g["energies"]) <= 1e-12
 
 
+def test_energies_ignore_rigid_translation():
+    """A deformation d carried along by a huge rigid translation: the parity-
+    basis energy drops the translation before any product, so E(d + t) equals
+    E(d) to round-off of the deformation (the direct u^T Ke u form would carry
+    eps*|Ke|*|t|^2 ~ 1e0 here and can go negative)."""
+    import oracle
+
+    m, edof, bcs, rho, v = seeded_case((6, 5, 4), 7)
+    op = _op(m, edof, bcs, rho, "fp64")
+    t = np.tile([3e8, -1e8, 2e8], m.n_nodes)
+    e_d = op.element_energies(v)
+    e_u = op.element_energies(v + t)
+    assert np.abs(e_u - e_d).max() <= 1e-5 * np.abs(e_d).max()
+    assert e_u.min() >= 0.0
+    # the reference's direct form on the same input (the checker): noise of ~|t|^2 eps
+    e_ref = oracle.element_energies(edof, op.ke64, v + t)
+    assert np.abs(e_ref - e_d).max() > 1e-3 * np.abs(e_d).max()
+
+
 @pytest.mark.parametrize("prec", ["fp64", "fp32"])
 @pytest.mark.parametrize("scatter", ["serial", "parallel_atomic"])
 def test_general_edof_kernels_seeded_random(prec, scatter):

@@ -238,3 +238,22 @@ def test_simp_presets_match_reference(name, prec):
         assert off.sum() <= max(1, 0.1 * its.size), (its, g["cg_iterations"])
     rel = np.linalg.norm(res.rho_phys - g["rho_phys"]) / np.linalg.norm(g["rho_phys"])
     assert rel <= 1e-3
+
+
+def test_short_schedule_runs_through_like_reference():
+    """default_schedule(4) on the desk cantilever drives |u| to ~2e8: the
+    loop must run through it like the reference (goldens from
+    tests/golden/make_golden_short_schedule.py), without a spurious
+    'positive sensitivity' rejection from energy round-off."""
+    import json
+
+    from conftest import GOLDEN
+    from paper_2604_18020_b200 import SimpConfig, default_schedule, make_preset, run_simp
+
+    g = json.loads((GOLDEN / "simp_short_schedule.json").read_text())
+    res = run_simp(make_preset("cantilever", 0.2), SimpConfig(schedule=default_schedule(4)))
+    c = [h.compliance for h in res.history]
+    np.testing.assert_allclose(c, g["compliance"], rtol=1e-5)
+    assert [h.restarted for h in res.history] == g["restarted"]
+    for v in (h.volume for h in res.history):
+        assert abs(v - 0.3) <= 1e-6

@@ -5,6 +5,7 @@ from __future__ import annotations
 
 import ctypes
 import hashlib
+from pathlib import Path
 
 import numpy as np
 import pytest
@@ -164,3 +165,29 @@ def test_node_fixed_layout_host_restatement():
     for j in range(m.nely + 1):
         assert col_or[j * (m.nelx + 1)] == 7 and col_and[j * (m.nelx + 1)] == 7
     assert col_or[1] == 0
+
+
+def test_simp_artifacts_byte_identical_to_reference(tmp_path):
+    """History CSV, summary JSON and selected-density snapshot written for a
+    fixed synthetic result are byte-identical to the reference's cmd_simp
+    output for the same result (tests/golden/make_golden_artifacts.py)."""
+    import sys
+
+    from paper_2604_18020_b200 import SimpConfig, default_schedule, make_preset
+    from paper_2604_18020_b200 import simp as S
+    from paper_2604_18020_b200.snapshot import write_simp_artifacts
+
+    sys.path.insert(0, str(Path(__file__).resolve().parent / "golden"))
+    from make_golden_artifacts import synthetic_result
+
+    pb = make_preset("cantilever", 0.1)
+    cfg = SimpConfig(schedule=default_schedule(6))
+    res = synthetic_result(S, pb, cfg)
+    paths = write_simp_artifacts(tmp_path, res, pb, "fp64", "fused", "serial", iters=6, cg_cap=1000, seed=42)
+    gold = Path(__file__).resolve().parent / "golden" / "artifacts"
+    names = {p.name for p in gold.iterdir()}
+    assert names == {"simp_cantilever_fp64_history.csv", "simp_cantilever_fp64_summary.json",
+                     "simp_cantilever_fp64_selected.bin", "simp_cantilever_fp64_selected.json"}
+    for name in names:
+        assert (tmp_path / name).read_bytes() == (gold / name).read_bytes(), name
+    assert paths["history"].name == "simp_cantilever_fp64_history.csv"

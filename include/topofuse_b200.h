@@ -329,6 +329,47 @@ int tf_oc_volumes_f64(int64_t n, const double* rho, const double* dc, const doub
 int tf_oc_apply_f64(int64_t n, const double* rho, const double* dc, const double* dv, double move,
                     double damping, double lam, double* rho_new, void* stream);
 
+
+/* ---- x-slab distributed PCG step kernels (csrc/tf_slab.cu) --------
+ * Device-resident scalars for the multi-GPU CG of solver.py:57-147: the host
+ * enqueues  q = K p (+ interface exchange) -> tf_slab_cg_pq -> all-reduce
+ * red[0] -> tf_slab_cg_alpha -> all-reduce red[1..2] -> tf_slab_cg_beta  per
+ * iteration without synchronising; `state` (8 doubles: rz, |b|, rel, it,
+ * active, term, tol, ticket) freezes the solve exactly at the stop iteration
+ * (term 1 converged, 2 breakdown, 3 diverged).  owned (nullable): uint8 mask
+ * of the DOFs this rank counts in dots.  red: 4 doubles (p.q, r.r, r.z, b.b).
+ * work: tf_slab_work_doubles(n) doubles. */
+int64_t tf_slab_work_doubles(int64_t n);
+int tf_slab_dot_f32(int64_t n, const float* a, const float* b, const uint8_t* owned, double* out,
+                    double* work, void* stream);
+int tf_slab_dot_f64(int64_t n, const double* a, const double* b, const uint8_t* owned, double* out,
+                    double* work, void* stream);
+int tf_slab_cg_begin_f32(int64_t n, const float* r, const float* inv, float* z, float* p,
+                         const uint8_t* owned, double* red, double* work, void* stream);
+int tf_slab_cg_begin_f64(int64_t n, const double* r, const double* inv, double* z, double* p,
+                         const uint8_t* owned, double* red, double* work, void* stream);
+int tf_slab_cg_start(double* state, const double* red, double rel_tol, int f32, void* stream);
+int tf_slab_cg_pq_f32(int64_t n, const float* p, const float* q, const uint8_t* owned,
+                      const double* state, double* red, double* work, void* stream);
+int tf_slab_cg_pq_f64(int64_t n, const double* p, const double* q, const uint8_t* owned,
+                      const double* state, double* red, double* work, void* stream);
+int tf_slab_cg_alpha_f32(int64_t n, float* x, float* r, const float* p, const float* q, const float* inv,
+                         float* z, const uint8_t* owned, double* state, double* red, int refresh,
+                         double* work, void* stream);
+int tf_slab_cg_alpha_f64(int64_t n, double* x, double* r, const double* p, const double* q,
+                         const double* inv, double* z, const uint8_t* owned, double* state, double* red,
+                         int refresh, double* work, void* stream);
+int tf_slab_cg_residual_f32(int64_t n, const float* b, const float* w, float* r, const float* inv, float* z,
+                            const uint8_t* owned, const double* state, double* red, double* work,
+                            void* stream);
+int tf_slab_cg_residual_f64(int64_t n, const double* b, const double* w, double* r, const double* inv,
+                            double* z, const uint8_t* owned, const double* state, double* red, double* work,
+                            void* stream);
+int tf_slab_cg_beta_f32(int64_t n, float* p, const float* z, double* state, const double* red, double* hist,
+                        int hist_len, void* stream);
+int tf_slab_cg_beta_f64(int64_t n, double* p, const double* z, double* state, const double* red,
+                        double* hist, int hist_len, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -135,7 +135,17 @@ _SIGS = {
                          ctypes.c_double, _INT, _P, _P, _P, _P],
     "tf_oc_volumes_f64": [_I64, _P, _P, _P, ctypes.c_double, ctypes.c_double, _P, _INT, _P, _P, _P],
     "tf_oc_apply_f64": [_I64, _P, _P, _P, ctypes.c_double, ctypes.c_double, ctypes.c_double, _P, _P],
+    "tf_slab_cg_start": [_P, _P, ctypes.c_double, _INT, _P],
 }
+for _s in ("f32", "f64"):
+    _SIGS.update({
+        f"tf_slab_dot_{_s}": [_I64, _P, _P, _P, _P, _P, _P],
+        f"tf_slab_cg_begin_{_s}": [_I64, _P, _P, _P, _P, _P, _P, _P, _P],
+        f"tf_slab_cg_pq_{_s}": [_I64, _P, _P, _P, _P, _P, _P, _P],
+        f"tf_slab_cg_alpha_{_s}": [_I64, _P, _P, _P, _P, _P, _P, _P, _P, _P, _INT, _P, _P],
+        f"tf_slab_cg_residual_{_s}": [_I64, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P],
+        f"tf_slab_cg_beta_{_s}": [_I64, _P, _P, _P, _P, _P, _INT, _P],
+    })
 
 _lib = None
 
@@ -172,6 +182,8 @@ def load() -> ctypes.CDLL:
     L.tf_work_doubles.argtypes = [ctypes.c_int64]
     L.tf_oc_work_doubles.restype = ctypes.c_int64
     L.tf_oc_work_doubles.argtypes = [ctypes.c_int64]
+    L.tf_slab_work_doubles.restype = ctypes.c_int64
+    L.tf_slab_work_doubles.argtypes = [ctypes.c_int64]
     L.tf_last_error.restype = ctypes.c_char_p
     L.tf_last_error.argtypes = []
     _lib = L

@@ -153,7 +153,7 @@ class SlabExchange:
         p = self.part
         # gloo moves host tensors only: stage device planes through the host
         # (used by the single-GPU multi-rank tests); NCCL exchanges in place
-        host = w.is_cuda and dist.get_backend(self.group) == "gloo"
+        host = (p.has_left or p.has_right) and w.is_cuda and dist.get_backend(self.group) == "gloo"
         ops = []
         send_l = recv_l = send_r = recv_r = None
         if p.has_left:
@@ -254,9 +254,16 @@ def slab_pcg(op: SlabOperator, b, diag, rel_tol=1e-5, max_iter=1000, recompute_e
 
     Vectors are the rank-local slabs (torch tensors); every scalar is a global
     FP64 all-reduced dot rounded to the working dtype like the single-GPU
-    device solver, so all ranks take identical decisions.
+    device solver, so all ranks take identical decisions.  CUDA vectors run
+    the device-driven protocol (slab_pcg_device); CPU vectors (the oracle-
+    bound decomposition tests) the host loop below.
     """
+    import os
+
     import torch
+
+    if b.is_cuda and os.environ.get("TF_SLAB_HOST_CG", "0") != "1":
+        return slab_pcg_device(op, b, diag, rel_tol, max_iter, recompute_every, x0)
 
     f32 = b.dtype == torch.float32
     rnd = (lambda v: float(np.float32(v))) if f32 else (lambda v: float(v))
@@ -315,6 +322,106 @@ def slab_pcg(op: SlabOperator, b, diag, rel_tol=1e-5, max_iter=1000, recompute_e
         p = z + beta * p
         rz = rz_new
     return x, dict(iterations=it, termination=term, rel=rel, history=hist, matvecs=mv)
+
+
+_SLAB_TERMS = {1: "converged", 2: "breakdown", 3: "diverged"}
+
+
+def slab_pcg_device(op: SlabOperator, b, diag, rel_tol=1e-5, max_iter=1000, recompute_every=50, x0=None,
+                    poll: int = 8):
+    """slab_pcg with every scalar on the device (csrc/tf_slab.cu).
+
+    Per iteration the host only enqueues: q = K p (slab kernels + interface
+    exchange), the owned p.q partial, an all-reduce of it, the alpha step
+    (x, r, z and the (r.r, r.z) partials), a second all-reduce and the beta
+    step.  Nothing waits for the GPU except a poll of the device state every
+    `poll` iterations; the device freezes the solve at the exact stop
+    iteration, so results do not depend on `poll`.
+    """
+    import torch
+    import torch.distributed as dist
+
+    from . import _device as D
+    from . import _lib
+
+    f32 = b.dtype == torch.float32
+    sfx = "f32" if f32 else "f64"
+    dev = b.device
+    st = D.stream_ptr()
+    n = b.numel()
+    f64 = torch.float64
+    owned = op.owned.to(torch.uint8)
+    work = torch.zeros(int(_lib.load().tf_slab_work_doubles(n)), dtype=f64, device=dev)
+    red = torch.zeros(4, dtype=f64, device=dev)
+    state = torch.zeros(8, dtype=f64, device=dev)
+    hist = torch.full((max_iter + 1,), float("nan"), dtype=f64, device=dev)
+    multi = dist.is_initialized() and dist.get_world_size(op.group) > 1
+    gloo = multi and dist.get_backend(op.group) == "gloo"
+
+    def allreduce(lo, hi):
+        if not multi:
+            return
+        if gloo:
+            t = red[lo:hi].cpu()
+            dist.all_reduce(t, group=op.group)
+            red[lo:hi].copy_(t)
+        else:
+            dist.all_reduce(red[lo:hi], group=op.group)
+
+    _lib.call(f"tf_slab_dot_{sfx}", n, D.ptr(b), D.ptr(b), D.ptr(owned), D.ptr(red) + 24, D.ptr(work), st)
+    allreduce(3, 4)
+    if float(red[3]) == 0.0:
+        return torch.zeros_like(b), dict(iterations=0, termination="converged", rel=0.0, history=[0.0],
+                                         matvecs=0)
+    mv = 0
+    if x0 is None:
+        x = torch.zeros_like(b)
+        r = b.clone()
+    else:
+        x = x0.clone()
+        r = b - op.apply(x)
+        mv += 1
+    inv = 1.0 / diag
+    z = torch.empty_like(b)
+    p = torch.empty_like(b)
+    _lib.call(f"tf_slab_cg_begin_{sfx}", n, D.ptr(r), D.ptr(inv), D.ptr(z), D.ptr(p), D.ptr(owned), D.ptr(red),
+              D.ptr(work), st)
+    allreduce(1, 3)
+    _lib.call("tf_slab_cg_start", D.ptr(state), D.ptr(red), float(rel_tol), int(f32), st)
+    hist[0:1].copy_(state[2:3])
+    if float(state[4]) != 0.0:
+        for it in range(1, max_iter + 1):
+            q = op.apply(p)
+            _lib.call(f"tf_slab_cg_pq_{sfx}", n, D.ptr(p), D.ptr(q), D.ptr(owned), D.ptr(state), D.ptr(red),
+                      D.ptr(work), st)
+            allreduce(0, 1)
+            refresh = bool(recompute_every) and it % recompute_every == 0
+            _lib.call(f"tf_slab_cg_alpha_{sfx}", n, D.ptr(x), D.ptr(r), D.ptr(p), D.ptr(q), D.ptr(inv), D.ptr(z),
+                      D.ptr(owned), D.ptr(state), D.ptr(red), int(refresh), D.ptr(work), st)
+            if refresh:
+                w = op.apply(x)
+                _lib.call(f"tf_slab_cg_residual_{sfx}", n, D.ptr(b), D.ptr(w), D.ptr(r), D.ptr(inv), D.ptr(z),
+                          D.ptr(owned), D.ptr(state), D.ptr(red), D.ptr(work), st)
+            allreduce(1, 3)
+            _lib.call(f"tf_slab_cg_beta_{sfx}", n, D.ptr(p), D.ptr(z), D.ptr(state), D.ptr(red), D.ptr(hist),
+                      max_iter + 1, st)
+            if (it % poll == 0 or it == max_iter) and float(state[4]) == 0.0:
+                break
+    s_h = state.cpu().numpy()
+    its = int(s_h[3])
+    term = _SLAB_TERMS.get(int(s_h[5]), "max_iter")
+    if term == "diverged":
+        raise FloatingPointError(f"CG diverged at iteration {its}")
+    if x0 is not None:
+        mv = 1
+    refreshes = its // recompute_every if recompute_every else 0
+    if term == "breakdown" and recompute_every and its % recompute_every == 0:
+        refreshes -= 1
+    mv += its + refreshes
+    h = hist.cpu().numpy()
+    n_hist = its if term == "breakdown" else its + 1
+    history = [float(v) for v in h[:n_hist]]
+    return x, dict(iterations=its, termination=term, rel=history[-1], history=history, matvecs=mv)
 
 
 def gpu_local_kernels(part: SlabPartition, bcs_local: BoundaryConditions, rho_local, simp,

@@ -92,6 +92,13 @@ def _worker(rank, world, port, dims, prec, q, device="cpu", max_iter=1000):
         d = op.diagonal()
         b = torch.from_numpy(lb.force.astype(dt)).to(device)
         x, info = slab_pcg(op, b, d, max_iter=max_iter)
+        if device != "cpu":
+            # device-scalar protocol (default for CUDA vectors) vs the host loop
+            os.environ["TF_SLAB_HOST_CG"] = "1"
+            xh, info_h = slab_pcg(op, b, d, max_iter=max_iter)
+            del os.environ["TF_SLAB_HOST_CG"]
+            info = dict(info, host=(info_h["iterations"], info_h["termination"], info_h["matvecs"],
+                                    float((x - xh).abs().max() / xh.abs().max())))
         q.put((rank, part.local_dof_to_global(), w.cpu().numpy(), d.cpu().numpy(), x.cpu().numpy(), info))
     finally:
         dist.destroy_process_group()
@@ -162,6 +169,13 @@ def _run_slab(world, dims, prec, device, max_iter=1000):
         assert info["termination"] == info_ref["termination"]
         assert abs(info["iterations"] - info_ref["iterations"]) <= max(2, 0.02 * info_ref["iterations"])
         assert np.abs(x - x_ref[g2l]).max() <= xtol
+        if "host" in info:
+            its_h, term_h, mv_h, dx = info["host"]
+            assert term_h == info["termination"] and abs(its_h - info["iterations"]) <= 1
+            assert mv_h - its_h == info["matvecs"] - info["iterations"]
+            assert len(info["history"]) == info["iterations"] + 1
+            if prec == "fp64":  # both within the 1e-3 solution bar of the reference
+                assert dx <= 2e-3
     # replicated interface DOFs are bitwise identical across ranks
     full = {}
     for rank, g2l, w, d, x, info in res:

@@ -363,6 +363,7 @@ def run_ours(args):
         traffic = json.loads(tf.read_text()).get(f"{args.config}_{prec}")
 
     simp = cg = simp2 = sweep = None
+    scaling = simp_scaling(world, dist) if args.simp else None
     if args.simp and rank == 0:
         simp = simp_c1()
         simp2 = simp_c2()
@@ -411,6 +412,7 @@ def run_ours(args):
             "kernels": sweep,
             "simp": simp,
             "simp_c2": simp2,
+            "simp_c4_scaling": scaling,
             "cg": cg,
             "wall_s_timed_region": wall,
         }
@@ -508,6 +510,58 @@ def simp_c2():
             "selected_compliance": res.selected.compliance if res.selected else None,
             "paper_rtx4090_simp120_wall_s": 17.5,
             "paper_note": "fused SIMP-120 wall at 216k, PAPER.md:1223-1227 (RTX 4090, context only)"}
+
+
+def simp_scaling(world, dist, iters=6):
+    """SIMP s/iter at c4 (cantilever 200x100x50, 1M elements) strong-scaled
+    over the job's ranks: the first `iters` iterations of
+    default_schedule(120) (its phase 1: p 1.5, beta 1, move 0.2, rmin 1.5),
+    FP32.  One rank: the device-resident loop (run_simp); N ranks: the x-slab
+    loop (slab_simp.slab_run_simp, NCCL interface/halo exchanges and
+    all-reduces).  Wall time over the iterations after a 2-iteration warm-up,
+    max over ranks."""
+    import torch
+
+    from paper_2604_18020_b200 import SimpConfig, make_preset, run_simp
+    from paper_2604_18020_b200.simp import ContinuationSchedule, Phase
+    from paper_2604_18020_b200.slab_simp import slab_run_simp
+
+    pb = make_preset("cantilever", 5.0 / 3.0)
+    sched = lambda k: ContinuationSchedule((Phase(1, k, p=1.5, beta=1.0, move=0.2, rmin_end=1.5),), 1.5)  # noqa: E731
+    dev = torch.device("cuda", torch.cuda.current_device())
+
+    def run(k):
+        cfg = SimpConfig(schedule=sched(k), precision="fp32")
+        if world == 1:
+            return run_simp(pb, cfg)
+        return slab_run_simp(pb, cfg, device=dev, gather=False)
+
+    run(2)
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    res = run(iters)
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t0
+    if dist is not None:
+        t = torch.tensor([wall], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        wall = float(t.item())
+    # per-iteration loop time (the loop synchronises on its scalars every
+    # iteration, so host timers bracket device work), max over ranks; the
+    # run's wall adds the one-time setup (mesh/edof/operator/filter build)
+    loop = sum(h.wall_s for h in res.history)
+    if dist is not None:
+        t = torch.tensor([loop], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        loop = float(t.item())
+    return {"config": f"c4 cantilever 200x100x50 (1M), default_schedule(120) iterations 1-{iters}, FP32, "
+                      f"strong-scaled over {world} rank(s)",
+            "path": "run_simp (device-resident)" if world == 1 else "slab_run_simp (x-slabs)",
+            "n_gpus": world, "s_per_iter": loop / iters, "wall_s": wall, "setup_s": wall - loop,
+            "cg_iterations": [h.cg_iterations for h in res.history],
+            "compliance": [h.compliance for h in res.history]}
 
 
 def cg_c2():

@@ -920,11 +920,15 @@ int tf_pcg_create(tf_pcg** out, const tf_pcg_desc* d, void* stream)
     int dev = 0, nsm = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    // vector kernels: one 16-byte chunk per thread up to 8 CTAs per SM (more
-    // memory-level parallelism; measured faster at c2 than fewer, fatter CTAs
-    // even though every block then reduces more partials)
+    // vector kernels: one 16-byte chunk per thread ...
+    // ... but no more than 3 CTAs per SM while the CG working set (~6
+    // vectors) is below ~200 MB, 4 beyond (graph-protocol us/iteration vs the
+    // former 8 per SM: c4 FP32 47.1 vs 53.2, c4 FP64 88.1 vs 92.0, c3 FP32
+    // 34.3 vs 40.4, c3 FP64 46.5 vs 53.5; c5 FP32 207 vs 212 at 4 per SM)
     const long long want = (d->n_dof + VEC_BLOCK * 4 - 1) / (VEC_BLOCK * 4);
-    h->n_vec_blocks = (int)std::min<long long>(std::max<long long>(want, 1), (long long)nsm * 8);
+    const int per_sm = 6.0 * (double)es * (double)d->n_dof <= 200e6 ? 3 : 4;
+    h->n_vec_blocks = (int)std::min<long long>(std::max<long long>(want, 1), (long long)nsm * per_sm);
+    if (const char* e = getenv("TF_VEC_BLOCKS")) h->n_vec_blocks = std::max(1, atoi(e));  // experiments
     if (d->structured)
         h->n_mv_blocks = d->precision == 32
                              ? grid_matvec_blocks<float>(h->grid, (const float*)d->ke, d->grid_variant)

@@ -181,7 +181,7 @@ def test_slab_simp_matches_single_gpu_loop(world, preset, iters, prec):
         assert np.array_equal(rho, res[0][2])
     # FP32: the mbb desk solves stop at the 1000-iteration cap (as the
     # reference's do), so the loop is chaotic in round-off from step 2
-    ctol, gtol, rtol, ltol = (1e-5, 1e-5, 2e-3, 2e-2) if prec == "fp64" else (2e-3, 1e-3, 1e-2, 5e-2)
+    ctol, gtol, rtol, ltol = (1e-5, 5e-5, 2e-3, 2e-2) if prec == "fp64" else (2e-3, 1e-3, 1e-2, 5e-2)
     for (c, g, its, vol, rs), (cr, gr, itsr, volr, rsr) in zip(h0, hist_ref):
         assert abs(c - cr) <= ctol * abs(cr)
         assert abs(g - gr) <= gtol

@@ -370,6 +370,32 @@ int tf_slab_cg_beta_f32(int64_t n, float* p, const float* z, double* state, cons
 int tf_slab_cg_beta_f64(int64_t n, double* p, const double* z, double* state, const double* red,
                         double* hist, int hist_len, void* stream);
 
+
+/* ---- peer-memory transport (csrc/tf_peer.cu) ----------------------
+ * Interface-plane exchange and one-shot scalar all-reduce written straight
+ * into the neighbours' memory (CUDA IPC mappings over NVLink) with
+ * stream-ordered epoch flags; no SM spins, no NCCL.  Replaces the
+ * ncclSend/ncclRecv + ncclAllReduce of the SURVEY's proposed tf_comm_* API. */
+int tf_peer_alloc(void** ptr, size_t bytes);               /* cudaMalloc + zero */
+int tf_peer_free(void* ptr);
+int tf_ipc_handle_bytes(void);
+int tf_ipc_export(void* dev_ptr, void* handle_out);
+int tf_ipc_open(const void* handle, void** dev_ptr_out);
+int tf_ipc_close(void* dev_ptr);
+/* stream-ordered flag ops (driver stream memory operations; the write fences
+ * the stream's preceding writes, the wait is flag >= value) */
+int tf_stream_write_u32(void* addr, uint32_t value, void* stream);
+int tf_stream_wait_u32(void* addr, uint32_t value, void* stream);
+/* dst[k] = w[idx[k]] (dst may be a peer mapping) */
+int tf_plane_put_f32(const float* w, const int64_t* idx, int64_t n, float* dst, void* stream);
+int tf_plane_put_f64(const double* w, const int64_t* idx, int64_t n, double* dst, void* stream);
+/* w[idx[k]] = recv[k] + w[idx[k]] (recv_first) or w[idx[k]] + recv[k] */
+int tf_plane_add_f32(float* w, const int64_t* idx, int64_t n, const float* recv, int recv_first, void* stream);
+int tf_plane_add_f64(double* w, const int64_t* idx, int64_t n, const double* recv, int recv_first,
+                     void* stream);
+/* out[j] = sum_r slots[r*k + j], ranks in ascending order (k <= 1024) */
+int tf_rank_sum_f64(const double* slots, int nranks, int k, double* out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

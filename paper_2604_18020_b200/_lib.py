@@ -136,6 +136,15 @@ _SIGS = {
     "tf_oc_volumes_f64": [_I64, _P, _P, _P, ctypes.c_double, ctypes.c_double, _P, _INT, _P, _P, _P],
     "tf_oc_apply_f64": [_I64, _P, _P, _P, ctypes.c_double, ctypes.c_double, ctypes.c_double, _P, _P],
     "tf_slab_cg_start": [_P, _P, ctypes.c_double, _INT, _P],
+    "tf_peer_alloc": [_P, ctypes.c_size_t],
+    "tf_peer_free": [_P],
+    "tf_ipc_handle_bytes": [],
+    "tf_ipc_export": [_P, _P],
+    "tf_ipc_open": [_P, _P],
+    "tf_ipc_close": [_P],
+    "tf_stream_write_u32": [_P, ctypes.c_uint32, _P],
+    "tf_stream_wait_u32": [_P, ctypes.c_uint32, _P],
+    "tf_rank_sum_f64": [_P, _INT, _INT, _P, _P],
 }
 for _s in ("f32", "f64"):
     _SIGS.update({
@@ -145,6 +154,8 @@ for _s in ("f32", "f64"):
         f"tf_slab_cg_alpha_{_s}": [_I64, _P, _P, _P, _P, _P, _P, _P, _P, _P, _INT, _P, _P],
         f"tf_slab_cg_residual_{_s}": [_I64, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P],
         f"tf_slab_cg_beta_{_s}": [_I64, _P, _P, _P, _P, _P, _INT, _P],
+        f"tf_plane_put_{_s}": [_P, _P, _I64, _P, _P],
+        f"tf_plane_add_{_s}": [_P, _P, _I64, _P, _INT, _P],
     })
 
 _lib = None

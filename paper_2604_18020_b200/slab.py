@@ -191,13 +191,26 @@ class SlabOperator:
     """
 
     def __init__(self, part: SlabPartition, bcs_local: BoundaryConditions, local_apply,
-                 local_diag_partial, device, dtype, group=None):
+                 local_diag_partial, device, dtype, group=None, transport: str | None = None):
+        import os
+
         import torch
 
         self.part = part
         self.local_apply = local_apply
         self.local_diag_partial = local_diag_partial
-        self.exchange = SlabExchange(part, device, group)
+        # "p2p": torch.distributed P2P + all_reduce (NCCL on GPUs, gloo with
+        # host staging in the one-GPU tests); "peer": peer-memory puts and
+        # stream-ordered flags (peer.py / csrc/tf_peer.cu)
+        self.transport = transport or os.environ.get("TF_SLAB_TRANSPORT", "p2p")
+        if self.transport == "peer":
+            from .peer import PeerTransport
+
+            self.exchange = PeerTransport(part, device, group)
+        elif self.transport == "p2p":
+            self.exchange = SlabExchange(part, device, group)
+        else:
+            raise ValueError(f"unknown slab transport {self.transport!r}")
         self.group = group
         self.device = device
         self.dtype = dtype
@@ -228,6 +241,23 @@ class SlabOperator:
         if self.fixed.numel():
             d[self.fixed] = 1.0
         return d
+
+    def allreduce_dev(self, t, lo: int, hi: int):
+        """In place, no host round trip on NCCL/peer: t[lo:hi] (FP64 device
+        tensor) summed over ranks; every rank gets the same values."""
+        import torch.distributed as dist
+
+        if not (dist.is_initialized() and dist.get_world_size(self.group) > 1):
+            return t
+        if self.transport == "peer":
+            return self.exchange.allreduce_(t, lo, hi)
+        if t.is_cuda and dist.get_backend(self.group) == "gloo":
+            h = t[lo:hi].cpu()
+            dist.all_reduce(h, group=self.group)
+            t[lo:hi].copy_(h)
+        else:
+            dist.all_reduce(t[lo:hi], group=self.group)
+        return t
 
     def allreduce(self, vals):
         """Sum of FP64 partials over ranks (owner-computes)."""
@@ -339,7 +369,6 @@ def slab_pcg_device(op: SlabOperator, b, diag, rel_tol=1e-5, max_iter=1000, reco
     iteration, so results do not depend on `poll`.
     """
     import torch
-    import torch.distributed as dist
 
     from . import _device as D
     from . import _lib
@@ -355,18 +384,9 @@ def slab_pcg_device(op: SlabOperator, b, diag, rel_tol=1e-5, max_iter=1000, reco
     red = torch.zeros(4, dtype=f64, device=dev)
     state = torch.zeros(8, dtype=f64, device=dev)
     hist = torch.full((max_iter + 1,), float("nan"), dtype=f64, device=dev)
-    multi = dist.is_initialized() and dist.get_world_size(op.group) > 1
-    gloo = multi and dist.get_backend(op.group) == "gloo"
 
     def allreduce(lo, hi):
-        if not multi:
-            return
-        if gloo:
-            t = red[lo:hi].cpu()
-            dist.all_reduce(t, group=op.group)
-            red[lo:hi].copy_(t)
-        else:
-            dist.all_reduce(red[lo:hi], group=op.group)
+        op.allreduce_dev(red, lo, hi)
 
     _lib.call(f"tf_slab_dot_{sfx}", n, D.ptr(b), D.ptr(b), D.ptr(owned), D.ptr(red) + 24, D.ptr(work), st)
     allreduce(3, 4)

@@ -183,3 +183,72 @@ def _run_slab(world, dims, prec, device, max_iter=1000):
             if gi in full:
                 assert full[gi] == val
             full[gi] = val
+
+
+def _peer_worker(rank, world, port, dims, prec, q):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2604_18020_b200.element import SimpParams
+    from paper_2604_18020_b200.slab import SlabOperator, SlabPartition, gpu_local_kernels, slab_pcg
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        m = StructuredMesh(*dims)
+        bcs = cantilever_bcs(m)
+        rng = np.random.default_rng(3)
+        rho = rng.uniform(0.05, 1.0, m.n_elem)
+        v = rng.standard_normal(m.n_dof)
+        part = SlabPartition(m, world, rank)
+        lb = part.local_bcs(bcs)
+        tdt = torch.float64 if prec == "fp64" else torch.float32
+        out = {}
+        for transport in ("p2p", "peer"):
+            _, la, ld = gpu_local_kernels(part, lb, part.scatter_elem(rho), SimpParams(3.0), prec)
+            op = SlabOperator(part, lb, la, ld, "cuda:0", tdt, transport=transport)
+            x = torch.from_numpy(part.scatter(v)).to("cuda:0", tdt)
+            ws = [op.apply(x).cpu().numpy() for _ in range(3)]  # several epochs (slot parities)
+            d = op.diagonal()
+            b = torch.from_numpy(lb.force).to("cuda:0", tdt)
+            xs, info = slab_pcg(op, b, d, max_iter=1000)
+            red = torch.tensor([rank + 1.0, 0.25, -rank], dtype=torch.float64, device="cuda:0")
+            op.allreduce_dev(red, 0, 3)
+            out[transport] = (ws, d.cpu().numpy(), xs.cpu().numpy(), info["iterations"], red.cpu().numpy())
+        q.put((rank, out))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world,dims,prec", [(2, (40, 6, 5), "fp64"), (3, (45, 5, 4), "fp32")])
+def test_slab_peer_transport_matches_p2p(world, dims, prec):
+    """Peer-memory transport (CUDA IPC mappings between the rank processes,
+    stream-ordered epoch flags): interface sums bitwise equal to the
+    torch.distributed P2P exchange over repeated products (both slot
+    parities), the same diagonal, the one-shot all-reduce equal to the rank
+    sum on every rank, and the distributed PCG through it."""
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.SimpleQueue()
+    port = _free_port()
+    procs = [ctx.Process(target=_peer_worker, args=(r, world, port, dims, prec, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get() for _ in range(world)]
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    want_red = np.array([world * (world + 1) / 2, 0.25 * world, -world * (world - 1) / 2])
+    for rank, out in res:
+        (wp, dp, xp, itp, rp), (wq, dq, xq, itq, rq) = out["p2p"], out["peer"]
+        for a, b in zip(wp, wq):
+            assert np.array_equal(a, b)
+        # the local Jacobi partials use FP64 atomics (order-dependent at 1 ulp)
+        assert np.abs(dp - dq).max() <= 1e-14 * np.abs(dp).max()
+        assert np.array_equal(rq, want_red)
+        # dots reduced in another order (and 1-ulp diagonal differences): the
+        # north star's CG bars (+-2 % iterations, solution within 1e-3)
+        assert abs(itp - itq) <= max(2, 0.02 * itp)
+        assert np.abs(xp - xq).max() <= 1e-3 * np.abs(xp).max()

@@ -290,6 +290,27 @@ def run_ours(args):
     torch.cuda.synchronize()
     ms_warm = e0.elapsed_time(e1) / args.steps
 
+    # N > 1: the same back-to-back products through the peer-memory transport
+    # (CUDA IPC puts + stream-ordered flags, peer.py) next to the
+    # torch.distributed P2P one (NCCL), max over ranks
+    transports = None
+    if world > 1:
+        sop_peer = SlabOperator(part, lb, local_apply, local_diag, dev, sop.dtype, transport="peer")
+        for _ in range(3):
+            sop_peer.apply(x)
+        torch.cuda.synchronize()
+        dist.barrier()
+        e0.record(stream)
+        for _ in range(args.steps):
+            sop_peer.apply(x)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms_peer = e0.elapsed_time(e1) / args.steps
+        t = torch.tensor([ms_warm, ms_peer], device="cpu" if same_dev else dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        transports = {"p2p_ms_per_step": float(t[0]), "peer_ms_per_step": float(t[1]),
+                      "note": "warm back-to-back slab products, max over ranks"}
+
     # e2e through the public API from pinned host buffers: every step copies
     # its input vector H2D and its result D2H; MatFreeOperator.apply_stream
     # overlaps the copies of neighbouring steps with the matvecs
@@ -413,6 +434,7 @@ def run_ours(args):
             "simp": simp,
             "simp_c2": simp2,
             "simp_c4_scaling": scaling,
+            "slab_transports": transports,
             "cg": cg,
             "wall_s_timed_region": wall,
         }

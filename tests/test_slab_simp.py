@@ -152,7 +152,7 @@ def test_slab_simp_matches_single_gpu_loop(world, preset, iters, prec):
     itself gives 164 vs 187 iterations at step 4 under its two CG protocols
     (resident vs graph), which differ in reduction order alone
     (scripts/slab_simp_probe.py).  So per-step counts are checked in total
-    (15%), compliances per step (1e-5 FP64), volumes against the OC
+    (15%), compliances per step (1e-4 FP64), volumes against the OC
     tolerance, densities in mean and L2."""
     import torch.multiprocessing as mp
 
@@ -181,7 +181,9 @@ def test_slab_simp_matches_single_gpu_loop(world, preset, iters, prec):
         assert np.array_equal(rho, res[0][2])
     # FP32: the mbb desk solves stop at the 1000-iteration cap (as the
     # reference's do), so the loop is chaotic in round-off from step 2
-    ctol, gtol, rtol, ltol = (1e-5, 5e-5, 2e-3, 2e-2) if prec == "fp64" else (2e-3, 1e-3, 1e-2, 5e-2)
+    # compliance per step: 1e-4 (north star 1e-3); the single-GPU loop's two
+    # CG protocols differ by up to 1.8e-5 at step 14 of the cantilever run
+    ctol, gtol, rtol, ltol = (1e-4, 5e-5, 2e-3, 2e-2) if prec == "fp64" else (2e-3, 1e-3, 1e-2, 5e-2)
     for (c, g, its, vol, rs), (cr, gr, itsr, volr, rsr) in zip(h0, hist_ref):
         assert abs(c - cr) <= ctol * abs(cr)
         assert abs(g - gr) <= gtol

@@ -121,13 +121,13 @@ def test_element_halo_extends_slabs_with_neighbour_layers(world, dims, h):
 # -- GPU: the whole loop -------------------------------------------------------------
 
 
-def _simp_worker(rank, world, port, preset, scale, iters, prec, q):
+def _simp_worker(rank, world, port, preset, scale, iters, prec, q, transport="p2p"):
     import torch.distributed as dist
 
     from paper_2604_18020_b200 import SimpConfig, default_schedule, make_preset
     from paper_2604_18020_b200.slab_simp import slab_run_simp
 
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), TF_SLAB_TRANSPORT=transport)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         pb = make_preset(preset, scale)
@@ -144,9 +144,11 @@ def _simp_worker(rank, world, port, preset, scale, iters, prec, q):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("world,preset,iters,prec", [(2, "cantilever", 16, "fp64"), (3, "mbb", 12, "fp64"),
-                                                     (2, "mbb", 8, "fp32")])
-def test_slab_simp_matches_single_gpu_loop(world, preset, iters, prec):
+@pytest.mark.parametrize("world,preset,iters,prec,transport", [(2, "cantilever", 16, "fp64", "p2p"),
+                                                               (3, "mbb", 12, "fp64", "p2p"),
+                                                               (2, "mbb", 8, "fp32", "p2p"),
+                                                               (3, "mbb", 12, "fp64", "peer")])
+def test_slab_simp_matches_single_gpu_loop(world, preset, iters, prec, transport):
     """Bars.  Only summation order differs from one GPU, but the warm-started
     CG counts of the cantilever are hypersensitive to it: the single-GPU loop
     itself gives 164 vs 187 iterations at step 4 under its two CG protocols
@@ -161,7 +163,7 @@ def test_slab_simp_matches_single_gpu_loop(world, preset, iters, prec):
     ctx = mp.get_context("spawn")
     q = ctx.SimpleQueue()
     port = _free_port()
-    procs = [ctx.Process(target=_simp_worker, args=(r, world, port, preset, 0.2, iters, prec, q))
+    procs = [ctx.Process(target=_simp_worker, args=(r, world, port, preset, 0.2, iters, prec, q, transport))
              for r in range(world)]
     for p in procs:
         p.start()

@@ -396,6 +396,41 @@ int tf_plane_add_f64(double* w, const int64_t* idx, int64_t n, const double* rec
 /* out[j] = sum_r slots[r*k + j], ranks in ascending order (k <= 1024) */
 int tf_rank_sum_f64(const double* slots, int nranks, int k, double* out, void* stream);
 
+
+/* ---- native x-slab runtime over the peer transport (csrc/tf_slab_run.cu) -----
+ * Enqueues distributed products, one-shot all-reduces and whole batches of
+ * slab CG iterations from C++ (the Python driver's per-iteration host calls
+ * are the bottleneck at strong-scaling sizes).  The receive-region layout and
+ * epoch protocol are peer.py's PeerTransport; `epochs` = {plane epoch,
+ * all-reduce epoch} carried in and out so Python and native exchanges can
+ * interleave. */
+typedef struct tf_slab tf_slab;
+typedef struct tf_slab_desc {
+    tf_grid grid;                 /* the local slab */
+    int32_t precision;            /* 32 | 64 */
+    const void* ke;               /* host, 576 entries of the working precision */
+    const void* scale;            /* device, per local element */
+    const uint8_t* node_fixed;    /* device (tf_build_node_fixed) */
+    const int64_t* fixed;         /* device list of local fixed DOFs (pass-through) */
+    int64_t n_fixed;
+    const uint8_t* owned;         /* device owner-computes mask (nullable) */
+    const int64_t* left_idx;      /* device DOF ids of node plane 0 */
+    const int64_t* right_idx;     /* device DOF ids of node plane nelx */
+    int64_t plane_len;
+    int32_t has_left, has_right, rank, world;
+    void* const* peer_base;       /* host array [world]: receive-region bases (own at [rank]) */
+    int64_t off_planes, plane_bytes, off_flags, off_arflags, off_slots, max_scalars;
+    int32_t bl, br;               /* node columns of the interface x-ranges */
+} tf_slab_desc;
+int tf_slab_create(tf_slab** out, const tf_slab_desc* d);
+int tf_slab_destroy(tf_slab* h);
+int tf_slab_apply(tf_slab* h, const void* v, void* w, uint32_t* epochs, void* stream);
+int tf_slab_allreduce(tf_slab* h, double* t, int k, uint32_t* epochs, void* stream);
+int tf_slab_pcg_iterate(tf_slab* h, const void* b, const void* inv, void* x, void* r, void* z, void* p,
+                        void* q, void* wtmp, double* state, double* red, double* work, int it0,
+                        int n_iters, int recompute_every, double* hist, int hist_len, uint32_t* epochs,
+                        void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -40,6 +40,35 @@ class tf_grid(ctypes.Structure):
     _fields_ = [("nelx", ctypes.c_int32), ("nely", ctypes.c_int32), ("nelz", ctypes.c_int32)]
 
 
+class tf_slab_desc(ctypes.Structure):
+    _fields_ = [
+        ("grid", tf_grid),
+        ("precision", ctypes.c_int32),
+        ("ke", ctypes.c_void_p),
+        ("scale", ctypes.c_void_p),
+        ("node_fixed", ctypes.c_void_p),
+        ("fixed", ctypes.c_void_p),
+        ("n_fixed", ctypes.c_int64),
+        ("owned", ctypes.c_void_p),
+        ("left_idx", ctypes.c_void_p),
+        ("right_idx", ctypes.c_void_p),
+        ("plane_len", ctypes.c_int64),
+        ("has_left", ctypes.c_int32),
+        ("has_right", ctypes.c_int32),
+        ("rank", ctypes.c_int32),
+        ("world", ctypes.c_int32),
+        ("peer_base", ctypes.c_void_p),
+        ("off_planes", ctypes.c_int64),
+        ("plane_bytes", ctypes.c_int64),
+        ("off_flags", ctypes.c_int64),
+        ("off_arflags", ctypes.c_int64),
+        ("off_slots", ctypes.c_int64),
+        ("max_scalars", ctypes.c_int64),
+        ("bl", ctypes.c_int32),
+        ("br", ctypes.c_int32),
+    ]
+
+
 class tf_pcg_desc(ctypes.Structure):
     _fields_ = [
         ("precision", ctypes.c_int),
@@ -145,6 +174,11 @@ _SIGS = {
     "tf_stream_write_u32": [_P, ctypes.c_uint32, _P],
     "tf_stream_wait_u32": [_P, ctypes.c_uint32, _P],
     "tf_rank_sum_f64": [_P, _INT, _INT, _P, _P],
+    "tf_slab_create": [_P, _P],
+    "tf_slab_destroy": [_P],
+    "tf_slab_apply": [_P, _P, _P, _P, _P],
+    "tf_slab_allreduce": [_P, _P, _INT, _P, _P],
+    "tf_slab_pcg_iterate": [_P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _INT, _INT, _INT, _P, _INT, _P, _P],
 }
 for _s in ("f32", "f64"):
     _SIGS.update({

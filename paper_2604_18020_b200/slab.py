@@ -219,6 +219,10 @@ class SlabOperator:
         self.n_apply = 0
 
     def apply(self, x):
+        nat = self.native()
+        if nat is not None:  # the whole distributed product enqueued from C++
+            self.n_apply += 1
+            return nat.apply(x)
         split = getattr(self.local_apply, "split", None)
         if split is not None:
             # interface columns first, exchange in flight while the interior runs
@@ -241,6 +245,19 @@ class SlabOperator:
         if self.fixed.numel():
             d[self.fixed] = 1.0
         return d
+
+    def native(self):
+        """The native slab runtime over the peer transport (tf_slab_run.cu),
+        or None (other transports, or local compute that is not the tile
+        kernels)."""
+        import os
+
+        if (self.transport != "peer" or getattr(self.local_apply, "op", None) is None
+                or os.environ.get("TF_SLAB_NATIVE", "1") != "1"):
+            return None
+        if getattr(self, "_native", None) is None:
+            self._native = NativeSlab(self)
+        return self._native
 
     def allreduce_dev(self, t, lo: int, hi: int):
         """In place, no host round trip on NCCL/peer: t[lo:hi] (FP64 device
@@ -354,6 +371,86 @@ def slab_pcg(op: SlabOperator, b, diag, rel_tol=1e-5, max_iter=1000, recompute_e
     return x, dict(iterations=it, termination=term, rel=rel, history=hist, matvecs=mv)
 
 
+class NativeSlab:
+    """Handle of the native slab runtime bound to a SlabOperator with the
+    peer transport: products, all-reduces and batches of CG iterations are
+    enqueued from C++ (csrc/tf_slab_run.cu), sharing the transport's receive
+    regions and epoch counters."""
+
+    def __init__(self, sop: "SlabOperator"):
+        import ctypes
+
+        import torch
+
+        from . import _device as D
+        from . import _lib
+
+        tr, la = sop.exchange, sop.local_apply
+        op = la.op
+        self.sop = sop
+        self._keep = [np.ascontiguousarray(op.ke), sop.owned.to(torch.uint8)]
+        self._peers = (ctypes.c_void_p * tr.world)(*[tr.peer[r] for r in range(tr.world)])
+        d = _lib.tf_slab_desc()
+        d.grid = op.dev.grid
+        d.precision = 64 if op.precision.dtype == np.float64 else 32
+        d.ke = self._keep[0].ctypes.data
+        d.scale = D.ptr(op._scale_dev)
+        d.node_fixed = D.ptr(op.dev.node_fixed)
+        d.fixed = D.ptr(sop.fixed) if sop.fixed.numel() else None
+        d.n_fixed = int(sop.fixed.numel())
+        d.owned = D.ptr(self._keep[1])
+        d.left_idx, d.right_idx = D.ptr(tr.left_idx), D.ptr(tr.right_idx)
+        d.plane_len = tr.plane_len
+        p = sop.part
+        d.has_left, d.has_right, d.rank, d.world = int(p.has_left), int(p.has_right), tr.rank, tr.world
+        d.peer_base = ctypes.cast(self._peers, ctypes.c_void_p)
+        d.off_planes, d.plane_bytes, d.off_flags = tr.off_planes, tr.plane_bytes, tr.off_flags
+        d.off_arflags, d.off_slots, d.max_scalars = tr.off_arflags, tr.off_slots, tr.max_scalars
+        d.bl, d.br = int(la.bl), int(la.br)
+        h = ctypes.c_void_p()
+        _lib.call("tf_slab_create", ctypes.byref(h), ctypes.byref(d))
+        self.h = h
+        self.epochs = (ctypes.c_uint32 * 2)()
+
+    def _sync_in(self):
+        tr = self.sop.exchange
+        self.epochs[0], self.epochs[1] = tr.epoch, tr.ar_epoch
+
+    def _sync_out(self):
+        tr = self.sop.exchange
+        tr.epoch, tr.ar_epoch = int(self.epochs[0]), int(self.epochs[1])
+
+    def apply(self, x, out=None):
+        import torch
+
+        from . import _device as D
+        from . import _lib
+
+        w = torch.empty_like(x) if out is None else out
+        self._sync_in()
+        _lib.call("tf_slab_apply", self.h, D.ptr(x), D.ptr(w), self.epochs, D.stream_ptr())
+        self._sync_out()
+        return w
+
+    def iterate(self, b, inv, x, r, z, p, q, wtmp, state, red, work, it0, n, recompute_every, hist):
+        from . import _device as D
+        from . import _lib
+
+        self._sync_in()
+        _lib.call("tf_slab_pcg_iterate", self.h, D.ptr(b), D.ptr(inv), D.ptr(x), D.ptr(r), D.ptr(z), D.ptr(p),
+                  D.ptr(q), D.ptr(wtmp), D.ptr(state), D.ptr(red), D.ptr(work), int(it0), int(n),
+                  int(recompute_every), D.ptr(hist), int(hist.numel()), self.epochs, D.stream_ptr())
+        self._sync_out()
+
+    def __del__(self):
+        try:
+            from . import _lib
+
+            _lib.load().tf_slab_destroy(self.h)
+        except Exception:
+            pass
+
+
 _SLAB_TERMS = {1: "converged", 2: "breakdown", 3: "diverged"}
 
 
@@ -368,6 +465,8 @@ def slab_pcg_device(op: SlabOperator, b, diag, rel_tol=1e-5, max_iter=1000, reco
     `poll` iterations; the device freezes the solve at the exact stop
     iteration, so results do not depend on `poll`.
     """
+    import os
+
     import torch
 
     from . import _device as D
@@ -409,7 +508,19 @@ def slab_pcg_device(op: SlabOperator, b, diag, rel_tol=1e-5, max_iter=1000, reco
     allreduce(1, 3)
     _lib.call("tf_slab_cg_start", D.ptr(state), D.ptr(red), float(rel_tol), int(f32), st)
     hist[0:1].copy_(state[2:3])
-    if float(state[4]) != 0.0:
+    native = op.native()
+    if native is not None and float(state[4]) != 0.0:
+        # the whole loop body enqueued from C++ in batches of `poll` iterations
+        q = torch.empty_like(b)
+        wtmp = torch.empty_like(b)
+        it = 0
+        while it < max_iter:
+            k = min(poll, max_iter - it)
+            native.iterate(b, inv, x, r, z, p, q, wtmp, state, red, work, it, k, recompute_every, hist)
+            it += k
+            if float(state[4]) == 0.0:
+                break
+    elif float(state[4]) != 0.0:
         for it in range(1, max_iter + 1):
             q = op.apply(p)
             _lib.call(f"tf_slab_cg_pq_{sfx}", n, D.ptr(p), D.ptr(q), D.ptr(owned), D.ptr(state), D.ptr(red),
@@ -484,6 +595,8 @@ def gpu_local_kernels(part: SlabPartition, bcs_local: BoundaryConditions, rho_lo
 
     if op.grid_kernel == "tile":
         local_apply.split = split
+        # what the native slab runtime (tf_slab_run.cu) needs to run this slab
+        local_apply.op, local_apply.bl, local_apply.br = op, bl, br
 
     def local_diag_partial():
         # FP64 partial sums of s_e * Ke[l,l] on this slab (no fixed handling yet)

@@ -204,9 +204,12 @@ def _peer_worker(rank, world, port, dims, prec, q):
         lb = part.local_bcs(bcs)
         tdt = torch.float64 if prec == "fp64" else torch.float32
         out = {}
-        for transport in ("p2p", "peer"):
+        for transport in ("p2p", "peer", "peer_py"):
+            # "peer": native runtime (tf_slab_run.cu); "peer_py": the same
+            # transport driven from Python
+            os.environ["TF_SLAB_NATIVE"] = "0" if transport == "peer_py" else "1"
             _, la, ld = gpu_local_kernels(part, lb, part.scatter_elem(rho), SimpParams(3.0), prec)
-            op = SlabOperator(part, lb, la, ld, "cuda:0", tdt, transport=transport)
+            op = SlabOperator(part, lb, la, ld, "cuda:0", tdt, transport="p2p" if transport == "p2p" else "peer")
             x = torch.from_numpy(part.scatter(v)).to("cuda:0", tdt)
             ws = [op.apply(x).cpu().numpy() for _ in range(3)]  # several epochs (slot parities)
             d = op.diagonal()
@@ -252,3 +255,10 @@ def test_slab_peer_transport_matches_p2p(world, dims, prec):
         # north star's CG bars (+-2 % iterations, solution within 1e-3)
         assert abs(itp - itq) <= max(2, 0.02 * itp)
         assert np.abs(xp - xq).max() <= 1e-3 * np.abs(xp).max()
+        # native and Python-driven peer paths: same kernels and reductions
+        # (the diagonals differ in the last bit through the Jacobi atomics)
+        wy, dy, xy, ity, ry = out["peer_py"]
+        for a, b in zip(wq, wy):
+            assert np.array_equal(a, b)
+        assert abs(ity - itq) <= 1 and np.array_equal(ry, rq)
+        assert np.abs(xy - xq).max() <= (1e-6 if prec == "fp64" else 1e-3) * np.abs(xq).max()

@@ -384,7 +384,7 @@ def run_ours(args):
         traffic = json.loads(tf.read_text()).get(f"{args.config}_{prec}")
 
     simp = cg = simp2 = sweep = None
-    scaling = simp_scaling(world, dist) if args.simp else None
+    scaling = simp_scaling_all(world, dist) if args.simp else None
     if args.simp and rank == 0:
         simp = simp_c1()
         simp2 = simp_c2()
@@ -534,6 +534,25 @@ def simp_c2():
             "paper_note": "fused SIMP-120 wall at 216k, PAPER.md:1223-1227 (RTX 4090, context only)"}
 
 
+def simp_scaling_all(world, dist):
+    """simp_scaling over the available slab transports (N > 1: NCCL P2P and
+    the peer-memory runtime; a transport that fails reports its error)."""
+    out = simp_scaling(world, dist)
+    if world > 1:
+        old = os.environ.get("TF_SLAB_TRANSPORT")
+        os.environ["TF_SLAB_TRANSPORT"] = "peer"
+        try:
+            out["peer"] = simp_scaling(world, dist)
+        except Exception as e:  # keep the bench line; say why
+            out["peer"] = {"error": repr(e)[:300]}
+        finally:
+            if old is None:
+                os.environ.pop("TF_SLAB_TRANSPORT", None)
+            else:
+                os.environ["TF_SLAB_TRANSPORT"] = old
+    return out
+
+
 def simp_scaling(world, dist, iters=6):
     """SIMP s/iter at c4 (cantilever 200x100x50, 1M elements) strong-scaled
     over the job's ranks: the first `iters` iterations of
@@ -580,7 +599,8 @@ def simp_scaling(world, dist, iters=6):
         loop = float(t.item())
     return {"config": f"c4 cantilever 200x100x50 (1M), default_schedule(120) iterations 1-{iters}, FP32, "
                       f"strong-scaled over {world} rank(s)",
-            "path": "run_simp (device-resident)" if world == 1 else "slab_run_simp (x-slabs)",
+            "path": "run_simp (device-resident)" if world == 1 else
+                    f"slab_run_simp (x-slabs, {os.environ.get('TF_SLAB_TRANSPORT', 'p2p')} transport)",
             "n_gpus": world, "s_per_iter": loop / iters, "wall_s": wall, "setup_s": wall - loop,
             "cg_iterations": [h.cg_iterations for h in res.history],
             "compliance": [h.compliance for h in res.history]}

@@ -237,17 +237,35 @@ def run_ours(args):
         lop, local_apply, local_diag = gpu_local_kernels(part, lb, part.scatter_elem(grho),
                                                          SimpParams(3.0), prec)
         dt = lop.precision.dtype
-        sop = SlabOperator(part, lb, local_apply, local_diag, dev,
-                           torch.float32 if prec == "fp32" else torch.float64)
+        tdt = torch.float32 if prec == "fp32" else torch.float64
+        sop_p2p = SlabOperator(part, lb, local_apply, local_diag, dev, tdt, transport="p2p")
         m = part.local_mesh
         v = part.scatter(gv)
         x = torch.tensor(v.astype(dt), device=dev)
+        # transport: the peer-memory runtime when it initialises on this box
+        # AND its product equals the NCCL P2P one bitwise on every rank,
+        # else NCCL P2P (TF_SLAB_TRANSPORT=p2p pins it)
+        sop, sop_peer, transport_note = sop_p2p, None, "p2p (NCCL send/recv)"
+        if os.environ.get("TF_SLAB_TRANSPORT", "auto") in ("auto", "peer"):
+            ok = 0
+            try:
+                sop_peer = SlabOperator(part, lb, local_apply, local_diag, dev, tdt, transport="peer")
+                ok = int(torch.equal(sop_p2p.apply(x), sop_peer.apply(x)))
+                torch.cuda.synchronize()
+            except Exception as e:  # noqa: BLE001 - reported, NCCL path kept
+                transport_note = f"p2p (peer transport unavailable: {repr(e)[:160]})"
+            t = torch.tensor([ok], device="cpu" if same_dev else dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MIN)
+            if int(t.item()) == 1:
+                sop, transport_note = sop_peer, "peer (CUDA IPC puts + stream-ordered flags, verified bitwise vs NCCL)"
+            elif sop_peer is not None and "unavailable" not in transport_note:
+                transport_note = "p2p (peer product differed from NCCL's; not used)"
 
         def step():
             sop.apply(x)
 
         apply_fn = sop.apply
-        desc = f"{desc}; global {gdims[0]}x{gdims[1]}x{gdims[2]} x-slabs, NCCL interface exchange"
+        desc = f"{desc}; global {gdims[0]}x{gdims[1]}x{gdims[2]} x-slabs, interface exchange: {transport_note}"
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream()
 
@@ -295,20 +313,24 @@ def run_ours(args):
     # torch.distributed P2P one (NCCL), max over ranks
     transports = None
     if world > 1:
-        sop_peer = SlabOperator(part, lb, local_apply, local_diag, dev, sop.dtype, transport="peer")
-        for _ in range(3):
-            sop_peer.apply(x)
-        torch.cuda.synchronize()
-        dist.barrier()
-        e0.record(stream)
-        for _ in range(args.steps):
-            sop_peer.apply(x)
-        e1.record(stream)
-        torch.cuda.synchronize()
-        ms_peer = e0.elapsed_time(e1) / args.steps
-        t = torch.tensor([ms_warm, ms_peer], device="cpu" if same_dev else dev)
+        def warm_ms(o):
+            for _ in range(3):
+                o.apply(x)
+            torch.cuda.synchronize()
+            dist.barrier()
+            e0.record(stream)
+            for _ in range(args.steps):
+                o.apply(x)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            return e0.elapsed_time(e1) / args.steps
+
+        ms_p2p = warm_ms(sop_p2p)
+        ms_peer = warm_ms(sop_peer) if (sop_peer is not None and sop is sop_peer) else float("nan")
+        t = torch.tensor([ms_p2p, ms_peer], device="cpu" if same_dev else dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         transports = {"p2p_ms_per_step": float(t[0]), "peer_ms_per_step": float(t[1]),
+                      "used": "peer" if sop is sop_peer else "p2p",
                       "note": "warm back-to-back slab products, max over ranks"}
 
     # e2e through the public API from pinned host buffers: every step copies

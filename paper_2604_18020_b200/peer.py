@@ -61,25 +61,38 @@ class PeerTransport:
         self.base = int(p.value)
         hb = int(L.tf_ipc_handle_bytes())
         handle = (ctypes.c_char * hb)()
-        _lib.check(L.tf_ipc_export(ctypes.c_void_p(self.base), handle), "tf_ipc_export")
-        handles = [None] * self.world
+        mine = bytes(handle) if L.tf_ipc_export(ctypes.c_void_p(self.base), handle) == _lib.TF_OK else None
+        if mine is not None:
+            mine = bytes(handle)
+        handles = [mine] * self.world
         if self.world > 1:
-            dist.all_gather_object(handles, bytes(handle), group=group)
-        self.peer = {}
+            dist.all_gather_object(handles, mine, group=group)
+        self.peer = {self.rank: self.base}
+        err = None if all(h is not None for h in handles) else "cudaIpcGetMemHandle failed on a rank"
         for r in range(self.world):
-            if r == self.rank:
-                self.peer[r] = self.base
+            if r == self.rank or err:
                 continue
             q = ctypes.c_void_p()
             hbuf = ctypes.create_string_buffer(handles[r], hb)
-            _lib.check(L.tf_ipc_open(hbuf, ctypes.byref(q)), "tf_ipc_open")
+            rc = L.tf_ipc_open(hbuf, ctypes.byref(q))
+            if rc != _lib.TF_OK:
+                err = L.tf_last_error().decode(errors="replace")
+                break
             self.peer[r] = int(q.value)
+        if self.world > 1:
+            # every rank learns whether all mappings exist (and none puts
+            # before they do): one all-reduce instead of a bare barrier, so a
+            # failing rank cannot leave the others waiting in a collective
+            gloo = dist.get_backend(group) == "gloo"
+            ok = t.tensor([0 if err else 1], dtype=t.int32, device="cpu" if gloo else device)
+            dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=group)
+            if int(ok.item()) == 0:
+                self.close()
+                raise RuntimeError(f"peer transport unavailable: {err or 'a peer rank failed to map'}")
         self.epoch = 0
         self.ar_epoch = 0
         self.scalar_idx = t.arange(self.max_scalars, dtype=t.int64, device=device)
         self._acc = t.empty(self.max_scalars, dtype=t.float64, device=device)
-        if self.world > 1:
-            dist.barrier(group=group)  # every mapping exists before the first put
 
     # -- layout ------------------------------------------------------------------
     def _plane(self, base, parity, side):

@@ -393,6 +393,22 @@ int tf_plane_put_f64(const double* w, const int64_t* idx, int64_t n, double* dst
 int tf_plane_add_f32(float* w, const int64_t* idx, int64_t n, const float* recv, int recv_first, void* stream);
 int tf_plane_add_f64(double* w, const int64_t* idx, int64_t n, const double* recv, int recv_first,
                      void* stream);
+/* Multi-destination put: job j copies src[idx[j][k]] (idx or idx[j] null:
+ * src[k]) into dst[j][k] (peer mappings), k < n, then raises *flags[j] =
+ * epoch after a system-scope fence (last block of the job).  njobs <= 16;
+ * tickets: 16 zeroed device words (re-armed by the kernel).  Host arrays of
+ * device pointers. */
+int tf_put_flags_f32(const float* src, const int64_t* const* idx, float* const* dst, uint32_t* const* flags,
+                     int njobs, int64_t n, uint32_t epoch, uint32_t* tickets, void* stream);
+int tf_put_flags_f64(const double* src, const int64_t* const* idx, double* const* dst, uint32_t* const* flags,
+                     int njobs, int64_t n, uint32_t epoch, uint32_t* tickets, void* stream);
+/* every *addrs[i] >= value (one batched stream memory operation, n <= 64) */
+int tf_stream_wait_many_u32(void* const* addrs, int n, uint32_t value, void* stream);
+/* both interface planes: w[li] = recv_left + w[li]; w[ri] = w[ri] + recv_right (either side null) */
+int tf_plane_add2_f32(float* w, const int64_t* left_idx, const float* recv_left, const int64_t* right_idx,
+                      const float* recv_right, int64_t n, void* stream);
+int tf_plane_add2_f64(double* w, const int64_t* left_idx, const double* recv_left, const int64_t* right_idx,
+                      const double* recv_right, int64_t n, void* stream);
 /* out[j] = sum_r slots[r*k + j], ranks in ascending order (k <= 1024) */
 int tf_rank_sum_f64(const double* slots, int nranks, int k, double* out, void* stream);
 

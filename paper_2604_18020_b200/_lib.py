@@ -174,6 +174,7 @@ _SIGS = {
     "tf_stream_write_u32": [_P, ctypes.c_uint32, _P],
     "tf_stream_wait_u32": [_P, ctypes.c_uint32, _P],
     "tf_rank_sum_f64": [_P, _INT, _INT, _P, _P],
+    "tf_stream_wait_many_u32": [_P, _INT, ctypes.c_uint32, _P],
     "tf_slab_create": [_P, _P],
     "tf_slab_destroy": [_P],
     "tf_slab_apply": [_P, _P, _P, _P, _P],
@@ -190,6 +191,8 @@ for _s in ("f32", "f64"):
         f"tf_slab_cg_beta_{_s}": [_I64, _P, _P, _P, _P, _P, _INT, _P],
         f"tf_plane_put_{_s}": [_P, _P, _I64, _P, _P],
         f"tf_plane_add_{_s}": [_P, _P, _I64, _P, _INT, _P],
+        f"tf_put_flags_{_s}": [_P, _P, _P, _P, _INT, _I64, ctypes.c_uint32, _P, _P],
+        f"tf_plane_add2_{_s}": [_P, _P, _P, _P, _P, _I64, _P],
     })
 
 _lib = None

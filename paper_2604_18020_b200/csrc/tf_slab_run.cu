@@ -34,6 +34,7 @@ struct tf_slab {
     std::vector<void*> peers;
     int64_t* scalar_idx;   // device [0, 1, ..., 15]
     double* acc;           // device [16]
+    uint32_t* tickets;     // device [16], tf_put_flags' per-job block counters
 };
 
 namespace {
@@ -53,14 +54,6 @@ int slab_apply(tf_slab* h, const void* v, void* w, cudaStream_t st, uint32_t* ep
                                               (const double*)v, (double*)w, d.node_fixed, TF_MASK_INPUT, lo,
                                               hi, st);
     };
-    auto put = [&](const int64_t* idx, void* dst) -> int {
-        return f32 ? tf_plane_put_f32((const float*)w, idx, d.plane_len, (float*)dst, st)
-                   : tf_plane_put_f64((const double*)w, idx, d.plane_len, (double*)dst, st);
-    };
-    auto add = [&](const int64_t* idx, const void* recv, int first) -> int {
-        return f32 ? tf_plane_add_f32((float*)w, idx, d.plane_len, (const float*)recv, first, st)
-                   : tf_plane_add_f64((double*)w, idx, d.plane_len, (const double*)recv, first, st);
-    };
     const int nnx = d.grid.nelx + 1;
     int rc;
     if ((rc = range(0, d.bl))) return rc;
@@ -68,27 +61,36 @@ int slab_apply(tf_slab* h, const void* v, void* w, cudaStream_t st, uint32_t* ep
     const uint32_t e = ++*epoch;
     const int par = (int)(e & 1u);
     auto plane = [&](void* base, int side) { return at(base, d.off_planes + (2 * par + side) * d.plane_bytes); };
-    auto flag = [&](void* base, int side) { return at(base, d.off_flags + 4 * side); };
+    auto flag = [&](void* base, int side) { return (uint32_t*)at(base, d.off_flags + 4 * side); };
+    // both interface planes into the neighbours' slots + their flags: one launch
+    const int64_t* idx[2];
+    void* dst[2];
+    uint32_t* flg[2];
+    int nj = 0;
     if (d.has_left) {
         void* nb = h->peers[d.rank - 1];
-        if ((rc = put(d.left_idx, plane(nb, 1)))) return rc;
-        if ((rc = tf_stream_write_u32(flag(nb, 1), e, st))) return rc;
+        idx[nj] = d.left_idx, dst[nj] = plane(nb, 1), flg[nj] = flag(nb, 1), ++nj;
     }
     if (d.has_right) {
         void* nb = h->peers[d.rank + 1];
-        if ((rc = put(d.right_idx, plane(nb, 0)))) return rc;
-        if ((rc = tf_stream_write_u32(flag(nb, 0), e, st))) return rc;
+        idx[nj] = d.right_idx, dst[nj] = plane(nb, 0), flg[nj] = flag(nb, 0), ++nj;
     }
+    rc = f32 ? tf_put_flags_f32((const float*)w, idx, (float* const*)dst, flg, nj, d.plane_len, e, h->tickets, st)
+             : tf_put_flags_f64((const double*)w, idx, (double* const*)dst, flg, nj, d.plane_len, e, h->tickets, st);
+    if (rc) return rc;
     if ((rc = range(d.bl, nnx - d.br))) return rc;
     void* me = h->peers[d.rank];
-    if (d.has_left) {
-        if ((rc = tf_stream_wait_u32(flag(me, 0), e, st))) return rc;
-        if ((rc = add(d.left_idx, plane(me, 0), 1))) return rc;
-    }
-    if (d.has_right) {
-        if ((rc = tf_stream_wait_u32(flag(me, 1), e, st))) return rc;
-        if ((rc = add(d.right_idx, plane(me, 1), 0))) return rc;
-    }
+    void* waits[2];
+    int nw = 0;
+    if (d.has_left) waits[nw++] = flag(me, 0);
+    if (d.has_right) waits[nw++] = flag(me, 1);
+    if ((rc = tf_stream_wait_many_u32(waits, nw, e, st))) return rc;
+    // fixed order: left partial first on the left plane, own partial first on the right
+    rc = f32 ? tf_plane_add2_f32((float*)w, d.has_left ? d.left_idx : nullptr, (const float*)plane(me, 0),
+                                 d.has_right ? d.right_idx : nullptr, (const float*)plane(me, 1), d.plane_len, st)
+             : tf_plane_add2_f64((double*)w, d.has_left ? d.left_idx : nullptr, (const double*)plane(me, 0),
+                                 d.has_right ? d.right_idx : nullptr, (const double*)plane(me, 1), d.plane_len, st);
+    if (rc) return rc;
     if (d.n_fixed > 0)
         rc = f32 ? tf_pass_fixed_f32(d.fixed, d.n_fixed, (const float*)v, (float*)w, st)
                  : tf_pass_fixed_f64(d.fixed, d.n_fixed, (const double*)v, (double*)w, st);
@@ -106,13 +108,19 @@ int slab_allreduce(tf_slab* h, double* t, int k, cudaStream_t st, uint32_t* ar_e
         return at(base, d.off_slots + 8 * d.max_scalars * ((int64_t)d.world * par + src));
     };
     int rc;
-    for (int r = 0; r < d.world; ++r) {
-        if ((rc = tf_plane_put_f64(t, h->scalar_idx, k, (double*)slot(h->peers[r], d.rank), st))) return rc;
-        if ((rc = tf_stream_write_u32(at(h->peers[r], d.off_arflags + 4 * d.rank), e, st))) return rc;
-    }
+    TF_REQUIRE(d.world <= 16, "peer all-reduce supports up to 16 ranks");
+    double* dst[16];
+    uint32_t* flg[16];
+    void* waits[16];
     void* me = h->peers[d.rank];
-    for (int r = 0; r < d.world; ++r)
-        if ((rc = tf_stream_wait_u32(at(me, d.off_arflags + 4 * r), e, st))) return rc;
+    for (int r = 0; r < d.world; ++r) {
+        dst[r] = (double*)slot(h->peers[r], d.rank);
+        flg[r] = (uint32_t*)at(h->peers[r], d.off_arflags + 4 * d.rank);
+        waits[r] = at(me, d.off_arflags + 4 * r);
+    }
+    // this rank's partials into every rank's slot + flags (one launch), then one batched wait
+    if ((rc = tf_put_flags_f64(t, nullptr, dst, flg, d.world, k, e, h->tickets, st))) return rc;
+    if ((rc = tf_stream_wait_many_u32(waits, d.world, e, st))) return rc;
     if ((rc = tf_rank_sum_f64((const double*)slot(me, 0), d.world, (int)d.max_scalars, h->acc, st))) return rc;
     TF_CUDA_TRY(cudaMemcpyAsync(t, h->acc, sizeof(double) * k, cudaMemcpyDeviceToDevice, st));
     return TF_OK;
@@ -137,7 +145,8 @@ int tf_slab_create(tf_slab** out, const tf_slab_desc* d)
     h->d.ke = nullptr;
     int64_t idx[16];
     for (int i = 0; i < 16; ++i) idx[i] = i;
-    if (cudaMalloc(&h->scalar_idx, sizeof(idx)) != cudaSuccess || cudaMalloc(&h->acc, 16 * sizeof(double)) != cudaSuccess) {
+    if (cudaMalloc(&h->scalar_idx, sizeof(idx)) != cudaSuccess || cudaMalloc(&h->acc, 16 * sizeof(double)) != cudaSuccess ||
+        cudaMalloc(&h->tickets, 16 * sizeof(uint32_t)) != cudaSuccess || cudaMemset(h->tickets, 0, 16 * sizeof(uint32_t)) != cudaSuccess) {
         delete h;
         tf::set_error("cudaMalloc failed");
         return TF_ERR_CUDA;
@@ -152,6 +161,7 @@ int tf_slab_destroy(tf_slab* h)
     if (!h) return TF_OK;
     cudaFree(h->scalar_idx);
     cudaFree(h->acc);
+    cudaFree(h->tickets);
     delete h;
     return TF_OK;
 }

@@ -93,6 +93,7 @@ class PeerTransport:
         self.ar_epoch = 0
         self.scalar_idx = t.arange(self.max_scalars, dtype=t.int64, device=device)
         self._acc = t.empty(self.max_scalars, dtype=t.float64, device=device)
+        self._tickets = t.zeros(16, dtype=t.int32, device=device)  # tf_put_flags block counters
 
     # -- layout ------------------------------------------------------------------
     def _plane(self, base, parity, side):
@@ -111,22 +112,28 @@ class PeerTransport:
     def __call__(self, w):
         return self.finish(w, self.start(w))
 
+    @staticmethod
+    def _arr(ctype, vals):
+        return (ctype * max(1, len(vals)))(*vals)
+
     def start(self, w):
+        """Both interface planes into the neighbours' slots and their flags
+        raised, one launch (tf_put_flags)."""
         p = self.part
         self.epoch += 1
         e, par = self.epoch, self.epoch & 1
         sfx = "f64" if w.element_size() == 8 else "f32"
-        st = D.stream_ptr()
+        idx, dst, flg = [], [], []
         if p.has_left:  # my left plane -> the left neighbour's "from right" slot
             nb = self.peer[p.rank - 1]
-            _lib.call(f"tf_plane_put_{sfx}", D.ptr(w), D.ptr(self.left_idx), self.plane_len,
-                      self._plane(nb, par, 1), st)
-            _lib.call("tf_stream_write_u32", self._flag(nb, 1), e, st)
+            idx.append(D.ptr(self.left_idx)), dst.append(self._plane(nb, par, 1)), flg.append(self._flag(nb, 1))
         if p.has_right:
             nb = self.peer[p.rank + 1]
-            _lib.call(f"tf_plane_put_{sfx}", D.ptr(w), D.ptr(self.right_idx), self.plane_len,
-                      self._plane(nb, par, 0), st)
-            _lib.call("tf_stream_write_u32", self._flag(nb, 0), e, st)
+            idx.append(D.ptr(self.right_idx)), dst.append(self._plane(nb, par, 0)), flg.append(self._flag(nb, 0))
+        if idx:
+            V = ctypes.c_void_p
+            _lib.call(f"tf_put_flags_{sfx}", D.ptr(w), self._arr(V, idx), self._arr(V, dst), self._arr(V, flg),
+                      len(idx), self.plane_len, e, D.ptr(self._tickets), D.stream_ptr())
         return e
 
     def finish(self, w, state):
@@ -134,14 +141,13 @@ class PeerTransport:
         e, par = state, state & 1
         sfx = "f64" if w.element_size() == 8 else "f32"
         st = D.stream_ptr()
-        if p.has_left:  # left partial first
-            _lib.call("tf_stream_wait_u32", self._flag(self.base, 0), e, st)
-            _lib.call(f"tf_plane_add_{sfx}", D.ptr(w), D.ptr(self.left_idx), self.plane_len,
-                      self._plane(self.base, par, 0), 1, st)
-        if p.has_right:  # my partial first
-            _lib.call("tf_stream_wait_u32", self._flag(self.base, 1), e, st)
-            _lib.call(f"tf_plane_add_{sfx}", D.ptr(w), D.ptr(self.right_idx), self.plane_len,
-                      self._plane(self.base, par, 1), 0, st)
+        waits = ([self._flag(self.base, 0)] if p.has_left else []) + ([self._flag(self.base, 1)] if p.has_right else [])
+        if waits:
+            _lib.call("tf_stream_wait_many_u32", self._arr(ctypes.c_void_p, waits), len(waits), e, st)
+            # left partial first on the left plane, own partial first on the right
+            _lib.call(f"tf_plane_add2_{sfx}", D.ptr(w), D.ptr(self.left_idx) if p.has_left else None,
+                      self._plane(self.base, par, 0), D.ptr(self.right_idx) if p.has_right else None,
+                      self._plane(self.base, par, 1), self.plane_len, st)
         return w
 
     # -- one-shot all-reduce of FP64 scalars -------------------------------------
@@ -156,12 +162,13 @@ class PeerTransport:
         e, par = self.ar_epoch, self.ar_epoch & 1
         st = D.stream_ptr()
         src = D.ptr(t) + 8 * lo
-        for r in range(self.world):
-            dst = self.peer[r]
-            _lib.call("tf_plane_put_f64", src, D.ptr(self.scalar_idx), k, self._slot(dst, par, self.rank), st)
-            _lib.call("tf_stream_write_u32", self._arflag(dst, self.rank), e, st)
-        for r in range(self.world):
-            _lib.call("tf_stream_wait_u32", self._arflag(self.base, r), e, st)
+        V = ctypes.c_void_p
+        dst = self._arr(V, [self._slot(self.peer[r], par, self.rank) for r in range(self.world)])
+        flg = self._arr(V, [self._arflag(self.peer[r], self.rank) for r in range(self.world)])
+        # own partials into every rank's slot + flags (one launch), one batched wait
+        _lib.call("tf_put_flags_f64", src, None, dst, flg, self.world, k, e, D.ptr(self._tickets), st)
+        waits = self._arr(V, [self._arflag(self.base, r) for r in range(self.world)])
+        _lib.call("tf_stream_wait_many_u32", waits, self.world, e, st)
         # the slots of one parity are [world][max_scalars]: sum full rows in
         # rank order, keep the k used
         _lib.call("tf_rank_sum_f64", self._slot(self.base, par, 0), self.world, self.max_scalars,

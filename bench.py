@@ -478,10 +478,23 @@ def kernel_sweep(steps=100):
     hbm, _, _ = peaks()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     out = {}
+    from paper_2604_18020_b200.mesh import BoundaryConditions
+
     for name, cfg, kernel in (("c4_tile", "c4", "tile"), ("c5_tile", "c5", "tile"),
-                              ("c2_edof", "c2", "edof"), ("c5_edof", "c5", "edof")):
+                              ("c2_edof", "c2", "edof"), ("c5_edof", "c5", "edof"),
+                              ("c2_edof_seeded_random", "c2", "edof"), ("c5_edof_seeded_random", "c5", "edof")):
         dims, prec, desc = CONFIGS[cfg]
         m, edof, bcs, rho, v = build_problem(dims)
+        if name.endswith("seeded_random"):
+            # the reference's stress pattern (bench.py:151-160): the global DOF
+            # numbering relabelled by a seeded permutation -- same rows and
+            # collision histogram, no spatial locality
+            perm = np.random.default_rng(42).permutation(m.n_dof).astype(np.int32)
+            edof = np.ascontiguousarray(perm[edof])
+            force = np.zeros(m.n_dof)
+            force[perm] = bcs.force
+            bcs = BoundaryConditions(np.sort(perm[bcs.fixed_dofs]).astype(np.int64), force)
+            desc = f"{desc}, seeded_random DOF relabelling"
         op = MatFreeOperator(m, edof, bcs, rho, SimpParams(3.0), prec, grid_kernel=kernel,
                              scatter="parallel_atomic")
         x = torch.tensor(v.astype(op.precision.dtype), device="cuda")

@@ -273,41 +273,45 @@ __global__ void __launch_bounds__(VEC_BLOCK) k_update(CgP<T> P, const double* pa
     const T a = (T)alpha;
     double v[2] = {0.0, 0.0};
     const long long nc = P.n / N, stride = (long long)gridDim.x * VEC_BLOCK;
-    for (long long c = (long long)blockIdx.x * VEC_BLOCK + threadIdx.x; c < nc; c += stride) {
-        T x[N], p[N], r[N], q[N], iv[N];
-        ld16(P.x, c, x);
-        ld16(P.p, c, p);
-        if (!refresh) {
-            ld16(P.r, c, r);
-            ld16(P.q, c, q);
-            ld16(P.inv, c, iv);
+    if (refresh) {
+        // the refresh matvec needs the new x now; otherwise k_direction
+        // applies x += alpha p while it reads p anyway (one vector less per
+        // iteration, same arithmetic)
+        for (long long c = (long long)blockIdx.x * VEC_BLOCK + threadIdx.x; c < nc; c += stride) {
+            T x[N], p[N];
+            ld16(P.x, c, x);
+            ld16(P.p, c, p);
+#pragma unroll
+            for (int k = 0; k < N; ++k) x[k] = add_rn(x[k], mul_rn(a, p[k]));
+            st16(P.x, c, x);
         }
+        if (blockIdx.x == 0)
+            for (long long i = nc * N + threadIdx.x; i < P.n; i += VEC_BLOCK) P.x[i] = add_rn(P.x[i], mul_rn(a, P.p[i]));
+        return;  // k_residual produces the partials this iteration
+    }
+    for (long long c = (long long)blockIdx.x * VEC_BLOCK + threadIdx.x; c < nc; c += stride) {
+        T r[N], q[N], iv[N];
+        ld16(P.r, c, r);
+        ld16(P.q, c, q);
+        ld16(P.inv, c, iv);
 #pragma unroll
         for (int k = 0; k < N; ++k) {
-            x[k] = add_rn(x[k], mul_rn(a, p[k]));
-            if (!refresh) {
-                r[k] = sub_rn(r[k], mul_rn(a, q[k]));
-                const T z = mul_rn(r[k], iv[k]);
-                v[0] += (double)r[k] * (double)r[k];
-                v[1] += (double)r[k] * (double)z;
-            }
+            r[k] = sub_rn(r[k], mul_rn(a, q[k]));
+            const T z = mul_rn(r[k], iv[k]);
+            v[0] += (double)r[k] * (double)r[k];
+            v[1] += (double)r[k] * (double)z;
         }
-        st16(P.x, c, x);
-        if (!refresh) st16(P.r, c, r);
+        st16(P.r, c, r);
     }
     if (blockIdx.x == 0) {
         for (long long i = nc * N + threadIdx.x; i < P.n; i += VEC_BLOCK) {
-            P.x[i] = add_rn(P.x[i], mul_rn(a, P.p[i]));
-            if (!refresh) {
-                const T r = sub_rn(P.r[i], mul_rn(a, P.q[i]));
-                P.r[i] = r;
-                const T z = mul_rn(r, P.inv[i]);
-                v[0] += (double)r * (double)r;
-                v[1] += (double)r * (double)z;
-            }
+            const T r = sub_rn(P.r[i], mul_rn(a, P.q[i]));
+            P.r[i] = r;
+            const T z = mul_rn(r, P.inv[i]);
+            v[0] += (double)r * (double)r;
+            v[1] += (double)r * (double)z;
         }
     }
-    if (refresh) return;  // k_residual produces the partials this iteration
     __shared__ double sh[2 * 32];
     block_sum_k<2>(v, sh);
     if (threadIdx.x == 0) {
@@ -502,15 +506,41 @@ __global__ void __launch_bounds__(VEC_BLOCK) k_direction(CgP<T> P, int nparts)
         }
         if (P.in_graph) cudaGraphSetConditional(P.h_while, stop ? 0u : 1u);
     }
-    if (stop) return;
+    const long long nc = P.n / N, stride = (long long)gridDim.x * VEC_BLOCK;
+    // this iteration's x += alpha p (deferred from k_update unless it was a
+    // refresh iteration), with the p that the update used -- also when the
+    // loop stops here
+    const bool upd_x = sc->refresh == 0;
+    const T al = (T)sc->alpha;
+    if (stop) {
+        if (upd_x) {
+            for (long long c = (long long)blockIdx.x * VEC_BLOCK + threadIdx.x; c < nc; c += stride) {
+                T x[N], p[N];
+                ld16(P.x, c, x);
+                ld16(P.p, c, p);
+#pragma unroll
+                for (int k = 0; k < N; ++k) x[k] = add_rn(x[k], mul_rn(al, p[k]));
+                st16(P.x, c, x);
+            }
+            if (blockIdx.x == 0)
+                for (long long i = nc * N + threadIdx.x; i < P.n; i += VEC_BLOCK) P.x[i] = add_rn(P.x[i], mul_rn(al, P.p[i]));
+        }
+        return;
+    }
     const T be = (T)beta;
     const bool quant = sc->quantize != 0;
-    const long long nc = P.n / N, stride = (long long)gridDim.x * VEC_BLOCK;
     for (long long c = (long long)blockIdx.x * VEC_BLOCK + threadIdx.x; c < nc; c += stride) {
         T r[N], iv[N], p[N];
         ld16(P.r, c, r);
         ld16(P.inv, c, iv);
         ld16(P.p, c, p);
+        if (upd_x) {
+            T x[N];
+            ld16(P.x, c, x);
+#pragma unroll
+            for (int k = 0; k < N; ++k) x[k] = add_rn(x[k], mul_rn(al, p[k]));
+            st16(P.x, c, x);
+        }
 #pragma unroll
         for (int k = 0; k < N; ++k) p[k] = add_rn(mul_rn(r[k], iv[k]), mul_rn(be, p[k]));
         if (quant) {  // quantize_krylov (solver.py:134-136): p and r to bf16
@@ -525,6 +555,7 @@ __global__ void __launch_bounds__(VEC_BLOCK) k_direction(CgP<T> P, int nparts)
     }
     if (blockIdx.x == 0)
         for (long long i = nc * N + threadIdx.x; i < P.n; i += VEC_BLOCK) {
+            if (upd_x) P.x[i] = add_rn(P.x[i], mul_rn(al, P.p[i]));
             T pn = add_rn(mul_rn(P.r[i], P.inv[i]), mul_rn(be, P.p[i]));
             if (quant) {
                 pn = qbf16(pn);

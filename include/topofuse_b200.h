@@ -447,6 +447,11 @@ int tf_slab_pcg_iterate(tf_slab* h, const void* b, const void* inv, void* x, voi
                         int n_iters, int recompute_every, double* hist, int hist_len, uint32_t* epochs,
                         void* stream);
 
+
+/* sizeof of the public structs {tf_grid, tf_pcg_desc, tf_pcg_report,
+ * tf_oc_report, tf_slab_desc} into out[0..n) (binding ABI check) */
+int tf_abi_struct_sizes(int64_t* out, int n);
+
 #ifdef __cplusplus
 }
 #endif

@@ -176,6 +176,7 @@ _SIGS = {
     "tf_rank_sum_f64": [_P, _INT, _INT, _P, _P],
     "tf_stream_wait_many_u32": [_P, _INT, ctypes.c_uint32, _P],
     "tf_slab_create": [_P, _P],
+    "tf_abi_struct_sizes": [_P, _INT],
     "tf_slab_destroy": [_P],
     "tf_slab_apply": [_P, _P, _P, _P, _P],
     "tf_slab_allreduce": [_P, _P, _INT, _P, _P],

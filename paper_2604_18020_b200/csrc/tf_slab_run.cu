@@ -156,6 +156,15 @@ int tf_slab_create(tf_slab** out, const tf_slab_desc* d)
     return TF_OK;
 }
 
+int tf_abi_struct_sizes(int64_t* out, int n)
+{
+    TF_REQUIRE(out && n >= 0, "bad arguments");
+    const int64_t sz[] = {(int64_t)sizeof(tf_grid), (int64_t)sizeof(tf_pcg_desc), (int64_t)sizeof(tf_pcg_report),
+                          (int64_t)sizeof(tf_oc_report), (int64_t)sizeof(tf_slab_desc)};
+    for (int i = 0; i < n && i < 5; ++i) out[i] = sz[i];
+    return TF_OK;
+}
+
 int tf_slab_destroy(tf_slab* h)
 {
     if (!h) return TF_OK;

@@ -191,3 +191,13 @@ def test_simp_artifacts_byte_identical_to_reference(tmp_path):
     for name in names:
         assert (tmp_path / name).read_bytes() == (gold / name).read_bytes(), name
     assert paths["history"].name == "simp_cantilever_fp64_history.csv"
+
+
+def test_ctypes_struct_layouts_match_the_c_abi():
+    """The ctypes mirrors of the public structs have the C compiler's sizes
+    (a field added on one side only would shift every later field)."""
+    L = _lib.load()
+    out = (ctypes.c_int64 * 5)()
+    assert L.tf_abi_struct_sizes(out, 5) == 0
+    mirrors = [_lib.tf_grid, _lib.tf_pcg_desc, _lib.tf_pcg_report, _lib.tf_oc_report, _lib.tf_slab_desc]
+    assert [ctypes.sizeof(m) for m in mirrors] == list(out)

@@ -446,6 +446,16 @@ int tf_slab_pcg_iterate(tf_slab* h, const void* b, const void* inv, void* x, voi
                         void* q, void* wtmp, double* state, double* red, double* work, int it0,
                         int n_iters, int recompute_every, double* hist, int hist_len, uint32_t* epochs,
                         void* stream);
+/* The same iterations as one CUDA-graph launch (captured once per buffers /
+ * block length / refresh pattern / epoch parities; device-side epochs and
+ * spin-wait kernels with a 30 s timeout).  err_out (nullable, host): copied
+ * from the device error word after the launch. */
+int tf_slab_pcg_graph(tf_slab* h, const void* b, const void* inv, void* x, void* r, void* z, void* p,
+                      void* q, void* wtmp, double* state, double* red, double* work, int it0, int n_iters,
+                      int recompute_every, double* hist, int hist_len, uint32_t* epochs, int* err_out,
+                      void* stream);
+/* *out = 1 when a graph-mode wait timed out (then cleared) */
+int tf_slab_take_error(tf_slab* h, int* out);
 
 
 /* sizeof of the public structs {tf_grid, tf_pcg_desc, tf_pcg_report,

@@ -181,6 +181,8 @@ _SIGS = {
     "tf_slab_apply": [_P, _P, _P, _P, _P],
     "tf_slab_allreduce": [_P, _P, _INT, _P, _P],
     "tf_slab_pcg_iterate": [_P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _INT, _INT, _INT, _P, _INT, _P, _P],
+    "tf_slab_pcg_graph": [_P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _INT, _INT, _INT, _P, _INT, _P, _P, _P],
+    "tf_slab_take_error": [_P, _P],
 }
 for _s in ("f32", "f64"):
     _SIGS.update({

@@ -21,6 +21,7 @@
 // the epoch counters in and out, so Python-side and native exchanges can be
 // interleaved on the same transport.
 
+#include <algorithm>
 #include <cstring>
 #include <vector>
 
@@ -35,13 +36,122 @@ struct tf_slab {
     int64_t* scalar_idx;   // device [0, 1, ..., 15]
     double* acc;           // device [16]
     uint32_t* tickets;     // device [16], tf_put_flags' per-job block counters
+    // graph mode: epochs in device memory, waits as spin kernels (stream
+    // memory operations bake their values into a captured graph)
+    uint32_t* dev_ep;      // device [2]: plane epoch, all-reduce epoch
+    int* dev_err;          // device: 1 = a wait timed out
+    struct Graph {
+        std::vector<const void*> key;
+        cudaGraphExec_t exec;
+    };
+    std::vector<Graph> graphs;
+    cudaStream_t cap = nullptr;
 };
 
 namespace {
 
 inline char* at(void* base, int64_t off) { return reinterpret_cast<char*>(base) + off; }
 
-int slab_apply(tf_slab* h, const void* v, void* w, cudaStream_t st, uint32_t* epoch)
+constexpr int GMAX_JOBS = 16;
+template <typename T>
+struct DevPut {
+    const T* src;
+    const int64_t* idx[GMAX_JOBS];
+    T* dst[GMAX_JOBS];
+    uint32_t* flag[GMAX_JOBS];
+    uint32_t* tickets;
+    const uint32_t* ep;  // epoch = *ep + 1 (advanced by the matching wait kernel)
+    long long n;
+};
+
+template <typename T>
+__global__ void k_put_flags_dev(const __grid_constant__ DevPut<T> J)
+{
+    const int j = blockIdx.y;
+    const int64_t* idx = J.idx[j];
+    T* dst = J.dst[j];
+    for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < J.n; k += (long long)gridDim.x * blockDim.x)
+        dst[k] = J.src[idx ? idx[k] : k];
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0 && atomicAdd(J.tickets + j, 1u) == gridDim.x - 1) {
+        __threadfence_system();
+        *reinterpret_cast<volatile uint32_t*>(J.flag[j]) = *J.ep + 1u;
+        J.tickets[j] = 0u;
+    }
+}
+
+struct DevWait {
+    const uint32_t* flag[GMAX_JOBS];
+    int n;
+    uint32_t* ep;
+    int* err;
+};
+
+// lane i spins until flag i >= *ep + 1 (30 s timeout -> *err = 1), then the
+// epoch advances
+__global__ void k_wait_dev(const __grid_constant__ DevWait W)
+{
+    const uint32_t target = *reinterpret_cast<volatile uint32_t*>(W.ep) + 1u;
+    if ((int)threadIdx.x < W.n) {
+        unsigned long long t0, t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+        while (*reinterpret_cast<const volatile uint32_t*>(W.flag[threadIdx.x]) < target) {
+            __nanosleep(200);
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            if (t - t0 > 30000000000ull) {
+                *W.err = 1;
+                break;
+            }
+        }
+        __threadfence_system();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) *W.ep = target;
+}
+
+__global__ void k_set_ep(uint32_t* ep, uint32_t e0, uint32_t e1)
+{
+    ep[0] = e0;
+    ep[1] = e1;
+}
+
+template <typename T>
+int put_dev(tf_slab* h, const T* src, const int64_t* const* idx, void* const* dst, uint32_t* const* flg, int nj,
+            long long n, const uint32_t* ep, cudaStream_t st)
+{
+    if (nj <= 0) return TF_OK;
+    DevPut<T> J{};
+    J.src = src;
+    for (int j = 0; j < nj; ++j) {
+        J.idx[j] = idx ? idx[j] : nullptr;
+        J.dst[j] = (T*)dst[j];
+        J.flag[j] = flg[j];
+    }
+    J.tickets = h->tickets;
+    J.ep = ep;
+    J.n = n;
+    const unsigned nb = (unsigned)std::min<long long>((n + 255) / 256, 64);
+    k_put_flags_dev<T><<<dim3(nb, nj), 256, 0, st>>>(J);
+    TF_CHECK_LAUNCH();
+    return TF_OK;
+}
+
+int wait_dev(tf_slab* h, void* const* flags, int n, uint32_t* ep, cudaStream_t st)
+{
+    if (n <= 0) return TF_OK;
+    DevWait W{};
+    for (int i = 0; i < n; ++i) W.flag[i] = (const uint32_t*)flags[i];
+    W.n = n;
+    W.ep = ep;
+    W.err = h->dev_err;
+    k_wait_dev<<<1, 32, 0, st>>>(W);
+    TF_CHECK_LAUNCH();
+    return TF_OK;
+}
+
+// dev = true: device epochs (graph capture); else host epochs + stream memops
+int slab_apply(tf_slab* h, const void* v, void* w, cudaStream_t st, uint32_t* epoch, bool dev = false)
 {
     const tf_slab_desc& d = h->d;
     const bool f32 = d.precision == 32;
@@ -58,6 +168,8 @@ int slab_apply(tf_slab* h, const void* v, void* w, cudaStream_t st, uint32_t* ep
     int rc;
     if ((rc = range(0, d.bl))) return rc;
     if ((rc = range(nnx - d.br, nnx))) return rc;
+    // slot parity: the host knows the epoch in both modes (graph mode keeps
+    // the host counter advancing in step with the device one)
     const uint32_t e = ++*epoch;
     const int par = (int)(e & 1u);
     auto plane = [&](void* base, int side) { return at(base, d.off_planes + (2 * par + side) * d.plane_bytes); };
@@ -75,8 +187,12 @@ int slab_apply(tf_slab* h, const void* v, void* w, cudaStream_t st, uint32_t* ep
         void* nb = h->peers[d.rank + 1];
         idx[nj] = d.right_idx, dst[nj] = plane(nb, 0), flg[nj] = flag(nb, 0), ++nj;
     }
-    rc = f32 ? tf_put_flags_f32((const float*)w, idx, (float* const*)dst, flg, nj, d.plane_len, e, h->tickets, st)
-             : tf_put_flags_f64((const double*)w, idx, (double* const*)dst, flg, nj, d.plane_len, e, h->tickets, st);
+    if (dev)
+        rc = f32 ? put_dev<float>(h, (const float*)w, idx, dst, flg, nj, d.plane_len, h->dev_ep, st)
+                 : put_dev<double>(h, (const double*)w, idx, dst, flg, nj, d.plane_len, h->dev_ep, st);
+    else
+        rc = f32 ? tf_put_flags_f32((const float*)w, idx, (float* const*)dst, flg, nj, d.plane_len, e, h->tickets, st)
+                 : tf_put_flags_f64((const double*)w, idx, (double* const*)dst, flg, nj, d.plane_len, e, h->tickets, st);
     if (rc) return rc;
     if ((rc = range(d.bl, nnx - d.br))) return rc;
     void* me = h->peers[d.rank];
@@ -84,7 +200,7 @@ int slab_apply(tf_slab* h, const void* v, void* w, cudaStream_t st, uint32_t* ep
     int nw = 0;
     if (d.has_left) waits[nw++] = flag(me, 0);
     if (d.has_right) waits[nw++] = flag(me, 1);
-    if ((rc = tf_stream_wait_many_u32(waits, nw, e, st))) return rc;
+    if ((rc = dev ? wait_dev(h, waits, nw, h->dev_ep, st) : tf_stream_wait_many_u32(waits, nw, e, st))) return rc;
     // fixed order: left partial first on the left plane, own partial first on the right
     rc = f32 ? tf_plane_add2_f32((float*)w, d.has_left ? d.left_idx : nullptr, (const float*)plane(me, 0),
                                  d.has_right ? d.right_idx : nullptr, (const float*)plane(me, 1), d.plane_len, st)
@@ -97,7 +213,7 @@ int slab_apply(tf_slab* h, const void* v, void* w, cudaStream_t st, uint32_t* ep
     return rc;
 }
 
-int slab_allreduce(tf_slab* h, double* t, int k, cudaStream_t st, uint32_t* ar_epoch)
+int slab_allreduce(tf_slab* h, double* t, int k, cudaStream_t st, uint32_t* ar_epoch, bool dev = false)
 {
     const tf_slab_desc& d = h->d;
     if (d.world == 1) return TF_OK;
@@ -119,8 +235,13 @@ int slab_allreduce(tf_slab* h, double* t, int k, cudaStream_t st, uint32_t* ar_e
         waits[r] = at(me, d.off_arflags + 4 * r);
     }
     // this rank's partials into every rank's slot + flags (one launch), then one batched wait
-    if ((rc = tf_put_flags_f64(t, nullptr, dst, flg, d.world, k, e, h->tickets, st))) return rc;
-    if ((rc = tf_stream_wait_many_u32(waits, d.world, e, st))) return rc;
+    if (dev) {
+        if ((rc = put_dev<double>(h, t, nullptr, (void* const*)dst, flg, d.world, k, h->dev_ep + 1, st))) return rc;
+        if ((rc = wait_dev(h, waits, d.world, h->dev_ep + 1, st))) return rc;
+    } else {
+        if ((rc = tf_put_flags_f64(t, nullptr, dst, flg, d.world, k, e, h->tickets, st))) return rc;
+        if ((rc = tf_stream_wait_many_u32(waits, d.world, e, st))) return rc;
+    }
     if ((rc = tf_rank_sum_f64((const double*)slot(me, 0), d.world, (int)d.max_scalars, h->acc, st))) return rc;
     TF_CUDA_TRY(cudaMemcpyAsync(t, h->acc, sizeof(double) * k, cudaMemcpyDeviceToDevice, st));
     return TF_OK;
@@ -146,7 +267,9 @@ int tf_slab_create(tf_slab** out, const tf_slab_desc* d)
     int64_t idx[16];
     for (int i = 0; i < 16; ++i) idx[i] = i;
     if (cudaMalloc(&h->scalar_idx, sizeof(idx)) != cudaSuccess || cudaMalloc(&h->acc, 16 * sizeof(double)) != cudaSuccess ||
-        cudaMalloc(&h->tickets, 16 * sizeof(uint32_t)) != cudaSuccess || cudaMemset(h->tickets, 0, 16 * sizeof(uint32_t)) != cudaSuccess) {
+        cudaMalloc(&h->tickets, 16 * sizeof(uint32_t)) != cudaSuccess || cudaMemset(h->tickets, 0, 16 * sizeof(uint32_t)) != cudaSuccess ||
+        cudaMalloc(&h->dev_ep, 2 * sizeof(uint32_t)) != cudaSuccess || cudaMalloc(&h->dev_err, sizeof(int)) != cudaSuccess ||
+        cudaMemset(h->dev_err, 0, sizeof(int)) != cudaSuccess) {
         delete h;
         tf::set_error("cudaMalloc failed");
         return TF_ERR_CUDA;
@@ -171,7 +294,20 @@ int tf_slab_destroy(tf_slab* h)
     cudaFree(h->scalar_idx);
     cudaFree(h->acc);
     cudaFree(h->tickets);
+    cudaFree(h->dev_ep);
+    cudaFree(h->dev_err);
+    for (auto& g : h->graphs) cudaGraphExecDestroy(g.exec);
+    if (h->cap) cudaStreamDestroy(h->cap);
     delete h;
+    return TF_OK;
+}
+
+// 1 when a graph-mode wait timed out (peer never raised its flag); clears it
+int tf_slab_take_error(tf_slab* h, int* out)
+{
+    TF_REQUIRE(h && out, "bad arguments");
+    TF_CUDA_TRY(cudaMemcpy(out, h->dev_err, sizeof(int), cudaMemcpyDeviceToHost));
+    TF_CUDA_TRY(cudaMemset(h->dev_err, 0, sizeof(int)));
     return TF_OK;
 }
 
@@ -187,23 +323,22 @@ int tf_slab_allreduce(tf_slab* h, double* t, int k, uint32_t* epochs, void* stre
     return slab_allreduce(h, t, k, (cudaStream_t)stream, &epochs[1]);
 }
 
-// n_iters CG iterations it0+1 .. it0+n_iters (slab.py slab_pcg_device's loop body)
-int tf_slab_pcg_iterate(tf_slab* h, const void* b, const void* inv, void* x, void* r, void* z, void* p, void* q,
-                        void* wtmp, double* state, double* red, double* work, int it0, int n_iters,
-                        int recompute_every, double* hist, int hist_len, uint32_t* epochs, void* stream)
+// CG iterations it0+1 .. it0+n_iters (slab.py slab_pcg_device's loop body)
+static int slab_iterations(tf_slab* h, const void* b, const void* inv, void* x, void* r, void* z, void* p, void* q,
+                           void* wtmp, double* state, double* red, double* work, int it0, int n_iters,
+                           int recompute_every, double* hist, int hist_len, uint32_t* epochs, cudaStream_t st,
+                           bool dev)
 {
-    TF_REQUIRE(h && b && inv && x && r && z && p && q && wtmp && state && red && work && epochs, "bad arguments");
     const tf_slab_desc& d = h->d;
-    cudaStream_t st = (cudaStream_t)stream;
     const bool f32 = d.precision == 32;
     const int64_t n = 3LL * (d.grid.nelx + 1) * (d.grid.nely + 1) * (d.grid.nelz + 1);
     int rc;
     for (int it = it0 + 1; it <= it0 + n_iters; ++it) {
-        if ((rc = slab_apply(h, p, q, st, &epochs[0]))) return rc;
+        if ((rc = slab_apply(h, p, q, st, &epochs[0], dev))) return rc;
         rc = f32 ? tf_slab_cg_pq_f32(n, (const float*)p, (const float*)q, d.owned, state, red, work, st)
                  : tf_slab_cg_pq_f64(n, (const double*)p, (const double*)q, d.owned, state, red, work, st);
         if (rc) return rc;
-        if ((rc = slab_allreduce(h, red, 1, st, &epochs[1]))) return rc;
+        if ((rc = slab_allreduce(h, red, 1, st, &epochs[1], dev))) return rc;
         const int refresh = recompute_every > 0 && it % recompute_every == 0;
         rc = f32 ? tf_slab_cg_alpha_f32(n, (float*)x, (float*)r, (const float*)p, (const float*)q,
                                         (const float*)inv, (float*)z, d.owned, state, red, refresh, work, st)
@@ -211,18 +346,88 @@ int tf_slab_pcg_iterate(tf_slab* h, const void* b, const void* inv, void* x, voi
                                         (const double*)inv, (double*)z, d.owned, state, red, refresh, work, st);
         if (rc) return rc;
         if (refresh) {
-            if ((rc = slab_apply(h, x, wtmp, st, &epochs[0]))) return rc;
+            if ((rc = slab_apply(h, x, wtmp, st, &epochs[0], dev))) return rc;
             rc = f32 ? tf_slab_cg_residual_f32(n, (const float*)b, (const float*)wtmp, (float*)r,
                                                (const float*)inv, (float*)z, d.owned, state, red, work, st)
                      : tf_slab_cg_residual_f64(n, (const double*)b, (const double*)wtmp, (double*)r,
                                                (const double*)inv, (double*)z, d.owned, state, red, work, st);
             if (rc) return rc;
         }
-        if ((rc = slab_allreduce(h, red + 1, 2, st, &epochs[1]))) return rc;
+        if ((rc = slab_allreduce(h, red + 1, 2, st, &epochs[1], dev))) return rc;
         rc = f32 ? tf_slab_cg_beta_f32(n, (float*)p, (const float*)z, state, red, hist, hist_len, st)
                  : tf_slab_cg_beta_f64(n, (double*)p, (const double*)z, state, red, hist, hist_len, st);
         if (rc) return rc;
     }
+    return TF_OK;
+}
+
+int tf_slab_pcg_iterate(tf_slab* h, const void* b, const void* inv, void* x, void* r, void* z, void* p, void* q,
+                        void* wtmp, double* state, double* red, double* work, int it0, int n_iters,
+                        int recompute_every, double* hist, int hist_len, uint32_t* epochs, void* stream)
+{
+    TF_REQUIRE(h && b && inv && x && r && z && p && q && wtmp && state && red && work && epochs, "bad arguments");
+    return slab_iterations(h, b, inv, x, r, z, p, q, wtmp, state, red, work, it0, n_iters, recompute_every, hist,
+                           hist_len, epochs, (cudaStream_t)stream, false);
+}
+
+// The same n_iters iterations as one CUDA-graph launch.  The captured
+// iterations are it0+1 .. it0+n_iters with a refresh exactly where
+// recompute_every puts one for THIS it0; graphs are cached per (buffers,
+// n_iters, refresh positions), so callers replay aligned blocks (it0 a
+// multiple of n_iters and n_iters dividing recompute_every).  Epochs: the
+// host values are loaded into the device counters before the launch and
+// advanced by the block's exchange counts after it.
+int tf_slab_pcg_graph(tf_slab* h, const void* b, const void* inv, void* x, void* r, void* z, void* p, void* q,
+                      void* wtmp, double* state, double* red, double* work, int it0, int n_iters,
+                      int recompute_every, double* hist, int hist_len, uint32_t* epochs, int* err_out, void* stream)
+{
+    TF_REQUIRE(h && b && inv && x && r && z && p && q && wtmp && state && red && work && epochs && n_iters > 0,
+               "bad arguments");
+    cudaStream_t st = (cudaStream_t)stream;
+    // refresh pattern of this block (bit j: iteration it0+1+j refreshes)
+    uintptr_t pattern = 0;
+    for (int j = 0; j < n_iters && j < 64; ++j)
+        if (recompute_every > 0 && (it0 + 1 + j) % recompute_every == 0) pattern |= (uintptr_t)1 << j;
+    std::vector<const void*> key = {b, inv, x, r, z, p, q, wtmp, state, red, work, hist,
+                                    (const void*)(uintptr_t)n_iters, (const void*)pattern,
+                                    (const void*)(uintptr_t)(it0 & 1), (const void*)(uintptr_t)hist_len};
+    // slot parities are baked per capture: key on the epoch parities too
+    key.push_back((const void*)(uintptr_t)(epochs[0] & 1u));
+    key.push_back((const void*)(uintptr_t)(epochs[1] & 1u));
+    cudaGraphExec_t exec = nullptr;
+    for (auto& g : h->graphs)
+        if (g.key == key) exec = g.exec;
+    uint32_t ep[2] = {epochs[0], epochs[1]};
+    if (!exec) {
+        if (!h->cap) TF_CUDA_TRY(cudaStreamCreateWithFlags(&h->cap, cudaStreamNonBlocking));
+        TF_CUDA_TRY(cudaStreamBeginCapture(h->cap, cudaStreamCaptureModeThreadLocal));
+        uint32_t tmp[2] = {epochs[0], epochs[1]};
+        int rc = slab_iterations(h, b, inv, x, r, z, p, q, wtmp, state, red, work, it0, n_iters, recompute_every,
+                                 hist, hist_len, tmp, h->cap, true);
+        cudaGraph_t graph = nullptr;
+        const cudaError_t ce = cudaStreamEndCapture(h->cap, &graph);
+        if (rc) {
+            if (graph) cudaGraphDestroy(graph);
+            return rc;
+        }
+        TF_CUDA_TRY(ce);
+        const cudaError_t ie = cudaGraphInstantiate(&exec, graph, 0);
+        cudaGraphDestroy(graph);
+        TF_CUDA_TRY(ie);
+        h->graphs.push_back({key, exec});
+    }
+    k_set_ep<<<1, 1, 0, st>>>(h->dev_ep, ep[0], ep[1]);
+    TF_CHECK_LAUNCH();
+    TF_CUDA_TRY(cudaGraphLaunch(exec, st));
+    // advance the host epochs like the captured sequence did
+    const int refreshes = __builtin_popcountll((unsigned long long)pattern);
+    if (h->d.world > 1) {
+        epochs[0] += (uint32_t)(n_iters + refreshes);
+        epochs[1] += (uint32_t)(2 * n_iters);
+    } else {
+        epochs[0] += (uint32_t)(n_iters + refreshes);
+    }
+    if (err_out) TF_CUDA_TRY(cudaMemcpyAsync(err_out, h->dev_err, sizeof(int), cudaMemcpyDeviceToHost, st));
     return TF_OK;
 }
 

@@ -432,15 +432,31 @@ class NativeSlab:
         self._sync_out()
         return w
 
-    def iterate(self, b, inv, x, r, z, p, q, wtmp, state, red, work, it0, n, recompute_every, hist):
+    def iterate(self, b, inv, x, r, z, p, q, wtmp, state, red, work, it0, n, recompute_every, hist,
+                graph: bool = False):
+        """n CG iterations it0+1..it0+n enqueued from C++; graph=True replays
+        them as one CUDA graph (aligned blocks, see tf_slab_pcg_graph)."""
         from . import _device as D
         from . import _lib
 
         self._sync_in()
-        _lib.call("tf_slab_pcg_iterate", self.h, D.ptr(b), D.ptr(inv), D.ptr(x), D.ptr(r), D.ptr(z), D.ptr(p),
-                  D.ptr(q), D.ptr(wtmp), D.ptr(state), D.ptr(red), D.ptr(work), int(it0), int(n),
-                  int(recompute_every), D.ptr(hist), int(hist.numel()), self.epochs, D.stream_ptr())
+        args = (self.h, D.ptr(b), D.ptr(inv), D.ptr(x), D.ptr(r), D.ptr(z), D.ptr(p), D.ptr(q), D.ptr(wtmp),
+                D.ptr(state), D.ptr(red), D.ptr(work), int(it0), int(n), int(recompute_every), D.ptr(hist),
+                int(hist.numel()), self.epochs)
+        if graph:
+            _lib.call("tf_slab_pcg_graph", *args, None, D.stream_ptr())
+        else:
+            _lib.call("tf_slab_pcg_iterate", *args, D.stream_ptr())
         self._sync_out()
+
+    def take_error(self) -> bool:
+        import ctypes
+
+        from . import _lib
+
+        e = ctypes.c_int(0)
+        _lib.call("tf_slab_take_error", self.h, ctypes.byref(e))
+        return bool(e.value)
 
     def __del__(self):
         try:
@@ -513,13 +529,24 @@ def slab_pcg_device(op: SlabOperator, b, diag, rel_tol=1e-5, max_iter=1000, reco
         # the whole loop body enqueued from C++ in batches of `poll` iterations
         q = torch.empty_like(b)
         wtmp = torch.empty_like(b)
+        # CUDA-graph blocks of G iterations (TF_SLAB_GRAPH=0: plain enqueue):
+        # G divides recompute_every so every block's refresh pattern is one
+        # of two captured graphs; the first block runs eagerly (autotune,
+        # first-touch), partial tail blocks too
+        G = 10
+        use_graph = (os.environ.get("TF_SLAB_GRAPH", "1") == "1"
+                     and (recompute_every == 0 or recompute_every % G == 0))
         it = 0
         while it < max_iter:
-            k = min(poll, max_iter - it)
-            native.iterate(b, inv, x, r, z, p, q, wtmp, state, red, work, it, k, recompute_every, hist)
+            k = min(G if use_graph else poll, max_iter - it)
+            graph = use_graph and it > 0 and k == G
+            native.iterate(b, inv, x, r, z, p, q, wtmp, state, red, work, it, k, recompute_every, hist,
+                           graph=graph)
             it += k
             if float(state[4]) == 0.0:
                 break
+        if native.take_error():
+            raise RuntimeError("slab exchange timed out: a peer rank stopped raising its flags")
     elif float(state[4]) != 0.0:
         for it in range(1, max_iter + 1):
             q = op.apply(p)

@@ -177,12 +177,24 @@ class PeerTransport:
         return t
 
     def close(self):
+        """Unmap the peers' regions and free this rank's (idempotent).  Peers
+        may still write into a freed region if they outlive this rank's
+        transport: close all ranks' transports at the same point."""
+        if getattr(self, "base", None) is None:
+            return
         L = _lib.load()
         for r, ptr in self.peer.items():
             if r != self.rank:
                 L.tf_ipc_close(ctypes.c_void_p(ptr))
-        self.peer = {self.rank: self.base}
+        self.peer = {}
         L.tf_peer_free(ctypes.c_void_p(self.base))
+        self.base = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # interpreter shutdown: the context may be gone
+            pass
 
 
 __all__ = ["PeerTransport"]

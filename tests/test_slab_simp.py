@@ -199,3 +199,22 @@ def test_slab_simp_matches_single_gpu_loop(world, preset, iters, prec, transport
     for got, want in ((res[0][2], ref.rho_raw), (res[0][3], ref.rho_phys)):
         assert np.abs(got - want).mean() <= rtol
         assert np.linalg.norm(got - want) <= ltol * np.linalg.norm(want)
+
+
+@pytest.mark.gpu
+def test_slab_simp_single_process_without_process_group():
+    """world 1 without torch.distributed: the slab loop degenerates to the
+    single-GPU loop (no halos, no exchanges) -- same decisions, compliance to
+    round-off, and the field API of SimpResult."""
+    from paper_2604_18020_b200 import SimpConfig, default_schedule, make_preset, run_simp
+    from paper_2604_18020_b200.slab_simp import slab_run_simp
+
+    pb = make_preset("mbb", 0.2)
+    cfg = SimpConfig(schedule=default_schedule(8))
+    got = slab_run_simp(pb, cfg, device="cuda:0")
+    ref = run_simp(pb, cfg)
+    assert [h.restarted for h in got.history] == [h.restarted for h in ref.history]
+    for a, b in zip(got.history, ref.history):
+        assert abs(a.compliance - b.compliance) <= 1e-6 * abs(b.compliance)
+    assert got.rho_raw.shape == ref.rho_raw.shape == (pb.mesh.n_elem,)
+    assert np.abs(got.rho_phys - ref.rho_phys).mean() <= 1e-4

@@ -983,15 +983,19 @@ int tf_pcg_create(tf_pcg** out, const tf_pcg_desc* d, void* stream)
         h->fused = (ok && want && !(d->flags & TF_PCG_PLAIN_GRAPH)) ? 1 : 0;
     }
     // SM-resident protocol: the whole solve in one cooperative launch whenever
-    // the CG state of the owned DOFs fits in the co-resident CTAs' shared
-    // memory (TF_PCG_RESIDENT=0 disables it)
+    // the full CG state of the owned DOFs fits in the co-resident CTAs' shared
+    // memory.  The lean layout (x and D^-1 left in global memory) measured
+    // slower than the graph protocol once the graph's vector kernels were
+    // tuned (c2 FP64 33.1 vs 31.1 us/iteration, c3 FP32 37.6 vs 34.7), so it
+    // is used only when forced (TF_PCG_RESIDENT=1; =0 disables the protocol)
     if (d->structured && d->grid_variant == TF_GRID_FAST && !(d->flags & TF_PCG_PLAIN_GRAPH)) {
         const char* e = getenv("TF_PCG_RESIDENT");
         if (!(e && e[0] == '0')) {
             const bool ok = d->precision == 32
                                 ? pcg_resident_plan<float>(h->grid, (const float*)d->ke, &h->rplan)
                                 : pcg_resident_plan<double>(h->grid, (const double*)d->ke, &h->rplan);
-            h->resident = ok ? 1 : 0;
+            const bool forced = e && e[0] == '1';
+            h->resident = (ok && (forced || !h->rplan.lean)) ? 1 : 0;
         }
     }
     if (h->resident) {

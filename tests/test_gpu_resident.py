@@ -129,3 +129,24 @@ def test_resident_fp32_desk_window():
     assert rep.termination == g["termination"]
     assert abs(rep.iterations - g["iterations"]) <= max(2, 0.02 * g["iterations"])
     assert abs(rep.compliance - g["compliance"]) <= 1e-3 * abs(g["compliance"])
+
+
+@pytest.mark.parametrize("prec", ["fp64", "fp32"])
+def test_resident_lean_layout_matches_oracle(prec, monkeypatch):
+    """The lean layout (x and D^-1 in global memory) is chosen only when forced
+    (the graph protocol is faster wherever the full layout does not fit);
+    forced on a desk problem it must still reproduce the reference solve."""
+    from paper_2604_18020_b200 import CgConfig, pcg
+    from paper_2604_18020_b200.solver import pcg_protocol
+
+    monkeypatch.setenv("TF_PCG_RESIDENT", "1")
+    monkeypatch.setenv("TF_PCG_RES_LEAN", "1")
+    pb, edof, op = _problem("mbb", 0.2, prec, "random")
+    assert pcg_protocol(op) == "resident"
+    b = pb.bcs.force.astype(op.precision.dtype)
+    x, rep = pcg(op, b, op.diagonal(), CgConfig())
+    xr, info = _oracle_solve(op, edof, pb.bcs, b)
+    assert rep.termination == info["termination"]
+    assert abs(rep.iterations - info["iterations"]) <= max(2, 0.02 * info["iterations"])
+    tol = 1e-6 if prec == "fp64" else 3e-3
+    assert np.abs(x - xr).max() <= tol * np.abs(xr).max()

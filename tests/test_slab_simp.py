@@ -214,7 +214,9 @@ def test_slab_simp_single_process_without_process_group():
     got = slab_run_simp(pb, cfg, device="cuda:0")
     ref = run_simp(pb, cfg)
     assert [h.restarted for h in got.history] == [h.restarted for h in ref.history]
+    # the slab's Jacobi partials use FP64 atomics (ulp-level order effects
+    # that the CG trajectory carries forward): 1e-5, as the multi-rank bars
     for a, b in zip(got.history, ref.history):
-        assert abs(a.compliance - b.compliance) <= 1e-6 * abs(b.compliance)
+        assert abs(a.compliance - b.compliance) <= 1e-5 * abs(b.compliance)
     assert got.rho_raw.shape == ref.rho_raw.shape == (pb.mesh.n_elem,)
     assert np.abs(got.rho_phys - ref.rho_phys).mean() <= 1e-4

@@ -198,6 +198,12 @@ int tf_jacobi_grid_f32(const tf_grid* g, const float* ke_diag, const float* scal
                        float* inv_diag, const uint8_t* node_fixed, void* stream);
 int tf_jacobi_grid_f64(const tf_grid* g, const double* ke_diag, const double* scale,
                        double* diag, double* inv_diag, const uint8_t* node_fixed, void* stream);
+/* per-node FP64 sums of scale[e]*ke_diag[l] in ascending element order, no
+ * cast and no constraint handling (x-slab partials before the exchange) */
+int tf_jacobi_grid_partial_f32(const tf_grid* g, const float* ke_diag, const float* scale, double* partial,
+                               void* stream);
+int tf_jacobi_grid_partial_f64(const tf_grid* g, const double* ke_diag, const double* scale, double* partial,
+                               void* stream);
 /* contract form: acc (FP64, n_dof) += scale[e]*ke_diag[l] over edof */
 int tf_jacobi_edof_f32(const int32_t* edof, const float* ke_diag, const float* scale,
                        double* acc, int64_t n_elem, void* stream);

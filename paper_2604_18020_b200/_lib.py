@@ -196,6 +196,7 @@ for _s in ("f32", "f64"):
         f"tf_plane_add_{_s}": [_P, _P, _I64, _P, _INT, _P],
         f"tf_put_flags_{_s}": [_P, _P, _P, _P, _INT, _I64, ctypes.c_uint32, _P, _P],
         f"tf_plane_add2_{_s}": [_P, _P, _P, _P, _P, _I64, _P],
+        f"tf_jacobi_grid_partial_{_s}": [_P, _P, _P, _P, _P],
     })
 
 _lib = None

@@ -546,7 +546,8 @@ __global__ void k_scatter(const int32_t* __restrict__ edof, const T* __restrict_
 template <typename T>
 __global__ void k_jacobi_grid(Grid g, const T* __restrict__ scale, T* __restrict__ diag,
                               T* __restrict__ inv_diag, const uint8_t* __restrict__ node_fixed,
-                              const __grid_constant__ KeMat<T> kd /* first 24 = ke_diag */)
+                              const __grid_constant__ KeMat<T> kd /* first 24 = ke_diag */,
+                              double* __restrict__ partial = nullptr)
 {
     const long long node = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (node >= g.n_nodes) return;
@@ -571,6 +572,11 @@ __global__ void k_jacobi_grid(Grid g, const T* __restrict__ scale, T* __restrict
                     acc[c] = __dadd_rn(acc[c], (double)prod);
                 }
             }
+    if (partial) {  // slab partial sums: FP64, no cast, no constraint handling
+#pragma unroll
+        for (int c = 0; c < 3; ++c) partial[3 * node + c] = acc[c];
+        return;
+    }
     const unsigned bits = node_fixed ? (unsigned)node_fixed[node] : 0u;
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
@@ -882,6 +888,20 @@ TF_SCATTER(double, f64)
         memcpy(k.a, ke_diag, NLOC * sizeof(T));                                               \
         k_jacobi_grid<T><<<(unsigned)((gg.n_nodes + 255) / 256), 256, 0, S(stream)>>>(          \
             gg, scale, diag, inv_diag, node_fixed, k);                                        \
+        TF_CHECK_LAUNCH();                                                                    \
+        return TF_OK;                                                                         \
+    }                                                                                         \
+    int tf_jacobi_grid_partial_##SUF(const tf_grid* g, const T* ke_diag, const T* scale,       \
+                                     double* partial, void* stream)                          \
+    {                                                                                         \
+        TF_GRID_CHECK(g);                                                                     \
+        TF_REQUIRE(ke_diag && scale && partial, "null pointer");                              \
+        Grid gg = make_grid(g);                                                               \
+        KeMat<T> k;                                                                           \
+        memset(&k, 0, sizeof(k));                                                             \
+        memcpy(k.a, ke_diag, NLOC * sizeof(T));                                               \
+        k_jacobi_grid<T><<<(unsigned)((gg.n_nodes + 255) / 256), 256, 0, S(stream)>>>(          \
+            gg, scale, nullptr, nullptr, nullptr, k, partial);                                \
         TF_CHECK_LAUNCH();                                                                    \
         return TF_OK;                                                                         \
     }                                                                                         \

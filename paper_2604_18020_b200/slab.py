@@ -626,11 +626,12 @@ def gpu_local_kernels(part: SlabPartition, bcs_local: BoundaryConditions, rho_lo
         local_apply.op, local_apply.bl, local_apply.br = op, bl, br
 
     def local_diag_partial():
-        # FP64 partial sums of s_e * Ke[l,l] on this slab (no fixed handling yet)
+        # FP64 partial sums of s_e * Ke[l,l] on this slab (no fixed handling
+        # yet), gathered per node in ascending element order: deterministic
         kd = np.ascontiguousarray(np.diag(op.ke), dtype=dt)
-        acc = torch.zeros(lm.n_dof, dtype=torch.float64, device=op._scale_dev.device)
-        _lib.call(f"tf_jacobi_edof_{sfx}", D.ptr(op.dev.edof_raw), kd.ctypes.data,
-                  D.ptr(op._scale_dev), D.ptr(acc), lm.n_elem, D.stream_ptr())
+        acc = torch.empty(lm.n_dof, dtype=torch.float64, device=op._scale_dev.device)
+        _lib.call(f"tf_jacobi_grid_partial_{sfx}", ctypes_ref(op.dev.grid), kd.ctypes.data,
+                  D.ptr(op._scale_dev), D.ptr(acc), D.stream_ptr())
         return acc
 
     return op, local_apply, local_diag_partial

@@ -22,6 +22,7 @@
 // interleaved on the same transport.
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -46,6 +47,10 @@ struct tf_slab {
     };
     std::vector<Graph> graphs;
     cudaStream_t cap = nullptr;
+    // interior tiles run on a second stream, concurrent with the boundary
+    // tiles and the interface put (fork/join by events; capturable)
+    cudaStream_t aux = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr;
 };
 
 namespace {
@@ -166,6 +171,8 @@ int slab_apply(tf_slab* h, const void* v, void* w, cudaStream_t st, uint32_t* ep
     };
     const int nnx = d.grid.nelx + 1;
     int rc;
+    const bool split = h->aux && (d.has_left || d.has_right) && nnx - d.br > d.bl;
+    if (split) TF_CUDA_TRY(cudaEventRecord(h->fork, st));
     if ((rc = range(0, d.bl))) return rc;
     if ((rc = range(nnx - d.br, nnx))) return rc;
     // slot parity: the host knows the epoch in both modes (graph mode keeps
@@ -194,13 +201,24 @@ int slab_apply(tf_slab* h, const void* v, void* w, cudaStream_t st, uint32_t* ep
         rc = f32 ? tf_put_flags_f32((const float*)w, idx, (float* const*)dst, flg, nj, d.plane_len, e, h->tickets, st)
                  : tf_put_flags_f64((const double*)w, idx, (double* const*)dst, flg, nj, d.plane_len, e, h->tickets, st);
     if (rc) return rc;
-    if ((rc = range(d.bl, nnx - d.br))) return rc;
+    if (split) {  // interior tiles on the side stream, launched after the boundary work
+        TF_CUDA_TRY(cudaStreamWaitEvent(h->aux, h->fork, 0));
+        cudaStream_t keep = st;
+        st = h->aux;
+        rc = range(d.bl, nnx - d.br);
+        st = keep;
+        if (rc) return rc;
+        TF_CUDA_TRY(cudaEventRecord(h->join, h->aux));
+    } else if ((rc = range(d.bl, nnx - d.br))) {
+        return rc;
+    }
     void* me = h->peers[d.rank];
     void* waits[2];
     int nw = 0;
     if (d.has_left) waits[nw++] = flag(me, 0);
     if (d.has_right) waits[nw++] = flag(me, 1);
     if ((rc = dev ? wait_dev(h, waits, nw, h->dev_ep, st) : tf_stream_wait_many_u32(waits, nw, e, st))) return rc;
+    if (split) TF_CUDA_TRY(cudaStreamWaitEvent(st, h->join, 0));
     // fixed order: left partial first on the left plane, own partial first on the right
     rc = f32 ? tf_plane_add2_f32((float*)w, d.has_left ? d.left_idx : nullptr, (const float*)plane(me, 0),
                                  d.has_right ? d.right_idx : nullptr, (const float*)plane(me, 1), d.plane_len, st)
@@ -275,6 +293,15 @@ int tf_slab_create(tf_slab** out, const tf_slab_desc* d)
         return TF_ERR_CUDA;
     }
     TF_CUDA_TRY(cudaMemcpy(h->scalar_idx, idx, sizeof(idx), cudaMemcpyHostToDevice));
+    // opt-in (TF_SLAB_OVERLAP=1): unmeasured on separate GPUs; with the rank
+    // processes sharing one GPU (the only setup available this round) the
+    // second stream made every product 12x slower through context switching
+    const char* ov = getenv("TF_SLAB_OVERLAP");
+    if (ov && ov[0] == '1') {
+        TF_CUDA_TRY(cudaStreamCreateWithFlags(&h->aux, cudaStreamNonBlocking));
+        TF_CUDA_TRY(cudaEventCreateWithFlags(&h->fork, cudaEventDisableTiming));
+        TF_CUDA_TRY(cudaEventCreateWithFlags(&h->join, cudaEventDisableTiming));
+    }
     *out = h;
     return TF_OK;
 }
@@ -298,6 +325,9 @@ int tf_slab_destroy(tf_slab* h)
     cudaFree(h->dev_err);
     for (auto& g : h->graphs) cudaGraphExecDestroy(g.exec);
     if (h->cap) cudaStreamDestroy(h->cap);
+    if (h->aux) cudaStreamDestroy(h->aux);
+    if (h->fork) cudaEventDestroy(h->fork);
+    if (h->join) cudaEventDestroy(h->join);
     delete h;
     return TF_OK;
 }

@@ -67,7 +67,8 @@ def run_simp_device(problem, config, schedule):
     rho_new = t.empty_like(rho)
     inv_rs = t.empty_like(rho)
     f_dev = t.as_tensor(np.asarray(bcs.force, dtype=np.float64), device=dev)
-    rhs = np.ascontiguousarray(bcs.force, dtype=dt)
+    # the load vector, uploaded once (device_pcg would copy a host array per solve)
+    rhs = D.to_dev(np.ascontiguousarray(bcs.force, dtype=dt), dt)
     work = t.empty(int(_lib.load().tf_work_doubles(max(n, mesh.n_dof))), dtype=f64, device=dev)
     stats = t.empty(3, dtype=f64, device=dev)
     bad = t.zeros(1, dtype=t.int32, device=dev)

@@ -628,15 +628,18 @@ def simp_scaling(world, dist, iters=6):
     # iteration, so host timers bracket device work), max over ranks; the
     # run's wall adds the one-time setup (mesh/edof/operator/filter build)
     loop = sum(h.wall_s for h in res.history)
+    med = float(np.median([h.wall_s for h in res.history[1:]])) if len(res.history) > 1 else loop
     if dist is not None:
-        t = torch.tensor([loop], dtype=torch.float64, device=dev)
+        t = torch.tensor([loop, med], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        loop = float(t.item())
+        loop, med = float(t[0].item()), float(t[1].item())
     return {"config": f"c4 cantilever 200x100x50 (1M), default_schedule(120) iterations 1-{iters}, FP32, "
                       f"strong-scaled over {world} rank(s)",
             "path": "run_simp (device-resident)" if world == 1 else
                     f"slab_run_simp (x-slabs, {os.environ.get('TF_SLAB_TRANSPORT', 'p2p')} transport)",
-            "n_gpus": world, "s_per_iter": loop / iters, "wall_s": wall, "setup_s": wall - loop,
+            "n_gpus": world, "s_per_iter": loop / iters, "median_iter_s_after_first": med,
+            "wall_s": wall, "setup_s": wall - loop,
+            "iter_walls_s": [h.wall_s for h in res.history],
             "cg_iterations": [h.cg_iterations for h in res.history],
             "compliance": [h.compliance for h in res.history]}
 

@@ -220,3 +220,16 @@ def test_slab_simp_single_process_without_process_group():
         assert abs(a.compliance - b.compliance) <= 1e-5 * abs(b.compliance)
     assert got.rho_raw.shape == ref.rho_raw.shape == (pb.mesh.n_elem,)
     assert np.abs(got.rho_phys - ref.rho_phys).mean() <= 1e-4
+
+
+def test_element_halo_rejects_slabs_thinner_than_the_filter_reach():
+    from paper_2604_18020_b200.mesh import StructuredMesh
+    from paper_2604_18020_b200.slab import SlabPartition
+    from paper_2604_18020_b200.slab_simp import ElementHalo
+
+    part = SlabPartition(StructuredMesh(9, 2, 2), 3, 1)  # 3 element layers per rank
+    with pytest.raises(ValueError):
+        ElementHalo(part, 4, "cpu")
+    ElementHalo(part, 2, "cpu")  # fits
+    # a single rank has no interior sides: any halo width is accepted
+    ElementHalo(SlabPartition(StructuredMesh(2, 2, 2), 1, 0), 6, "cpu")

@@ -257,3 +257,29 @@ def test_short_schedule_runs_through_like_reference():
     assert [h.restarted for h in res.history] == g["restarted"]
     for v in (h.volume for h in res.history):
         assert abs(v - 0.3) <= 1e-6
+
+
+def test_projected_volume_simp_matches_reference():
+    """volume_on="projected" (the host-side filter/OC variant, reference
+    simp.py:393-401) on the desk cantilever through the beta continuation:
+    golden from tests/golden/make_golden_projected.py."""
+    import json
+
+    from conftest import GOLDEN
+    from paper_2604_18020_b200 import SimpConfig, default_schedule, make_preset, run_simp
+
+    g = json.loads((GOLDEN / "simp_projected.json").read_text())
+    res = run_simp(make_preset("cantilever", 0.2), SimpConfig(schedule=default_schedule(12), volume_on="projected"))
+    c = np.array([h.compliance for h in res.history])
+    np.testing.assert_allclose(c, g["compliance"], rtol=1e-4)
+    assert [h.restarted for h in res.history] == g["restarted"]
+    # the recorded volume is the raw mean; the bisection only pins the
+    # PROJECTED mean (to 1e-6), so the raw mean carries the CG round-off more
+    np.testing.assert_allclose([h.volume for h in res.history], g["volume"], rtol=1e-3)
+    # warm-started solves right after a beta jump are hypersensitive to
+    # round-off (step 5: 481 vs 392 here, compliance still within 1e-4; the
+    # same effect as the cantilever's 164 vs 187 between our own two CG
+    # protocols, tests/test_slab_simp.py): total CG within 15 %
+    its = np.array([h.cg_iterations for h in res.history])
+    assert abs(its.sum() - sum(g["cg_iterations"])) <= 0.15 * sum(g["cg_iterations"])
+    assert abs(float(res.rho_phys.mean()) - g["rho_phys_mean"]) <= 1e-4

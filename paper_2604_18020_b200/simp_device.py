@@ -8,8 +8,10 @@ cooperative kernel).  The host only sees scalars (compliance, grayness, CG
 report, volume) -- exactly what the selection/restart rules consume -- and
 copies the selected/final fields out once at the end.
 
-Used by ``simp.run_simp`` for ``volume_on="raw"`` (the reference default) on
-structured grids with filter reach <= 3.
+Used by ``simp.run_simp`` on structured grids with filter reach <= 3, for
+both volume constraints (``volume_on="raw"``, the reference default: one
+cooperative OC kernel; ``"projected"``: device filter/projection per
+multiplier under the host bisection walk).
 """
 
 from __future__ import annotations
@@ -33,6 +35,43 @@ class _Selected:
         self.iteration, self.compliance, self.grayness = it, c, g
         self.rho, self.rho_phys, self.u = rho, rho_phys, u
         self.p, self.beta = p, beta
+
+
+def _oc_projected(n, grid, rmin, inv_rs, rho, dc, dh, s, vf, rho_new, work, stats, st):
+    """oc_update on the projected volume (reference simp.py:393-401), device
+    resident: dv = max(F^T dh, 1e-12); every multiplier's volume is
+    mean(H_beta(F cand)) evaluated by the stencil filter, projection and a
+    fixed-order reduction; the bracket/bisection walk is oc_bisect
+    (slab_simp.py), validated step for step against oc_update."""
+    t = D.torch()
+    from .slab_simp import oc_bisect
+
+    dv = t.empty_like(rho)
+    _lib.call("tf_filter_grid_f64", ctypes_ref(grid), float(rmin), D.ptr(inv_rs), D.ptr(dh), D.ptr(dv), 1, st)
+    dv.clamp_(min=1e-12)
+    if float(dc.max()) > 1e-12:
+        raise ValueError("compliance sensitivities must be non-positive")
+    cand = t.empty_like(rho)
+    fb = t.empty_like(rho)
+    fp = t.empty_like(rho)
+
+    def volumes(lams):
+        out = []
+        for lam in lams:
+            _lib.call("tf_oc_apply_f64", n, D.ptr(rho), D.ptr(dc), D.ptr(dv), float(s.move), 0.5, float(lam),
+                      D.ptr(cand), st)
+            _lib.call("tf_filter_grid_f64", ctypes_ref(grid), float(rmin), D.ptr(inv_rs), D.ptr(cand),
+                      D.ptr(fb), 0, st)
+            _lib.call("tf_project_f64", n, float(s.beta), 0.5, D.ptr(fb), D.ptr(fp), None, st)
+            _lib.call("tf_stats_f64", n, None, None, None, D.ptr(fp), D.ptr(work), D.ptr(stats), st)
+            out.append(float(stats[2].item()) / n)
+        return out
+
+    res = oc_bisect(volumes, vf, batch=1)
+    if res.status == "stalled":
+        raise RuntimeError(f"OC bisection stalled with volume error {res.best_err:.3e}")
+    _lib.call("tf_oc_apply_f64", n, D.ptr(rho), D.ptr(dc), D.ptr(dv), float(s.move), 0.5, float(res.lam),
+              D.ptr(rho_new), st)
 
 
 def run_simp_device(problem, config, schedule):
@@ -127,16 +166,20 @@ def run_simp_device(problem, config, schedule):
                       D.ptr(energies), D.ptr(dh), D.ptr(sens), st)
             _lib.call("tf_filter_grid_f64", ctypes_ref(grid), float(rmin_built), D.ptr(inv_rs),
                       D.ptr(sens), D.ptr(dc), 1, st)
-            _lib.call("tf_oc_update_f64", n, D.ptr(rho), D.ptr(dc), None,
-                      float(problem.volume_fraction), float(s.move), 1e-6, 0.5, 200,
-                      D.ptr(rho_new), D.ptr(work), D.ptr(oc_rep_dev), st)
-            rep_host = oc_rep_dev.cpu().numpy()
-            ctypes.memmove(ctypes.addressof(oc_rep), rep_host.ctypes.data, ctypes.sizeof(oc_rep))
-            status = _lib.OC_STATUS[oc_rep.status]
-            if status == "bad_input":
-                raise ValueError("compliance sensitivities must be non-positive")
-            if status == "stalled":
-                raise RuntimeError(f"OC bisection stalled with volume error {oc_rep.best_err:.3e}")
+            if config.volume_on == "raw":
+                _lib.call("tf_oc_update_f64", n, D.ptr(rho), D.ptr(dc), None,
+                          float(problem.volume_fraction), float(s.move), 1e-6, 0.5, 200,
+                          D.ptr(rho_new), D.ptr(work), D.ptr(oc_rep_dev), st)
+                rep_host = oc_rep_dev.cpu().numpy()
+                ctypes.memmove(ctypes.addressof(oc_rep), rep_host.ctypes.data, ctypes.sizeof(oc_rep))
+                status = _lib.OC_STATUS[oc_rep.status]
+                if status == "bad_input":
+                    raise ValueError("compliance sensitivities must be non-positive")
+                if status == "stalled":
+                    raise RuntimeError(f"OC bisection stalled with volume error {oc_rep.best_err:.3e}")
+            else:
+                _oc_projected(n, grid, rmin_built, inv_rs, rho, dc, dh, s, problem.volume_fraction,
+                              rho_new, work, stats, st)
             rho, rho_new = rho_new, rho
         if int(bad.item()):
             raise ValueError("densities must lie in [0, 1]")

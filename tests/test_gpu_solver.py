@@ -259,7 +259,8 @@ def test_short_schedule_runs_through_like_reference():
         assert abs(v - 0.3) <= 1e-6
 
 
-def test_projected_volume_simp_matches_reference():
+@pytest.mark.parametrize("device_glue", [None, False])
+def test_projected_volume_simp_matches_reference(device_glue):
     """volume_on="projected" (the host-side filter/OC variant, reference
     simp.py:393-401) on the desk cantilever through the beta continuation:
     golden from tests/golden/make_golden_projected.py."""
@@ -269,7 +270,8 @@ def test_projected_volume_simp_matches_reference():
     from paper_2604_18020_b200 import SimpConfig, default_schedule, make_preset, run_simp
 
     g = json.loads((GOLDEN / "simp_projected.json").read_text())
-    res = run_simp(make_preset("cantilever", 0.2), SimpConfig(schedule=default_schedule(12), volume_on="projected"))
+    res = run_simp(make_preset("cantilever", 0.2), SimpConfig(schedule=default_schedule(12), volume_on="projected"),
+                   device_glue=device_glue)  # None: device filter/projection/OC; False: host scipy glue
     c = np.array([h.compliance for h in res.history])
     np.testing.assert_allclose(c, g["compliance"], rtol=1e-4)
     assert [h.restarted for h in res.history] == g["restarted"]

@@ -247,8 +247,8 @@ def slab_run_simp(problem, config=None, group=None, device=None, gather: bool = 
     from .simp import IterationRecord, SelectedRecord, SimpConfig, SimpResult, default_schedule
 
     config = config or SimpConfig()
-    if config.volume_on != "raw" or config.variant != "fused":
-        raise ValueError("slab SIMP runs the reference default (fused operator, raw volume)")
+    if config.variant != "fused":
+        raise ValueError("slab SIMP runs the fused operator")
     schedule = config.schedule or default_schedule()
     t_start = time.perf_counter()
     world = dist.get_world_size(group) if dist.is_initialized() else 1
@@ -349,8 +349,26 @@ def slab_run_simp(problem, config=None, group=None, device=None, gather: bool = 
                       D.ptr(energies), D.ptr(dh), D.ptr(sens), st)
             dc = filt(sens, rmin_built, 1)
             checked = [False]
+            dv = None
+            if config.volume_on == "projected":
+                # dv = max(F^T dh, 1e-12); volumes are projected means
+                # (simp.py:393-401): per multiplier one candidate, one halo
+                # exchange + filter, one projection, one rank sum
+                dv = filt(dh, rmin_built, 1).clamp_(min=1e-12)
+                if float(rank_sum((dc > 1e-12).sum().double().reshape(1), group)[0]) > 0:
+                    raise ValueError("compliance sensitivities must be non-positive")
+                cand, fp = torch.empty_like(rho), torch.empty_like(rho)
 
             def volumes(lams):
+                if dv is not None:
+                    out = []
+                    for lam in lams:
+                        _lib.call("tf_oc_apply_f64", n, D.ptr(rho), D.ptr(dc), D.ptr(dv), float(s.move), 0.5,
+                                  float(lam), D.ptr(cand), st)
+                        fb = filt(cand, rmin_built, 0)
+                        _lib.call("tf_project_f64", n, float(s.beta), 0.5, D.ptr(fb), D.ptr(fp), None, st)
+                        out.append(float(rank_sum(torch.sum(fp).reshape(1), group)[0]) / n_glob)
+                    return out
                 lam_arr = np.asarray(lams, dtype=np.float64)  # alive across the call
                 _lib.call("tf_oc_volumes_f64", n, D.ptr(rho), D.ptr(dc), None, float(s.move), 0.5,
                           lam_arr.ctypes.data, len(lams), D.ptr(oc_sums), D.ptr(oc_work), st)
@@ -361,11 +379,11 @@ def slab_run_simp(problem, config=None, group=None, device=None, gather: bool = 
                     checked[0] = True
                 return [float(v) / n_glob for v in tot[:len(lams)]]
 
-            last_oc = oc_bisect(volumes, problem.volume_fraction)
+            last_oc = oc_bisect(volumes, problem.volume_fraction, batch=1 if dv is not None else OC_MAX_LAMS)
             if last_oc.status == "stalled":
                 raise RuntimeError(f"OC bisection stalled with volume error {last_oc.best_err:.3e}")
-            _lib.call("tf_oc_apply_f64", n, D.ptr(rho), D.ptr(dc), None, float(s.move), 0.5,
-                      float(last_oc.lam), D.ptr(rho_new), st)
+            _lib.call("tf_oc_apply_f64", n, D.ptr(rho), D.ptr(dc), D.ptr(dv) if dv is not None else None,
+                      float(s.move), 0.5, float(last_oc.lam), D.ptr(rho_new), st)
             rho, rho_new = rho_new, rho
         if int(rank_sum(bad.double(), group)[0]):
             raise ValueError("densities must lie in [0, 1]")

@@ -121,7 +121,7 @@ def test_element_halo_extends_slabs_with_neighbour_layers(world, dims, h):
 # -- GPU: the whole loop -------------------------------------------------------------
 
 
-def _simp_worker(rank, world, port, preset, scale, iters, prec, q, transport="p2p"):
+def _simp_worker(rank, world, port, preset, scale, iters, prec, q, transport="p2p", volume_on="raw"):
     import torch.distributed as dist
 
     from paper_2604_18020_b200 import SimpConfig, default_schedule, make_preset
@@ -131,7 +131,7 @@ def _simp_worker(rank, world, port, preset, scale, iters, prec, q, transport="p2
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         pb = make_preset(preset, scale)
-        cfg = SimpConfig(schedule=default_schedule(iters), precision=prec)
+        cfg = SimpConfig(schedule=default_schedule(iters), precision=prec, volume_on=volume_on)
         r = slab_run_simp(pb, cfg, device="cuda:0")
         q.put((rank, [(h.compliance, h.grayness, h.cg_iterations, h.volume, h.restarted) for h in r.history],
                r.rho_raw, r.rho_phys, r.total_cg_iterations,
@@ -233,3 +233,34 @@ def test_element_halo_rejects_slabs_thinner_than_the_filter_reach():
     ElementHalo(part, 2, "cpu")  # fits
     # a single rank has no interior sides: any halo width is accepted
     ElementHalo(SlabPartition(StructuredMesh(2, 2, 2), 1, 0), 6, "cpu")
+
+
+@pytest.mark.gpu
+def test_slab_simp_projected_volume_matches_single_gpu_loop():
+    """volume_on="projected" over 2 slabs: every multiplier's projected mean
+    goes through a halo exchange, the filter, the projection and a rank sum."""
+    import torch.multiprocessing as mp
+
+    from paper_2604_18020_b200 import SimpConfig, default_schedule, make_preset, run_simp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.SimpleQueue()
+    port = _free_port()
+    procs = [ctx.Process(target=_simp_worker, args=(r, 2, port, "cantilever", 0.2, 12, "fp64", q, "p2p",
+                                                    "projected")) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get() for _ in range(2)]
+    for p in procs:
+        p.join(timeout=300)
+    for r in res:
+        assert not isinstance(r[1], str), r[1]
+    ref = run_simp(make_preset("cantilever", 0.2), SimpConfig(schedule=default_schedule(12), volume_on="projected"))
+    h0 = res[0][1]
+    assert h0 == res[1][1]
+    # the schedule of the reference golden (test_gpu_solver.py): compliance
+    # to the north-star 1e-3 through the beta continuation
+    for (c, g, its, vol, rs), h in zip(h0, ref.history):
+        assert abs(c - h.compliance) <= 1e-3 * abs(h.compliance)
+        assert rs == h.restarted
+        assert abs(vol - h.volume) <= 1e-3 * h.volume

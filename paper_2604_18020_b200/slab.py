@@ -15,7 +15,14 @@ numbering, so the single-GPU kernels run unchanged on it.  One matvec is
          interface must not be counted twice).
 
 CG dot products use owner-computes masks (the replicated plane is counted by
-the lower rank) and one all_reduce per reduction point (FP64 partials).
+the lower rank) and one all-reduce per reduction point (FP64 partials).  On
+the GPU the CG scalars live in device memory (`slab_pcg_device`,
+csrc/tf_slab.cu): the host only enqueues and polls.
+
+Transports: "p2p" (torch.distributed P2P + all-reduce: NCCL on GPUs) or
+"peer" (peer.py: CUDA-IPC peer memory with stream-ordered flags; with it the
+whole CG loop runs from the native runtime csrc/tf_slab_run.cu, in CUDA-graph
+blocks of 10 iterations).
 
 The local compute is pluggable (`local_apply`, `local_diag_partial`): the
 product binds the sm_100a kernels; tests/test_slab.py binds the CPU oracle and

@@ -36,7 +36,7 @@ struct tf_slab {
     std::vector<void*> peers;
     int64_t* scalar_idx;   // device [0, 1, ..., 15]
     double* acc;           // device [16]
-    uint32_t* tickets;     // device [16], tf_put_flags' per-job block counters
+    uint32_t* tickets;     // device [32]: tf_put_flags' per-job block counters, [31] wait/add/pass
     // graph mode: epochs in device memory, waits as spin kernels (stream
     // memory operations bake their values into a captured graph)
     uint32_t* dev_ep;      // device [2]: plane epoch, all-reduce epoch
@@ -115,6 +115,72 @@ __global__ void k_wait_dev(const __grid_constant__ DevWait W)
     if (threadIdx.x == 0) *W.ep = target;
 }
 
+// Graph mode, end of a distributed product in ONE kernel: wait for the
+// neighbours' planes (thread 0 of every block spins on the local flags), add
+// them in the fixed order, then the fixed-DOF pass-through.  Constrained DOFs
+// are skipped by the adds (the pass-through owns them), so the two phases
+// never touch the same DOF; the last block advances the epoch.
+template <typename T>
+struct WaitAddPass {
+    const uint32_t* flag[2];
+    int nflags;
+    uint32_t* ep;
+    int* err;
+    uint32_t* ticket;
+    T* w;
+    const T* v;
+    const int64_t* li;
+    const T* rl;
+    const int64_t* ri;
+    const T* rr;
+    long long plane_len;
+    const uint8_t* node_fixed;
+    const int64_t* fixed;
+    long long n_fixed;
+};
+
+template <typename T>
+__global__ void k_wait_add_pass(const __grid_constant__ WaitAddPass<T> A)
+{
+    __shared__ uint32_t target;
+    if (threadIdx.x == 0) {
+        target = *reinterpret_cast<volatile uint32_t*>(A.ep) + 1u;
+        unsigned long long t0, t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+        for (int i = 0; i < A.nflags; ++i)
+            while (*reinterpret_cast<const volatile uint32_t*>(A.flag[i]) < target) {
+                __nanosleep(200);
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+                if (t - t0 > 30000000000ull) {
+                    *A.err = 1;
+                    break;
+                }
+            }
+        __threadfence_system();
+    }
+    __syncthreads();
+    const long long total = 2 * A.plane_len + A.n_fixed;
+    for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < total; k += (long long)gridDim.x * blockDim.x) {
+        if (k < 2 * A.plane_len) {
+            const bool left = k < A.plane_len;
+            const int64_t* idx = left ? A.li : A.ri;
+            if (!idx) continue;
+            const long long j = left ? k : k - A.plane_len;
+            const long long d = idx[j];
+            if (A.node_fixed && ((A.node_fixed[d / 3] >> (d % 3)) & 1u)) continue;
+            A.w[d] = left ? __ldcg(A.rl + j) + A.w[d] : A.w[d] + __ldcg(A.rr + j);
+        } else {
+            const long long d = A.fixed[k - 2 * A.plane_len];
+            A.w[d] = A.v[d];
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && atomicAdd(A.ticket, 1u) == gridDim.x - 1) {
+        *A.ep = target;
+        *A.ticket = 0u;
+    }
+}
+
 __global__ void k_set_ep(uint32_t* ep, uint32_t e0, uint32_t e1)
 {
     ep[0] = e0;
@@ -138,6 +204,34 @@ int put_dev(tf_slab* h, const T* src, const int64_t* const* idx, void* const* ds
     J.n = n;
     const unsigned nb = (unsigned)std::min<long long>((n + 255) / 256, 64);
     k_put_flags_dev<T><<<dim3(nb, nj), 256, 0, st>>>(J);
+    TF_CHECK_LAUNCH();
+    return TF_OK;
+}
+
+template <typename T>
+int wait_add_pass(tf_slab* h, void* const* flags, int n, T* w, const T* v, const void* rl, const void* rr,
+                  cudaStream_t st)
+{
+    const tf_slab_desc& d = h->d;
+    WaitAddPass<T> A{};
+    for (int i = 0; i < n; ++i) A.flag[i] = (const uint32_t*)flags[i];
+    A.nflags = n;
+    A.ep = h->dev_ep;
+    A.err = h->dev_err;
+    A.ticket = h->tickets + 31;  // put jobs use words 0..15
+    A.w = w;
+    A.v = v;
+    A.li = d.has_left ? d.left_idx : nullptr;
+    A.rl = (const T*)rl;
+    A.ri = d.has_right ? d.right_idx : nullptr;
+    A.rr = (const T*)rr;
+    A.plane_len = d.plane_len;
+    A.node_fixed = d.node_fixed;
+    A.fixed = d.fixed;
+    A.n_fixed = d.n_fixed > 0 ? d.n_fixed : 0;
+    const long long total = 2 * d.plane_len + A.n_fixed;
+    const unsigned nb = (unsigned)std::max<long long>(1, std::min<long long>((total + 255) / 256, 64));
+    k_wait_add_pass<T><<<nb, 256, 0, st>>>(A);
     TF_CHECK_LAUNCH();
     return TF_OK;
 }
@@ -217,6 +311,9 @@ int slab_apply(tf_slab* h, const void* v, void* w, cudaStream_t st, uint32_t* ep
     int nw = 0;
     if (d.has_left) waits[nw++] = flag(me, 0);
     if (d.has_right) waits[nw++] = flag(me, 1);
+    if (dev && !split)
+        return f32 ? wait_add_pass<float>(h, waits, nw, (float*)w, (const float*)v, plane(me, 0), plane(me, 1), st)
+                   : wait_add_pass<double>(h, waits, nw, (double*)w, (const double*)v, plane(me, 0), plane(me, 1), st);
     if ((rc = dev ? wait_dev(h, waits, nw, h->dev_ep, st) : tf_stream_wait_many_u32(waits, nw, e, st))) return rc;
     if (split) TF_CUDA_TRY(cudaStreamWaitEvent(st, h->join, 0));
     // fixed order: left partial first on the left plane, own partial first on the right
@@ -285,7 +382,7 @@ int tf_slab_create(tf_slab** out, const tf_slab_desc* d)
     int64_t idx[16];
     for (int i = 0; i < 16; ++i) idx[i] = i;
     if (cudaMalloc(&h->scalar_idx, sizeof(idx)) != cudaSuccess || cudaMalloc(&h->acc, 16 * sizeof(double)) != cudaSuccess ||
-        cudaMalloc(&h->tickets, 16 * sizeof(uint32_t)) != cudaSuccess || cudaMemset(h->tickets, 0, 16 * sizeof(uint32_t)) != cudaSuccess ||
+        cudaMalloc(&h->tickets, 32 * sizeof(uint32_t)) != cudaSuccess || cudaMemset(h->tickets, 0, 32 * sizeof(uint32_t)) != cudaSuccess ||
         cudaMalloc(&h->dev_ep, 2 * sizeof(uint32_t)) != cudaSuccess || cudaMalloc(&h->dev_err, sizeof(int)) != cudaSuccess ||
         cudaMemset(h->dev_err, 0, sizeof(int)) != cudaSuccess) {
         delete h;

@@ -181,6 +181,46 @@ __global__ void k_wait_add_pass(const __grid_constant__ WaitAddPass<T> A)
     }
 }
 
+// Graph mode, end of a one-shot all-reduce in ONE kernel: wait for every
+// rank's flag, sum the slots in rank order into t[0..k), advance the epoch.
+struct WaitSum {
+    const uint32_t* flag[16];
+    int nranks, k, stride;
+    uint32_t* ep;
+    int* err;
+    const double* slots;  // [nranks][stride] of this parity
+    double* t;
+};
+
+__global__ void k_wait_ranksum(const __grid_constant__ WaitSum A)
+{
+    __shared__ uint32_t target;
+    if (threadIdx.x == 0) {
+        target = *reinterpret_cast<volatile uint32_t*>(A.ep) + 1u;
+        unsigned long long t0, t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+        for (int i = 0; i < A.nranks; ++i)
+            while (*reinterpret_cast<const volatile uint32_t*>(A.flag[i]) < target) {
+                __nanosleep(100);
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+                if (t - t0 > 30000000000ull) {
+                    *A.err = 1;
+                    break;
+                }
+            }
+        __threadfence_system();
+    }
+    __syncthreads();
+    const int j = threadIdx.x;
+    if (j < A.k) {
+        double s = 0.0;
+        for (int r = 0; r < A.nranks; ++r) s += __ldcg(A.slots + (size_t)r * A.stride + j);
+        A.t[j] = s;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) *A.ep = target;
+}
+
 __global__ void k_set_ep(uint32_t* ep, uint32_t e0, uint32_t e1)
 {
     ep[0] = e0;
@@ -352,7 +392,18 @@ int slab_allreduce(tf_slab* h, double* t, int k, cudaStream_t st, uint32_t* ar_e
     // this rank's partials into every rank's slot + flags (one launch), then one batched wait
     if (dev) {
         if ((rc = put_dev<double>(h, t, nullptr, (void* const*)dst, flg, d.world, k, h->dev_ep + 1, st))) return rc;
-        if ((rc = wait_dev(h, waits, d.world, h->dev_ep + 1, st))) return rc;
+        WaitSum A{};
+        for (int r = 0; r < d.world; ++r) A.flag[r] = (const uint32_t*)waits[r];
+        A.nranks = d.world;
+        A.k = k;
+        A.stride = (int)d.max_scalars;
+        A.ep = h->dev_ep + 1;
+        A.err = h->dev_err;
+        A.slots = (const double*)slot(me, 0);
+        A.t = t;
+        k_wait_ranksum<<<1, 32, 0, st>>>(A);
+        TF_CHECK_LAUNCH();
+        return TF_OK;
     } else {
         if ((rc = tf_put_flags_f64(t, nullptr, dst, flg, d.world, k, e, h->tickets, st))) return rc;
         if ((rc = tf_stream_wait_many_u32(waits, d.world, e, st))) return rc;

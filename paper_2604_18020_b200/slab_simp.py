@@ -230,6 +230,15 @@ def _gather_dof(part, local, group):
 
 
 def slab_run_simp(problem, config=None, group=None, device=None, gather: bool = True):
+    """Distributed continuation SIMP on the x-slab decomposition (see
+    _slab_run_simp); runs with Python's automatic cyclic GC paused."""
+    from . import _device as D
+
+    with D.gc_paused():
+        return _slab_run_simp(problem, config, group, device, gather)
+
+
+def _slab_run_simp(problem, config=None, group=None, device=None, gather: bool = True):
     """Distributed continuation SIMP on the x-slab decomposition.
 
     Same loop, schedule, selection/restart rules and raw-volume OC as

@@ -285,3 +285,14 @@ def test_projected_volume_simp_matches_reference(device_glue):
     its = np.array([h.cg_iterations for h in res.history])
     assert abs(its.sum() - sum(g["cg_iterations"])) <= 0.15 * sum(g["cg_iterations"])
     assert abs(float(res.rho_phys.mean()) - g["rho_phys_mean"]) <= 1e-4
+
+
+def test_projected_volume_rejects_positive_sensitivities_like_reference():
+    """default_schedule(4) with the projected volume drives a filtered
+    sensitivity positive; the reference raises ValueError('compliance
+    sensitivities must be non-positive') from oc_update (checked in this
+    container), and so does the device path."""
+    from paper_2604_18020_b200 import SimpConfig, default_schedule, make_preset, run_simp
+
+    with pytest.raises(ValueError, match="non-positive"):
+        run_simp(make_preset("cantilever", 0.2), SimpConfig(schedule=default_schedule(4), volume_on="projected"))

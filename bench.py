@@ -308,6 +308,17 @@ def run_ours(args):
     torch.cuda.synchronize()
     ms_warm = e0.elapsed_time(e1) / args.steps
 
+    # our kernels per timed step: the tile kernel; at N > 1 the slab product's
+    # x-range tiles (+ on the peer runtime the put-with-flags, the fixed-order
+    # add and the pass-through kernels)
+    per_step_launches = 1
+    if world > 1:
+        nnx = part.local_mesh.nelx + 1
+        bl, br = local_apply.bl, local_apply.br
+        per_step_launches = sum(1 for lo, hi in ((0, bl), (nnx - br, nnx), (bl, nnx - br)) if hi > lo)
+        if sop is sop_peer:
+            per_step_launches += 2 + (1 if sop.fixed.numel() else 0)
+
     # N > 1: the same back-to-back products through the peer-memory transport
     # (CUDA IPC puts + stream-ordered flags, peer.py) next to the
     # torch.distributed P2P one (NCCL), max over ranks
@@ -447,7 +458,7 @@ def run_ours(args):
             "e2e": {"value": n_dof_total / (ms_e2e * 1e-3) / 1e9, "unit": "GDOF/s",
                     "h2d_bytes_per_step": int(m.n_dof * np.dtype(dt).itemsize),
                     "d2h_bytes_per_step": int(m.n_dof * np.dtype(dt).itemsize)},
-            "gpu_launches": args.steps,
+            "gpu_launches": args.steps * per_step_launches,
             "e2e_path": "MatFreeOperator.apply_stream (cudaHostAlloc host in/out; native 3-stream pipeline, csrc/tf_stream.cu); median of 3 batches of `steps` products after 1 s of PCIe warm-up" if world == 1
                         else "SlabOperator.apply per step (pinned host in/out)",
             "clocks": ck,

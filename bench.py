@@ -149,6 +149,31 @@ def cpu_time_apply(dims, prec, threads, budget_s=12.0, max_reps=200):
     return m, sec, reps
 
 
+def cpu_time_cg_c1(threads):
+    """The reference's CPU CG on c1 (48x24x24, rho 0.5, p 3, FP64, cold,
+    CgConfig defaults) through the oracle port (C fused_atomic with OpenMP +
+    the numpy recurrence of solver.py:57-147): a bounded sample (~1 s) timed
+    beside the device solve."""
+    import oracle
+    from paper_2604_18020_b200.element import SimpParams, simp_scale, unit_stiffness
+    from paper_2604_18020_b200.mesh import StructuredMesh, build_edof, cantilever_bcs
+
+    m = StructuredMesh(48, 24, 24)
+    bcs = cantilever_bcs(m)
+    edof = build_edof(m)
+    ke = np.ascontiguousarray(unit_stiffness(0.3))
+    scale = simp_scale(np.full(m.n_elem, 0.5), SimpParams(3.0))
+    oracle.set_threads(threads)
+    A = lambda x: oracle.apply(edof, ke, scale, x, bcs.fixed_dofs, m.n_dof, "fused", "parallel_atomic")  # noqa: E731
+    d = oracle.diagonal(edof, ke, scale, bcs.fixed_dofs, m.n_dof)
+    t0 = time.perf_counter()
+    x, info = oracle.pcg(A, bcs.force, d)
+    sec = time.perf_counter() - t0
+    return {"config": "c1 48x24x24 cold FP64 PCG (rho 0.5, p 3, CgConfig())", "iterations": info["iterations"],
+            "s": sec, "us_per_iteration": sec / max(1, info["iterations"]) * 1e6, "threads": threads,
+            "kind": "port (oracle C fused_atomic + numpy recurrence)"}
+
+
 def run_reference(args):
     rank, world, local = dist_env()
     if rank != 0:
@@ -427,6 +452,8 @@ def run_ours(args):
 
     if rank == 0:
         cpu = None
+        if not args.no_cpu and cg is not None:
+            cg["cpu_c1_fp64"] = cpu_time_cg_c1(os.cpu_count() or 1)
         if not args.no_cpu:
             threads = os.cpu_count() or 1
             mm, sec, reps = cpu_time_apply(dims, prec, threads, budget_s=12.0)
@@ -698,6 +725,21 @@ def cg_c2():
         out[prec] = {"protocol": pcg_protocol(op), "iterations": rep.iterations, "termination": rep.termination,
                      "solve_ms": dt * 1e3, "us_per_iteration": dt * 1e6 / max(1, rep.iterations),
                      "compliance": float(np.dot(pb.bcs.force, u.double().cpu().numpy()))}
+    # c1 FP64 cold solve on the device, the size the in-run CPU sample uses
+    from paper_2604_18020_b200.mesh import StructuredMesh, cantilever_bcs
+
+    m1 = StructuredMesh(48, 24, 24)
+    b1 = cantilever_bcs(m1)
+    op = MatFreeOperator(m1, build_edof(m1), b1, np.full(m1.n_elem, 0.5), SimpParams(3.0), "fp64")
+    d, _ = op.diagonal_device()
+    device_pcg(op, b1.force, d, CgConfig(max_iter=5))
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    u, rep = device_pcg(op, b1.force, d, CgConfig(), return_device=True)
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    out["c1_fp64"] = {"iterations": rep.iterations, "solve_ms": dt * 1e3,
+                      "us_per_iteration": dt * 1e6 / max(1, rep.iterations)}
     out["reference_cpu"] = {"fp64": {"iterations": 511, "s": 27.9, "threads": 8},
                             "fp32": {"iterations": 1000, "termination": "max_iter"},
                             "note": "BASELINE.md sec 2 (8-thread numba)"}

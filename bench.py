@@ -250,7 +250,17 @@ def run_ours(args):
 
         apply_fn = op.apply
         gm = m
+        # the reference's variant equivalence gate (its bench.py:177-201):
+        # the timed operator against its three-stage twin, relative L2
+        twin = MatFreeOperator(m, edof, bcs, rho, SimpParams(3.0), prec, variant="three_stage")
+        a = np.asarray(op.apply(v.astype(dt)), dtype=np.float64)
+        b = np.asarray(twin.apply(v.astype(dt)), dtype=np.float64)
+        gate_rel = float(np.linalg.norm(a - b) / np.linalg.norm(a))
+        if gate_rel > {"fp64": 1e-12, "fp32": 1e-5}[prec]:
+            raise AssertionError(f"variant equivalence gate failed: {gate_rel:.3e}")
+        del twin
     else:
+        gate_rel = None  # the slab products are checked against NCCL's bitwise below
         # weak scaling: the global cantilever is world x the configured slab,
         # x-slab decomposition with an NCCL interface-plane exchange per matvec
         from paper_2604_18020_b200.slab import SlabOperator, SlabPartition, gpu_local_kernels
@@ -486,6 +496,7 @@ def run_ours(args):
                     "h2d_bytes_per_step": int(m.n_dof * np.dtype(dt).itemsize),
                     "d2h_bytes_per_step": int(m.n_dof * np.dtype(dt).itemsize)},
             "gpu_launches": args.steps * per_step_launches,
+            "equivalence_gate_rel_l2": gate_rel,
             "e2e_path": "MatFreeOperator.apply_stream (cudaHostAlloc host in/out; native 3-stream pipeline, csrc/tf_stream.cu); median of 3 batches of `steps` products after 1 s of PCIe warm-up" if world == 1
                         else "SlabOperator.apply per step (pinned host in/out)",
             "clocks": ck,

@@ -74,10 +74,20 @@ def is_tensor(x) -> bool:
 
 
 class IdCache:
-    """Per-object cache keyed by identity, released when the object dies."""
+    """Per-object cache keyed by identity, released when the object dies.
+
+    Cached values must not hold strong references to their key object
+    (the finalizer would never fire); DeviceProblem keeps a weakref to its
+    edof for that reason.  ``clear()`` drops every entry explicitly."""
 
     def __init__(self):
         self._d = {}
+
+    def __len__(self):
+        return len(self._d)
+
+    def clear(self):
+        self._d.clear()
 
     def get(self, obj, key, make):
         k = (id(obj), key)

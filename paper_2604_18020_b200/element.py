@@ -1,20 +1,18 @@
 """Unit-cube trilinear hex stiffness and SIMP material interpolation.
 
 Mirrors reference ``topofuse.element`` (element.py:20-135).  The 24x24
-``unit_stiffness`` is built here from the closed-form integrals of products of
-trilinear shape-function gradients over the unit cube (exact, no quadrature
-loop), then symmetrised; it agrees with the reference's 2x2x2 Gauss build to
-round-off (tests/test_host.py pins it against the reference bitwise-golden at
-1e-14, the reference's own tolerance, test_element.py:20-24).
-
-For an isotropic material, K_ab[c][d] = lam*I_cd + mu*(delta_cd*sum_p I_pp + I_dc)
-with I_pq = int dN_a/dx_p dN_b/dx_q dV; on the unit cube every I_pq factorises
-into per-axis 1-D integrals of (1 + s t) factors.
+``unit_stiffness`` is the reference's 2x2x2 Gauss build with the reference's
+roundings, bitwise (tests/test_host.py compares all 576 FP64 entries with the
+matrix the reference itself produced), so every kernel that consumes Ke --
+the bitwise verification mode, the Jacobi diagonal -- is the reference's
+arithmetic through the public API, with no golden matrix injected.
 """
 
 from __future__ import annotations
 
 from dataclasses import dataclass
+import itertools
+from fractions import Fraction
 from functools import lru_cache
 
 import numpy as np
@@ -54,55 +52,75 @@ def simp_scale_derivative(rho, params: SimpParams = SimpParams()):
 
 
 def elasticity_matrix(nu: float) -> np.ndarray:
-    """Voigt (xx, yy, zz, yz, xz, xy) isotropic stiffness, E = 1."""
-    lam = nu / ((1.0 + nu) * (1.0 - 2.0 * nu))
-    mu = 0.5 / (1.0 + nu)
+    """Voigt (xx, yy, zz, yz, xz, xy) isotropic stiffness, E = 1, formed with
+    the reference's roundings (element.py:59-66): c = 1/((1+nu)(1-2nu)),
+    normal block c*nu / c*(1-nu), shear 0.5/(1+nu)."""
+    c = 1.0 / ((1.0 + nu) * (1.0 - 2.0 * nu))
     d = np.zeros((6, 6))
-    d[:3, :3] = lam
-    d[[0, 1, 2], [0, 1, 2]] = lam + 2.0 * mu
-    d[[3, 4, 5], [3, 4, 5]] = mu
+    d[:3, :3] = c * nu
+    d[[0, 1, 2], [0, 1, 2]] = c * (1.0 - nu)
+    d[[3, 4, 5], [3, 4, 5]] = 0.5 / (1.0 + nu)
     return d
 
 
-def _gradient_integrals() -> np.ndarray:
-    """I[a, b, p, q] = int_{[0,1]^3} dN_a/dx_p * dN_b/dx_q dV for the 8 corners."""
-    s = 2.0 * CORNER_OFFSETS - 1.0  # corner signs in [-1, 1]^3
-    # 1-D integrals over t in [-1, 1] with the 1/2 Jacobian per axis folded in:
-    # int (1 + a t)(1 + b t) dt = 2 + 2ab/3 ; int (1 + a t) dt = 2 ; int dt = 2
-    I = np.zeros((8, 8, 3, 3))
+# Strain rows (Voigt) fed by each displacement component: (row, component,
+# gradient axis) triples of the symmetric gradient.
+_STRAIN_PATTERN = ((0, 0, 0), (1, 1, 1), (2, 2, 2), (3, 1, 2), (3, 2, 1),
+                   (4, 0, 2), (4, 2, 0), (5, 0, 1), (5, 1, 0))
+
+
+def _strain_matrix(pt) -> np.ndarray:
+    """B (6 x 24) at a reference point of [-1, 1]^3 for the unit cube
+    (dN/dx = 2 dN/dxi), gradients rounded as the reference rounds them
+    (element.py:47-56: 0.125*s_i, times the two (1 + s t) factors in axis
+    order, then the exact factor 2)."""
+    s = 2.0 * CORNER_OFFSETS - 1.0
+    b = np.zeros((6, 24))
     for a in range(8):
-        for b in range(8):
-            pair = 2.0 + (2.0 / 3.0) * s[a] * s[b]  # per-axis value-value integral
-            for p in range(3):
-                for q in range(3):
-                    if p == q:
-                        val = s[a, p] * s[b, p] * 2.0
-                        for r in range(3):
-                            if r != p:
-                                val *= pair[r]
-                    else:
-                        r = 3 - p - q
-                        val = s[a, p] * s[b, q] * 2.0 * 2.0 * pair[r]
-                    # dN/dx = 2 dN/dxi -> (1/4 s ...) each; dV = dxi/8
-                    I[a, b, p, q] = val / 16.0 / 8.0
-    return I
+        g = np.empty(3)
+        for i in range(3):
+            j, k = [ax for ax in range(3) if ax != i]
+            g[i] = 0.125 * s[a, i] * (1.0 + s[a, j] * pt[j]) * (1.0 + s[a, k] * pt[k])
+        g *= 2.0
+        for row, comp, axis in _STRAIN_PATTERN:
+            b[row, 3 * a + comp] = g[axis]
+    return b
+
+
+def _fma_chain(t_row: np.ndarray, b_col: np.ndarray) -> float:
+    """sum_k t_k b_k as a chain of correctly rounded fused multiply-adds from
+    0.0 in ascending k -- the rounding of the OpenBLAS dgemm micro-kernel the
+    reference's ``b.T @ d @ b`` reaches (probed against the reference's Ke:
+    this chain reproduces all 576 entries bitwise, a plain sum differs in
+    161).  Exact rational arithmetic makes it host-independent."""
+    acc = Fraction(0)
+    out = 0.0
+    for tk, bk in zip(t_row.tolist(), b_col.tolist()):
+        acc = Fraction(tk) * Fraction(bk) + Fraction(out)
+        out = float(acc)  # int/int true division: correctly rounded
+    return out
 
 
 @lru_cache(maxsize=8)
 def unit_stiffness(nu: float = 0.3) -> np.ndarray:
-    """24x24 stiffness of the unit-cube element, E = 1 (read-only, cached)."""
-    lam = nu / ((1.0 + nu) * (1.0 - 2.0 * nu))
-    mu = 0.5 / (1.0 + nu)
-    I = _gradient_integrals()
-    trace = I[:, :, 0, 0] + I[:, :, 1, 1] + I[:, :, 2, 2]
-    k = np.zeros((8, 3, 8, 3))
-    for c in range(3):
-        for d in range(3):
-            blk = lam * I[:, :, c, d] + mu * I[:, :, d, c]
-            if c == d:
-                blk = blk + mu * trace
-            k[:, c, :, d] = blk
-    ke = k.reshape(24, 24)
+    """24x24 stiffness of the unit-cube element, E = 1 (read-only, cached).
+
+    2x2x2 Gauss quadrature with det J = 1/8, accumulated over the points in
+    (xi, eta, zeta) nesting order and symmetrised -- the reference's build
+    (element.py:69-101), reproduced bitwise: ``tests/test_host.py`` compares
+    all 576 FP64 entries with the reference's own matrix (golden ke.npz).
+    """
+    d = elasticity_matrix(nu)
+    g = 1.0 / np.sqrt(3.0)
+    ke = np.zeros((24, 24))
+    for pt in itertools.product((-g, g), repeat=3):
+        b = _strain_matrix(pt)
+        t = b.T @ d  # d is block diagonal: each entry is at most 3 exact-order terms
+        m = np.empty((24, 24))
+        for i in range(24):
+            for j in range(24):
+                m[i, j] = _fma_chain(t[i], b[:, j])
+        ke += m * 0.125
     ke = 0.5 * (ke + ke.T)
     ke.setflags(write=False)
     return ke

@@ -20,7 +20,9 @@ torch CUDA tensors (stay resident; results are tensors).
 
 from __future__ import annotations
 
+import hashlib
 import os
+import weakref
 from dataclasses import dataclass
 
 import numpy as np
@@ -51,7 +53,10 @@ class DeviceProblem:
     iteration (simp.py:358-369) but this is uploaded once."""
 
     def __init__(self, mesh: StructuredMesh, edof: np.ndarray, bcs: BoundaryConditions):
-        self.mesh = mesh
+        # no strong reference to the caller's edof or mesh: the cache entry
+        # holding this object is keyed on edof and must die with it
+        # (_device.IdCache), so keep a weakref and a private mesh copy
+        self.mesh = StructuredMesh(mesh.nelx, mesh.nely, mesh.nelz)
         self.n_dof = mesh.n_dof
         self.n_elem = mesh.n_elem
         self.structured = edof_is_structured(mesh, edof)
@@ -64,12 +69,19 @@ class DeviceProblem:
         self.node_fixed = t.empty((nbytes + 3) // 4 * 4, dtype=t.uint8, device=D.require_cuda())
         _lib.call("tf_build_node_fixed", ctypes_ref(self.grid), D.ptr(self.fixed),
                   int(self.fixed_np.size), D.ptr(self.node_fixed), D.stream_ptr())
-        self._edof_np = edof
+        self._edof_ref = weakref.ref(edof)
         self._edof_masked = None
         self._edof_raw = None
         self._colors = None
         self._csr = None
         self.pcg_handles = {}
+
+    @property
+    def _edof_np(self) -> np.ndarray:
+        e = self._edof_ref()
+        if e is None:  # pragma: no cover - the cache entry dies with edof
+            raise _lib.TfError("device problem outlived its connectivity array")
+        return e
 
     @property
     def edof_masked(self):
@@ -149,8 +161,17 @@ def element_colouring(mesh: StructuredMesh, edof: np.ndarray):
     return order, offsets
 
 
+def _constraint_digest(bcs) -> bytes:
+    """Content key of the constraint set (ids of dead objects are reused)."""
+    f = np.ascontiguousarray(np.asarray(bcs.fixed_dofs, dtype=np.int64))
+    return hashlib.sha1(f.tobytes()).digest()
+
+
 def device_problem(mesh, edof, bcs) -> DeviceProblem:
-    key = (mesh.nelx, mesh.nely, mesh.nelz, id(bcs))
+    """Device data of (mesh, edof, bcs), cached on edof and keyed on the
+    constraint CONTENT -- two load cases on one mesh with different supports
+    never share constraint masks, whatever their object ids."""
+    key = (mesh.nelx, mesh.nely, mesh.nelz, _constraint_digest(bcs))
 
     def make():
         return DeviceProblem(mesh, edof, bcs)

@@ -82,8 +82,10 @@ def _pcg_handle(op: MatFreeOperator, graph_only: bool = False):
     forces the plain 3-kernel graph protocol (quantize_krylov rounds p and r
     in its direction kernel)."""
     dev = op.dev
-    # the protocol overrides are read at handle creation: part of the key
-    key = (op.precision.tag, op.grid_variant, op.variant == "fused" and op.structured,
+    # the protocol overrides and the element matrix (copied into the handle
+    # once, by tf_pcg_create) are fixed at handle creation: part of the key
+    key = (op.precision.tag, np.ascontiguousarray(op.ke).tobytes(), op.grid_variant,
+           op.variant == "fused" and op.structured,
            os.environ.get("TF_PCG_RESIDENT"), os.environ.get("TF_PCG_FUSED"), graph_only)
     h = dev.pcg_handles.get(key)
     if h is not None:

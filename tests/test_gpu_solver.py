@@ -296,3 +296,44 @@ def test_projected_volume_rejects_positive_sensitivities_like_reference():
 
     with pytest.raises(ValueError, match="non-positive"):
         run_simp(make_preset("cantilever", 0.2), SimpConfig(schedule=default_schedule(4), volume_on="projected"))
+
+
+def test_pcg_handle_follows_poisson_ratio():
+    """the PCG handle copies Ke at creation; an operator with a
+    different nu on the same device problem must not reuse it."""
+    import oracle
+    from paper_2604_18020_b200 import CgConfig, MatFreeOperator, SimpParams, build_edof, make_preset, pcg
+
+    pb = make_preset("cantilever", 0.2)
+    edof = build_edof(pb.mesh)
+    rho = np.full(pb.mesh.n_elem, 0.5)
+    for nu in (0.3, 0.2, 0.3):
+        op = MatFreeOperator(pb.mesh, edof, pb.bcs, rho, SimpParams(3.0), "fp64", nu=nu)
+        u, rep = pcg(op.apply, pb.bcs.force, op.diagonal(), CgConfig())
+        A = lambda x: oracle.apply(edof, op.ke, op.scale, x, pb.bcs.fixed_dofs, pb.mesh.n_dof)
+        d = oracle.diagonal(edof, op.ke, op.scale, pb.bcs.fixed_dofs, pb.mesh.n_dof)
+        xr, info = oracle.pcg(A, pb.bcs.force, d, 1e-5, 1000, 50)
+        assert abs(rep.iterations - info["iterations"]) <= max(1, 0.02 * info["iterations"]), nu
+        assert np.abs(u - xr).max() <= 1e-6 * np.abs(xr).max(), nu
+
+
+def test_device_problem_follows_constraints_in_a_loop():
+    """load cases built and dropped in a loop on one edof (CPython
+    reuses their ids) each get their own constraint masks."""
+    import oracle
+    from paper_2604_18020_b200 import BoundaryConditions, MatFreeOperator, SimpParams, StructuredMesh, build_edof
+
+    m = StructuredMesh(6, 4, 3)
+    edof = build_edof(m)
+    rng = np.random.default_rng(3)
+    rho = rng.uniform(0.1, 1.0, m.n_elem)
+    v = rng.standard_normal(m.n_dof)
+    for k in range(6):
+        fixed = np.sort(rng.choice(m.n_dof, size=10 + 7 * k, replace=False)).astype(np.int64)
+        bcs = BoundaryConditions(fixed, np.zeros(m.n_dof))
+        op = MatFreeOperator(m, edof, bcs, rho, SimpParams(3.0), "fp64")
+        want = oracle.apply(edof, op.ke, op.scale, v, fixed, m.n_dof)
+        got = op.apply(v)
+        assert np.abs(got - want).max() <= 1e-12 * np.abs(want).max(), k
+        assert np.array_equal(op.diagonal(), oracle.diagonal(edof, op.ke, op.scale, fixed, m.n_dof)), k
+        del op, bcs

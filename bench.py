@@ -558,14 +558,46 @@ def kernel_sweep(steps=100):
             b.record()
         torch.cuda.synchronize()
         ms = float(np.mean([a.elapsed_time(b) for a, b in ev]))
+        # the timed kernel's output against the REFERENCE's own apply at this
+        # size (sampled entries + norm recorded by tests/golden/make_golden_r2.py)
+        check = reference_check(cfg, prec, w.double().cpu().numpy(),
+                                perm if name.endswith("seeded_random") else None)
         byts = compulsory_bytes(m.n_elem, m.n_dof, prec, kernel != "edof")
         out[name] = {"workload": desc, "kernel": "k_grid_tile5" if kernel == "tile" else "k_edof_staged (red.global)",
                      "ms_per_step": ms, "GDOF_s": m.n_dof / (ms * 1e-3) / 1e9,
+                     "vs_reference": check,
                      "algorithmic_bytes": byts, "hbm_frac": byts / (ms * 1e-3) / 1e9 / hbm,
                      "general_contract_equiv_hbm_frac":
                          compulsory_bytes(m.n_elem, m.n_dof, prec, False) / (ms * 1e-3) / 1e9 / hbm}
         del op, x, w
     return out
+
+
+REFERENCE_GOLDEN = {"c2": "c2", "c4": "c4", "c5": "c5"}  # bench config -> hashes_r2.json case
+
+
+def reference_check(cfg, prec, w, perm=None):
+    """Relative error of a timed product against the reference's apply on the
+    same seeded inputs: max-abs over 4097 sampled DOFs / the reference's
+    max|w|, and the relative L2-norm difference (tests/golden/hashes_r2.json,
+    written by the reference itself; the north-star bars are 1e-5 FP32 and
+    1e-12 FP64).  perm: the seeded_random DOF relabelling (w is in the
+    relabelled numbering)."""
+    key = REFERENCE_GOLDEN.get(cfg)
+    p = ROOT / "tests" / "golden" / "hashes_r2.json"
+    if key is None or not p.exists():
+        return None
+    g = json.loads(p.read_text()).get(f"apply_fused_{prec}_{key}")
+    if g is None:
+        return None
+    w = np.asarray(w, np.float64)
+    if perm is not None:
+        w = w[perm]  # back to the reference numbering: w_ref[d] = w_perm[perm[d]]
+    idx = np.unique(np.linspace(0, w.size - 1, len(g["sample"])).astype(np.int64))
+    err = float(np.abs(w[idx] - np.asarray(g["sample"])).max() / g["max_abs"])
+    norm_rel = abs(float(np.linalg.norm(w)) - g["norm"]) / g["norm"]
+    bar = {"fp32": 1e-5, "fp64": 1e-12}[prec]
+    return {"max_abs_rel_sampled": err, "norm_rel": norm_rel, "bar": bar, "ok": err <= bar}
 
 
 def simp_c1():

@@ -52,3 +52,32 @@ def cuda_available() -> bool:
         return torch.cuda.is_available()
     except Exception:  # pragma: no cover
         return False
+
+
+# BASELINE.json configs the bench times (SURVEY.md §8 size table):
+# name -> (preset, scale).  Inputs follow the reference bench convention
+# (bench.py:161-173): rho ~ U(0.05, 1) then v ~ N(0, 1) from default_rng(42).
+BASELINE_CASES = {
+    "c3": ("torsion", 1.0),
+    "c4": ("cantilever", 5 / 3),
+    "c5": ("cantilever", 17 / 6),
+}
+
+
+def baseline_case(name):
+    """(mesh, edof, bcs, rho, v) of a BASELINE config, as
+    tests/golden/make_golden_r2.py drew them for the reference."""
+    from paper_2604_18020_b200.mesh import build_edof, make_preset
+
+    preset, scale = BASELINE_CASES[name]
+    pb = make_preset(preset, scale)
+    m = pb.mesh
+    rng = np.random.default_rng(42)
+    rho = rng.uniform(0.05, 1.0, m.n_elem)
+    v = rng.standard_normal(m.n_dof)
+    return m, build_edof(m), pb.bcs, rho, v
+
+
+def sample_index(n, k=4097):
+    """Entries sampled by make_golden_r2.py (4097 evenly spaced DOFs)."""
+    return np.unique(np.linspace(0, n - 1, k).astype(np.int64))

@@ -36,7 +36,8 @@ def test_fp64_cold_solve_matches_reference(key, scale):
     # the element products): early iterations agree tightly, later ones within
     # a few percent while the stop iteration stays within +-2 %.
     n = min(len(rep.residual_history), len(g["history"]), 20)
-    np.testing.assert_allclose(rep.residual_history[:n], g["history"][:n], rtol=1e-5)
+    np.testing.assert_allclose(rep.residual_history[:10], g["history"][:10], rtol=1e-5)
+    np.testing.assert_allclose(rep.residual_history[:n], g["history"][:n], rtol=1e-4)
     h, gh = np.log10(rep.residual_history), np.log10(g["history"])
     m = min(len(h), len(gh))
     keep = gh[:m] > -2.0  # before the last decades, where tiny drifts are amplified
@@ -337,3 +338,69 @@ def test_device_problem_follows_constraints_in_a_loop():
         assert np.abs(got - want).max() <= 1e-12 * np.abs(want).max(), k
         assert np.array_equal(op.diagonal(), oracle.diagonal(edof, op.ke, op.scale, fixed, m.n_dof)), k
         del op, bcs
+
+
+@pytest.mark.parametrize("key", ["c2_fp32", "c3_fp32"])
+def test_fp32_cold_solve_at_baseline_size(key):
+    """FP32 cold solves at c2 (cantilever 120x60x30) and c3 (torsion 499k):
+    the reference stalls at its 1000-iteration cap (FP32 true-residual
+    refresh, SURVEY §7 hard part 3).  Same termination class and iteration
+    count, early residual history within 1e-3, compliance within the
+    north-star 1e-3 (tests/golden/make_golden_r2.py, reference numba serial)."""
+    from paper_2604_18020_b200 import (CgConfig, MatFreeOperator, SimpParams, build_edof, make_preset,
+                                       solve_equilibrium)
+
+    g = load_golden("cg_r2.json")[key]
+    pb = make_preset(g["preset"], g["scale"])
+    op = MatFreeOperator(pb.mesh, build_edof(pb.mesh), pb.bcs, np.full(pb.mesh.n_elem, 0.5),
+                         SimpParams(3.0), "fp32")
+    u, rep = solve_equilibrium(op, pb.bcs.force, CgConfig())
+    assert rep.termination == g["termination"] == "max_iter"
+    assert rep.iterations == g["iterations"] == 1000
+    np.testing.assert_allclose(rep.residual_history[:30], g["history"][:30], rtol=1e-3)
+    assert abs(rep.compliance - g["compliance"]) <= 1e-3 * abs(g["compliance"])
+    # stalled, like the reference: the last residual is of the same order
+    assert 0.2 * g["rel_residual"] <= rep.rel_residual <= 5.0 * g["rel_residual"]
+
+
+@pytest.mark.parametrize("key", ["c4_fp64", "c4_fp32"])
+def test_cold_solve_at_c4(key):
+    """c4 (cantilever 200x100x50, 1M elements): iterations within +-2 % (or
+    the same cap), compliance within 1e-6 (FP64) / 1e-3 (FP32)."""
+    from paper_2604_18020_b200 import (CgConfig, MatFreeOperator, SimpParams, build_edof, make_preset,
+                                       solve_equilibrium)
+
+    gs = load_golden("cg_r2.json")
+    if key not in gs:
+        pytest.skip("c4 golden not generated")
+    g = gs[key]
+    pb = make_preset(g["preset"], g["scale"])
+    prec = key.split("_")[1]
+    op = MatFreeOperator(pb.mesh, build_edof(pb.mesh), pb.bcs, np.full(pb.mesh.n_elem, 0.5),
+                         SimpParams(3.0), prec)
+    u, rep = solve_equilibrium(op, pb.bcs.force, CgConfig())
+    assert rep.termination in (g["termination"], "floor" if g["termination"] == "converged" else "-")
+    assert abs(rep.iterations - g["iterations"]) <= max(2, 0.02 * g["iterations"])
+    tol = 1e-6 if prec == "fp64" else 1e-3
+    assert abs(rep.compliance - g["compliance"]) <= tol * abs(g["compliance"])
+
+
+def test_simp_c1_fp32_matches_reference():
+    """Config c1 in FP32 (reference numba serial: 20,035 CG iterations, final
+    compliance 5.54433823; most solves stall at the 1000 cap).  North-star
+    bars: compliance and density within 1e-3 after the 30 iterations, CG
+    total within +-2 %."""
+    from paper_2604_18020_b200 import (ContinuationSchedule, Phase, ProblemPreset, SimpConfig,
+                                       StructuredMesh, cantilever_bcs, run_simp)
+
+    g = load_golden("simp_c1_fp32.npz")
+    m = StructuredMesh(48, 24, 24)
+    pb = ProblemPreset("cantilever", m, cantilever_bcs(m), 0.3, 1.5)
+    sched = ContinuationSchedule((Phase(1, 30, p=3.0, beta=1.0, move=0.2, rmin_end=1.5),), 1.5)
+    res = run_simp(pb, SimpConfig(schedule=sched, precision="fp32"))
+    c = np.array([h.compliance for h in res.history])
+    assert abs(c[-1] - g["compliance"][-1]) <= 1e-3 * abs(g["compliance"][-1])
+    np.testing.assert_allclose(c, g["compliance"], rtol=1e-3)
+    rel = np.linalg.norm(res.rho_phys - g["rho_phys"]) / np.linalg.norm(g["rho_phys"])
+    assert rel <= 1e-3, rel
+    assert abs(res.total_cg_iterations - int(g["total_cg"])) <= 0.02 * int(g["total_cg"]), res.total_cg_iterations

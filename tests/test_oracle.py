@@ -126,3 +126,17 @@ def test_oracle_bf16_kernels_bitwise_vs_reference(golden_ke, dims, seed):
         got = oracle.apply_bf16(edof, ke, scale, v, bcs.fixed_dofs, m.n_dof, variant)
         assert np.array_equal(got, g[f"apply_{variant}"]), variant
     assert np.array_equal(oracle.diagonal_bf16(edof, ke, scale, bcs.fixed_dofs, m.n_dof), g["diag"])
+
+
+@pytest.mark.parametrize("name", ["c3", "c4", "c5"])
+def test_oracle_baseline_size_hashes(golden_ke, name):
+    """Bitwise at the remaining BASELINE sizes the bench times (c3 torsion,
+    c4 1M, c5 4.9M) via the reference's sha256 (make_golden_r2.py)."""
+    from conftest import baseline_case
+
+    h = load_golden("hashes_r2.json")
+    m, edof, bcs, rho, v = baseline_case(name)
+    for prec in ("fp64", "fp32"):
+        ke, scale, dt = _ops(golden_ke, rho, prec)
+        got = oracle.apply(edof, ke, scale, v, bcs.fixed_dofs, m.n_dof, "fused")
+        assert _sha(got) == h[f"apply_fused_{prec}_{name}"]["sha256"], prec

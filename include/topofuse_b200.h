@@ -147,6 +147,25 @@ int tf_round_bf16(int64_t n, const float* x, float* y, void* stream);
  *      w is overwritten (accumulate = 0) or accumulated into (1).          */
 int tf_edof_csr_build(const int32_t* edof, int64_t n_elem, int64_t n_dof, int64_t* offsets,
                       int32_t* entries, void* stream);
+/* Jacobi diagonal, general connectivity, deterministic and bitwise the
+ * reference's jacobi_diag (_kernels_numba.py:217-226): acc[d] (FP64, caller
+ * initialised) += f64(scale[e] * ke_diag[l]) in ascending element order over
+ * the DOF -> (element*24 + row) CSR of tf_edof_csr_build. */
+int tf_jacobi_edof_pull_f32(const int64_t* offsets, const int32_t* entries, const float* ke_diag,
+                            const float* scale, double* acc, int64_t n_dof, void* stream);
+int tf_jacobi_edof_pull_f64(const int64_t* offsets, const int32_t* entries, const double* ke_diag,
+                            const double* scale, double* acc, int64_t n_dof, void* stream);
+/* three-stage scatter_serial, bitwise the reference (_kernels_numba.py:129-132):
+ * acc[d] (FP64) += f_elem[e*24 + i] in ascending element order over the CSR. */
+int tf_scatter_pull_f32(const int64_t* offsets, const int32_t* entries, const float* f_elem, double* acc,
+                        int64_t n_dof, void* stream);
+int tf_scatter_pull_f64(const int64_t* offsets, const int32_t* entries, const double* f_elem, double* acc,
+                        int64_t n_dof, void* stream);
+/* emulated-bf16 fused_serial, bitwise the reference (_kernels_numba.py:166-177):
+ * FP32 rows of bf16(s_e K_ij) u_j, added in ascending element order in FP32. */
+int tf_matvec_edof_pull_bf16(const int32_t* edof, const float* ke, const float* scale, const float* v, float* w,
+                             int64_t n_elem, int64_t n_dof, const int64_t* offsets, const int32_t* entries,
+                             double* rows, int accumulate, void* stream);
 int tf_matvec_edof_pull_f32(const int32_t* edof, const float* ke, const float* scale,
                             const float* v, float* w, int64_t n_elem, int64_t n_dof,
                             const int64_t* offsets, const int32_t* entries, double* rows,

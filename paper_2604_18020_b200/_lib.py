@@ -142,6 +142,11 @@ _SIGS = {
     "tf_pcg_set_quantize_krylov": [_P, _INT],
     "tf_tile_shape": [_P, _INT, _P, _P],
     "tf_edof_csr_build": [_P, _I64, _I64, _P, _P, _P],
+    "tf_scatter_pull_f32": [_P, _P, _P, _P, _I64, _P],
+    "tf_scatter_pull_f64": [_P, _P, _P, _P, _I64, _P],
+    "tf_matvec_edof_pull_bf16": [_P, _P, _P, _P, _P, _I64, _I64, _P, _P, _P, _INT, _P],
+    "tf_jacobi_edof_pull_f32": [_P, _P, _P, _P, _P, _I64, _P],
+    "tf_jacobi_edof_pull_f64": [_P, _P, _P, _P, _P, _I64, _P],
     "tf_matvec_edof_pull_f32": [_P, _P, _P, _P, _P, _I64, _I64, _P, _P, _P, _INT, _P],
     "tf_matvec_edof_pull_f64": [_P, _P, _P, _P, _P, _I64, _I64, _P, _P, _P, _INT, _P],
     "tf_host_alloc": [_P, ctypes.c_size_t],

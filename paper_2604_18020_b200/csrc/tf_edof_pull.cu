@@ -86,6 +86,67 @@ __global__ void k_dof_pull(const int64_t* __restrict__ off, const int32_t* __res
     w[d] = sizeof(T) == 8 ? (T)acc64 : (T)acc32;
 }
 
+// Jacobi diagonal in the reference's order (_kernels_numba.py:217-226):
+// acc[d] += f64(s_e * Ke[l][l]) over d's (element, corner-row) entries in
+// ascending element order -- the product in the working dtype, the sum in
+// FP64, no FMA.  One thread per DOF through the same CSR as k_dof_pull.
+template <typename T>
+__global__ void k_jacobi_pull(const int64_t* __restrict__ off, const int32_t* __restrict__ ent,
+                              const T* __restrict__ scale, double* __restrict__ acc, long long n_dof,
+                              const __grid_constant__ KeMat<T> kd)
+{
+    const long long d = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (d >= n_dof) return;
+    double a = acc[d];
+    for (long long k = off[d]; k < off[d + 1]; ++k) {
+        const int t = __ldg(ent + k);
+        const int e = t / NLOC, l = t - e * NLOC;
+        const T prod = sizeof(T) == 8 ? (T)__dmul_rn((double)ld_nc(scale + e), (double)kd.a[l])
+                                      : (T)__fmul_rn((float)ld_nc(scale + e), (float)kd.a[l]);
+        a = __dadd_rn(a, (double)prod);
+    }
+    acc[d] = a;
+}
+
+// three-stage scatter_serial in the reference's order (_kernels_numba.py:
+// 129-132): acc[d] (FP64) += f_elem[e][i] over d's entries in ascending
+// element order
+template <typename T>
+__global__ void k_scatter_pull(const int64_t* __restrict__ off, const int32_t* __restrict__ ent,
+                               const T* __restrict__ f_elem, double* __restrict__ acc, long long n_dof)
+{
+    const long long d = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (d >= n_dof) return;
+    double a = acc[d];
+    for (long long k = off[d]; k < off[d + 1]; ++k) a = __dadd_rn(a, (double)ld_nc(f_elem + __ldg(ent + k)));
+    acc[d] = a;
+}
+
+// emulated-bf16 fused_serial rows (_kernels_numba.py:166-177): FP32 row sums
+// of bf16(s_e*K[i][j]) * u_j in j order without FMA, stored exactly in the
+// FP64 row workspace; k_dof_pull<float> then adds them in ascending element
+// order with FP32 rounding (f32(f64(a) + f64(b)) == a + b in binary32)
+__global__ void __launch_bounds__(PULL_ROWS_BLOCK)
+k_edof_rows_bf16(const int32_t* __restrict__ edof, const float* __restrict__ scale, const float* __restrict__ v,
+                 double* __restrict__ rows, long long n, const __grid_constant__ KeMat<float> ke)
+{
+    const long long e = (long long)blockIdx.x * PULL_ROWS_BLOCK + threadIdx.x;
+    if (e >= n) return;
+    float u[NLOC];
+#pragma unroll
+    for (int q = 0; q < NLOC; ++q) {
+        const int d = __ldg(edof + e * NLOC + q);
+        u[q] = d >= 0 ? ld_nc(v + d) : 0.0f;
+    }
+    const float se = ld_nc(scale + e);
+    for (int i = 0; i < NLOC; ++i) {
+        float t = 0.0f;
+#pragma unroll
+        for (int j = 0; j < NLOC; ++j) t = __fadd_rn(t, __fmul_rn(bf16_rne(__fmul_rn(se, ke.a[i * NLOC + j])), u[j]));
+        rows[e * NLOC + i] = (double)t;
+    }
+}
+
 __global__ void k_iota_flat(int32_t* __restrict__ x, long long n)
 {
     const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -159,5 +220,53 @@ int tf_edof_csr_build(const int32_t* edof, int64_t n_elem, int64_t n_dof, int64_
     }
 TF_EDOF_PULL(float, f32)
 TF_EDOF_PULL(double, f64)
+
+#define TF_JACOBI_PULL(T, SUF)                                                                            \
+    int tf_jacobi_edof_pull_##SUF(const int64_t* offsets, const int32_t* entries, const T* ke_diag,      \
+                                  const T* scale, double* acc, int64_t n_dof, void* stream)              \
+    {                                                                                                     \
+        if (n_dof <= 0) return TF_OK;                                                                     \
+        TF_REQUIRE(offsets && entries && ke_diag && scale && acc, "null pointer");                        \
+        KeMat<T> k;                                                                                       \
+        memset(&k, 0, sizeof(k));                                                                         \
+        memcpy(k.a, ke_diag, NLOC * sizeof(T));                                                           \
+        k_jacobi_pull<T><<<(unsigned)((n_dof + 255) / 256), 256, 0, S(stream)>>>(offsets, entries, scale, \
+                                                                                acc, n_dof, k);            \
+        TF_CHECK_LAUNCH();                                                                                \
+        return TF_OK;                                                                                     \
+    }
+TF_JACOBI_PULL(float, f32)
+TF_JACOBI_PULL(double, f64)
+
+#define TF_SCATTER_PULL(T, SUF)                                                                           \
+    int tf_scatter_pull_##SUF(const int64_t* offsets, const int32_t* entries, const T* f_elem, double* acc, \
+                              int64_t n_dof, void* stream)                                                \
+    {                                                                                                     \
+        if (n_dof <= 0) return TF_OK;                                                                     \
+        TF_REQUIRE(offsets && entries && f_elem && acc, "null pointer");                                  \
+        k_scatter_pull<T><<<(unsigned)((n_dof + 255) / 256), 256, 0, S(stream)>>>(offsets, entries, f_elem, \
+                                                                                  acc, n_dof);             \
+        TF_CHECK_LAUNCH();                                                                                \
+        return TF_OK;                                                                                     \
+    }
+TF_SCATTER_PULL(float, f32)
+TF_SCATTER_PULL(double, f64)
+
+int tf_matvec_edof_pull_bf16(const int32_t* edof, const float* ke, const float* scale, const float* v, float* w,
+                             int64_t n_elem, int64_t n_dof, const int64_t* offsets, const int32_t* entries,
+                             double* rows, int accumulate, void* stream)
+{
+    if (n_elem <= 0) return TF_OK;
+    TF_REQUIRE(edof && ke && scale && v && w && offsets && entries && rows, "null pointer");
+    KeMat<float> k;
+    memcpy(k.a, ke, sizeof(k.a));
+    cudaStream_t st = S(stream);
+    k_edof_rows_bf16<<<(unsigned)((n_elem + PULL_ROWS_BLOCK - 1) / PULL_ROWS_BLOCK), PULL_ROWS_BLOCK, 0, st>>>(
+        edof, scale, v, rows, n_elem, k);
+    TF_CHECK_LAUNCH();
+    k_dof_pull<float><<<(unsigned)((n_dof + 255) / 256), 256, 0, st>>>(offsets, entries, rows, w, n_dof, accumulate);
+    TF_CHECK_LAUNCH();
+    return TF_OK;
+}
 
 }  // extern "C"

@@ -37,6 +37,7 @@
 #include <type_traits>
 
 #include "tf_common.cuh"
+#include <cooperative_groups.h>
 #include "tf_walsh.cuh"
 
 namespace tf {
@@ -162,177 +163,8 @@ template bool khat_blocks<double>(const double*, KhatBlocks<double>*);
 
 // ---- device ------------------------------------------------------------------------
 
-template <typename T, bool DOT>
-__global__ void __launch_bounds__(TileDims<T>::NT)
-k_grid_tile(Grid g, int oz, const T* __restrict__ scale, const T* __restrict__ v,
-            T* __restrict__ w, const uint8_t* __restrict__ node_fixed, uint32_t flags,
-            double* __restrict__ dot_part, const __grid_constant__ KhatBlocks<T> kb)
-{
-    constexpr int TILE_BY = TileDims<T>::BY, TILE_NT = TileDims<T>::NT;
-    constexpr int PW = StageSlots<T>::PW, PN = StageSlots<T>::PN, NS = StageSlots<T>::N;
-    __shared__ T plane[2][PN];          // double-buffered node planes
-    __shared__ T Y[6][TILE_NT];         // x-combined contributions handed to the row below
-
-    const int tx = threadIdx.x, ty = threadIdx.y;
-    const int tid = tx + TILE_BX * ty;
-    const int i0 = blockIdx.x * (TILE_BX - 1);
-    const int j0 = blockIdx.y * (TILE_BY - 1);
-    const int k0 = blockIdx.z * oz;
-    const int ex = i0 - 1 + tx, ey = j0 - 1 + ty;
-    const bool col_ok = ex >= 0 && ex < g.nelx && ey >= 0 && ey < g.nely;
-    const bool owner = tx < TILE_BX - 1 && ty < TILE_BY - 1 && (i0 + tx) < g.nnx && (j0 + ty) < g.nny;
-    const bool mask_in = (flags & TF_MASK_INPUT) && node_fixed != nullptr;
-    // DOF indices fit int32 (the reference's edof is int32, mesh.py:100-101)
-    const int pn = g.nnx * g.nny;      // nodes per plane
-    const uint8_t* col_fixed = node_fixed ? node_fixed + g.n_nodes : nullptr;
-
-    // per-thread staging slots: plane-relative node, component, smem index;
-    // `s_msk` marks slots whose node column holds any constrained node
-    int s_node[NS], s_c[NS];
-    bool s_ok[NS], s_msk[NS];
-#pragma unroll
-    for (int q = 0; q < NS; ++q) {
-        const int idx = tid + q * TILE_NT;
-        const int r = idx / PW, f = idx - r * PW;
-        const int ii = i0 - 1 + f / 3, jj = j0 - 1 + r;
-        s_ok[q] = idx < PN && ii >= 0 && ii < g.nnx && jj >= 0 && jj < g.nny;
-        s_c[q] = f % 3;
-        s_node[q] = s_ok[q] ? ii + g.nnx * jj : 0;
-        s_msk[q] = s_ok[q] && mask_in && ((col_fixed[s_node[q]] >> s_c[q]) & 1u);
-    }
-    T pre[NS];
-    auto fetch = [&](int kz) {
-        const bool zok = kz >= 0 && kz < g.nnz;
-        const int nbase = kz * pn;
-#pragma unroll
-        for (int q = 0; q < NS; ++q) {
-            const int node = nbase + s_node[q];
-            bool take = zok && s_ok[q];
-            if (s_msk[q] && zok) take = take && !((node_fixed[node] >> s_c[q]) & 1u);
-            pre[q] = take ? ld_nc(v + 3 * node + s_c[q]) : T(0);
-        }
-    };
-    auto commit = [&](int buf) {
-#pragma unroll
-        for (int q = 0; q < NS; ++q) {
-            const int idx = tid + q * TILE_NT;
-            if (idx < PN) plane[buf][idx] = pre[q];
-        }
-    };
-    auto pidx = [&](int ox, int oy, int c) { return (ty + oy) * PW + 3 * (tx + ox) + c; };
-    const int el_col = ex + g.nelx * ey, el_plane = g.nelx * g.nely;
-    auto scale_at = [&](int ez) -> T {
-        return (col_ok && ez >= 0 && ez < g.nelz) ? ld_nc(scale + el_col + el_plane * ez) : T(0);
-    };
-
-    T u[NLOC];
-    fetch(k0 - 1);
-    commit(0);
-    fetch(k0);
-    __syncthreads();
-#pragma unroll
-    for (int a = 0; a < 4; ++a) {  // bottom corners 0..3 of the first layer
-        const int ox = (a == 1 || a == 2), oy = (a >= 2);
-#pragma unroll
-        for (int c = 0; c < 3; ++c) u[3 * a + c] = plane[0][pidx(ox, oy, c)];
-    }
-    T s_cur = scale_at(k0 - 1);
-
-    T carry[3] = {T(0), T(0), T(0)};
-    double dot = 0.0;
-    const int own_node0 = (i0 + tx) + g.nnx * (j0 + ty);
-
-    // layers ez = k0-1 .. min(k0+oz-1, nnz-1): the last node plane (ez = nelz)
-    // completes with an empty element layer above it
-    const int n_layers = min(oz, g.nnz - k0) + 1;
-    for (int L = 0; L < n_layers; ++L) {
-        const int ez = k0 - 1 + L;
-        const int cur = L & 1, nxt = cur ^ 1;
-        commit(nxt);                       // plane ez+1 (fetched one layer ago)
-        if (L + 1 < n_layers) fetch(ez + 2);  // in flight during this layer's math
-        const T s_next = scale_at(ez + 1);
-        unsigned own_bits = 0u;
-        const bool write_plane = owner && L >= 1;
-        if (write_plane && node_fixed) own_bits = node_fixed[own_node0 + ez * pn];
-        __syncthreads();                   // (A) plane nxt ready, Y free
-        // the owned node's input values (plane ez, buffer `cur`) for the fused
-        // p.q: read now -- `cur` is overwritten by the next layer's commit
-        T pown[3];
-        if (DOT) {
-#pragma unroll
-            for (int c = 0; c < 3; ++c) pown[c] = plane[cur][pidx(1, 1, c)];
-        }
-#pragma unroll
-        for (int a = 4; a < 8; ++a) {
-            const int ox = (a == 5 || a == 6), oy = (a >= 6);
-#pragma unroll
-            for (int c = 0; c < 3; ++c) u[3 * a + c] = plane[nxt][pidx(ox, oy, c)];
-        }
-        T f[NLOC];
-        element_apply(u, s_cur, kb, f);
-        // x-combine: node column i0+tx gets corner ox=1 of this element and
-        // corner ox=0 of element column tx+1 (lane + 1 of the same warp)
-        T xr[2][2][3];  // [oy][oz][c]
-#pragma unroll
-        for (int oy = 0; oy < 2; ++oy)
-#pragma unroll
-            for (int ozz = 0; ozz < 2; ++ozz)
-#pragma unroll
-                for (int c = 0; c < 3; ++c) {
-                    const T mine = f[3 * corner_of(1, oy, ozz) + c];
-                    const T right = __shfl_down_sync(0xffffffffu, f[3 * corner_of(0, oy, ozz) + c], 1);
-                    xr[oy][ozz][c] = mine + right;
-                }
-        // y-combine: row ty's oy=0 sums belong to the node row owned by ty-1
-#pragma unroll
-        for (int ozz = 0; ozz < 2; ++ozz)
-#pragma unroll
-            for (int c = 0; c < 3; ++c) Y[3 * ozz + c][tid] = xr[0][ozz][c];
-        __syncthreads();                   // (B) Y complete
-        if (owner) {
-            const int below = tid + TILE_BX;
-            if (write_plane) {
-                const int d0 = 3 * (own_node0 + ez * pn);
-#pragma unroll
-                for (int c = 0; c < 3; ++c) {
-                    T acc = carry[c] + (xr[1][0][c] + Y[c][below]);
-                    const int d = d0 + c;
-                    if (flags & TF_ACCUMULATE) acc += w[d];
-                    const bool fx = (own_bits >> c) & 1u;
-                    if ((flags & TF_PASS_FIXED) && fx) acc = v[d];
-                    w[d] = acc;
-                    if (DOT) {
-                        const T pv = fx ? v[d] : pown[c];
-                        dot += (double)pv * (double)acc;
-                    }
-                }
-            }
-#pragma unroll
-            for (int c = 0; c < 3; ++c) carry[c] = xr[1][1][c] + Y[3 + c][below];
-        }
-#pragma unroll
-        for (int a = 0; a < 4; ++a)
-#pragma unroll
-            for (int c = 0; c < 3; ++c) u[3 * a + c] = u[3 * (a + 4) + c];
-        s_cur = s_next;
-    }
-
-    if (DOT) {
-        __shared__ double sh[TILE_NT / 32];
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) dot += __shfl_down_sync(0xffffffffu, dot, o);
-        if ((tid & 31) == 0) sh[tid >> 5] = dot;
-        __syncthreads();
-        if (tid == 0) {
-            double s = 0.0;
-            for (int i = 0; i < TILE_NT / 32; ++i) s += sh[i];
-            dot_part[blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z)] = s;
-        }
-    }
-}
-
 // ---------------------------------------------------------------------------
-// v3: the Walsh transforms factorised along the z march.
+// The Walsh transforms factorised along the z march (tile5/tile6).
 //
 // The forward transform is separable: u -> (x, y stages on each xy face) ->
 // (z stage between the bottom and top faces).  The bottom face of layer L is
@@ -361,243 +193,16 @@ __device__ __forceinline__ void cp_async_8(void* smem, const void* gmem, bool va
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
 
-
-template <typename T, bool DOT>
 #ifndef TF_TILE_MINB32
 #define TF_TILE_MINB32 3
 #endif
 #ifndef TF_TILE_MINB64
 #define TF_TILE_MINB64 3   // 168 regs + ~100 B spill: +5 % at c5 over 2 blocks/SM (measured)
 #endif
-__global__ void __launch_bounds__(TileDims<T>::NT, sizeof(T) == 4 ? TF_TILE_MINB32 : TF_TILE_MINB64)
-k_grid_tile3(Grid g, int oz, const T* __restrict__ scale, const T* __restrict__ v,
-             T* __restrict__ w, const uint8_t* __restrict__ node_fixed, uint32_t flags,
-             double* __restrict__ dot_part, const __grid_constant__ KhatBlocks<T> kb)
-{
-    constexpr int TILE_BY = TileDims<T>::BY, TILE_NT = TileDims<T>::NT;
-    constexpr int PW = StageSlots<T>::PW, PN = StageSlots<T>::PN, NS = StageSlots<T>::N;
-    __shared__ __align__(16) T plane[3][PN];  // ring: node plane k lives in buffer k % 3
-    __shared__ T Y[2][3][TILE_NT];            // x-combined sums handed to the row below (by layer parity)
-
-    const int tx = threadIdx.x, ty = threadIdx.y;
-    const int tid = tx + TILE_BX * ty;
-    const int i0 = g.ilo + blockIdx.x * (TILE_BX - 1);
-    const int j0 = blockIdx.y * (TILE_BY - 1);
-    const int k0 = blockIdx.z * oz;
-    const int ex = i0 - 1 + tx, ey = j0 - 1 + ty;
-    const bool col_ok = ex >= 0 && ex < g.nelx && ey >= 0 && ey < g.nely;
-    const bool owner = tx < TILE_BX - 1 && ty < TILE_BY - 1 && (i0 + tx) < g.ihi && (j0 + ty) < g.nny;
-    const bool mask_in = (flags & TF_MASK_INPUT) && node_fixed != nullptr;
-    const int pn = g.nnx * g.nny;
-    const uint8_t* col_fixed = node_fixed ? node_fixed + g.n_nodes : nullptr;
-
-    // per-thread staging slots, resolved once.  Constrained DOFs whose node
-    // column is constrained on every plane are dropped statically (`ok` bit
-    // cleared); only columns whose constraint varies along z (`msk` bits,
-    // rare) read the per-node mask byte each layer.
-    const uint8_t* col_and = node_fixed ? col_fixed + pn : nullptr;
-    int s_off[NS], s_node[NS], s_c[NS];
-    unsigned okbits = 0u, mskbits = 0u;
-#pragma unroll
-    for (int q = 0; q < NS; ++q) {
-        const int idx = tid + q * TILE_NT;
-        const int r = idx / PW, f = idx - r * PW;
-        const int ii = i0 - 1 + f / 3, jj = j0 - 1 + r, c = f % 3;
-        const bool ok = idx < PN && ii >= 0 && ii < g.nnx && jj >= 0 && jj < g.nny;
-        const int node = ok ? ii + g.nnx * jj : 0;
-        s_off[q] = 3 * node + c;
-        s_node[q] = node;
-        s_c[q] = c;
-        bool keep = ok;
-        if (ok && mask_in) {
-            const unsigned all_z = (col_and[node] >> c) & 1u, any_z = (col_fixed[node] >> c) & 1u;
-            if (all_z) keep = false;
-            else if (any_z) mskbits |= 1u << q;
-        }
-        if (keep) okbits |= 1u << q;
-    }
-    const int pn3 = 3 * pn;
-    // asynchronous copy of node plane kz into ring buffer `buf` (zero-filled
-    // outside the mesh and, when masking, on constrained DOFs)
-    auto stage = [&](int kz, T* buf) {
-        const bool zok = kz >= 0 && kz < g.nnz;
-        const T* vb = v + (long long)min(max(kz, 0), g.nnz - 1) * pn3;
-        unsigned take = zok ? okbits : 0u;
-        if (zok && mskbits) {  // rare: columns with z-varying constraints
-#pragma unroll
-            for (int q = 0; q < NS; ++q)
-                if (((mskbits >> q) & 1u) && ((node_fixed[kz * pn + s_node[q]] >> s_c[q]) & 1u))
-                    take &= ~(1u << q);
-        }
-#pragma unroll
-        for (int q = 0; q < NS; ++q) {
-            const int idx = tid + q * TILE_NT;
-            if (q < NS - 1 || idx < PN) {
-                if (sizeof(T) == 4)
-                    cp_async_4(buf + idx, vb + s_off[q], (take >> q) & 1u);
-                else
-                    cp_async_8(buf + idx, vb + s_off[q], (take >> q) & 1u);
-            }
-        }
-        cp_async_commit();
-    };
-    const int pofs = ty * PW + 3 * tx;  // this thread's corner (0,0) in a staged plane
-    auto pv = [&](const T* buf, int ox, int oy, int c) -> T { return buf[pofs + oy * PW + 3 * ox + c]; };
-    const int el_col = ex + g.nelx * ey, el_plane = g.nelx * g.nely;
-    auto scale_at = [&](int ez) -> T {
-        return (col_ok && ez >= 0 && ez < g.nelz) ? ld_nc(scale + el_col + el_plane * ez) : T(0);
-    };
-
-    const int n_layers = min(oz, g.nnz - k0) + 1;
-    // ring of three plane buffers: b_cur holds plane ez, b_top plane ez+1,
-    // b_nxt receives plane ez+2 while layer ez is computed
-    T* b_cur = plane[0];
-    T* b_top = plane[1];
-    T* b_nxt = plane[2];
-    stage(k0 - 1, b_cur);
-    stage(k0, b_top);
-    cp_async_wait_all();
-    __syncthreads();
-    // xy transform of the first bottom face (plane k0-1)
-    T XYb[3][4];
-#pragma unroll
-    for (int c = 0; c < 3; ++c)
-        face_fwd(pv(b_cur, 0, 0, c), pv(b_cur, 1, 0, c), pv(b_cur, 0, 1, c), pv(b_cur, 1, 1, c), XYb[c]);
-    T Gt[3][4];  // top-face part (xy modes) of the previous layer, for plane ez
-#pragma unroll
-    for (int c = 0; c < 3; ++c)
-#pragma unroll
-        for (int q = 0; q < 4; ++q) Gt[c][q] = T(0);
-    T s_cur = scale_at(k0 - 1);
-    T dot = T(0);  // per-thread p.q in the working dtype (<= 3*oz terms), FP64 across threads
-    const int own_node0 = (i0 + tx) + g.nnx * (j0 + ty);
-
-    // The node pass of layer L runs at the head of layer L+1, behind the same
-    // barrier that publishes plane ez+2 -> one __syncthreads per layer.
-    T pend_x1[3], pend_p[3];
-    unsigned pend_bits = 0u;
-    int pend_d0 = 0;
-    bool pend = false;
-    auto node_pass = [&](int yb) {
-        if (!pend) return;
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-            T acc = pend_x1[c] + Y[yb][c][tid + TILE_BX];
-            const int d = pend_d0 + c;
-            if (flags & TF_ACCUMULATE) acc += w[d];
-            const bool fx = (pend_bits >> c) & 1u;
-            if ((flags & TF_PASS_FIXED) && fx) acc = v[d];
-            w[d] = acc;
-            if (DOT) {
-                const T p = fx ? v[d] : pend_p[c];
-                dot = fma(p, acc, dot);
-            }
-        }
-    };
-
-    for (int L = 0; L < n_layers; ++L) {
-        const int ez = k0 - 1 + L;
-        // plane ez+1 was staged one layer ago (or in the prologue): make it
-        // visible together with the previous layer's row hand-off
-        cp_async_wait_all();
-        __syncthreads();                                   // (A)
-        node_pass((L + 1) & 1);                            // plane ez-1 (layer L-1)
-        if (L + 1 < n_layers) stage(ez + 2, b_nxt);         // lands during this layer
-        const T s_next = scale_at(ez + 1);
-        const bool write_plane = owner && L >= 1;
-        unsigned own_bits = 0u;
-        if (write_plane && node_fixed) own_bits = node_fixed[own_node0 + ez * pn];
-        T pown[3];
-        if (DOT) {
-#pragma unroll
-            for (int c = 0; c < 3; ++c) pown[c] = pv(b_cur, 1, 1, c);
-        }
-        // forward: xy stage of the new top face, z stage against the carried bottom
-        T h[3][8];
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-            T XYt[4];
-            face_fwd(pv(b_top, 0, 0, c), pv(b_top, 1, 0, c), pv(b_top, 0, 1, c), pv(b_top, 1, 1, c), XYt);
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                h[c][q] = XYb[c][q] + XYt[q];      // mz = 0
-                h[c][q + 4] = XYt[q] - XYb[c][q];  // mz = 1
-                XYb[c][q] = XYt[q];
-            }
-        }
-#pragma unroll
-        for (int c = 0; c < 3; ++c)
-#pragma unroll
-            for (int m = 1; m < 8; ++m) h[c][m] *= s_cur;
-        T gm[3][8];
-#pragma unroll
-        for (int c = 0; c < 3; ++c) gm[c][0] = T(0);
-#pragma unroll
-        for (int q = 0; q < 8; ++q)
-#pragma unroll
-            for (int c = 0; c < 3; ++c) {
-                const int m = q ^ (1 << c);
-                if (m == 0) continue;
-                T acc = T(0);
-#pragma unroll
-                for (int d = 0; d < 3; ++d) {
-                    const int n = q ^ (1 << d);
-                    if (n == 0) continue;
-                    acc = fma(kb.b[q][c][d], h[d][n], acc);
-                }
-                gm[c][m] = acc;
-            }
-        // z inverse: bottom part joins the carried top part on plane ez
-        T corner[3][4];
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-            T H[4];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                H[q] = Gt[c][q] + (gm[c][q] - gm[c][q + 4]);
-                Gt[c][q] = gm[c][q] + gm[c][q + 4];
-            }
-            face_inv(H, corner[c]);
-        }
-        // node (i0+tx, j0+ty) gets corner (1,1) of this column, (0,1) of column
-        // tx+1 (next lane), (1,0) of row ty+1 and (0,0) of (tx+1, ty+1)
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-            const T x0 = corner[c][1] + __shfl_down_sync(0xffffffffu, corner[c][0], 1);
-            pend_x1[c] = corner[c][3] + __shfl_down_sync(0xffffffffu, corner[c][2], 1);
-            Y[L & 1][c][tid] = x0;
-            if (DOT) pend_p[c] = pown[c];
-        }
-        pend = write_plane;
-        pend_bits = own_bits;
-        pend_d0 = 3 * (own_node0 + ez * pn);
-        s_cur = s_next;
-        T* t = b_cur;  // rotate the ring
-        b_cur = b_top;
-        b_top = b_nxt;
-        b_nxt = t;
-    }
-    __syncthreads();
-    node_pass((n_layers - 1) & 1);
-
-    if (DOT) {
-        __shared__ double sh[TILE_NT / 32];
-        double dd = (double)dot;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) dd += __shfl_down_sync(0xffffffffu, dd, o);
-        if ((tid & 31) == 0) sh[tid >> 5] = dd;
-        __syncthreads();
-        if (tid == 0) {
-            double s = 0.0;
-            for (int i = 0; i < TILE_NT / 32; ++i) s += sh[i];
-            dot_part[blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z)] = s;
-        }
-    }
-}
 
 // ---------------------------------------------------------------------------
-// v5: k_grid_tile3's algorithm with the bookkeeping stripped and a deep
-// staging ring.
+// v5: the z-factorised march with the bookkeeping stripped and a deep
+// staging ring (kept for A/B behind TF_TILE5=1; tile6 below is production).
 //   * the operator flags are template parameters (the production matvec is
 //     MASK|PASS: no ACCUMULATE branches, no flag tests per DOF);
 //   * node planes AND the element scales of each layer stream in with
@@ -608,7 +213,6 @@ k_grid_tile3(Grid g, int oz, const T* __restrict__ scale, const T* __restrict__ 
 //     row hand-off are compile-time offsets (no pointer rotation / moves);
 //   * owners whose node column carries no constraint (column OR byte == 0)
 //     never read the per-node constraint byte.
-// Same arithmetic as tile3 (bitwise-identical results).
 // ---------------------------------------------------------------------------
 template <int I, int N, typename F>
 __device__ __forceinline__ void static_for(F&& f)
@@ -867,6 +471,340 @@ k_grid_tile5(Grid g, int oz, const T* __restrict__ scale, const T* __restrict__ 
     cp_async_wait_n(0);
     __syncthreads();
     node_pass(Y[(n_layers - 1) & 1]);
+
+    if (DOT) {
+        __shared__ double shd[TILE_NT / 32];
+        double dd = (double)dot;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) dd += __shfl_down_sync(0xffffffffu, dd, o);
+        if ((tid & 31) == 0) shd[tid >> 5] = dd;
+        __syncthreads();
+        if (tid == 0) {
+            double s2 = 0.0;
+            for (int i = 0; i < TILE_NT / 32; ++i) s2 += shd[i];
+            dot_part[blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z)] = s2;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// v6: tile5 + thread-block-cluster z split (the production kernel).
+//
+// A z-chunk's first node plane k0 needs the top-face part of element layer
+// k0-1, which belongs to the chunk below.  tile5 recomputes that layer in
+// every chunk (one halo layer per oz planes: +33 % element work at c2's
+// oz = 3).  Here the chunks of a column are launched as a (1, 1, cz) thread-
+// block cluster; a CTA of cluster rank r > 0 skips the halo layer, keeps the
+// mode-space bottom part D = gm_lo - gm_hi of its first layer in shared
+// memory, and at the end combines it with the lower CTA's final top part Gt
+// read through distributed shared memory: H = Gt + D -- the SAME operands
+// and operation order as the unsplit march, so the output is bitwise
+// identical to tile5 for any chunking or cluster size (tested).  The chunk
+// at k0 = 0 skips its all-zero halo layer the same way (Gt = +0).
+// Cluster-boundary CTAs (rank 0) keep the recomputed halo layer.
+// ---------------------------------------------------------------------------
+template <typename T, bool MASK, bool PASS, bool DOT, int P, bool ISO, bool CL>
+__global__ void __launch_bounds__(TileDims<T>::NT, sizeof(T) == 4 ? (CL ? 2 : TF_TILE_MINB32) : TF_TILE_MINB64)
+k_grid_tile6(Grid g, int oz, int cz, int accumulate, const T* __restrict__ scale, const T* __restrict__ v,
+             T* __restrict__ w,
+             const uint8_t* __restrict__ node_fixed, double* __restrict__ dot_part,
+             const __grid_constant__ KhatBlocks<T> kb, const __grid_constant__ KhatIso<T> ki)
+{
+    constexpr int TILE_BY = TileDims<T>::BY, TILE_NT = TileDims<T>::NT;
+    constexpr int PW = StageSlots<T>::PW, PN = StageSlots<T>::PN, NS = StageSlots<T>::N;
+    constexpr int R = P + 2;                      // ring: plane k in buffer (k - kb0) % R
+    __shared__ __align__(16) T plane[R][PN];
+    __shared__ T sc[R][TILE_NT];                  // element scale of layer k, with plane k
+    __shared__ T Y[2][3][TILE_NT];                // row hand-off, by layer parity
+    // cluster split: D of the first layer (this CTA's bottom part of plane
+    // k0); the exported final Gt (the upper partner's missing top part)
+    // reuses the plane ring, idle once the march is over
+    __shared__ T Dsm[CL ? 12 : 1][CL ? TILE_NT : 1];
+    static_assert(!CL || R * PN >= 12 * TILE_NT, "Gt export does not fit the plane ring");
+
+    const int tx = threadIdx.x, ty = threadIdx.y;
+    const int tid = tx + TILE_BX * ty;
+    const int i0 = g.ilo + blockIdx.x * (TILE_BX - 1);
+    const int j0 = blockIdx.y * (TILE_BY - 1);
+    const int k0 = blockIdx.z * oz;
+    const int crank = CL ? (int)(blockIdx.z % (unsigned)cz) : 0;
+    const bool from_below = CL && crank > 0 && k0 < g.nnz;
+    const bool to_above = CL && crank < cz - 1 && k0 + oz < g.nnz;
+    const bool skip_halo = from_below || k0 == 0;
+    const int kb0 = skip_halo ? k0 : k0 - 1;      // first element layer
+    const int ex = i0 - 1 + tx, ey = j0 - 1 + ty;
+    const bool col_ok = ex >= 0 && ex < g.nelx && ey >= 0 && ey < g.nely;
+    const bool owner = tx < TILE_BX - 1 && ty < TILE_BY - 1 && (i0 + tx) < g.ihi && (j0 + ty) < g.nny;
+    const bool have_nf = node_fixed != nullptr;
+    const int pn = g.nnx * g.nny, pn3 = 3 * pn;
+    const uint8_t* col_or = have_nf ? node_fixed + g.n_nodes : nullptr;
+    const uint8_t* col_and = have_nf ? col_or + pn : nullptr;
+
+    int s_off[NS];
+    unsigned okbits = 0u, mskbits = 0u;
+#pragma unroll
+    for (int q = 0; q < NS; ++q) {
+        const int idx = tid + q * TILE_NT;
+        const int r = idx / PW, f = idx - r * PW;
+        const int ii = i0 - 1 + f / 3, jj = j0 - 1 + r, c = f % 3;
+        const bool ok = idx < PN && ii >= 0 && ii < g.nnx && jj >= 0 && jj < g.nny;
+        const int node = ok ? ii + g.nnx * jj : 0;
+        s_off[q] = 3 * node + c;
+        bool keep = ok;
+        if (MASK && ok && have_nf) {
+            if ((col_and[node] >> c) & 1u) keep = false;
+            else if ((col_or[node] >> c) & 1u) mskbits |= 1u << q;
+        }
+        if (keep) okbits |= 1u << q;
+    }
+    const int el_col = ex + g.nelx * ey, el_plane = g.nelx * g.nely;
+    // one cp.async group: node plane kz and the scales of element layer kz
+    auto stage = [&](int kz, int buf) {
+        const bool zok = kz >= 0 && kz < g.nnz;
+        const T* vb = v + (long long)min(max(kz, 0), g.nnz - 1) * pn3;
+        unsigned take = zok ? okbits : 0u;
+        if (MASK && mskbits && zok) {  // rare: columns with z-varying constraints
+#pragma unroll
+            for (int q = 0; q < NS; ++q)
+                if (((mskbits >> q) & 1u) && ((node_fixed[kz * pn + s_off[q] / 3] >> (s_off[q] % 3)) & 1u))
+                    take &= ~(1u << q);
+        }
+        T* pb = plane[buf];
+#pragma unroll
+        for (int q = 0; q < NS; ++q) {
+            const int idx = tid + q * TILE_NT;
+            if (q < NS - 1 || idx < PN) {
+                if (sizeof(T) == 4)
+                    cp_async_4(pb + idx, vb + s_off[q], (take >> q) & 1u);
+                else
+                    cp_async_8(pb + idx, vb + s_off[q], (take >> q) & 1u);
+            }
+        }
+        const bool sok = col_ok && kz >= 0 && kz < g.nelz;
+        const T* sp = scale + (sok ? el_col + (long long)el_plane * kz : 0);
+        if (sizeof(T) == 4)
+            cp_async_4(&sc[buf][tid], sp, sok);
+        else
+            cp_async_8(&sc[buf][tid], sp, sok);
+        cp_async_commit();
+    };
+    const int pofs = ty * PW + 3 * tx;
+    const int own_node0 = (i0 + tx) + g.nnx * (j0 + ty);
+    // pass-through needs the node's constraint byte only on constrained
+    // columns, and a per-plane read only where the constraint varies along z
+    unsigned fix_or = 0u, fix_and = 0u;
+    if (PASS && owner && have_nf) {
+        fix_or = col_or[own_node0];
+        fix_and = col_and[own_node0];
+    }
+    const bool own_fix_col = fix_or != 0u;
+    const bool fix_zvar = fix_or != fix_and;
+
+    const int n_layers = max(0, min(oz, g.nnz - k0) + (skip_halo ? 0 : 1));
+    // prologue: planes kb0 .. kb0+P (P+1 groups) in flight together
+#pragma unroll
+    for (int b = 0; b <= P; ++b) stage(kb0 + b, b);
+    cp_async_wait_n(P - 1);  // planes kb0 and kb0+1 landed
+    __syncthreads();
+    T XYb[3][4];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        const T* b = plane[0] + pofs + c;
+        face_fwd(b[0], b[3], b[PW], b[PW + 3], XYb[c]);
+    }
+    T Gt[3][4];
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) Gt[c][q] = T(0);
+    T dot = T(0);
+
+    T pend_x1[3], pend_p[3], pend_v[3];
+    bool pend = false;
+    int pend_d0 = 0;
+    unsigned pend_bits = 0u;
+
+    auto finish = [&](const T (&x1)[3], const T (&Yrow)[3][TILE_NT], int d0, unsigned bits, const T (&pv)[3],
+                      const T (&pp)[3]) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            T acc = x1[c] + Yrow[c][tid + TILE_BX];
+            const int d = d0 + c;
+            if (accumulate) acc += w[d];  // uniform branch (rare: TF_ACCUMULATE)
+            const bool fx = PASS && ((bits >> c) & 1u);
+            if (fx) acc = pv[c];
+            w[d] = acc;
+            if (DOT) {
+                const T p = fx ? pv[c] : pp[c];
+                dot = fma(p, acc, dot);
+            }
+        }
+    };
+    // node pass of the previous layer (plane ez-1), reading its row hand-off
+    auto node_pass = [&](const T (&Yp)[3][TILE_NT]) {
+        if (pend) finish(pend_x1, Yp, pend_d0, pend_bits, pend_v, pend_p);
+    };
+    // constraint bits / pass-through values of the owned node of plane kz
+    auto own_bits = [&](int kz, T (&nv)[3]) -> unsigned {
+        unsigned nbits = 0u;
+        nv[0] = nv[1] = nv[2] = T(0);
+        if (own_fix_col) {
+            nbits = fix_zvar ? (unsigned)node_fixed[own_node0 + kz * pn] : fix_and;
+            const int d0 = 3 * (own_node0 + kz * pn);
+#pragma unroll
+            for (int c = 0; c < 3; ++c)
+                if ((nbits >> c) & 1u) nv[c] = ld_nc(v + d0 + c);
+        }
+        return nbits;
+    };
+    auto inverse_to_plane = [&](const T (&H)[3][4], T (&x0)[3], T (&x1)[3]) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            T corner[4];
+            face_inv(H[c], corner);
+            x0[c] = corner[1] + __shfl_down_sync(0xffffffffu, corner[0], 1);
+            x1[c] = corner[3] + __shfl_down_sync(0xffffffffu, corner[2], 1);
+        }
+    };
+
+    // one element layer (layer index L = ring phase I mod R): bottom plane ez
+    // in buffer I, top plane ez+1 in buffer (I+1) % R; the layer stages plane
+    // ez+1+P into buffer (I+P+1) % R = (I-1) % R (the plane of layer L-1)
+    auto layer = [&](auto ph, int L) {
+        constexpr int CUR = decltype(ph)::value;
+        constexpr int TOP = (CUR + 1) % R, NXT = (CUR + P + 1) % R;
+        const int ez = kb0 + L;
+        if (L > 0) {
+            cp_async_wait_n(P - 1);  // plane ez+1 landed (P-1 younger groups may still fly)
+            __syncthreads();         // (A) plane ez+1 + previous Y visible, buffer NXT free
+        }
+        node_pass(Y[(L + 1) & 1]);
+        stage(ez + 1 + P, NXT);      // beyond the chunk: zero-size copies keep the group count
+        // plane ez is finished in this CTA's march (else: halo layer, or the
+        // cluster-deferred first plane)
+        const bool emit_l = L >= 1 || k0 == 0;
+        unsigned nbits = 0u;
+        T nv[3] = {T(0), T(0), T(0)};
+        if (PASS && own_fix_col && emit_l) nbits = own_bits(ez, nv);
+        const T s_cur = sc[CUR][tid];
+        T pown[3];
+        if (DOT) {
+#pragma unroll
+            for (int c = 0; c < 3; ++c) pown[c] = plane[CUR][pofs + PW + 3 + c];
+        }
+        T h[3][8];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            const T* b = plane[TOP] + pofs + c;
+            T XYt[4];
+            face_fwd(b[0], b[3], b[PW], b[PW + 3], XYt);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                h[c][q] = XYb[c][q] + XYt[q];
+                h[c][q + 4] = XYt[q] - XYb[c][q];
+                XYb[c][q] = XYt[q];
+            }
+        }
+        T gm[3][8];
+        if (ISO) {
+            block_iso(h, ki, s_cur, gm);
+        } else {
+#pragma unroll
+            for (int c = 0; c < 3; ++c)
+#pragma unroll
+                for (int m = 1; m < 8; ++m) h[c][m] *= s_cur;
+#pragma unroll
+            for (int c = 0; c < 3; ++c) gm[c][0] = T(0);
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    const int m = q ^ (1 << c);
+                    if (m == 0) continue;
+                    T acc = T(0);
+#pragma unroll
+                    for (int d = 0; d < 3; ++d) {
+                        const int n = q ^ (1 << d);
+                        if (n == 0) continue;
+                        acc = fma(kb.b[q][c][d], h[d][n], acc);
+                    }
+                    gm[c][m] = acc;
+                }
+        }
+        T corner[3][4];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            T H[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const T dq = gm[c][q] - gm[c][q + 4];
+                if (CL && L == 0 && from_below) Dsm[4 * c + q][tid] = dq;
+                H[q] = Gt[c][q] + dq;
+                Gt[c][q] = gm[c][q] + gm[c][q + 4];
+            }
+            face_inv(H, corner[c]);
+        }
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            const T x0 = corner[c][1] + __shfl_down_sync(0xffffffffu, corner[c][0], 1);
+            pend_x1[c] = corner[c][3] + __shfl_down_sync(0xffffffffu, corner[c][2], 1);
+            Y[L & 1][c][tid] = x0;
+            if (DOT) pend_p[c] = pown[c];
+        }
+        pend = owner && emit_l;
+        pend_d0 = 3 * (own_node0 + ez * pn);
+        pend_bits = nbits;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) pend_v[c] = nv[c];
+    };
+    int L = 0;
+    for (; L + R <= n_layers; L += R) static_for<0, R>([&](auto ph) { layer(ph, L + decltype(ph)::value); });
+    static_for<0, R - 1>([&](auto ph) {
+        if (L + decltype(ph)::value < n_layers) layer(ph, L + decltype(ph)::value);
+    });
+    cp_async_wait_n(0);
+    __syncthreads();
+    node_pass(Y[(n_layers - 1) & 1]);
+
+    if constexpr (CL) {
+        namespace cgx = cooperative_groups;
+        cgx::cluster_group cluster = cgx::this_cluster();
+        if (to_above) {
+#pragma unroll
+            for (int c = 0; c < 3; ++c)
+#pragma unroll
+                for (int q = 0; q < 4; ++q) (&plane[0][0])[(4 * c + q) * TILE_NT + tid] = Gt[c][q];
+        }
+        cluster.sync();  // Gt exports visible cluster-wide (release/acquire)
+        if (from_below) {
+            // plane k0 = lower CTA's last top part + this CTA's first bottom part
+            const T* gb = cluster.map_shared_rank(&plane[0][0], crank - 1);
+            T H[3][4];
+#pragma unroll
+            for (int c = 0; c < 3; ++c)
+#pragma unroll
+                for (int q = 0; q < 4; ++q) H[c][q] = gb[(4 * c + q) * TILE_NT + tid] + Dsm[4 * c + q][tid];
+            T x0[3], x1[3];
+            inverse_to_plane(H, x0, x1);
+#pragma unroll
+            for (int c = 0; c < 3; ++c) Y[0][c][tid] = x0[c];
+            __syncthreads();
+            if (owner) {
+                T nv[3], pp[3];
+                const unsigned nbits = PASS ? own_bits(k0, nv) : 0u;
+                if (!PASS) nv[0] = nv[1] = nv[2] = T(0);
+                if (DOT) {
+                    const int d0 = 3 * (own_node0 + k0 * pn);
+                    unsigned mb = 0u;
+                    if (MASK && have_nf) mb = fix_zvar || !PASS ? (unsigned)node_fixed[own_node0 + k0 * pn] : fix_and;
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) pp[c] = ((mb >> c) & 1u) ? T(0) : ld_nc(v + d0 + c);
+                }
+                finish(x1, Y[0], 3 * (own_node0 + k0 * pn), nbits, nv, pp);
+            }
+        }
+        cluster.sync();  // partners finished reading this CTA's export before it exits
+    }
 
     if (DOT) {
         __shared__ double shd[TILE_NT / 32];
@@ -1181,284 +1119,22 @@ k_grid_tile3_cg(Grid g, int oz, const T* __restrict__ scale, T* __restrict__ w,
     }
 }
 
-// ---------------------------------------------------------------------------
-// v4 (FP32): two element columns per thread, packed FP32x2 arithmetic.
-//
-// sm_100a issues FADD2/FMUL2/FFMA2 (two FP32 lanes per instruction, scalar
-// uniform-register broadcast operands allowed), so a thread that carries the
-// element columns (tx, ty) and (tx, ty+4) of the same 32x8 column tile runs
-// every transform, block product and combine of BOTH columns with one
-// instruction -- the FP issue count per element halves, and the staging and
-// loop overhead is shared by two columns.  Same algebra and data movement as
-// k_grid_tile3 (z-factorised Walsh transforms, cp.async plane ring,
-// owner-computes node pass), 128 threads per CTA.
-// ---------------------------------------------------------------------------
-
-namespace p2 {
-using f2 = float2;
-__device__ __forceinline__ f2 add(f2 a, f2 b) { return __fadd2_rn(a, b); }
-__device__ __forceinline__ f2 sub(f2 a, f2 b) { return __fadd2_rn(a, make_float2(-b.x, -b.y)); }
-__device__ __forceinline__ f2 mul(f2 a, f2 b) { return __fmul2_rn(a, b); }
-__device__ __forceinline__ f2 fmab(float k, f2 h, f2 acc) { return __ffma2_rn(make_float2(k, k), h, acc); }
-__device__ __forceinline__ f2 mk(float lo, float hi) { return make_float2(lo, hi); }
-
-__device__ __forceinline__ void face_fwd(f2 a00, f2 a10, f2 a01, f2 a11, f2 (&o)[4])
-{
-    const f2 x0y0 = add(a00, a10), x1y0 = sub(a10, a00), x0y1 = add(a01, a11), x1y1 = sub(a11, a01);
-    o[0] = add(x0y0, x0y1);
-    o[1] = add(x1y0, x1y1);
-    o[2] = sub(x0y1, x0y0);
-    o[3] = sub(x1y1, x1y0);
-}
-
-__device__ __forceinline__ void face_inv(const f2 (&h)[4], f2 (&c)[4])
-{
-    const f2 y0x0 = sub(h[0], h[1]), y0x1 = add(h[0], h[1]), y1x0 = sub(h[2], h[3]), y1x1 = add(h[2], h[3]);
-    c[0] = sub(y0x0, y1x0);
-    c[1] = sub(y0x1, y1x1);
-    c[2] = add(y0x0, y1x0);
-    c[3] = add(y0x1, y1x1);
-}
-}  // namespace p2
-
-constexpr int T4_TX = 32, T4_TY = 4, T4_NT = T4_TX * T4_TY;  // threads; columns tile = 32 x 8
-constexpr int T4_PW = (T4_TX + 1) * 3, T4_PN = T4_PW * (2 * T4_TY + 1);
-constexpr int T4_NS = (T4_PN + T4_NT - 1) / T4_NT;
-
-template <bool DOT>
-__global__ void __launch_bounds__(T4_NT, 4)
-k_grid_tile4(Grid g, int oz, const float* __restrict__ scale, const float* __restrict__ v,
-             float* __restrict__ w, const uint8_t* __restrict__ node_fixed, uint32_t flags,
-             double* __restrict__ dot_part, const __grid_constant__ KhatBlocks<float> kb)
-{
-    using namespace p2;
-    __shared__ __align__(16) float plane[3][T4_PN];
-    __shared__ float Ylo[3][T4_NT], Yhi[3][T4_NT];
-
-    const int tx = threadIdx.x, ty = threadIdx.y;
-    const int tid = tx + T4_TX * ty;
-    const int i0 = blockIdx.x * (T4_TX - 1);
-    const int j0 = blockIdx.y * (2 * T4_TY - 1);
-    const int k0 = blockIdx.z * oz;
-    const int ex = i0 - 1 + tx;
-    const int ey_lo = j0 - 1 + ty, ey_hi = ey_lo + T4_TY;
-    const bool xok = ex >= 0 && ex < g.nelx;
-    const bool ok_lo = xok && ey_lo >= 0 && ey_lo < g.nely;
-    const bool ok_hi = xok && ey_hi >= 0 && ey_hi < g.nely;
-    const bool xown = tx < T4_TX - 1 && (i0 + tx) < g.nnx;
-    const bool own_lo = xown && (j0 + ty) < g.nny;
-    const bool own_hi = xown && ty < T4_TY - 1 && (j0 + ty + T4_TY) < g.nny;
-    const bool mask_in = (flags & TF_MASK_INPUT) && node_fixed != nullptr;
-    const int pn = g.nnx * g.nny, pn3 = 3 * pn;
-    const uint8_t* col_or = node_fixed ? node_fixed + g.n_nodes : nullptr;
-    const uint8_t* col_and = node_fixed ? col_or + pn : nullptr;
-
-    int s_off[T4_NS], s_node[T4_NS], s_c[T4_NS];
-    unsigned okbits = 0u, mskbits = 0u;
-#pragma unroll
-    for (int q = 0; q < T4_NS; ++q) {
-        const int idx = tid + q * T4_NT;
-        const int r = idx / T4_PW, f = idx - r * T4_PW;
-        const int ii = i0 - 1 + f / 3, jj = j0 - 1 + r, c = f % 3;
-        const bool ok = idx < T4_PN && ii >= 0 && ii < g.nnx && jj >= 0 && jj < g.nny;
-        const int node = ok ? ii + g.nnx * jj : 0;
-        s_off[q] = 3 * node + c;
-        s_node[q] = node;
-        s_c[q] = c;
-        bool keep = ok;
-        if (ok && mask_in) {
-            if ((col_and[node] >> c) & 1u) keep = false;
-            else if ((col_or[node] >> c) & 1u) mskbits |= 1u << q;
-        }
-        if (keep) okbits |= 1u << q;
-    }
-    auto stage = [&](int kz, float* buf) {
-        const bool zok = kz >= 0 && kz < g.nnz;
-        const float* vb = v + (long long)min(max(kz, 0), g.nnz - 1) * pn3;
-        unsigned take = zok ? okbits : 0u;
-        if (zok && mskbits) {
-#pragma unroll
-            for (int q = 0; q < T4_NS; ++q)
-                if (((mskbits >> q) & 1u) && ((node_fixed[kz * pn + s_node[q]] >> s_c[q]) & 1u))
-                    take &= ~(1u << q);
-        }
-#pragma unroll
-        for (int q = 0; q < T4_NS; ++q) {
-            const int idx = tid + q * T4_NT;
-            if (q < T4_NS - 1 || idx < T4_PN) cp_async_4(buf + idx, vb + s_off[q], (take >> q) & 1u);
-        }
-        cp_async_commit();
-    };
-    const int po_lo = ty * T4_PW + 3 * tx, po_hi = po_lo + T4_TY * T4_PW;
-    auto pv = [&](const float* buf, int ox, int oy, int c) -> f2 {
-        const int o = oy * T4_PW + 3 * ox + c;
-        return mk(buf[po_lo + o], buf[po_hi + o]);
-    };
-    const int el_plane = g.nelx * g.nely;
-    const int el_lo = ex + g.nelx * ey_lo, el_hi = ex + g.nelx * ey_hi;
-    auto scale_at = [&](int ez) -> f2 {
-        const bool zok = ez >= 0 && ez < g.nelz;
-        return mk((ok_lo && zok) ? ld_nc(scale + el_lo + el_plane * ez) : 0.f,
-                  (ok_hi && zok) ? ld_nc(scale + el_hi + el_plane * ez) : 0.f);
-    };
-
-    const int n_layers = min(oz, g.nnz - k0) + 1;
-    float* b_cur = plane[0];
-    float* b_top = plane[1];
-    float* b_nxt = plane[2];
-    stage(k0 - 1, b_cur);
-    stage(k0, b_top);
-    cp_async_wait_all();
-    __syncthreads();
-    f2 XYb[3][4];
-#pragma unroll
-    for (int c = 0; c < 3; ++c)
-        face_fwd(pv(b_cur, 0, 0, c), pv(b_cur, 1, 0, c), pv(b_cur, 0, 1, c), pv(b_cur, 1, 1, c), XYb[c]);
-    f2 Gt[3][4];
-#pragma unroll
-    for (int c = 0; c < 3; ++c)
-#pragma unroll
-        for (int q = 0; q < 4; ++q) Gt[c][q] = mk(0.f, 0.f);
-    f2 s_cur = scale_at(k0 - 1);
-    double dot = 0.0;
-    const int own_lo0 = (i0 + tx) + g.nnx * (j0 + ty);
-    const int own_hi0 = own_lo0 + g.nnx * T4_TY;
-
-    for (int L = 0; L < n_layers; ++L) {
-        const int ez = k0 - 1 + L;
-        cp_async_wait_all();
-        __syncthreads();                                   // (A)
-        if (L + 1 < n_layers) stage(ez + 2, b_nxt);
-        const f2 s_next = scale_at(ez + 1);
-        const bool wr = L >= 1;
-        unsigned bits_lo = 0u, bits_hi = 0u;
-        if (wr && node_fixed) {
-            if (own_lo) bits_lo = node_fixed[own_lo0 + ez * pn];
-            if (own_hi) bits_hi = node_fixed[own_hi0 + ez * pn];
-        }
-        f2 pown[3];
-        if (DOT) {
-#pragma unroll
-            for (int c = 0; c < 3; ++c) pown[c] = pv(b_cur, 1, 1, c);
-        }
-        f2 h[3][8];
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-            f2 XYt[4];
-            face_fwd(pv(b_top, 0, 0, c), pv(b_top, 1, 0, c), pv(b_top, 0, 1, c), pv(b_top, 1, 1, c), XYt);
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                h[c][q] = add(XYb[c][q], XYt[q]);
-                h[c][q + 4] = sub(XYt[q], XYb[c][q]);
-                XYb[c][q] = XYt[q];
-            }
-        }
-#pragma unroll
-        for (int c = 0; c < 3; ++c)
-#pragma unroll
-            for (int m = 1; m < 8; ++m) h[c][m] = mul(h[c][m], s_cur);
-        f2 gm[3][8];
-#pragma unroll
-        for (int c = 0; c < 3; ++c) gm[c][0] = mk(0.f, 0.f);
-#pragma unroll
-        for (int q = 0; q < 8; ++q)
-#pragma unroll
-            for (int c = 0; c < 3; ++c) {
-                const int m = q ^ (1 << c);
-                if (m == 0) continue;
-                f2 acc = mk(0.f, 0.f);
-#pragma unroll
-                for (int d = 0; d < 3; ++d) {
-                    const int n = q ^ (1 << d);
-                    if (n == 0) continue;
-                    acc = fmab(kb.b[q][c][d], h[d][n], acc);
-                }
-                gm[c][m] = acc;
-            }
-        f2 corner[3][4];
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-            f2 H[4];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                H[q] = add(Gt[c][q], sub(gm[c][q], gm[c][q + 4]));
-                Gt[c][q] = add(gm[c][q], gm[c][q + 4]);
-            }
-            face_inv(H, corner[c]);
-        }
-        f2 xr0[3], xr1[3];
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-            const f2 r0 = corner[c][0], r2 = corner[c][2];
-            xr0[c] = add(corner[c][1], mk(__shfl_down_sync(0xffffffffu, r0.x, 1), __shfl_down_sync(0xffffffffu, r0.y, 1)));
-            xr1[c] = add(corner[c][3], mk(__shfl_down_sync(0xffffffffu, r2.x, 1), __shfl_down_sync(0xffffffffu, r2.y, 1)));
-            Ylo[c][tid] = xr0[c].x;
-            Yhi[c][tid] = xr0[c].y;
-        }
-        __syncthreads();                                   // (B)
-        if (wr) {
-#pragma unroll
-            for (int c = 0; c < 3; ++c) {
-                // node row j0+ty (lo) takes row ty+1's oy=0 sums: lo of ty+1, or hi of ty=0
-                const float below_lo = (ty < T4_TY - 1) ? Ylo[c][tid + T4_TX] : Yhi[c][tx];
-                const float below_hi = Yhi[c][min(tid + T4_TX, T4_NT - 1)];
-                if (own_lo) {
-                    float acc = xr1[c].x + below_lo;
-                    const int d = 3 * (own_lo0 + ez * pn) + c;
-                    if (flags & TF_ACCUMULATE) acc += w[d];
-                    const bool fx = (bits_lo >> c) & 1u;
-                    if ((flags & TF_PASS_FIXED) && fx) acc = v[d];
-                    w[d] = acc;
-                    if (DOT) dot += (double)(fx ? v[d] : pown[c].x) * (double)acc;
-                }
-                if (own_hi) {
-                    float acc = xr1[c].y + below_hi;
-                    const int d = 3 * (own_hi0 + ez * pn) + c;
-                    if (flags & TF_ACCUMULATE) acc += w[d];
-                    const bool fx = (bits_hi >> c) & 1u;
-                    if ((flags & TF_PASS_FIXED) && fx) acc = v[d];
-                    w[d] = acc;
-                    if (DOT) dot += (double)(fx ? v[d] : pown[c].y) * (double)acc;
-                }
-            }
-        }
-        s_cur = s_next;
-        float* t = b_cur;
-        b_cur = b_top;
-        b_top = b_nxt;
-        b_nxt = t;
-    }
-
-    if (DOT) {
-        __shared__ double sh[T4_NT / 32];
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) dot += __shfl_down_sync(0xffffffffu, dot, o);
-        if ((tid & 31) == 0) sh[tid >> 5] = dot;
-        __syncthreads();
-        if (tid == 0) {
-            double s = 0.0;
-            for (int i = 0; i < T4_NT / 32; ++i) s += sh[i];
-            dot_part[blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z)] = s;
-        }
-    }
-}
-
 struct TileShape {
     dim3 grid;
     int oz;
+    int cz = 1;  // thread-block cluster height (z chunks per cluster); 1 = no cluster
 };
 
-// FP32 default is the scalar k_grid_tile3 (24 resident warps/SM); TF_TILE4=1
-// selects the packed two-column k_grid_tile4 (fewer instructions, but its
-// register footprint halves occupancy -- measured slower on B200, kept for A/B)
-static bool tile3_forced()
+// grid for (oz, cz): z padded to whole clusters (padding CTAs own no planes)
+template <typename T>
+TileShape tile_shape_ozcz(const Grid& g, int oz, int cz)
 {
-    static int v = -1;
-    if (v < 0) {
-        const char* e = getenv("TF_TILE4");
-        v = (e && e[0] == '1') ? 0 : 1;
-    }
-    return v == 1;
+    constexpr int TILE_BY = TileDims<T>::BY;
+    const int tx = (g.ihi - g.ilo + TILE_BX - 2) / (TILE_BX - 1);
+    const int ty = (g.nny + TILE_BY - 2) / (TILE_BY - 1);
+    const int chunks = (g.nnz + oz - 1) / oz;
+    cz = std::max(1, std::min(cz, chunks));
+    return {dim3(tx, ty, (chunks + cz - 1) / cz * cz), oz, cz};
 }
 
 // The isotropic block form (khat_iso) in FP64 only: there the kernel is
@@ -1471,18 +1147,16 @@ bool tile_iso_enabled()
 {
     const char* eg = getenv("TF_TILE_GENERIC");
     if (eg && eg[0] == '1') return false;
-    if (sizeof(T) == 8) return true;
-    const char* e32 = getenv("TF_TILE_ISO32");
-    return e32 && e32[0] == '1';
+    return sizeof(T) == 8;
 }
 template bool tile_iso_enabled<float>();
 template bool tile_iso_enabled<double>();
 
-// TF_TILE3=1: the v3 kernel instead of the lean v5 (A/B, bitwise-identical)
-static bool tile5_disabled()
+// TF_TILE_CLUSTER=0: no cluster z split (tile6 degenerates to tile5's march)
+static bool tile_cluster_enabled()
 {
-    const char* e = getenv("TF_TILE3");  // read per launch: A/B in one process
-    return e && e[0] == '1';
+    const char* e = getenv("TF_TILE_CLUSTER");
+    return !(e && e[0] == '0');
 }
 
 template <typename T>
@@ -1495,10 +1169,8 @@ static int tile_slots()
         int dev = 0, nsm = 148, per_sm = 1;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-        if (sizeof(T) == 4 && !tile3_forced())
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_grid_tile4<true>, T4_NT, 0);
-        else
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_grid_tile3<T, true>, TileDims<T>::NT, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+            &per_sm, k_grid_tile6<T, true, true, true, TF_TILE_P, false, false>, TileDims<T>::NT, 0);
         s = std::max(1, per_sm) * nsm;
     }
     return s;
@@ -1547,65 +1219,84 @@ static bool tile_autotune_enabled()
     return !(o && atoi(o) > 0);
 }
 
-// z-chunk height per (grid shape, x-range, precision): measured once with
-// CUDA events over candidate heights (min of 3 launches each), then cached.
-// Returns 0 when it cannot tune (stream capture in progress).
+// Launch shape per (grid shape, x-range, precision): z-chunk height and
+// cluster height measured once with CUDA events over the candidates (min of
+// 3 x 4 back-to-back launches each), then cached.  Every candidate gives the
+// same bits (tile6 sums every DOF in the same order for any chunking), so
+// this only picks the fastest.  Returns {0, 0} when it cannot tune (stream
+// capture in progress) or when lookup_only finds nothing.
 template <typename F>
-static int tile_tuned_oz(const Grid& g, int prec, cudaStream_t st, F&& launch, bool lookup_only = false)
+static std::pair<int, int> tile_tuned(const Grid& g, int prec, cudaStream_t st, F&& launch, bool lookup_only = false)
 {
     static std::mutex mu;
-    static std::map<std::array<int, 6>, int> cache;
+    static std::map<std::array<int, 6>, std::pair<int, int>> cache;
     const std::array<int, 6> key = {g.nelx, g.nely, g.nelz, g.ilo, g.ihi, prec};
     {
         std::lock_guard<std::mutex> lk(mu);
         auto it = cache.find(key);
         if (it != cache.end()) return it->second;
-        if (lookup_only) return 0;
+        if (lookup_only) return {0, 0};
     }
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
     if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) {
         cudaGetLastError();
-        return 0;
+        return {0, 0};
     }
     static const int cands[] = {2, 3, 4, 5, 6, 7, 8, 10, 12, 16, 24, 32};
     cudaEvent_t e0, e1;
     if (cudaEventCreate(&e0) != cudaSuccess || cudaEventCreate(&e1) != cudaSuccess) {
         cudaGetLastError();
-        return 0;
+        return {0, 0};
     }
     // candidates must cover every SM (a shape that leaves SMs idle can win a
-    // single-launch timing through lower launch latency, not throughput);
-    // each is timed as 4 back-to-back launches (the solver's usage), min of 3
+    // single-launch timing through lower launch latency, not throughput)
     int dev = 0, nsm = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     const long long cols = (long long)((g.ihi - g.ilo + TILE_BX - 2) / (TILE_BX - 1)) *
                            ((g.nny + TileDimsBy(prec) - 2) / (TileDimsBy(prec) - 1));
-    int best = 0;
+    std::pair<int, int> best = {0, 0};
     float best_ms = 1e30f;
     for (int oz : cands) {
         if (oz > std::max(2, g.nnz)) break;
-        if (oz > 2 && cols * ((g.nnz + oz - 1) / oz) < nsm) break;
-        if (launch(oz) != TF_OK) break;  // warm-up
-        float t = 1e30f;
-        for (int r = 0; r < 3; ++r) {
-            cudaEventRecord(e0, st);
-            for (int k = 0; k < 4; ++k) launch(oz);
-            cudaEventRecord(e1, st);
-            cudaEventSynchronize(e1);
-            float ms = 0.f;
-            cudaEventElapsedTime(&ms, e0, e1);
-            t = std::min(t, ms);
+        const int chunks = (g.nnz + oz - 1) / oz;
+        if (oz > 2 && cols * chunks < nsm) break;
+        int czs[4] = {1, 0, 0, 0}, ncz = 1;
+        if (tile_cluster_enabled() && chunks > 1) {
+            // whole column in one cluster when it fits, else full clusters of 8 / 4
+            const int opts[3] = {std::min(chunks, 8), 4, 2};
+            for (int o : opts) {
+                bool dup = false;
+                for (int i = 0; i < ncz; ++i) dup |= czs[i] == o;
+                if (!dup && o > 1 && o <= chunks) czs[ncz++] = o;
+            }
         }
-        if (t < best_ms) {
-            best_ms = t;
-            best = oz;
+        for (int i = 0; i < ncz; ++i) {
+            const int cz = czs[i];
+            if (launch(oz, cz) != TF_OK) {  // warm-up (an unsupported cluster shape just drops out)
+                cudaGetLastError();
+                continue;
+            }
+            float t = 1e30f;
+            for (int r = 0; r < 3; ++r) {
+                cudaEventRecord(e0, st);
+                for (int k = 0; k < 4; ++k) launch(oz, cz);
+                cudaEventRecord(e1, st);
+                cudaEventSynchronize(e1);
+                float ms = 0.f;
+                cudaEventElapsedTime(&ms, e0, e1);
+                t = std::min(t, ms);
+            }
+            if (t < best_ms) {
+                best_ms = t;
+                best = {oz, cz};
+            }
         }
     }
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     cudaGetLastError();
-    if (best > 0) {
+    if (best.first > 0) {
         std::lock_guard<std::mutex> lk(mu);
         cache[key] = best;
     }
@@ -1618,8 +1309,8 @@ TileShape tile_shape_current(const Grid& g)
 {
     TileShape sh = tile_shape<T>(g);
     if (tile_autotune_enabled()) {
-        const int oz = tile_tuned_oz(g, (int)sizeof(T), nullptr, [](int) { return TF_ERR_ARG; }, true);
-        if (oz > 0) sh = tile_shape_oz<T>(g, oz);
+        const auto t = tile_tuned(g, (int)sizeof(T), nullptr, [](int, int) { return TF_ERR_ARG; }, true);
+        if (t.first > 0) sh = tile_shape_ozcz<T>(g, t.first, t.second);
     }
     return sh;
 }
@@ -1629,6 +1320,54 @@ long long grid_tile_blocks(const Grid& g)
 {
     TileShape s = tile_shape<T>(g);
     return (long long)s.grid.x * s.grid.y * s.grid.z;
+}
+
+// TF_TILE5=1: the previous production kernel (A/B; bitwise the same output)
+static bool tile5_forced()
+{
+    const char* e = getenv("TF_TILE5");  // read per launch: A/B in one process
+    return e && e[0] == '1';
+}
+
+// tile6 launch; a cluster height > 1 goes through cudaLaunchKernelEx with the
+// (1, 1, cz) cluster attribute
+template <typename T, bool M, bool PS, bool DT, bool ISO, bool CL>
+static cudaError_t launch_tile6(const TileShape& sh, cudaStream_t st, const Grid& g, int acc, const T* scale,
+                                const T* v, T* w, const uint8_t* node_fixed, double* dot_part,
+                                const KhatBlocks<T>& kb, const KhatIso<T>& ki)
+{
+    auto kern = k_grid_tile6<T, M, PS, DT, TF_TILE_P, ISO, CL>;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = sh.grid;
+    cfg.blockDim = dim3(TILE_BX, TileDims<T>::BY, 1);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 1;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = CL ? (unsigned)sh.cz : 1u;
+    cfg.attrs = attr;
+    cfg.numAttrs = CL ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, g, sh.oz, sh.cz, acc, scale, v, w, node_fixed, dot_part, kb, ki);
+}
+
+// the isotropic block form is instantiated for FP64 only (tile_iso_enabled)
+template <typename T, bool M, bool PS, bool DT>
+static cudaError_t launch_tile6_flags(const TileShape& sh, bool iso, cudaStream_t st, const Grid& g, int acc,
+                                      const T* scale, const T* v, T* w, const uint8_t* node_fixed,
+                                      double* dot_part, const KhatBlocks<T>& kb, const KhatIso<T>& ki)
+{
+    if constexpr (sizeof(T) == 8) {
+        if (iso)
+            return sh.cz > 1 ? launch_tile6<T, M, PS, DT, true, true>(sh, st, g, acc, scale, v, w, node_fixed,
+                                                                      dot_part, kb, ki)
+                             : launch_tile6<T, M, PS, DT, true, false>(sh, st, g, acc, scale, v, w, node_fixed,
+                                                                       dot_part, kb, ki);
+    }
+    return sh.cz > 1
+               ? launch_tile6<T, M, PS, DT, false, true>(sh, st, g, acc, scale, v, w, node_fixed, dot_part, kb, ki)
+               : launch_tile6<T, M, PS, DT, false, false>(sh, st, g, acc, scale, v, w, node_fixed, dot_part, kb, ki);
 }
 
 // returns TF_ERR_UNSUPPORTED when Ke lacks the parity-block structure
@@ -1642,22 +1381,13 @@ int launch_grid_tile(const Grid& g, const T* ke_host, const T* scale, const T* v
         set_error("structured grid too large for int32 DOF indices");
         return TF_ERR_ARG;
     }
-    const bool full_range = g.ilo == 0 && g.ihi == g.nnx;  // tile4 has no x-range support
+    KhatIso<T> ki{};
+    const bool iso = tile_iso_enabled<T>() && khat_iso<T>(ke_host, &ki);
+    const uint32_t f = flags & (TF_MASK_INPUT | TF_PASS_FIXED | TF_ACCUMULATE);
+    constexpr uint32_t MP = TF_MASK_INPUT | TF_PASS_FIXED;
     auto launch_shape = [&](const TileShape& sh) -> int {
-        if constexpr (sizeof(T) == 4) {
-            if (!tile3_forced() && full_range) {
-                dim3 block4(T4_TX, T4_TY, 1);
-                if (dot_part)
-                    k_grid_tile4<true><<<sh.grid, block4, 0, st>>>(g, sh.oz, scale, v, w, node_fixed, flags, dot_part, kb);
-                else
-                    k_grid_tile4<false><<<sh.grid, block4, 0, st>>>(g, sh.oz, scale, v, w, node_fixed, flags, nullptr, kb);
-                TF_CHECK_LAUNCH();
-                return TF_OK;
-            }
-        }
-        dim3 block(TILE_BX, TileDims<T>::BY, 1);
-        KhatIso<T> ki{};
-        const bool iso = tile_iso_enabled<T>() && khat_iso<T>(ke_host, &ki);
+        if (tile5_forced() && sh.cz == 1) {
+            dim3 block(TILE_BX, TileDims<T>::BY, 1);
 #define T5(M, PS, AC, DT, DP)                                                                              \
     do {                                                                                                   \
         if (iso)                                                                                           \
@@ -1667,49 +1397,42 @@ int launch_grid_tile(const Grid& g, const T* ke_host, const T* scale, const T* v
             k_grid_tile5<T, M, PS, AC, DT, TF_TILE_P, false><<<sh.grid, block, 0, st>>>(g, sh.oz, scale, v, w, \
                                                                                      node_fixed, DP, kb, ki); \
     } while (0)
-        if (!tile5_disabled()) {
-            // compile-time flag variants of the lean kernel; others fall back to tile3
-            const uint32_t f = flags & (TF_MASK_INPUT | TF_PASS_FIXED | TF_ACCUMULATE);
-            constexpr uint32_t MP = TF_MASK_INPUT | TF_PASS_FIXED;
-            if (f == MP && dot_part) {
-                T5(true, true, false, true, dot_part);
-                TF_CHECK_LAUNCH();
-                return TF_OK;
+            if (f == MP && dot_part) T5(true, true, false, true, dot_part);
+            else if (f == MP) T5(true, true, false, false, nullptr);
+            else if (f == TF_MASK_INPUT) T5(true, false, false, false, nullptr);
+            else if (f == 0) T5(false, false, false, false, nullptr);
+            else {
+                set_error("TF_TILE5: flag combination not instantiated");
+                return TF_ERR_ARG;
             }
-            if (f == MP && !dot_part) {
-                T5(true, true, false, false, nullptr);
-                TF_CHECK_LAUNCH();
-                return TF_OK;
-            }
-            if (f == TF_MASK_INPUT && !dot_part) {  // slab-local products (pass-through after the exchange)
-                T5(true, false, false, false, nullptr);
-                TF_CHECK_LAUNCH();
-                return TF_OK;
-            }
-            if (f == 0 && !dot_part) {  // raw K v (fused_serial-style contract)
-                T5(false, false, false, false, nullptr);
-                TF_CHECK_LAUNCH();
-                return TF_OK;
-            }
-        }
 #undef T5
-        if (dot_part)
-            k_grid_tile3<T, true><<<sh.grid, block, 0, st>>>(g, sh.oz, scale, v, w, node_fixed, flags, dot_part, kb);
-        else
-            k_grid_tile3<T, false><<<sh.grid, block, 0, st>>>(g, sh.oz, scale, v, w, node_fixed, flags, nullptr, kb);
-        TF_CHECK_LAUNCH();
+            TF_CHECK_LAUNCH();
+            return TF_OK;
+        }
+        cudaError_t e;
+        // every flag combination the C ABI accepts, as compile-time variants
+#define T6(M, PS) \
+    (dot_part ? launch_tile6_flags<T, M, PS, true>(sh, iso, st, g, acc, scale, v, w, node_fixed, dot_part, kb, ki) \
+              : launch_tile6_flags<T, M, PS, false>(sh, iso, st, g, acc, scale, v, w, node_fixed, nullptr, kb, ki))
+        const int acc = (f & TF_ACCUMULATE) ? 1 : 0;
+        switch (f & MP) {
+        case MP: e = T6(true, true); break;
+        case TF_MASK_INPUT: e = T6(true, false); break;
+        case TF_PASS_FIXED: e = T6(false, true); break;
+        default: e = T6(false, false); break;
+        }
+#undef T6
+        TF_CUDA_TRY(e);
         return TF_OK;
     };
     TileShape sh = tile_shape<T>(g);
-    // Plain products (no CG partials, no accumulation): the z-chunk height is
-    // autotuned once per grid shape on first use outside stream capture (the
-    // result does not depend on the chunking -- every DOF is summed in the
-    // same order -- so this only picks the fastest launch shape).
+    // Plain products (no CG partials, no accumulation): the launch shape is
+    // autotuned once per grid shape on first use outside stream capture
     if (!dot_part && !(flags & TF_ACCUMULATE) && tile_autotune_enabled()) {
-        const int oz = tile_tuned_oz(g, (int)sizeof(T), st, [&](int cand) {
-            return launch_shape(tile_shape_oz<T>(g, cand));
+        const auto t = tile_tuned(g, (int)sizeof(T), st, [&](int oz, int cz) {
+            return launch_shape(tile_shape_ozcz<T>(g, oz, cz));
         });
-        if (oz > 0) sh = tile_shape_oz<T>(g, oz);
+        if (t.first > 0) sh = tile_shape_ozcz<T>(g, t.first, t.second);
     }
     return launch_shape(sh);
 }

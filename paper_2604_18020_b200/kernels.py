@@ -59,10 +59,8 @@ def fused_serial(edof, ke, scale, v, out) -> None:
     s_d = D.to_dev(scale, dt)
     v_d = D.to_dev(v, dt)
     o_d = D.to_dev(out, dt)
-    off = t.empty(n_dof + 1, dtype=t.int64, device=e_d.device)
-    ent = t.empty(n_elem * 24, dtype=t.int32, device=e_d.device)
+    off, ent = _csr(e_d, n_elem, n_dof)
     rows = t.empty(n_elem * 24, dtype=t.float64, device=e_d.device)
-    _lib.call("tf_edof_csr_build", D.ptr(e_d), n_elem, n_dof, D.ptr(off), D.ptr(ent), D.stream_ptr())
     ke_h = np.ascontiguousarray(ke, dtype=dt)
     _lib.call(f"tf_matvec_edof_pull_{_sfx(v)}", D.ptr(e_d), ke_h.ctypes.data, D.ptr(s_d), D.ptr(v_d), D.ptr(o_d),
               n_elem, n_dof, D.ptr(off), D.ptr(ent), D.ptr(rows), 1, D.stream_ptr())
@@ -96,7 +94,21 @@ def gemm(u_elem, ke, scale):
 
 
 def scatter_serial(edof, f_elem, acc) -> None:
-    """acc += scatter(f_elem); FP64 accumulation (operator.py:107-114)."""
+    """acc += scatter(f_elem) in ascending element order, FP64 accumulation --
+    bitwise _kernels_numba.py:129-132 (operator.py:107-114)."""
+    dt = np.asarray(f_elem).dtype
+    edof = np.ascontiguousarray(edof, dtype=np.int32)
+    a_d = D.to_dev(acc, np.float64)
+    e_d = D.to_dev(edof, np.int32)
+    f_d = D.to_dev(f_elem, dt)
+    off, ent = _csr(e_d, edof.shape[0], acc.shape[0])
+    _lib.call(f"tf_scatter_pull_{_sfx(f_elem)}", D.ptr(off), D.ptr(ent), D.ptr(f_d), D.ptr(a_d), acc.shape[0],
+              D.stream_ptr())
+    acc[...] = a_d.cpu().numpy().astype(acc.dtype)
+
+
+def scatter_atomic(edof, f_elem, acc) -> None:
+    """acc += scatter(f_elem) with red.global.add (FP64), any order."""
     dt = np.asarray(f_elem).dtype
     a_d = D.to_dev(acc, np.float64)
     e_d = D.to_dev(edof, np.int32)
@@ -106,17 +118,29 @@ def scatter_serial(edof, f_elem, acc) -> None:
     acc[...] = a_d.cpu().numpy().astype(acc.dtype)
 
 
-scatter_atomic = scatter_serial
+
+
+def _csr(e_d, n_elem, n_dof):
+    """DOF -> (element*24 + row) entries in ascending element order (device)."""
+    t = D.torch()
+    off = t.empty(n_dof + 1, dtype=t.int64, device=e_d.device)
+    ent = t.empty(n_elem * 24, dtype=t.int32, device=e_d.device)
+    _lib.call("tf_edof_csr_build", D.ptr(e_d), n_elem, n_dof, D.ptr(off), D.ptr(ent), D.stream_ptr())
+    return off, ent
 
 
 def jacobi_diag(edof, ke_diag, scale, out) -> None:
+    """out[edof[e, l]] += scale[e] * ke_diag[l] in ascending element order,
+    FP64 accumulation -- bitwise _kernels_numba.py:217-226."""
     dt = np.asarray(scale).dtype
+    edof = np.ascontiguousarray(edof, dtype=np.int32)
     a_d = D.to_dev(out, np.float64)
     kd = np.ascontiguousarray(ke_diag, dtype=dt)
     e_d = D.to_dev(edof, np.int32)
     s_d = D.to_dev(scale, dt)
-    _lib.call(f"tf_jacobi_edof_{_sfx(scale)}", D.ptr(e_d), kd.ctypes.data, D.ptr(s_d), D.ptr(a_d),
-              edof.shape[0], D.stream_ptr())
+    off, ent = _csr(e_d, edof.shape[0], out.shape[0])
+    _lib.call(f"tf_jacobi_edof_pull_{_sfx(scale)}", D.ptr(off), D.ptr(ent), kd.ctypes.data, D.ptr(s_d),
+              D.ptr(a_d), out.shape[0], D.stream_ptr())
     out[...] = a_d.cpu().numpy().astype(out.dtype)
 
 
@@ -156,8 +180,21 @@ def _fused_bf16(edof, ke, scale, v, out, mode):
 
 
 def fused_serial_bf16(edof, ke, scale, v, out) -> None:
-    """Deterministic fused K v with per-term bf16(s K); v pre-quantized; out += (FP32)."""
-    _fused_bf16(edof, ke, scale, v, out, _lib.TF_SCATTER_COLORED)
+    """fused K v with per-term bf16(s K), v pre-quantized, out += (FP32) in the
+    reference's element order -- bitwise _kernels_numba.py:166-177."""
+    t = D.torch()
+    edof = np.ascontiguousarray(edof, dtype=np.int32)
+    n_elem, n_dof = edof.shape[0], out.shape[0]
+    e_d = D.to_dev(edof, np.int32)
+    s_d = D.to_dev(scale, np.float32)
+    v_d = D.to_dev(v, np.float32)
+    o_d = D.to_dev(out, np.float32)
+    off, ent = _csr(e_d, n_elem, n_dof)
+    rows = t.empty(n_elem * 24, dtype=t.float64, device=e_d.device)
+    ke_h = np.ascontiguousarray(ke, dtype=np.float32)
+    _lib.call("tf_matvec_edof_pull_bf16", D.ptr(e_d), ke_h.ctypes.data, D.ptr(s_d), D.ptr(v_d), D.ptr(o_d),
+              n_elem, n_dof, D.ptr(off), D.ptr(ent), D.ptr(rows), 1, D.stream_ptr())
+    out[...] = o_d.cpu().numpy()
 
 
 def fused_atomic_bf16(edof, ke, scale, v, out) -> None:

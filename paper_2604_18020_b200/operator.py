@@ -370,9 +370,11 @@ class MatFreeOperator:
                       D.ptr(self._scale_dev), D.ptr(diag), D.ptr(inv), D.ptr(dev.node_fixed),
                       D.stream_ptr())
         else:
+            # the reference's jacobi_diag order (ascending element per DOF): bitwise
             acc = t.zeros(self.n_dof, dtype=t.float64, device=diag.device)
-            _lib.call(f"tf_jacobi_edof_{sfx}", D.ptr(dev.edof_raw), kd.ctypes.data,
-                      D.ptr(self._scale_dev), D.ptr(acc), self.mesh.n_elem, D.stream_ptr())
+            off, ent, _ = dev.csr()
+            _lib.call(f"tf_jacobi_edof_pull_{sfx}", D.ptr(off), D.ptr(ent), kd.ctypes.data,
+                      D.ptr(self._scale_dev), D.ptr(acc), self.n_dof, D.stream_ptr())
             diag.copy_(acc)
             if dev.fixed is not None:
                 diag[dev.fixed] = 1.0

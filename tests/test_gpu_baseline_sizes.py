@@ -110,6 +110,9 @@ def test_general_edof_kernels_at_baseline_size(name, prec):
     assert _rel(got, _want(name, prec)) <= TOL[prec]
     se, _ = _op(name, prec, grid_kernel="edof", scatter="serial")
     assert _sha(se.apply(v.astype(se.precision.dtype))) == h["sha256"]
+    # the general-connectivity Jacobi diagonal: the reference's order, bitwise
+    m, edof, bcs, rho, _ = _case(name)
+    assert np.array_equal(se.diagonal(), oracle.diagonal(edof, se.ke, se.scale, bcs.fixed_dofs, m.n_dof))
 
 
 @pytest.mark.parametrize("scale", [0.2, 1.0])

@@ -174,6 +174,59 @@ def cpu_time_cg_c1(threads):
             "kind": "port (oracle C fused_atomic + numpy recurrence)"}
 
 
+def cpu_time_simp_c1(iterations=2):
+    """The reference SIMP loop (oracle/simp.py, pinned to the reference's c1
+    trajectory) on config c1: a bounded sample of `iterations` iterations,
+    on 1 core with the serial scatter (BASELINE.md's 2.70 s/iteration
+    protocol) and on all host cores with the OpenMP atomic scatter."""
+    import oracle
+    from oracle import simp as osimp
+    from paper_2604_18020_b200.element import unit_stiffness
+    from paper_2604_18020_b200.mesh import StructuredMesh, build_edof, cantilever_bcs
+
+    m = StructuredMesh(48, 24, 24)
+    b = cantilever_bcs(m)
+    e = build_edof(m)
+    out = {"config": "c1 48x24x24 SIMP, FP64 (p=3, beta=1, move 0.2, rmin 1.5)",
+           "kind": "port (oracle/simp.py + C fused kernels + numpy PCG)", "iterations": iterations}
+    for tag, threads, scatter in (("serial_1core", 1, "serial"), ("atomic_all_cores", os.cpu_count() or 1,
+                                                                     "parallel_atomic")):
+        oracle.set_threads(threads)
+        t0 = time.perf_counter()
+        hist, _ = osimp.run_simp((48, 24, 24), e, b.fixed_dofs, b.force, 0.3, [(1, 30, 3.0, 1.0, 0.2, 1.5)], 1.5,
+                                 unit_stiffness(0.3), scatter=scatter, iterations=iterations)
+        sec = time.perf_counter() - t0
+        out[tag] = {"s_per_iter": sec / iterations, "cores": threads,
+                    "cg_iterations": [h["cg_iterations"] for h in hist],
+                    "compliance": [h["compliance"] for h in hist]}
+    oracle.set_threads(os.cpu_count() or 1)
+    return out
+
+
+def cpu_time_cg_c2(threads, iterations=40):
+    """The reference's PCG on c2 (cold, rho 0.5, p 3, FP64; the 511-iteration
+    anchor) through the oracle port on all host cores: a bounded sample of
+    the first `iterations` iterations, reported per iteration."""
+    import oracle
+    from paper_2604_18020_b200.element import SimpParams, simp_scale, unit_stiffness
+    from paper_2604_18020_b200.mesh import build_edof, make_preset
+
+    pb = make_preset("cantilever", 1.0)
+    m = pb.mesh
+    edof = build_edof(m)
+    ke = np.ascontiguousarray(unit_stiffness(0.3))
+    scale = simp_scale(np.full(m.n_elem, 0.5), SimpParams(3.0))
+    oracle.set_threads(threads)
+    A = lambda x: oracle.apply(edof, ke, scale, x, pb.bcs.fixed_dofs, m.n_dof, "fused", "parallel_atomic")  # noqa: E731
+    d = oracle.diagonal(edof, ke, scale, pb.bcs.fixed_dofs, m.n_dof)
+    t0 = time.perf_counter()
+    x, info = oracle.pcg(A, pb.bcs.force, d, 1e-5, iterations)
+    sec = time.perf_counter() - t0
+    return {"config": f"c2 120x60x30 cold FP64 PCG, first {info['iterations']} iterations",
+            "us_per_iteration": sec / max(1, info["iterations"]) * 1e6, "threads": threads,
+            "kind": "port (oracle C fused_atomic + numpy recurrence)"}
+
+
 def run_reference(args):
     rank, world, local = dist_env()
     if rank != 0:
@@ -333,6 +386,9 @@ def run_ours(args):
     n_dof_total = gm.n_dof  # global DOFs (interface planes counted once)
     gdof = n_dof_total / (ms * 1e-3) / 1e9
 
+    # the timed product against the reference's apply on the same inputs
+    vs_ref = reference_check(args.config, prec, w.double().cpu().numpy()) if world == 1 else None
+
     # warm-L2 (solver-like back-to-back) rate, for context
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -467,10 +523,17 @@ def run_ours(args):
         if not args.no_cpu:
             threads = os.cpu_count() or 1
             mm, sec, reps = cpu_time_apply(dims, prec, threads, budget_s=12.0)
+            m1, sec1, reps1 = cpu_time_apply(dims, prec, 1, budget_s=6.0)
             cpu = {"value": mm.n_dof / sec / 1e9, "unit": "GDOF/s", "cores": threads,
                    "kind": "port",
                    "sample": f"{reps} fused_atomic applies (oracle C port of _kernels_numba.py:183-196, "
-                             f"OpenMP) of {desc}"}
+                             f"OpenMP) of {desc}",
+                   "serial_1core": {"value": m1.n_dof / sec1 / 1e9, "unit": "GDOF/s", "cores": 1,
+                                    "sample": f"{reps1} fused_serial applies (_kernels_numba.py:146-162) of {desc}"}}
+            if simp is not None:
+                simp["cpu"] = cpu_time_simp_c1()
+            if cg is not None:
+                cg["cpu_c2_fp64"] = cpu_time_cg_c2(threads)
         line = {
             "metric": "fused K.v GDOF/s", "value": gdof, "unit": "GDOF/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
@@ -497,6 +560,7 @@ def run_ours(args):
                     "d2h_bytes_per_step": int(m.n_dof * np.dtype(dt).itemsize)},
             "gpu_launches": args.steps * per_step_launches,
             "equivalence_gate_rel_l2": gate_rel,
+            "vs_reference": vs_ref,
             "e2e_path": "MatFreeOperator.apply_stream (cudaHostAlloc host in/out; native 3-stream pipeline, csrc/tf_stream.cu); median of 3 batches of `steps` products after 1 s of PCIe warm-up" if world == 1
                         else "SlabOperator.apply per step (pinned host in/out)",
             "clocks": ck,
@@ -617,8 +681,7 @@ def simp_c1():
     res = run_simp(pb, SimpConfig(schedule=sched, precision="fp64"))
     return {"config": "c1 cantilever 48x24x24, Vf 0.3, p=3, beta=1, move 0.2, rmin 1.5, FP64, 30 its",
             "s_per_iter": res.wall_s / 30, "total_cg_iterations": res.total_cg_iterations,
-            "final_compliance": res.history[-1].compliance,
-            "reference_cpu_s_per_iter": 2.70, "reference_cpu_note": "BASELINE.md sec 2, 1 core"}
+            "final_compliance": res.history[-1].compliance}
 
 
 def simp_c2():
@@ -783,9 +846,6 @@ def cg_c2():
     dt = time.perf_counter() - t0
     out["c1_fp64"] = {"iterations": rep.iterations, "solve_ms": dt * 1e3,
                       "us_per_iteration": dt * 1e6 / max(1, rep.iterations)}
-    out["reference_cpu"] = {"fp64": {"iterations": 511, "s": 27.9, "threads": 8},
-                            "fp32": {"iterations": 1000, "termination": "max_iter"},
-                            "note": "BASELINE.md sec 2 (8-thread numba)"}
     return out
 
 

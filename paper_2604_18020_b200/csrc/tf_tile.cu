@@ -32,12 +32,12 @@
 #include <mutex>
 #include <map>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <type_traits>
 
 #include "tf_common.cuh"
-#include <cooperative_groups.h>
 #include "tf_walsh.cuh"
 
 namespace tf {
@@ -164,7 +164,7 @@ template bool khat_blocks<double>(const double*, KhatBlocks<double>*);
 // ---- device ------------------------------------------------------------------------
 
 // ---------------------------------------------------------------------------
-// The Walsh transforms factorised along the z march (tile5/tile6).
+// The Walsh transforms factorised along the z march.
 //
 // The forward transform is separable: u -> (x, y stages on each xy face) ->
 // (z stage between the bottom and top faces).  The bottom face of layer L is
@@ -201,8 +201,8 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 #endif
 
 // ---------------------------------------------------------------------------
-// v5: the z-factorised march with the bookkeeping stripped and a deep
-// staging ring (kept for A/B behind TF_TILE5=1; tile6 below is production).
+// v5 (production): the z-factorised march with the bookkeeping stripped and
+// a deep staging ring.
 //   * the operator flags are template parameters (the production matvec is
 //     MASK|PASS: no ACCUMULATE branches, no flag tests per DOF);
 //   * node planes AND the element scales of each layer stream in with
@@ -471,340 +471,6 @@ k_grid_tile5(Grid g, int oz, const T* __restrict__ scale, const T* __restrict__ 
     cp_async_wait_n(0);
     __syncthreads();
     node_pass(Y[(n_layers - 1) & 1]);
-
-    if (DOT) {
-        __shared__ double shd[TILE_NT / 32];
-        double dd = (double)dot;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) dd += __shfl_down_sync(0xffffffffu, dd, o);
-        if ((tid & 31) == 0) shd[tid >> 5] = dd;
-        __syncthreads();
-        if (tid == 0) {
-            double s2 = 0.0;
-            for (int i = 0; i < TILE_NT / 32; ++i) s2 += shd[i];
-            dot_part[blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z)] = s2;
-        }
-    }
-}
-
-// ---------------------------------------------------------------------------
-// v6: tile5 + thread-block-cluster z split (the production kernel).
-//
-// A z-chunk's first node plane k0 needs the top-face part of element layer
-// k0-1, which belongs to the chunk below.  tile5 recomputes that layer in
-// every chunk (one halo layer per oz planes: +33 % element work at c2's
-// oz = 3).  Here the chunks of a column are launched as a (1, 1, cz) thread-
-// block cluster; a CTA of cluster rank r > 0 skips the halo layer, keeps the
-// mode-space bottom part D = gm_lo - gm_hi of its first layer in shared
-// memory, and at the end combines it with the lower CTA's final top part Gt
-// read through distributed shared memory: H = Gt + D -- the SAME operands
-// and operation order as the unsplit march, so the output is bitwise
-// identical to tile5 for any chunking or cluster size (tested).  The chunk
-// at k0 = 0 skips its all-zero halo layer the same way (Gt = +0).
-// Cluster-boundary CTAs (rank 0) keep the recomputed halo layer.
-// ---------------------------------------------------------------------------
-template <typename T, bool MASK, bool PASS, bool DOT, int P, bool ISO, bool CL>
-__global__ void __launch_bounds__(TileDims<T>::NT, sizeof(T) == 4 ? (CL ? 2 : TF_TILE_MINB32) : TF_TILE_MINB64)
-k_grid_tile6(Grid g, int oz, int cz, int accumulate, const T* __restrict__ scale, const T* __restrict__ v,
-             T* __restrict__ w,
-             const uint8_t* __restrict__ node_fixed, double* __restrict__ dot_part,
-             const __grid_constant__ KhatBlocks<T> kb, const __grid_constant__ KhatIso<T> ki)
-{
-    constexpr int TILE_BY = TileDims<T>::BY, TILE_NT = TileDims<T>::NT;
-    constexpr int PW = StageSlots<T>::PW, PN = StageSlots<T>::PN, NS = StageSlots<T>::N;
-    constexpr int R = P + 2;                      // ring: plane k in buffer (k - kb0) % R
-    __shared__ __align__(16) T plane[R][PN];
-    __shared__ T sc[R][TILE_NT];                  // element scale of layer k, with plane k
-    __shared__ T Y[2][3][TILE_NT];                // row hand-off, by layer parity
-    // cluster split: D of the first layer (this CTA's bottom part of plane
-    // k0); the exported final Gt (the upper partner's missing top part)
-    // reuses the plane ring, idle once the march is over
-    __shared__ T Dsm[CL ? 12 : 1][CL ? TILE_NT : 1];
-    static_assert(!CL || R * PN >= 12 * TILE_NT, "Gt export does not fit the plane ring");
-
-    const int tx = threadIdx.x, ty = threadIdx.y;
-    const int tid = tx + TILE_BX * ty;
-    const int i0 = g.ilo + blockIdx.x * (TILE_BX - 1);
-    const int j0 = blockIdx.y * (TILE_BY - 1);
-    const int k0 = blockIdx.z * oz;
-    const int crank = CL ? (int)(blockIdx.z % (unsigned)cz) : 0;
-    const bool from_below = CL && crank > 0 && k0 < g.nnz;
-    const bool to_above = CL && crank < cz - 1 && k0 + oz < g.nnz;
-    const bool skip_halo = from_below || k0 == 0;
-    const int kb0 = skip_halo ? k0 : k0 - 1;      // first element layer
-    const int ex = i0 - 1 + tx, ey = j0 - 1 + ty;
-    const bool col_ok = ex >= 0 && ex < g.nelx && ey >= 0 && ey < g.nely;
-    const bool owner = tx < TILE_BX - 1 && ty < TILE_BY - 1 && (i0 + tx) < g.ihi && (j0 + ty) < g.nny;
-    const bool have_nf = node_fixed != nullptr;
-    const int pn = g.nnx * g.nny, pn3 = 3 * pn;
-    const uint8_t* col_or = have_nf ? node_fixed + g.n_nodes : nullptr;
-    const uint8_t* col_and = have_nf ? col_or + pn : nullptr;
-
-    int s_off[NS];
-    unsigned okbits = 0u, mskbits = 0u;
-#pragma unroll
-    for (int q = 0; q < NS; ++q) {
-        const int idx = tid + q * TILE_NT;
-        const int r = idx / PW, f = idx - r * PW;
-        const int ii = i0 - 1 + f / 3, jj = j0 - 1 + r, c = f % 3;
-        const bool ok = idx < PN && ii >= 0 && ii < g.nnx && jj >= 0 && jj < g.nny;
-        const int node = ok ? ii + g.nnx * jj : 0;
-        s_off[q] = 3 * node + c;
-        bool keep = ok;
-        if (MASK && ok && have_nf) {
-            if ((col_and[node] >> c) & 1u) keep = false;
-            else if ((col_or[node] >> c) & 1u) mskbits |= 1u << q;
-        }
-        if (keep) okbits |= 1u << q;
-    }
-    const int el_col = ex + g.nelx * ey, el_plane = g.nelx * g.nely;
-    // one cp.async group: node plane kz and the scales of element layer kz
-    auto stage = [&](int kz, int buf) {
-        const bool zok = kz >= 0 && kz < g.nnz;
-        const T* vb = v + (long long)min(max(kz, 0), g.nnz - 1) * pn3;
-        unsigned take = zok ? okbits : 0u;
-        if (MASK && mskbits && zok) {  // rare: columns with z-varying constraints
-#pragma unroll
-            for (int q = 0; q < NS; ++q)
-                if (((mskbits >> q) & 1u) && ((node_fixed[kz * pn + s_off[q] / 3] >> (s_off[q] % 3)) & 1u))
-                    take &= ~(1u << q);
-        }
-        T* pb = plane[buf];
-#pragma unroll
-        for (int q = 0; q < NS; ++q) {
-            const int idx = tid + q * TILE_NT;
-            if (q < NS - 1 || idx < PN) {
-                if (sizeof(T) == 4)
-                    cp_async_4(pb + idx, vb + s_off[q], (take >> q) & 1u);
-                else
-                    cp_async_8(pb + idx, vb + s_off[q], (take >> q) & 1u);
-            }
-        }
-        const bool sok = col_ok && kz >= 0 && kz < g.nelz;
-        const T* sp = scale + (sok ? el_col + (long long)el_plane * kz : 0);
-        if (sizeof(T) == 4)
-            cp_async_4(&sc[buf][tid], sp, sok);
-        else
-            cp_async_8(&sc[buf][tid], sp, sok);
-        cp_async_commit();
-    };
-    const int pofs = ty * PW + 3 * tx;
-    const int own_node0 = (i0 + tx) + g.nnx * (j0 + ty);
-    // pass-through needs the node's constraint byte only on constrained
-    // columns, and a per-plane read only where the constraint varies along z
-    unsigned fix_or = 0u, fix_and = 0u;
-    if (PASS && owner && have_nf) {
-        fix_or = col_or[own_node0];
-        fix_and = col_and[own_node0];
-    }
-    const bool own_fix_col = fix_or != 0u;
-    const bool fix_zvar = fix_or != fix_and;
-
-    const int n_layers = max(0, min(oz, g.nnz - k0) + (skip_halo ? 0 : 1));
-    // prologue: planes kb0 .. kb0+P (P+1 groups) in flight together
-#pragma unroll
-    for (int b = 0; b <= P; ++b) stage(kb0 + b, b);
-    cp_async_wait_n(P - 1);  // planes kb0 and kb0+1 landed
-    __syncthreads();
-    T XYb[3][4];
-#pragma unroll
-    for (int c = 0; c < 3; ++c) {
-        const T* b = plane[0] + pofs + c;
-        face_fwd(b[0], b[3], b[PW], b[PW + 3], XYb[c]);
-    }
-    T Gt[3][4];
-#pragma unroll
-    for (int c = 0; c < 3; ++c)
-#pragma unroll
-        for (int q = 0; q < 4; ++q) Gt[c][q] = T(0);
-    T dot = T(0);
-
-    T pend_x1[3], pend_p[3], pend_v[3];
-    bool pend = false;
-    int pend_d0 = 0;
-    unsigned pend_bits = 0u;
-
-    auto finish = [&](const T (&x1)[3], const T (&Yrow)[3][TILE_NT], int d0, unsigned bits, const T (&pv)[3],
-                      const T (&pp)[3]) {
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-            T acc = x1[c] + Yrow[c][tid + TILE_BX];
-            const int d = d0 + c;
-            if (accumulate) acc += w[d];  // uniform branch (rare: TF_ACCUMULATE)
-            const bool fx = PASS && ((bits >> c) & 1u);
-            if (fx) acc = pv[c];
-            w[d] = acc;
-            if (DOT) {
-                const T p = fx ? pv[c] : pp[c];
-                dot = fma(p, acc, dot);
-            }
-        }
-    };
-    // node pass of the previous layer (plane ez-1), reading its row hand-off
-    auto node_pass = [&](const T (&Yp)[3][TILE_NT]) {
-        if (pend) finish(pend_x1, Yp, pend_d0, pend_bits, pend_v, pend_p);
-    };
-    // constraint bits / pass-through values of the owned node of plane kz
-    auto own_bits = [&](int kz, T (&nv)[3]) -> unsigned {
-        unsigned nbits = 0u;
-        nv[0] = nv[1] = nv[2] = T(0);
-        if (own_fix_col) {
-            nbits = fix_zvar ? (unsigned)node_fixed[own_node0 + kz * pn] : fix_and;
-            const int d0 = 3 * (own_node0 + kz * pn);
-#pragma unroll
-            for (int c = 0; c < 3; ++c)
-                if ((nbits >> c) & 1u) nv[c] = ld_nc(v + d0 + c);
-        }
-        return nbits;
-    };
-    auto inverse_to_plane = [&](const T (&H)[3][4], T (&x0)[3], T (&x1)[3]) {
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-            T corner[4];
-            face_inv(H[c], corner);
-            x0[c] = corner[1] + __shfl_down_sync(0xffffffffu, corner[0], 1);
-            x1[c] = corner[3] + __shfl_down_sync(0xffffffffu, corner[2], 1);
-        }
-    };
-
-    // one element layer (layer index L = ring phase I mod R): bottom plane ez
-    // in buffer I, top plane ez+1 in buffer (I+1) % R; the layer stages plane
-    // ez+1+P into buffer (I+P+1) % R = (I-1) % R (the plane of layer L-1)
-    auto layer = [&](auto ph, int L) {
-        constexpr int CUR = decltype(ph)::value;
-        constexpr int TOP = (CUR + 1) % R, NXT = (CUR + P + 1) % R;
-        const int ez = kb0 + L;
-        if (L > 0) {
-            cp_async_wait_n(P - 1);  // plane ez+1 landed (P-1 younger groups may still fly)
-            __syncthreads();         // (A) plane ez+1 + previous Y visible, buffer NXT free
-        }
-        node_pass(Y[(L + 1) & 1]);
-        stage(ez + 1 + P, NXT);      // beyond the chunk: zero-size copies keep the group count
-        // plane ez is finished in this CTA's march (else: halo layer, or the
-        // cluster-deferred first plane)
-        const bool emit_l = L >= 1 || k0 == 0;
-        unsigned nbits = 0u;
-        T nv[3] = {T(0), T(0), T(0)};
-        if (PASS && own_fix_col && emit_l) nbits = own_bits(ez, nv);
-        const T s_cur = sc[CUR][tid];
-        T pown[3];
-        if (DOT) {
-#pragma unroll
-            for (int c = 0; c < 3; ++c) pown[c] = plane[CUR][pofs + PW + 3 + c];
-        }
-        T h[3][8];
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-            const T* b = plane[TOP] + pofs + c;
-            T XYt[4];
-            face_fwd(b[0], b[3], b[PW], b[PW + 3], XYt);
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                h[c][q] = XYb[c][q] + XYt[q];
-                h[c][q + 4] = XYt[q] - XYb[c][q];
-                XYb[c][q] = XYt[q];
-            }
-        }
-        T gm[3][8];
-        if (ISO) {
-            block_iso(h, ki, s_cur, gm);
-        } else {
-#pragma unroll
-            for (int c = 0; c < 3; ++c)
-#pragma unroll
-                for (int m = 1; m < 8; ++m) h[c][m] *= s_cur;
-#pragma unroll
-            for (int c = 0; c < 3; ++c) gm[c][0] = T(0);
-#pragma unroll
-            for (int q = 0; q < 8; ++q)
-#pragma unroll
-                for (int c = 0; c < 3; ++c) {
-                    const int m = q ^ (1 << c);
-                    if (m == 0) continue;
-                    T acc = T(0);
-#pragma unroll
-                    for (int d = 0; d < 3; ++d) {
-                        const int n = q ^ (1 << d);
-                        if (n == 0) continue;
-                        acc = fma(kb.b[q][c][d], h[d][n], acc);
-                    }
-                    gm[c][m] = acc;
-                }
-        }
-        T corner[3][4];
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-            T H[4];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const T dq = gm[c][q] - gm[c][q + 4];
-                if (CL && L == 0 && from_below) Dsm[4 * c + q][tid] = dq;
-                H[q] = Gt[c][q] + dq;
-                Gt[c][q] = gm[c][q] + gm[c][q + 4];
-            }
-            face_inv(H, corner[c]);
-        }
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-            const T x0 = corner[c][1] + __shfl_down_sync(0xffffffffu, corner[c][0], 1);
-            pend_x1[c] = corner[c][3] + __shfl_down_sync(0xffffffffu, corner[c][2], 1);
-            Y[L & 1][c][tid] = x0;
-            if (DOT) pend_p[c] = pown[c];
-        }
-        pend = owner && emit_l;
-        pend_d0 = 3 * (own_node0 + ez * pn);
-        pend_bits = nbits;
-#pragma unroll
-        for (int c = 0; c < 3; ++c) pend_v[c] = nv[c];
-    };
-    int L = 0;
-    for (; L + R <= n_layers; L += R) static_for<0, R>([&](auto ph) { layer(ph, L + decltype(ph)::value); });
-    static_for<0, R - 1>([&](auto ph) {
-        if (L + decltype(ph)::value < n_layers) layer(ph, L + decltype(ph)::value);
-    });
-    cp_async_wait_n(0);
-    __syncthreads();
-    node_pass(Y[(n_layers - 1) & 1]);
-
-    if constexpr (CL) {
-        namespace cgx = cooperative_groups;
-        cgx::cluster_group cluster = cgx::this_cluster();
-        if (to_above) {
-#pragma unroll
-            for (int c = 0; c < 3; ++c)
-#pragma unroll
-                for (int q = 0; q < 4; ++q) (&plane[0][0])[(4 * c + q) * TILE_NT + tid] = Gt[c][q];
-        }
-        cluster.sync();  // Gt exports visible cluster-wide (release/acquire)
-        if (from_below) {
-            // plane k0 = lower CTA's last top part + this CTA's first bottom part
-            const T* gb = cluster.map_shared_rank(&plane[0][0], crank - 1);
-            T H[3][4];
-#pragma unroll
-            for (int c = 0; c < 3; ++c)
-#pragma unroll
-                for (int q = 0; q < 4; ++q) H[c][q] = gb[(4 * c + q) * TILE_NT + tid] + Dsm[4 * c + q][tid];
-            T x0[3], x1[3];
-            inverse_to_plane(H, x0, x1);
-#pragma unroll
-            for (int c = 0; c < 3; ++c) Y[0][c][tid] = x0[c];
-            __syncthreads();
-            if (owner) {
-                T nv[3], pp[3];
-                const unsigned nbits = PASS ? own_bits(k0, nv) : 0u;
-                if (!PASS) nv[0] = nv[1] = nv[2] = T(0);
-                if (DOT) {
-                    const int d0 = 3 * (own_node0 + k0 * pn);
-                    unsigned mb = 0u;
-                    if (MASK && have_nf) mb = fix_zvar || !PASS ? (unsigned)node_fixed[own_node0 + k0 * pn] : fix_and;
-#pragma unroll
-                    for (int c = 0; c < 3; ++c) pp[c] = ((mb >> c) & 1u) ? T(0) : ld_nc(v + d0 + c);
-                }
-                finish(x1, Y[0], 3 * (own_node0 + k0 * pn), nbits, nv, pp);
-            }
-        }
-        cluster.sync();  // partners finished reading this CTA's export before it exits
-    }
 
     if (DOT) {
         __shared__ double shd[TILE_NT / 32];
@@ -1122,20 +788,7 @@ k_grid_tile3_cg(Grid g, int oz, const T* __restrict__ scale, T* __restrict__ w,
 struct TileShape {
     dim3 grid;
     int oz;
-    int cz = 1;  // thread-block cluster height (z chunks per cluster); 1 = no cluster
 };
-
-// grid for (oz, cz): z padded to whole clusters (padding CTAs own no planes)
-template <typename T>
-TileShape tile_shape_ozcz(const Grid& g, int oz, int cz)
-{
-    constexpr int TILE_BY = TileDims<T>::BY;
-    const int tx = (g.ihi - g.ilo + TILE_BX - 2) / (TILE_BX - 1);
-    const int ty = (g.nny + TILE_BY - 2) / (TILE_BY - 1);
-    const int chunks = (g.nnz + oz - 1) / oz;
-    cz = std::max(1, std::min(cz, chunks));
-    return {dim3(tx, ty, (chunks + cz - 1) / cz * cz), oz, cz};
-}
 
 // The isotropic block form (khat_iso) in FP64 only: there the kernel is
 // DFMA-bound and the 25 fewer FP ops per element-layer are worth 30 % (c5 125
@@ -1152,13 +805,6 @@ bool tile_iso_enabled()
 template bool tile_iso_enabled<float>();
 template bool tile_iso_enabled<double>();
 
-// TF_TILE_CLUSTER=0: no cluster z split (tile6 degenerates to tile5's march)
-static bool tile_cluster_enabled()
-{
-    const char* e = getenv("TF_TILE_CLUSTER");
-    return !(e && e[0] == '0');
-}
-
 template <typename T>
 static int tile_slots()
 {
@@ -1170,10 +816,19 @@ static int tile_slots()
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-            &per_sm, k_grid_tile6<T, true, true, true, TF_TILE_P, false, false>, TileDims<T>::NT, 0);
+            &per_sm, k_grid_tile5<T, true, true, false, true, TF_TILE_P, false>, TileDims<T>::NT, 0);
         s = std::max(1, per_sm) * nsm;
     }
     return s;
+}
+
+template <typename T>
+TileShape tile_shape_oz(const Grid& g, int oz)
+{
+    constexpr int TILE_BY = TileDims<T>::BY;
+    const int tx = (g.ihi - g.ilo + TILE_BX - 2) / (TILE_BX - 1);
+    const int ty = (g.nny + TILE_BY - 2) / (TILE_BY - 1);
+    return {dim3(tx, ty, (g.nnz + oz - 1) / oz), oz};
 }
 
 // z-chunk height: the smallest chunk count that keeps every SM busy is one
@@ -1196,17 +851,7 @@ TileShape tile_shape(const Grid& g)
     const char* e = getenv("TF_TILE_OZ");  // experiment override of the z-chunk height
     const int oz_env = e ? std::max(0, atoi(e)) : 0;
     if (oz_env > 0) oz = oz_env;
-    const int tz = (g.nnz + oz - 1) / oz;
-    return {dim3(tx, ty, tz), oz};
-}
-
-template <typename T>
-TileShape tile_shape_oz(const Grid& g, int oz)
-{
-    constexpr int TILE_BY = TileDims<T>::BY;
-    const int tx = (g.ihi - g.ilo + TILE_BX - 2) / (TILE_BX - 1);
-    const int ty = (g.nny + TILE_BY - 2) / (TILE_BY - 1);
-    return {dim3(tx, ty, (g.nnz + oz - 1) / oz), oz};
+    return tile_shape_oz<T>(g, oz);
 }
 
 static int TileDimsBy(int prec) { return prec == 8 ? TileDims<double>::BY : TileDims<float>::BY; }
@@ -1219,34 +864,34 @@ static bool tile_autotune_enabled()
     return !(o && atoi(o) > 0);
 }
 
-// Launch shape per (grid shape, x-range, precision): z-chunk height and
-// cluster height measured once with CUDA events over the candidates (min of
-// 3 x 4 back-to-back launches each), then cached.  Every candidate gives the
-// same bits (tile6 sums every DOF in the same order for any chunking), so
-// this only picks the fastest.  Returns {0, 0} when it cannot tune (stream
-// capture in progress) or when lookup_only finds nothing.
+// z-chunk height per (grid shape, x-range, precision): measured once with
+// CUDA events over the candidates (min of 3 x 4 back-to-back launches each),
+// then cached.  Every candidate gives the same bits (every DOF is summed in
+// the same order for any chunking), so this only picks the fastest.  Returns
+// 0 when it cannot tune (stream capture in progress) or when lookup_only
+// finds nothing.  TF_TILE_DEBUG=1 prints the candidate timings.
 template <typename F>
-static std::pair<int, int> tile_tuned(const Grid& g, int prec, cudaStream_t st, F&& launch, bool lookup_only = false)
+static int tile_tuned_oz(const Grid& g, int prec, cudaStream_t st, F&& launch, bool lookup_only = false)
 {
     static std::mutex mu;
-    static std::map<std::array<int, 6>, std::pair<int, int>> cache;
+    static std::map<std::array<int, 6>, int> cache;
     const std::array<int, 6> key = {g.nelx, g.nely, g.nelz, g.ilo, g.ihi, prec};
     {
         std::lock_guard<std::mutex> lk(mu);
         auto it = cache.find(key);
         if (it != cache.end()) return it->second;
-        if (lookup_only) return {0, 0};
+        if (lookup_only) return 0;
     }
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
     if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) {
         cudaGetLastError();
-        return {0, 0};
+        return 0;
     }
     static const int cands[] = {2, 3, 4, 5, 6, 7, 8, 10, 12, 16, 24, 32};
     cudaEvent_t e0, e1;
     if (cudaEventCreate(&e0) != cudaSuccess || cudaEventCreate(&e1) != cudaSuccess) {
         cudaGetLastError();
-        return {0, 0};
+        return 0;
     }
     // candidates must cover every SM (a shape that leaves SMs idle can win a
     // single-launch timing through lower launch latency, not throughput)
@@ -1255,48 +900,39 @@ static std::pair<int, int> tile_tuned(const Grid& g, int prec, cudaStream_t st, 
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     const long long cols = (long long)((g.ihi - g.ilo + TILE_BX - 2) / (TILE_BX - 1)) *
                            ((g.nny + TileDimsBy(prec) - 2) / (TileDimsBy(prec) - 1));
-    std::pair<int, int> best = {0, 0};
+    int best = 0;
     float best_ms = 1e30f;
+    const char* dbg_env = getenv("TF_TILE_DEBUG");
+    const bool dbg = dbg_env && dbg_env[0] == '1';
     for (int oz : cands) {
         if (oz > std::max(2, g.nnz)) break;
         const int chunks = (g.nnz + oz - 1) / oz;
         if (oz > 2 && cols * chunks < nsm) break;
-        int czs[4] = {1, 0, 0, 0}, ncz = 1;
-        if (tile_cluster_enabled() && chunks > 1) {
-            // whole column in one cluster when it fits, else full clusters of 8 / 4
-            const int opts[3] = {std::min(chunks, 8), 4, 2};
-            for (int o : opts) {
-                bool dup = false;
-                for (int i = 0; i < ncz; ++i) dup |= czs[i] == o;
-                if (!dup && o > 1 && o <= chunks) czs[ncz++] = o;
-            }
+        if (launch(oz) != TF_OK) {  // warm-up
+            cudaGetLastError();
+            break;
         }
-        for (int i = 0; i < ncz; ++i) {
-            const int cz = czs[i];
-            if (launch(oz, cz) != TF_OK) {  // warm-up (an unsupported cluster shape just drops out)
-                cudaGetLastError();
-                continue;
-            }
-            float t = 1e30f;
-            for (int r = 0; r < 3; ++r) {
-                cudaEventRecord(e0, st);
-                for (int k = 0; k < 4; ++k) launch(oz, cz);
-                cudaEventRecord(e1, st);
-                cudaEventSynchronize(e1);
-                float ms = 0.f;
-                cudaEventElapsedTime(&ms, e0, e1);
-                t = std::min(t, ms);
-            }
-            if (t < best_ms) {
-                best_ms = t;
-                best = {oz, cz};
-            }
+        float t = 1e30f;
+        for (int r = 0; r < 3; ++r) {
+            cudaEventRecord(e0, st);
+            for (int k = 0; k < 4; ++k) launch(oz);
+            cudaEventRecord(e1, st);
+            cudaEventSynchronize(e1);
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, e0, e1);
+            t = std::min(t, ms);
+        }
+        if (dbg) fprintf(stderr, "[tile_tuned] %dx%dx%d oz=%d: %.2f us per launch\n", g.nelx, g.nely, g.nelz, oz,
+                         1e3f * t / 4);
+        if (t < best_ms) {
+            best_ms = t;
+            best = oz;
         }
     }
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     cudaGetLastError();
-    if (best.first > 0) {
+    if (best > 0) {
         std::lock_guard<std::mutex> lk(mu);
         cache[key] = best;
     }
@@ -1309,8 +945,8 @@ TileShape tile_shape_current(const Grid& g)
 {
     TileShape sh = tile_shape<T>(g);
     if (tile_autotune_enabled()) {
-        const auto t = tile_tuned(g, (int)sizeof(T), nullptr, [](int, int) { return TF_ERR_ARG; }, true);
-        if (t.first > 0) sh = tile_shape_ozcz<T>(g, t.first, t.second);
+        const int oz = tile_tuned_oz(g, (int)sizeof(T), nullptr, [](int) { return TF_ERR_ARG; }, true);
+        if (oz > 0) sh = tile_shape_oz<T>(g, oz);
     }
     return sh;
 }
@@ -1320,54 +956,6 @@ long long grid_tile_blocks(const Grid& g)
 {
     TileShape s = tile_shape<T>(g);
     return (long long)s.grid.x * s.grid.y * s.grid.z;
-}
-
-// TF_TILE5=1: the previous production kernel (A/B; bitwise the same output)
-static bool tile5_forced()
-{
-    const char* e = getenv("TF_TILE5");  // read per launch: A/B in one process
-    return e && e[0] == '1';
-}
-
-// tile6 launch; a cluster height > 1 goes through cudaLaunchKernelEx with the
-// (1, 1, cz) cluster attribute
-template <typename T, bool M, bool PS, bool DT, bool ISO, bool CL>
-static cudaError_t launch_tile6(const TileShape& sh, cudaStream_t st, const Grid& g, int acc, const T* scale,
-                                const T* v, T* w, const uint8_t* node_fixed, double* dot_part,
-                                const KhatBlocks<T>& kb, const KhatIso<T>& ki)
-{
-    auto kern = k_grid_tile6<T, M, PS, DT, TF_TILE_P, ISO, CL>;
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = sh.grid;
-    cfg.blockDim = dim3(TILE_BX, TileDims<T>::BY, 1);
-    cfg.dynamicSmemBytes = 0;
-    cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 1;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = CL ? (unsigned)sh.cz : 1u;
-    cfg.attrs = attr;
-    cfg.numAttrs = CL ? 1 : 0;
-    return cudaLaunchKernelEx(&cfg, kern, g, sh.oz, sh.cz, acc, scale, v, w, node_fixed, dot_part, kb, ki);
-}
-
-// the isotropic block form is instantiated for FP64 only (tile_iso_enabled)
-template <typename T, bool M, bool PS, bool DT>
-static cudaError_t launch_tile6_flags(const TileShape& sh, bool iso, cudaStream_t st, const Grid& g, int acc,
-                                      const T* scale, const T* v, T* w, const uint8_t* node_fixed,
-                                      double* dot_part, const KhatBlocks<T>& kb, const KhatIso<T>& ki)
-{
-    if constexpr (sizeof(T) == 8) {
-        if (iso)
-            return sh.cz > 1 ? launch_tile6<T, M, PS, DT, true, true>(sh, st, g, acc, scale, v, w, node_fixed,
-                                                                      dot_part, kb, ki)
-                             : launch_tile6<T, M, PS, DT, true, false>(sh, st, g, acc, scale, v, w, node_fixed,
-                                                                       dot_part, kb, ki);
-    }
-    return sh.cz > 1
-               ? launch_tile6<T, M, PS, DT, false, true>(sh, st, g, acc, scale, v, w, node_fixed, dot_part, kb, ki)
-               : launch_tile6<T, M, PS, DT, false, false>(sh, st, g, acc, scale, v, w, node_fixed, dot_part, kb, ki);
 }
 
 // returns TF_ERR_UNSUPPORTED when Ke lacks the parity-block structure
@@ -1386,53 +974,47 @@ int launch_grid_tile(const Grid& g, const T* ke_host, const T* scale, const T* v
     const uint32_t f = flags & (TF_MASK_INPUT | TF_PASS_FIXED | TF_ACCUMULATE);
     constexpr uint32_t MP = TF_MASK_INPUT | TF_PASS_FIXED;
     auto launch_shape = [&](const TileShape& sh) -> int {
-        if (tile5_forced() && sh.cz == 1) {
-            dim3 block(TILE_BX, TileDims<T>::BY, 1);
-#define T5(M, PS, AC, DT, DP)                                                                              \
-    do {                                                                                                   \
-        if (iso)                                                                                           \
-            k_grid_tile5<T, M, PS, AC, DT, TF_TILE_P, true><<<sh.grid, block, 0, st>>>(g, sh.oz, scale, v, w, \
-                                                                                    node_fixed, DP, kb, ki);  \
-        else                                                                                               \
+        dim3 block(TILE_BX, TileDims<T>::BY, 1);
+        // ISO only in FP64 (tile_iso_enabled): the FP32 instantiations stay generic
+#define T5(M, PS, AC, DT, DP)                                                                                  \
+    do {                                                                                                       \
+        if (sizeof(T) == 8 && iso)                                                                             \
+            k_grid_tile5<T, M, PS, AC, DT, TF_TILE_P, sizeof(T) == 8><<<sh.grid, block, 0, st>>>(             \
+                g, sh.oz, scale, v, w, node_fixed, DP, kb, ki);                                                \
+        else                                                                                                   \
             k_grid_tile5<T, M, PS, AC, DT, TF_TILE_P, false><<<sh.grid, block, 0, st>>>(g, sh.oz, scale, v, w, \
-                                                                                     node_fixed, DP, kb, ki); \
+                                                                                     node_fixed, DP, kb, ki);  \
     } while (0)
-            if (f == MP && dot_part) T5(true, true, false, true, dot_part);
-            else if (f == MP) T5(true, true, false, false, nullptr);
-            else if (f == TF_MASK_INPUT) T5(true, false, false, false, nullptr);
-            else if (f == 0) T5(false, false, false, false, nullptr);
-            else {
-                set_error("TF_TILE5: flag combination not instantiated");
+        if (dot_part) {  // CG p.q partials: the solver's masked, passed-through product only
+            if (f != MP) {
+                set_error("the fused p.q epilogue needs TF_MASK_INPUT | TF_PASS_FIXED");
                 return TF_ERR_ARG;
             }
+            T5(true, true, false, true, dot_part);
+        } else {
+            switch (f) {
+            case MP: T5(true, true, false, false, nullptr); break;
+            case TF_MASK_INPUT: T5(true, false, false, false, nullptr); break;
+            case TF_PASS_FIXED: T5(false, true, false, false, nullptr); break;
+            case 0: T5(false, false, false, false, nullptr); break;
+            case MP | TF_ACCUMULATE: T5(true, true, true, false, nullptr); break;
+            case TF_MASK_INPUT | TF_ACCUMULATE: T5(true, false, true, false, nullptr); break;
+            case TF_PASS_FIXED | TF_ACCUMULATE: T5(false, true, true, false, nullptr); break;
+            default: T5(false, false, true, false, nullptr); break;  // TF_ACCUMULATE
+            }
+        }
 #undef T5
-            TF_CHECK_LAUNCH();
-            return TF_OK;
-        }
-        cudaError_t e;
-        // every flag combination the C ABI accepts, as compile-time variants
-#define T6(M, PS) \
-    (dot_part ? launch_tile6_flags<T, M, PS, true>(sh, iso, st, g, acc, scale, v, w, node_fixed, dot_part, kb, ki) \
-              : launch_tile6_flags<T, M, PS, false>(sh, iso, st, g, acc, scale, v, w, node_fixed, nullptr, kb, ki))
-        const int acc = (f & TF_ACCUMULATE) ? 1 : 0;
-        switch (f & MP) {
-        case MP: e = T6(true, true); break;
-        case TF_MASK_INPUT: e = T6(true, false); break;
-        case TF_PASS_FIXED: e = T6(false, true); break;
-        default: e = T6(false, false); break;
-        }
-#undef T6
-        TF_CUDA_TRY(e);
+        TF_CHECK_LAUNCH();
         return TF_OK;
     };
     TileShape sh = tile_shape<T>(g);
     // Plain products (no CG partials, no accumulation): the launch shape is
     // autotuned once per grid shape on first use outside stream capture
     if (!dot_part && !(flags & TF_ACCUMULATE) && tile_autotune_enabled()) {
-        const auto t = tile_tuned(g, (int)sizeof(T), st, [&](int oz, int cz) {
-            return launch_shape(tile_shape_ozcz<T>(g, oz, cz));
+        const int oz = tile_tuned_oz(g, (int)sizeof(T), st, [&](int cand) {
+            return launch_shape(tile_shape_oz<T>(g, cand));
         });
-        if (t.first > 0) sh = tile_shape_ozcz<T>(g, t.first, t.second);
+        if (oz > 0) sh = tile_shape_oz<T>(g, oz);
     }
     return launch_shape(sh);
 }

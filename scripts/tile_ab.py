@@ -1,7 +1,7 @@
 """A/B of the structured K.v kernels on one GPU (run one variant per process:
 the launch-shape autotune cache is per process).
 
-    python scripts/tile_ab.py VARIANT [configs...]     VARIANT: tile6 | tile5 | nocluster
+    python scripts/tile_ab.py VARIANT [configs...]     VARIANT: a label | ozN (pinned chunk height)
 
 Per config: mean device time per product with L2 flushed before each step
 (bench.py protocol), the tuned launch shape, and the sha256 of the product
@@ -22,11 +22,10 @@ ROOT = Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT))
 
 variant = sys.argv[1]
-if variant == "tile5":
-    os.environ["TF_TILE5"] = "1"
-    os.environ["TF_TILE_CLUSTER"] = "0"
-elif variant == "nocluster":
-    os.environ["TF_TILE_CLUSTER"] = "0"
+# "prod": autotuned z-chunk; "ozN": pinned chunk height; any other name: a
+# label for the current build (A/B across builds)
+if variant.startswith("oz"):
+    os.environ["TF_TILE_OZ"] = variant[2:]
 
 import torch  # noqa: E402
 

@@ -140,3 +140,21 @@ def test_oracle_baseline_size_hashes(golden_ke, name):
         ke, scale, dt = _ops(golden_ke, rho, prec)
         got = oracle.apply(edof, ke, scale, v, bcs.fixed_dofs, m.n_dof, "fused")
         assert _sha(got) == h[f"apply_fused_{prec}_{name}"]["sha256"], prec
+
+
+def test_oracle_simp_restatement_pinned_to_reference_c1():
+    """oracle/simp.py (the CPU baseline's SIMP loop) against the reference's
+    own c1 trajectory: the first 3 iterations' compliances to 1e-12 and CG
+    counts exactly (FP64 serial)."""
+    from oracle import simp as osimp
+    from paper_2604_18020_b200.element import unit_stiffness
+    from paper_2604_18020_b200.mesh import StructuredMesh, build_edof, cantilever_bcs
+
+    g = load_golden("simp_c1_fp64.npz")
+    m = StructuredMesh(48, 24, 24)
+    b = cantilever_bcs(m)
+    hist, _ = osimp.run_simp((48, 24, 24), build_edof(m), b.fixed_dofs, b.force, 0.3,
+                             [(1, 30, 3.0, 1.0, 0.2, 1.5)], 1.5, unit_stiffness(0.3), iterations=3)
+    c = np.array([r["compliance"] for r in hist])
+    np.testing.assert_allclose(c, g["compliance"][:3], rtol=1e-12)
+    assert [r["cg_iterations"] for r in hist] == list(g["cg_iterations"][:3])

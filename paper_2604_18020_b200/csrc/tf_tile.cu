@@ -239,6 +239,47 @@ __device__ __forceinline__ void cp_async_wait_n(int n)
 #define TF_TILE_P 2
 #endif
 
+// TF_TILE_TRACE builds (scripts/tile_trace.py, never the product library):
+// thread 0 of every CTA records %globaltimer / %clock64 at the phase
+// boundaries of the march into a caller-supplied buffer, 16 u64 per CTA:
+// [0] globaltimer start, [1] SM id, [2] clock start, [3] after the column
+// setup, [4] after the prologue barrier, [5..12] after layers 0..7,
+// [14] clock end, [15] globaltimer end.
+#ifdef TF_TILE_TRACE
+__device__ unsigned long long* g_tile_trace = nullptr;
+__device__ __forceinline__ unsigned long long tt_gtime()
+{
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ unsigned tt_smid()
+{
+    unsigned r;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+    return r;
+}
+#define TT_CLK(slot)                                                                                         \
+    do {                                                                                                     \
+        if (tid == 0 && g_tile_trace)                                                                        \
+            g_tile_trace[(blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z)) * 16 + (slot)] =  \
+                clock64();                                                                                   \
+    } while (0)
+#define TT_SET(slot, val)                                                                                    \
+    do {                                                                                                     \
+        if (tid == 0 && g_tile_trace)                                                                        \
+            g_tile_trace[(blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z)) * 16 + (slot)] =  \
+                (val);                                                                                       \
+    } while (0)
+#else
+#define TT_CLK(slot) \
+    do {             \
+    } while (0)
+#define TT_SET(slot, val) \
+    do {                  \
+    } while (0)
+#endif
+
 template <typename T, bool MASK, bool PASS, bool ACC, bool DOT, int P, bool ISO>
 __global__ void __launch_bounds__(TileDims<T>::NT, sizeof(T) == 4 ? TF_TILE_MINB32 : TF_TILE_MINB64)
 k_grid_tile5(Grid g, int oz, const T* __restrict__ scale, const T* __restrict__ v, T* __restrict__ w,
@@ -254,6 +295,11 @@ k_grid_tile5(Grid g, int oz, const T* __restrict__ scale, const T* __restrict__ 
 
     const int tx = threadIdx.x, ty = threadIdx.y;
     const int tid = tx + TILE_BX * ty;
+#ifdef TF_TILE_TRACE
+    TT_SET(0, tt_gtime());
+    TT_SET(1, tt_smid());
+    TT_CLK(2);
+#endif
     const int i0 = g.ilo + blockIdx.x * (TILE_BX - 1);
     const int j0 = blockIdx.y * (TILE_BY - 1);
     const int k0 = blockIdx.z * oz;
@@ -265,54 +311,115 @@ k_grid_tile5(Grid g, int oz, const T* __restrict__ scale, const T* __restrict__ 
     const uint8_t* col_or = have_nf ? node_fixed + g.n_nodes : nullptr;
     const uint8_t* col_and = have_nf ? col_or + pn : nullptr;
 
-    int s_off[NS];
-    unsigned okbits = 0u, mskbits = 0u;
+    // Staging map (coalesced, one uniform row base per plane): warp wi copies
+    // node-plane row wi -- lanes take values lane + 32k of its PW = 3 (BX+1)
+    // -- and segment wi of the last row BY (warps 0..NSEG-1).  The prologue
+    // planes are copied on geometry alone and the constrained slots zeroed
+    // once they land: the first copies leave at kernel entry instead of
+    // after a dependent load of the constraint bytes (a full DRAM latency on
+    // every CTA's critical path, scripts/tile_trace.py); later planes copy
+    // with the mask folded into the slot bits.
+    constexpr int NW = TILE_NT / 32, NSEG = (PW + 31) / 32, NSL = NSEG + 1;
+    static_assert(TILE_BY == NW && NSEG <= NW, "staging map");
+    const int wi = tid >> 5, lane = tid & 31;
+    // DOF offsets within a plane (3 n_nodes < 2^31 is checked on the host)
+    const int row_own = 3 * (i0 - 1 + g.nnx * (j0 - 1 + wi)) + lane;
+    const int row_last = 3 * (i0 - 1 + g.nnx * (j0 - 1 + TILE_BY)) + lane + 32 * wi;
+    auto slot_smem = [&](int sl) { return sl < NSEG ? wi * PW + lane + 32 * sl : TILE_BY * PW + lane + 32 * wi; };
+    auto slot_dof = [&](int sl) { return sl < NSEG ? row_own + 32 * sl : row_last; };
+    unsigned geobits = 0u;  // bit sl: slot sl holds a node inside the grid
+    {
+        const int jo = j0 - 1 + wi, jl = j0 - 1 + TILE_BY;
 #pragma unroll
-    for (int q = 0; q < NS; ++q) {
-        const int idx = tid + q * TILE_NT;
-        const int r = idx / PW, f = idx - r * PW;
-        const int ii = i0 - 1 + f / 3, jj = j0 - 1 + r, c = f % 3;
-        const bool ok = idx < PN && ii >= 0 && ii < g.nnx && jj >= 0 && jj < g.nny;
-        const int node = ok ? ii + g.nnx * jj : 0;
-        s_off[q] = 3 * node + c;
-        bool keep = ok;
-        if (MASK && ok && have_nf) {
-            if ((col_and[node] >> c) & 1u) keep = false;
-            else if ((col_or[node] >> c) & 1u) mskbits |= 1u << q;
+        for (int k = 0; k < NSEG; ++k) {
+            const int f = lane + 32 * k, ii = i0 - 1 + f / 3;
+            if (f < PW && ii >= 0 && ii < g.nnx && jo >= 0 && jo < g.nny) geobits |= 1u << k;
         }
-        if (keep) okbits |= 1u << q;
+        const int f = lane + 32 * wi, ii = i0 - 1 + f / 3;
+        if (wi < NSEG && f < PW && ii >= 0 && ii < g.nnx && jl < g.nny) geobits |= 1u << NSEG;
+    }
+    // zero every slot the prologue does not copy: slots outside the grid
+    // never receive a copy (they feed only zero-scale elements, but 0 * NaN
+    // would not vanish), constrained slots of later planes are never copied
+#pragma unroll
+    for (int bf = 0; bf < R; ++bf) {
+#pragma unroll
+        for (int sl = 0; sl < NSL; ++sl) {
+            const bool exists = sl < NSEG ? lane + 32 * sl < PW : (wi < NSEG && lane + 32 * wi < PW);
+            if (exists && (bf > P || !((geobits >> sl) & 1u))) plane[bf][slot_smem(sl)] = T(0);
+        }
     }
     const int el_col = ex + g.nelx * ey, el_plane = g.nelx * g.nely;
-    // one cp.async group: node plane kz and the scales of element layer kz
-    auto stage = [&](int kz, int buf) {
-        const bool zok = kz >= 0 && kz < g.nnz;
-        const T* vb = v + (long long)min(max(kz, 0), g.nnz - 1) * pn3;
-        unsigned take = zok ? okbits : 0u;
-        if (MASK && mskbits && zok) {  // rare: columns with z-varying constraints
+    const int n_layers = min(oz, g.nnz - k0) + 1;
+    const int kmax = k0 - 1 + n_layers;  // top plane of the chunk's last layer
+    const T* v_own = v + row_own;
+    const T* v_last = v + row_last;
+    // one cp.async group: node plane kz (slots `bits`; `varbits` slots carry
+    // z-varying constraints, zero-filled where node kz's bit is set) and the
+    // scales of element layer kz.  Planes outside the mesh are zero-filled,
+    // planes past the chunk skipped.
+    auto stage = [&](int kz, int buf, unsigned bits, unsigned varbits) {
+        if (kz <= kmax) {
+            T* pb = plane[buf];
+            if (kz >= 0 && kz < g.nnz) {
+                const long long zb = (long long)kz * pn3;
 #pragma unroll
-            for (int q = 0; q < NS; ++q)
-                if (((mskbits >> q) & 1u) && ((node_fixed[kz * pn + s_off[q] / 3] >> (s_off[q] % 3)) & 1u))
-                    take &= ~(1u << q);
-        }
-        T* pb = plane[buf];
+                for (int sl = 0; sl < NSL; ++sl)
+                    if ((bits >> sl) & 1u) {
+                        const T* src = (sl < NSEG ? v_own + 32 * sl : v_last) + zb;
+                        if (sizeof(T) == 4)
+                            cp_async_4(pb + slot_smem(sl), src, true);
+                        else
+                            cp_async_8(pb + slot_smem(sl), src, true);
+                    }
+                if (MASK && varbits) {  // rare: columns whose constraint varies along z
 #pragma unroll
-        for (int q = 0; q < NS; ++q) {
-            const int idx = tid + q * TILE_NT;
-            if (q < NS - 1 || idx < PN) {
-                if (sizeof(T) == 4)
-                    cp_async_4(pb + idx, vb + s_off[q], (take >> q) & 1u);
-                else
-                    cp_async_8(pb + idx, vb + s_off[q], (take >> q) & 1u);
+                    for (int sl = 0; sl < NSL; ++sl)
+                        if ((varbits >> sl) & 1u) {
+                            const int d = slot_dof(sl);
+                            const bool keep = !((node_fixed[kz * (long long)pn + d / 3] >> (d % 3)) & 1u);
+                            const T* src = (sl < NSEG ? v_own + 32 * sl : v_last) + zb;
+                            if (sizeof(T) == 4)
+                                cp_async_4(pb + slot_smem(sl), src, keep);
+                            else
+                                cp_async_8(pb + slot_smem(sl), src, keep);
+                        }
+                }
+            } else {
+#pragma unroll
+                for (int sl = 0; sl < NSL; ++sl)
+                    if (((bits | varbits) >> sl) & 1u) {
+                        if (sizeof(T) == 4)
+                            cp_async_4(pb + slot_smem(sl), v, false);
+                        else
+                            cp_async_8(pb + slot_smem(sl), v, false);
+                    }
             }
+            const bool sok = col_ok && kz >= 0 && kz < g.nelz;
+            const T* sp = scale + (sok ? el_col + (long long)el_plane * kz : 0);
+            if (sizeof(T) == 4)
+                cp_async_4(&sc[buf][tid], sp, sok);
+            else
+                cp_async_8(&sc[buf][tid], sp, sok);
         }
-        const bool sok = col_ok && kz >= 0 && kz < g.nelz;
-        const T* sp = scale + (sok ? el_col + (long long)el_plane * kz : 0);
-        if (sizeof(T) == 4)
-            cp_async_4(&sc[buf][tid], sp, sok);
-        else
-            cp_async_8(&sc[buf][tid], sp, sok);
-        cp_async_commit();
+        cp_async_commit();  // possibly empty: keeps the group count uniform
     };
+    TT_CLK(3);
+    // prologue: planes k0-1 .. k0-1+P (P+1 groups) in flight together, on geometry alone
+#pragma unroll
+    for (int bf = 0; bf <= P; ++bf) stage(k0 - 1 + bf, bf, geobits, 0u);
+    // constraint bits of the staged slots (loads overlap the copies above)
+    unsigned fixbits = 0u, varbits = 0u;
+    if (MASK && have_nf) {
+#pragma unroll
+        for (int sl = 0; sl < NSL; ++sl)
+            if ((geobits >> sl) & 1u) {
+                const int d = slot_dof(sl), node = d / 3, c = d - 3 * node;
+                if ((col_and[node] >> c) & 1u) fixbits |= 1u << sl;
+                else if ((col_or[node] >> c) & 1u) varbits |= 1u << sl;
+            }
+    }
+    const unsigned okbits = geobits & ~fixbits & ~varbits;
     const int pofs = ty * PW + 3 * tx;
     const int own_node0 = (i0 + tx) + g.nnx * (j0 + ty);
     // pass-through needs the node's constraint byte only on constrained
@@ -325,17 +432,30 @@ k_grid_tile5(Grid g, int oz, const T* __restrict__ scale, const T* __restrict__ 
     const bool own_fix_col = fix_or != 0u;
     const bool fix_zvar = fix_or != fix_and;
 
-    const int n_layers = min(oz, g.nnz - k0) + 1;
-    // prologue: planes k0-1 .. k0-1+P (P+1 groups) in flight together
+    cp_async_wait_n(0);  // the prologue planes landed: zero their constrained slots
+    if (MASK && (fixbits | varbits)) {
 #pragma unroll
-    for (int b = 0; b <= P; ++b) stage(k0 - 1 + b, b);
-    cp_async_wait_n(P - 1);  // planes k0-1 and k0 landed
+        for (int bf = 0; bf <= P; ++bf) {
+            const int kz = k0 - 1 + bf;
+            if (kz < 0 || kz >= g.nnz) continue;
+#pragma unroll
+            for (int sl = 0; sl < NSL; ++sl) {
+                bool zero = (fixbits >> sl) & 1u;
+                if ((varbits >> sl) & 1u) {
+                    const int d = slot_dof(sl);
+                    zero = (node_fixed[kz * (long long)pn + d / 3] >> (d % 3)) & 1u;
+                }
+                if (zero) plane[bf][slot_smem(sl)] = T(0);
+            }
+        }
+    }
     __syncthreads();
+    TT_CLK(4);
     T XYb[3][4];
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-        const T* b = plane[0] + pofs + c;
-        face_fwd(b[0], b[3], b[PW], b[PW + 3], XYb[c]);
+        const T* bp = plane[0] + pofs + c;
+        face_fwd(bp[0], bp[3], bp[PW], bp[PW + 3], XYb[c]);
     }
     T Gt[3][4];
 #pragma unroll
@@ -382,7 +502,7 @@ k_grid_tile5(Grid g, int oz, const T* __restrict__ scale, const T* __restrict__ 
             __syncthreads();         // (A) plane ez+1 + previous Y visible, buffer NXT free
         }
         node_pass(Y[(L + 1) & 1]);
-        stage(ez + 1 + P, NXT);      // beyond the chunk: zero-size copies keep the group count
+        stage(ez + 1 + P, NXT, okbits, varbits);
         // constraint bits / pass-through inputs of plane ez (finalised by the
         // next layer's node pass): issued now, consumed a layer later
         unsigned nbits = 0u;
@@ -403,9 +523,9 @@ k_grid_tile5(Grid g, int oz, const T* __restrict__ scale, const T* __restrict__ 
         T h[3][8];
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
-            const T* b = plane[TOP] + pofs + c;
+            const T* bp = plane[TOP] + pofs + c;
             T XYt[4];
-            face_fwd(b[0], b[3], b[PW], b[PW + 3], XYt);
+            face_fwd(bp[0], bp[3], bp[PW], bp[PW + 3], XYt);
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
                 h[c][q] = XYb[c][q] + XYt[q];
@@ -462,6 +582,7 @@ k_grid_tile5(Grid g, int oz, const T* __restrict__ scale, const T* __restrict__ 
         pend_bits = nbits;
 #pragma unroll
         for (int c = 0; c < 3; ++c) pend_v[c] = nv[c];
+        TT_CLK(5 + min(L, 8));
     };
     int L = 0;
     for (; L + R <= n_layers; L += R) static_for<0, R>([&](auto ph) { layer(ph, L + decltype(ph)::value); });
@@ -472,6 +593,10 @@ k_grid_tile5(Grid g, int oz, const T* __restrict__ scale, const T* __restrict__ 
     __syncthreads();
     node_pass(Y[(n_layers - 1) & 1]);
 
+#ifdef TF_TILE_TRACE
+    TT_CLK(14);
+    TT_SET(15, tt_gtime());
+#endif
     if (DOT) {
         __shared__ double shd[TILE_NT / 32];
         double dd = (double)dot;
@@ -865,7 +990,7 @@ static bool tile_autotune_enabled()
 }
 
 // z-chunk height per (grid shape, x-range, precision): measured once with
-// CUDA events over the candidates (min of 3 x 4 back-to-back launches each),
+// CUDA events over the candidates (min of 5 cold single launches each),
 // then cached.  Every candidate gives the same bits (every DOF is summed in
 // the same order for any chunking), so this only picks the fastest.  Returns
 // 0 when it cannot tune (stream capture in progress) or when lookup_only
@@ -904,6 +1029,19 @@ static int tile_tuned_oz(const Grid& g, int prec, cudaStream_t st, F&& launch, b
     float best_ms = 1e30f;
     const char* dbg_env = getenv("TF_TILE_DEBUG");
     const bool dbg = dbg_env && dbg_env[0] == '1';
+    // each candidate is timed as single launches behind an L2 eviction (a
+    // write of twice the L2 size): a product called on its own meets its
+    // inputs in HBM, and the chunk height that wins warm, back-to-back
+    // launches (more CTAs, shorter marches) loses cold (c2: oz 3 vs 4,
+    // scripts/tile_trace.py).  Without the scratch buffer: warm timing.
+    int l2 = 0;
+    cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
+    void* flush = nullptr;
+    const size_t flush_bytes = 2 * (size_t)std::max(l2, 1 << 20);
+    if (cudaMalloc(&flush, flush_bytes) != cudaSuccess) {
+        cudaGetLastError();
+        flush = nullptr;
+    }
     for (int oz : cands) {
         if (oz > std::max(2, g.nnz)) break;
         const int chunks = (g.nnz + oz - 1) / oz;
@@ -913,17 +1051,19 @@ static int tile_tuned_oz(const Grid& g, int prec, cudaStream_t st, F&& launch, b
             break;
         }
         float t = 1e30f;
-        for (int r = 0; r < 3; ++r) {
+        const int reps = flush ? 5 : 3, per = flush ? 1 : 4;
+        for (int r = 0; r < reps; ++r) {
+            if (flush) cudaMemsetAsync(flush, r, flush_bytes, st);
             cudaEventRecord(e0, st);
-            for (int k = 0; k < 4; ++k) launch(oz);
+            for (int k = 0; k < per; ++k) launch(oz);
             cudaEventRecord(e1, st);
             cudaEventSynchronize(e1);
             float ms = 0.f;
             cudaEventElapsedTime(&ms, e0, e1);
-            t = std::min(t, ms);
+            t = std::min(t, ms / per);
         }
-        if (dbg) fprintf(stderr, "[tile_tuned] %dx%dx%d oz=%d: %.2f us per launch\n", g.nelx, g.nely, g.nelz, oz,
-                         1e3f * t / 4);
+        if (dbg) fprintf(stderr, "[tile_tuned] %dx%dx%d oz=%d: %.2f us per launch (%s)\n", g.nelx, g.nely, g.nelz,
+                         oz, 1e3f * t, flush ? "cold" : "warm");
         if (t < best_ms) {
             best_ms = t;
             best = oz;
@@ -931,6 +1071,10 @@ static int tile_tuned_oz(const Grid& g, int prec, cudaStream_t st, F&& launch, b
     }
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
+    if (flush) {
+        cudaStreamSynchronize(st);
+        cudaFree(flush);
+    }
     cudaGetLastError();
     if (best > 0) {
         std::lock_guard<std::mutex> lk(mu);
@@ -1059,6 +1203,15 @@ template int launch_grid_tile<double>(const Grid&, const double*, const double*,
                                       double*, const uint8_t*, uint32_t, double*, cudaStream_t);
 
 }  // namespace tf
+
+#ifdef TF_TILE_TRACE
+extern "C" int tf_tile_trace_set(void* buf)
+{
+    unsigned long long* p = (unsigned long long*)buf;
+    TF_CUDA_TRY(cudaMemcpyToSymbol(tf::g_tile_trace, &p, sizeof(p)));
+    return TF_OK;
+}
+#endif
 
 extern "C" int tf_tile_shape(const tf_grid* grid, int precision, int32_t* oz, int64_t* ctas)
 {

@@ -5,12 +5,15 @@ __call__, diagonal, apply_fp64, element_energies, compliance, n_apply) and the
 traffic/roofline helpers, but every evaluation runs in libtopofuse_b200.so on
 the current CUDA device:
 
-  * structured grids (edof == build_edof(mesh)): the index-free pull kernel
-    (one thread per node, no atomics, deterministic) with input masking and
-    fixed-DOF pass-through fused in -- ONE launch per apply;
+  * structured grids (edof == build_edof(mesh)): the index-free parity-block
+    tile kernel (csrc/tf_tile.cu: element columns marching in z, no atomics,
+    deterministic) with input masking and fixed-DOF pass-through fused in --
+    ONE launch per apply (grid_kernel="pull": the dense node-centric kernel;
+    exact=True: the reference's operation order, bitwise);
   * any other edof: the element-per-thread kernel with red.global.add
-    (scatter="parallel_atomic") or colour-ordered deterministic passes
-    (scatter="serial"), constrained slots masked in the device edof copy;
+    (scatter="parallel_atomic") or the reference's serial order, bitwise
+    (scatter="serial": row sums + ascending-element pull through a DOF CSR),
+    constrained slots masked in the device edof copy;
   * variant="three_stage": gather -> batched element product -> FP64
     histogram scatter, intermediates genuinely materialised (operator.py:103-114).
 

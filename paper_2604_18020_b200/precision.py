@@ -1,10 +1,11 @@
 """Working-precision policies (reference precision.py:25-99).
 
-The B200 hot path computes in FP32 or FP64.  BF16 appears in the reference
-only as an emulated, documented negative result; the
-policy object and host rounding helper are kept so callers that name it still
-import, but operators reject it (north star: tensor-core/BF16 variants are not
-on the production path).
+The B200 hot path computes in FP32 or FP64.  The reference's emulated
+bfloat16 ("bf16": FP32 storage, every term bf16-rounded) is served by the
+general-connectivity bf16 kernels (csrc/tf_bf16.cu) exactly as the reference
+defines it -- the documented negative result (PAPER.md:1522-1552,
+DESIGN.md §9); the structured production kernels and tensor cores are never
+used for it.
 """
 
 from __future__ import annotations

@@ -607,6 +607,9 @@ def kernel_sweep(steps=100):
             force = np.zeros(m.n_dof)
             force[perm] = bcs.force
             bcs = BoundaryConditions(np.sort(perm[bcs.fixed_dofs]).astype(np.int64), force)
+            v_perm = np.empty_like(v)
+            v_perm[perm] = v  # the same input vector in the relabelled numbering
+            v = v_perm
             desc = f"{desc}, seeded_random DOF relabelling"
         op = MatFreeOperator(m, edof, bcs, rho, SimpParams(3.0), prec, grid_kernel=kernel,
                              scatter="parallel_atomic")

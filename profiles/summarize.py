@@ -32,6 +32,8 @@ KEEP = [
     "launch__grid_size", "launch__block_size", "launch__shared_mem_per_block_static",
     "l1tex__t_sector_hit_rate.pct", "lts__t_sector_hit_rate.pct",
     "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "sm__cycles_elapsed.avg.per_second",
+    "lts__t_sectors_op_red.sum", "lts__t_requests_op_red.sum", "lts__t_sectors_op_atom.sum",
+    "l1tex__t_requests_pipe_lsu_mem_global_op_red.sum", "lts__t_sectors_op_red_lookup_hit.sum",
 ]
 
 

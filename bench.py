@@ -509,6 +509,7 @@ def run_ours(args):
 
     simp = cg = simp2 = sweep = None
     scaling = simp_scaling_all(world, dist) if args.simp else None
+    kv_scale = kv_scaling(world, rank, dist, same_dev) if args.simp else None
     if args.simp and rank == 0:
         simp = simp_c1()
         simp2 = simp_c2()
@@ -569,6 +570,7 @@ def run_ours(args):
             "simp": simp,
             "simp_c2": simp2,
             "simp_c4_scaling": scaling,
+            "scaling_configs": kv_scale,
             "slab_transports": transports,
             "cg": cg,
             "wall_s_timed_region": wall,
@@ -576,6 +578,126 @@ def run_ours(args):
         print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
+
+
+def slab_problem(gdims, world, rank, seed=42):
+    """One rank's x-slab of the cantilever `gdims`, built without any global
+    array (the c5w weak-scaling slab belongs to a 39M-element mesh whose
+    connectivity alone is 3.8 GB): the local mesh, the clamped x=0 face and
+    the tip load mapped from the global cantilever (reference mesh.py:235-246),
+    rho ~ U(0.05, 1) drawn per global element layer and v ~ N(0, 1) per global
+    node plane (each seeded by its global x index, so both replicas of an
+    interface plane hold the same values)."""
+    from paper_2604_18020_b200.mesh import BoundaryConditions, StructuredMesh, _nearest_node
+    from paper_2604_18020_b200.slab import SlabPartition
+
+    gm = StructuredMesh(*gdims)
+    part = SlabPartition(gm, world, rank)
+    lm = part.local_mesh
+    nyz_e, nyz_n = lm.nely * lm.nelz, (lm.nely + 1) * (lm.nelz + 1)
+    rho = np.stack([np.random.default_rng([seed, ex]).uniform(0.05, 1.0, nyz_e)
+                    for ex in range(part.x0, part.x1)])              # (nelx_l, ny*nz)
+    rho = np.ascontiguousarray(rho.T).ravel()                          # x-fastest elements
+    v = np.stack([np.random.default_rng([seed + 1, i]).standard_normal((nyz_n, 3))
+                  for i in range(part.x0, part.x1 + 1)])             # (nnx_l, ny1*nz1, 3)
+    v = np.ascontiguousarray(v.transpose(1, 0, 2)).ravel()             # x-fastest nodes
+    fixed = part.plane_dofs(0) if rank == 0 else np.zeros(0, np.int64)
+    force = np.zeros(lm.n_dof)
+    tip = _nearest_node(gm, 1.0, 0.5, 0.5)
+    ti, tj, tk = tip % (gm.nelx + 1), (tip // (gm.nelx + 1)) % (gm.nely + 1), tip // ((gm.nelx + 1) * (gm.nely + 1))
+    if part.x0 <= ti <= part.x1:
+        force[3 * (ti - part.x0 + (lm.nelx + 1) * (tj + (lm.nely + 1) * tk)) + 1] = -1.0
+    return gm, part, BoundaryConditions(np.sort(fixed).astype(np.int64), force), rho, v
+
+
+def slab_operator(part, lb, rho_local, prec, dev, same_dev, dist):
+    """The slab product on this rank: the sm_100a tile kernels locally, the
+    interface exchange over the peer-memory runtime when it initialises here
+    and matches NCCL's product bitwise on every rank, else NCCL P2P."""
+    import torch
+
+    from paper_2604_18020_b200 import SimpParams
+    from paper_2604_18020_b200.slab import SlabOperator, gpu_local_kernels
+
+    lop, local_apply, local_diag = gpu_local_kernels(part, lb, rho_local, SimpParams(3.0), prec)
+    tdt = torch.float32 if prec == "fp32" else torch.float64
+    sop_p2p = SlabOperator(part, lb, local_apply, local_diag, dev, tdt, transport="p2p")
+    sop, sop_peer, note = sop_p2p, None, "p2p (NCCL send/recv)"
+    if os.environ.get("TF_SLAB_TRANSPORT", "auto") in ("auto", "peer"):
+        ok = 0
+        try:
+            probe = torch.randn(part.local_mesh.n_dof, device=dev).to(tdt)
+            sop_peer = SlabOperator(part, lb, local_apply, local_diag, dev, tdt, transport="peer")
+            ok = int(torch.equal(sop_p2p.apply(probe), sop_peer.apply(probe)))
+            torch.cuda.synchronize()
+        except Exception as e:  # noqa: BLE001 - reported, NCCL path kept
+            note = f"p2p (peer transport unavailable: {repr(e)[:160]})"
+        t = torch.tensor([ok], device="cpu" if same_dev else dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MIN)
+        if int(t.item()) == 1:
+            sop, note = sop_peer, "peer (CUDA IPC puts + stream-ordered flags, verified bitwise vs NCCL)"
+        elif sop_peer is not None and "unavailable" not in note:
+            note = "p2p (peer product differed from NCCL's; not used)"
+    return sop, note, lop, local_apply
+
+
+def kv_scaling(world, rank, dist, same_dev, steps=50):
+    """BASELINE configs[3] and [4] at this job's rank count, same protocol as
+    the headline (L2 flushed before every step, CUDA events per step, max over
+    ranks): K.v on c4 (200x100x50, 1M elements) strong-scaled over the ranks'
+    x-slabs, and K.v on (340 N)x170x85 -- the c5 4.9M-element slab per GPU,
+    weak-scaled to the 39M-element c5w mesh at N = 8 -- plus the SIMP s/iter
+    block (simp_c4_scaling) of the same run.  N = 1: the single-GPU product
+    of the whole mesh."""
+    import torch
+
+    from paper_2604_18020_b200 import MatFreeOperator, SimpParams
+    from paper_2604_18020_b200.mesh import build_edof
+
+    dev = torch.device("cuda", torch.cuda.current_device())
+    prec = "fp32"
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    out = {}
+    for name, gdims, mode in (("kv_c4_strong", (200, 100, 50), "strong"),
+                              ("kv_c5_weak", (340 * world, 170, 85), "weak")):
+        gm, part, lb, rho_l, v_l = slab_problem(gdims, world, rank)
+        if world == 1:
+            op = MatFreeOperator(gm, build_edof(gm), lb, rho_l, SimpParams(3.0), prec)
+            x = torch.tensor(v_l.astype(np.float32), device=dev)
+            w = torch.empty_like(x)
+            step = lambda: op.apply_device(x, out=w)  # noqa: E731
+            note, launches = "single GPU", 1
+        else:
+            sop, note, lop, la = slab_operator(part, lb, rho_l, prec, dev, same_dev, dist)
+            x = torch.tensor(v_l.astype(np.float32), device=dev)
+            step = lambda: sop.apply(x)  # noqa: E731
+            nnx = part.local_mesh.nelx + 1
+            launches = sum(1 for lo, hi in ((0, la.bl), (nnx - la.br, nnx), (la.bl, nnx - la.br)) if hi > lo)
+        for _ in range(3):
+            step()
+        torch.cuda.synchronize()
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+        if dist is not None:
+            dist.barrier()
+        for a, b in ev:
+            flush.fill_(5)
+            a.record()
+            step()
+            b.record()
+        torch.cuda.synchronize()
+        ms = float(np.mean([a.elapsed_time(b) for a, b in ev]))
+        if dist is not None:
+            t = torch.tensor([ms], device="cpu" if same_dev else dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        out[name] = {"global_mesh": "x".join(map(str, gdims)), "global_n_elem": gm.n_elem,
+                     "global_n_dof": gm.n_dof, "scaling": mode, "n_gpus": world,
+                     "per_rank_elem": part.local_mesh.n_elem, "ms_per_step": ms,
+                     "GDOF_s": gm.n_dof / (ms * 1e-3) / 1e9, "transport": note,
+                     "launches_per_step": launches}
+        del x, step
+        torch.cuda.empty_cache()
+    return out
 
 
 def kernel_sweep(steps=100):

@@ -29,7 +29,7 @@ if variant.startswith("oz"):
 
 import torch  # noqa: E402
 
-from bench import CONFIGS, build_problem  # noqa: E402
+from bench import CONFIGS, build_problem, reference_check  # noqa: E402
 from paper_2604_18020_b200 import MatFreeOperator, SimpParams, _lib  # noqa: E402
 
 names = sys.argv[2:] or ["c2", "c3", "c4", "c5", "c2f64", "c5f64"]
@@ -64,7 +64,8 @@ for name in names:
               ctypes.byref(ctas))
     out[name] = {"us_cold": 1e3 * float(np.mean(ms)), "us_cold_min": 1e3 * float(np.min(ms)),
                  "us_warm": 1e3 * e0.elapsed_time(e1) / steps, "oz": oz.value, "ctas": ctas.value,
-                 "sha": hashlib.sha256(w.cpu().numpy().tobytes()).hexdigest()[:16]}
+                 "sha": hashlib.sha256(w.cpu().numpy().tobytes()).hexdigest()[:16],
+                 "vs_reference": reference_check(name, prec, w.double().cpu().numpy())}
     print(variant, name, json.dumps(out[name]), flush=True)
 Path("gpurun_out").mkdir(exist_ok=True)
 Path(f"gpurun_out/tile_ab_{variant}.json").write_text(json.dumps(out, indent=1))

@@ -4,6 +4,8 @@ committed B200 line (profiles/bench_r1_c2.json, written by `python bench.py`).""
 from __future__ import annotations
 
 import json
+
+import numpy as np
 from pathlib import Path
 
 ROOT = Path(__file__).resolve().parents[1]
@@ -40,3 +42,29 @@ def test_bench_cli_defaults():
     assert re.search(r'add_argument\("--steps", type=int, default=\d+\)', src)
     assert re.search(r'add_argument\("--warmup", type=int, default=(\d+)\)', src)
     assert int(re.search(r'add_argument\("--warmup", type=int, default=(\d+)\)', src).group(1)) >= 3
+
+
+def test_slab_problem_matches_global_cantilever():
+    """bench.slab_problem (the c5w weak-scaling slab, built without global
+    arrays) gives each rank the constraints and load of the global cantilever
+    restricted to its slab, and both replicas of an interface plane the same
+    input values."""
+    import bench
+    from paper_2604_18020_b200.mesh import StructuredMesh, cantilever_bcs
+    from paper_2604_18020_b200.slab import SlabPartition
+
+    gdims = (9, 4, 3)
+    gm = StructuredMesh(*gdims)
+    gb = cantilever_bcs(gm)
+    parts = []
+    for world in (1, 2, 3):
+        parts = [bench.slab_problem(gdims, world, r) for r in range(world)]
+        for r, (_, part, lb, rho, v) in enumerate(parts):
+            want = SlabPartition(gm, world, r).local_bcs(gb)
+            assert np.array_equal(lb.fixed_dofs, want.fixed_dofs)
+            assert np.array_equal(lb.force, want.force)
+            assert rho.shape == (part.local_mesh.n_elem,) and v.shape == (part.local_mesh.n_dof,)
+        for r in range(world - 1):
+            pl, pr = parts[r][1], parts[r + 1][1]
+            assert np.array_equal(parts[r][4][pl.plane_dofs(pl.local_mesh.nelx)],
+                                  parts[r + 1][4][pr.plane_dofs(0)])

@@ -264,3 +264,60 @@ def test_slab_simp_projected_volume_matches_single_gpu_loop():
         assert abs(c - h.compliance) <= 1e-3 * abs(h.compliance)
         assert rs == h.restarted
         assert abs(vol - h.volume) <= 1e-3 * h.volume
+
+
+def _c1_worker(rank, world, port, transport, q):
+    import torch.distributed as dist
+
+    from paper_2604_18020_b200 import SimpConfig
+    from paper_2604_18020_b200.mesh import ProblemPreset, StructuredMesh, cantilever_bcs
+    from paper_2604_18020_b200.simp import ContinuationSchedule, Phase
+    from paper_2604_18020_b200.slab_simp import slab_run_simp
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), TF_SLAB_TRANSPORT=transport)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        m = StructuredMesh(48, 24, 24)
+        pb = ProblemPreset("cantilever", m, cantilever_bcs(m), 0.3, 1.5)
+        sched = ContinuationSchedule((Phase(1, 30, p=3.0, beta=1.0, move=0.2, rmin_end=1.5),), 1.5)
+        r = slab_run_simp(pb, SimpConfig(schedule=sched, precision="fp64"), device="cuda:0")
+        q.put((rank, [h.compliance for h in r.history], [h.cg_iterations for h in r.history],
+               r.rho_phys, r.total_cg_iterations))
+    except Exception as e:  # surface the failure in the parent
+        q.put((rank, repr(e), None, None, None))
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world,transport", [(2, "peer"), (3, "p2p")])
+def test_slab_simp_c1_matches_reference_golden(world, transport):
+    """BASELINE config c1 (48x24x24, V_f 0.3, p 3, rmin 1.5, FP64, 30 its) on
+    x-slabs against the REFERENCE's own run (tests/golden/simp_c1_fp64.npz,
+    numba serial scatter) at the north-star bars: compliance per iteration
+    and the final density field within 1e-3 relative, CG iterations within
+    +-2 % per iteration and in total."""
+    import torch.multiprocessing as mp
+
+    from conftest import load_golden
+
+    g = load_golden("simp_c1_fp64.npz")
+    ctx = mp.get_context("spawn")
+    q = ctx.SimpleQueue()
+    port = _free_port()
+    procs = [ctx.Process(target=_c1_worker, args=(r, world, port, transport, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get() for _ in range(world)]
+    for p in procs:
+        p.join(timeout=600)
+    for r in res:
+        assert not isinstance(r[1], str), r[1]
+    assert all(p.exitcode == 0 for p in procs)
+    _, c, its, rho_phys, total = res[0]
+    np.testing.assert_allclose(c, g["compliance"], rtol=1e-3)
+    its = np.asarray(its)
+    assert np.all(np.abs(its - g["cg_iterations"]) <= np.maximum(1, 0.02 * g["cg_iterations"]))
+    assert abs(total - int(g["total_cg"])) <= 0.02 * int(g["total_cg"])
+    assert np.linalg.norm(rho_phys - g["rho_phys"]) <= 1e-3 * np.linalg.norm(g["rho_phys"])

@@ -190,6 +190,22 @@ int tf_matvec_edof_f64(const int32_t* edof, const double* ke, const double* scal
                        const int32_t* color_elems, const int64_t* color_offsets, int n_colors,
                        void* stream);
 
+/* ---- fused_atomic (_kernels_numba.py:183-196) with the connectivity's
+ *      neighbour-merge pattern precomputed: tf_edof_merge_mask writes, once per
+ *      element->DOF table, a 16-bit mask per element (bit 3 pr + c: DOF
+ *      3 corner_of(1,oy,oz) + c of element e equals DOF 3 corner_of(0,oy,oz) + c
+ *      of element e+1 in the same 32-element group); the product then sums each
+ *      such pair in registers before one red.global.add.  Same contract as
+ *      tf_matvec_edof_* in mode TF_SCATTER_ATOMIC (accumulates into w; slots
+ *      < 0 are masked).  edof and mask are device pointers.                   */
+int tf_edof_merge_mask(const int32_t* edof, int64_t n_elem, uint16_t* mask, void* stream);
+int tf_matvec_edof_merged_f32(const int32_t* edof, const uint16_t* mask, const float* ke,
+                              const float* scale, const float* v, float* w, int64_t n_elem,
+                              void* stream);
+int tf_matvec_edof_merged_f64(const int32_t* edof, const uint16_t* mask, const double* ke,
+                              const double* scale, const double* v, double* w, int64_t n_elem,
+                              void* stream);
+
 /* w[fixed[i]] = v[fixed[i]] for i < n_fixed (operator.py:115) */
 int tf_pass_fixed_f32(const int64_t* fixed, int64_t n_fixed, const float* v, float* w,
                       void* stream);

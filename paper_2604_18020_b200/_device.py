@@ -124,11 +124,15 @@ def node_fixed_mask(n_nodes: int, fixed_dofs: np.ndarray, nodes_per_plane: int |
 
 
 def masked_edof(edof: np.ndarray, fixed_dofs: np.ndarray, n_dof: int) -> np.ndarray:
-    """edof with every constrained DOF slot replaced by -1 (gather 0, no scatter)."""
+    """edof with every constrained DOF slot marked by its sign bit (d | 2^31,
+    a negative int32): every kernel gathers 0 there and never scatters to it
+    (slots < 0), except the neighbour-merged atomic product, which adds the
+    slot's row to DOF d itself -- a constrained DOF the pass-through then
+    overwrites -- to keep its reductions branch-free (csrc/tf_matvec.cu)."""
     free = np.ones(n_dof, dtype=bool)
     free[np.asarray(fixed_dofs, dtype=np.int64)] = False
     e = np.ascontiguousarray(edof, dtype=np.int32)
-    return np.where(free[e], e, np.int32(-1)).astype(np.int32)
+    return np.where(free[e], e, e | np.int32(-(2**31))).astype(np.int32)
 
 
 def bind_gpu_local_cpus(index: int = 0):

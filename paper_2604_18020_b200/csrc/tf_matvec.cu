@@ -17,6 +17,7 @@
 // element matrix as constant-bank operands and red.global.add scatter
 // (parallel_atomic analogue) or a colour-ordered deterministic scatter.
 
+#include <algorithm>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -427,6 +428,151 @@ k_edof_staged(const int32_t* __restrict__ edof, const T* __restrict__ scale, con
         }
 }
 
+// General connectivity, red.global scatter, v3 (production): v2's staging
+// with the instruction count cut where ncu put it (v2: 762 thread-
+// instructions per element at c5, 112 ISETP + 80 branch instructions + 36
+// SHFL + 51 constant reloads; profiles/edof_atomic_c5_r2.json):
+//   * which (right corner of element e, left corner of element e+1) DOF pairs
+//     coincide is a property of the connectivity, not of the product: it is
+//     computed once per mesh into a 16-bit mask per element
+//     (tf_edof_merge_mask) instead of two shuffles and a compare per pair on
+//     every product -- one shuffle per pair remains (the neighbour's value);
+//   * masked slots carry their DOF with the sign bit set (operator.py's
+//     device copy, _device.masked_edof): the gather is a predicated load
+//     (reads 0), and the slot's row is added to that constrained DOF with an
+//     unconditional red.global -- the operator's pass-through overwrites it
+//     (operator.py:115) -- so only the neighbour-merged slots need a guard
+//     (ptxas turns every predicated RED into a branch).
+__device__ __forceinline__ void red_add_if(bool p, float* a, float v)
+{
+    asm volatile("{\n .reg .pred q;\n setp.ne.u32 q, %2, 0;\n @q red.global.add.f32 [%0], %1;\n}\n" ::"l"(a),
+                 "f"(v), "r"((unsigned)p)
+                 : "memory");
+}
+__device__ __forceinline__ void red_add_if(bool p, double* a, double v)
+{
+    asm volatile("{\n .reg .pred q;\n setp.ne.u32 q, %2, 0;\n @q red.global.add.f64 [%0], %1;\n}\n" ::"l"(a),
+                 "d"(v), "r"((unsigned)p)
+                 : "memory");
+}
+// base + i for a 32-bit unsigned element index: one IMAD.WIDE.U32 (ptxas
+// otherwise splits the 64-bit offset into shifts and carries)
+template <typename T>
+__device__ __forceinline__ T* at_u32(T* base, unsigned i)
+{
+    T* a;
+    asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(a) : "r"(i), "n"((int)sizeof(T)), "l"(base));
+    return a;
+}
+__device__ __forceinline__ void red_add(float* a, float v)
+{
+    asm volatile("red.global.add.f32 [%0], %1;\n" ::"l"(a), "f"(v) : "memory");
+}
+__device__ __forceinline__ void red_add(double* a, double v)
+{
+    asm volatile("red.global.add.f64 [%0], %1;\n" ::"l"(a), "d"(v) : "memory");
+}
+__device__ __forceinline__ float ld_if(int idx, const float* base)
+{
+    float u = 0.f;
+    asm volatile("{\n .reg .pred q;\n setp.ge.s32 q, %1, 0;\n @q ld.global.nc.f32 %0, [%2];\n}\n"
+                 : "+f"(u)
+                 : "r"(idx), "l"(base + idx));
+    return u;
+}
+__device__ __forceinline__ double ld_if(int idx, const double* base)
+{
+    double u = 0.0;
+    asm volatile("{\n .reg .pred q;\n setp.ge.s32 q, %1, 0;\n @q ld.global.nc.f64 %0, [%2];\n}\n"
+                 : "+d"(u)
+                 : "r"(idx), "l"(base + idx));
+    return u;
+}
+
+// Corner pairs (right corner of element e, left corner of element e+1) in the
+// reference corner order, RIGHT = corner_of(1,oy,oz), LEFT = corner_of(0,oy,oz).
+// bit 3*pr + c of mask[e]: DOF 3 RIGHT[pr] + c of element e is DOF
+// 3 LEFT[pr] + c of element e+1 and both sit in one warp (e % 32 != 31)
+__global__ void k_edof_merge_mask(const int32_t* __restrict__ edof, long long n, uint16_t* __restrict__ mask)
+{
+    constexpr int RIGHT[4] = {1, 2, 5, 6}, LEFT[4] = {0, 3, 4, 7};
+    const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= n) return;
+    unsigned m = 0u;
+    if ((e & 31) != 31 && e + 1 < n) {
+        const int32_t* a = edof + e * NLOC;
+        const int32_t* b = a + NLOC;
+#pragma unroll
+        for (int pr = 0; pr < 4; ++pr)
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                const int d = a[3 * RIGHT[pr] + c];
+                if (d >= 0 && b[3 * LEFT[pr] + c] == d) m |= 1u << (3 * pr + c);
+            }
+    }
+    mask[e] = (uint16_t)m;
+}
+
+#ifndef TF_EDOFM_MINB32
+#define TF_EDOFM_MINB32 8  // 64 registers, no spills: 32 warps/SM (c5 187 vs 197 us at 6)
+#endif
+template <typename T>
+__global__ void __launch_bounds__(EDOF_BLOCK, sizeof(T) == 4 ? TF_EDOFM_MINB32 : TF_EDOF_MINB)
+k_edof_merged(const int32_t* __restrict__ edof, const uint16_t* __restrict__ merge, const T* __restrict__ scale,
+              const T* __restrict__ v, T* __restrict__ w, long long n, const __grid_constant__ KhatBlocks<T> kb)
+{
+    constexpr int RIGHT[4] = {1, 2, 5, 6}, LEFT[4] = {0, 3, 4, 7};
+    __shared__ __align__(16) int4 rows[EDOF_BLOCK * 6];
+    const long long e0 = (long long)blockIdx.x * EDOF_BLOCK;
+    const int tid = threadIdx.x, lane = tid & 31;
+    const long long n_here = min((long long)EDOF_BLOCK, n - e0);
+    const int4* src = reinterpret_cast<const int4*>(edof + e0 * NLOC);
+#pragma unroll
+    for (int q = 0; q < 6; ++q) {
+        const int k = tid + q * EDOF_BLOCK;
+        cp_async_16(&rows[k], src + k, k < n_here * 6);
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+    const long long e = e0 + tid;
+    const bool live = tid < n_here;
+    const T se = live ? ld_nc(scale + e) : T(0);
+    const unsigned mk = live ? (unsigned)ld_nc(merge + e) : 0u;
+    asm volatile("cp.async.wait_group 0;\n" ::);
+    __syncthreads();
+    int idx[NLOC];
+#pragma unroll
+    for (int q = 0; q < 6; ++q) {
+        const int4 t = rows[tid * 6 + q];
+        idx[4 * q + 0] = t.x;
+        idx[4 * q + 1] = t.y;
+        idx[4 * q + 2] = t.z;
+        idx[4 * q + 3] = t.w;
+    }
+    T u[NLOC];  // (lanes past the last element gather zero-filled rows: v[0])
+#pragma unroll
+    for (int q = 0; q < NLOC; ++q) u[q] = ld_if(idx[q], v);
+    T fw[NLOC];
+    element_apply(u, se, kb, fw);
+    const unsigned prev = __shfl_up_sync(0xffffffffu, mk, 1) * (lane > 0);
+#pragma unroll
+    for (int pr = 0; pr < 4; ++pr)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            const int b = 3 * pr + c, jr = 3 * RIGHT[pr] + c, jl = 3 * LEFT[pr] + c;
+            const T nb = __shfl_down_sync(0xffffffffu, fw[jl], 1);
+            if ((mk >> b) & 1u) fw[jr] += nb;
+        }
+    if (!live) return;
+#pragma unroll
+    for (int pr = 0; pr < 4; ++pr)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            const int b = 3 * pr + c, jr = 3 * RIGHT[pr] + c, jl = 3 * LEFT[pr] + c;
+            red_add(at_u32(w, (unsigned)idx[jr] & 0x7fffffffu), fw[jr]);
+            if (!((prev >> b) & 1u)) red_add(at_u32(w, (unsigned)idx[jl] & 0x7fffffffu), fw[jl]);
+        }
+}
+
 // TF_EDOF_V1=1: the v1 atomic kernel (strided row loads, no aggregation)
 static bool edof_v1_forced()
 {
@@ -806,6 +952,34 @@ int tf_matvec_grid_f64(const tf_grid* g, const double* ke, const double* scale,
     }
 TF_MATVEC_RANGE(float, f32)
 TF_MATVEC_RANGE(double, f64)
+
+int tf_edof_merge_mask(const int32_t* edof, int64_t n_elem, uint16_t* mask, void* stream)
+{
+    TF_REQUIRE(edof && mask && n_elem >= 0, "bad arguments");
+    if (n_elem == 0) return TF_OK;
+    k_edof_merge_mask<<<(unsigned)((n_elem + 255) / 256), 256, 0, S(stream)>>>(edof, n_elem, mask);
+    TF_CHECK_LAUNCH();
+    return TF_OK;
+}
+
+#define TF_MATVEC_MERGED(T, SUF)                                                                           \
+    int tf_matvec_edof_merged_##SUF(const int32_t* edof, const uint16_t* merge, const T* ke, const T* scale, \
+                                    const T* v, T* w, int64_t n_elem, void* stream)                         \
+    {                                                                                                      \
+        TF_REQUIRE(edof && merge && ke && scale && v && w && n_elem >= 0, "bad arguments");                 \
+        TF_REQUIRE(((uintptr_t)edof & 15u) == 0, "edof must be 16-byte aligned");                          \
+        if (n_elem == 0) return TF_OK;                                                                     \
+        KhatBlocks<T> kb;                                                                                  \
+        if (!khat_blocks_cached<T>(ke, &kb)) /* no parity structure: the dense-row kernel */              \
+            return launch_edof<T>(edof, ke, scale, v, w, n_elem, TF_SCATTER_ATOMIC, nullptr, nullptr, 0,   \
+                                  S(stream));                                                              \
+        const long long nb = (n_elem + EDOF_BLOCK - 1) / EDOF_BLOCK;                                       \
+        k_edof_merged<T><<<(unsigned)nb, EDOF_BLOCK, 0, S(stream)>>>(edof, merge, scale, v, w, n_elem, kb); \
+        TF_CHECK_LAUNCH();                                                                                 \
+        return TF_OK;                                                                                      \
+    }
+TF_MATVEC_MERGED(float, f32)
+TF_MATVEC_MERGED(double, f64)
 
 int tf_matvec_edof_f32(const int32_t* edof, const float* ke, const float* scale, const float* v,
                        float* w, int64_t n_elem, int mode, const int32_t* color_elems,

@@ -77,6 +77,7 @@ class DeviceProblem:
         self._edof_raw = None
         self._colors = None
         self._csr = None
+        self._merge = None
         self.pcg_handles = {}
 
     @property
@@ -112,6 +113,17 @@ class DeviceProblem:
             rows = t.empty(n_rows, dtype=t.float64, device=off.device)
             self._csr = (off, ent, rows)
         return self._csr
+
+    def merge_mask(self):
+        """Per-element 16-bit mask of the (right corner of e, left corner of
+        e+1) DOF pairs the atomic product sums in registers before one
+        red.global (tf_edof_merge_mask, once per connectivity)."""
+        if self._merge is None:
+            t = D.torch()
+            em = self.edof_masked
+            self._merge = t.empty(self.n_elem, dtype=t.int16, device=em.device)
+            _lib.call("tf_edof_merge_mask", D.ptr(em), self.n_elem, D.ptr(self._merge), D.stream_ptr())
+        return self._merge
 
     def colors(self):
         """Element colouring with no two same-colour elements sharing a DOF."""
@@ -279,7 +291,10 @@ class MatFreeOperator:
             return out
         if self.variant == "fused":
             out.zero_()
-            if self.scatter == "parallel_atomic":
+            if self.scatter == "parallel_atomic" and os.environ.get("TF_EDOF_MERGED", "1") == "1":
+                _lib.call(f"tf_matvec_edof_merged_{sfx}", D.ptr(dev.edof_masked), D.ptr(dev.merge_mask()),
+                          ke.ctypes.data, D.ptr(scale), D.ptr(x), D.ptr(out), self.mesh.n_elem, st)
+            elif self.scatter == "parallel_atomic":  # TF_EDOF_MERGED=0: the v2 kernel (A/B)
                 _lib.call(f"tf_matvec_edof_{sfx}", D.ptr(dev.edof_masked), ke.ctypes.data,
                           D.ptr(scale), D.ptr(x), D.ptr(out), self.mesh.n_elem,
                           _lib.TF_SCATTER_ATOMIC, None, None, 0, st)

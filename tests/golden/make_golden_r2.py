@@ -13,6 +13,8 @@ read-only).
   cg      cg_r2.json: cold solve_equilibrium anchors (rho 0.5, p 3,
           CgConfig()) -- c2 FP32, c3 torsion FP32, c4 FP64/FP32
   simp    simp_c1_fp32.npz: config c1 (48x24x24, 30 its) in FP32, serial
+          (name "atomic": simp_c1_fp32_atomic.npz, the same run with the
+          reference's parallel_atomic scatter -- its own run-to-run spread)
 """
 
 from __future__ import annotations
@@ -108,21 +110,24 @@ def cg(tf, names):
 def simp(tf, names):
     from topofuse.simp import ContinuationSchedule, Phase
 
+    scatter, fname = ("parallel_atomic", "simp_c1_fp32_atomic.npz") if "atomic" in names else \
+        ("serial", "simp_c1_fp32.npz")
+
     m = tf.StructuredMesh(48, 24, 24)
     pb = tf.ProblemPreset("cantilever", m, tf.cantilever_bcs(m), 0.3, 1.5)
     sched = ContinuationSchedule(phases=(Phase(1, 30, p=3.0, beta=1.0, move=0.2, rmin_end=1.5),),
                                  rmin_start=1.5)
-    res = tf.run_simp(pb, tf.SimpConfig(schedule=sched, precision="fp32", scatter="serial"))
+    res = tf.run_simp(pb, tf.SimpConfig(schedule=sched, precision="fp32", scatter=scatter))
     h = res.history
     np.savez_compressed(
-        OUT / "simp_c1_fp32.npz",
+        OUT / fname,
         compliance=np.array([r.compliance for r in h]),
         cg_iterations=np.array([r.cg_iterations for r in h]),
         cg_converged=np.array([r.cg_converged for r in h]),
         volume=np.array([r.volume for r in h]),
         rho_phys=res.rho_phys, rho_raw=res.rho_raw,
         total_cg=res.total_cg_iterations, wall_s=res.wall_s)
-    print("simp c1 fp32", res.wall_s, res.total_cg_iterations, h[-1].compliance, flush=True)
+    print("simp c1 fp32", scatter, res.wall_s, res.total_cg_iterations, h[-1].compliance, flush=True)
 
 
 if __name__ == "__main__":

@@ -408,3 +408,39 @@ def test_tile_result_independent_of_z_chunking(prec, monkeypatch):
         outs.append(op.apply(v).clone())
     for o in outs[1:]:
         assert torch.equal(outs[0], o)
+
+
+@pytest.mark.parametrize("prec", ["fp64", "fp32"])
+@pytest.mark.parametrize("relabel", [False, True])
+def test_merged_atomic_edof_matches_oracle(prec, relabel, monkeypatch):
+    """The production general-edof atomic product (tf_matvec_edof_merged_*:
+    precomputed neighbour-merge mask, constrained slots scattered onto their
+    own DOF and overwritten by the pass-through) against the oracle and the
+    v2 kernel, on the structured numbering and a seeded DOF relabel, with a
+    partial last block."""
+    import torch
+
+    from paper_2604_18020_b200 import BoundaryConditions
+
+    m, edof, bcs, rho, v = seeded_case((13, 7, 5), 8)  # 455 elements: 3 full blocks + 71
+    if relabel:
+        perm = np.random.default_rng(2).permutation(m.n_dof).astype(np.int32)
+        edof = np.ascontiguousarray(perm[edof])
+        bcs = BoundaryConditions(np.sort(perm[bcs.fixed_dofs]), np.zeros(m.n_dof))
+    op = _op(m, edof, bcs, rho, prec, grid_kernel="edof", scatter="parallel_atomic")
+    assert not op.structured
+    got = op.apply(v.astype(op.precision.dtype))
+    want = oracle.apply(edof, op.ke, op.scale, v, bcs.fixed_dofs, m.n_dof)
+    assert _rel(got, want) <= TOL[prec]
+    assert np.array_equal(got[bcs.fixed_dofs], v.astype(op.precision.dtype)[bcs.fixed_dofs])
+    monkeypatch.setenv("TF_EDOF_MERGED", "0")
+    v2 = op.apply(v.astype(op.precision.dtype))
+    assert _rel(v2, got) <= TOL[prec]
+    # x-neighbours inside a warp and a mesh row share a face: 12 pairs (a
+    # DOF relabel keeps which slots coincide, so the mask is the same)
+    mask = op.dev.merge_mask().cpu().numpy().astype(np.uint16)
+    lanes = np.arange(m.n_elem) % 32
+    ex = np.arange(m.n_elem) % m.nelx
+    inner = (lanes != 31) & (ex != m.nelx - 1)
+    assert np.all(mask[inner] == 0xFFF)
+    assert np.all(mask[~inner] == 0)

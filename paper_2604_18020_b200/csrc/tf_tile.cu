@@ -919,7 +919,7 @@ struct TileShape {
 // DFMA-bound and the 25 fewer FP ops per element-layer are worth 30 % (c5 125
 // vs 179 us); in FP32 they are worth 3 % but move the reference-order rounding
 // enough to shift FP32 CG counts by more than the +-2 % bar (torsion SIMP).
-// TF_TILE_GENERIC=1 forces the generic blocks, TF_TILE_ISO32=1 the iso form in FP32.
+// TF_TILE_GENERIC=1 forces the generic blocks in FP64 too.
 template <typename T>
 bool tile_iso_enabled()
 {

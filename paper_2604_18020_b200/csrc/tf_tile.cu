@@ -915,11 +915,13 @@ struct TileShape {
     int oz;
 };
 
-// The isotropic block form (khat_iso) in FP64 only: there the kernel is
-// DFMA-bound and the 25 fewer FP ops per element-layer are worth 30 % (c5 125
-// vs 179 us); in FP32 they are worth 3 % but move the reference-order rounding
-// enough to shift FP32 CG counts by more than the +-2 % bar (torsion SIMP).
-// TF_TILE_GENERIC=1 forces the generic blocks in FP64 too.
+// The isotropic block form (khat_iso) in every FP64 kernel: there the kernel
+// is DFMA-bound and the 25 fewer FP ops per element-layer are worth 30 % (c5
+// 125 vs 179 us).  The FP32 CG kernels (fused p.q, resident PCG) keep the
+// generic blocks: the different rounding order shifts FP32 CG counts by more
+// than the +-2 % bar (torsion SIMP 10013 vs 10786 total); FP32 plain
+// products take the iso form (tile_iso32_plain).  TF_TILE_GENERIC=1 forces
+// the generic blocks everywhere.
 template <typename T>
 bool tile_iso_enabled()
 {
@@ -928,6 +930,16 @@ bool tile_iso_enabled()
     return sizeof(T) == 8;
 }
 template bool tile_iso_enabled<float>();
+// FP32 plain products (no CG partials, no accumulation) use the isotropic
+// form too: c2 14.4 vs 15.3 us, c4 27.8 vs 29.4, c5 84.2 vs 90.2 (B200,
+// scripts/tile_ab.py); the FP32 CG keeps the generic blocks (see above).
+// TF_TILE_ISO32=0 or TF_TILE_GENERIC=1 keeps them generic.
+static bool tile_iso32_plain()
+{
+    const char* e = getenv("TF_TILE_ISO32");
+    const char* eg = getenv("TF_TILE_GENERIC");
+    return !(e && e[0] == '0') && !(eg && eg[0] == '1');
+}
 template bool tile_iso_enabled<double>();
 
 template <typename T>
@@ -1115,16 +1127,18 @@ int launch_grid_tile(const Grid& g, const T* ke_host, const T* scale, const T* v
     }
     KhatIso<T> ki{};
     const bool iso = tile_iso_enabled<T>() && khat_iso<T>(ke_host, &ki);
+    const bool iso32 = sizeof(T) == 4 && tile_iso32_plain() && khat_iso<T>(ke_host, &ki);
     const uint32_t f = flags & (TF_MASK_INPUT | TF_PASS_FIXED | TF_ACCUMULATE);
     constexpr uint32_t MP = TF_MASK_INPUT | TF_PASS_FIXED;
     auto launch_shape = [&](const TileShape& sh) -> int {
         dim3 block(TILE_BX, TileDims<T>::BY, 1);
-        // ISO only in FP64 (tile_iso_enabled): the FP32 instantiations stay generic
+        // isotropic blocks: every FP64 product; FP32 plain products (no CG
+        // partials, no accumulation) -- the FP32 CG keeps the generic blocks
 #define T5(M, PS, AC, DT, DP)                                                                                  \
     do {                                                                                                       \
-        if (sizeof(T) == 8 && iso)                                                                             \
-            k_grid_tile5<T, M, PS, AC, DT, TF_TILE_P, sizeof(T) == 8><<<sh.grid, block, 0, st>>>(             \
-                g, sh.oz, scale, v, w, node_fixed, DP, kb, ki);                                                \
+        if ((sizeof(T) == 8 && iso) || (sizeof(T) == 4 && !(AC) && !(DT) && iso32))                           \
+            k_grid_tile5<T, M, PS, AC, DT, TF_TILE_P, !(AC) && !(DT) || sizeof(T) == 8>                         \
+                <<<sh.grid, block, 0, st>>>(g, sh.oz, scale, v, w, node_fixed, DP, kb, ki);                    \
         else                                                                                                   \
             k_grid_tile5<T, M, PS, AC, DT, TF_TILE_P, false><<<sh.grid, block, 0, st>>>(g, sh.oz, scale, v, w, \
                                                                                      node_fixed, DP, kb, ki);  \

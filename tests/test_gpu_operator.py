@@ -357,11 +357,11 @@ def test_node_range_launches_compose_bitwise(prec):
 @pytest.mark.parametrize("prec", ["fp64", "fp32"])
 def test_tile_block_forms_agree(preset, scale, prec, monkeypatch):
     """The tile kernel's two element-block forms -- the generic parity blocks
-    (FP32 production) and the isotropic form (33 FP ops, scale folded into
-    the coefficients; FP64 production, TF_TILE_GENERIC=1 forces the generic
-    form) -- are the same algebra in a different rounding order: they agree
-    to round-off, including masked input with z-varying constraints (mbb) and
-    pass-through; repeated launches are bitwise equal."""
+    (the FP32 CG kernels) and the isotropic form (33 FP ops, scale folded into
+    the coefficients; FP64 and FP32 plain products; TF_TILE_GENERIC=1 forces
+    the generic form) -- are the same algebra in a different rounding order:
+    they agree to round-off, including masked input with z-varying
+    constraints (mbb) and pass-through; repeated launches are bitwise equal."""
     import torch
 
     from paper_2604_18020_b200 import build_edof, make_preset
@@ -377,11 +377,9 @@ def test_tile_block_forms_agree(preset, scale, prec, monkeypatch):
     gen = op.apply(v).clone()
     assert torch.equal(op.apply(v), gen)
     monkeypatch.setenv("TF_TILE_GENERIC", "0")
-    prod = op.apply(v)  # FP64: the isotropic form; FP32: the generic blocks again
-    if prec == "fp32":
-        assert torch.equal(prod, gen)
-    else:
-        assert float((prod - gen).abs().max()) <= 1e-13 * float(gen.abs().max())
+    prod = op.apply(v)  # the isotropic form (every FP64 product, FP32 plain products)
+    tol = 1e-13 if prec == "fp64" else 2e-6
+    assert float((prod - gen).abs().max()) <= tol * float(gen.abs().max())
 
 
 @pytest.mark.parametrize("prec", ["fp64", "fp32"])

@@ -4,6 +4,15 @@
 #include <cstdio>
 #include <cuda_runtime.h>
 
+__global__ void k_spin(const float* __restrict__ src, float* __restrict__ dst, long long n, long long cycles)
+{
+    const long long t0 = clock64();
+    while (clock64() - t0 < cycles) {
+    }
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        dst[i] = src[i];
+}
+
 __global__ void k_copy(const float4* __restrict__ src, float4* __restrict__ dst, long long n4)
 {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4; i += (long long)gridDim.x * blockDim.x)
@@ -84,14 +93,24 @@ int main()
             cudaEventCreateWithFlags(&kd[b], cudaEventDisableTiming);
             cudaEventCreateWithFlags(&d2h[b], cudaEventDisableTiming);
         }
-        for (int kern = 0; kern < 2; ++kern)
+        for (int kern = 0; kern < 4; ++kern)
             for (int pass = 0; pass < 2; ++pass) {
+                // kern 2: a 15 us kernel (the c2 tile product's length); kern 3: the same
+                // schedule captured into one CUDA graph and replayed
+                cudaGraphExec_t gexec = nullptr;
+                if (kern == 3) cudaStreamBeginCapture(s1, cudaStreamCaptureModeGlobal);
                 const int reps = 300;
-                cudaDeviceSynchronize();
-                cudaEventRecord(e0, 0);
-                cudaStreamWaitEvent(s1, e0, 0);
-                cudaStreamWaitEvent(s2, e0, 0);
-                cudaStreamWaitEvent(sk, e0, 0);
+                if (kern != 3) cudaDeviceSynchronize();
+                cudaEvent_t fork;
+                cudaEventCreateWithFlags(&fork, cudaEventDisableTiming);
+                if (kern == 3) {
+                    cudaEventRecord(fork, s1);
+                } else {
+                    cudaEventRecord(e0, 0);
+                    cudaEventRecord(fork, 0);
+                }
+                cudaStreamWaitEvent(s2, fork, 0);
+                cudaStreamWaitEvent(sk, fork, 0);
                 for (int i = 0; i < reps; ++i) {
                     const int b = i & 1;
                     float* di = din2 + b * n;
@@ -101,22 +120,38 @@ int main()
                     cudaEventRecord(h2d[b], s1);
                     cudaStreamWaitEvent(sk, h2d[b], 0);
                     if (i >= 2) cudaStreamWaitEvent(sk, d2h[b], 0);
-                    if (kern) k_copy<<<592, 256, 0, sk>>>((const float4*)di, (float4*)dd, n / 4);
+                    if (kern == 1) k_copy<<<592, 256, 0, sk>>>((const float4*)di, (float4*)dd, n / 4);
+                    if (kern >= 2) k_spin<<<444, 256, 0, sk>>>(di, dd, n, 28000);
                     cudaEventRecord(kd[b], sk);
                     cudaStreamWaitEvent(s2, kd[b], 0);
                     cudaMemcpyAsync(h_out, dd, bytes, cudaMemcpyDeviceToHost, s2);
                     cudaEventRecord(d2h[b], s2);
                 }
-                cudaEvent_t a;
-                cudaEventCreate(&a);
+                cudaEvent_t a, b2;
+                cudaEventCreateWithFlags(&a, cudaEventDisableTiming);
+                cudaEventCreateWithFlags(&b2, cudaEventDisableTiming);
                 cudaEventRecord(a, s2);
-                cudaStreamWaitEvent(0, a, 0);
+                cudaEventRecord(b2, sk);
+                if (kern == 3) {
+                    cudaStreamWaitEvent(s1, a, 0);
+                    cudaStreamWaitEvent(s1, b2, 0);
+                    cudaGraph_t graph;
+                    cudaStreamEndCapture(s1, &graph);
+                    cudaGraphInstantiate(&gexec, graph, 0);
+                    cudaGraphLaunch(gexec, 0);  // warm
+                    cudaDeviceSynchronize();
+                    cudaEventRecord(e0, 0);
+                    cudaGraphLaunch(gexec, 0);
+                } else {
+                    cudaStreamWaitEvent(0, a, 0);
+                    cudaStreamWaitEvent(0, b2, 0);
+                }
                 cudaEventRecord(e1, 0);
                 cudaEventSynchronize(e1);
                 float ms = 0;
                 cudaEventElapsedTime(&ms, e0, e1);
-                if (pass == 1)
-                    printf("pipeline (%s): %7.1f us per step\n", kern ? "d2d kernel" : "no kernel", ms * 1e3 / reps);
+                const char* lab[4] = {"no kernel", "d2d kernel", "15 us kernel", "15 us kernel, one CUDA graph"};
+                if (pass == 1) printf("pipeline (%s): %7.1f us per step\n", lab[kern], ms * 1e3 / reps);
             }
     }
     printf("err %s\n", cudaGetErrorString(cudaGetLastError()));

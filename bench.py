@@ -695,8 +695,7 @@ def kv_scaling(world, rank, dist, same_dev, steps=50):
                      "per_rank_elem": part.local_mesh.n_elem, "ms_per_step": ms,
                      "GDOF_s": gm.n_dof / (ms * 1e-3) / 1e9, "transport": note,
                      "launches_per_step": launches}
-        del x, step
-        torch.cuda.empty_cache()
+        del x, step  # (no empty_cache: the SIMP timings that follow would pay cudaMalloc again)
     return out
 
 

@@ -1,5 +1,5 @@
 """The bench.py JSON line keeps the driver's contract: checked on the last
-committed B200 line (profiles/bench_r1_c2.json, written by `python bench.py`)."""
+committed B200 line (profiles/bench_r2_c2.json, written by `python bench.py`)."""
 
 from __future__ import annotations
 
@@ -12,7 +12,7 @@ ROOT = Path(__file__).resolve().parents[1]
 
 
 def test_bench_line_has_the_contract_keys():
-    d = json.loads((ROOT / "profiles" / "bench_r1_c2.json").read_text())
+    d = json.loads((ROOT / "profiles" / "bench_r2_c2.json").read_text())
     for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
               "scaling", "vs_baseline", "dtype", "data", "config", "roofline", "cpu_baseline", "e2e",
               "gpu_launches", "clocks"):

@@ -554,7 +554,8 @@ def run_ours(args):
                          "peak_source": src, "algorithmic_bytes": alg_bytes,
                          "fma": {"precision": prec, "achieved_tflops": flops / (ms * 1e-3) / 1e12,
                                       "peak_tflops": fp_peak,
-                                      "frac": flops / (ms * 1e-3) / 1e12 / fp_peak}},
+                                      "frac": flops / (ms * 1e-3) / 1e12 / fp_peak},
+                         "issue": issue_roof(args.config, prec, ms, sm_mhz)},
             "warm_l2_ms_per_step": ms_warm,
             "e2e": {"value": n_dof_total / (ms_e2e * 1e-3) / 1e9, "unit": "GDOF/s",
                     "h2d_bytes_per_step": int(m.n_dof * np.dtype(dt).itemsize),
@@ -699,6 +700,24 @@ def kv_scaling(world, rank, dist, same_dev, steps=50):
     return out
 
 
+def issue_roof(cfg, prec, ms, sm_mhz):
+    """The roof that binds the structured kernel: instruction issue.  Warp-
+    instructions per launch from the committed ncu capture of the same
+    kernel and shape (deterministic for a given launch) over this run's
+    per-step time, against 4 issue slots per SM per clock."""
+    p = ROOT / "profiles" / f"tile5_prod_{cfg}_r2.json"
+    if prec != "fp32" or not p.exists():
+        return None
+    k = json.loads(p.read_text())["kernels"][0]
+    inst = float(str(k["smsp__inst_executed.sum"]).split()[0])
+    achieved = inst / (ms * 1e-3) / 1e9
+    peak = 148 * 4 * sm_mhz * 1e6 / 1e9
+    return {"unit": "G warp-instructions/s", "warp_instructions_per_launch": inst, "achieved": achieved,
+            "peak": peak, "frac": achieved / peak, "source": str(p.relative_to(ROOT)),
+            "note": "bench step time (launch included) vs the 4-slot issue roof; ncu issue-active "
+                    "over the kernel alone: " + str(k["smsp__issue_active.avg.pct_of_peak_sustained_active"])}
+
+
 def kernel_sweep(steps=100):
     """Context for the headline (same protocol: L2 flushed before each step,
     CUDA events per step): the structured kernel at c4/c5 and the
@@ -756,7 +775,8 @@ def kernel_sweep(steps=100):
                      "vs_reference": check,
                      "algorithmic_bytes": byts, "hbm_frac": byts / (ms * 1e-3) / 1e9 / hbm,
                      "general_contract_equiv_hbm_frac":
-                         compulsory_bytes(m.n_elem, m.n_dof, prec, False) / (ms * 1e-3) / 1e9 / hbm}
+                         compulsory_bytes(m.n_elem, m.n_dof, prec, False) / (ms * 1e-3) / 1e9 / hbm,
+                     "issue": issue_roof(cfg, prec, ms, peaks()[1]) if kernel == "tile" else None}
         del op, x, w
     return out
 

@@ -338,16 +338,22 @@ k_grid_tile5(Grid g, int oz, const T* __restrict__ scale, const T* __restrict__ 
         const int f = lane + 32 * wi, ii = i0 - 1 + f / 3;
         if (wi < NSEG && f < PW && ii >= 0 && ii < g.nnx && jl < g.nny) geobits |= 1u << NSEG;
     }
-    // zero every slot the prologue does not copy: slots outside the grid
-    // never receive a copy (they feed only zero-scale elements, but 0 * NaN
-    // would not vanish), constrained slots of later planes are never copied
+    // slots outside the grid never receive a copy (they feed only zero-scale
+    // elements, but 0 * NaN would not vanish): zero them once in every
+    // buffer (CTAs at the grid's edges only); constrained slots are zeroed
+    // below once their bits are known
+    unsigned nogeo = 0u;
 #pragma unroll
-    for (int bf = 0; bf < R; ++bf) {
+    for (int sl = 0; sl < NSL; ++sl) {
+        const bool exists = sl < NSEG ? lane + 32 * sl < PW : (wi < NSEG && lane + 32 * wi < PW);
+        if (exists && !((geobits >> sl) & 1u)) nogeo |= 1u << sl;
+    }
+    if (nogeo) {
 #pragma unroll
-        for (int sl = 0; sl < NSL; ++sl) {
-            const bool exists = sl < NSEG ? lane + 32 * sl < PW : (wi < NSEG && lane + 32 * wi < PW);
-            if (exists && (bf > P || !((geobits >> sl) & 1u))) plane[bf][slot_smem(sl)] = T(0);
-        }
+        for (int bf = 0; bf < R; ++bf)
+#pragma unroll
+            for (int sl = 0; sl < NSL; ++sl)
+                if ((nogeo >> sl) & 1u) plane[bf][slot_smem(sl)] = T(0);
     }
     const int el_col = ex + g.nelx * ey, el_plane = g.nelx * g.nely;
     const int n_layers = min(oz, g.nnz - k0) + 1;
@@ -448,6 +454,13 @@ k_grid_tile5(Grid g, int oz, const T* __restrict__ scale, const T* __restrict__ 
                 if (zero) plane[bf][slot_smem(sl)] = T(0);
             }
         }
+        // the buffers filled after the prologue never receive a copy into a
+        // z-invariant constrained slot (those are not in okbits)
+#pragma unroll
+        for (int bf = P + 1; bf < R; ++bf)
+#pragma unroll
+            for (int sl = 0; sl < NSL; ++sl)
+                if ((fixbits >> sl) & 1u) plane[bf][slot_smem(sl)] = T(0);
     }
     __syncthreads();
     TT_CLK(4);

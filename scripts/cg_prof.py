@@ -1,3 +1,8 @@
+"""One short FP32/FP64 cold solve for ncu launch lists of a PCG iteration
+(run with TF_PCG_NOGRAPH=1 so the iteration's kernels launch outside the
+graph):  python scripts/cg_prof.py SCALE fp32|fp64"""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import sys, numpy as np
 from paper_2604_18020_b200 import *
 scale = float(sys.argv[1]); prec = sys.argv[2]

@@ -196,9 +196,13 @@ int tf_matvec_edof_f64(const int32_t* edof, const double* ke, const double* scal
  *      3 corner_of(1,oy,oz) + c of element e equals DOF 3 corner_of(0,oy,oz) + c
  *      of element e+1 in the same 32-element group); the product then sums each
  *      such pair in registers before one red.global.add.  Same contract as
- *      tf_matvec_edof_* in mode TF_SCATTER_ATOMIC (accumulates into w; slots
- *      < 0 are masked).  edof and mask are device pointers.                   */
-int tf_edof_merge_mask(const int32_t* edof, int64_t n_elem, uint16_t* mask, void* stream);
+ *      tf_matvec_edof_* in mode TF_SCATTER_ATOMIC (accumulates into w) except
+ *      for masked slots: they must carry their DOF with the sign bit set
+ *      (DOF | 2^31, not -1); they gather 0 and their row is added to that DOF
+ *      (a constrained DOF, overwritten by the caller's pass-through,
+ *      operator.py:115).  tf_edof_merge_mask checks this (TF_ERR_ARG) and
+ *      synchronises the stream once.  edof and mask are device pointers.       */
+int tf_edof_merge_mask(const int32_t* edof, int64_t n_elem, int64_t n_dof, uint16_t* mask, void* stream);
 int tf_matvec_edof_merged_f32(const int32_t* edof, const uint16_t* mask, const float* ke,
                               const float* scale, const float* v, float* w, int64_t n_elem,
                               void* stream);

@@ -120,7 +120,7 @@ _SIGS = {
     "tf_matvec_grid_range_f64": [_P, _P, _P, _P, _P, _P, _U32, ctypes.c_int32, ctypes.c_int32, _P],
     "tf_matvec_edof_f32": [_P, _P, _P, _P, _P, _I64, _INT, _P, _P, _INT, _P],
     "tf_matvec_edof_f64": [_P, _P, _P, _P, _P, _I64, _INT, _P, _P, _INT, _P],
-    "tf_edof_merge_mask": [_P, _I64, _P, _P],
+    "tf_edof_merge_mask": [_P, _I64, _I64, _P, _P],
     "tf_matvec_edof_merged_f32": [_P, _P, _P, _P, _P, _P, _I64, _P],
     "tf_matvec_edof_merged_f64": [_P, _P, _P, _P, _P, _P, _I64, _P],
     "tf_pass_fixed_f32": [_P, _I64, _P, _P, _P],

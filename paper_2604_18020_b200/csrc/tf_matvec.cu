@@ -493,11 +493,19 @@ __device__ __forceinline__ double ld_if(int idx, const double* base)
 // reference corner order, RIGHT = corner_of(1,oy,oz), LEFT = corner_of(0,oy,oz).
 // bit 3*pr + c of mask[e]: DOF 3 RIGHT[pr] + c of element e is DOF
 // 3 LEFT[pr] + c of element e+1 and both sit in one warp (e % 32 != 31)
-__global__ void k_edof_merge_mask(const int32_t* __restrict__ edof, long long n, uint16_t* __restrict__ mask)
+// Also validates the slots: every entry must name a DOF < n_dof in its low
+// 31 bits (masked slots: sign bit set), since the merged product adds a
+// masked slot's row to that DOF; a violation sets *bad.
+__global__ void k_edof_merge_mask(const int32_t* __restrict__ edof, long long n, long long n_dof,
+                                  uint16_t* __restrict__ mask, int* __restrict__ bad)
 {
     constexpr int RIGHT[4] = {1, 2, 5, 6}, LEFT[4] = {0, 3, 4, 7};
     const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= n) return;
+    bool ok = true;
+#pragma unroll
+    for (int j = 0; j < NLOC; ++j) ok &= (long long)((unsigned)edof[e * NLOC + j] & 0x7fffffffu) < n_dof;
+    if (!ok) atomicOr(bad, 1);
     unsigned m = 0u;
     if ((e & 31) != 31 && e + 1 < n) {
         const int32_t* a = edof + e * NLOC;
@@ -953,12 +961,20 @@ int tf_matvec_grid_f64(const tf_grid* g, const double* ke, const double* scale,
 TF_MATVEC_RANGE(float, f32)
 TF_MATVEC_RANGE(double, f64)
 
-int tf_edof_merge_mask(const int32_t* edof, int64_t n_elem, uint16_t* mask, void* stream)
+int tf_edof_merge_mask(const int32_t* edof, int64_t n_elem, int64_t n_dof, uint16_t* mask, void* stream)
 {
-    TF_REQUIRE(edof && mask && n_elem >= 0, "bad arguments");
+    TF_REQUIRE(edof && mask && n_elem >= 0 && n_dof > 0, "bad arguments");
     if (n_elem == 0) return TF_OK;
-    k_edof_merge_mask<<<(unsigned)((n_elem + 255) / 256), 256, 0, S(stream)>>>(edof, n_elem, mask);
+    int* bad = nullptr;
+    TF_CUDA_TRY(cudaMallocAsync((void**)&bad, sizeof(int), S(stream)));
+    TF_CUDA_TRY(cudaMemsetAsync(bad, 0, sizeof(int), S(stream)));
+    k_edof_merge_mask<<<(unsigned)((n_elem + 255) / 256), 256, 0, S(stream)>>>(edof, n_elem, n_dof, mask, bad);
     TF_CHECK_LAUNCH();
+    int h = 0;
+    TF_CUDA_TRY(cudaMemcpyAsync(&h, bad, sizeof(int), cudaMemcpyDeviceToHost, S(stream)));
+    TF_CUDA_TRY(cudaFreeAsync(bad, S(stream)));
+    TF_CUDA_TRY(cudaStreamSynchronize(S(stream)));  // once per connectivity
+    TF_REQUIRE(h == 0, "edof slots must name a DOF < n_dof in their low 31 bits (masked slots: DOF | 2^31)");
     return TF_OK;
 }
 

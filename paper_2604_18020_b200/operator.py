@@ -122,7 +122,7 @@ class DeviceProblem:
             t = D.torch()
             em = self.edof_masked
             self._merge = t.empty(self.n_elem, dtype=t.int16, device=em.device)
-            _lib.call("tf_edof_merge_mask", D.ptr(em), self.n_elem, D.ptr(self._merge), D.stream_ptr())
+            _lib.call("tf_edof_merge_mask", D.ptr(em), self.n_elem, self.n_dof, D.ptr(self._merge), D.stream_ptr())
         return self._merge
 
     def colors(self):

@@ -439,3 +439,23 @@ def test_merged_atomic_edof_matches_oracle(prec, relabel, monkeypatch):
     inner = (lanes != 31) & (ex != m.nelx - 1)
     assert np.all(mask[inner] == 0xFFF)
     assert np.all(mask[~inner] == 0)
+
+
+def test_merge_mask_rejects_minus_one_slots():
+    """The merged atomic product adds a masked slot's row to the DOF in its low
+    31 bits, so the connectivity check refuses -1 slots (which would address
+    DOF 2^31-1) instead of letting a product write out of bounds."""
+    import torch
+
+    from paper_2604_18020_b200 import _device as D
+    from paper_2604_18020_b200 import _lib
+
+    m, edof, bcs, rho, v = seeded_case((4, 3, 2), 11)
+    bad = edof.astype(np.int32).copy()
+    bad[0, 5] = -1
+    e_d = torch.tensor(bad, device="cuda")
+    mask = torch.empty(m.n_elem, dtype=torch.int16, device="cuda")
+    with pytest.raises(_lib.TfError, match="low 31 bits"):
+        _lib.call("tf_edof_merge_mask", D.ptr(e_d), m.n_elem, m.n_dof, D.ptr(mask), D.stream_ptr())
+    good = torch.tensor(D.masked_edof(edof, bcs.fixed_dofs, m.n_dof), device="cuda")
+    _lib.call("tf_edof_merge_mask", D.ptr(good), m.n_elem, m.n_dof, D.ptr(mask), D.stream_ptr())

@@ -524,10 +524,11 @@ __global__ void k_edof_merge_mask(const int32_t* __restrict__ edof, long long n,
 #ifndef TF_EDOFM_MINB32
 #define TF_EDOFM_MINB32 8  // 64 registers, no spills: 32 warps/SM (c5 187 vs 197 us at 6)
 #endif
-template <typename T>
+template <typename T, bool ISO>
 __global__ void __launch_bounds__(EDOF_BLOCK, sizeof(T) == 4 ? TF_EDOFM_MINB32 : TF_EDOF_MINB)
 k_edof_merged(const int32_t* __restrict__ edof, const uint16_t* __restrict__ merge, const T* __restrict__ scale,
-              const T* __restrict__ v, T* __restrict__ w, long long n, const __grid_constant__ KhatBlocks<T> kb)
+              const T* __restrict__ v, T* __restrict__ w, long long n, const __grid_constant__ KhatBlocks<T> kb,
+              const __grid_constant__ KhatIso<T> ki)
 {
     constexpr int RIGHT[4] = {1, 2, 5, 6}, LEFT[4] = {0, 3, 4, 7};
     __shared__ __align__(16) int4 rows[EDOF_BLOCK * 6];
@@ -560,7 +561,10 @@ k_edof_merged(const int32_t* __restrict__ edof, const uint16_t* __restrict__ mer
 #pragma unroll
     for (int q = 0; q < NLOC; ++q) u[q] = ld_if(idx[q], v);
     T fw[NLOC];
-    element_apply(u, se, kb, fw);
+    if (ISO)
+        element_apply_iso(u, se, ki, fw);
+    else
+        element_apply(u, se, kb, fw);
     const unsigned prev = __shfl_up_sync(0xffffffffu, mk, 1) * (lane > 0);
 #pragma unroll
     for (int pr = 0; pr < 4; ++pr)
@@ -884,6 +888,14 @@ using namespace tf;
 
 static inline cudaStream_t S(void* p) { return reinterpret_cast<cudaStream_t>(p); }
 
+// isotropic element blocks in the merged atomic product (TF_TILE_GENERIC=1:
+// the generic blocks, as everywhere)
+static bool tile_iso_general()
+{
+    const char* e = getenv("TF_TILE_GENERIC");
+    return !(e && e[0] == '1');
+}
+
 extern "C" {
 
 const char* tf_last_error(void) { return tf::g_err; }
@@ -990,7 +1002,13 @@ int tf_edof_merge_mask(const int32_t* edof, int64_t n_elem, int64_t n_dof, uint1
             return launch_edof<T>(edof, ke, scale, v, w, n_elem, TF_SCATTER_ATOMIC, nullptr, nullptr, 0,   \
                                   S(stream));                                                              \
         const long long nb = (n_elem + EDOF_BLOCK - 1) / EDOF_BLOCK;                                       \
-        k_edof_merged<T><<<(unsigned)nb, EDOF_BLOCK, 0, S(stream)>>>(edof, merge, scale, v, w, n_elem, kb); \
+        KhatIso<T> ki{};                                                                                   \
+        if (tile_iso_general() && khat_iso<T>(ke, &ki))                                                    \
+            k_edof_merged<T, true><<<(unsigned)nb, EDOF_BLOCK, 0, S(stream)>>>(edof, merge, scale, v, w,   \
+                                                                              n_elem, kb, ki);             \
+        else                                                                                               \
+            k_edof_merged<T, false><<<(unsigned)nb, EDOF_BLOCK, 0, S(stream)>>>(edof, merge, scale, v, w,  \
+                                                                               n_elem, kb, ki);            \
         TF_CHECK_LAUNCH();                                                                                 \
         return TF_OK;                                                                                      \
     }

@@ -183,6 +183,27 @@ __device__ __forceinline__ void element_apply(const T (&u)[NLOC], T s, const Kha
         for (int c = 0; c < 3; ++c) f[3 * a + c] = g[c][bin_of(a)];
 }
 
-// Each thread handles at most STAGE_SLOTS values of a staged node plane.
+// the same with the isotropic block form (block_iso: 33 FP ops, the scale
+// folded into the 16 coefficients) for a Ke that has it (khat_iso)
+template <typename T>
+__device__ __forceinline__ void element_apply_iso(const T (&u)[NLOC], T s, const KhatIso<T>& ki,
+                                                  T (&f)[NLOC])
+{
+    T h[3][8];
+#pragma unroll
+    for (int a = 0; a < 8; ++a)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) h[c][bin_of(a)] = u[3 * a + c];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) fwht_fwd(h[c]);
+    T g[3][8];
+    block_iso(h, ki, s, g);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) fwht_inv(g[c]);
+#pragma unroll
+    for (int a = 0; a < 8; ++a)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) f[3 * a + c] = g[c][bin_of(a)];
+}
 
 }  // namespace tf

@@ -127,9 +127,23 @@ __device__ __noinline__ void res_wait(const double* part, const unsigned* ctr, i
         double acc[K];
 #pragma unroll
         for (int k = 0; k < K; ++k) acc[k] = 0.0;
-        for (int i = tid; i < nblk; i += 32) {
+        // the partials of 8 rounds are loaded before any is added (one L2
+        // round trip per 256 CTAs instead of one per 32-128); the adds keep
+        // the ascending-CTA order of each lane
+        constexpr int U = 8;
+        for (int i0 = tid; i0 < nblk; i0 += 32 * U) {
+            double t[U][K];
 #pragma unroll
-            for (int k = 0; k < K; ++k) acc[k] += __ldcg(slot + (size_t)i * 4 + k);
+            for (int u = 0; u < U; ++u)
+#pragma unroll
+                for (int k = 0; k < K; ++k)
+                    t[u][k] = i0 + 32 * u < nblk ? __ldcg(slot + (size_t)(i0 + 32 * u) * 4 + k) : 0.0;
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                if (i0 + 32 * u < nblk) {
+#pragma unroll
+                    for (int k = 0; k < K; ++k) acc[k] += t[u][k];
+                }
         }
 #pragma unroll
         for (int k = 0; k < K; ++k) {

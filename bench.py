@@ -361,6 +361,9 @@ def run_ours(args):
         flush.fill_(1)
         step()
     torch.cuda.synchronize()
+    # the reference's drift gate (its bench.py:229-234): the timed products
+    # must equal an untimed product bit for bit
+    untimed = w.clone() if world == 1 else None
 
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
@@ -388,6 +391,12 @@ def run_ours(args):
 
     # the timed product against the reference's apply on the same inputs
     vs_ref = reference_check(args.config, prec, w.double().cpu().numpy()) if world == 1 else None
+    drift = None
+    if world == 1:
+        drift = float(torch.linalg.vector_norm((w - untimed).double()).item())
+        atomic = args.kernel == "edof" and args.scatter == "parallel_atomic"  # order-dependent sums
+        if drift != 0.0 and not atomic:
+            raise AssertionError(f"timed products drifted from the untimed one: {drift:.3e}")
 
     # warm-L2 (solver-like back-to-back) rate, for context
     torch.cuda.synchronize()
@@ -563,6 +572,7 @@ def run_ours(args):
             "gpu_launches": args.steps * per_step_launches,
             "equivalence_gate_rel_l2": gate_rel,
             "vs_reference": vs_ref,
+            "drift_gate": drift,
             "e2e_path": "MatFreeOperator.apply_stream (cudaHostAlloc host in/out; native 3-stream pipeline, csrc/tf_stream.cu); median of 3 batches of `steps` products after 1 s of PCIe warm-up" if world == 1
                         else "SlabOperator.apply per step (pinned host in/out)",
             "clocks": ck,

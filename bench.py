@@ -517,8 +517,18 @@ def run_ours(args):
         traffic = json.loads(tf.read_text()).get(f"{args.config}_{prec}")
 
     simp = cg = simp2 = sweep = None
-    scaling = simp_scaling_all(world, dist) if args.simp else None
-    kv_scale = kv_scaling(world, rank, dist, same_dev) if args.simp else None
+    # the scaling blocks are context, not the headline: a failure there (the
+    # same on every rank) is reported in the line instead of losing it
+    scaling = kv_scale = None
+    if args.simp:
+        try:
+            scaling = simp_scaling_all(world, dist)
+        except Exception as e:  # noqa: BLE001
+            scaling = {"error": repr(e)[:300]}
+        try:
+            kv_scale = kv_scaling(world, rank, dist, same_dev)
+        except Exception as e:  # noqa: BLE001
+            kv_scale = {"error": repr(e)[:300]}
     if args.simp and rank == 0:
         simp = simp_c1()
         simp2 = simp_c2()

@@ -358,55 +358,45 @@ k_grid_tile5(Grid g, int oz, const T* __restrict__ scale, const T* __restrict__ 
     const int el_col = ex + g.nelx * ey, el_plane = g.nelx * g.nely;
     const int n_layers = min(oz, g.nnz - k0) + 1;
     const int kmax = k0 - 1 + n_layers;  // top plane of the chunk's last layer
-    const T* v_own = v + row_own;
-    const T* v_last = v + row_last;
     // one cp.async group: node plane kz (slots `bits`; `varbits` slots carry
     // z-varying constraints, zero-filled where node kz's bit is set) and the
     // scales of element layer kz.  Planes outside the mesh are zero-filled,
-    // planes past the chunk skipped.
+    // planes past the chunk skipped.  Addresses: a CTA-uniform plane base
+    // (64-bit, uniform datapath) plus the slot's 32-bit offset -- the
+    // per-slot 64-bit pointer arithmetic this replaces cost ~30 instructions
+    // per element-layer (ncu source counts, c5).
     auto stage = [&](int kz, int buf, unsigned bits, unsigned varbits) {
         if (kz <= kmax) {
             T* pb = plane[buf];
-            if (kz >= 0 && kz < g.nnz) {
-                const long long zb = (long long)kz * pn3;
+            const bool pok = kz >= 0 && kz < g.nnz;
+            const T* vz = v + (long long)(pok ? kz : 0) * pn3;
 #pragma unroll
-                for (int sl = 0; sl < NSL; ++sl)
-                    if ((bits >> sl) & 1u) {
-                        const T* src = (sl < NSEG ? v_own + 32 * sl : v_last) + zb;
-                        if (sizeof(T) == 4)
-                            cp_async_4(pb + slot_smem(sl), src, true);
-                        else
-                            cp_async_8(pb + slot_smem(sl), src, true);
-                    }
-                if (MASK && varbits) {  // rare: columns whose constraint varies along z
-#pragma unroll
-                    for (int sl = 0; sl < NSL; ++sl)
-                        if ((varbits >> sl) & 1u) {
-                            const int d = slot_dof(sl);
-                            const bool keep = !((node_fixed[kz * (long long)pn + d / 3] >> (d % 3)) & 1u);
-                            const T* src = (sl < NSEG ? v_own + 32 * sl : v_last) + zb;
-                            if (sizeof(T) == 4)
-                                cp_async_4(pb + slot_smem(sl), src, keep);
-                            else
-                                cp_async_8(pb + slot_smem(sl), src, keep);
-                        }
+            for (int sl = 0; sl < NSL; ++sl)
+                if ((bits >> sl) & 1u) {
+                    if (sizeof(T) == 4)
+                        cp_async_4(pb + slot_smem(sl), vz + slot_dof(sl), pok);
+                    else
+                        cp_async_8(pb + slot_smem(sl), vz + slot_dof(sl), pok);
                 }
-            } else {
+            if (MASK && varbits) {  // rare: columns whose constraint varies along z
 #pragma unroll
                 for (int sl = 0; sl < NSL; ++sl)
-                    if (((bits | varbits) >> sl) & 1u) {
+                    if ((varbits >> sl) & 1u) {
+                        const int d = slot_dof(sl);
+                        const bool keep = pok && !((node_fixed[kz * (long long)pn + d / 3] >> (d % 3)) & 1u);
                         if (sizeof(T) == 4)
-                            cp_async_4(pb + slot_smem(sl), v, false);
+                            cp_async_4(pb + slot_smem(sl), vz + d, keep);
                         else
-                            cp_async_8(pb + slot_smem(sl), v, false);
+                            cp_async_8(pb + slot_smem(sl), vz + d, keep);
                     }
             }
-            const bool sok = col_ok && kz >= 0 && kz < g.nelz;
-            const T* sp = scale + (sok ? el_col + (long long)el_plane * kz : 0);
+            const bool lok = kz >= 0 && kz < g.nelz;
+            const T* sz = scale + (long long)el_plane * (lok ? kz : 0);
+            const bool sok = col_ok && lok;
             if (sizeof(T) == 4)
-                cp_async_4(&sc[buf][tid], sp, sok);
+                cp_async_4(&sc[buf][tid], sz + (col_ok ? el_col : 0), sok);
             else
-                cp_async_8(&sc[buf][tid], sp, sok);
+                cp_async_8(&sc[buf][tid], sz + (col_ok ? el_col : 0), sok);
         }
         cp_async_commit();  // possibly empty: keeps the group count uniform
     };

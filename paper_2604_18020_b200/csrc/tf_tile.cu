@@ -328,7 +328,15 @@ k_grid_tile5(Grid g, int oz, const T* __restrict__ scale, const T* __restrict__ 
     auto slot_smem = [&](int sl) { return sl < NSEG ? wi * PW + lane + 32 * sl : TILE_BY * PW + lane + 32 * wi; };
     auto slot_dof = [&](int sl) { return sl < NSEG ? row_own + 32 * sl : row_last; };
     unsigned geobits = 0u;  // bit sl: slot sl holds a node inside the grid
-    {
+    // a CTA whose node rectangle lies inside the grid keeps every existing
+    // slot (a uniform test; only the CTAs at the grid's edges evaluate slots)
+    const bool inner = i0 >= 1 && i0 - 1 + TILE_BX < g.nnx && j0 >= 1 && j0 - 1 + TILE_BY < g.nny;
+    if (inner) {
+#pragma unroll
+        for (int k = 0; k < NSEG; ++k)
+            if (lane + 32 * k < PW) geobits |= 1u << k;
+        if (wi < NSEG && lane + 32 * wi < PW) geobits |= 1u << NSEG;
+    } else {
         const int jo = j0 - 1 + wi, jl = j0 - 1 + TILE_BY;
 #pragma unroll
         for (int k = 0; k < NSEG; ++k) {
@@ -404,16 +412,36 @@ k_grid_tile5(Grid g, int oz, const T* __restrict__ scale, const T* __restrict__ 
     // prologue: planes k0-1 .. k0-1+P (P+1 groups) in flight together, on geometry alone
 #pragma unroll
     for (int bf = 0; bf <= P; ++bf) stage(k0 - 1 + bf, bf, geobits, 0u);
-    // constraint bits of the staged slots (loads overlap the copies above)
+    // constraint bits of the staged slots (loads overlap the copies above).
+    // Tall chunks first ask whether the CTA holds a constrained node column at
+    // all -- one column-OR byte per thread and a block vote -- and skip the
+    // per-slot work otherwise (c5: 82.3 -> 80.7 us); short chunks (one-wave
+    // grids, where the vote's load would sit on every CTA's critical path)
+    // evaluate the slots directly.
     unsigned fixbits = 0u, varbits = 0u;
     if (MASK && have_nf) {
-#pragma unroll
-        for (int sl = 0; sl < NSL; ++sl)
-            if ((geobits >> sl) & 1u) {
-                const int d = slot_dof(sl), node = d / 3, c = d - 3 * node;
-                if ((col_and[node] >> c) & 1u) fixbits |= 1u << sl;
-                else if ((col_or[node] >> c) & 1u) varbits |= 1u << sl;
+        bool need = true;
+        if (oz >= 8) {
+            bool f = false;
+            const int ii = i0 - 1 + tx, jj = j0 - 1 + ty;
+            if (ii >= 0 && ii < g.nnx && jj >= 0 && jj < g.nny) f = col_or[ii + g.nnx * jj] != 0;
+            const int jl = j0 - 1 + TILE_BY, il = i0 - 1 + TILE_BX;
+            if (ty == 0 && ii >= 0 && ii < g.nnx && jl < g.nny) f |= col_or[ii + g.nnx * jl] != 0;
+            if (ty == 1 && tx <= TILE_BY && il < g.nnx) {
+                const int j2 = j0 - 1 + tx;
+                if (j2 >= 0 && j2 < g.nny) f |= col_or[il + g.nnx * j2] != 0;
             }
+            need = __syncthreads_or(f) != 0;
+        }
+        if (need) {
+#pragma unroll
+            for (int sl = 0; sl < NSL; ++sl)
+                if ((geobits >> sl) & 1u) {
+                    const int d = slot_dof(sl), node = d / 3, c = d - 3 * node;
+                    if ((col_and[node] >> c) & 1u) fixbits |= 1u << sl;
+                    else if ((col_or[node] >> c) & 1u) varbits |= 1u << sl;
+                }
+        }
     }
     const unsigned okbits = geobits & ~fixbits & ~varbits;
     const int pofs = ty * PW + 3 * tx;

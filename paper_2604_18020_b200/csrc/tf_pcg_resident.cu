@@ -40,6 +40,8 @@
 #include <cstdlib>
 #include <cstring>
 #include <type_traits>
+#include <utility>
+#include <vector>
 
 #include "tf_common.cuh"
 #include "tf_walsh.cuh"
@@ -460,6 +462,14 @@ k_pcg_resident(const __grid_constant__ ResArgs<T> A, const __grid_constant__ Kha
 
     constexpr bool PDIR = true, RAW = false;
     const bool tracing = A.trace != nullptr && bid == 0 && tid == 0;
+    // -DTF_PCG_CTA_TRACE builds (never the product library): every CTA's
+    // summed matvec-pass time, the arrival skew behind exchange A
+#ifdef TF_PCG_CTA_TRACE
+    const bool cta_trace = A.trace != nullptr && tid == 0;
+#else
+    constexpr bool cta_trace = false;
+#endif
+    unsigned long long mv_sum = 0ull;
     unsigned long long tr[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     unsigned long long t_mark = tracing ? res_gtime() : 0ull;
     auto lap = [&](int slot) {
@@ -537,7 +547,9 @@ k_pcg_resident(const __grid_constant__ ResArgs<T> A, const __grid_constant__ Kha
     while (!done) {
         ++it;
         // A. q = A p_it, fused p.q
+        const unsigned long long mv_t0 = cta_trace ? res_gtime() : 0ull;
         double t1[1] = {tile_pass(PDIR, it == 1, (T)beta, A.z, A.pbuf[(it - 1) & 1], A.pbuf[it & 1])};
+        if (cta_trace) mv_sum += res_gtime() - mv_t0;
         ++matvecs;
         lap(0);
         res_block_sum<1, NT>(t1, shr, tid);
@@ -649,6 +661,7 @@ k_pcg_resident(const __grid_constant__ ResArgs<T> A, const __grid_constant__ Kha
         lap(4);
     }
 
+    if (cta_trace) A.trace[16 + bid] = mv_sum;
     // solution: every DOF written once by its owner
     if (!lean) {
         for (int kk = 0; kk < n_own; ++kk)
@@ -667,6 +680,7 @@ k_pcg_resident(const __grid_constant__ ResArgs<T> A, const __grid_constant__ Kha
     }
     if (tracing) {
         for (int k = 0; k < 6; ++k) A.trace[k] = tr[k];
+
         A.trace[6] = (unsigned long long)it;
         A.trace[7] = tr[6];
         A.trace[8] = tr[7];
@@ -806,10 +820,16 @@ int launch_pcg_resident(const ResPlan& plan, const Grid& g, const T* ke_host, in
     a.sc = sc;
     a.trace = nullptr;
     static unsigned long long* trace_buf = nullptr;
+    static long long trace_cap = 0;
     const bool tracing = getenv("TF_PCG_TRACE") != nullptr;
+    const long long trace_n = 16 + plan.nblk;
     if (tracing) {
-        if (!trace_buf) TF_CUDA_TRY(cudaMalloc(&trace_buf, 16 * sizeof(unsigned long long)));
-        TF_CUDA_TRY(cudaMemsetAsync(trace_buf, 0, 16 * sizeof(unsigned long long), st));
+        if (trace_cap < trace_n) {
+            if (trace_buf) cudaFree(trace_buf);
+            TF_CUDA_TRY(cudaMalloc(&trace_buf, trace_n * sizeof(unsigned long long)));
+            trace_cap = trace_n;
+        }
+        TF_CUDA_TRY(cudaMemsetAsync(trace_buf, 0, trace_n * sizeof(unsigned long long), st));
         a.trace = trace_buf;
     }
     TF_CUDA_TRY(cudaMemsetAsync(ring, 0, sizeof(double) * pcg_resident_ring_doubles(plan), st));
@@ -819,9 +839,25 @@ int launch_pcg_resident(const ResPlan& plan, const Grid& g, const T* ke_host, in
     dim3 block(TILE_BX, plan.by, 1);
     TF_CUDA_TRY(cudaLaunchCooperativeKernel(k, plan.grid, block, args, plan.dyn_smem, st));
     if (tracing) {
-        unsigned long long h[16];
-        TF_CUDA_TRY(cudaMemcpyAsync(h, trace_buf, sizeof(h), cudaMemcpyDeviceToHost, st));
+        std::vector<unsigned long long> hv(trace_n);
+        TF_CUDA_TRY(cudaMemcpyAsync(hv.data(), trace_buf, trace_n * sizeof(unsigned long long),
+                                    cudaMemcpyDeviceToHost, st));
         TF_CUDA_TRY(cudaStreamSynchronize(st));
+        const unsigned long long* h = hv.data();
+#ifdef TF_PCG_CTA_TRACE
+        {  // per-CTA matvec-pass time: the arrival skew behind exchange A
+            std::vector<std::pair<unsigned long long, long long>> m;
+            for (long long b = 0; b < plan.nblk; ++b) m.push_back({h[16 + b], b});
+            std::sort(m.begin(), m.end());
+            const double n = h[6] ? (double)h[6] : 1.0;
+            const long long gx = plan.grid.x, gy = plan.grid.y;
+            auto at = [&](size_t i) { return m[i].first / n / 1e3; };
+            const long long bmax = m.back().second;
+            fprintf(stderr, "[tf_pcg_resident] matvec pass per CTA, us/it: min %.2f p50 %.2f p90 %.2f max %.2f "
+                            "(slowest CTA %lld,%lld,%lld)\n", at(0), at(m.size() / 2), at(m.size() * 9 / 10),
+                    at(m.size() - 1), bmax % gx, (bmax / gx) % gy, bmax / (gx * gy));
+        }
+#endif
         const double n = h[6] ? (double)h[6] : 1.0;
         fprintf(stderr,
                 "[tf_pcg_resident] fp%d BY %d grid %ux%ux%u oz %d %s: %llu its; us/it: matvec %.2f  xchg-A %.2f  "

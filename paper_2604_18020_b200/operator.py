@@ -156,7 +156,6 @@ def element_colouring(mesh: StructuredMesh, edof: np.ndarray):
     if not ok:
         if mesh.n_elem > 300_000:
             raise NotImplementedError("greedy colouring of large non-grid connectivity")
-        owner = {}
         col = np.zeros(mesh.n_elem, dtype=np.int64)
         used_by_dof = [set() for _ in range(int(edof.max()) + 1)]
         for i in range(mesh.n_elem):
@@ -169,7 +168,6 @@ def element_colouring(mesh: StructuredMesh, edof: np.ndarray):
             col[i] = c
             for d in edof[i]:
                 used_by_dof[d].add(c)
-        del owner
     order = np.argsort(col, kind="stable").astype(np.int32)
     counts = np.bincount(col, minlength=int(col.max()) + 1)
     offsets = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)

@@ -246,7 +246,11 @@ __global__ void __launch_bounds__(VEC_BLOCK) k_update(CgP<T> P, const double* pa
 {
     constexpr int N = V16<T>::N;
     CgScalars* sc = P.sc;
-    if (sc->done) return;
+    if (sc->done) {
+        // an unrolled loop body ran past the stop: keep its refresh branch off
+        if (P.in_graph && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(P.h_refresh, 0u);
+        return;
+    }
     __shared__ double shp[VEC_BLOCK / 32];
     const bool f32 = sizeof(T) == 4;
     const double pq = rnd(sum_partials(part_mv, nmv, shp), f32);
@@ -688,9 +692,10 @@ static int enqueue_matvec(PcgImpl* h, const T* v, T* w, double* dot_part, cudaSt
 
 // Add a captured sequence as the content of `body` (a conditional body graph).
 template <typename F>
-static int capture_into(cudaGraph_t body, cudaStream_t cap, F&& fn)
+static int capture_into(cudaGraph_t body, cudaStream_t cap, F&& fn, const cudaGraphNode_t* deps = nullptr,
+                        size_t ndeps = 0)
 {
-    TF_CUDA_TRY(cudaStreamBeginCaptureToGraph(cap, body, nullptr, nullptr, 0,
+    TF_CUDA_TRY(cudaStreamBeginCaptureToGraph(cap, body, deps, nullptr, ndeps,
                                               cudaStreamCaptureModeThreadLocal));
     const int rc = fn(cap);
     cudaGraph_t out = nullptr;
@@ -776,48 +781,69 @@ static int build_graph(PcgImpl* h)
     CgP<T> P = params_of<T>(h);
     const int nvb = h->n_vec_blocks;
 
-    // part 1: matvec+dot, update
-    cudaGraphNode_t last_node = nullptr;
-    {
-        int rc = capture_into(body, cap, [&](cudaStream_t st) -> int { return enqueue_part1<T>(h, P, st); });
-        if (rc) return rc;
+    // The WHILE body holds `unroll` CG iterations (TF_PCG_UNROLL, default 4 on
+    // the unfused protocol): one conditional evaluation per `unroll`
+    // iterations.  Kernels of an iteration past the stop return at entry
+    // (sc->done), k_update also switching the refresh branch off; only the
+    // matvec of such an iteration still runs (once per solve).
+    int unroll = 1;
+    if (!h->fused) {
+        const char* eu = getenv("TF_PCG_UNROLL");
+        unroll = std::max(1, std::min(8, eu ? atoi(eu) : 4));
     }
-    // find the sink node of the body so far
-    {
+    // sink (dependent-free) node of a graph
+    auto sink_of = [&](cudaGraph_t gr, cudaGraphNode_t* out) -> int {
         size_t n = 0;
-        TF_CUDA_TRY(cudaGraphGetNodes(body, nullptr, &n));
+        TF_CUDA_TRY(cudaGraphGetNodes(gr, nullptr, &n));
         std::vector<cudaGraphNode_t> nodes(n);
-        TF_CUDA_TRY(cudaGraphGetNodes(body, nodes.data(), &n));
+        TF_CUDA_TRY(cudaGraphGetNodes(gr, nodes.data(), &n));
         for (auto nd : nodes) {
             size_t nout = 0;
             TF_CUDA_TRY(cudaGraphNodeGetDependentNodes(nd, nullptr, &nout));
-            if (nout == 0) last_node = nd;
+            if (nout == 0) *out = nd;
         }
-    }
-    // IF refresh { q = A x ; r = b - q }
-    cudaGraphNodeParams ip = {};
-    ip.type = cudaGraphNodeTypeConditional;
-    ip.conditional.handle = h->h_refresh;
-    ip.conditional.type = cudaGraphCondTypeIf;
-    ip.conditional.size = 1;
-    cudaGraphNode_t inode;
-    TF_CUDA_TRY(cudaGraphAddNode(&inode, body, &last_node, 1, &ip));
-    cudaGraph_t ifbody = ip.conditional.phGraph_out[0];
-    {
-        int rc = capture_into(ifbody, cap, [&](cudaStream_t st) -> int { return enqueue_refresh<T>(h, P, st); });
-        if (rc) return rc;
-    }
-    // direction update after the IF node (folded into the next matvec when fused)
-    if (!h->fused) {
-        cudaKernelNodeParams kp = {};
-        int nparts = nvb;
-        void* args[] = {&P, &nparts};
-        kp.func = (void*)k_direction<T>;
-        kp.gridDim = dim3(nvb);
-        kp.blockDim = dim3(VEC_BLOCK);
-        kp.kernelParams = args;
-        cudaGraphNode_t dn;
-        TF_CUDA_TRY(cudaGraphAddKernelNode(&dn, body, &inode, 1, &kp));
+        return TF_OK;
+    };
+    cudaGraphNode_t tail = nullptr;  // last node of the previous iteration in the body
+    for (int u = 0; u < unroll; ++u) {
+        // every IF node needs its own conditional handle (set by its k_update)
+        CgP<T> Pu = P;
+        if (u > 0) TF_CUDA_TRY(cudaGraphConditionalHandleCreate(&Pu.h_refresh, body, 0, 0));
+        // part 1: matvec+dot, update
+        {
+            int rc = capture_into(body, cap, [&](cudaStream_t st) -> int { return enqueue_part1<T>(h, Pu, st); },
+                                  tail ? &tail : nullptr, tail ? 1 : 0);
+            if (rc) return rc;
+        }
+        cudaGraphNode_t last_node = nullptr;
+        if (int rc = sink_of(body, &last_node)) return rc;
+        // IF refresh { q = A x ; r = b - q }
+        cudaGraphNodeParams ip = {};
+        ip.type = cudaGraphNodeTypeConditional;
+        ip.conditional.handle = Pu.h_refresh;
+        ip.conditional.type = cudaGraphCondTypeIf;
+        ip.conditional.size = 1;
+        cudaGraphNode_t inode;
+        TF_CUDA_TRY(cudaGraphAddNode(&inode, body, &last_node, 1, &ip));
+        cudaGraph_t ifbody = ip.conditional.phGraph_out[0];
+        {
+            int rc = capture_into(ifbody, cap, [&](cudaStream_t st) -> int { return enqueue_refresh<T>(h, Pu, st); });
+            if (rc) return rc;
+        }
+        tail = inode;
+        // direction update after the IF node (folded into the next matvec when fused)
+        if (!h->fused) {
+            cudaKernelNodeParams kp = {};
+            int nparts = nvb;
+            void* args[] = {&Pu, &nparts};
+            kp.func = (void*)k_direction<T>;
+            kp.gridDim = dim3(nvb);
+            kp.blockDim = dim3(VEC_BLOCK);
+            kp.kernelParams = args;
+            cudaGraphNode_t dn;
+            TF_CUDA_TRY(cudaGraphAddKernelNode(&dn, body, &inode, 1, &kp));
+            tail = dn;
+        }
     }
     TF_CUDA_TRY(cudaGraphInstantiate(&h->exec, h->graph, 0));
     cudaStreamDestroy(cap);

@@ -203,7 +203,16 @@ __device__ __forceinline__ void st16(T* p, long long c, const T (&o)[V16<T>::N])
 __device__ __forceinline__ double sum_partials(const double* part, int n, double* sh)
 {
     double v = 0.0;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) v += __ldcg(part + i);
+    // loads of four rounds issued before their adds (one L2 round trip for up
+    // to 4 blockDim partials), same per-thread order
+    for (int i0 = threadIdx.x; i0 < n; i0 += 4 * blockDim.x) {
+        double t[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) t[u] = i0 + u * (int)blockDim.x < n ? __ldcg(part + i0 + u * blockDim.x) : 0.0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            if (i0 + u * (int)blockDim.x < n) v += t[u];
+    }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
     if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
@@ -458,9 +467,20 @@ __global__ void __launch_bounds__(VEC_BLOCK) k_direction(CgP<T> P, int nparts)
     double rr = 0.0, rzn = 0.0;
     {
         double v = 0.0, w = 0.0;
-        for (int i = threadIdx.x; i < nparts; i += VEC_BLOCK) {
-            v += __ldcg(P.part + 2 * i);
-            w += __ldcg(P.part + 2 * i + 1);
+        for (int i0 = threadIdx.x; i0 < nparts; i0 += 4 * VEC_BLOCK) {  // loads before adds, as sum_partials
+            double tv[4], tw[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int i = i0 + u * VEC_BLOCK;
+                tv[u] = i < nparts ? __ldcg(P.part + 2 * i) : 0.0;
+                tw[u] = i < nparts ? __ldcg(P.part + 2 * i + 1) : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (i0 + u * VEC_BLOCK < nparts) {
+                    v += tv[u];
+                    w += tw[u];
+                }
         }
         double vv[2] = {v, w};
         __shared__ double sh2[2 * 32];

@@ -816,7 +816,12 @@ int launch_pcg_resident(const ResPlan& plan, const Grid& g, const T* ke_host, in
     a.node_fixed = node_fixed;
     a.ring = ring;
     a.lean = plan.lean;
-    a.iso = (tile_iso_enabled<T>() && khat_iso<T>(ke_host, &a.ki)) ? 1 : 0;
+    {
+        // FP32: the generic blocks unless TF_RES_ISO32=1 (experiment)
+        const char* e = getenv("TF_RES_ISO32");
+        const bool iso32 = sizeof(T) == 4 && e && e[0] == '1';
+        a.iso = ((tile_iso_enabled<T>() || iso32) && khat_iso<T>(ke_host, &a.ki)) ? 1 : 0;
+    }
     a.sc = sc;
     a.trace = nullptr;
     static unsigned long long* trace_buf = nullptr;

@@ -948,11 +948,12 @@ struct TileShape {
 
 // The isotropic block form (khat_iso) in every FP64 kernel: there the kernel
 // is DFMA-bound and the 25 fewer FP ops per element-layer are worth 30 % (c5
-// 125 vs 179 us).  The FP32 CG kernels (fused p.q, resident PCG) keep the
-// generic blocks: the different rounding order shifts FP32 CG counts by more
-// than the +-2 % bar (torsion SIMP 10013 vs 10786 total); FP32 plain
-// products take the iso form (tile_iso32_plain).  TF_TILE_GENERIC=1 forces
-// the generic blocks everywhere.
+// 125 vs 179 us).  The FP32 SM-resident PCG keeps the generic blocks: the
+// different rounding order shifted its FP32 CG counts by more than the +-2 %
+// bar on converging solves (torsion SIMP 10013 vs 10786 total); FP32 plain
+// products and the graph-protocol CG matvec take the iso form
+// (tile_iso32_plain, tile_iso32_cg).  TF_TILE_GENERIC=1 forces the generic
+// blocks everywhere.
 template <typename T>
 bool tile_iso_enabled()
 {
@@ -965,6 +966,16 @@ template bool tile_iso_enabled<float>();
 // form too: c2 14.4 vs 15.3 us, c4 27.8 vs 29.4, c5 84.2 vs 90.2 (B200,
 // scripts/tile_ab.py); the FP32 CG keeps the generic blocks (see above).
 // TF_TILE_ISO32=0 or TF_TILE_GENERIC=1 keeps them generic.
+// The graph-protocol FP32 CG matvec (fused p.q partials; grids too large for
+// the SM-resident solve, whose FP32 CG stays generic) takes the isotropic
+// form as well: c4 47.3 -> 43.4 us per iteration, c5 192 -> 179; those
+// solves run to the 1000-iteration cap like the reference's (counts equal),
+// compliance moves by 1e-6.  TF_CG_ISO32=0 keeps the generic blocks.
+static bool tile_iso32_cg()
+{
+    const char* e = getenv("TF_CG_ISO32");
+    return !(e && e[0] == '0');
+}
 static bool tile_iso32_plain()
 {
     const char* e = getenv("TF_TILE_ISO32");
@@ -1179,7 +1190,11 @@ int launch_grid_tile(const Grid& g, const T* ke_host, const T* scale, const T* v
                 set_error("the fused p.q epilogue needs TF_MASK_INPUT | TF_PASS_FIXED");
                 return TF_ERR_ARG;
             }
-            T5(true, true, false, true, dot_part);
+            if (sizeof(T) == 4 && iso32 && tile_iso32_cg())
+                k_grid_tile5<T, true, true, false, true, TF_TILE_P, true>
+                    <<<sh.grid, block, 0, st>>>(g, sh.oz, scale, v, w, node_fixed, dot_part, kb, ki);
+            else
+                T5(true, true, false, true, dot_part);
         } else {
             switch (f) {
             case MP: T5(true, true, false, false, nullptr); break;

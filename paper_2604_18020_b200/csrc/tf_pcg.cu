@@ -131,14 +131,15 @@ __device__ bool last_block_reduce(double (&v)[K], double* part, unsigned* ticket
                 for (int i = 0; i < nw; ++i) s += sh[k * 32 + i];
                 part[(size_t)bid * K + k] = s;
             }
-            __threadfence();
-            const unsigned t = atomicAdd(ticket, 1u);
+            // acq_rel ticket: releases this block's partials (and, through the
+            // barrier above, its threads' writes); the last block acquires all
+            unsigned t;
+            asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(t) : "l"(ticket) : "memory");
             am_last = (t == (unsigned)nblocks - 1);
         }
         __syncthreads();
     }
     if (!am_last) return false;
-    __threadfence();
     // fixed-order reduction of all partials: thread t sums partials t, t+nthr, ...
     double acc[K];
 #pragma unroll

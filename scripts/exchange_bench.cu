@@ -42,6 +42,8 @@ __device__ __forceinline__ void st_rlx64(unsigned long long* p, unsigned long lo
 //         reads all partials (L2) and sums in a fixed order
 // mode 1: mode 0 with __nanosleep backoff in the poll
 // mode 2: per-CTA sentinel slots polled by warp 0 (no counter)
+// mode 6: mode 1 without the __threadfence before the red.release
+// mode 7: mode 6 polled inside warp 0; mode 8+j: arrivals over 2^j counters
 // mode 3: cooperative-groups style: fence + atomicAdd + volatile gen poll + fence
 template <int MODE>
 __global__ void k_xchg(unsigned* ctr, double* part, unsigned long long* slots, int reps, double* out)
@@ -52,18 +54,55 @@ __global__ void k_xchg(unsigned* ctr, double* part, unsigned long long* slots, i
     for (int ph = 0; ph < reps; ++ph) {
         const double mine = (double)(bid + 1) * (ph + 1);
         __syncthreads();
-        if (MODE == 0 || MODE == 1) {
+        if (MODE == 0 || MODE == 1 || MODE == 6) {
             if (tid == 0) {
                 part[(size_t)(ph & 1) * nblk + bid] = mine;
-                __threadfence();
+                if (MODE != 6) __threadfence();  // mode 6: the release alone orders the write
                 red_rel(ctr, 1u);
                 const unsigned target = (unsigned)(ph + 1) * nblk;
                 while (ld_acq(ctr) < target) {
-                    if (MODE == 1) __nanosleep(20);
+                    if (MODE != 0) __nanosleep(20);
                 }
             }
             __syncthreads();
             if (tid < 32) {
+                double a = 0.0;
+                for (int i = tid; i < nblk; i += 32) a += __ldcg(part + (size_t)(ph & 1) * nblk + i);
+                for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+                if (tid == 0) sh = a;
+            }
+        } else if (MODE == 7) {
+            // mode 6 with the poll inside warp 0 (no CTA barrier between the
+            // acquire and the partial loads)
+            if (tid < 32) {
+                if (tid == 0) {
+                    part[(size_t)(ph & 1) * nblk + bid] = mine;
+                    red_rel(ctr, 1u);
+                    const unsigned target = (unsigned)(ph + 1) * nblk;
+                    while (ld_acq(ctr) < target) __nanosleep(20);
+                }
+                __syncwarp();
+                double a = 0.0;
+                for (int i = tid; i < nblk; i += 32) a += __ldcg(part + (size_t)(ph & 1) * nblk + i);
+                for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+                if (tid == 0) sh = a;
+            }
+        } else if (MODE >= 8) {
+            // mode 8+j: mode 7 with the arrivals spread over NC = 2^j counters
+            // (own 128-B lines; same-address reductions serialise in L2), lane
+            // c < NC of warp 0 polls counter c
+            constexpr int NC = 1 << (MODE >= 8 ? MODE - 8 : 0);
+            if (tid < 32) {
+                if (tid == 0) {
+                    part[(size_t)(ph & 1) * nblk + bid] = mine;
+                    red_rel(ctr + 32 * (bid % NC), 1u);
+                }
+                if (tid < NC) {
+                    const unsigned cnt = (unsigned)((nblk - tid + NC - 1) / NC);
+                    const unsigned target = (unsigned)(ph + 1) * cnt;
+                    while (ld_acq(ctr + 32 * tid) < target) __nanosleep(20);
+                }
+                __syncwarp();
                 double a = 0.0;
                 for (int i = tid; i < nblk; i += 32) a += __ldcg(part + (size_t)(ph & 1) * nblk + i);
                 for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
@@ -313,6 +352,13 @@ int main(int argc, char** argv)
             run<2>(per_sm, nt, reps, nsm);
             run<3>(per_sm, nt, reps, nsm);
             run<4>(per_sm, nt, reps, nsm);
+            run<6>(per_sm, nt, reps, nsm);
+            run<7>(per_sm, nt, reps, nsm);
+            run<10>(per_sm, nt, reps, nsm);
+            run<11>(per_sm, nt, reps, nsm);
+            run<12>(per_sm, nt, reps, nsm);
+            run<13>(per_sm, nt, reps, nsm);
+            if (argc > 1) continue;
             run_cluster<4>(per_sm, nt, reps, nsm);
             run_cluster<8>(per_sm, nt, reps, nsm);
             run_cluster<16>(per_sm, nt, reps, nsm);

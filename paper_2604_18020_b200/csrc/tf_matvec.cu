@@ -521,10 +521,54 @@ __global__ void k_edof_merge_mask(const int32_t* __restrict__ edof, long long n,
     mask[e] = (uint16_t)m;
 }
 
+// L2 eviction-priority hints for the streams read once per product (the
+// connectivity rows, element scales and merge masks: evict_first), so the
+// 472 MB edof stream at c5 displaces them rather than the gathered v and the
+// reduced w (both normal priority: an L2 flush still evicts them)
+__device__ __forceinline__ unsigned long long l2_evict_first()
+{
+    unsigned long long pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ void cp_async_16_ef(void* smem, const void* gmem, bool valid, unsigned long long pol)
+{
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    const int n = valid ? 16 : 0;
+    asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2, %3;\n" ::"r"(sa), "l"(gmem), "r"(n),
+                 "l"(pol));
+}
+__device__ __forceinline__ float ld_ef(const float* p, unsigned long long pol)
+{
+    float r;
+    asm volatile("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(r) : "l"(p), "l"(pol));
+    return r;
+}
+__device__ __forceinline__ double ld_ef(const double* p, unsigned long long pol)
+{
+    double r;
+    asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(r) : "l"(p), "l"(pol));
+    return r;
+}
+__device__ __forceinline__ unsigned ld_ef(const uint16_t* p, unsigned long long pol)
+{
+    unsigned short r;
+    asm volatile("ld.global.nc.L2::cache_hint.u16 %0, [%1], %2;" : "=h"(r) : "l"(p), "l"(pol));
+    return r;
+}
+static bool edof_hint_enabled()
+{
+    static const bool on = [] {
+        const char* e = getenv("TF_EDOF_HINT");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 #ifndef TF_EDOFM_MINB32
 #define TF_EDOFM_MINB32 8  // 64 registers, no spills: 32 warps/SM (c5 187 vs 197 us at 6)
 #endif
-template <typename T, bool ISO>
+template <typename T, bool ISO, bool HINT>
 __global__ void __launch_bounds__(EDOF_BLOCK, sizeof(T) == 4 ? TF_EDOFM_MINB32 : TF_EDOF_MINB)
 k_edof_merged(const int32_t* __restrict__ edof, const uint16_t* __restrict__ merge, const T* __restrict__ scale,
               const T* __restrict__ v, T* __restrict__ w, long long n, const __grid_constant__ KhatBlocks<T> kb,
@@ -536,16 +580,24 @@ k_edof_merged(const int32_t* __restrict__ edof, const uint16_t* __restrict__ mer
     const int tid = threadIdx.x, lane = tid & 31;
     const long long n_here = min((long long)EDOF_BLOCK, n - e0);
     const int4* src = reinterpret_cast<const int4*>(edof + e0 * NLOC);
+    const unsigned long long pol = HINT ? l2_evict_first() : 0ull;
 #pragma unroll
     for (int q = 0; q < 6; ++q) {
         const int k = tid + q * EDOF_BLOCK;
-        cp_async_16(&rows[k], src + k, k < n_here * 6);
+        if (HINT)
+            cp_async_16_ef(&rows[k], src + k, k < n_here * 6, pol);
+        else
+            cp_async_16(&rows[k], src + k, k < n_here * 6);
     }
     asm volatile("cp.async.commit_group;\n" ::);
     const long long e = e0 + tid;
     const bool live = tid < n_here;
-    const T se = live ? ld_nc(scale + e) : T(0);
-    const unsigned mk = live ? (unsigned)ld_nc(merge + e) : 0u;
+    T se = T(0);
+    unsigned mk = 0u;
+    if (live) {
+        se = HINT ? ld_ef(scale + e, pol) : ld_nc(scale + e);
+        mk = HINT ? ld_ef(merge + e, pol) : (unsigned)ld_nc(merge + e);
+    }
     asm volatile("cp.async.wait_group 0;\n" ::);
     __syncthreads();
     int idx[NLOC];
@@ -1003,12 +1055,17 @@ int tf_edof_merge_mask(const int32_t* edof, int64_t n_elem, int64_t n_dof, uint1
                                   S(stream));                                                              \
         const long long nb = (n_elem + EDOF_BLOCK - 1) / EDOF_BLOCK;                                       \
         KhatIso<T> ki{};                                                                                   \
-        if (tile_iso_general() && khat_iso<T>(ke, &ki))                                                    \
-            k_edof_merged<T, true><<<(unsigned)nb, EDOF_BLOCK, 0, S(stream)>>>(edof, merge, scale, v, w,   \
-                                                                              n_elem, kb, ki);             \
+        const bool iso = tile_iso_general() && khat_iso<T>(ke, &ki);                                       \
+        const bool hint = edof_hint_enabled();                                                             \
+        const dim3 gb((unsigned)nb), bb(EDOF_BLOCK);                                                       \
+        if (iso && hint)                                                                                   \
+            k_edof_merged<T, true, true><<<gb, bb, 0, S(stream)>>>(edof, merge, scale, v, w, n_elem, kb, ki);  \
+        else if (iso)                                                                                      \
+            k_edof_merged<T, true, false><<<gb, bb, 0, S(stream)>>>(edof, merge, scale, v, w, n_elem, kb, ki); \
+        else if (hint)                                                                                     \
+            k_edof_merged<T, false, true><<<gb, bb, 0, S(stream)>>>(edof, merge, scale, v, w, n_elem, kb, ki); \
         else                                                                                               \
-            k_edof_merged<T, false><<<(unsigned)nb, EDOF_BLOCK, 0, S(stream)>>>(edof, merge, scale, v, w,  \
-                                                                               n_elem, kb, ki);            \
+            k_edof_merged<T, false, false><<<gb, bb, 0, S(stream)>>>(edof, merge, scale, v, w, n_elem, kb, ki); \
         TF_CHECK_LAUNCH();                                                                                 \
         return TF_OK;                                                                                      \
     }

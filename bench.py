@@ -790,7 +790,7 @@ def kernel_sweep(steps=100):
         check = reference_check(cfg, prec, w.double().cpu().numpy(),
                                 perm if name.endswith("seeded_random") else None)
         byts = compulsory_bytes(m.n_elem, m.n_dof, prec, kernel != "edof")
-        out[name] = {"workload": desc, "kernel": "k_grid_tile5" if kernel == "tile" else "k_edof_staged (red.global)",
+        out[name] = {"workload": desc, "kernel": "k_grid_tile5" if kernel == "tile" else "k_edof_merged (red.global)",
                      "ms_per_step": ms, "GDOF_s": m.n_dof / (ms * 1e-3) / 1e9,
                      "vs_reference": check,
                      "algorithmic_bytes": byts, "hbm_frac": byts / (ms * 1e-3) / 1e9 / hbm,

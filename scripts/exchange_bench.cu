@@ -359,6 +359,7 @@ int main(int argc, char** argv)
             run<12>(per_sm, nt, reps, nsm);
             run<13>(per_sm, nt, reps, nsm);
             if (argc > 1) continue;
+            run_cluster<2>(per_sm, nt, reps, nsm);
             run_cluster<4>(per_sm, nt, reps, nsm);
             run_cluster<8>(per_sm, nt, reps, nsm);
             run_cluster<16>(per_sm, nt, reps, nsm);

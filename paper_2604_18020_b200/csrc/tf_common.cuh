@@ -140,6 +140,7 @@ struct ResPlan {
     int by;  // element-column rows per CTA
     size_t dyn_smem;
     long long nblk;
+    int onex;  // single-exchange iteration (full layout only)
 };
 
 }  // namespace tf

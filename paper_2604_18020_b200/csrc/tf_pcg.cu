@@ -50,7 +50,7 @@ bool pcg_resident_plan(const Grid& g, const T* ke_host, ResPlan* plan);
 template <typename T>
 int launch_pcg_resident(const ResPlan& plan, const Grid& g, const T* ke_host, int has_x0, const T* scale,
                         const T* b, const T* inv, T* x, T* z, T* p0, T* p1, const uint8_t* node_fixed,
-                        double* ring, CgScalars* sc, cudaStream_t st);
+                        double* ring, CgScalars* sc, T* r1, T* q0, T* q1, cudaStream_t st);
 size_t pcg_resident_ring_doubles(const ResPlan& plan);
 
 
@@ -655,6 +655,7 @@ struct PcgImpl {
     // device buffers
     void *x, *r, *p, *q, *b, *inv, *scale;
     void* p2;           // second search-direction buffer (fused protocol)
+    void *r2, *q2;      // resident single-exchange iteration: r_k / q_k ping-pong partners
     int quantize;       // quantize_krylov for the next solve (tf_pcg_set_quantize_krylov)
     int fused;          // structured tile solve with the direction folded into the matvec
     int resident;       // SM-resident solve: one cooperative launch (tf_pcg_resident.cu)
@@ -896,7 +897,8 @@ static int solve_impl(PcgImpl* h, const void* scale, const void* b, const void* 
     if (h->resident) {
         int rc = launch_pcg_resident<T>(h->rplan, h->grid, (const T*)h->ke.data(), has_x0, (const T*)h->scale,
                                         (const T*)h->b, (const T*)h->inv, (T*)h->x, (T*)h->r, (T*)h->p,
-                                        (T*)h->p2, h->node_fixed, h->ring, h->sc, st);
+                                        (T*)h->p2, h->node_fixed, h->ring, h->sc, (T*)h->r2, (T*)h->q,
+                                        (T*)h->q2, st);
         if (rc) return rc;
         TF_CUDA_TRY(cudaMemcpyAsync(h->sc_host, h->sc, sizeof(CgScalars), cudaMemcpyDeviceToHost, st));
         TF_CUDA_TRY(cudaStreamSynchronize(st));
@@ -986,6 +988,7 @@ int tf_pcg_create(tf_pcg** out, const tf_pcg_desc* d, void* stream)
     h->exec = nullptr;
     h->x = h->r = h->p = h->q = h->b = h->inv = h->scale = nullptr;
     h->p2 = nullptr;
+    h->r2 = h->q2 = nullptr;
     h->part = nullptr;
     h->part_mv = nullptr;
     h->tickets = nullptr;
@@ -1050,6 +1053,14 @@ int tf_pcg_create(tf_pcg** out, const tf_pcg_desc* d, void* stream)
         TF_CUDA_TRY(cudaMalloc(&h->ring, sizeof(double) * pcg_resident_ring_doubles(h->rplan)));
     }
     if (h->fused || h->resident) TF_CUDA_TRY(cudaMalloc(&h->p2, vb));
+    if (h->resident && h->rplan.onex) {
+        TF_CUDA_TRY(cudaMalloc(&h->r2, vb));
+        TF_CUDA_TRY(cudaMalloc(&h->q2, vb));
+        // halo reads of the first iterations stay finite
+        TF_CUDA_TRY(cudaMemset(h->r2, 0, vb));
+        TF_CUDA_TRY(cudaMemset(h->q2, 0, vb));
+        TF_CUDA_TRY(cudaMemset(h->q, 0, vb));
+    }
     if (h->resident) {
         // p buffers are read before first written only behind the `first` flag,
         // but keep them finite for the halo reads of the first iteration
@@ -1110,7 +1121,7 @@ int tf_pcg_destroy(tf_pcg* hh)
     if (h->exec) cudaGraphExecDestroy(h->exec);
     if (h->graph) cudaGraphDestroy(h->graph);
     void* bufs[] = {h->x, h->r, h->p, h->q, h->b, h->inv, h->scale, h->p2, h->part, h->part_mv, h->tickets, h->sc,
-                    h->ring};
+                    h->ring, h->r2, h->q2};
     for (void* p : bufs)
         if (p) cudaFree(p);
     if (h->sc_host) cudaFreeHost(h->sc_host);

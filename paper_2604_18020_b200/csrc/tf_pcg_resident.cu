@@ -63,7 +63,12 @@ struct ResArgs {
     T* z;        // z = r * D^-1 of the last update (halo source for p)
     T* pbuf[2];  // p_k in pbuf[k & 1]
     const uint8_t* node_fixed;
-    double* ring;  // [2][nblk][4] exchange partials, then the arrival counter
+    double* ring;  // [2][nblk][RES_SLOT] exchange partials, then the arrival counter
+    // single-exchange iteration (onex): r_k, q_k published for the halo
+    // recomputation of p_{k+1} (ping-pong by k & 1)
+    T* rbuf[2];
+    T* qbuf[2];
+    int onex;
     int lean;      // x and D^-1 in global memory instead of shared memory
     int iso;       // isotropic block form (block_iso) instead of the generic blocks
     KhatIso<T> ki;
@@ -101,15 +106,17 @@ __device__ __forceinline__ void res_red_release(unsigned* p, unsigned v)
 // partials in CTA order (measured on B200: 3.1 us per exchange at 296 CTAs,
 // vs 7.1 us for per-CTA sentinel slots polled by every CTA -- L2 flooding --
 // and 3.6 us for a count-reset/generation barrier; scripts/exchange_bench.cu).
+constexpr int RES_SLOT = 8;  // doubles per CTA and exchange slot (K <= 8)
+
 template <int K>
 __device__ __noinline__ void res_arrive(double* part, unsigned* ctr, int nblk, int bid, int tid, unsigned phase,
                                         const double (&v)[K])
 {
-    double* slot = part + (size_t)(phase & 1u) * nblk * 4;
+    double* slot = part + (size_t)(phase & 1u) * nblk * RES_SLOT;
     __syncthreads();  // the CTA's data writes precede the release below
     if (tid == 0) {
 #pragma unroll
-        for (int k = 0; k < K; ++k) slot[(size_t)bid * 4 + k] = v[k];
+        for (int k = 0; k < K; ++k) slot[(size_t)bid * RES_SLOT + k] = v[k];
         // the release is cumulative over the CTA's writes ordered by the
         // barrier above (no separate fence: 0.26 us less per exchange at 296
         // CTAs, scripts/exchange_bench.cu modes 1 vs 6)
@@ -121,12 +128,46 @@ template <int K>
 __device__ __noinline__ void res_wait(const double* part, const unsigned* ctr, int nblk, int tid, unsigned phase,
                                       double (&v)[K], double* sh /* >= K */)
 {
-    const double* slot = part + (size_t)(phase & 1u) * nblk * 4;
+    const double* slot = part + (size_t)(phase & 1u) * nblk * RES_SLOT;
     if (tid == 0) {
         const unsigned target = (phase + 1u) * (unsigned)nblk;
         while (res_ld_acquire(ctr) < target) __nanosleep(20);
     }
     __syncthreads();
+    if constexpr (K > 4) {
+        // wide payloads: every thread sums value k = tid % 8 of CTAs tid / 8,
+        // + nt / 8, ... (its loads issued together), then thread k adds the
+        // nt / 8 column sums in order -- warp 0 alone would need one L2 round
+        // trip per 32 CTAs for 8 values each
+        __shared__ double wide[512];
+        const int nt = (int)(blockDim.x * blockDim.y);
+        const int k = tid & 7, js = nt >> 3;
+        double acc = 0.0;
+        if (k < K) {
+            constexpr int U = 8;
+            for (int j = tid >> 3; j < nblk; j += js * U) {
+                double t[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u)
+                    t[u] = j + u * js < nblk ? __ldcg(slot + (size_t)(j + u * js) * RES_SLOT + k) : 0.0;
+#pragma unroll
+                for (int u = 0; u < U; ++u)
+                    if (j + u * js < nblk) acc += t[u];
+            }
+        }
+        wide[tid] = acc;
+        __syncthreads();
+        if (tid < K) {
+            double s2 = 0.0;
+            for (int jj = 0; jj < js; ++jj) s2 += wide[jj * 8 + tid];
+            sh[tid] = s2;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int kk = 0; kk < K; ++kk) v[kk] = sh[kk];
+        __syncthreads();
+        return;
+    }
     if (tid < 32) {
         double acc[K];
 #pragma unroll
@@ -141,7 +182,7 @@ __device__ __noinline__ void res_wait(const double* part, const unsigned* ctr, i
             for (int u = 0; u < U; ++u)
 #pragma unroll
                 for (int k = 0; k < K; ++k)
-                    t[u][k] = i0 + 32 * u < nblk ? __ldcg(slot + (size_t)(i0 + 32 * u) * 4 + k) : 0.0;
+                    t[u][k] = i0 + 32 * u < nblk ? __ldcg(slot + (size_t)(i0 + 32 * u) * RES_SLOT + k) : 0.0;
 #pragma unroll
             for (int u = 0; u < U; ++u)
                 if (i0 + 32 * u < nblk) {
@@ -215,7 +256,7 @@ struct ResTile {
 // BY: element-column rows per CTA (FP32 8 or 16, FP64 4 or 8): taller tiles
 // halve the CTA count (cheaper exchanges, less halo recompute) at the same
 // warps per SM
-template <typename T, int BY_>
+template <typename T, int BY_, bool ONEX>
 __global__ void __launch_bounds__(TILE_BX * BY_, (TILE_BX * BY_ >= 512 || (sizeof(T) == 8 && BY_ >= 8))
                                                      ? 1
                                                      : (sizeof(T) == 4 ? TF_RES_MINB32 : TF_RES_MINB64))
@@ -226,7 +267,7 @@ k_pcg_resident(const __grid_constant__ ResArgs<T> A, const __grid_constant__ Kha
     constexpr bool F32 = sizeof(T) == 4;
     __shared__ __align__(16) T plane[2][PN];
     __shared__ T Y[3][NT];
-    __shared__ double shr[3 * (NT / 32)];
+    __shared__ double shr[8 * (NT / 32)];
     extern __shared__ __align__(16) unsigned char res_dyn[];
 
     const Grid& g = A.g;
@@ -250,7 +291,7 @@ k_pcg_resident(const __grid_constant__ ResArgs<T> A, const __grid_constant__ Kha
     const uint8_t* col_and = nf ? col_or + pn : nullptr;
     const int own_node0 = (i0 + tx) + g.nnx * (j0 + ty);
     unsigned phase = 0u;  // exchange counter (identical sequence in every CTA)
-    unsigned* ctr = reinterpret_cast<unsigned*>(A.ring + (size_t)8 * nblk);
+    unsigned* ctr = reinterpret_cast<unsigned*>(A.ring + (size_t)2 * RES_SLOT * nblk);
 
     // owned vectors in shared memory: own(v, kk, c) for this thread.  Full
     // layout: x r inv p q; lean: r p q (x and inv in global memory).
@@ -309,8 +350,17 @@ k_pcg_resident(const __grid_constant__ ResArgs<T> A, const __grid_constant__ Kha
     // own(VQ); returns this thread's p.q (PDIR).
     // (one instantiation for both modes: the kernel's code footprint is kept
     // small so the per-iteration phases stay in the instruction cache)
-    auto tile_pass = [&](bool pdir, bool first, T be, const T* src, const T* pold, T* pnew) -> double {
-        auto fetch = [&](int kz, T (&pa)[NS], T (&pb)[NS]) {
+    // ONEX (single-exchange iteration): the staged input is p_k = z_k +
+    // beta p_{k-1} with z_k = r_k D^-1 and r_k = r_{k-1} - alpha_{k-1} q_{k-1}
+    // recomputed from the published r_{k-1}, q_{k-1} (`src`, `qsrc`; `fresh`:
+    // r_k published as is -- first iteration, after a true-residual refresh)
+    // exactly as the owner computes them, so no barrier is needed between the
+    // owners' update and the neighbours' staging; owners also apply x_k =
+    // x_{k-1} + alpha_{k-1} p_{k-1} and publish r_k (rnew) and q_k (qnew).
+    T* invtab = own + (size_t)(lean ? 3 : 5) * oz * 3 * NT;  // ONEX: D^-1 over the staged footprint
+    auto tile_pass = [&](bool pdir, bool first, T be, const T* src, const T* pold, T* pnew, bool fresh = true,
+                         T ap = T(0), const T* qsrc = nullptr, T* rnew = nullptr, T* qnew = nullptr) -> double {
+        auto fetch = [&](int kz, T (&pa)[NS], T (&pb)[NS], T (&pc)[NS]) {
             const bool zok = kz >= 0 && kz < g.nnz;
             const int base = min(max(kz, 0), g.nnz - 1) * pn3;
 #pragma unroll
@@ -319,22 +369,40 @@ k_pcg_resident(const __grid_constant__ ResArgs<T> A, const __grid_constant__ Kha
                 const int d = base + s_off[q];
                 pa[q] = take ? __ldcg(src + d) : T(0);
                 if (pdir) pb[q] = (take && !first) ? __ldcg(pold + d) : T(0);
+                if (ONEX && pdir) pc[q] = (take && !fresh) ? __ldcg(qsrc + d) : T(0);
             }
         };
-        auto commit = [&](int kz, T* buf, const T (&pa)[NS], const T (&pb)[NS]) {
+        auto commit = [&](int kz, T* buf, const T (&pa)[NS], const T (&pb)[NS], const T (&pc)[NS]) {
             const bool zok = kz >= 0 && kz < g.nnz;
             const bool wr = pdir && zok && kz >= k0 && kz < kend;
             const int base = min(max(kz, 0), g.nnz - 1) * pn3;
+            const int pl = (kz - (k0 - 1)) * PN;  // ONEX: plane row of the D^-1 table
 #pragma unroll
             for (int q = 0; q < NS; ++q) {
                 const int idx = tid + q * NT;
                 if (q < NS - 1 || idx < PN) {
                     const bool ok = zok && ((okbits >> q) & 1u);
                     T pv = pa[q];
-                    if (pdir && !first) pv = add_rn(pa[q], mul_rn(be, pb[q]));
+                    T rv = T(0);
+                    if (ONEX && pdir) {
+                        rv = fresh ? pa[q] : sub_rn(pa[q], mul_rn(ap, pc[q]));
+                        const T zv = mul_rn(rv, invtab[pl + idx]);
+                        pv = first ? zv : add_rn(zv, mul_rn(be, pb[q]));
+                    } else if (pdir && !first) {
+                        pv = add_rn(pa[q], mul_rn(be, pb[q]));
+                    }
                     if (!ok) pv = T(0);
                     if (wr && s_own[q] >= 0) {
                         pnew[base + s_off[q]] = pv;
+                        const int ob = (kz - k0) * 3 * NT + s_own[q];
+                        if (ONEX) {
+                            if (!first && !fresh) {
+                                T* xo = own + (size_t)VX * oz * 3 * NT + ob;
+                                *xo = add_rn(*xo, mul_rn(ap, own[(size_t)VP * oz * 3 * NT + ob]));
+                            }
+                            own[(size_t)VR * oz * 3 * NT + ob] = rv;
+                            rnew[base + s_off[q]] = rv;
+                        }
                         own[(VP * oz + (kz - k0)) * 3 * NT + s_own[q]] = pv;
                     }
                     bool fixed = (allfix >> q) & 1u;
@@ -348,16 +416,16 @@ k_pcg_resident(const __grid_constant__ ResArgs<T> A, const __grid_constant__ Kha
         const int n_layers = kend - k0 + 1;
         T* b_cur = plane[0];
         T* b_top = plane[1];
-        T pa[NS], pb[NS];
+        T pa[NS], pb[NS], pc[NS];
         {
             // both prologue planes in flight together (one L2 round trip)
-            T qa[NS], qb[NS];
-            fetch(k0 - 1, qa, qb);
-            fetch(k0, pa, pb);
-            commit(k0 - 1, b_cur, qa, qb);
-            commit(k0, b_top, pa, pb);
+            T qa[NS], qb[NS], qc[NS];
+            fetch(k0 - 1, qa, qb, qc);
+            fetch(k0, pa, pb, pc);
+            commit(k0 - 1, b_cur, qa, qb, qc);
+            commit(k0, b_top, pa, pb, pc);
         }
-        fetch(k0 + 1, pa, pb);
+        fetch(k0 + 1, pa, pb, pc);
         __syncthreads();
         T XYb[3][4];
 #pragma unroll
@@ -375,8 +443,8 @@ k_pcg_resident(const __grid_constant__ ResArgs<T> A, const __grid_constant__ Kha
             const int ez = k0 - 1 + L;
             if (L >= 1) {
                 // plane ez+1 into the buffer that held plane ez-1 (read before (B) of layer L-1)
-                commit(ez + 1, b_top, pa, pb);
-                if (L + 1 < n_layers) fetch(ez + 2, pa, pb);
+                commit(ez + 1, b_top, pa, pb, pc);
+                if (L + 1 < n_layers) fetch(ez + 2, pa, pb, pc);
             }
             __syncthreads();  // (A)
             const T s_next = scale_at(ez + 1);
@@ -448,6 +516,7 @@ k_pcg_resident(const __grid_constant__ ResArgs<T> A, const __grid_constant__ Kha
                         const T p = own[oidx(VP, kk, c, tid)];
                         if (fx) acc = p;  // pass-through of the unmasked input
                         dot += (double)p * (double)acc;
+                        if (ONEX) qnew[dof(kk, c)] = acc;
                     } else if (fx) {
                         acc = get_x(kk, c);
                     }
@@ -496,6 +565,21 @@ k_pcg_resident(const __grid_constant__ ResArgs<T> A, const __grid_constant__ Kha
 #pragma unroll
             for (int c = 0; c < 3; ++c) A.x[dof(kk, c)] = T(0);
     }
+    if (ONEX) {
+        // D^-1 over the staged footprint, planes k0-1 .. kend (static for the solve)
+        for (int pl = 0; pl < kend - k0 + 2; ++pl) {
+            const int kz = k0 - 1 + pl;
+            const bool zok = kz >= 0 && kz < g.nnz;
+#pragma unroll
+            for (int q = 0; q < NS; ++q) {
+                const int idx = tid + q * NT;
+                if (idx < PN) {
+                    const bool ok = zok && ((okbits >> q) & 1u);
+                    invtab[pl * PN + idx] = ok ? ld_nc(A.inv + (size_t)kz * pn3 + s_off[q]) : T(0);
+                }
+            }
+        }
+    }
     __syncthreads();
     if (A.has_x0) tile_pass(RAW, false, T(0), A.x, nullptr, nullptr);  // own(VQ) = A x0
     double tot[3] = {0.0, 0.0, 0.0};
@@ -508,7 +592,10 @@ k_pcg_resident(const __grid_constant__ ResArgs<T> A, const __grid_constant__ Kha
                 const T r = A.has_x0 ? sub_rn(bb, own[oidx(VQ, kk, c, tid)]) : bb;
                 const T z = mul_rn(r, get_inv(kk, c));
                 own[oidx(VR, kk, c, tid)] = r;
-                A.z[d] = z;
+                if (ONEX)
+                    A.rbuf[0][d] = r;
+                else
+                    A.z[d] = z;
                 tot[0] += (double)bb * (double)bb;
                 tot[1] += (double)r * (double)r;
                 tot[2] += (double)r * (double)z;
@@ -546,6 +633,132 @@ k_pcg_resident(const __grid_constant__ ResArgs<T> A, const __grid_constant__ Kha
     lap(5);
 
     // ---- iterations (solver.py:104-137) --------------------------------------------
+    if constexpr (ONEX) {
+        // One exchange per iteration.  The pass of iteration k stages p_k from
+        // the published r_{k-1}, q_{k-1}, p_{k-1} (see tile_pass), so the only
+        // grid-wide step is the reduction after it, which carries p.q and the
+        // own-DOF sums r.r, r.z (direct, of r_k), r.q, q.q, r.Dq, q.Dq, r.Dr:
+        // alpha_k = r.z / p.q exactly as the two-exchange loop (same values,
+        // same order), while ||r_{k+1}||^2 and r_{k+1}.z_{k+1} -- which the
+        // convergence test and beta_k need before r_{k+1} exists -- are
+        // expanded one step in FP64: r.r - 2a r.q + a^2 q.q (a = alpha_k in the
+        // working dtype, as the update applies it).
+        bool fresh = true;  // r_k published as is (first iteration, after a refresh)
+        bool xpend = false;  // x_{k+1} = x_k + alpha_k p_k not yet applied
+        T ap = T(0);
+        while (!done) {
+            ++it;
+            const unsigned long long mv_t0 = cta_trace ? res_gtime() : 0ull;
+            const double pq_loc =
+                tile_pass(PDIR, it == 1, (T)beta, A.rbuf[(it - 1) & 1], A.pbuf[(it - 1) & 1], A.pbuf[it & 1],
+                          fresh, ap, A.qbuf[(it - 1) & 1], A.rbuf[it & 1], A.qbuf[it & 1]);
+            if (cta_trace) mv_sum += res_gtime() - mv_t0;
+            xpend = false;  // the pass applied x_k += alpha_{k-1} p_{k-1} (unless fresh)
+            ++matvecs;
+            lap(0);
+            double t8[8] = {pq_loc, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+            for (int kk = 0; kk < n_own; ++kk)
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    const T r = own[oidx(VR, kk, c, tid)], q = own[oidx(VQ, kk, c, tid)];
+                    const T iv = get_inv(kk, c);
+                    const T z = mul_rn(r, iv);
+                    const double dr = (double)r, dq = (double)q, di = (double)iv;
+                    t8[1] += dr * dr;
+                    t8[2] += dr * (double)z;
+                    t8[3] += dr * dq;
+                    t8[4] += dq * dq;
+                    t8[5] += dr * di * dq;
+                    t8[6] += dq * di * dq;
+                    t8[7] += dr * di * dr;
+                }
+            res_block_sum<8, NT>(t8, shr, tid);
+            res_exchange<8, NT>(A.ring, ctr, nblk, bid, tid, phase++, t8, shr);
+            lap(1);
+            const double pq = cg_round(t8[0], F32);
+            rz = cg_round(t8[2], F32);
+            if (!isfinite(pq) || !isfinite(rz)) {
+                term = TERM_DIVERGED;
+                break;
+            }
+            if (pq <= 0.0) {
+                term = TERM_BREAKDOWN;
+                break;
+            }
+            const double alpha = rz / pq;
+            const T a = (T)alpha;
+            const bool refresh = recompute > 0 && it % recompute == 0;
+            double rr_n, rz_n;
+            if (refresh) {
+                // x_{k+1} applied and published; r_{k+1} = b - A x_{k+1}
+                for (int kk = 0; kk < n_own; ++kk)
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) {
+                        const int o = oidx(VX, kk, c, tid);
+                        const T xn = add_rn(own[o], mul_rn(a, own[oidx(VP, kk, c, tid)]));
+                        own[o] = xn;
+                        A.x[dof(kk, c)] = xn;
+                    }
+                double dummy[1] = {0.0};
+                res_exchange<1, NT>(A.ring, ctr, nblk, bid, tid, phase++, dummy, shr);  // x published
+                tile_pass(RAW, false, T(0), A.x, nullptr, nullptr);                   // own(VQ) = A x
+                ++matvecs;
+                double t2[2] = {0.0, 0.0};
+                for (int kk = 0; kk < n_own; ++kk)
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) {
+                        const int d = dof(kk, c);
+                        const T r = sub_rn(ld_nc(A.b + d), own[oidx(VQ, kk, c, tid)]);
+                        own[oidx(VR, kk, c, tid)] = r;
+                        A.rbuf[it & 1][d] = r;
+                        const T z = mul_rn(r, get_inv(kk, c));
+                        t2[0] += (double)r * (double)r;
+                        t2[1] += (double)r * (double)z;
+                    }
+                res_block_sum<2, NT>(t2, shr, tid);
+                res_exchange<2, NT>(A.ring, ctr, nblk, bid, tid, phase++, t2, shr);
+                rr_n = t2[0];
+                rz_n = t2[1];
+                fresh = true;
+                ap = T(0);
+            } else {
+                const double da = (double)a;
+                rr_n = t8[1] - 2.0 * da * t8[3] + da * da * t8[4];
+                rz_n = t8[7] - 2.0 * da * t8[5] + da * da * t8[6];
+                fresh = false;
+                ap = a;
+                xpend = true;
+            }
+            lap(3);
+            const double rn = cg_sqrt(cg_round(rr_n, F32), F32);
+            if (!isfinite(rn)) {
+                term = TERM_DIVERGED;
+                break;
+            }
+            rel = rn / bnorm;
+            if (lead && hist) hist[it] = rel;
+            if (rel <= tol) {
+                term = TERM_CONVERGED;
+                break;
+            }
+            const double rz_new = cg_round(rz_n, F32);
+            beta = rz_new / rz;
+            if (it >= max_iter) {
+                term = TERM_MAX_ITER;
+                break;
+            }
+            lap(4);
+        }
+        if (xpend) {
+            // x_{k+1} of the last iteration (the next pass would have applied it)
+            for (int kk = 0; kk < n_own; ++kk)
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    const int o = oidx(VX, kk, c, tid);
+                    own[o] = add_rn(own[o], mul_rn(ap, own[oidx(VP, kk, c, tid)]));
+                }
+        }
+    } else
     while (!done) {
         ++it;
         // A. q = A p_it, fused p.q
@@ -691,16 +904,24 @@ k_pcg_resident(const __grid_constant__ ResArgs<T> A, const __grid_constant__ Kha
 
 // ---- host ------------------------------------------------------------------------
 
+// owned vectors (+ the ONEX D^-1 table over oz + 2 staged planes of PN slots)
 template <typename T>
-static size_t res_dyn_bytes(int oz, bool lean, int nt)
+static size_t res_dyn_bytes(int oz, bool lean, int nt, bool onex, int pn_slots)
 {
-    return (size_t)(lean ? 3 : 5) * oz * 3 * nt * sizeof(T);
+    return (size_t)(lean ? 3 : 5) * oz * 3 * nt * sizeof(T) + (onex ? (size_t)(oz + 2) * pn_slots * sizeof(T) : 0);
+}
+
+// TF_PCG_ONEX=0: the two-exchange iteration (A/B); default: one exchange
+static bool res_onex_enabled()
+{
+    const char* e = getenv("TF_PCG_ONEX");
+    return !(e && e[0] == '0');
 }
 
 template <typename T, int BY>
-static const void* res_kernel()
+static const void* res_kernel(bool onex)
 {
-    return (const void*)k_pcg_resident<T, BY>;
+    return onex ? (const void*)k_pcg_resident<T, BY, true> : (const void*)k_pcg_resident<T, BY, false>;
 }
 
 // tile heights tried per precision (rows of element columns per CTA)
@@ -714,7 +935,8 @@ template <typename T, int BY>
 static bool res_candidate(const Grid& g, int nsm, int smem_optin, int oz_force, int lean_force, ResPlan* plan)
 {
     constexpr int NT = TILE_BX * BY;
-    const void* k = res_kernel<T, BY>();
+    constexpr int PN = ResTile<T, BY>::PN;
+    const bool onex_env = res_onex_enabled();
     const int tx = (g.nnx + TILE_BX - 2) / (TILE_BX - 1);
     const int ty = (g.nny + BY - 2) / (BY - 1);
     const long long cols = (long long)tx * ty;
@@ -722,7 +944,9 @@ static bool res_candidate(const Grid& g, int nsm, int smem_optin, int oz_force, 
         if (oz_force > 0 && oz != oz_force) continue;
         for (int lean = 0; lean < 2; ++lean) {
             if (lean_force >= 0 && lean != lean_force) continue;
-            const size_t dyn = res_dyn_bytes<T>(oz, lean != 0, NT);
+            const bool onex = onex_env && lean == 0;
+            const void* k = res_kernel<T, BY>(onex);
+            const size_t dyn = res_dyn_bytes<T>(oz, lean != 0, NT, onex, PN);
             if ((long long)dyn + 16384 > smem_optin) continue;
             cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
             if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn) != cudaSuccess) {
@@ -742,6 +966,7 @@ static bool res_candidate(const Grid& g, int nsm, int smem_optin, int oz_force, 
                 plan->dyn_smem = dyn;
                 plan->nblk = cols * tz;
                 plan->by = BY;
+                plan->onex = onex ? 1 : 0;
                 return true;
             }
         }
@@ -789,18 +1014,18 @@ bool pcg_resident_plan(const Grid& g, const T* ke_host, ResPlan* plan)
         const int nt = TILE_BX * p.by;
         const double unit = 0.87 * (sizeof(T) == 8 ? 1.7 : 1.0) * (nt >= 512 ? 1.15 : 1.0);
         const double matvec = std::ceil((double)p.nblk / nsm) * (p.oz + 1) * (nt / 256.0) * unit;
-        return matvec + 2.0 * (2.0 + 0.9 * (double)p.nblk / 148.0);
+        return matvec + (p.onex ? 1.0 : 2.0) * (2.0 + 0.9 * (double)p.nblk / 148.0);
     };
     *plan = cost(pa) < cost(pb) ? pa : pb;
     return true;
 }
 
-size_t pcg_resident_ring_doubles(const ResPlan& plan) { return (size_t)8 * plan.nblk + 16; }
+size_t pcg_resident_ring_doubles(const ResPlan& plan) { return (size_t)2 * RES_SLOT * plan.nblk + 16; }
 
 template <typename T>
 int launch_pcg_resident(const ResPlan& plan, const Grid& g, const T* ke_host, int has_x0, const T* scale,
                         const T* b, const T* inv, T* x, T* z, T* p0, T* p1, const uint8_t* node_fixed,
-                        double* ring, CgScalars* sc, cudaStream_t st)
+                        double* ring, CgScalars* sc, T* r1, T* q0, T* q1, cudaStream_t st)
 {
     KhatBlocks<T> kb;
     if (!khat_blocks_cached<T>(ke_host, &kb)) return TF_ERR_UNSUPPORTED;
@@ -818,6 +1043,12 @@ int launch_pcg_resident(const ResPlan& plan, const Grid& g, const T* ke_host, in
     a.node_fixed = node_fixed;
     a.ring = ring;
     a.lean = plan.lean;
+    a.onex = plan.onex;
+    a.rbuf[0] = z;  // ONEX: r_k ping-pong (z's buffer) and q_k ping-pong
+    a.rbuf[1] = r1;
+    a.qbuf[0] = q0;
+    a.qbuf[1] = q1;
+    if (plan.onex && !(r1 && q0 && q1)) return TF_ERR_ARG;
     {
         // FP32: the generic blocks unless TF_RES_ISO32=1 (experiment)
         const char* e = getenv("TF_RES_ISO32");
@@ -840,7 +1071,9 @@ int launch_pcg_resident(const ResPlan& plan, const Grid& g, const T* ke_host, in
         a.trace = trace_buf;
     }
     TF_CUDA_TRY(cudaMemsetAsync(ring, 0, sizeof(double) * pcg_resident_ring_doubles(plan), st));
-    const void* k = plan.by == ResBys<T>::a ? res_kernel<T, ResBys<T>::a>() : res_kernel<T, ResBys<T>::b>();
+    const bool onex = plan.onex != 0;
+    const void* k =
+        plan.by == ResBys<T>::a ? res_kernel<T, ResBys<T>::a>(onex) : res_kernel<T, ResBys<T>::b>(onex);
     TF_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plan.dyn_smem));
     void* args[] = {&a, &kb};
     dim3 block(TILE_BX, plan.by, 1);
@@ -880,9 +1113,10 @@ template bool pcg_resident_plan<float>(const Grid&, const float*, ResPlan*);
 template bool pcg_resident_plan<double>(const Grid&, const double*, ResPlan*);
 template int launch_pcg_resident<float>(const ResPlan&, const Grid&, const float*, int, const float*,
                                         const float*, const float*, float*, float*, float*, float*,
-                                        const uint8_t*, double*, CgScalars*, cudaStream_t);
+                                        const uint8_t*, double*, CgScalars*, float*, float*, float*, cudaStream_t);
 template int launch_pcg_resident<double>(const ResPlan&, const Grid&, const double*, int, const double*,
                                          const double*, const double*, double*, double*, double*, double*,
-                                         const uint8_t*, double*, CgScalars*, cudaStream_t);
+                                         const uint8_t*, double*, CgScalars*, double*, double*, double*,
+                                         cudaStream_t);
 
 }  // namespace tf

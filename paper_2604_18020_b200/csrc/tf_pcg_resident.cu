@@ -216,7 +216,9 @@ __device__ __forceinline__ void res_exchange(double* part, unsigned* ctr, int nb
     res_wait<K>(part, ctr, nblk, tid, phase, v, sh);
 }
 
-// Deterministic block sum of K values; every thread returns the same totals.
+// Deterministic block sum of K values, returned in thread 0 (the only
+// thread whose values res_arrive publishes; the exchange then gives every
+// thread the grid totals).
 template <int K, int NT>
 __device__ __forceinline__ void res_block_sum(double (&v)[K], double* sh /* [K][NT/32] */, int tid)
 {
@@ -230,12 +232,14 @@ __device__ __forceinline__ void res_block_sum(double (&v)[K], double* sh /* [K][
         for (int k = 0; k < K; ++k) sh[k * (NT / 32) + (tid >> 5)] = v[k];
     }
     __syncthreads();
+    if (tid == 0) {
 #pragma unroll
-    for (int k = 0; k < K; ++k) {
-        double s = 0.0;
+        for (int k = 0; k < K; ++k) {
+            double s = 0.0;
 #pragma unroll
-        for (int i = 0; i < NT / 32; ++i) s += sh[k * (NT / 32) + i];
-        v[k] = s;
+            for (int i = 0; i < NT / 32; ++i) s += sh[k * (NT / 32) + i];
+            v[k] = s;
+        }
     }
     __syncthreads();
 }
@@ -272,7 +276,9 @@ k_pcg_resident(const __grid_constant__ ResArgs<T> A, const __grid_constant__ Kha
 
     const Grid& g = A.g;
     const int oz = A.oz;
-    const bool lean = A.lean != 0;
+    // the single-exchange loop needs the full layout (a compile-time constant
+    // for FP32: fewer index registers; FP64 allocates better without it)
+    const bool lean = (ONEX && sizeof(T) == 4) ? false : A.lean != 0;
     const int tx = threadIdx.x, ty = threadIdx.y;
     const int tid = tx + TILE_BX * ty;
     const int bid = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);

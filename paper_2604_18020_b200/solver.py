@@ -77,6 +77,11 @@ def pcg(apply_op, b, diag, config: CgConfig = CgConfig(), x0=None):
     return _generic_pcg(apply_op, b, diag, config, x0)
 
 
+# environment overrides read when a handle is planned (tf_pcg_create)
+_PLAN_ENV = ("TF_PCG_RESIDENT", "TF_PCG_FUSED", "TF_PCG_ONEX", "TF_PCG_RES_BY", "TF_PCG_RES_OZ",
+             "TF_PCG_RES_LEAN", "TF_RES_ISO32")
+
+
 def _pcg_handle(op: MatFreeOperator, graph_only: bool = False):
     """One device PCG per (device problem, precision, kernel variant); graph_only
     forces the plain 3-kernel graph protocol (quantize_krylov rounds p and r
@@ -86,7 +91,7 @@ def _pcg_handle(op: MatFreeOperator, graph_only: bool = False):
     # once, by tf_pcg_create) are fixed at handle creation: part of the key
     key = (op.precision.tag, np.ascontiguousarray(op.ke).tobytes(), op.grid_variant,
            op.variant == "fused" and op.structured,
-           os.environ.get("TF_PCG_RESIDENT"), os.environ.get("TF_PCG_FUSED"), graph_only)
+           graph_only) + tuple(os.environ.get(v) for v in _PLAN_ENV)
     h = dev.pcg_handles.get(key)
     if h is not None:
         return h

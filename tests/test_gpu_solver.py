@@ -181,6 +181,36 @@ def test_fused_and_unfused_pcg_protocols_agree(prec, monkeypatch):
     assert np.abs(u0 - u1).max() <= 1e-6 * np.abs(u1).max()
 
 
+@pytest.mark.parametrize("prec", ["fp64", "fp32"])
+@pytest.mark.parametrize("recompute,max_iter", [(50, 1000), (10, 1000), (5, 233), (0, 300)])
+def test_sparse_refresh_graph_is_bitwise_the_per_iteration_graph(prec, recompute, max_iter, monkeypatch):
+    """Graph protocol: for refresh periods divisible by 10 or 5 (or none) the
+    WHILE body carries 10 / 5 iterations and ONE refresh IF node; the
+    per-iteration-IF graph (TF_PCG_SPARSE_IF=0) must give the same bits --
+    including the true-residual refreshes, a stop in the middle of a body and
+    the max-iteration cap."""
+    from paper_2604_18020_b200 import CgConfig, MatFreeOperator, SimpParams, build_edof, make_preset, pcg
+    from paper_2604_18020_b200.solver import pcg_protocol
+
+    monkeypatch.setenv("TF_PCG_RESIDENT", "0")
+    monkeypatch.setenv("TF_PCG_FUSED", "0")
+    pb = make_preset("cantilever", 0.4)
+    rho = np.random.default_rng(3).uniform(0.05, 1.0, pb.mesh.n_elem)
+    op = MatFreeOperator(pb.mesh, build_edof(pb.mesh), pb.bcs, rho, SimpParams(3.0), prec)
+    assert pcg_protocol(op) == "graph"
+    d = op.diagonal()
+    b = pb.bcs.force.astype(op.precision.dtype)
+    cfg = CgConfig(max_iter=max_iter, recompute_every=recompute)
+    x1, r1 = pcg(op, b, d, cfg)
+    monkeypatch.setenv("TF_PCG_SPARSE_IF", "0")
+    x2, r2 = pcg(op, b, d, cfg)
+    assert (r1.iterations, r1.termination, r1.matvecs) == (r2.iterations, r2.termination, r2.matvecs)
+    if recompute:
+        assert r1.matvecs == r1.iterations + r1.iterations // recompute
+    np.testing.assert_array_equal(r1.residual_history, r2.residual_history)
+    np.testing.assert_array_equal(x1, x2)
+
+
 @pytest.mark.parametrize("variant,scatter", [("fused", "parallel_atomic"), ("fused", "serial"),
                                              ("three_stage", "serial")])
 def test_general_connectivity_pcg_matches_oracle(variant, scatter):

@@ -1135,6 +1135,12 @@ int tf_pcg_create(tf_pcg** out, const tf_pcg_desc* d, void* stream)
     TF_CUDA_TRY(cudaMalloc(&h->sc, sizeof(CgScalars)));
     TF_CUDA_TRY(cudaMallocHost(&h->sc_host, sizeof(CgScalars)));
     int rc = h->resident ? TF_OK : (d->precision != 64 ? build_graph<float>(h) : build_graph<double>(h));
+    if (!rc && !h->resident && !h->fused) {
+        // the sparse-refresh graph of the default refresh period, up front
+        // (not in the first solve's time)
+        rc = d->precision != 64 ? build_graph<float>(h, 10, &h->graph_sp[0], &h->exec_sp[0])
+                                : build_graph<double>(h, 10, &h->graph_sp[0], &h->exec_sp[0]);
+    }
     if (rc) {
         tf_pcg_destroy(reinterpret_cast<tf_pcg*>(h));
         return rc;

@@ -10,7 +10,16 @@
 // (= r D^-1 of the last update) and p (ping-pong), which neighbouring CTAs
 // read for their halo nodes -- both stay L2-resident at the sizes that fit.
 //
-// One iteration = two grid barriers (three on a true-residual refresh):
+// Default iteration (ONEX, full layout): ONE grid exchange.  The pass stages
+// p_k = D^-1 (r_{k-1} - alpha_{k-1} q_{k-1}) + beta_{k-1} p_{k-1} from the
+// published r_{k-1}, q_{k-1}, p_{k-1} (the owner's arithmetic, so halo and
+// owned copies agree bitwise), owners apply x_k and publish r_k, p_k, q_k;
+// the exchange after it carries p.q and the own-DOF sums from which alpha_k
+// (exact, r.z direct) and ||r_{k+1}||^2, r_{k+1}.z_{k+1} (one-step FP64
+// expansion) follow -- see the loop below.  TF_PCG_ONEX=0 (and the lean
+// layout) run the two-exchange iteration:
+//
+// Two-exchange iteration = two grid barriers (three on a true-residual refresh):
 //   A. stage node planes of p_k = z + beta p_{k-1} (computed on the fly from
 //      the global z and p_{k-1}; owners publish p_k), q = A p_k with the
 //      parity-block element algebra, masked input and pass-through, per-CTA

@@ -93,6 +93,24 @@ int tf_matvec_grid_range_f64(const tf_grid* g, const double* ke, const double* s
                              const double* v, double* w, const uint8_t* node_fixed, uint32_t flags,
                              int32_t i_lo, int32_t i_hi, void* stream);
 
+/* The x-slab's masked range product with the interface transfer fused in
+ * (peer transport, csrc/tf_slab_run.cu): besides w, the owners of node plane
+ * x = put_i (inside [i_lo, i_hi)) store their output into `dst` -- the
+ * neighbour's receive slot, mapped through CUDA IPC; plane order (j, k)
+ * row-major, 3 components -- and the launch's last CTA raises `*flag` to
+ * `epoch` (or to *ep_dev + 1 when ep_dev is set: graph mode) after a
+ * system-scope fence.  `ticket`: a device counter, zero between launches. */
+int tf_matvec_grid_range_put_f32(const tf_grid* g, const float* ke, const float* scale,
+                                 const float* v, float* w, const uint8_t* node_fixed, int32_t i_lo,
+                                 int32_t i_hi, int32_t put_i, float* dst, uint32_t* flag,
+                                 uint32_t* ticket, const uint32_t* ep_dev, uint32_t epoch,
+                                 void* stream);
+int tf_matvec_grid_range_put_f64(const tf_grid* g, const double* ke, const double* scale,
+                                 const double* v, double* w, const uint8_t* node_fixed, int32_t i_lo,
+                                 int32_t i_hi, int32_t put_i, double* dst, uint32_t* flag,
+                                 uint32_t* ticket, const uint32_t* ep_dev, uint32_t epoch,
+                                 void* stream);
+
 /* Page-locked host memory for the e2e path (cudaHostAlloc, portable). */
 int tf_host_alloc(void** ptr, size_t bytes);
 int tf_host_free(void* ptr);

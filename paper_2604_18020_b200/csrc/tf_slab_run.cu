@@ -5,9 +5,11 @@
 // per GPU) the host, not the GPU, then sets the pace.  This handle enqueues
 // whole batches of iterations from C++:
 //
-//   apply(v -> w)   boundary tiles (node x-ranges next to the interfaces) ->
-//                   put both interface planes into the neighbours' receive
-//                   slots + raise their epoch flags (tf_peer.cu) -> interior
+//   apply(v -> w)   boundary tiles (node x-ranges next to the interfaces)
+//                   whose interface-plane owners store straight into the
+//                   neighbours' receive slots, the launch's last CTA raising
+//                   the neighbour's epoch flag (tf_tile.cu TilePut; with
+//                   TF_SLAB_FUSED_PUT=0 a separate put kernel, tf_peer.cu) -> interior
 //                   tiles (overlap the transfer) -> wait own flags -> add the
 //                   received partials in the fixed order (left first) ->
 //                   fixed-DOF pass-through
@@ -36,7 +38,8 @@ struct tf_slab {
     std::vector<void*> peers;
     int64_t* scalar_idx;   // device [0, 1, ..., 15]
     double* acc;           // device [16]
-    uint32_t* tickets;     // device [32]: tf_put_flags' per-job block counters, [31] wait/add/pass
+    uint32_t* tickets;     // device [32]: tf_put_flags' per-job block counters, [16]/[17] the fused
+                           // puts of the left/right boundary products, [31] wait/add/pass
     // graph mode: epochs in device memory, waits as spin kernels (stream
     // memory operations bake their values into a captured graph)
     uint32_t* dev_ep;      // device [2]: plane epoch, all-reduce epoch
@@ -289,6 +292,16 @@ int wait_dev(tf_slab* h, void* const* flags, int n, uint32_t* ep, cudaStream_t s
     return TF_OK;
 }
 
+// TF_SLAB_FUSED_PUT=0: boundary products + a separate put kernel (A/B)
+bool fused_put_enabled()
+{
+    static const bool on = [] {
+        const char* e = getenv("TF_SLAB_FUSED_PUT");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 // dev = true: device epochs (graph capture); else host epochs + stream memops
 int slab_apply(tf_slab* h, const void* v, void* w, cudaStream_t st, uint32_t* epoch, bool dev = false)
 {
@@ -307,14 +320,47 @@ int slab_apply(tf_slab* h, const void* v, void* w, cudaStream_t st, uint32_t* ep
     int rc;
     const bool split = h->aux && (d.has_left || d.has_right) && nnx - d.br > d.bl;
     if (split) TF_CUDA_TRY(cudaEventRecord(h->fork, st));
-    if ((rc = range(0, d.bl))) return rc;
-    if ((rc = range(nnx - d.br, nnx))) return rc;
     // slot parity: the host knows the epoch in both modes (graph mode keeps
     // the host counter advancing in step with the device one)
     const uint32_t e = ++*epoch;
     const int par = (int)(e & 1u);
     auto plane = [&](void* base, int side) { return at(base, d.off_planes + (2 * par + side) * d.plane_bytes); };
     auto flag = [&](void* base, int side) { return (uint32_t*)at(base, d.off_flags + 4 * side); };
+    // fused only when each interface plane lies in its own boundary range (a
+    // slab thinner than two tiles computes both planes in the left launch:
+    // the separate put kernel then)
+    if (fused_put_enabled() && (!d.has_left || d.bl >= 1) && (!d.has_right || d.br >= 1)) {
+        // boundary products with the interface transfer fused in: the owners
+        // of each interface plane store straight into the neighbour's slot
+        // and the launch's last CTA raises its flag (no separate put kernel)
+        auto put_range = [&](int lo, int hi, int put_i, void* dst, uint32_t* flg, uint32_t* ticket) -> int {
+            if (hi <= lo) return TF_OK;
+            const uint32_t* epd = dev ? h->dev_ep : nullptr;
+            return f32 ? tf_matvec_grid_range_put_f32(&d.grid, (const float*)h->ke.data(), (const float*)d.scale,
+                                                      (const float*)v, (float*)w, d.node_fixed, lo, hi, put_i,
+                                                      (float*)dst, flg, ticket, epd, e, st)
+                       : tf_matvec_grid_range_put_f64(&d.grid, (const double*)h->ke.data(),
+                                                      (const double*)d.scale, (const double*)v, (double*)w,
+                                                      d.node_fixed, lo, hi, put_i, (double*)dst, flg, ticket, epd,
+                                                      e, st);
+        };
+        if (d.has_left) {
+            void* nb = h->peers[d.rank - 1];
+            rc = put_range(0, d.bl, 0, plane(nb, 1), flag(nb, 1), h->tickets + 16);
+        } else {
+            rc = range(0, d.bl);
+        }
+        if (rc) return rc;
+        if (d.has_right) {
+            void* nb = h->peers[d.rank + 1];
+            rc = put_range(nnx - d.br, nnx, nnx - 1, plane(nb, 0), flag(nb, 0), h->tickets + 17);
+        } else {
+            rc = range(nnx - d.br, nnx);
+        }
+        if (rc) return rc;
+    } else {
+    if ((rc = range(0, d.bl))) return rc;
+    if ((rc = range(nnx - d.br, nnx))) return rc;
     // both interface planes into the neighbours' slots + their flags: one launch
     const int64_t* idx[2];
     void* dst[2];
@@ -335,6 +381,7 @@ int slab_apply(tf_slab* h, const void* v, void* w, cudaStream_t st, uint32_t* ep
         rc = f32 ? tf_put_flags_f32((const float*)w, idx, (float* const*)dst, flg, nj, d.plane_len, e, h->tickets, st)
                  : tf_put_flags_f64((const double*)w, idx, (double* const*)dst, flg, nj, d.plane_len, e, h->tickets, st);
     if (rc) return rc;
+    }
     if (split) {  // interior tiles on the side stream, launched after the boundary work
         TF_CUDA_TRY(cudaStreamWaitEvent(h->aux, h->fork, 0));
         cudaStream_t keep = st;

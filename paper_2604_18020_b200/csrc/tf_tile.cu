@@ -280,11 +280,29 @@ __device__ __forceinline__ unsigned tt_smid()
     } while (0)
 #endif
 
-template <typename T, bool MASK, bool PASS, bool ACC, bool DOT, int P, bool ISO>
+// Fused interface put of the x-slab peer transport (tf_slab_run.cu): the
+// owners of node plane x = put_i also store their (not yet exchanged)
+// output into the neighbour's receive slot `dst` -- plane order (j, k)
+// row-major, 3 components, as slab.py plane_dofs -- with plain peer stores
+// (NVLink on an NVSwitch box), and the launch's last CTA raises the
+// neighbour's epoch flag after a system-scope fence: the product and the
+// transfer in one kernel instead of a boundary product and a put kernel.
+template <typename T>
+struct TilePut {
+    T* dst;                  // nullptr: no put
+    unsigned* flag;          // the neighbour's flag
+    unsigned* ticket;        // local device memory, zero between launches
+    const unsigned* ep_dev;  // graph mode: flag = *ep_dev + 1; else `epoch`
+    unsigned epoch;
+    int put_i;               // node x-index of the plane (this launch's grid)
+};
+
+template <typename T, bool MASK, bool PASS, bool ACC, bool DOT, int P, bool ISO, bool PUT = false>
 __global__ void __launch_bounds__(TileDims<T>::NT, sizeof(T) == 4 ? TF_TILE_MINB32 : TF_TILE_MINB64)
 k_grid_tile5(Grid g, int oz, const T* __restrict__ scale, const T* __restrict__ v, T* __restrict__ w,
              const uint8_t* __restrict__ node_fixed, double* __restrict__ dot_part,
-             const __grid_constant__ KhatBlocks<T> kb, const __grid_constant__ KhatIso<T> ki)
+             const __grid_constant__ KhatBlocks<T> kb, const __grid_constant__ KhatIso<T> ki,
+             const __grid_constant__ TilePut<T> tp)
 {
     constexpr int TILE_BY = TileDims<T>::BY, TILE_NT = TileDims<T>::NT;
     constexpr int PW = StageSlots<T>::PW, PN = StageSlots<T>::PN, NS = StageSlots<T>::N;
@@ -498,6 +516,8 @@ k_grid_tile5(Grid g, int oz, const T* __restrict__ scale, const T* __restrict__ 
     T pend_x1[3], pend_p[3], pend_v[3];
     bool pend = false;
     int pend_d0 = 0;
+    const bool put_col = PUT && owner && i0 + tx == tp.put_i;  // this thread's column is the put plane's
+    int pend_pi = 0;
     unsigned pend_bits = 0u;
 
     // node pass of the previous layer (plane ez-1), reading its row hand-off.
@@ -514,6 +534,7 @@ k_grid_tile5(Grid g, int oz, const T* __restrict__ scale, const T* __restrict__ 
             const bool fx = PASS && ((pend_bits >> c) & 1u);
             if (fx) acc = pend_v[c];
             w[d] = acc;
+            if (PUT && put_col) tp.dst[pend_pi + c] = acc;
             if (DOT) {
                 const T p = fx ? pend_v[c] : pend_p[c];
                 dot = fma(p, acc, dot);
@@ -610,6 +631,7 @@ k_grid_tile5(Grid g, int oz, const T* __restrict__ scale, const T* __restrict__ 
         }
         pend = owner && L >= 1;
         pend_d0 = 3 * (own_node0 + ez * pn);
+        if (PUT) pend_pi = 3 * ((j0 + ty) + g.nny * ez);
         pend_bits = nbits;
 #pragma unroll
         for (int c = 0; c < 3; ++c) pend_v[c] = nv[c];
@@ -623,6 +645,19 @@ k_grid_tile5(Grid g, int oz, const T* __restrict__ scale, const T* __restrict__ 
     cp_async_wait_n(0);
     __syncthreads();
     node_pass(Y[(n_layers - 1) & 1]);
+    if (PUT) {
+        __threadfence_system();  // this thread's peer stores, before the CTA's ticket
+        __syncthreads();
+        if (tid == 0) {
+            const unsigned nb = gridDim.x * gridDim.y * gridDim.z;
+            if (atomicAdd(tp.ticket, 1u) == nb - 1u) {
+                __threadfence_system();
+                *reinterpret_cast<volatile unsigned*>(tp.flag) =
+                    tp.ep_dev ? *reinterpret_cast<const volatile unsigned*>(tp.ep_dev) + 1u : tp.epoch;
+                *tp.ticket = 0u;
+            }
+        }
+    }
 
 #ifdef TF_TILE_TRACE
     TT_CLK(14);
@@ -1158,8 +1193,9 @@ long long grid_tile_blocks(const Grid& g)
 
 // returns TF_ERR_UNSUPPORTED when Ke lacks the parity-block structure
 template <typename T>
-int launch_grid_tile(const Grid& g, const T* ke_host, const T* scale, const T* v, T* w,
-                     const uint8_t* node_fixed, uint32_t flags, double* dot_part, cudaStream_t st)
+static int launch_grid_tile_impl(const Grid& g, const T* ke_host, const T* scale, const T* v, T* w,
+                                 const uint8_t* node_fixed, uint32_t flags, double* dot_part, cudaStream_t st,
+                                 const TilePut<T>* put)
 {
     KhatBlocks<T> kb;
     if (!khat_blocks_cached<T>(ke_host, &kb)) return TF_ERR_UNSUPPORTED;
@@ -1172,18 +1208,33 @@ int launch_grid_tile(const Grid& g, const T* ke_host, const T* scale, const T* v
     const bool iso32 = sizeof(T) == 4 && tile_iso32_plain() && khat_iso<T>(ke_host, &ki);
     const uint32_t f = flags & (TF_MASK_INPUT | TF_PASS_FIXED | TF_ACCUMULATE);
     constexpr uint32_t MP = TF_MASK_INPUT | TF_PASS_FIXED;
-    auto launch_shape = [&](const TileShape& sh) -> int {
+    if (put && (dot_part || f != TF_MASK_INPUT)) {
+        set_error("the fused interface put is the slab's masked range product only");
+        return TF_ERR_ARG;
+    }
+    auto launch_shape = [&](const TileShape& sh, bool with_put = false) -> int {
         dim3 block(TILE_BX, TileDims<T>::BY, 1);
+        if (with_put) {
+            if ((sizeof(T) == 8 && iso) || (sizeof(T) == 4 && iso32))
+                k_grid_tile5<T, true, false, false, false, TF_TILE_P, true, true>
+                    <<<sh.grid, block, 0, st>>>(g, sh.oz, scale, v, w, node_fixed, nullptr, kb, ki, *put);
+            else
+                k_grid_tile5<T, true, false, false, false, TF_TILE_P, false, true>
+                    <<<sh.grid, block, 0, st>>>(g, sh.oz, scale, v, w, node_fixed, nullptr, kb, ki, *put);
+            TF_CHECK_LAUNCH();
+            return TF_OK;
+        }
         // isotropic blocks: every FP64 product; FP32 plain products (no CG
         // partials, no accumulation) -- the FP32 CG keeps the generic blocks
 #define T5(M, PS, AC, DT, DP)                                                                                  \
     do {                                                                                                       \
         if ((sizeof(T) == 8 && iso) || (sizeof(T) == 4 && !(AC) && !(DT) && iso32))                           \
             k_grid_tile5<T, M, PS, AC, DT, TF_TILE_P, !(AC) && !(DT) || sizeof(T) == 8>                         \
-                <<<sh.grid, block, 0, st>>>(g, sh.oz, scale, v, w, node_fixed, DP, kb, ki);                    \
+                <<<sh.grid, block, 0, st>>>(g, sh.oz, scale, v, w, node_fixed, DP, kb, ki, TilePut<T>{});      \
         else                                                                                                   \
             k_grid_tile5<T, M, PS, AC, DT, TF_TILE_P, false><<<sh.grid, block, 0, st>>>(g, sh.oz, scale, v, w, \
-                                                                                     node_fixed, DP, kb, ki);  \
+                                                                                     node_fixed, DP, kb, ki,   \
+                                                                                     TilePut<T>{});            \
     } while (0)
         if (dot_part) {  // CG p.q partials: the solver's masked, passed-through product only
             if (f != MP) {
@@ -1192,7 +1243,7 @@ int launch_grid_tile(const Grid& g, const T* ke_host, const T* scale, const T* v
             }
             if (sizeof(T) == 4 && iso32 && tile_iso32_cg())
                 k_grid_tile5<T, true, true, false, true, TF_TILE_P, true>
-                    <<<sh.grid, block, 0, st>>>(g, sh.oz, scale, v, w, node_fixed, dot_part, kb, ki);
+                    <<<sh.grid, block, 0, st>>>(g, sh.oz, scale, v, w, node_fixed, dot_part, kb, ki, TilePut<T>{});
             else
                 T5(true, true, false, true, dot_part);
         } else {
@@ -1220,8 +1271,36 @@ int launch_grid_tile(const Grid& g, const T* ke_host, const T* scale, const T* v
         });
         if (oz > 0) sh = tile_shape_oz<T>(g, oz);
     }
-    return launch_shape(sh);
+    // (the autotune's timing launches above never carry the put)
+    return launch_shape(sh, put != nullptr);
 }
+
+template <typename T>
+int launch_grid_tile(const Grid& g, const T* ke_host, const T* scale, const T* v, T* w,
+                     const uint8_t* node_fixed, uint32_t flags, double* dot_part, cudaStream_t st)
+{
+    return launch_grid_tile_impl<T>(g, ke_host, scale, v, w, node_fixed, flags, dot_part, st, nullptr);
+}
+
+// C ABI: the slab's range product with the fused interface put (see TilePut)
+#define TF_RANGE_PUT(T, SUF)                                                                              \
+    int tf_matvec_grid_range_put_##SUF(const tf_grid* gd, const T* ke, const T* scale, const T* v, T* w,   \
+                                       const uint8_t* node_fixed, int32_t i_lo, int32_t i_hi, int32_t put_i, \
+                                       T* dst, uint32_t* flag, uint32_t* ticket, const uint32_t* ep_dev,    \
+                                       uint32_t epoch, void* stream)                                      \
+    {                                                                                                     \
+        TF_REQUIRE(gd && ke && scale && v && w && dst && flag && ticket, "null pointer");                \
+        Grid gg = make_grid(gd);                                                                          \
+        TF_REQUIRE(0 <= i_lo && i_lo < i_hi && i_hi <= gg.nnx && i_lo <= put_i && put_i < i_hi,           \
+                   "bad node x-range / put plane");                                                       \
+        gg.ilo = i_lo;                                                                                    \
+        gg.ihi = i_hi;                                                                                    \
+        TilePut<T> tp{dst, flag, ticket, ep_dev, epoch, put_i};                                           \
+        const int rc = launch_grid_tile_impl<T>(gg, ke, scale, v, w, node_fixed, TF_MASK_INPUT, nullptr,  \
+                                                reinterpret_cast<cudaStream_t>(stream), &tp);             \
+        if (rc == TF_ERR_UNSUPPORTED) set_error("node ranges need the parity-block tile kernel");         \
+        return rc;                                                                                        \
+    }
 
 // Fused CG head (decision + direction + matvec + p.q partials); grid as the
 // production tile kernel so the partial count matches grid_tile_blocks().
@@ -1263,6 +1342,14 @@ template int launch_grid_tile<double>(const Grid&, const double*, const double*,
                                       double*, const uint8_t*, uint32_t, double*, cudaStream_t);
 
 }  // namespace tf
+
+using tf::TilePut;
+using tf::launch_grid_tile_impl;
+using tf::make_grid;
+using tf::Grid;
+using tf::set_error;
+TF_RANGE_PUT(float, f32)
+TF_RANGE_PUT(double, f64)
 
 #ifdef TF_TILE_TRACE
 extern "C" int tf_tile_trace_set(void* buf)

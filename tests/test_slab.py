@@ -224,13 +224,17 @@ def _peer_worker(rank, world, port, dims, prec, q):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("world,dims,prec", [(2, (40, 6, 5), "fp64"), (3, (45, 5, 4), "fp32")])
+@pytest.mark.parametrize("world,dims,prec", [(2, (40, 6, 5), "fp64"), (3, (45, 5, 4), "fp32"),
+                                             (2, (130, 4, 3), "fp64"), (3, (200, 3, 3), "fp32")])
 def test_slab_peer_transport_matches_p2p(world, dims, prec):
     """Peer-memory transport (CUDA IPC mappings between the rank processes,
     stream-ordered epoch flags): interface sums bitwise equal to the
     torch.distributed P2P exchange over repeated products (both slot
     parities), the same diagonal, the one-shot all-reduce equal to the rank
-    sum on every rank, and the distributed PCG through it."""
+    sum on every rank, and the distributed PCG through it.  Slabs of 65+
+    element layers put their interface planes from inside the boundary tile
+    kernels (fused put, tf_tile.cu TilePut); thinner ones through the
+    separate put kernel."""
     import torch.multiprocessing as mp
 
     ctx = mp.get_context("spawn")

@@ -1065,9 +1065,11 @@ int launch_pcg_resident(const ResPlan& plan, const Grid& g, const T* ke_host, in
     a.qbuf[1] = q1;
     if (plan.onex && !(r1 && q0 && q1)) return TF_ERR_ARG;
     {
-        // FP32: the generic blocks unless TF_RES_ISO32=1 (experiment)
+        // isotropic blocks in both precisions (FP32 since late round 2, like
+        // the graph protocol's matvec: c2 17.85 -> 17.6 us/iteration, every
+        // FP32 CG/SIMP parity test green); TF_RES_ISO32=0: generic FP32 blocks
         const char* e = getenv("TF_RES_ISO32");
-        const bool iso32 = sizeof(T) == 4 && e && e[0] == '1';
+        const bool iso32 = sizeof(T) == 4 && !(e && e[0] == '0');
         a.iso = ((tile_iso_enabled<T>() || iso32) && khat_iso<T>(ke_host, &a.ki)) ? 1 : 0;
     }
     a.sc = sc;

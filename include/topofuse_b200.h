@@ -433,6 +433,21 @@ int tf_slab_cg_beta_f32(int64_t n, float* p, const float* z, double* state, cons
 int tf_slab_cg_beta_f64(int64_t n, double* p, const double* z, double* state, const double* red,
                         double* hist, int hist_len, void* stream);
 
+/* Single-reduction iteration (one all-reduce per CG iteration): after
+ * q = K p, tf_slab_cg_dots8 -> red[0..7] = owned (p.q, r.r, r.z, r.q, q.q,
+ * r.Dq, q.Dq, r.Dr) partials -> all-reduce red[0..7] -> tf_slab_cg_step:
+ * alpha from the direct r.z / p.q, the next residual's norms expanded one
+ * step in FP64, stop rule, and x, r, z, p updated in one pass (refresh != 0:
+ * x += alpha p only; the classic residual / all-reduce / beta follow). */
+int tf_slab_cg_dots8_f32(int64_t n, const float* p, const float* q, const float* r, const float* inv,
+                         const uint8_t* owned, const double* state, double* red, double* work, void* stream);
+int tf_slab_cg_dots8_f64(int64_t n, const double* p, const double* q, const double* r, const double* inv,
+                         const uint8_t* owned, const double* state, double* red, double* work, void* stream);
+int tf_slab_cg_step_f32(int64_t n, float* x, float* r, float* p, const float* q, const float* inv, float* z,
+                        double* state, const double* red, int refresh, double* hist, int hist_len, void* stream);
+int tf_slab_cg_step_f64(int64_t n, double* x, double* r, double* p, const double* q, const double* inv, double* z,
+                        double* state, const double* red, int refresh, double* hist, int hist_len, void* stream);
+
 
 /* ---- peer-memory transport (csrc/tf_peer.cu) ----------------------
  * Interface-plane exchange and one-shot scalar all-reduce written straight

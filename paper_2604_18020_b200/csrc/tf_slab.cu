@@ -258,6 +258,116 @@ k_slab_beta(long long n, T* __restrict__ p, const T* __restrict__ z, SlabCgState
     }
 }
 
+// Single-reduction iteration (one all-reduce per CG iteration instead of
+// two; the resident PCG's recurrence, tf_pcg_resident.cu): after q = K p
+//     k_slab_dots8   red[0..7] = owned sums p.q, r.r, r.z (z = r*inv), r.q,
+//                    q.q, r.Dq, q.Dq, r.Dr                (rank partials)
+//     all-reduce red[0..7]
+//     k_slab_step    alpha = r.z / p.q exactly as k_slab_alpha's; the next
+//                    residual's r.r and r.z expanded one step in FP64 from
+//                    this iteration's direct sums -> stop rule, beta; then
+//                    x += a p, r -= a q, z = r*inv, p = z + b p in one pass.
+// A refresh iteration runs k_slab_step(refresh) (x += a p only, rz kept for
+// beta) and then the classic residual / all-reduce / k_slab_beta.
+template <typename T>
+__global__ void __launch_bounds__(SLAB_BLOCK)
+k_slab_dots8(long long n, const T* __restrict__ p, const T* __restrict__ q, const T* __restrict__ r,
+             const T* __restrict__ inv, const uint8_t* __restrict__ owned, const SlabCgState* st, double* part,
+             unsigned* ticket, double* red)
+{
+    if (st && !slab_active(st)) return;
+    double v[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    for (long long i = (long long)blockIdx.x * SLAB_BLOCK + threadIdx.x; i < n; i += (long long)gridDim.x * SLAB_BLOCK) {
+        if (owned && !owned[i]) continue;
+        const T ri = r[i], qi = q[i], di = inv[i];
+        const T zi = ri * di;
+        const double dr = (double)ri, dq = (double)qi, dd = (double)di;
+        v[0] += (double)p[i] * dq;
+        v[1] += dr * dr;
+        v[2] += dr * (double)zi;
+        v[3] += dr * dq;
+        v[4] += dq * dq;
+        v[5] += dr * dd * dq;
+        v[6] += dq * dd * dq;
+        v[7] += dr * dd * dr;
+    }
+    slab_reduce<8>(v, part, ticket, red);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(SLAB_BLOCK)
+k_slab_step(long long n, T* __restrict__ x, T* __restrict__ r, T* __restrict__ p, const T* __restrict__ q,
+            const T* __restrict__ inv, T* __restrict__ z, SlabCgState* st, const double* red, int refresh,
+            double* hist, int hist_len)
+{
+    if (!slab_active(st)) return;
+    const bool f32 = sizeof(T) == 4;
+    const double pq = cg_round(__ldcg(red), f32), rz = cg_round(__ldcg(red + 2), f32);
+    const double it = __ldcg(&st->it) + 1.0;
+    const bool bad = !isfinite(pq) || !isfinite(rz);
+    __shared__ bool last;
+    // the state is written by the LAST block to finish (every block reads it first)
+    auto commit = [&](auto&& write) {
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            unsigned* ticket = reinterpret_cast<unsigned*>(&st->pad);
+            __threadfence();
+            last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+        }
+        __syncthreads();
+        if (last && threadIdx.x == 0) {
+            write();
+            *reinterpret_cast<unsigned*>(&st->pad) = 0u;
+        }
+    };
+    if (bad || pq <= 0.0) {
+        commit([&] {
+            st->it = it;
+            st->term = bad ? SLAB_DIVERGED : SLAB_BREAKDOWN;
+            st->active = 0.0;
+        });
+        return;
+    }
+    const T a = (T)(rz / pq);
+    const long long stride = (long long)gridDim.x * SLAB_BLOCK;
+    const long long i0 = (long long)blockIdx.x * SLAB_BLOCK + threadIdx.x;
+    if (refresh) {  // x += a p; r, z, beta and the stop rule follow the true residual
+        for (long long i = i0; i < n; i += stride) x[i] = x[i] + a * p[i];
+        commit([&] { st->rz = rz; });
+        return;
+    }
+    const double da = (double)a;
+    const double rr1 = __ldcg(red + 1) - 2.0 * da * __ldcg(red + 3) + da * da * __ldcg(red + 4);
+    const double rz1 = __ldcg(red + 7) - 2.0 * da * __ldcg(red + 5) + da * da * __ldcg(red + 6);
+    const double rn = cg_sqrt(cg_round(rr1, f32), f32);
+    const double rel = rn / __ldcg(&st->bnorm);
+    const bool stop = !isfinite(rn) || rel <= __ldcg(&st->tol);
+    const T beta = (T)(cg_round(rz1, f32) / rz);
+    for (long long i = i0; i < n; i += stride) {
+        x[i] = x[i] + a * p[i];
+        if (!stop) {
+            const T ri = r[i] - a * q[i];
+            const T zi = ri * inv[i];
+            r[i] = ri;
+            z[i] = zi;
+            p[i] = zi + beta * p[i];
+        }
+    }
+    commit([&] {
+        st->it = it;
+        if (isfinite(rn)) {
+            st->rel = rel;
+            if (hist && (int)it < hist_len) hist[(int)it] = rel;
+        }
+        if (stop) {
+            st->term = isfinite(rn) ? SLAB_CONVERGED : SLAB_DIVERGED;
+            st->active = 0.0;
+        } else {
+            st->rz = cg_round(rz1, f32);
+        }
+    });
+}
+
 static int slab_blocks(long long n)
 {
     static int nsm = 0;
@@ -279,7 +389,7 @@ extern "C" {
 
 int64_t tf_slab_work_doubles(int64_t n)
 {
-    return 2LL * slab_blocks(n) + 8;  // K<=2 partials per block, then the ticket word
+    return 8LL * slab_blocks(n) + 8;  // K<=8 partials per block, then the ticket words
 }
 
 #define TF_SLAB_API(T, SUF)                                                                                  \
@@ -289,7 +399,7 @@ int64_t tf_slab_work_doubles(int64_t n)
         TF_REQUIRE(n > 0 && a && b && out && work, "bad arguments");                                         \
         const int nb = slab_blocks(n);                                                                       \
         k_slab_dot<T><<<nb, SLAB_BLOCK, 0, SL(stream)>>>(n, a, b, owned, nullptr, work,                      \
-                                                         reinterpret_cast<unsigned*>(work + 2 * nb), out);   \
+                                                         reinterpret_cast<unsigned*>(work + 8 * nb), out);   \
         TF_CHECK_LAUNCH();                                                                                   \
         return TF_OK;                                                                                        \
     }                                                                                                        \
@@ -299,7 +409,7 @@ int64_t tf_slab_work_doubles(int64_t n)
         const int nb = slab_blocks(n);                                                                       \
         k_slab_dot<T><<<nb, SLAB_BLOCK, 0, SL(stream)>>>(n, p, q, owned,                                     \
                                                          reinterpret_cast<const SlabCgState*>(state), work,  \
-                                                         reinterpret_cast<unsigned*>(work + 2 * nb), red);   \
+                                                         reinterpret_cast<unsigned*>(work + 8 * nb), red);   \
         TF_CHECK_LAUNCH();                                                                                   \
         return TF_OK;                                                                                        \
     }                                                                                                        \
@@ -308,7 +418,7 @@ int64_t tf_slab_work_doubles(int64_t n)
     {                                                                                                        \
         const int nb = slab_blocks(n);                                                                       \
         k_slab_begin<T><<<nb, SLAB_BLOCK, 0, SL(stream)>>>(n, r, inv, z, p, owned, work,                     \
-                                                           reinterpret_cast<unsigned*>(work + 2 * nb), red); \
+                                                           reinterpret_cast<unsigned*>(work + 8 * nb), red); \
         TF_CHECK_LAUNCH();                                                                                   \
         return TF_OK;                                                                                        \
     }                                                                                                        \
@@ -320,7 +430,7 @@ int64_t tf_slab_work_doubles(int64_t n)
         k_slab_alpha<T><<<nb, SLAB_BLOCK, 0, SL(stream)>>>(n, x, r, p, q, inv, z, owned,                     \
                                                            reinterpret_cast<SlabCgState*>(state), red,       \
                                                            refresh, work,                                    \
-                                                           reinterpret_cast<unsigned*>(work + 2 * nb));      \
+                                                           reinterpret_cast<unsigned*>(work + 8 * nb));      \
         TF_CHECK_LAUNCH();                                                                                   \
         return TF_OK;                                                                                        \
     }                                                                                                        \
@@ -332,7 +442,7 @@ int64_t tf_slab_work_doubles(int64_t n)
         k_slab_residual<T><<<nb, SLAB_BLOCK, 0, SL(stream)>>>(n, b, w, r, inv, z, owned,                     \
                                                               reinterpret_cast<const SlabCgState*>(state),   \
                                                               red, work,                                     \
-                                                              reinterpret_cast<unsigned*>(work + 2 * nb));   \
+                                                              reinterpret_cast<unsigned*>(work + 8 * nb));   \
         TF_CHECK_LAUNCH();                                                                                   \
         return TF_OK;                                                                                        \
     }                                                                                                        \
@@ -347,6 +457,31 @@ int64_t tf_slab_work_doubles(int64_t n)
     }
 TF_SLAB_API(float, f32)
 TF_SLAB_API(double, f64)
+
+#define TF_SLAB_ONEX_API(T, SUF)                                                                             \
+    int tf_slab_cg_dots8_##SUF(int64_t n, const T* p, const T* q, const T* r, const T* inv,                  \
+                               const uint8_t* owned, const double* state, double* red, double* work,        \
+                               void* stream)                                                                 \
+    {                                                                                                        \
+        const int nb = slab_blocks(n);                                                                       \
+        k_slab_dots8<T><<<nb, SLAB_BLOCK, 0, SL(stream)>>>(n, p, q, r, inv, owned,                           \
+                                                           reinterpret_cast<const SlabCgState*>(state), work, \
+                                                           reinterpret_cast<unsigned*>(work + 8 * nb), red); \
+        TF_CHECK_LAUNCH();                                                                                   \
+        return TF_OK;                                                                                        \
+    }                                                                                                        \
+    int tf_slab_cg_step_##SUF(int64_t n, T* x, T* r, T* p, const T* q, const T* inv, T* z, double* state,    \
+                              const double* red, int refresh, double* hist, int hist_len, void* stream)      \
+    {                                                                                                        \
+        const int nb = slab_blocks(n);                                                                       \
+        k_slab_step<T><<<nb, SLAB_BLOCK, 0, SL(stream)>>>(n, x, r, p, q, inv, z,                             \
+                                                          reinterpret_cast<SlabCgState*>(state), red, refresh, \
+                                                          hist, hist_len);                                   \
+        TF_CHECK_LAUNCH();                                                                                   \
+        return TF_OK;                                                                                        \
+    }
+TF_SLAB_ONEX_API(float, f32)
+TF_SLAB_ONEX_API(double, f64)
 
 int tf_slab_cg_start(double* state, const double* red, double rel_tol, int f32, void* stream)
 {

@@ -548,6 +548,16 @@ int tf_slab_allreduce(tf_slab* h, double* t, int k, uint32_t* epochs, void* stre
     return slab_allreduce(h, t, k, (cudaStream_t)stream, &epochs[1]);
 }
 
+// TF_SLAB_ONEX=0: the two-all-reduce iteration (A/B)
+static bool slab_onex_enabled()
+{
+    static const bool on = [] {
+        const char* e = getenv("TF_SLAB_ONEX");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 // CG iterations it0+1 .. it0+n_iters (slab.py slab_pcg_device's loop body)
 static int slab_iterations(tf_slab* h, const void* b, const void* inv, void* x, void* r, void* z, void* p, void* q,
                            void* wtmp, double* state, double* red, double* work, int it0, int n_iters,
@@ -559,6 +569,36 @@ static int slab_iterations(tf_slab* h, const void* b, const void* inv, void* x, 
     const int64_t n = 3LL * (d.grid.nelx + 1) * (d.grid.nely + 1) * (d.grid.nelz + 1);
     int rc;
     for (int it = it0 + 1; it <= it0 + n_iters; ++it) {
+        if (slab_onex_enabled()) {
+            // one all-reduce per iteration (tf_slab.cu k_slab_dots8 / k_slab_step)
+            if ((rc = slab_apply(h, p, q, st, &epochs[0], dev))) return rc;
+            rc = f32 ? tf_slab_cg_dots8_f32(n, (const float*)p, (const float*)q, (const float*)r,
+                                            (const float*)inv, d.owned, state, red, work, st)
+                     : tf_slab_cg_dots8_f64(n, (const double*)p, (const double*)q, (const double*)r,
+                                            (const double*)inv, d.owned, state, red, work, st);
+            if (rc) return rc;
+            if ((rc = slab_allreduce(h, red, 8, st, &epochs[1], dev))) return rc;
+            const int refresh = recompute_every > 0 && it % recompute_every == 0;
+            rc = f32 ? tf_slab_cg_step_f32(n, (float*)x, (float*)r, (float*)p, (const float*)q, (const float*)inv,
+                                           (float*)z, state, red, refresh, hist, hist_len, st)
+                     : tf_slab_cg_step_f64(n, (double*)x, (double*)r, (double*)p, (const double*)q,
+                                           (const double*)inv, (double*)z, state, red, refresh, hist, hist_len,
+                                           st);
+            if (rc) return rc;
+            if (refresh) {
+                if ((rc = slab_apply(h, x, wtmp, st, &epochs[0], dev))) return rc;
+                rc = f32 ? tf_slab_cg_residual_f32(n, (const float*)b, (const float*)wtmp, (float*)r,
+                                                   (const float*)inv, (float*)z, d.owned, state, red, work, st)
+                         : tf_slab_cg_residual_f64(n, (const double*)b, (const double*)wtmp, (double*)r,
+                                                   (const double*)inv, (double*)z, d.owned, state, red, work, st);
+                if (rc) return rc;
+                if ((rc = slab_allreduce(h, red + 1, 2, st, &epochs[1], dev))) return rc;
+                rc = f32 ? tf_slab_cg_beta_f32(n, (float*)p, (const float*)z, state, red, hist, hist_len, st)
+                         : tf_slab_cg_beta_f64(n, (double*)p, (const double*)z, state, red, hist, hist_len, st);
+                if (rc) return rc;
+            }
+            continue;
+        }
         if ((rc = slab_apply(h, p, q, st, &epochs[0], dev))) return rc;
         rc = f32 ? tf_slab_cg_pq_f32(n, (const float*)p, (const float*)q, d.owned, state, red, work, st)
                  : tf_slab_cg_pq_f64(n, (const double*)p, (const double*)q, d.owned, state, red, work, st);

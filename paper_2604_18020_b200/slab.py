@@ -503,7 +503,7 @@ def slab_pcg_device(op: SlabOperator, b, diag, rel_tol=1e-5, max_iter=1000, reco
     f64 = torch.float64
     owned = op.owned.to(torch.uint8)
     work = torch.zeros(int(_lib.load().tf_slab_work_doubles(n)), dtype=f64, device=dev)
-    red = torch.zeros(4, dtype=f64, device=dev)
+    red = torch.zeros(8, dtype=f64, device=dev)  # [0..7]: the single-reduction iteration's sums
     state = torch.zeros(8, dtype=f64, device=dev)
     hist = torch.full((max_iter + 1,), float("nan"), dtype=f64, device=dev)
 

@@ -214,7 +214,14 @@ def _peer_worker(rank, world, port, dims, prec, q):
             ws = [op.apply(x).cpu().numpy() for _ in range(3)]  # several epochs (slot parities)
             d = op.diagonal()
             b = torch.from_numpy(lb.force).to("cuda:0", tdt)
-            xs, info = slab_pcg(op, b, d, max_iter=1000)
+            # the native runtime runs the single-reduction recurrence, the
+            # Python p2p loop the two-reduction one: full solves where they
+            # converge (the short FP64 beam), a fixed 60 iterations on the
+            # slender beams that do not converge within 1000 (FP32, and the
+            # long fused-put slabs), where round-off differences between any
+            # two orderings grow chaotically past ~100 iterations
+            long_or_fp32 = prec == "fp32" or dims[0] >= 100
+            xs, info = slab_pcg(op, b, d, max_iter=60 if long_or_fp32 else 1000)
             red = torch.tensor([rank + 1.0, 0.25, -rank], dtype=torch.float64, device="cuda:0")
             op.allreduce_dev(red, 0, 3)
             out[transport] = (ws, d.cpu().numpy(), xs.cpu().numpy(), info["iterations"], red.cpu().numpy())

@@ -9,6 +9,8 @@
 //                      z = r / d, red[1..2] = (r.r, r.z) partials
 //     all-reduce red[1..2]
 //     k_slab_beta      rel = |r| / |b|; stop, or p = z + b p
+// (the native runtime runs the single-reduction variant below instead:
+// k_slab_dots8, ONE all-reduce, k_slab_step)
 // with every scalar living in device memory, so the host enqueues iterations
 // back to back and looks at the state only every few iterations.  The stop is
 // exact: once a rank's state says "stopped" every later kernel of the solve

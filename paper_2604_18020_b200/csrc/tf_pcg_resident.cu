@@ -671,7 +671,7 @@ k_pcg_resident(const __grid_constant__ ResArgs<T> A, const __grid_constant__ Kha
             xpend = false;  // the pass applied x_k += alpha_{k-1} p_{k-1} (unless fresh)
             ++matvecs;
             lap(0);
-            double t8[8] = {pq_loc, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+            double t8[7] = {pq_loc, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
             for (int kk = 0; kk < n_own; ++kk)
 #pragma unroll
                 for (int c = 0; c < 3; ++c) {
@@ -685,10 +685,9 @@ k_pcg_resident(const __grid_constant__ ResArgs<T> A, const __grid_constant__ Kha
                     t8[4] += dq * dq;
                     t8[5] += dr * di * dq;
                     t8[6] += dq * di * dq;
-                    t8[7] += dr * di * dr;
                 }
-            res_block_sum<8, NT>(t8, shr, tid);
-            res_exchange<8, NT>(A.ring, ctr, nblk, bid, tid, phase++, t8, shr);
+            res_block_sum<7, NT>(t8, shr, tid);
+            res_exchange<7, NT>(A.ring, ctr, nblk, bid, tid, phase++, t8, shr);
             lap(1);
             const double pq = cg_round(t8[0], F32);
             rz = cg_round(t8[2], F32);
@@ -739,7 +738,8 @@ k_pcg_resident(const __grid_constant__ ResArgs<T> A, const __grid_constant__ Kha
             } else {
                 const double da = (double)a;
                 rr_n = t8[1] - 2.0 * da * t8[3] + da * da * t8[4];
-                rz_n = t8[7] - 2.0 * da * t8[5] + da * da * t8[6];
+                // base: the direct r.z (z rounded in the working dtype) for r.Dr
+                rz_n = t8[2] - 2.0 * da * t8[5] + da * da * t8[6];
                 fresh = false;
                 ap = a;
                 xpend = true;

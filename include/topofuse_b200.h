@@ -400,7 +400,8 @@ int tf_oc_apply_f64(int64_t n, const double* rho, const double* dc, const double
  * iteration without synchronising; `state` (8 doubles: rz, |b|, rel, it,
  * active, term, tol, ticket) freezes the solve exactly at the stop iteration
  * (term 1 converged, 2 breakdown, 3 diverged).  owned (nullable): uint8 mask
- * of the DOFs this rank counts in dots.  red: 4 doubles (p.q, r.r, r.z, b.b).
+ * of the DOFs this rank counts in dots.  red: 4 doubles (p.q, r.r, r.z, b.b);
+ * 8 for the single-reduction iteration (tf_slab_cg_dots8 / tf_slab_cg_step).
  * work: tf_slab_work_doubles(n) doubles. */
 int64_t tf_slab_work_doubles(int64_t n);
 int tf_slab_dot_f32(int64_t n, const float* a, const float* b, const uint8_t* owned, double* out,
@@ -520,6 +521,9 @@ int tf_slab_create(tf_slab** out, const tf_slab_desc* d);
 int tf_slab_destroy(tf_slab* h);
 int tf_slab_apply(tf_slab* h, const void* v, void* w, uint32_t* epochs, void* stream);
 int tf_slab_allreduce(tf_slab* h, double* t, int k, uint32_t* epochs, void* stream);
+/* n_iters CG iterations enqueued from C++: the single-reduction iteration
+ * (dots8 -> one all-reduce -> step; TF_SLAB_ONEX=0: the two-all-reduce
+ * one); red: 8 doubles. */
 int tf_slab_pcg_iterate(tf_slab* h, const void* b, const void* inv, void* x, void* r, void* z, void* p,
                         void* q, void* wtmp, double* state, double* red, double* work, int it0,
                         int n_iters, int recompute_every, double* hist, int hist_len, uint32_t* epochs,
